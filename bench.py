@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark of the SAME Gibbs hot path (BASELINE.json metric: node-samples/s).
+
+Workload (BASELINE.json configs[1], "C2"): Koller student network, 1M cases per
+GPU, 50% of cells hidden, SAME m = 10, one minibatch of 1M cases, moving-sum
+accumulator, sampled Dirichlet CPT update, fast RNG mode.  One step = one
+minibatch visit = conditional tables + fused sweep/tally + accumulator +
+Dirichlet update (+ the count all-reduce when N > 1).  Synthetic data of that
+shape comes from the reference's own forward_sample/mask streams, generated
+on the device.  node-samples per step = n_vars x cases x m (sampler.py:475).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: per-step CUDA events on the launching stream, L2 flushed (256 MB
+write) between timed steps, max over ranks.  Prints ONE JSON line on rank 0.
+``--impl reference`` times the CPU oracle (NumPy restatement of the reference,
+oracle/) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_VARS = 5
+CASES = 1_000_000
+M = 10
+HIDE = 0.5
+BYTES_PER_NODE_SAMPLE = 1.5  # n*L*(1+f) int8 algorithmic bytes, f = 0.5
+METRIC = "node-samples/sec"
+UNIT = "node-samples/s"
+
+
+def workload_config(n_gpus: int, rng: str) -> dict:
+    return {
+        "workload": "C2: koller-student (5 vars), 1M cases/GPU, 50% hidden, SAME m=10, minibatch=1M, "
+                    "moving-sum, Dirichlet CPT update",
+        "network": "koller-student",
+        "cases_per_gpu": CASES,
+        "global_minibatch": CASES * n_gpus,
+        "m": M,
+        "hidden_fraction": HIDE,
+        "rng": rng,
+        "parallelism": f"case-sharded x{n_gpus}, int64 count all-reduce" if n_gpus > 1 else "single GPU",
+        "l2": "flushed between timed steps (256 MB write outside the step events)",
+    }
+
+
+# ---------------------------------------------------------------- CPU oracle legs
+
+def _oracle_worker(args):
+    """Time oracle steps (sweep + tally + moving sum + Dirichlet) on a case slice."""
+    cases, m, steps, budget_s, slice_id = args
+    import numpy as np
+
+    import oracle as O
+
+    net, truth = O.koller()
+    dense = O.mask_dense(O.forward_sample(net, truth, cases, 100 + slice_id), HIDE, 200 + slice_id)
+    groups = O.greedy_coloring(net)
+    cur = O.init_cpts(net, 300)
+    total = [np.zeros((net.rows(v), net.cards[v])) for v in range(net.n)]
+    values, missing = O.replicate(dense, m)
+    weights = np.ones(values.shape[1])
+    O.init_latent(net, values, missing, 300, 0, 0)
+    prev = None
+    times = []
+    t_start = time.perf_counter()
+    for s in range(steps):
+        t0 = time.perf_counter()
+        counts = O.sweep(net, groups, cur, values, missing, weights, O.site_seed(300, "sweep", s, 0, 0))
+        O.moving_sum(total, prev, counts)
+        prev = counts
+        cur = O.sample_cpts(total, [1.0] * net.n, O.site_seed(300, "cpt_update", s, 0))
+        times.append(time.perf_counter() - t0)
+        if budget_s and time.perf_counter() - t_start > budget_s:
+            break
+    return times
+
+
+def cpu_baseline(budget_s: float = 12.0) -> dict:
+    """Single-core oracle on a 100k-case slice of the workload (rank 0, N=1)."""
+    cases = 100_000
+    times = _oracle_worker((cases, M, 1000, budget_s, 0))
+    per = statistics.median(times[1:] if len(times) > 2 else times)
+    return {"value": N_VARS * cases * M / per, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle (NumPy restatement of samegibbs) single process, 100k-case slice x m=10, "
+                      f"{len(times)} steps of sweep+tally+moving-sum+Dirichlet, median step {per * 1e3:.1f} ms"}
+
+
+def reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    total_steps = args.steps + args.warmup
+    # bound the run to roughly a minute of CPU time per process
+    cases = int(min(100_000, max(2_000, 60.0 / total_steps * 12e6 / (N_VARS * M))) // 1000 * 1000)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_oracle_worker, [(cases, M, total_steps, 0, i) for i in range(procs)])
+    wall = time.perf_counter() - t0
+    timed = [r[args.warmup:] for r in res]
+    per_step = max(sum(t) for t in timed) / max(1, args.steps)  # slowest worker bounds the aggregate
+    value = procs * N_VARS * cases * M / per_step
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.gpus, "numpy"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{procs} independent single-threaded oracle processes, each on its own "
+                                   f"{cases}-case slice x m=10 (aggregate upper bound; the reference's own "
+                                   f"threads knob does not scale), wall {wall:.1f} s"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are best effort metadata
+            self.nvml = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                mask = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nvml:
+            self.t.join()
+
+    def summary(self) -> dict:
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- our arm
+
+def load_traffic():
+    """Per-launch DRAM bytes of the sweep kernel from the committed ncu summary (or None)."""
+    for p in sorted((ROOT / "profiles").glob("ncu_sweep_*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+            if d.get("kernel") and d.get("cases") == CASES and d.get("m") == M:
+                return d.get("dram_bytes_per_launch"), p.name
+        except Exception:  # noqa: BLE001
+            continue
+    return None, None
+
+
+def our_arm(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1511_06416_b200 as sg
+    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200.engine import Engine
+    from paper_1511_06416_b200.io import bundled_network_path, load_network_file
+
+    net, truth = load_network_file(bundled_network_path("koller"))
+    cfg = sg.SamplerConfig(same_m=M, minibatch_size=CASES, num_passes=1, seed=300, rng=args.rng)
+    obs = sg.forward_sample_device(net, truth, CASES, seed=100, hide_fraction=HIDE, mask_seed=200,
+                                   case_base=rank * CASES)
+    comm = (lambda c: dist.all_reduce(c)) if world > 1 else None
+    eng = Engine(net, cfg, case_base=rank * CASES, comm=comm)
+    mb = next(iter(sg.DeviceSource(obs, CASES, CASES)))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    for w in range(args.warmup):
+        eng.visit(mb, w, M)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    eng.sweep_events = []
+    launches0 = _lib.launch_count
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            starts[k].record()
+            eng.visit(mb, args.warmup + k, M)
+            ends[k].record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    sweep_ms = [a.elapsed_time(b) / nsw for a, b, nsw in eng.sweep_events]
+    eng.sweep_events = None
+    err = eng.err.read()
+    if err:
+        raise RuntimeError(f"device error word {err}")
+    ms = statistics.mean(step_ms)
+    sw = statistics.mean(sweep_ms)
+    if world > 1:
+        t = torch.tensor([ms, sw], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, sw = float(t[0]), float(t[1])
+    node_samples = N_VARS * CASES * M  # per GPU per step
+    value = world * node_samples / (ms * 1e-3)
+
+    # ---- e2e through the public API: pinned host minibatch -> device, step, CPTs back to host
+    host_obs = torch.empty((N_VARS, CASES), dtype=torch.int8, pin_memory=True)
+    host_obs.copy_(obs[:, :CASES])
+    hmb = sg.Minibatch(index=0, values=host_obs, weights=np.ones(CASES), num_real=CASES)
+    cpt_host = torch.empty(eng.pack.cells, dtype=torch.float64, pin_memory=True)
+    e2e_steps = max(3, min(args.steps, 50))
+    for w in range(2):
+        eng.visit(hmb, 10_000 + w, M)
+        cpt_host.copy_(eng.cpt, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(e2e_steps):
+        eng.visit(hmb, 20_000 + k, M)
+        cpt_host.copy_(eng.cpt, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    e2e_value = world * node_samples / (e2e_ms * 1e-3)
+
+    if rank == 0:
+        import json as _json
+
+        peaks = {}
+        try:
+            peaks = _json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+            peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+        except Exception:  # noqa: BLE001
+            peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+        algo_bytes = BYTES_PER_NODE_SAMPLE * node_samples
+        achieved = algo_bytes / (sw * 1e-3) / 1e9
+        traffic, traffic_src = load_traffic()
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int8 states, u32 draws, f64 CPTs", "data": "synthetic",
+            "config": workload_config(world, args.rng),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_sweep (sg_sweep)",
+                         "kernel_ms": sw, "algorithmic_bytes_per_launch": algo_bytes,
+                         "bytes_per_node_sample": BYTES_PER_NODE_SAMPLE, "peak_source": peak_src,
+                         "traffic_source": traffic_src, "sweep_share_of_step": sw / ms},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N_VARS * CASES,
+                    "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--rng", choices=["fast", "numpy"], default="fast")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

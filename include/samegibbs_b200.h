@@ -1,0 +1,233 @@
+/*
+ * samegibbs_b200.h -- C-ABI of the B200-native SAME Gibbs sweep.
+ *
+ * The reference (samegibbs 0.1.0, pure Python/NumPy) has no FFI layer: its
+ * boundary is the Python function API.  Each entry point below replaces one
+ * numpy hot site of that API; the Python package paper_1511_06416_b200 binds
+ * them with ctypes (INTEGRATION.md shows the binding).  Conventions:
+ *
+ *   - every pointer argument marked [dev] is device memory, caller-allocated;
+ *   - every call is stream-ordered on the caller's cudaStream_t (passed as
+ *     void*), never synchronises, and returns an sg_status;
+ *   - kernels report data-dependent failures through a device error word
+ *     (int32, bit flags SG_ERR_*), which the caller reads after syncing;
+ *   - no exceptions, no torch types, no allocation inside the library.
+ *
+ * Data layout in HBM:
+ *   obs    int8  [n][ld_obs]        observed state or -1 (missing) per case
+ *   states int8  [n][m][pitch]      lane states; lane (r, c) = replica r of
+ *                                   case c (reference lane r*B + c,
+ *                                   sampler.py:174-187).  Bit 7 set = latent
+ *                                   cell (resampled), low 7 bits = state.
+ *   cpt    f64   [cells]            all CPTs, var-major, row-major rows
+ *   counts u64   [cells]            integer tallies, same indexing as cpt
+ */
+#ifndef SAMEGIBBS_B200_H
+#define SAMEGIBBS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_ABI_VERSION 1
+
+typedef enum sg_status {
+  SG_OK = 0,
+  SG_EINVAL = 1,     /* bad argument (sizes, null pointers, unsupported shape) */
+  SG_ECUDA = 2,      /* a CUDA launch failed (sg_last_error() has the text) */
+  SG_ECAPACITY = 3   /* shape exceeds a compiled-in capacity */
+} sg_status;
+
+/* device error-word bits */
+#define SG_ERR_ZERO_SUPPORT 1u      /* a latent cell had all-zero weights (ZeroSupport) */
+#define SG_ERR_STATE_RANGE 2u       /* an observed state >= its cardinality */
+#define SG_ERR_REJECT_OVERFLOW 4u   /* too many Lemire rejections in one init stream */
+
+/* RNG modes of sg_sweep / sg_init_states */
+#define SG_RNG_FAST 0      /* Philox4x32-10, counters (case, var, replica quad) */
+#define SG_RNG_NUMPY 1     /* numpy Philox4x64-10 stream per variable (bit-exact) */
+#define SG_RNG_INJECTED 2  /* caller-supplied fp64 uniforms, reference order */
+
+/* accumulator modes of sg_accumulate */
+#define SG_ACC_MOVING 0
+#define SG_ACC_EXPONENTIAL 1
+
+/*
+ * Network pack: structure of the Bayesian network flattened into device
+ * arrays (built once per run by netpack.py from network.py's parents,
+ * strides, child links and colour groups; reference sampler.py:190-202,
+ * network.py:42-48, 147-180).  All arrays [dev].
+ */
+typedef struct sg_net {
+  int32_t n;              /* variables */
+  int32_t num_groups;     /* colour groups */
+  int32_t max_card;
+  int32_t max_mb;         /* largest Markov blanket */
+  int32_t max_group;      /* largest colour group */
+  int32_t direct_vars;    /* variables without a conditional table */
+  int64_t cells;          /* total CPT cells == count cells */
+  int64_t rows;           /* total CPT rows */
+  int64_t ptab_size;      /* doubles in the parity conditional table */
+  int64_t ftab_size;      /* uint32 in the fast conditional table */
+  int64_t table_entries;  /* total Markov-blanket configurations */
+  const int32_t* card;        /* [n] */
+  const int32_t* group_start; /* [G+1] into order */
+  const int32_t* order;       /* [n] variables in colour-group order */
+  const int32_t* par_start;   /* [n+1] */
+  const int32_t* par_var;     /* [P] parents of v, ascending */
+  const int32_t* par_stride;  /* [P] mixed-radix stride (first parent most significant) */
+  const int32_t* par_slot;    /* [P] slot of that parent in MB(v) */
+  const int32_t* mb_start;    /* [n+1] */
+  const int32_t* mb_var;      /* [M] Markov blanket of v, ascending */
+  const int32_t* mb_stride;   /* [M] stride of that member in v's table index */
+  const int32_t* chl_start;   /* [n+1] child links of v, ascending child */
+  const int32_t* chl_var;     /* [K] child */
+  const int32_t* chl_vstride; /* [K] stride of v inside the child's row index */
+  const int32_t* chl_slot;    /* [K] slot of the child in MB(v) */
+  const int32_t* chl_pstart;  /* [K+1] */
+  const int32_t* chl_pslot;   /* [Q] slots of the child's other parents */
+  const int32_t* chl_pstride; /* [Q] their strides in the child's row index */
+  const int64_t* cpt_off;     /* [n] first cell of T_v */
+  const int64_t* row_off;     /* [n+1] first row of T_v (rows prefix) */
+  const int64_t* tab_entries; /* [n] MB configurations of v's table, 0 = direct */
+  const int64_t* tab_start;   /* [n+1] prefix of tab_entries */
+  const int64_t* ptab_off;    /* [n] first double of v's parity table */
+  const int64_t* ftab_off;    /* [n] first uint32 of v's fast table */
+  const int32_t* row_var;     /* [rows] variable owning each CPT row */
+} sg_net;
+
+/* A replicated minibatch resident on the device. */
+typedef struct sg_batch {
+  int8_t* states;           /* [dev] [n][m][pitch] */
+  int32_t m;                /* SAME replication factor */
+  int32_t cases;            /* B: cases in the minibatch incl. reference padding */
+  int32_t pitch;            /* row pitch in cases, multiple of 16, >= cases */
+  int32_t num_real;         /* cases with lane weight 1 (c < num_real) */
+  int64_t case_base;        /* global index of case 0 (shard offset) for FAST counters */
+  const int32_t* rank;      /* [dev] [n][ld_rank] latent rank of (v,c) among the
+                               minibatch's latent cases of v (NUMPY / INJECTED) */
+  int32_t ld_rank;
+  int32_t pad_;
+  const int64_t* nmiss;     /* [dev] [n] latent cases of v in the global minibatch */
+} sg_batch;
+
+/* Version of this ABI (SG_ABI_VERSION). */
+int sg_abi_version(void);
+
+/* Text of the last failing call on this host thread ("" if none). */
+const char* sg_last_error(void);
+
+/*
+ * Conditional tables: for every variable whose Markov blanket has at most
+ * SG table capacity configurations, precompute the reference's fp64
+ * full-conditional weights (sampler.py:226-242: parent row, then each child
+ * ascending, left-to-right products, numpy pairwise norm) for every blanket
+ * configuration.  ptab gets cum[0..card-2], norm per entry (bit-exact draw
+ * `u*norm > cum_s`); ftab gets ceil(cum_s/norm * 2^31) thresholds (FAST).
+ * Replaces the per-lane gathers of _resample_variable.
+ */
+int sg_build_tables(const sg_net* net, const double* cpt, double* ptab,
+                    uint32_t* ftab, void* stream);
+
+/*
+ * Latent ranks: rank[v][c] = #{c' < c : obs[v][c'] < 0} and
+ * nmiss[v] = #{c < cases : obs[v][c] < 0}; rank may be NULL (counts only).
+ * scratch: [dev] int64 of
+ * n * ceil(cases / 4096) words.  Replaces the ordering that
+ * np.flatnonzero(values[v] < 0) imposes (sampler.py:180) on the uniforms.
+ */
+int sg_rank_latent(int32_t n, const int8_t* obs, int32_t ld_obs, int32_t cases,
+                   int32_t* rank, int32_t ld_rank, int64_t* nmiss,
+                   int64_t* scratch, void* stream);
+
+/*
+ * Replicate a minibatch into lane states and draw initial latent states
+ * (replicate_minibatch sampler.py:174-187 + init_latent sampler.py:205-214).
+ * rng_mode FAST: key = fast_key; NUMPY: keys [dev] [n][2] = stream_key(seed,
+ * "latent_init", pass, mb, v), numpy Generator.integers(0, card) (Lemire on
+ * 32-bit halves) reproduced bit-exactly.  rej_scratch: [dev] int64 of
+ * n * 66 words (NUMPY only).  err: [dev] error word.
+ */
+int sg_init_states(const sg_net* net, const sg_batch* batch, const int8_t* obs,
+                   int32_t ld_obs, int32_t rng_mode, uint64_t fast_key,
+                   const uint64_t* keys, int64_t* rej_scratch, int32_t* err,
+                   void* stream);
+
+/*
+ * One chromatic Gibbs sweep over every lane of the batch (gibbs_pass
+ * sampler.py:251-284) and, when counts != NULL, the count tally of the final
+ * assignments (tally_counts model.py:148-165, lanes c < num_real only),
+ * added into counts (caller zeroes).
+ *   FAST:     fast_key = derive_seed(seed, "sweep", pass, mb, s)
+ *   NUMPY:    keys [dev] [n][2] = stream_key(sweep_seed, "var", v)
+ *   INJECTED: uniforms [dev] concatenated per variable (ascending v), each
+ *             m*nmiss[v] long in reference lane order; inj_off [dev] [n]
+ */
+int sg_sweep(const sg_net* net, const sg_batch* batch, const double* cpt,
+             const double* ptab, const uint32_t* ftab, int32_t rng_mode,
+             uint64_t fast_key, const uint64_t* keys, const double* uniforms,
+             const int64_t* inj_off, uint64_t* counts, int32_t* err,
+             void* stream);
+
+/* Count tally alone (tally_counts model.py:148-165) over lanes c < num_real. */
+int sg_tally(const sg_net* net, const sg_batch* batch, uint64_t* counts,
+             void* stream);
+
+/*
+ * Weighted tally with arbitrary fp64 lane weights w[m*cases] (the
+ * tally_counts API with non-0/1 weights); fp64 atomics, not order-exact.
+ */
+int sg_tally_weighted(const sg_net* net, const sg_batch* batch,
+                      const double* weights, double* counts, void* stream);
+
+/*
+ * Count accumulator (update_moving_sum / update_exponential,
+ * sampler.py:337-351, CountSet.add/scale model.py:56-62), fp64 in the
+ * reference's rounding order.  MOVING: total += -prev (if prev != NULL),
+ * total += new.  EXPONENTIAL: total *= decay, total += new.
+ */
+int sg_accumulate(int32_t mode, double* total, const uint64_t* new_counts,
+                  const uint64_t* prev_counts, double decay, int64_t cells,
+                  void* stream);
+
+/* Same with fp64 count deltas (CountSet objects that are not integer). */
+int sg_accumulate_f64(int32_t mode, double* total, const double* new_counts,
+                      const double* prev_counts, double decay, int64_t cells,
+                      void* stream);
+
+/* Posterior-mean rows (c + alpha_v) / sum (mean_cpts model.py:188-194), bit-exact. */
+int sg_mean_cpts(const sg_net* net, const double* total, const double* alpha,
+                 double* cpt_out, void* stream);
+
+/*
+ * Dirichlet row draws (sample_cpts model.py:179-185): gamma(c + alpha_v) by
+ * Marsaglia-Tsang (shape < 1 boosted), in log space, Philox4x32 keyed by
+ * key = derive_seed(seed, "cpt_update", pass, mb).  Statistical parity.
+ */
+int sg_sample_cpts(const sg_net* net, const double* total, const double* alpha,
+                   uint64_t key, double* cpt_out, void* stream);
+
+/*
+ * Forward sampling + masking on the device (forward_sample datagen.py:91-107,
+ * mask datagen.py:110-121), bit-exact with the reference for dense inputs:
+ * keys [dev] [n][2] = stream_key(seed, "forward_sample", v); topo [dev] [n];
+ * out int8 [n][ld_out].  mask_key = stream_key(mask_seed, "mask") (two
+ * words); hide <= 0 disables masking.  Entry k of the mask stream is
+ * (case k / n, variable k % n), the reference's case-major order.
+ */
+int sg_forward_sample(const sg_net* net, const double* cpt, const int32_t* topo,
+                      const uint64_t* keys, int64_t cases, int64_t case_base,
+                      int8_t* out, int64_t ld_out, double hide,
+                      uint64_t mask_key0, uint64_t mask_key1, void* stream);
+
+/* Largest state of each variable's observed cells (range check, sampler.py:429-430). */
+int sg_check_range(const sg_net* net, const int8_t* obs, int32_t ld_obs,
+                   int32_t cases, int32_t* err, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SAMEGIBBS_B200_H */

@@ -1,0 +1,72 @@
+"""Ahead-of-time build of the CUDA library (sm_100a) into the package directory.
+
+The library is a plain C-ABI shared object (no torch types), built with nvcc
+directly so that it travels with the repository snapshot to the GPU box.
+``--fmad=false`` keeps every fp64 product and sum separately rounded, as
+numpy rounds them (bit-exact contract).
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libsamegibbs_b200.so"
+SOURCES = ["sg_common.cu", "sg_tables.cu", "sg_sweep.cu", "sg_batch.cu", "sg_model.cu", "sg_data.cu"]
+HEADERS = ["sg_device.cuh"]
+ROOT = PKG.parent
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    return "nvcc"
+
+
+def flags() -> list[str]:
+    return [
+        "-gencode", "arch=compute_100a,code=sm_100a",
+        "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
+        "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
+        "-I", str(ROOT / "include"),
+    ]
+
+
+def _stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "samegibbs_b200.h"]
+    return any(p.stat().st_mtime > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every .cu into libsamegibbs_b200.so (objects in csrc/build)."""
+    if not force and not _stale():
+        return LIB
+    out = CSRC / "build"
+    out.mkdir(exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        obj = out / (Path(src).stem + ".o")
+        cmd = [nvcc(), *flags(), "-c", str(CSRC / src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        objs.append(str(obj))
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
+           "-Xcompiler", "-fPIC"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    print(LIB)

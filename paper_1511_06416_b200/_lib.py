@@ -1,0 +1,116 @@
+"""ctypes binding of the C-ABI library ``libsamegibbs_b200.so``.
+
+This is the whole Python<->CUDA boundary: plain pointers, sizes and a
+``cudaStream_t`` (``torch.cuda.current_stream().cuda_stream``) go in, an
+``sg_status`` comes out.  The structures mirror ``include/samegibbs_b200.h``
+field for field.  There is no fallback: if the library is missing or the
+machine has no CUDA device, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, c_double, c_int32, c_int64, c_uint64, c_void_p
+from pathlib import Path
+
+from .errors import DeviceError
+
+LIB_PATH = Path(__file__).resolve().parent / "libsamegibbs_b200.so"
+
+SG_OK, SG_EINVAL, SG_ECUDA, SG_ECAPACITY = 0, 1, 2, 3
+SG_ERR_ZERO_SUPPORT, SG_ERR_STATE_RANGE, SG_ERR_REJECT_OVERFLOW = 1, 2, 4
+SG_RNG_FAST, SG_RNG_NUMPY, SG_RNG_INJECTED = 0, 1, 2
+SG_ACC_MOVING, SG_ACC_EXPONENTIAL = 0, 1
+REJ_SLACK = 64
+
+NET_POINTERS = (
+    "card", "group_start", "order", "par_start", "par_var", "par_stride", "par_slot",
+    "mb_start", "mb_var", "mb_stride", "chl_start", "chl_var", "chl_vstride", "chl_slot",
+    "chl_pstart", "chl_pslot", "chl_pstride", "cpt_off", "row_off", "tab_entries",
+    "tab_start", "ptab_off", "ftab_off", "row_var",
+)
+
+
+class SgNet(ctypes.Structure):
+    _fields_ = [
+        ("n", c_int32), ("num_groups", c_int32), ("max_card", c_int32), ("max_mb", c_int32),
+        ("max_group", c_int32), ("direct_vars", c_int32),
+        ("cells", c_int64), ("rows", c_int64), ("ptab_size", c_int64), ("ftab_size", c_int64),
+        ("table_entries", c_int64),
+    ] + [(name, c_void_p) for name in NET_POINTERS]
+
+
+class SgBatch(ctypes.Structure):
+    _fields_ = [
+        ("states", c_void_p), ("m", c_int32), ("cases", c_int32), ("pitch", c_int32),
+        ("num_real", c_int32), ("case_base", c_int64), ("rank", c_void_p), ("ld_rank", c_int32),
+        ("pad_", c_int32), ("nmiss", c_void_p),
+    ]
+
+
+_SIGNATURES = {
+    "sg_abi_version": ([], c_int32),
+    "sg_last_error": ([], ctypes.c_char_p),
+    "sg_build_tables": ([POINTER(SgNet), c_void_p, c_void_p, c_void_p, c_void_p], c_int32),
+    "sg_rank_latent": ([c_int32, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p,
+                        c_void_p], c_int32),
+    "sg_init_states": ([POINTER(SgNet), POINTER(SgBatch), c_void_p, c_int32, c_int32, c_uint64, c_void_p,
+                        c_void_p, c_void_p, c_void_p], c_int32),
+    "sg_sweep": ([POINTER(SgNet), POINTER(SgBatch), c_void_p, c_void_p, c_void_p, c_int32, c_uint64,
+                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p], c_int32),
+    "sg_tally": ([POINTER(SgNet), POINTER(SgBatch), c_void_p, c_void_p], c_int32),
+    "sg_tally_weighted": ([POINTER(SgNet), POINTER(SgBatch), c_void_p, c_void_p, c_void_p], c_int32),
+    "sg_accumulate": ([c_int32, c_void_p, c_void_p, c_void_p, c_double, c_int64, c_void_p], c_int32),
+    "sg_accumulate_f64": ([c_int32, c_void_p, c_void_p, c_void_p, c_double, c_int64, c_void_p], c_int32),
+    "sg_mean_cpts": ([POINTER(SgNet), c_void_p, c_void_p, c_void_p, c_void_p], c_int32),
+    "sg_sample_cpts": ([POINTER(SgNet), c_void_p, c_void_p, c_uint64, c_void_p, c_void_p], c_int32),
+    "sg_forward_sample": ([POINTER(SgNet), c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64,
+                           c_double, c_uint64, c_uint64, c_void_p], c_int32),
+    "sg_check_range": ([POINTER(SgNet), c_void_p, c_int32, c_int32, c_void_p, c_void_p], c_int32),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lib = None
+
+
+def load(path: Path | None = None) -> ctypes.CDLL:
+    """Load (once) and type the library; raises DeviceError when it is absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise DeviceError(
+            f"CUDA library {p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.sg_abi_version() != 1:
+        raise DeviceError("libsamegibbs_b200 ABI version mismatch")
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    if status != SG_OK:
+        msg = load().sg_last_error().decode(errors="replace")
+        raise DeviceError(f"{what} failed with status {status}: {msg}")
+
+
+# kernels each entry point launches (for the bench's gpu_launches count)
+KERNELS_PER_CALL = {
+    "sg_build_tables": 1, "sg_rank_latent": 3, "sg_init_states": 1, "sg_sweep": 1, "sg_tally": 1,
+    "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
+    "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
+}
+launch_count = 0
+
+
+def call(name: str, *args) -> None:
+    global launch_count
+    check(getattr(load(), name)(*args), name)
+    launch_count += KERNELS_PER_CALL.get(name, 0)

@@ -1,0 +1,169 @@
+// Device-side building blocks shared by every kernel of the sweep path.
+//
+//  * Philox4x64-10 exactly as numpy's Philox bit generator consumes it
+//    (reference rng.py:23-25 -> numpy Generator.random / integers), and
+//    Philox4x32-10 (Random123 constants) for the fast RNG mode.
+//  * numpy's pairwise float64 summation, which decides `norm` in
+//    _resample_variable (sampler.py:242) and the row sums of mean_cpts
+//    (model.py:193) for rows of 8 or more states.
+//  * The reference's full-conditional weight product (sampler.py:226-240).
+//
+// The library is compiled with --fmad=false and every fp64 step uses the
+// explicitly rounded intrinsics, so no product/sum is ever contracted into an
+// FMA: the reference rounds each numpy operation separately.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/samegibbs_b200.h"
+
+#define SG_THREADS 256
+#define SG_MAX_CARD 64      // states per variable (int8 lane state keeps 7 bits)
+#define SG_MAX_MB 64        // Markov-blanket members gathered per draw
+#define SG_REJ_SLACK 64     // Lemire rejections tolerated per init stream
+
+namespace sg {
+
+// ---------------------------------------------------------------- Philox
+struct u64x4 {
+  uint64_t a, b, c, d;
+};
+struct u32x4 {
+  uint32_t a, b, c, d;
+};
+
+__device__ __forceinline__ u64x4 philox4x64_10(u64x4 x, uint64_t k0, uint64_t k1) {
+  const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  const uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += W0;
+      k1 += W1;
+    }
+    const uint64_t lo0 = M0 * x.a, hi0 = __umul64hi(M0, x.a);
+    const uint64_t lo1 = M1 * x.c, hi1 = __umul64hi(M1, x.c);
+    x = u64x4{hi1 ^ x.b ^ k0, lo1, hi0 ^ x.d ^ k1, lo0};
+  }
+  return x;
+}
+
+__device__ __forceinline__ u32x4 philox4x32_10(u32x4 x, uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += W0;
+      k1 += W1;
+    }
+    const uint32_t lo0 = M0 * x.a, hi0 = __umulhi(M0, x.a);
+    const uint32_t lo1 = M1 * x.c, hi1 = __umulhi(M1, x.c);
+    x = u32x4{hi1 ^ x.b ^ k0, lo1, hi0 ^ x.d ^ k1, lo0};
+  }
+  return x;
+}
+
+__device__ __forceinline__ uint64_t pick(const u64x4& w, int i) {
+  return i == 0 ? w.a : i == 1 ? w.b : i == 2 ? w.c : w.d;
+}
+__device__ __forceinline__ uint32_t pick(const u32x4& w, int i) {
+  return i == 0 ? w.a : i == 1 ? w.b : i == 2 ? w.c : w.d;
+}
+
+// numpy Generator(Philox(key)).random(): draw i of the stream.
+__device__ __forceinline__ uint64_t np_raw64(uint64_t i, uint64_t k0, uint64_t k1) {
+  const u64x4 w = philox4x64_10(u64x4{(i >> 2) + 1ull, 0ull, 0ull, 0ull}, k0, k1);
+  return pick(w, int(i & 3));
+}
+__device__ __forceinline__ double np_uniform(uint64_t i, uint64_t k0, uint64_t k1) {
+  return double(np_raw64(i, k0, k1) >> 11) * 0x1.0p-53;
+}
+// 32-bit word j of the stream as numpy's next_uint32 hands it out: low half,
+// then high half of each 64-bit draw.
+__device__ __forceinline__ uint32_t np_word32(uint64_t j, uint64_t k0, uint64_t k1) {
+  const uint64_t w = np_raw64(j >> 1, k0, k1);
+  return (j & 1) ? uint32_t(w >> 32) : uint32_t(w);
+}
+
+// Fast-mode counter for (case, variable, replica quad, purpose).
+__device__ __forceinline__ u32x4 fast_block(uint64_t key, uint64_t gcase, uint32_t v,
+                                            uint32_t quad, uint32_t purpose) {
+  return philox4x32_10(u32x4{uint32_t(gcase), v, quad, uint32_t(gcase >> 32) ^ (purpose << 24)},
+                       uint32_t(key), uint32_t(key >> 32));
+}
+
+// ---------------------------------------------------------------- fp64
+// numpy pairwise_sum (8 accumulators from 8 elements up, halving above 128),
+// i.e. ndarray.sum(axis=-1) of a contiguous row of length n.
+__device__ __forceinline__ double np_pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = __dadd_rn(s, a[i]);
+    return s;
+  }
+  // n <= SG_MAX_CARD (64) <= 128: single block of 8 accumulators.
+  double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+    r0 = __dadd_rn(r0, a[i + 0]);
+    r1 = __dadd_rn(r1, a[i + 1]);
+    r2 = __dadd_rn(r2, a[i + 2]);
+    r3 = __dadd_rn(r3, a[i + 3]);
+    r4 = __dadd_rn(r4, a[i + 4]);
+    r5 = __dadd_rn(r5, a[i + 5]);
+    r6 = __dadd_rn(r6, a[i + 6]);
+    r7 = __dadd_rn(r7, a[i + 7]);
+  }
+  double s = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                       __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; ++i) s = __dadd_rn(s, a[i]);
+  return s;
+}
+
+// Reference full-conditional weights of v given its Markov-blanket states
+// s[slot] (sampler.py:226-240): w = T_v[cfg, :], then for each child c in
+// ascending order w[t] *= T_c[cfg0_c + t*stride_vc, x_c].
+__device__ __forceinline__ void conditional_weights(const sg_net& net, int v, const int* s,
+                                                    const double* __restrict__ cpt, double* w) {
+  const int card = __ldg(net.card + v);
+  int64_t cfg = 0;
+  for (int j = __ldg(net.par_start + v), e = __ldg(net.par_start + v + 1); j < e; ++j)
+    cfg += int64_t(s[__ldg(net.par_slot + j)]) * __ldg(net.par_stride + j);
+  const double* row = cpt + __ldg(net.cpt_off + v) + cfg * card;
+  for (int t = 0; t < card; ++t) w[t] = __ldg(row + t);
+  for (int k = __ldg(net.chl_start + v), ke = __ldg(net.chl_start + v + 1); k < ke; ++k) {
+    const int c = __ldg(net.chl_var + k);
+    const int cc = __ldg(net.card + c);
+    const int xc = s[__ldg(net.chl_slot + k)];
+    int64_t cfg0 = 0;
+    for (int q = __ldg(net.chl_pstart + k), qe = __ldg(net.chl_pstart + k + 1); q < qe; ++q)
+      cfg0 += int64_t(s[__ldg(net.chl_pslot + q)]) * __ldg(net.chl_pstride + q);
+    const int64_t vs = __ldg(net.chl_vstride + k);
+    const double* tc = cpt + __ldg(net.cpt_off + c) + xc;
+    for (int t = 0; t < card; ++t) w[t] = __dmul_rn(w[t], __ldg(tc + (cfg0 + t * vs) * cc));
+  }
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace sg
+
+// ---------------------------------------------------------------- host side
+namespace sg {
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+}  // namespace sg
+
+#define SG_REQUIRE(cond, ...)        \
+  do {                               \
+    if (!(cond)) {                   \
+      ::sg::set_error(__VA_ARGS__);  \
+      return SG_EINVAL;              \
+    }                                \
+  } while (0)

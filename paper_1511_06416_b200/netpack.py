@@ -1,0 +1,292 @@
+"""Flatten a Network + colouring into the device arrays of ``sg_net``.
+
+Host precompute, once per run (reference: ``_NetCache`` sampler.py:190-202,
+``parent_strides`` network.py:42-48, ``color_graph(moralize(net))``
+sampler.py:409).  Besides the reference's parent strides and child links it
+derives each variable's Markov blanket and the blanket -> table index map
+used by the conditional tables (sg_tables.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._lib import NET_POINTERS, SgNet
+from .network import Coloring, Network, color_graph, moralize
+
+# A variable's full conditional is tabulated when its blanket has at most this
+# many configurations and the tables stay within the byte budget below; the
+# others are evaluated per lane from the CPTs ("direct" variables).
+TABLE_MAX_ENTRIES = 1 << 16
+TABLE_BUDGET_BYTES = 512 << 20
+MAX_CARD = 64
+MAX_MB = 64
+
+
+@dataclass
+class NetLayout:
+    """Host-side (numpy) description; the device copy is built by :class:`NetPack`."""
+
+    n: int
+    cards: np.ndarray
+    rows: np.ndarray
+    cpt_off: np.ndarray      # [n+1] cell prefix
+    row_off: np.ndarray      # [n+1]
+    groups: tuple[tuple[int, ...], ...]
+    topo: np.ndarray
+    int32: dict[str, np.ndarray]
+    int64: dict[str, np.ndarray]
+    scalars: dict[str, int]
+
+    @property
+    def cells(self) -> int:
+        return int(self.cpt_off[-1])
+
+
+def layout(net: Network, coloring: Coloring | None = None,
+           table_max_entries: int = TABLE_MAX_ENTRIES,
+           table_budget_bytes: int = TABLE_BUDGET_BYTES) -> NetLayout:
+    n = net.num_vars
+    if coloring is None:
+        coloring = color_graph(moralize(net))
+    cards = np.asarray(net.cardinalities, dtype=np.int64)
+    if n and cards.max() > MAX_CARD:
+        raise ValueError(f"cardinality {int(cards.max())} exceeds the device limit {MAX_CARD}")
+    rows = np.array([net.num_parent_configs(v) for v in range(n)], dtype=np.int64)
+    cpt_off = np.zeros(n + 1, dtype=np.int64)
+    cpt_off[1:] = np.cumsum(rows * cards)
+    row_off = np.zeros(n + 1, dtype=np.int64)
+    row_off[1:] = np.cumsum(rows)
+
+    order = [v for grp in coloring.groups for v in grp]
+    group_start = np.zeros(len(coloring.groups) + 1, dtype=np.int64)
+    group_start[1:] = np.cumsum([len(g) for g in coloring.groups])
+
+    par_start, par_var, par_stride, par_slot = [0], [], [], []
+    mb_start, mb_var, mb_stride = [0], [], []
+    chl_start, chl_var, chl_vstride, chl_slot = [0], [], [], []
+    chl_pstart, chl_pslot, chl_pstride = [0], [], []
+    mb_sizes, mb_confs = [], []
+    blankets = []
+    for v in range(n):
+        blanket = set(net.parents[v]) | set(net.children[v])
+        for c in net.children[v]:
+            blanket |= set(net.parents[c])
+        blanket.discard(v)
+        mb = sorted(blanket)
+        if len(mb) > MAX_MB:
+            raise ValueError(f"Markov blanket of variable {v} has {len(mb)} members (limit {MAX_MB})")
+        blankets.append(mb)
+        slot = {u: k for k, u in enumerate(mb)}
+        strides = []
+        acc = 1
+        for u in reversed(mb):
+            strides.append(acc)
+            acc = acc * int(cards[u])
+        strides.reverse()
+        confs = acc
+        mb_confs.append(confs)
+        mb_sizes.append(len(mb))
+        mb_var.extend(mb)
+        # strides of huge blankets are meaningless (direct variables); clamp to int32
+        mb_stride.extend(min(s, 2**31 - 1) for s in strides)
+        mb_start.append(len(mb_var))
+        ps = net.parent_strides(v)
+        for j, p in enumerate(net.parents[v]):
+            par_var.append(p)
+            par_stride.append(int(ps[j]))
+            par_slot.append(slot[p])
+        par_start.append(len(par_var))
+        for c in net.children[v]:
+            cps = net.parent_strides(c)
+            j = net.parents[c].index(v)
+            chl_var.append(c)
+            chl_vstride.append(int(cps[j]))
+            chl_slot.append(slot[c])
+            for q, p in enumerate(net.parents[c]):
+                if p != v:
+                    chl_pslot.append(slot[p])
+                    chl_pstride.append(int(cps[q]))
+            chl_pstart.append(len(chl_pslot))
+        chl_start.append(len(chl_var))
+
+    # choose tabulated variables: smallest tables first under the byte budget
+    tab_entries = np.zeros(n, dtype=np.int64)
+    budget = table_budget_bytes
+    for v in sorted(range(n), key=lambda v: mb_confs[v]):
+        e = mb_confs[v]
+        nbytes = e * int(cards[v]) * 8
+        if e <= table_max_entries and nbytes <= budget:
+            tab_entries[v] = e
+            budget -= nbytes
+    tab_start = np.zeros(n + 1, dtype=np.int64)
+    tab_start[1:] = np.cumsum(tab_entries)
+    ptab_len = tab_entries * cards
+    ftab_len = tab_entries * (cards - 1)
+    ptab_off = np.zeros(n, dtype=np.int64)
+    ftab_off = np.zeros(n, dtype=np.int64)
+    if n:
+        ptab_off[1:] = np.cumsum(ptab_len)[:-1]
+        ftab_off[1:] = np.cumsum(ftab_len)[:-1]
+    row_var = np.repeat(np.arange(n, dtype=np.int64), rows)
+
+    def i32(x):
+        a = np.asarray(x, dtype=np.int64)
+        if a.size and (a.max() > 2**31 - 1 or a.min() < -2**31):
+            raise ValueError("index overflow in network pack")
+        return a.astype(np.int32)
+
+    int32 = {
+        "card": i32(cards), "group_start": i32(group_start), "order": i32(order),
+        "par_start": i32(par_start), "par_var": i32(par_var), "par_stride": i32(par_stride),
+        "par_slot": i32(par_slot), "mb_start": i32(mb_start), "mb_var": i32(mb_var),
+        "mb_stride": i32(mb_stride), "chl_start": i32(chl_start), "chl_var": i32(chl_var),
+        "chl_vstride": i32(chl_vstride), "chl_slot": i32(chl_slot), "chl_pstart": i32(chl_pstart),
+        "chl_pslot": i32(chl_pslot), "chl_pstride": i32(chl_pstride), "row_var": i32(row_var),
+    }
+    int64 = {
+        "cpt_off": cpt_off[:n].copy(), "row_off": row_off, "tab_entries": tab_entries,
+        "tab_start": tab_start, "ptab_off": ptab_off, "ftab_off": ftab_off,
+    }
+    scalars = {
+        "n": n,
+        "num_groups": len(coloring.groups),
+        "max_card": int(cards.max()) if n else 0,
+        "max_mb": max(mb_sizes) if n else 0,
+        "max_group": max((len(g) for g in coloring.groups), default=0),
+        "direct_vars": int((tab_entries == 0).sum()),
+        "cells": int(cpt_off[-1]),
+        "rows": int(row_off[-1]),
+        "ptab_size": int(ptab_len.sum()),
+        "ftab_size": int(ftab_len.sum()),
+        "table_entries": int(tab_entries.sum()),
+    }
+    return NetLayout(n=n, cards=cards, rows=rows, cpt_off=cpt_off, row_off=row_off,
+                     groups=coloring.groups, topo=np.asarray(net.topo_order, dtype=np.int32),
+                     int32=int32, int64=int64, scalars=scalars)
+
+
+class NetPack:
+    """Device-resident ``sg_net``: two flat tensors plus the C struct of pointers."""
+
+    def __init__(self, net: Network, device: torch.device, coloring: Coloring | None = None, **kw):
+        self.net = net
+        self.layout = lay = layout(net, coloring, **kw)
+        self.device = device
+        self._views: dict[str, torch.Tensor] = {}
+        offs32, offs64 = {}, {}
+        parts32, parts64 = [], []
+        pos = 0
+        for k, a in lay.int32.items():
+            offs32[k] = pos
+            pos += max(len(a), 1)
+            parts32.append(a if len(a) else np.zeros(1, np.int32))
+        pos64 = 0
+        for k, a in lay.int64.items():
+            offs64[k] = pos64
+            pos64 += max(len(a), 1)
+            parts64.append(a if len(a) else np.zeros(1, np.int64))
+        self.buf32 = torch.from_numpy(np.concatenate(parts32)).to(device)
+        self.buf64 = torch.from_numpy(np.concatenate(parts64)).to(device)
+        self.topo = torch.from_numpy(lay.topo).to(device)
+        s = SgNet()
+        for k, v in lay.scalars.items():
+            setattr(s, k, v)
+        for k in NET_POINTERS:
+            if k in offs32:
+                setattr(s, k, self.buf32.data_ptr() + 4 * offs32[k])
+            else:
+                setattr(s, k, self.buf64.data_ptr() + 8 * offs64[k])
+        self.struct = s
+        self.ref = ctypes.byref(self.struct)
+
+    @property
+    def n(self) -> int:
+        return self.layout.n
+
+    @property
+    def cells(self) -> int:
+        return self.layout.cells
+
+    def flatten(self, tables) -> np.ndarray:
+        """Concatenate per-variable tables (CptSet/CountSet order) into one fp64 vector."""
+        if len(tables) != self.n:
+            raise ValueError("table count does not match the network")
+        out = np.empty(self.cells, dtype=np.float64)
+        for v, t in enumerate(tables):
+            a, b = self.layout.cpt_off[v], self.layout.cpt_off[v + 1]
+            t = np.asarray(t, dtype=np.float64)
+            if t.size != b - a:
+                raise ValueError(f"table {v} has {t.size} cells, expected {b - a}")
+            out[a:b] = t.ravel()
+        return out
+
+    def split(self, flat: np.ndarray) -> list[np.ndarray]:
+        lay = self.layout
+        return [flat[lay.cpt_off[v]:lay.cpt_off[v + 1]].reshape(int(lay.rows[v]), int(lay.cards[v])).copy()
+                for v in range(self.n)]
+
+
+class TablePack:
+    """``sg_net`` carrying only the row layout of a table set (shapes).
+
+    The row-wise kernels (sg_mean_cpts, sg_sample_cpts) read nothing but
+    card / cpt_off / row_off / row_var, so a bare CountSet can be processed
+    without its network (the reference's mean_cpts/sample_cpts take none).
+    """
+
+    _cache: dict = {}
+
+    def __init__(self, shapes, device: torch.device):
+        n = len(shapes)
+        rows = np.array([r for r, _ in shapes], dtype=np.int64)
+        cards = np.array([k for _, k in shapes], dtype=np.int64)
+        if n and cards.max() > MAX_CARD:
+            raise ValueError(f"cardinality {int(cards.max())} exceeds the device limit {MAX_CARD}")
+        cpt_off = np.zeros(n + 1, dtype=np.int64)
+        cpt_off[1:] = np.cumsum(rows * cards)
+        row_off = np.zeros(n + 1, dtype=np.int64)
+        row_off[1:] = np.cumsum(rows)
+        self.cpt_off, self.rows, self.cards = cpt_off, rows, cards
+        self.card_t = torch.from_numpy(cards.astype(np.int32)).to(device)
+        self.rowvar_t = torch.from_numpy(np.repeat(np.arange(n, dtype=np.int32), rows)).to(device)
+        self.off_t = torch.from_numpy(np.concatenate([cpt_off[:n], row_off])).to(device)
+        s = SgNet()
+        s.n = n
+        s.max_card = int(cards.max()) if n else 0
+        s.cells = int(cpt_off[-1])
+        s.rows = int(row_off[-1])
+        s.card = self.card_t.data_ptr()
+        s.row_var = self.rowvar_t.data_ptr()
+        s.cpt_off = self.off_t.data_ptr()
+        s.row_off = self.off_t.data_ptr() + 8 * n
+        self.struct = s
+        self.ref = ctypes.byref(s)
+
+    @classmethod
+    def get(cls, shapes, device: torch.device) -> "TablePack":
+        key = (shapes, device.index)
+        pack = cls._cache.get(key)
+        if pack is None:
+            pack = cls._cache[key] = cls(shapes, device)
+        return pack
+
+    @property
+    def n(self) -> int:
+        return len(self.rows)
+
+    @property
+    def cells(self) -> int:
+        return int(self.cpt_off[-1])
+
+    def flatten(self, tables) -> np.ndarray:
+        return np.concatenate([np.asarray(t, dtype=np.float64).ravel() for t in tables]) if tables else \
+            np.zeros(0)
+
+    def split(self, flat: np.ndarray) -> list[np.ndarray]:
+        return [flat[self.cpt_off[v]:self.cpt_off[v + 1]].reshape(int(self.rows[v]), int(self.cards[v])).copy()
+                for v in range(self.n)]
