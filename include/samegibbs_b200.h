@@ -96,7 +96,21 @@ typedef struct sg_net {
   const int64_t* ptab_off;    /* [n] first double of v's parity table */
   const int64_t* ftab_off;    /* [n] first uint32 of v's fast table */
   const int32_t* row_var;     /* [rows] variable owning each CPT row */
+  /* joint-state tally: when prod(card) <= SG_JOINT_MAX the sweep histograms
+     whole-lane configurations J = sum_v x_v * joint_radix[v] and expands
+     them to CPT cells through joint_cell[J][v] (0 disables). */
+  int64_t joint_size;
+  const int32_t* joint_radix; /* [n] */
+  const int32_t* joint_cell;  /* [joint_size][n] */
+  /* compact per-variable draw descriptor, SG_DESC_WORDS int32 each:
+     card, nmb (-1 = evaluate from CPTs), ftab offset, ptab offset,
+     mb_var[SG_DESC_MB], mb_stride[SG_DESC_MB] */
+  const int32_t* var_desc;    /* [n][SG_DESC_WORDS] */
 } sg_net;
+
+#define SG_JOINT_MAX 128
+#define SG_DESC_MB 8
+#define SG_DESC_WORDS (4 + 2 * SG_DESC_MB)
 
 /* A replicated minibatch resident on the device. */
 typedef struct sg_batch {
@@ -126,7 +140,9 @@ const char* sg_last_error(void);
  * ascending, left-to-right products, numpy pairwise norm) for every blanket
  * configuration.  ptab gets cum[0..card-2], norm per entry (bit-exact draw
  * `u*norm > cum_s`); ftab gets ceil(cum_s/norm * 2^31) thresholds (FAST).
- * Replaces the per-lane gathers of _resample_variable.
+ * ftab holds ftab_size + 1 words: the last one is set non-zero when some
+ * entry has no support (all weights zero), which arms the ZeroSupport
+ * check in sg_sweep.  Replaces the per-lane gathers of _resample_variable.
  */
 int sg_build_tables(const sg_net* net, const double* cpt, double* ptab,
                     uint32_t* ftab, void* stream);
@@ -160,16 +176,17 @@ int sg_init_states(const sg_net* net, const sg_batch* batch, const int8_t* obs,
  * sampler.py:251-284) and, when counts != NULL, the count tally of the final
  * assignments (tally_counts model.py:148-165, lanes c < num_real only),
  * added into counts (caller zeroes).
- *   FAST:     fast_key = derive_seed(seed, "sweep", pass, mb, s)
+ *   FAST:     fast_key = derive_seed(seed, "sweep", pass, mb, s), or read from
+ *             fast_key_dev [dev] when that is non-NULL (graph replay)
  *   NUMPY:    keys [dev] [n][2] = stream_key(sweep_seed, "var", v)
  *   INJECTED: uniforms [dev] concatenated per variable (ascending v), each
  *             m*nmiss[v] long in reference lane order; inj_off [dev] [n]
  */
 int sg_sweep(const sg_net* net, const sg_batch* batch, const double* cpt,
              const double* ptab, const uint32_t* ftab, int32_t rng_mode,
-             uint64_t fast_key, const uint64_t* keys, const double* uniforms,
-             const int64_t* inj_off, uint64_t* counts, int32_t* err,
-             void* stream);
+             uint64_t fast_key, const uint64_t* fast_key_dev, const uint64_t* keys,
+             const double* uniforms, const int64_t* inj_off, uint64_t* counts,
+             int32_t* err, void* stream);
 
 /* Count tally alone (tally_counts model.py:148-165) over lanes c < num_real. */
 int sg_tally(const sg_net* net, const sg_batch* batch, uint64_t* counts,
@@ -207,7 +224,7 @@ int sg_mean_cpts(const sg_net* net, const double* total, const double* alpha,
  * key = derive_seed(seed, "cpt_update", pass, mb).  Statistical parity.
  */
 int sg_sample_cpts(const sg_net* net, const double* total, const double* alpha,
-                   uint64_t key, double* cpt_out, void* stream);
+                   uint64_t key, const uint64_t* key_dev, double* cpt_out, void* stream);
 
 /*
  * Forward sampling + masking on the device (forward_sample datagen.py:91-107,
@@ -221,6 +238,69 @@ int sg_forward_sample(const sg_net* net, const double* cpt, const int32_t* topo,
                       const uint64_t* keys, int64_t cases, int64_t case_base,
                       int8_t* out, int64_t ld_out, double hide,
                       uint64_t mask_key0, uint64_t mask_key1, void* stream);
+
+/*
+ * Packed-lane path for small networks (FAST RNG mode): when the whole lane
+ * state fits in one byte (sum of per-variable field widths <= 7), a lane is
+ * a uint8 word S; the conditional table of v is indexed by S & mbmask[v];
+ * cases are bucketed by latent pattern so warps run one variable loop.
+ * Draws and counters equal sg_sweep's FAST mode (same states and counts).
+ *   lanes   uint8 [m][lane_ld]  lane words, slot order
+ *   pattern uint8 [cases]       latent-variable bit mask of each slot
+ *   case_id int32 [cases]       minibatch case held by each slot
+ */
+#define SG_SMALL_MAXV 7
+#define SG_SMALL_MAXBITS 7
+
+typedef struct sg_small {
+  int32_t n;          /* variables (<= SG_SMALL_MAXV) */
+  int32_t bits;       /* lane-word bits (<= SG_SMALL_MAXBITS) */
+  int32_t tab_words;  /* uint32 words of the sparse conditional table */
+  int32_t pad_;
+  int32_t order[SG_SMALL_MAXV];   /* colour-group order */
+  int32_t off[SG_SMALL_MAXV];     /* bit offset of v's field */
+  int32_t width[SG_SMALL_MAXV];   /* bit width of v's field */
+  uint32_t mbmask[SG_SMALL_MAXV]; /* lane-word bits of v's Markov blanket */
+  int32_t card[SG_SMALL_MAXV];
+  int32_t toff[SG_SMALL_MAXV];    /* first word of v's sparse table ((card-1) words per S) */
+} sg_small;
+
+/* Gather sg_build_tables' FAST thresholds into the sparse per-lane-word table
+   stab [tab_words]. */
+int sg_small_tables(const sg_net* net, const sg_small* sp, const uint32_t* ftab,
+                    uint32_t* stab, void* stream);
+
+/* Bucket the minibatch's cases by latent pattern and (init != 0) build their
+   lane words with FAST initial draws (same draws as sg_init_states).
+   scratch: [dev] int32 of 128 + ceil(cases / 4) words. */
+int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t ld_obs,
+                     int32_t cases, int32_t m, int64_t case_base,
+                     uint64_t init_key, int32_t init, int32_t* scratch,
+                     uint8_t* pattern, int32_t* case_id, uint8_t* lanes,
+                     int32_t lane_ld, void* stream);
+
+/* Sweep + tally on packed lanes.  jcell [dev] [2^bits][n]: CPT cell of each
+   variable for each lane word; zs_flag = ftab + ftab_size (arms the
+   ZeroSupport check).  counts may be NULL. */
+int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern,
+                   const int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
+                   int32_t cases, int32_t num_real, int32_t m, int64_t case_base,
+                   uint64_t key, const uint64_t* key_dev, const int32_t* jcell, int32_t cells,
+                   uint64_t* counts, const uint32_t* zs_flag, int32_t* err,
+                   void* stream);
+
+/* Layout switches between packed lanes and sg_batch int8 lane states. */
+int sg_small_import(const sg_small* sp, const sg_batch* batch, const int32_t* case_id,
+                    uint8_t* lanes, int32_t lane_ld, void* stream);
+int sg_small_export(const sg_small* sp, const sg_batch* batch, const int32_t* case_id,
+                    const uint8_t* pattern, const uint8_t* lanes, int32_t lane_ld,
+                    void* stream);
+
+/* Device key cursor for CUDA-graph replay of minibatch steps:
+   current[0..kps) = table[*index * kps ...]; *index += 1.  Kernels given
+   key_dev = current + k then read fresh keys on every replay. */
+int sg_keys_advance(const uint64_t* table, int32_t* index, int32_t kps,
+                    uint64_t* current, void* stream);
 
 /* Largest state of each variable's observed cells (range check, sampler.py:429-430). */
 int sg_check_range(const sg_net* net, const int8_t* obs, int32_t ld_obs,

@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsamegibbs_b200.so"
-SOURCES = ["sg_common.cu", "sg_tables.cu", "sg_sweep.cu", "sg_batch.cu", "sg_model.cu", "sg_data.cu"]
+SOURCES = ["sg_common.cu", "sg_tables.cu", "sg_sweep.cu", "sg_batch.cu", "sg_model.cu", "sg_data.cu", "sg_small.cu"]
 HEADERS = ["sg_device.cuh"]
 ROOT = PKG.parent
 

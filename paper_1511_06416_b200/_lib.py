@@ -31,13 +31,17 @@ NET_POINTERS = (
 )
 
 
+NET_POINTERS_TAIL = ("joint_radix", "joint_cell", "var_desc")
+
+
 class SgNet(ctypes.Structure):
     _fields_ = [
         ("n", c_int32), ("num_groups", c_int32), ("max_card", c_int32), ("max_mb", c_int32),
         ("max_group", c_int32), ("direct_vars", c_int32),
         ("cells", c_int64), ("rows", c_int64), ("ptab_size", c_int64), ("ftab_size", c_int64),
         ("table_entries", c_int64),
-    ] + [(name, c_void_p) for name in NET_POINTERS]
+    ] + [(name, c_void_p) for name in NET_POINTERS] + [("joint_size", c_int64)] + \
+        [(name, c_void_p) for name in NET_POINTERS_TAIL]
 
 
 class SgBatch(ctypes.Structure):
@@ -46,6 +50,17 @@ class SgBatch(ctypes.Structure):
         ("num_real", c_int32), ("case_base", c_int64), ("rank", c_void_p), ("ld_rank", c_int32),
         ("pad_", c_int32), ("nmiss", c_void_p),
     ]
+
+
+SMALL_MAXV = 7
+SMALL_MAXBITS = 7
+
+
+class SgSmall(ctypes.Structure):
+    _fields_ = [("n", c_int32), ("bits", c_int32), ("tab_words", c_int32), ("pad_", c_int32)] + \
+        [(name, ctypes.c_int32 * SMALL_MAXV) for name in ("order", "off", "width")] + \
+        [("mbmask", ctypes.c_uint32 * SMALL_MAXV)] + \
+        [(name, ctypes.c_int32 * SMALL_MAXV) for name in ("card", "toff")]
 
 
 _SIGNATURES = {
@@ -57,16 +72,26 @@ _SIGNATURES = {
     "sg_init_states": ([POINTER(SgNet), POINTER(SgBatch), c_void_p, c_int32, c_int32, c_uint64, c_void_p,
                         c_void_p, c_void_p, c_void_p], c_int32),
     "sg_sweep": ([POINTER(SgNet), POINTER(SgBatch), c_void_p, c_void_p, c_void_p, c_int32, c_uint64,
-                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p], c_int32),
+                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p], c_int32),
     "sg_tally": ([POINTER(SgNet), POINTER(SgBatch), c_void_p, c_void_p], c_int32),
     "sg_tally_weighted": ([POINTER(SgNet), POINTER(SgBatch), c_void_p, c_void_p, c_void_p], c_int32),
     "sg_accumulate": ([c_int32, c_void_p, c_void_p, c_void_p, c_double, c_int64, c_void_p], c_int32),
     "sg_accumulate_f64": ([c_int32, c_void_p, c_void_p, c_void_p, c_double, c_int64, c_void_p], c_int32),
     "sg_mean_cpts": ([POINTER(SgNet), c_void_p, c_void_p, c_void_p, c_void_p], c_int32),
-    "sg_sample_cpts": ([POINTER(SgNet), c_void_p, c_void_p, c_uint64, c_void_p, c_void_p], c_int32),
+    "sg_sample_cpts": ([POINTER(SgNet), c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_void_p], c_int32),
     "sg_forward_sample": ([POINTER(SgNet), c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64,
                            c_double, c_uint64, c_uint64, c_void_p], c_int32),
     "sg_check_range": ([POINTER(SgNet), c_void_p, c_int32, c_int32, c_void_p, c_void_p], c_int32),
+    "sg_small_tables": ([POINTER(SgNet), POINTER(SgSmall), c_void_p, c_void_p, c_void_p], c_int32),
+    "sg_small_prepare": ([POINTER(SgSmall), c_void_p, c_int32, c_int32, c_int32, c_int64, c_uint64, c_int32,
+                          c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p], c_int32),
+    "sg_small_sweep": ([POINTER(SgSmall), c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32,
+                        c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
+                        c_void_p], c_int32),
+    "sg_keys_advance": ([c_void_p, c_void_p, c_int32, c_void_p, c_void_p], c_int32),
+    "sg_small_import": ([POINTER(SgSmall), POINTER(SgBatch), c_void_p, c_void_p, c_int32, c_void_p], c_int32),
+    "sg_small_export": ([POINTER(SgSmall), POINTER(SgBatch), c_void_p, c_void_p, c_void_p, c_int32, c_void_p],
+                        c_int32),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -106,6 +131,8 @@ KERNELS_PER_CALL = {
     "sg_build_tables": 1, "sg_rank_latent": 3, "sg_init_states": 1, "sg_sweep": 1, "sg_tally": 1,
     "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
+    "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
+    "sg_keys_advance": 1,
 }
 launch_count = 0
 

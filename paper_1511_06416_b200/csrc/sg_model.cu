@@ -98,7 +98,8 @@ __device__ double log_gamma_draw(CellStream& rs, double a) {
 }
 
 __global__ void k_sample_cpts(const sg_net net, const double* __restrict__ total, const double* __restrict__ alpha,
-                              uint64_t key, double* __restrict__ out) {
+                              uint64_t key, const uint64_t* __restrict__ key_dev, double* __restrict__ out) {
+  if (key_dev) key = __ldg(key_dev);
   for (int64_t row = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; row < net.rows;
        row += int64_t(gridDim.x) * blockDim.x) {
     const int v = __ldg(net.row_var + row);
@@ -161,10 +162,10 @@ extern "C" int sg_mean_cpts(const sg_net* net, const double* total, const double
 }
 
 extern "C" int sg_sample_cpts(const sg_net* net, const double* total, const double* alpha, uint64_t key,
-                              double* cpt_out, void* stream) {
+                              const uint64_t* key_dev, double* cpt_out, void* stream) {
   using namespace sg;
   SG_REQUIRE(net && total && alpha && cpt_out, "sg_sample_cpts: null argument");
   SG_REQUIRE(net->max_card <= SG_MAX_CARD, "sg_sample_cpts: card capacity exceeded");
-  k_sample_cpts<<<grid_for(net->rows), 256, 0, (cudaStream_t)stream>>>(*net, total, alpha, key, cpt_out);
+  k_sample_cpts<<<grid_for(net->rows), 256, 0, (cudaStream_t)stream>>>(*net, total, alpha, key, key_dev, cpt_out);
   return check_launch("sg_sample_cpts");
 }

@@ -6,263 +6,508 @@
 // tallies the final assignments (tally_counts model.py:148-165).
 //
 // B200 design.  Lanes never interact: the Markov blanket of (v, lane) lives
-// in the same lane.  A CTA therefore owns a tile of TC cases x all m replicas
-// x all n variables, stages the tile's int8 lane states in shared memory once
-// (one coalesced HBM read), runs every colour group on-chip, tallies the
-// final states, and writes the tile back (one HBM write).  Per colour group
-// the CTA compacts the latent (variable, case) cells of the group into an
-// item list (warp ballots), so threads only spend work on latent cells; an
-// item carries all m replicas of one latent case (SAME replicas share the
-// observed mask), in quads of 4 replicas = one Philox4x32 call in FAST mode.
-// The draw itself is one Markov-blanket index + one conditional-table read
-// (sg_tables.cu), or the reference's weight product for variables whose
-// blanket is too large to tabulate.
+// in the same lane.  A CTA owns a tile of TC cases x all m replicas x all n
+// variables:
+//   1. one coalesced 16-byte-per-thread HBM read stages the tile's lane
+//      states in shared memory, splitting the latent flags (bit 7) into one
+//      32-case bit mask per variable (SAME replicas share the mask);
+//   2. per colour group, the latent (variable, case) cells are compacted,
+//      variable-major, into an item list (block scan over mask popcounts);
+//      an item carries all m replicas of its case, handled in quads of 4
+//      independent draws = one Philox4x32 call (FAST mode);
+//   3. a draw is a Markov-blanket index (one LDS.U8 + IMAD per member, the
+//      member count a template parameter) and a conditional-table read
+//      (sg_tables.cu) compared with the uniform, or the reference's weight
+//      product for variables without a table;
+//   4. the tally histograms the final lanes on-chip -- whole-lane joint
+//      states in per-thread byte counters for small networks (Koller: 48
+//      joint states), per-cell counters otherwise -- and flushes one atomic
+//      per touched CPT cell per CTA;
+//   5. one coalesced HBM write puts the tile back.
 #include "sg_device.cuh"
 
 namespace sg {
 
-enum TallyMode { TALLY_NONE = 0, TALLY_PRIVATE = 1, TALLY_SHARED = 2, TALLY_GLOBAL = 3 };
+enum TallyMode { TALLY_NONE = 0, TALLY_JOINT = 1, TALLY_CELL8 = 2, TALLY_SHARED = 3, TALLY_GLOBAL = 4 };
 
 struct SweepArgs {
   const double* cpt;
   const double* ptab;
   const uint32_t* ftab;
   uint64_t fast_key;
+  const uint64_t* fast_key_dev;  // when set, the FAST key is read from device memory (graph replay)
   const uint64_t* keys;
   const double* uniforms;
   const int64_t* inj_off;
   uint64_t* counts;
   int32_t* err;
-  int tc;           // cases per tile
+  int tc;            // cases per tile (multiple of 32)
   int tally_mode;
-  int stage_tables; // 1: tables copied into shared memory
-  int64_t tab_bytes;
+  int64_t tab_bytes; // bytes of the table this mode reads (staged when SMALL)
 };
 
 struct SmemLayout {
-  size_t st, items, tabs, hist, total;
+  size_t st, lat, items, desc, tabs, hist, cellacc, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline SmemLayout smem_layout(const sg_net& net, int m, int tc, int tally_mode,
-                                                  int stage_tables, int64_t tab_bytes) {
+// SMALL: descriptors and conditional tables live in shared memory.
+__host__ __device__ inline SmemLayout smem_layout(const sg_net& net, int m, int tc, int tally_mode, bool small,
+                                                  int64_t tab_bytes) {
   SmemLayout L;
-  L.st = 0;
-  size_t off = align16(size_t(net.n) * m * tc);
+  size_t off = 0;
+  L.st = off;
+  off += align16(size_t(net.n) * m * tc);
+  L.lat = off;
+  off += align16(size_t(net.n) * (tc / 32) * 4);
   L.items = off;
   off += align16(size_t(net.max_group) * tc * 4);
+  L.desc = off;
+  if (small) off += align16(size_t(net.n) * SG_DESC_WORDS * 4);
   L.tabs = off;
-  if (stage_tables) off += align16(size_t(tab_bytes));
+  if (small) off += align16(size_t(tab_bytes));
   L.hist = off;
-  if (tally_mode == TALLY_PRIVATE) off += size_t(net.cells) * SG_THREADS * 4;
+  if (tally_mode == TALLY_JOINT) off += align16(size_t(net.joint_size) * SG_THREADS);
+  else if (tally_mode == TALLY_CELL8) off += align16(size_t(net.cells) * SG_THREADS);
   else if (tally_mode == TALLY_SHARED) off += align16(size_t(net.cells) * 4);
+  L.cellacc = off;
+  if (tally_mode == TALLY_JOINT) off += align16(size_t(net.cells) * 4 + 64);
   L.total = off;
   return L;
 }
 
-template <int MODE>
-__device__ __forceinline__ void draw_item(const sg_net& net, const sg_batch& bt, const SweepArgs& a,
-                                          const int8_t* __restrict__ st_in, int8_t* st, int tc,
-                                          const double* ptab, const uint32_t* ftab, int v, int c,
-                                          int rq, int c0, bool& zero_support) {
-  const int m = bt.m;
-  const int card = __ldg(net.card + v);
-  const int64_t nent = __ldg(net.tab_entries + v);
-  const int mb0 = __ldg(net.mb_start + v), mb1 = __ldg(net.mb_start + v + 1);
-  const int r0 = rq * 4;
-  const int r1 = min(r0 + 4, m);
-  const int64_t gcase = bt.case_base + c0 + c;
+// Byte slot of thread tid in a per-thread byte-counter row of SG_THREADS
+// bytes: lane l of every warp lands in bank l, so a warp's increments never
+// conflict whatever bins its lanes hit.
+static_assert(SG_THREADS == 256, "hist_slot assumes 8 warps per CTA");
+__device__ __forceinline__ int hist_slot(int tid) {
+  return ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
+}
 
-  u32x4 fastw = {0, 0, 0, 0};
-  if (MODE == SG_RNG_FAST) fastw = fast_block(a.fast_key, uint64_t(gcase), uint32_t(v), uint32_t(rq), 0u);
-  int64_t rank = 0, nmiss = 0;
+// Expand 4 flag bits (bit i -> byte i) into 0x80 markers.
+__device__ __forceinline__ uint32_t flags_to_bytes(uint32_t nib) {
+  return ((nib * 0x00204081u) & 0x01010101u) << 7;
+}
+
+// Gather bit 7 of each byte of w into bits 0..3.
+__device__ __forceinline__ uint32_t byte_flags(uint32_t w) {
+  return (((w & 0x80808080u) >> 7) * 0x01020408u) >> 24;
+}
+
+// Block-wide exclusive scan of one int per thread; *total gets the sum.
+__device__ __forceinline__ int block_scan(int x, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  int base = 0, sum = 0;
+#pragma unroll
+  for (int w = 0; w < SG_THREADS / 32; ++w) {
+    const int t = s_warp[w];
+    base += w < warp ? t : 0;
+    sum += t;
+  }
+  __syncthreads();
+  *total = sum;
+  return base + inc - x;
+}
+
+// Direct evaluation for variables without a table (blanket too large).
+__device__ __noinline__ int draw_direct(const sg_net& net, const double* cpt, const int8_t* st, int mtc, int roff,
+                                        int c, int v, double u, bool& zero_support) {
+  const int card = __ldg(net.card + v);
+  int s[SG_MAX_MB];
+  for (int k = __ldg(net.mb_start + v), k0 = k, e = __ldg(net.mb_start + v + 1); k < e; ++k)
+    s[k - k0] = st[__ldg(net.mb_var + k) * mtc + roff + c];
+  double w[SG_MAX_CARD];
+  conditional_weights(net, v, s, cpt, w);
+  const double norm = np_pairwise_sum(w, card);
+  if (!(norm > 0.0)) zero_support = true;
+  const double au = __dmul_rn(u, norm);
+  double cum = 0.0;
+  int x = 0;
+  for (int t = 0; t < card - 1; ++t) {
+    cum = t ? __dadd_rn(cum, w[t]) : w[0];
+    x += (au > cum);
+  }
+  return x;
+}
+
+struct ItemCtx {
+  int8_t* st;
+  int mtc, tc, m;
+  int64_t gcase0;  // global index of the tile's case 0
+  int c0;
+  uint64_t key;    // FAST key of this sweep
+};
+
+// Draw all m replicas of latent cell (v, c); K = Markov-blanket members
+// (K < 0: evaluate from the CPTs).  Quads of 4 replicas are independent
+// draws, written out so the compiler can overlap their loads.
+template <int MODE, int K>
+__device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, const SweepArgs& a,
+                                          const int32_t* dv, const uint32_t* ftab, const double* ptab,
+                                          const sg_batch& bt, int v, int c, bool zs_armed, bool& zs) {
+  const int card = dv[0];
+  const int mtc = x.mtc, tc = x.tc, m = x.m;
+  int rows[K > 0 ? K : 1], strd[K > 0 ? K : 1];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    rows[k] = dv[4 + k] * mtc + c;
+    strd[k] = dv[4 + SG_DESC_MB + k];
+  }
+  int8_t* out = x.st + v * mtc + c;
+  const uint32_t* tf = ftab + (K >= 0 ? dv[2] : 0);
+  const double* tp = ptab + (K >= 0 ? dv[3] : 0);
+  int64_t rank = 0, nmiss = 0, ioff = 0;
   uint64_t k0 = 0, k1 = 0;
   if (MODE != SG_RNG_FAST) {
-    rank = __ldg(bt.rank + int64_t(v) * bt.ld_rank + c0 + c);
+    rank = __ldg(bt.rank + int64_t(v) * bt.ld_rank + x.c0 + c);
     nmiss = __ldg(bt.nmiss + v);
     if (MODE == SG_RNG_NUMPY) {
       k0 = __ldg(a.keys + 2 * v);
       k1 = __ldg(a.keys + 2 * v + 1);
+    } else {
+      ioff = __ldg(a.inj_off + v);
     }
   }
-
-  for (int r = r0; r < r1; ++r) {
-    // ---- uniform
-    uint32_t u31 = 0;
-    double u = 0.0;
+  const int Q = (m + 3) >> 2;
+  for (int rq = 0; rq < Q; ++rq) {
+    uint32_t u31[4];
+    double u[4];
     if (MODE == SG_RNG_FAST) {
-      const uint32_t w = pick(fastw, r - r0);
-      u31 = w >> 1;
-      u = double(w) * 0x1.0p-32;
+      const u32x4 w = fast_block(x.key, uint64_t(x.gcase0 + c), uint32_t(v), uint32_t(rq), 0u);
+      u31[0] = w.a >> 1;
+      u31[1] = w.b >> 1;
+      u31[2] = w.c >> 1;
+      u31[3] = w.d >> 1;
+      u[0] = double(w.a) * 0x1.0p-32;
+      u[1] = double(w.b) * 0x1.0p-32;
+      u[2] = double(w.c) * 0x1.0p-32;
+      u[3] = double(w.d) * 0x1.0p-32;
     } else {
-      const int64_t idx = int64_t(r) * nmiss + rank;  // reference lane order
-      if (MODE == SG_RNG_NUMPY) u = np_uniform(uint64_t(idx), k0, k1);
-      else u = __ldg(a.uniforms + __ldg(a.inj_off + v) + idx);
-    }
-    // ---- draw
-    int x = 0;
-    if (nent > 0) {
-      int64_t e = 0;
-      for (int k = mb0; k < mb1; ++k) {
-        const int uvar = __ldg(net.mb_var + k);
-        e += int64_t(st[(uvar * m + r) * tc + c] & 0x7F) * __ldg(net.mb_stride + k);
-      }
-      if (MODE == SG_RNG_FAST) {
-        const uint32_t* th = ftab + __ldg(net.ftab_off + v) + e * (card - 1);
-        if (th[0] == 0xFFFFFFFFu) zero_support = true;
-        for (int s = 0; s < card - 1; ++s) x += (u31 >= th[s]);
-      } else {
-        const double* p = ptab + __ldg(net.ptab_off + v) + e * card;
-        const double norm = p[card - 1];
-        if (!(norm > 0.0)) zero_support = true;
-        const double au = __dmul_rn(u, norm);
-        for (int s = 0; s < card - 1; ++s) x += (au > p[s]);
-      }
-    } else {
-      int s[SG_MAX_MB];
-      for (int k = mb0; k < mb1; ++k) {
-        const int uvar = __ldg(net.mb_var + k);
-        s[k - mb0] = st[(uvar * m + r) * tc + c] & 0x7F;
-      }
-      double w[SG_MAX_CARD];
-      conditional_weights(net, v, s, a.cpt, w);
-      const double norm = np_pairwise_sum(w, card);
-      if (!(norm > 0.0)) zero_support = true;
-      const double au = __dmul_rn(u, norm);
-      double cum = 0.0;
-      for (int t = 0; t < card - 1; ++t) {
-        cum = t ? __dadd_rn(cum, w[t]) : w[0];
-        x += (au > cum);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = min(rq * 4 + j, m - 1);
+        const int64_t idx = int64_t(r) * nmiss + rank;  // reference lane order (sampler.py:245)
+        u[j] = MODE == SG_RNG_NUMPY ? np_uniform(uint64_t(idx), k0, k1) : __ldg(a.uniforms + ioff + idx);
+        u31[j] = 0;
       }
     }
-    st[(v * m + r) * tc + c] = int8_t(0x80 | x);
+    int xs[4];
+    if (K >= 0) {
+      int e[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int roff = min(rq * 4 + j, m - 1) * tc;
+        int acc = 0;
+#pragma unroll
+        for (int k = 0; k < (K > 0 ? K : 0); ++k) acc += int(x.st[rows[k] + roff]) * strd[k];
+        e[j] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int s = 0;
+        if (MODE == SG_RNG_FAST) {
+          const uint32_t* th = tf + e[j] * (card - 1);
+          const uint32_t t0 = th[0];
+          if (zs_armed && t0 == 0xFFFFFFFFu) zs = true;
+          s = u31[j] >= t0;
+          if (card > 2) {
+            s += u31[j] >= th[1];
+            if (card > 3) {
+              s += u31[j] >= th[2];
+              for (int q = 3; q < card - 1; ++q) s += (u31[j] >= th[q]);
+            }
+          }
+        } else {
+          const double* p = tp + int64_t(e[j]) * card;
+          const double norm = p[card - 1];
+          if (!(norm > 0.0)) zs = true;
+          const double au = __dmul_rn(u[j], norm);
+          for (int q = 0; q < card - 1; ++q) s += (au > p[q]);
+        }
+        xs[j] = s;
+      }
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        const int r = min(rq * 4 + j, m - 1);
+        xs[j] = draw_direct(net, a.cpt, x.st, mtc, r * tc, c, v, u[j], zs);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (rq * 4 + j < m) out[(rq * 4 + j) * tc] = int8_t(xs[j]);
   }
-  (void)st_in;
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(SG_THREADS)
+__device__ __forceinline__ void draw_dispatch(int nmb, const ItemCtx& x, const sg_net& net, const SweepArgs& a,
+                                              const int32_t* dv, const uint32_t* ftab, const double* ptab,
+                                              const sg_batch& bt, int v, int c, bool zs_armed, bool& zs) {
+  switch (nmb) {
+    case 0: draw_cell<MODE, 0>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    case 1: draw_cell<MODE, 1>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    case 2: draw_cell<MODE, 2>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    case 3: draw_cell<MODE, 3>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    case 4: draw_cell<MODE, 4>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    case 5: draw_cell<MODE, 5>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    case 6: draw_cell<MODE, 6>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    case 7: draw_cell<MODE, 7>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    case 8: draw_cell<MODE, 8>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+    default: draw_cell<MODE, -1>(x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs); break;
+  }
+}
+
+// Joint-state tally of N <= 7 variables (prod card <= SG_JOINT_MAX).
+template <int N>
+__device__ __forceinline__ void tally_joint(const int8_t* st, int mtc, int tc, int m, int nreal,
+                                            const int32_t* radix, uint8_t* hist8, int slot) {
+  int R[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) R[k] = __ldg(radix + k);
+  for (int r = 0; r < m; ++r) {
+    const int8_t* row = st + r * tc;
+    for (int c = threadIdx.x; c < nreal; c += SG_THREADS) {
+      int J = 0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) J += int(row[k * mtc + c]) * R[k];
+      hist8[J * SG_THREADS + slot] += 1;
+    }
+  }
+}
+
+template <int MODE, bool SMALL>
+__global__ void __launch_bounds__(SG_THREADS, MODE == SG_RNG_FAST ? 4 : 2)
 k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int s_nitems;
+  __shared__ int s_warp[SG_THREADS / 32];
   __shared__ int s_err;
   const int tc = a.tc;
   const int m = bt.m;
   const int n = net.n;
-  const SmemLayout L = smem_layout(net, m, tc, a.tally_mode, a.stage_tables, a.tab_bytes);
+  const int mtc = m * tc;
+  const int words = tc >> 5;  // flag words per variable
+  const SmemLayout L = smem_layout(net, m, tc, a.tally_mode, SMALL, a.tab_bytes);
   int8_t* st = reinterpret_cast<int8_t*>(smem + L.st);
+  uint32_t* lat = reinterpret_cast<uint32_t*>(smem + L.lat);
+  uint16_t* lat16 = reinterpret_cast<uint16_t*>(smem + L.lat);
   uint32_t* items = reinterpret_cast<uint32_t*>(smem + L.items);
   const int c0 = blockIdx.x * tc;
-  const int ncase = min(tc, bt.cases - c0);        // sampled cases of this tile
+  const int ncase = min(tc, bt.cases - c0);             // sampled cases of this tile
   const int nreal = max(0, min(tc, bt.num_real - c0));  // tallied cases
-  const int nload = min(tc, bt.pitch - c0);        // resident cases (multiple of 16)
+  const int nload = min(tc, bt.pitch - c0);             // resident cases (multiple of 16)
   const int tid = threadIdx.x;
   if (tid == 0) s_err = 0;
 
-  // ---- stage lane states: rows (v, r) of nload bytes, 16 B per thread-load
+  // ---- 1. stage lane states (flags stripped) + latent masks
+  // A thread always handles chunk `ch` of rows row0, row0 + step, ... (tc/16
+  // divides the CTA size), so (v, r) advance without divisions.
+  const int per_row = tc >> 4;
+  const int lg_row = __ffs(per_row) - 1;
+  const int my_ch = tid & (per_row - 1);
+  const int row_step = SG_THREADS >> lg_row;
+  const int row0 = tid >> lg_row;
+  const int v0 = row0 / m, r0 = row0 - v0 * m;
   {
     const int chunks = nload >> 4;
-    const int per_row = tc >> 4;
-    const int total = n * m * chunks;
-    for (int i = tid; i < total; i += SG_THREADS) {
-      const int row = i / chunks, ch = i - row * chunks;
-      const int4 val = *reinterpret_cast<const int4*>(bt.states + int64_t(row) * bt.pitch + c0 + ch * 16);
+    const int ch = my_ch;
+    int v = v0, r = r0;
+    for (int row = row0; ch < chunks && row < n * m; row += row_step) {
+      int4 val = __ldcs(reinterpret_cast<const int4*>(bt.states + int64_t(row) * bt.pitch + c0 + ch * 16));
+      const bool first = r == 0;
+      r += row_step;
+      const int vcur = v;
+      while (r >= m) {
+        r -= m;
+        ++v;
+      }
+      if (first) {  // replica 0 carries the mask of all replicas
+        const int v = vcur;
+        uint32_t bits = byte_flags(val.x) | (byte_flags(val.y) << 4) | (byte_flags(val.z) << 8) |
+                        (byte_flags(val.w) << 12);
+        const int cc = ch * 16;
+        if (cc + 16 > ncase) bits &= cc >= ncase ? 0u : ((1u << (ncase - cc)) - 1u);
+        lat16[v * (words * 2) + ch] = uint16_t(bits);
+      }
+      val.x &= 0x7F7F7F7F;
+      val.y &= 0x7F7F7F7F;
+      val.z &= 0x7F7F7F7F;
+      val.w &= 0x7F7F7F7F;
       reinterpret_cast<int4*>(st)[row * per_row + ch] = val;
     }
+    if (nload < tc) {  // tile past the row pitch: clear the masks of unloaded chunks
+      const int hw = words * 2;
+      for (int i = tid; i < n * hw; i += SG_THREADS)
+        if ((i % hw) * 16 >= nload) lat16[i] = 0;
+    }
   }
+  const int32_t* desc = net.var_desc;
   const double* ptab = a.ptab;
   const uint32_t* ftab = a.ftab;
-  if (a.stage_tables) {
-    const int words = int(a.tab_bytes >> 2);
+  const bool zs_armed = a.ftab && net.table_entries > 0 && __ldg(a.ftab + net.ftab_size) != 0u;
+  if (SMALL) {
+    int32_t* d = reinterpret_cast<int32_t*>(smem + L.desc);
+    for (int i = tid; i < n * SG_DESC_WORDS; i += SG_THREADS) d[i] = __ldg(net.var_desc + i);
+    desc = d;
+    // tables always addressed in shared memory here (empty when no variable has one)
+    const int tw = int(a.tab_bytes >> 2);
     uint32_t* dst = reinterpret_cast<uint32_t*>(smem + L.tabs);
     const uint32_t* src = MODE == SG_RNG_FAST ? a.ftab : reinterpret_cast<const uint32_t*>(a.ptab);
-    for (int i = tid; i < words; i += SG_THREADS) dst[i] = __ldg(src + i);
-    if (MODE == SG_RNG_FAST) ftab = dst;
-    else ptab = reinterpret_cast<const double*>(dst);
+    for (int i = tid; i < tw; i += SG_THREADS) dst[i] = __ldg(src + i);
+    ftab = dst;
+    ptab = reinterpret_cast<const double*>(dst);
   }
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
-  if (a.counts && a.tally_mode == TALLY_PRIVATE) {
-    const int words = int(net.cells) * SG_THREADS;
-    for (int i = tid; i < words; i += SG_THREADS) hist[i] = 0;
-  } else if (a.counts && a.tally_mode == TALLY_SHARED) {
-    for (int i = tid; i < int(net.cells); i += SG_THREADS) hist[i] = 0;
+  uint8_t* hist8 = reinterpret_cast<uint8_t*>(smem + L.hist);
+  uint32_t* hist32 = reinterpret_cast<uint32_t*>(smem + L.hist);
+  uint32_t* cellacc = reinterpret_cast<uint32_t*>(smem + L.cellacc);
+  if (a.counts) {
+    if (a.tally_mode == TALLY_JOINT || a.tally_mode == TALLY_CELL8) {
+      const int bytes = (a.tally_mode == TALLY_JOINT ? int(net.joint_size) : int(net.cells)) * SG_THREADS;
+      for (int i = tid; i < bytes / 4; i += SG_THREADS) hist32[i] = 0;
+      if (a.tally_mode == TALLY_JOINT)
+        for (int i = tid; i < int(net.cells); i += SG_THREADS) cellacc[i] = 0;
+    } else if (a.tally_mode == TALLY_SHARED) {
+      for (int i = tid; i < int(net.cells); i += SG_THREADS) hist32[i] = 0;
+    }
   }
   __syncthreads();
 
-  // ---- colour groups, strictly in order
-  const int warp = tid >> 5, lane = tid & 31;
-  const int nchunk = (ncase + 31) >> 5;
-  const int Q = (m + 3) >> 2;
-  bool zero_support = false;
+  // ---- 2-3. colour groups, strictly in order
+  ItemCtx x;
+  x.st = st;
+  x.mtc = mtc;
+  x.tc = tc;
+  x.m = m;
+  x.gcase0 = bt.case_base + c0;
+  x.key = a.fast_key_dev ? __ldg(a.fast_key_dev) : a.fast_key;
+  x.c0 = c0;
+  bool zs = false;
   for (int g = 0; g < net.num_groups; ++g) {
     const int gs = __ldg(net.group_start + g), ge = __ldg(net.group_start + g + 1);
-    if (tid == 0) s_nitems = 0;
-    __syncthreads();
-    const int units = (ge - gs) * nchunk;
-    for (int uidx = warp; uidx < units; uidx += SG_THREADS / 32) {
-      const int vi = gs + uidx / nchunk;
-      const int ch = uidx - (uidx / nchunk) * nchunk;
-      const int v = __ldg(net.order + vi);
-      const int c = ch * 32 + lane;
-      const bool lat = c < ncase && (st[(v * m) * tc + c] & 0x80);
-      const unsigned mask = __ballot_sync(0xffffffffu, lat);
-      int base = 0;
-      if (lane == 0 && mask) base = atomicAdd(&s_nitems, __popc(mask));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (lat) items[base + __popc(mask & lanemask_lt())] = (uint32_t(v) << 16) | uint32_t(c);
+    // variable-major compaction of the group's latent cells
+    const int units = (ge - gs) * words;
+    int nitems = 0;
+    for (int u0 = 0; u0 < units; u0 += SG_THREADS) {
+      const int uidx = u0 + tid;
+      uint32_t mask = 0;
+      int v = 0, w = 0;
+      if (uidx < units) {
+        const int vi = gs + uidx / words;
+        w = uidx - (uidx / words) * words;
+        v = __ldg(net.order + vi);
+        mask = lat[v * words + w];
+      }
+      int chunk_total;
+      int pos = nitems + block_scan(__popc(mask), s_warp, &chunk_total);
+      const uint32_t hi = uint32_t(v) << 16;
+      while (mask) {
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        items[pos++] = hi | uint32_t(w * 32 + b);
+      }
+      nitems += chunk_total;
     }
     __syncthreads();
-    const int work = s_nitems * Q;
-    for (int j = tid; j < work; j += SG_THREADS) {
-      const int it = j / Q, rq = j - it * Q;
+    for (int it = tid; it < nitems; it += SG_THREADS) {
       const uint32_t item = items[it];
-      draw_item<MODE>(net, bt, a, nullptr, st, tc, ptab, ftab, int(item >> 16), int(item & 0xFFFFu),
-                      rq, c0, zero_support);
+      const int v = int(item >> 16), c = int(item & 0xFFFFu);
+      const int32_t* dv = desc + v * SG_DESC_WORDS;
+      draw_dispatch<MODE>(dv[1], x, net, a, dv, ftab, ptab, bt, v, c, zs_armed, zs);
     }
     __syncthreads();
   }
-  if (zero_support) atomicOr(&s_err, int(SG_ERR_ZERO_SUPPORT));
+  if (zs) atomicOr(&s_err, int(SG_ERR_ZERO_SUPPORT));
 
-  // ---- tally of the final assignments over real lanes
+  // ---- 4. tally of the final assignments over real lanes
   if (a.counts && nreal > 0) {
-    const int lanes = m * nreal;
-    for (int j = tid; j < lanes; j += SG_THREADS) {
-      const int r = j / nreal, c = j - r * nreal;
-      for (int v = 0; v < n; ++v) {
-        int64_t cfg = 0;
-        for (int p = __ldg(net.par_start + v), pe = __ldg(net.par_start + v + 1); p < pe; ++p)
-          cfg += int64_t(st[(__ldg(net.par_var + p) * m + r) * tc + c] & 0x7F) * __ldg(net.par_stride + p);
-        const int card = __ldg(net.card + v);
-        const int64_t cell = __ldg(net.cpt_off + v) + cfg * card + (st[(v * m + r) * tc + c] & 0x7F);
-        if (a.tally_mode == TALLY_PRIVATE) hist[cell * SG_THREADS + tid] += 1u;
-        else if (a.tally_mode == TALLY_SHARED) atomicAdd(hist + cell, 1u);
-        else atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, 1ull);
+    const int slot = hist_slot(tid);
+    if (a.tally_mode == TALLY_JOINT) {
+      switch (n) {
+        case 1: tally_joint<1>(st, mtc, tc, m, nreal, net.joint_radix, hist8, slot); break;
+        case 2: tally_joint<2>(st, mtc, tc, m, nreal, net.joint_radix, hist8, slot); break;
+        case 3: tally_joint<3>(st, mtc, tc, m, nreal, net.joint_radix, hist8, slot); break;
+        case 4: tally_joint<4>(st, mtc, tc, m, nreal, net.joint_radix, hist8, slot); break;
+        case 5: tally_joint<5>(st, mtc, tc, m, nreal, net.joint_radix, hist8, slot); break;
+        case 6: tally_joint<6>(st, mtc, tc, m, nreal, net.joint_radix, hist8, slot); break;
+        default: tally_joint<7>(st, mtc, tc, m, nreal, net.joint_radix, hist8, slot); break;
       }
-    }
-    __syncthreads();
-    if (a.tally_mode == TALLY_PRIVATE) {
-      for (int cell = tid; cell < int(net.cells); cell += SG_THREADS) {
-        uint32_t sum = 0;
-        for (int t = 0; t < SG_THREADS; ++t) sum += hist[cell * SG_THREADS + ((t + cell) & (SG_THREADS - 1))];
-        if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, (unsigned long long)sum);
+      __syncthreads();
+      // bins -> cells: each warp sums a bin's 256 byte counters with dp4a
+      const int warp = tid >> 5, lane_id = tid & 31;
+      for (int J = warp; J < int(net.joint_size); J += SG_THREADS / 32) {
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(hist8 + J * SG_THREADS);
+        int sum = __dp4a(int(row[lane_id]), 0x01010101, 0);
+        sum = __dp4a(int(row[lane_id + 32]), 0x01010101, sum);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (sum && lane_id < n) atomicAdd(cellacc + __ldg(net.joint_cell + J * n + lane_id), uint32_t(sum));
       }
-    } else if (a.tally_mode == TALLY_SHARED) {
+      __syncthreads();
       for (int cell = tid; cell < int(net.cells); cell += SG_THREADS)
-        if (hist[cell]) atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell,
-                                  (unsigned long long)hist[cell]);
+        if (cellacc[cell])
+          atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, (unsigned long long)cellacc[cell]);
+    } else {
+      for (int r = 0; r < m; ++r) {
+        const int8_t* lane_row = st + r * tc;
+        for (int c = tid; c < nreal; c += SG_THREADS) {
+          for (int v = 0; v < n; ++v) {
+            int cfg = 0;
+            for (int p = __ldg(net.par_start + v), pe = __ldg(net.par_start + v + 1); p < pe; ++p)
+              cfg += int(lane_row[__ldg(net.par_var + p) * mtc + c]) * __ldg(net.par_stride + p);
+            const int64_t cell =
+                __ldg(net.cpt_off + v) + int64_t(cfg) * __ldg(net.card + v) + lane_row[v * mtc + c];
+            if (a.tally_mode == TALLY_CELL8) hist8[cell * SG_THREADS + slot] += 1;
+            else if (a.tally_mode == TALLY_SHARED) atomicAdd(hist32 + cell, 1u);
+            else atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, 1ull);
+          }
+        }
+      }
+      __syncthreads();
+      if (a.tally_mode == TALLY_CELL8) {
+        const int warp = tid >> 5, lane_id = tid & 31;
+        for (int cell = warp; cell < int(net.cells); cell += SG_THREADS / 32) {
+          const uint32_t* row = reinterpret_cast<const uint32_t*>(hist8 + size_t(cell) * SG_THREADS);
+          int sum = __dp4a(int(row[lane_id]), 0x01010101, 0);
+          sum = __dp4a(int(row[lane_id + 32]), 0x01010101, sum);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+          if (sum && lane_id == 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, (unsigned long long)sum);
+        }
+      } else if (a.tally_mode == TALLY_SHARED) {
+        for (int cell = tid; cell < int(net.cells); cell += SG_THREADS)
+          if (hist32[cell])
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, (unsigned long long)hist32[cell]);
+      }
     }
   }
 
-  // ---- write the tile back
+  // ---- 5. write the tile back (flags restored from the masks)
   {
     const int chunks = nload >> 4;
-    const int per_row = tc >> 4;
-    const int total = n * m * chunks;
-    for (int i = tid; i < total; i += SG_THREADS) {
-      const int row = i / chunks, ch = i - row * chunks;
-      *reinterpret_cast<int4*>(bt.states + int64_t(row) * bt.pitch + c0 + ch * 16) =
-          reinterpret_cast<const int4*>(st)[row * per_row + ch];
+    const int ch = my_ch;
+    int v = v0, r = r0;
+    for (int row = row0; ch < chunks && row < n * m; row += row_step) {
+      const uint32_t bits = lat16[v * (words * 2) + ch];
+      r += row_step;
+      while (r >= m) {
+        r -= m;
+        ++v;
+      }
+      int4 val = reinterpret_cast<const int4*>(st)[row * per_row + ch];
+      val.x |= flags_to_bytes(bits & 0xF);
+      val.y |= flags_to_bytes((bits >> 4) & 0xF);
+      val.z |= flags_to_bytes((bits >> 8) & 0xF);
+      val.w |= flags_to_bytes((bits >> 12) & 0xF);
+      __stcs(reinterpret_cast<int4*>(bt.states + int64_t(row) * bt.pitch + c0 + ch * 16), val);
     }
   }
   __syncthreads();
@@ -292,14 +537,14 @@ k_tally(const sg_net net, const sg_batch bt, unsigned long long* counts,
   }
 }
 
-static int choose_tile(const sg_net& net, int m, int cases, int tally_mode, int stage, int64_t tab_bytes,
-                       int* tc_out, size_t* smem_out) {
+static int choose_tile(const sg_net& net, int m, int cases, const SweepArgs& a, bool small, int* tc_out,
+                       size_t* smem_out) {
   int best = 0;
   // largest power-of-two tile (<= 512 cases) whose shared memory leaves room
-  // for at least two CTAs per SM; fall back to one CTA of up to 200 KB.
+  // for two CTAs per SM; fall back to one CTA of up to 200 KB.
   for (int budget : {100 * 1024, 200 * 1024}) {
     for (int tc = 512; tc >= 32; tc >>= 1) {
-      const SmemLayout L = smem_layout(net, m, tc, tally_mode, stage, tab_bytes);
+      const SmemLayout L = smem_layout(net, m, tc, a.tally_mode, small, a.tab_bytes);
       if (L.total <= size_t(budget)) {
         best = tc;
         break;
@@ -311,16 +556,28 @@ static int choose_tile(const sg_net& net, int m, int cases, int tally_mode, int 
   // do not make tiles much larger than the minibatch
   while (best > 32 && best / 2 >= cases) best >>= 1;
   *tc_out = best;
-  *smem_out = smem_layout(net, m, best, tally_mode, stage, tab_bytes).total;
+  *smem_out = smem_layout(net, m, best, a.tally_mode, small, a.tab_bytes).total;
   return SG_OK;
+}
+
+template <int MODE, bool SMALL>
+static void launch_sweep(const sg_net& net, const sg_batch& bt, const SweepArgs& a, int blocks, size_t smem,
+                         cudaStream_t s) {
+  static size_t configured = 0;  // raise the opt-in once per instantiation (graph-capture friendly)
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_sweep<MODE, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  k_sweep<MODE, SMALL><<<blocks, SG_THREADS, smem, s>>>(net, bt, a);
 }
 
 }  // namespace sg
 
 extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* cpt,
                         const double* ptab, const uint32_t* ftab, int32_t rng_mode,
-                        uint64_t fast_key, const uint64_t* keys, const double* uniforms,
-                        const int64_t* inj_off, uint64_t* counts, int32_t* err, void* stream) {
+                        uint64_t fast_key, const uint64_t* fast_key_dev, const uint64_t* keys,
+                        const double* uniforms, const int64_t* inj_off, uint64_t* counts, int32_t* err,
+                        void* stream) {
   using namespace sg;
   SG_REQUIRE(net && batch && err, "sg_sweep: null argument");
   SG_REQUIRE(batch->states, "sg_sweep: null states");
@@ -331,6 +588,7 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
   SG_REQUIRE(net->n < 32768, "sg_sweep: n=%d exceeds 32767", net->n);
   SG_REQUIRE(net->max_card <= SG_MAX_CARD && net->max_mb <= SG_MAX_MB,
              "sg_sweep: card/blanket capacity exceeded");
+  SG_REQUIRE(net->var_desc, "sg_sweep: network pack has no variable descriptors");
   SG_REQUIRE(rng_mode >= SG_RNG_FAST && rng_mode <= SG_RNG_INJECTED, "sg_sweep: bad rng mode %d",
              rng_mode);
   if (rng_mode != SG_RNG_FAST)
@@ -344,40 +602,45 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
   SweepArgs a;
   a.cpt = cpt;
   a.ptab = ptab;
-  a.ftab = ftab;
+  a.ftab = net->table_entries > 0 ? ftab : nullptr;
   a.fast_key = fast_key;
+  a.fast_key_dev = fast_key_dev;
   a.keys = keys;
   a.uniforms = uniforms;
   a.inj_off = inj_off;
   a.counts = counts;
   a.err = err;
-  a.tab_bytes = rng_mode == SG_RNG_FAST ? net->ftab_size * 4 : net->ptab_size * 8;
-  a.stage_tables = (net->table_entries > 0 && a.tab_bytes <= 32 * 1024) ? 1 : 0;
+  a.tc = 0;
+  const int64_t tab_bytes = net->table_entries > 0
+                                ? (rng_mode == SG_RNG_FAST ? net->ftab_size * 4 : net->ptab_size * 8)
+                                : 0;
+  const bool small = net->n <= 256 && tab_bytes <= 32 * 1024;
+  a.tab_bytes = small ? tab_bytes : 0;
+  // tally strategy; byte counters hold at most 255 lanes per thread
+  const int max_lanes_per_thread = (batch->m * 512 + SG_THREADS - 1) / SG_THREADS;
+  const bool bytes_ok = max_lanes_per_thread <= 255;
   if (!counts) a.tally_mode = TALLY_NONE;
-  else if (net->cells * SG_THREADS * 4 <= 40 * 1024) a.tally_mode = TALLY_PRIVATE;
+  else if (bytes_ok && net->joint_size > 0 && net->joint_size <= SG_JOINT_MAX && net->n <= 7 &&
+           net->joint_radix && net->joint_cell)
+    a.tally_mode = TALLY_JOINT;
+  else if (bytes_ok && net->cells <= 128) a.tally_mode = TALLY_CELL8;
   else if (net->cells * 4 <= 48 * 1024) a.tally_mode = TALLY_SHARED;
   else a.tally_mode = TALLY_GLOBAL;
   size_t smem = 0;
-  int st = choose_tile(*net, batch->m, batch->cases, a.tally_mode, a.stage_tables, a.tab_bytes, &a.tc, &smem);
+  int st = choose_tile(*net, batch->m, batch->cases, a, small, &a.tc, &smem);
   if (st != SG_OK) {
     set_error("sg_sweep: tile of n=%d x m=%d does not fit in shared memory", net->n, batch->m);
     return st;
   }
   const int blocks = (batch->cases + a.tc - 1) / a.tc;
   cudaStream_t s = (cudaStream_t)stream;
-  switch (rng_mode) {
-    case SG_RNG_FAST:
-      cudaFuncSetAttribute(k_sweep<SG_RNG_FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      k_sweep<SG_RNG_FAST><<<blocks, SG_THREADS, smem, s>>>(*net, *batch, a);
-      break;
-    case SG_RNG_NUMPY:
-      cudaFuncSetAttribute(k_sweep<SG_RNG_NUMPY>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      k_sweep<SG_RNG_NUMPY><<<blocks, SG_THREADS, smem, s>>>(*net, *batch, a);
-      break;
-    default:
-      cudaFuncSetAttribute(k_sweep<SG_RNG_INJECTED>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      k_sweep<SG_RNG_INJECTED><<<blocks, SG_THREADS, smem, s>>>(*net, *batch, a);
-      break;
+  switch (rng_mode * 2 + (small ? 1 : 0)) {
+    case 0: launch_sweep<SG_RNG_FAST, false>(*net, *batch, a, blocks, smem, s); break;
+    case 1: launch_sweep<SG_RNG_FAST, true>(*net, *batch, a, blocks, smem, s); break;
+    case 2: launch_sweep<SG_RNG_NUMPY, false>(*net, *batch, a, blocks, smem, s); break;
+    case 3: launch_sweep<SG_RNG_NUMPY, true>(*net, *batch, a, blocks, smem, s); break;
+    case 4: launch_sweep<SG_RNG_INJECTED, false>(*net, *batch, a, blocks, smem, s); break;
+    default: launch_sweep<SG_RNG_INJECTED, true>(*net, *batch, a, blocks, smem, s); break;
   }
   return check_launch("sg_sweep");
 }

@@ -50,6 +50,7 @@ k_build_tables(const sg_net net, const double* __restrict__ cpt, double* __restr
       fe[t] = (t == 0 && !ok) ? 0xFFFFFFFFu : uint32_t(q);
     }
     pe[card - 1] = norm;
+    if (!ok) atomicOr(reinterpret_cast<int*>(ftab + net.ftab_size), 1);
   }
 }
 
@@ -66,6 +67,7 @@ extern "C" int sg_build_tables(const sg_net* net, const double* cpt, double* pta
              SG_MAX_MB);
   const int64_t blocks64 = (net->table_entries + SG_THREADS - 1) / SG_THREADS;
   const int blocks = int(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
+  cudaMemsetAsync(ftab + net->ftab_size, 0, sizeof(uint32_t), (cudaStream_t)stream);
   sg::k_build_tables<<<blocks, SG_THREADS, 0, (cudaStream_t)stream>>>(*net, cpt, ptab, ftab);
   return sg::check_launch("sg_build_tables");
 }

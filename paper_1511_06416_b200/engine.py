@@ -48,8 +48,38 @@ class PinnedRing:
         return self.bufs[i], self.events[i]
 
 
+class SmallBatch:
+    """Packed-lane minibatch (sg_small layout): one uint8 word per lane, slots bucketed by latent pattern."""
+
+    def __init__(self, n: int, m: int, cases: int, dev: torch.device):
+        self.n, self.m, self.cases = n, m, cases
+        self.lane_ld = max(16, (cases + 15) // 16 * 16)
+        self.lanes = torch.empty((m, self.lane_ld), dtype=torch.uint8, device=dev)
+        self.pattern = torch.empty(max(1, cases), dtype=torch.uint8, device=dev)
+        self.case_id = torch.empty(max(1, cases), dtype=torch.int32, device=dev)
+        self.scratch = torch.empty(128 + (cases + 3) // 4 + 1, dtype=torch.int32, device=dev)
+        self.nmiss = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.num_real = cases
+        self.dev = dev
+
+    def count_latent(self, obs: torch.Tensor, ld: int) -> None:
+        nblk = max(1, (self.cases + 4095) // 4096)
+        scratch = torch.empty(self.n * nblk, dtype=torch.int64, device=self.dev)
+        _lib.call("sg_rank_latent", self.n, obs.data_ptr(), ld, self.cases, None, 0, self.nmiss.data_ptr(),
+                  scratch.data_ptr(), stream_handle())
+        self._scratch = scratch
+
+    def nmiss_total(self) -> int:
+        return int(self.nmiss.sum().item())
+
+    @property
+    def states(self) -> torch.Tensor:
+        return self.lanes
+
+
 class Engine:
-    def __init__(self, net: Network, cfg: SamplerConfig, case_base: int = 0, comm=None):
+    def __init__(self, net: Network, cfg: SamplerConfig, case_base: int = 0, comm=None,
+                 small: bool | None = None):
         self.net = net
         self.cfg = cfg
         self.dev = device()
@@ -65,7 +95,7 @@ class Engine:
         self.total = torch.zeros(cells, dtype=torch.float64, device=d)
         self.counts = torch.zeros(cells, dtype=torch.int64, device=d)
         self.ptab = torch.empty(max(1, lay.scalars["ptab_size"]), dtype=torch.float64, device=d)
-        self.ftab = torch.empty(max(1, lay.scalars["ftab_size"]), dtype=torch.int32, device=d)
+        self.ftab = torch.empty(lay.scalars["ftab_size"] + 1, dtype=torch.int32, device=d)
         self.alpha = torch.from_numpy(cfg.prior.vector(self.n)).to(d)
         self.err = ErrorWord(d)
         self.rng_mode = _lib.SG_RNG_NUMPY if cfg.rng == "numpy" else _lib.SG_RNG_FAST
@@ -79,6 +109,11 @@ class Engine:
         self._obs_rings: dict[int, PinnedRing] = {}
         self.batch_bytes = 0
         self.sweep_events = None  # list -> (start, end, sweeps) CUDA events around each visit's sweeps
+        # packed-lane path: FAST RNG and a lane state that fits one byte (sg_small.cu)
+        can_small = self.rng_mode == _lib.SG_RNG_FAST and self.pack.small is not None
+        self.use_small = can_small if small is None else (bool(small) and can_small)
+        if self.use_small:
+            self.stab = torch.empty(max(1, self.pack.small.tab_words), dtype=torch.int32, device=d)
 
     # ------------------------------------------------------------ helpers
     def _upload_keys(self, seed: int, label: str, context: tuple) -> None:
@@ -130,36 +165,51 @@ class Engine:
 
     # ------------------------------------------------------------ one visit
     def visit(self, mb, pass_index: int, m: int) -> None:
+        """One minibatch visit (sampler.py:428-471): stage, S sweeps, tally, accumulate, CPT update."""
         cfg = self.cfg
         s = stream_handle()
         obs, ld = self._obs_for(mb)
         size = mb.size
-        stored = self.latent.get(mb.index) if cfg.accumulator_mode == "moving_sum" else None
-        if stored is not None and stored.m == m and stored.cases == size:
-            db = stored
-            db.set_obs(obs)
-        else:
-            db = DeviceBatch(self.n, m, size, int(mb.num_real), self.dev, self.case_base)
-            db.set_obs(obs)
-        db.struct.num_real = int(mb.num_real)
+        moving = cfg.accumulator_mode == "moving_sum"
+        stored = self.latent.get(mb.index) if moving else None
+        if stored is not None and not (stored.m == m and stored.cases == size):
+            stored = None
         _lib.call("sg_check_range", self.pack.ref, obs.data_ptr(), ld, size, self.err.ptr, s)
-        if self.rng_mode == _lib.SG_RNG_NUMPY:
-            db.compute_ranks()
-        elif db is not stored and cfg.accumulator_mode == "moving_sum":
-            db.compute_nmiss()  # latent counts for the memory accounting only
-        if db is not stored:
-            if self.rng_mode == _lib.SG_RNG_NUMPY:
-                self._upload_keys(cfg.seed, "latent_init", (pass_index, mb.index))
-                _lib.call("sg_init_states", self.pack.ref, db.ref, obs.data_ptr(), ld, _lib.SG_RNG_NUMPY, 0,
-                          self.keys.data_ptr(), self.rej.data_ptr(), self.err.ptr, s)
-            else:
+        if self.use_small:
+            db = stored if stored is not None else SmallBatch(self.n, m, size, self.dev)
+            db.num_real = int(mb.num_real)
+            if stored is None:
                 key = derive_seed(cfg.seed, "latent_init", pass_index, mb.index)
-                _lib.call("sg_init_states", self.pack.ref, db.ref, obs.data_ptr(), ld, _lib.SG_RNG_FAST, key,
-                          None, None, self.err.ptr, s)
+                _lib.call("sg_small_prepare", self.pack.small_ref, obs.data_ptr(), ld, size, m, self.case_base,
+                          key, 1, db.scratch.data_ptr(), db.pattern.data_ptr(), db.case_id.data_ptr(),
+                          db.lanes.data_ptr(), db.lane_ld, s)
+                if moving:
+                    db.count_latent(obs, ld)
+        else:
+            db = stored if stored is not None else DeviceBatch(self.n, m, size, int(mb.num_real), self.dev,
+                                                               self.case_base)
+            db.set_obs(obs)
+            db.struct.num_real = int(mb.num_real)
+            if self.rng_mode == _lib.SG_RNG_NUMPY:
+                db.compute_ranks()
+            elif stored is None and moving:
+                db.compute_nmiss()  # latent counts for the memory accounting only
+            if stored is None:
+                if self.rng_mode == _lib.SG_RNG_NUMPY:
+                    self._upload_keys(cfg.seed, "latent_init", (pass_index, mb.index))
+                    _lib.call("sg_init_states", self.pack.ref, db.ref, obs.data_ptr(), ld, _lib.SG_RNG_NUMPY, 0,
+                              self.keys.data_ptr(), self.rej.data_ptr(), self.err.ptr, s)
+                else:
+                    key = derive_seed(cfg.seed, "latent_init", pass_index, mb.index)
+                    _lib.call("sg_init_states", self.pack.ref, db.ref, obs.data_ptr(), ld, _lib.SG_RNG_FAST, key,
+                              None, None, self.err.ptr, s)
         _lib.call("sg_build_tables", self.pack.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
                   self.ftab.data_ptr(), s)
-        new_counts = torch.zeros_like(self.counts) if cfg.accumulator_mode == "moving_sum" else self.counts
-        if new_counts is self.counts:
+        if self.use_small:
+            _lib.call("sg_small_tables", self.pack.ref, self.pack.small_ref, self.ftab.data_ptr(),
+                      self.stab.data_ptr(), s)
+        new_counts = torch.zeros_like(self.counts) if moving else self.counts
+        if not moving:
             new_counts.zero_()
         S = cfg.sweeps_per_minibatch
         timing = self.sweep_events
@@ -169,21 +219,27 @@ class Engine:
         for sw in range(S):
             sweep_seed = derive_seed(cfg.seed, "sweep", pass_index, mb.index, sw)
             counts_ptr = new_counts.data_ptr() if sw == S - 1 else None
-            if self.rng_mode == _lib.SG_RNG_NUMPY:
+            if self.use_small:
+                _lib.call("sg_small_sweep", self.pack.small_ref, self.stab.data_ptr(), db.pattern.data_ptr(),
+                          db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m,
+                          self.case_base, sweep_seed, None, self.pack.small_jcell.data_ptr(), self.pack.cells,
+                          counts_ptr,
+                          self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"], self.err.ptr, s)
+            elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
                 _lib.call("sg_sweep", self.pack.ref, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
-                          self.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, self.keys.data_ptr(), None, None,
+                          self.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, None, self.keys.data_ptr(), None, None,
                           counts_ptr, self.err.ptr, s)
             else:
                 _lib.call("sg_sweep", self.pack.ref, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
-                          self.ftab.data_ptr(), _lib.SG_RNG_FAST, sweep_seed, None, None, None, counts_ptr,
+                          self.ftab.data_ptr(), _lib.SG_RNG_FAST, sweep_seed, None, None, None, None, counts_ptr,
                           self.err.ptr, s)
         if timing is not None:
             ev1.record()
             timing.append((ev0, ev1, S))
         if self.comm is not None:
             self.comm(new_counts)
-        if cfg.accumulator_mode == "moving_sum":
+        if moving:
             prev = self.prev_counts.get(mb.index)
             _lib.call("sg_accumulate", _lib.SG_ACC_MOVING, self.total.data_ptr(), new_counts.data_ptr(),
                       None if prev is None else prev.data_ptr(), 1.0, self.pack.cells, s)
@@ -197,10 +253,20 @@ class Engine:
                       self.cpt.data_ptr(), s)
         else:
             key = derive_seed(derive_seed(cfg.seed, "cpt_update", pass_index, mb.index), "sample_cpts")
-            _lib.call("sg_sample_cpts", self.pack.ref, self.total.data_ptr(), self.alpha.data_ptr(), key,
+            _lib.call("sg_sample_cpts", self.pack.ref, self.total.data_ptr(), self.alpha.data_ptr(), key, None,
                       self.cpt.data_ptr(), s)
         self.batch_bytes = max(self.batch_bytes, self.n * m * size * 4 + m * size * 8)
         self._last_batch = db
+
+    def lane_states(self, mb_index: int) -> torch.Tensor:
+        """int8 [n][m][pitch] lane states of a resident minibatch (generic layout, flags in bit 7)."""
+        db = self.latent[mb_index] if mb_index in self.latent else self._last_batch
+        if isinstance(db, SmallBatch):
+            out = DeviceBatch(self.n, db.m, db.cases, db.cases, self.dev)
+            _lib.call("sg_small_export", self.pack.small_ref, out.ref, db.case_id.data_ptr(), db.pattern.data_ptr(),
+                      db.lanes.data_ptr(), db.lane_ld, stream_handle())
+            return out.states
+        return db.states
 
     # ------------------------------------------------------------ run
     def current_cpts(self) -> CptSet:
@@ -241,3 +307,118 @@ class Engine:
                                    + list(self.prev_counts.values())
                                    + [db.states for db in self.latent.values()]))
         return self.current_cpts(), trace
+
+
+class StepGraphs:
+    """CUDA-graph replay of the steady-state visit of one resident minibatch.
+
+    A moving-sum visit whose lanes are already resident (every pass after the
+    first) is a fixed sequence of ~7 launches; replaying it as a graph removes
+    the host's per-launch cost.  The per-visit random keys (sweep keys, the
+    Dirichlet key) are precomputed for the planned passes into a device table
+    that ``sg_keys_advance`` steps through at the head of each replay, and the
+    new/previous count buffers alternate between two graphs.  Replays run
+    exactly the kernels ``Engine.visit`` launches with exactly the same keys,
+    so results equal eager visits bit for bit (FAST RNG mode).
+    """
+
+    def __init__(self, eng: Engine, mb, m: int, pass_indices, obs_buffer: torch.Tensor | None = None):
+        """``obs_buffer``: device int8 (n, pitch) tensor the graphs read the
+        minibatch's observations from; the caller keeps it filled (e.g. a
+        device-resident source).  Default: a private buffer that
+        :meth:`step` refills from the minibatch passed to it."""
+        cfg = eng.cfg
+        if eng.rng_mode != _lib.SG_RNG_FAST or cfg.accumulator_mode != "moving_sum":
+            raise ValueError("graph replay needs the fast RNG and the moving-sum accumulator")
+        db = eng.latent.get(mb.index)
+        if db is None or db.m != m or db.cases != mb.size:
+            raise ValueError("visit the minibatch once (eagerly) before capturing its graph")
+        self.eng, self.mb, self.m, self.db = eng, mb, m, db
+        S = cfg.sweeps_per_minibatch
+        self.kps = kps = S + 1
+        passes = list(pass_indices)
+        table = np.empty((len(passes), kps), dtype=np.uint64)
+        for i, p in enumerate(passes):
+            for s in range(S):
+                table[i, s] = derive_seed(cfg.seed, "sweep", p, mb.index, s)
+            table[i, S] = derive_seed(derive_seed(cfg.seed, "cpt_update", p, mb.index), "sample_cpts")
+        d = eng.dev
+        self.table = torch.from_numpy(table.view(np.int64)).to(d)
+        self.idx = torch.zeros(1, dtype=torch.int32, device=d)
+        self.cur = torch.zeros(kps, dtype=torch.int64, device=d)
+        self.planned = len(passes)
+        self.replayed = 0
+        prev = eng.prev_counts[mb.index]
+        self.cbuf = [torch.zeros_like(prev), prev.clone()]
+        if obs_buffer is None:
+            src, _ = eng._obs_for(mb)
+            obs_buffer = torch.empty((eng.n, _pitch(mb.size)), dtype=torch.int8, device=d)
+            obs_buffer[:, :src.shape[1]].copy_(src[:, :obs_buffer.shape[1]])
+        if obs_buffer.stride(0) % 16 or obs_buffer.stride(1) != 1 or obs_buffer.data_ptr() % 16:
+            raise ValueError("obs_buffer must be an int8 (n, pitch) tensor with 16-byte aligned rows")
+        self.obs, self.ld = obs_buffer, obs_buffer.stride(0)
+        self.graphs = []
+        torch.cuda.synchronize()
+        for parity in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._record(parity)
+            self.graphs.append(g)
+        torch.cuda.synchronize()
+
+    def _record(self, p: int) -> None:
+        eng, db, m, cfg = self.eng, self.db, self.m, self.eng.cfg
+        s = stream_handle()
+        size = self.mb.size
+        cur = self.cur.data_ptr()
+        new, prev = self.cbuf[p], self.cbuf[1 - p]
+        _lib.call("sg_keys_advance", self.table.data_ptr(), self.idx.data_ptr(), self.kps, cur, s)
+        _lib.call("sg_check_range", eng.pack.ref, self.obs.data_ptr(), self.ld, size, eng.err.ptr, s)
+        _lib.call("sg_build_tables", eng.pack.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(), eng.ftab.data_ptr(), s)
+        if eng.use_small:
+            _lib.call("sg_small_tables", eng.pack.ref, eng.pack.small_ref, eng.ftab.data_ptr(), eng.stab.data_ptr(), s)
+        new.zero_()
+        S = cfg.sweeps_per_minibatch
+        for sw in range(S):
+            counts_ptr = new.data_ptr() if sw == S - 1 else None
+            if eng.use_small:
+                _lib.call("sg_small_sweep", eng.pack.small_ref, eng.stab.data_ptr(), db.pattern.data_ptr(),
+                          db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m,
+                          eng.case_base, 0, cur + 8 * sw, eng.pack.small_jcell.data_ptr(), eng.pack.cells,
+                          counts_ptr, eng.ftab.data_ptr() + 4 * eng.pack.layout.scalars["ftab_size"], eng.err.ptr, s)
+            else:
+                _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
+                          eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
+                          eng.err.ptr, s)
+        if eng.comm is not None:
+            eng.comm(new)
+        _lib.call("sg_accumulate", _lib.SG_ACC_MOVING, eng.total.data_ptr(), new.data_ptr(), prev.data_ptr(), 1.0,
+                  eng.pack.cells, s)
+        if cfg.map_estimate:
+            _lib.call("sg_mean_cpts", eng.pack.ref, eng.total.data_ptr(), eng.alpha.data_ptr(), eng.cpt.data_ptr(), s)
+        else:
+            _lib.call("sg_sample_cpts", eng.pack.ref, eng.total.data_ptr(), eng.alpha.data_ptr(), 0, cur + 8 * S,
+                      eng.cpt.data_ptr(), s)
+
+    def step(self, mb=None) -> None:
+        """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
+        if self.replayed >= self.planned:
+            raise IndexError("all planned visits have been replayed")
+        if mb is not None:
+            vals = mb.values
+            if not (isinstance(vals, torch.Tensor) and vals.is_cuda and vals.data_ptr() == self.obs.data_ptr()):
+                src = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(np.asarray(vals, dtype=np.int8))
+                self.obs[:, :mb.size].copy_(src, non_blocking=True)
+        self.graphs[self.replayed % 2].replay()
+        self.replayed += 1
+        _lib.launch_count += self.launches_per_step
+
+    @property
+    def launches_per_step(self) -> int:
+        n = 5 + self.eng.cfg.sweeps_per_minibatch + (1 if self.eng.use_small else 0)
+        return n
+
+    def finish(self) -> None:
+        """Hand the last visit's counts back to the engine's moving-sum bookkeeping."""
+        if self.replayed:
+            self.eng.prev_counts[self.mb.index] = self.cbuf[(self.replayed - 1) % 2].clone()

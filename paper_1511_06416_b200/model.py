@@ -208,7 +208,7 @@ def sample_cpts(counts: CountSet, prior: DirichletPrior, seed: int, net: Network
     total = torch.from_numpy(pack.flatten(counts.tables)).to(dev)
     out = torch.empty_like(total)
     _lib.call("sg_sample_cpts", pack.ref, total.data_ptr(), _alpha_dev(prior, pack.n, dev).data_ptr(),
-              derive_seed(seed, "sample_cpts"), out.data_ptr(), stream_handle())
+              derive_seed(seed, "sample_cpts"), None, out.data_ptr(), stream_handle())
     return CptSet(pack.split(out.cpu().numpy()))
 
 

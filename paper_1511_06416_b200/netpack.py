@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from ._lib import NET_POINTERS, SgNet
+from ._lib import NET_POINTERS, NET_POINTERS_TAIL, SgNet
 from .network import Coloring, Network, color_graph, moralize
 
 # A variable's full conditional is tabulated when its blanket has at most this
@@ -25,6 +25,9 @@ TABLE_MAX_ENTRIES = 1 << 16
 TABLE_BUDGET_BYTES = 512 << 20
 MAX_CARD = 64
 MAX_MB = 64
+JOINT_MAX = 128        # SG_JOINT_MAX
+DESC_MB = 8            # SG_DESC_MB
+DESC_WORDS = 4 + 2 * DESC_MB
 
 
 @dataclass
@@ -134,6 +137,37 @@ def layout(net: Network, coloring: Coloring | None = None,
         ftab_off[1:] = np.cumsum(ftab_len)[:-1]
     row_var = np.repeat(np.arange(n, dtype=np.int64), rows)
 
+    # compact draw descriptors (sg_sweep): card, nmb | -1, ftab off, ptab off, mb vars, mb strides
+    desc = np.zeros((n, DESC_WORDS), dtype=np.int64)
+    for v in range(n):
+        mb = blankets[v]
+        desc[v, 0] = cards[v]
+        if tab_entries[v] > 0 and len(mb) <= DESC_MB:
+            desc[v, 1] = len(mb)
+            desc[v, 2] = ftab_off[v]
+            desc[v, 3] = ptab_off[v]
+            desc[v, 4:4 + len(mb)] = mb
+            desc[v, 4 + DESC_MB:4 + DESC_MB + len(mb)] = mb_stride[mb_start[v]:mb_start[v + 1]]
+        else:
+            desc[v, 1] = -1
+    # joint-state tally tables (small networks)
+    joint = int(np.prod(cards)) if n else 0
+    if 0 < joint <= JOINT_MAX:
+        radix = np.ones(n, dtype=np.int64)
+        for v in range(n - 2, -1, -1):
+            radix[v] = radix[v + 1] * cards[v + 1]
+        states = (np.arange(joint)[:, None] // radix[None, :]) % cards[None, :]
+        jcell = np.zeros((joint, n), dtype=np.int64)
+        for v in range(n):
+            cfg = np.zeros(joint, dtype=np.int64)
+            for p, s in zip(net.parents[v], net.parent_strides(v)):
+                cfg += states[:, p] * int(s)
+            jcell[:, v] = cpt_off[v] + cfg * cards[v] + states[:, v]
+    else:
+        joint = 0
+        radix = np.zeros(1, dtype=np.int64)
+        jcell = np.zeros((1, 1), dtype=np.int64)
+
     def i32(x):
         a = np.asarray(x, dtype=np.int64)
         if a.size and (a.max() > 2**31 - 1 or a.min() < -2**31):
@@ -147,6 +181,7 @@ def layout(net: Network, coloring: Coloring | None = None,
         "mb_stride": i32(mb_stride), "chl_start": i32(chl_start), "chl_var": i32(chl_var),
         "chl_vstride": i32(chl_vstride), "chl_slot": i32(chl_slot), "chl_pstart": i32(chl_pstart),
         "chl_pslot": i32(chl_pslot), "chl_pstride": i32(chl_pstride), "row_var": i32(row_var),
+        "joint_radix": i32(radix), "joint_cell": i32(jcell.ravel()), "var_desc": i32(desc.ravel()),
     }
     int64 = {
         "cpt_off": cpt_off[:n].copy(), "row_off": row_off, "tab_entries": tab_entries,
@@ -164,10 +199,62 @@ def layout(net: Network, coloring: Coloring | None = None,
         "ptab_size": int(ptab_len.sum()),
         "ftab_size": int(ftab_len.sum()),
         "table_entries": int(tab_entries.sum()),
+        "joint_size": joint,
     }
     return NetLayout(n=n, cards=cards, rows=rows, cpt_off=cpt_off, row_off=row_off,
                      groups=coloring.groups, topo=np.asarray(net.topo_order, dtype=np.int32),
                      int32=int32, int64=int64, scalars=scalars)
+
+
+def small_plan(net: Network, lay: NetLayout):
+    """Packed-lane plan (``sg_small``) when the lane state fits in one byte.
+
+    Returns ``(SgSmall, jcell)`` or None.  Field widths are ceil(log2(card));
+    jcell[S, v] is the CPT cell variable v contributes to for lane word S.
+    """
+    from ._lib import SMALL_MAXBITS, SMALL_MAXV, SgSmall
+
+    n = net.num_vars
+    if n == 0 or n > SMALL_MAXV:
+        return None
+    cards = [int(k) for k in net.cardinalities]
+    width = [max(1, (k - 1).bit_length()) for k in cards]
+    bits = sum(width)
+    if bits > SMALL_MAXBITS:
+        return None
+    off = [0] * n
+    for v in range(1, n):
+        off[v] = off[v - 1] + width[v - 1]
+    mb_start = lay.int32["mb_start"]
+    mb_var = lay.int32["mb_var"]
+    sp = SgSmall()
+    sp.n, sp.bits = n, bits
+    order = [v for grp in lay.groups for v in grp]
+    toff, words = [], 0
+    for v in range(n):
+        toff.append(words)
+        words += (1 << bits) * (cards[v] - 1)
+    sp.tab_words = words
+    for v in range(n):
+        sp.order[v] = order[v]
+        sp.off[v] = off[v]
+        sp.width[v] = width[v]
+        sp.card[v] = cards[v]
+        sp.toff[v] = toff[v]
+        mask = 0
+        for u in mb_var[mb_start[v]:mb_start[v + 1]]:
+            mask |= ((1 << width[u]) - 1) << off[u]
+        sp.mbmask[v] = mask
+    S = np.arange(1 << bits)
+    fields = np.stack([(S >> off[v]) & ((1 << width[v]) - 1) for v in range(n)], axis=1)
+    valid = (fields < np.asarray(cards)[None, :]).all(axis=1)
+    jcell = np.zeros((1 << bits, n), dtype=np.int64)
+    for v in range(n):
+        cfg = np.zeros(1 << bits, dtype=np.int64)
+        for p, st in zip(net.parents[v], net.parent_strides(v)):
+            cfg += fields[:, p] * int(st)
+        jcell[:, v] = np.where(valid, lay.cpt_off[v] + cfg * cards[v] + fields[:, v], 0)
+    return sp, jcell.astype(np.int32)
 
 
 class NetPack:
@@ -196,13 +283,20 @@ class NetPack:
         s = SgNet()
         for k, v in lay.scalars.items():
             setattr(s, k, v)
-        for k in NET_POINTERS:
+        for k in NET_POINTERS + NET_POINTERS_TAIL:
             if k in offs32:
                 setattr(s, k, self.buf32.data_ptr() + 4 * offs32[k])
             else:
                 setattr(s, k, self.buf64.data_ptr() + 8 * offs64[k])
         self.struct = s
         self.ref = ctypes.byref(self.struct)
+        plan = small_plan(net, lay)
+        self.small = None
+        if plan is not None:
+            sp, jcell = plan
+            self.small = sp
+            self.small_ref = ctypes.byref(sp)
+            self.small_jcell = torch.from_numpy(jcell.ravel()).to(device)
 
     @property
     def n(self) -> int:

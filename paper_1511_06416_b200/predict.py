@@ -52,7 +52,7 @@ def predict_missing(net, cpts, context, targets, num_samples: int, seed: int, bu
               ikeys.data_ptr(), rej.data_ptr(), err.ptr, s)
     cpt = torch.from_numpy(pack.flatten(cpts.tables)).to(dev)
     ptab = torch.empty(max(1, pack.layout.scalars["ptab_size"]), dtype=torch.float64, device=dev)
-    ftab = torch.empty(max(1, pack.layout.scalars["ftab_size"]), dtype=torch.int32, device=dev)
+    ftab = torch.empty(pack.layout.scalars["ftab_size"] + 1, dtype=torch.int32, device=dev)
     _lib.call("sg_build_tables", pack.ref, cpt.data_ptr(), ptab.data_ptr(), ftab.data_ptr(), s)
     max_card = int(max((net.cardinalities[v] for v in t_vars), default=0))
     freq = torch.zeros((len(t_vars), max(max_card, 1)), dtype=torch.float64, device=dev)
@@ -62,7 +62,7 @@ def predict_missing(net, cpts, context, targets, num_samples: int, seed: int, bu
     for it in range(burn_in + num_samples):
         keys = keys_for(derive_seed(seed, "predict", it), "var")
         _lib.call("sg_sweep", pack.ref, db.ref, cpt.data_ptr(), ptab.data_ptr(), ftab.data_ptr(),
-                  _lib.SG_RNG_NUMPY, 0, keys.data_ptr(), None, None, None, err.ptr, s)
+                  _lib.SG_RNG_NUMPY, 0, None, keys.data_ptr(), None, None, None, err.ptr, s)
         if it >= burn_in and len(t_vars):
             states = (db.states[tv, 0, tc].to(torch.int64) & 0x7F)
             freq.index_put_((rows, states), torch.ones_like(rows, dtype=torch.float64), accumulate=True)

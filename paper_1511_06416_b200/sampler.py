@@ -330,7 +330,7 @@ def _device_pass(net: Network, coloring: Coloring, cpts: CptSet, batch: Replicat
     db.compute_ranks()
     cpt = torch.from_numpy(pack.flatten(cpts.tables)).to(dev)
     ptab = torch.empty(max(1, pack.layout.scalars["ptab_size"]), dtype=torch.float64, device=dev)
-    ftab = torch.empty(max(1, pack.layout.scalars["ftab_size"]), dtype=torch.int32, device=dev)
+    ftab = torch.empty(pack.layout.scalars["ftab_size"] + 1, dtype=torch.int32, device=dev)
     s = stream_handle()
     _lib.call("sg_build_tables", pack.ref, cpt.data_ptr(), ptab.data_ptr(), ftab.data_ptr(), s)
     err = ErrorWord(dev)
@@ -349,14 +349,14 @@ def _device_pass(net: Network, coloring: Coloring, cpts: CptSet, batch: Replicat
         u_dev = torch.from_numpy(flat).to(dev)
         off_dev = torch.from_numpy(off).to(dev)
         _lib.call("sg_sweep", pack.ref, db.ref, cpt.data_ptr(), ptab.data_ptr(), ftab.data_ptr(),
-                  _lib.SG_RNG_INJECTED, 0, None, u_dev.data_ptr(), off_dev.data_ptr(), cptr, err.ptr, s)
+                  _lib.SG_RNG_INJECTED, 0, None, None, u_dev.data_ptr(), off_dev.data_ptr(), cptr, err.ptr, s)
     elif rng == "fast":
         _lib.call("sg_sweep", pack.ref, db.ref, cpt.data_ptr(), ptab.data_ptr(), ftab.data_ptr(),
-                  _lib.SG_RNG_FAST, int(sweep_seed) & 0xFFFFFFFFFFFFFFFF, None, None, None, cptr, err.ptr, s)
+                  _lib.SG_RNG_FAST, int(sweep_seed) & 0xFFFFFFFFFFFFFFFF, None, None, None, None, cptr, err.ptr, s)
     else:
         keys = _var_keys(sweep_seed, "var", (), n, dev)
         _lib.call("sg_sweep", pack.ref, db.ref, cpt.data_ptr(), ptab.data_ptr(), ftab.data_ptr(),
-                  _lib.SG_RNG_NUMPY, 0, keys.data_ptr(), None, None, cptr, err.ptr, s)
+                  _lib.SG_RNG_NUMPY, 0, None, keys.data_ptr(), None, None, cptr, err.ptr, s)
     word = err.read()
     _raise_errors(word)
     _download_states(db, batch)

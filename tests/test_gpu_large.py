@@ -51,12 +51,11 @@ def test_config2_fast_mode_properties(config2):
     mb = next(iter(src))
     eng.visit(mb, 0, M)
     torch.cuda.synchronize()
-    db = eng.latent[0]
     counts = eng.prev_counts[0].cpu().numpy()
     for v in range(net.num_vars):
         a, b = eng.pack.layout.cpt_off[v], eng.pack.layout.cpt_off[v + 1]
         assert counts[a:b].sum() == M * CASES
-    st = db.states[:, :, :CASES]
+    st = eng.lane_states(0)[:, :, :CASES]
     lat = (st < 0)
     o = obs[:, :CASES]
     # observed cells hold the data in every replica; latent flags follow the mask
