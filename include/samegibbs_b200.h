@@ -296,6 +296,39 @@ int sg_small_export(const sg_small* sp, const sg_batch* batch, const int32_t* ca
                     const uint8_t* pattern, const uint8_t* lanes, int32_t lane_ld,
                     void* stream);
 
+/*
+ * The model-sized tail of a minibatch step, fused: accumulator
+ * (sg_accumulate) -> CPT update (sg_mean_cpts / sg_sample_cpts) ->
+ * conditional tables (sg_build_tables) -> packed tables (sg_small_tables,
+ * when sp != NULL) -> clear the next visit's count buffer -> advance the key
+ * cursor (sg_keys_advance).  One single-CTA kernel when the model has at
+ * most 4096 cells, else the separate launches; identical results either
+ * way.  Optional members may be NULL.
+ */
+typedef struct sg_finish {
+  int32_t acc_mode;           /* SG_ACC_MOVING / SG_ACC_EXPONENTIAL */
+  int32_t map_estimate;       /* 1: posterior mean, 0: Dirichlet draw */
+  double decay;               /* exponential decay */
+  double* total;              /* [dev] [cells] fp64 running total */
+  const uint64_t* new_counts; /* [dev] [cells] this visit's tally */
+  const uint64_t* prev_counts;/* [dev] [cells] this minibatch's previous tally (moving) or NULL */
+  const double* alpha;        /* [dev] [n] prior concentration per variable */
+  uint64_t key;               /* Dirichlet key derive_seed(derive_seed(seed,"cpt_update",pass,mb),"sample_cpts") */
+  const uint64_t* key_dev;    /* [dev] or NULL: read the key from device memory */
+  double* cpt;                /* [dev] [cells] out: CPTs of the next visit */
+  double* ptab;               /* [dev] parity table (sg_build_tables) */
+  uint32_t* ftab;             /* [dev] fast table + zero-support flag word */
+  uint32_t* stab;             /* [dev] packed table (sp != NULL) */
+  uint64_t* clear_counts;     /* [dev] [cells] buffer to zero, or NULL */
+  const uint64_t* key_table;  /* [dev] [steps][kps] key cursor table, or NULL */
+  int32_t* key_index;         /* [dev] cursor */
+  int32_t kps;                /* keys per step */
+  int32_t pad_;
+  uint64_t* key_current;      /* [dev] [kps] */
+} sg_finish;
+
+int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_finish* f, void* stream);
+
 /* Device key cursor for CUDA-graph replay of minibatch steps:
    current[0..kps) = table[*index * kps ...]; *index += 1.  Kernels given
    key_dev = current + k then read fresh keys on every replay. */

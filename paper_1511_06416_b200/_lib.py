@@ -63,6 +63,16 @@ class SgSmall(ctypes.Structure):
         [(name, ctypes.c_int32 * SMALL_MAXV) for name in ("card", "toff")]
 
 
+class SgFinish(ctypes.Structure):
+    _fields_ = [
+        ("acc_mode", c_int32), ("map_estimate", c_int32), ("decay", c_double),
+        ("total", c_void_p), ("new_counts", c_void_p), ("prev_counts", c_void_p), ("alpha", c_void_p),
+        ("key", c_uint64), ("key_dev", c_void_p), ("cpt", c_void_p), ("ptab", c_void_p), ("ftab", c_void_p),
+        ("stab", c_void_p), ("clear_counts", c_void_p), ("key_table", c_void_p), ("key_index", c_void_p),
+        ("kps", c_int32), ("pad_", c_int32), ("key_current", c_void_p),
+    ]
+
+
 _SIGNATURES = {
     "sg_abi_version": ([], c_int32),
     "sg_last_error": ([], ctypes.c_char_p),
@@ -89,6 +99,7 @@ _SIGNATURES = {
                         c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
                         c_void_p], c_int32),
     "sg_keys_advance": ([c_void_p, c_void_p, c_int32, c_void_p, c_void_p], c_int32),
+    "sg_step_finish": ([POINTER(SgNet), c_void_p, POINTER(SgFinish), c_void_p], c_int32),
     "sg_small_import": ([POINTER(SgSmall), POINTER(SgBatch), c_void_p, c_void_p, c_int32, c_void_p], c_int32),
     "sg_small_export": ([POINTER(SgSmall), POINTER(SgBatch), c_void_p, c_void_p, c_void_p, c_int32, c_void_p],
                         c_int32),
@@ -132,7 +143,7 @@ KERNELS_PER_CALL = {
     "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
     "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
-    "sg_keys_advance": 1,
+    "sg_keys_advance": 1, "sg_step_finish": 1,
 }
 launch_count = 0
 

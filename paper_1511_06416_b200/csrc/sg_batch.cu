@@ -203,11 +203,23 @@ __global__ void __launch_bounds__(256) k_init_states(const sg_net net, const sg_
 
 __global__ void __launch_bounds__(256) k_check_range(const sg_net net, const int8_t* __restrict__ obs, int ld,
                                                      int cases, int32_t* err) {
+  // 16 cases per thread-load; bytes compared as signed SIMD lanes against card-1
   const int v = blockIdx.y;
-  const int card = __ldg(net.card + v);
-  bool bad = false;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cases; c += gridDim.x * blockDim.x)
-    bad |= obs[int64_t(v) * ld + c] >= card;
+  const uint32_t lim = 0x01010101u * uint32_t(__ldg(net.card + v) - 1);
+  const int chunks = (cases + 15) >> 4;
+  unsigned bad = 0;
+  for (int ch = blockIdx.x * blockDim.x + threadIdx.x; ch < chunks; ch += gridDim.x * blockDim.x) {
+    const int4 q = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld + ch * 16));
+    uint32_t w[4] = {uint32_t(q.x), uint32_t(q.y), uint32_t(q.z), uint32_t(q.w)};
+    const int left = cases - ch * 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t gt = __vcmpgts4(w[i], lim);  // 0xFF in every byte holding a state > card-1
+      const int valid = left - 4 * i;
+      if (valid < 4) gt &= valid <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - valid)));
+      bad |= gt;
+    }
+  }
   if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
 }
 
@@ -262,8 +274,11 @@ extern "C" int sg_check_range(const sg_net* net, const int8_t* obs, int32_t ld_o
                               void* stream) {
   using namespace sg;
   SG_REQUIRE(net && obs && err, "sg_check_range: null argument");
+  SG_REQUIRE(ld_obs % 16 == 0 && (reinterpret_cast<uintptr_t>(obs) & 15) == 0 && ld_obs >= cases,
+             "sg_check_range: obs rows must be 16-byte aligned");
   if (cases == 0) return SG_OK;
-  const int gx = std::min((cases + 255) / 256, 256);
+  const int chunks = (cases + 15) / 16;
+  const int gx = std::min((chunks + 255) / 256, 1024);
   k_check_range<<<dim3(gx, net->n), 256, 0, (cudaStream_t)stream>>>(*net, obs, ld_obs, cases, err);
   return check_launch("sg_check_range");
 }

@@ -122,17 +122,26 @@ __device__ __forceinline__ double np_pairwise_sum(const double* a, int n) {
   return s;
 }
 
+// CPT reads: through the read-only path when the CPTs are kernel inputs,
+// plain loads when the same kernel just wrote them (sg_step_finish).
+template <bool RO>
+__device__ __forceinline__ double cpt_load(const double* p) {
+  if (RO) return __ldg(p);
+  return *p;
+}
+
 // Reference full-conditional weights of v given its Markov-blanket states
 // s[slot] (sampler.py:226-240): w = T_v[cfg, :], then for each child c in
 // ascending order w[t] *= T_c[cfg0_c + t*stride_vc, x_c].
+template <bool RO = true>
 __device__ __forceinline__ void conditional_weights(const sg_net& net, int v, const int* s,
-                                                    const double* __restrict__ cpt, double* w) {
+                                                    const double* cpt, double* w) {
   const int card = __ldg(net.card + v);
   int64_t cfg = 0;
   for (int j = __ldg(net.par_start + v), e = __ldg(net.par_start + v + 1); j < e; ++j)
     cfg += int64_t(s[__ldg(net.par_slot + j)]) * __ldg(net.par_stride + j);
   const double* row = cpt + __ldg(net.cpt_off + v) + cfg * card;
-  for (int t = 0; t < card; ++t) w[t] = __ldg(row + t);
+  for (int t = 0; t < card; ++t) w[t] = cpt_load<RO>(row + t);
   for (int k = __ldg(net.chl_start + v), ke = __ldg(net.chl_start + v + 1); k < ke; ++k) {
     const int c = __ldg(net.chl_var + k);
     const int cc = __ldg(net.card + c);
@@ -142,8 +151,127 @@ __device__ __forceinline__ void conditional_weights(const sg_net& net, int v, co
       cfg0 += int64_t(s[__ldg(net.chl_pslot + q)]) * __ldg(net.chl_pstride + q);
     const int64_t vs = __ldg(net.chl_vstride + k);
     const double* tc = cpt + __ldg(net.cpt_off + c) + xc;
-    for (int t = 0; t < card; ++t) w[t] = __dmul_rn(w[t], __ldg(tc + (cfg0 + t * vs) * cc));
+    for (int t = 0; t < card; ++t) w[t] = __dmul_rn(w[t], cpt_load<RO>(tc + (cfg0 + t * vs) * cc));
   }
+}
+
+// Sequential draws of one Philox4x32 substream (counter = (cell, call, hi, tag))
+// for the Dirichlet CPT update.
+struct CellStream {
+  uint32_t k0, k1, cell_lo, cell_hi, call;
+  u32x4 buf;
+  int used;
+  __device__ CellStream(uint64_t key, uint64_t cell)
+      : k0(uint32_t(key)), k1(uint32_t(key >> 32)), cell_lo(uint32_t(cell)), cell_hi(uint32_t(cell >> 32)),
+        call(0), used(4) {}
+  __device__ uint32_t next() {
+    if (used == 4) {
+      buf = philox4x32_10(u32x4{cell_lo, call++, cell_hi, 0x5A4D0001u}, k0, k1);
+      used = 0;
+    }
+    return pick(buf, used++);
+  }
+  // uniform in (0, 1): 53 bits, never 0
+  __device__ double uniform() {
+    const uint64_t hi = next() >> 5, lo = next() >> 6;  // 27 + 26 bits
+    return (double((hi << 26) | lo) + 0.5) * 0x1.0p-53;
+  }
+  __device__ double normal() {
+    const double u1 = uniform(), u2 = uniform();
+    return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+};
+
+// log of a Gamma(a, 1) draw, a > 0 (Marsaglia & Tsang 2000; a < 1 via
+// Gamma(a) = Gamma(a + 1) * U^(1/a), kept in log space so tiny shapes never
+// underflow -- the degenerate-row redraw of model.py:168-176 is not needed).
+__device__ __forceinline__ double log_gamma_draw(CellStream& rs, double a) {
+  double boost = 0.0;
+  if (a < 1.0) {
+    boost = log(rs.uniform()) / a;
+    a += 1.0;
+  }
+  const double d = a - 1.0 / 3.0;
+  const double c = 1.0 / sqrt(9.0 * d);
+  for (;;) {
+    double x, v;
+    do {
+      x = rs.normal();
+      v = 1.0 + c * x;
+    } while (v <= 0.0);
+    v = v * v * v;
+    const double u = rs.uniform();
+    const double x2 = x * x;
+    if (u < 1.0 - 0.0331 * x2 * x2 || log(u) < 0.5 * x2 + d * (1.0 - v + log(v)))
+      return log(d) + log(v) + boost;
+  }
+}
+
+// Normalise one row of log-gamma draws into Dirichlet probabilities.
+__device__ __forceinline__ void dirichlet_normalise(const double* lg, int card, double* out) {
+  double mx = -INFINITY;
+  for (int s = 0; s < card; ++s) mx = fmax(mx, lg[s]);
+  double e[SG_MAX_CARD];
+  double sum = 0.0;
+  for (int s = 0; s < card; ++s) {
+    e[s] = exp(lg[s] - mx);
+    sum += e[s];
+  }
+  for (int s = 0; s < card; ++s) out[s] = e[s] / sum;
+}
+
+// One conditional-table entry from the weights w[0..card) of a blanket
+// configuration: pe = cum[0..card-2], norm; fe = ceil(cum/norm * 2^31)
+// thresholds (0xFFFFFFFF in slot 0 and *zs_flag set when norm <= 0).
+__device__ __forceinline__ void table_entry(const double* w, int card, double* pe, uint32_t* fe,
+                                            uint32_t* zs_flag) {
+  const double norm = np_pairwise_sum(w, card);
+  const bool ok = norm > 0.0;
+  double cum = 0.0;
+  for (int t = 0; t < card - 1; ++t) {
+    cum = t ? __dadd_rn(cum, w[t]) : w[0];
+    pe[t] = cum;
+    double q = ok ? ceil(__ddiv_rn(cum, norm) * 2147483648.0) : 0.0;
+    q = fmin(q, 2147483648.0);
+    fe[t] = (t == 0 && !ok) ? 0xFFFFFFFFu : uint32_t(q);
+  }
+  pe[card - 1] = norm;
+  if (!ok) atomicOr(reinterpret_cast<int*>(zs_flag), 1);
+}
+
+__device__ __forceinline__ int small_field(uint32_t S, const sg_small& sp, int v) {
+  return int((S >> sp.off[v]) & ((1u << sp.width[v]) - 1u));
+}
+
+// Packed-lane table word(s) i = (v, S): the generic FAST thresholds of the
+// blanket configuration that lane word S encodes (0 for unused words).
+// Plain loads: ftab may have been written by the same kernel.
+__device__ __forceinline__ void small_table_entry(const sg_net& net, const sg_small& sp, const uint32_t* ftab,
+                                                  uint32_t* stab, int i) {
+  const int v = i >> sp.bits;
+  const uint32_t S = uint32_t(i & ((1 << sp.bits) - 1));
+  const int card = sp.card[v];
+  uint32_t* out = stab + sp.toff[v] + S * (card - 1);
+  bool valid = (S & ~sp.mbmask[v]) == 0u;
+  int64_t e = 0;
+  for (int k = __ldg(net.mb_start + v), ke = __ldg(net.mb_start + v + 1); k < ke && valid; ++k) {
+    const int u = __ldg(net.mb_var + k);
+    const int s = small_field(S, sp, u);
+    valid = s < sp.card[u];
+    e += int64_t(s) * __ldg(net.mb_stride + k);
+  }
+  const uint32_t* src = ftab + __ldg(net.ftab_off + v) + e * (card - 1);
+  for (int t = 0; t < card - 1; ++t) out[t] = valid ? src[t] : 0u;
+}
+
+// Variable owning CPT cell `cell` (binary search over cpt_off).
+__device__ __forceinline__ int cell_var(const sg_net& net, int64_t cell) {
+  int lo = 0, hi = net.n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(net.cpt_off + mid) <= cell) lo = mid; else hi = mid;
+  }
+  return lo;
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

@@ -25,30 +25,13 @@ namespace sg {
 
 static constexpr int SMALL_PATTERNS = 1 << SG_SMALL_MAXV;
 
-__device__ __forceinline__ int small_field(uint32_t S, const sg_small& sp, int v) {
-  return int((S >> sp.off[v]) & ((1u << sp.width[v]) - 1u));
-}
-
 // Sparse conditional tables: entry S (S & ~mbmask_v == 0) of v = generic
 // table entry of the blanket configuration encoded in S.
 __global__ void k_small_tables(const sg_net net, const sg_small sp, const uint32_t* __restrict__ ftab,
                                uint32_t* __restrict__ stab) {
   const int total = sp.n << sp.bits;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int v = i >> sp.bits;
-    const uint32_t S = uint32_t(i & ((1 << sp.bits) - 1));
-    const int card = sp.card[v];
-    uint32_t* out = stab + sp.toff[v] + S * (card - 1);
-    bool valid = (S & ~sp.mbmask[v]) == 0u;
-    int64_t e = 0;
-    for (int k = __ldg(net.mb_start + v), ke = __ldg(net.mb_start + v + 1); k < ke && valid; ++k) {
-      const int u = __ldg(net.mb_var + k);
-      const int s = small_field(S, sp, u);
-      valid = s < sp.card[u];
-      e += int64_t(s) * __ldg(net.mb_stride + k);
-    }
-    for (int t = 0; t < card - 1; ++t) out[t] = valid ? __ldg(ftab + __ldg(net.ftab_off + v) + e * (card - 1) + t) : 0u;
-  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
+    small_table_entry(net, sp, ftab, stab, i);
 }
 
 // Pattern histogram of the minibatch's cases.

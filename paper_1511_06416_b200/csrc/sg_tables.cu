@@ -37,20 +37,8 @@ k_build_tables(const sg_net net, const double* __restrict__ cpt, double* __restr
     }
     double w[SG_MAX_CARD];
     conditional_weights(net, v, s, cpt, w);
-    const double norm = np_pairwise_sum(w, card);
-    double* pe = ptab + __ldg(net.ptab_off + v) + e * card;
-    uint32_t* fe = ftab + __ldg(net.ftab_off + v) + e * (card - 1);
-    double cum = 0.0;
-    const bool ok = norm > 0.0;
-    for (int t = 0; t < card - 1; ++t) {
-      cum = t ? __dadd_rn(cum, w[t]) : w[0];
-      pe[t] = cum;
-      double q = ok ? ceil(__ddiv_rn(cum, norm) * 2147483648.0) : 0.0;
-      q = fmin(q, 2147483648.0);
-      fe[t] = (t == 0 && !ok) ? 0xFFFFFFFFu : uint32_t(q);
-    }
-    pe[card - 1] = norm;
-    if (!ok) atomicOr(reinterpret_cast<int*>(ftab + net.ftab_size), 1);
+    table_entry(w, card, ptab + __ldg(net.ptab_off + v) + e * card, ftab + __ldg(net.ftab_off + v) + e * (card - 1),
+                ftab + net.ftab_size);
   }
 }
 

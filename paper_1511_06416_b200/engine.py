@@ -114,6 +114,7 @@ class Engine:
         self.use_small = can_small if small is None else (bool(small) and can_small)
         if self.use_small:
             self.stab = torch.empty(max(1, self.pack.small.tab_words), dtype=torch.int32, device=d)
+        self.tables_fresh = False  # conditional tables reflect self.cpt
 
     # ------------------------------------------------------------ helpers
     def _upload_keys(self, seed: int, label: str, context: tuple) -> None:
@@ -203,11 +204,13 @@ class Engine:
                     key = derive_seed(cfg.seed, "latent_init", pass_index, mb.index)
                     _lib.call("sg_init_states", self.pack.ref, db.ref, obs.data_ptr(), ld, _lib.SG_RNG_FAST, key,
                               None, None, self.err.ptr, s)
-        _lib.call("sg_build_tables", self.pack.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
-                  self.ftab.data_ptr(), s)
-        if self.use_small:
-            _lib.call("sg_small_tables", self.pack.ref, self.pack.small_ref, self.ftab.data_ptr(),
-                      self.stab.data_ptr(), s)
+        if not self.tables_fresh:  # the previous visit's finish built them from the current CPTs
+            _lib.call("sg_build_tables", self.pack.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
+                      self.ftab.data_ptr(), s)
+            if self.use_small:
+                _lib.call("sg_small_tables", self.pack.ref, self.pack.small_ref, self.ftab.data_ptr(),
+                          self.stab.data_ptr(), s)
+            self.tables_fresh = True
         new_counts = torch.zeros_like(self.counts) if moving else self.counts
         if not moving:
             new_counts.zero_()
@@ -239,24 +242,45 @@ class Engine:
             timing.append((ev0, ev1, S))
         if self.comm is not None:
             self.comm(new_counts)
+        prev = self.prev_counts.get(mb.index) if moving else None
+        key = 0 if cfg.map_estimate else derive_seed(derive_seed(cfg.seed, "cpt_update", pass_index, mb.index),
+                                                     "sample_cpts")
+        f = self.finish_args(new_counts, prev, key)
+        _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
         if moving:
-            prev = self.prev_counts.get(mb.index)
-            _lib.call("sg_accumulate", _lib.SG_ACC_MOVING, self.total.data_ptr(), new_counts.data_ptr(),
-                      None if prev is None else prev.data_ptr(), 1.0, self.pack.cells, s)
             self.prev_counts[mb.index] = new_counts
             self.latent[mb.index] = db
-        else:
-            _lib.call("sg_accumulate", _lib.SG_ACC_EXPONENTIAL, self.total.data_ptr(), new_counts.data_ptr(),
-                      None, cfg.exp_decay, self.pack.cells, s)
-        if cfg.map_estimate:
-            _lib.call("sg_mean_cpts", self.pack.ref, self.total.data_ptr(), self.alpha.data_ptr(),
-                      self.cpt.data_ptr(), s)
-        else:
-            key = derive_seed(derive_seed(cfg.seed, "cpt_update", pass_index, mb.index), "sample_cpts")
-            _lib.call("sg_sample_cpts", self.pack.ref, self.total.data_ptr(), self.alpha.data_ptr(), key, None,
-                      self.cpt.data_ptr(), s)
         self.batch_bytes = max(self.batch_bytes, self.n * m * size * 4 + m * size * 8)
         self._last_batch = db
+
+    def finish_args(self, new_counts, prev_counts, key: int, key_dev: int | None = None, clear=None,
+                    cursor=None):
+        """``sg_finish`` of one visit: accumulate, CPT update, next visit's tables."""
+        cfg = self.cfg
+        f = _lib.SgFinish()
+        f.acc_mode = _lib.SG_ACC_MOVING if cfg.accumulator_mode == "moving_sum" else _lib.SG_ACC_EXPONENTIAL
+        f.map_estimate = 1 if cfg.map_estimate else 0
+        f.decay = cfg.exp_decay
+        f.total = self.total.data_ptr()
+        f.new_counts = new_counts.data_ptr()
+        f.prev_counts = None if prev_counts is None else prev_counts.data_ptr()
+        f.alpha = self.alpha.data_ptr()
+        f.key = key
+        f.key_dev = key_dev
+        f.cpt = self.cpt.data_ptr()
+        f.ptab = self.ptab.data_ptr()
+        f.ftab = self.ftab.data_ptr()
+        f.stab = self.stab.data_ptr() if self.use_small else None
+        f.clear_counts = None if clear is None else clear.data_ptr()
+        if cursor is not None:
+            table, index, kps, current = cursor
+            f.key_table, f.key_index, f.kps, f.key_current = table.data_ptr(), index.data_ptr(), kps, current.data_ptr()
+        self._finish_keepalive = f
+        return f
+
+    @property
+    def small_ptr(self):
+        return self.pack.small_ref if self.use_small else None
 
     def lane_states(self, mb_index: int) -> torch.Tensor:
         """int8 [n][m][pitch] lane states of a resident minibatch (generic layout, flags in bit 7)."""
@@ -358,6 +382,12 @@ class StepGraphs:
             raise ValueError("obs_buffer must be an int8 (n, pitch) tensor with 16-byte aligned rows")
         self.obs, self.ld = obs_buffer, obs_buffer.stride(0)
         self.graphs = []
+        self._finish_args = []
+        if not eng.tables_fresh:
+            raise ValueError("engine tables are stale")
+        # keys of the first replayed visit; every replay's finish advances the cursor
+        _lib.call("sg_keys_advance", self.table.data_ptr(), self.idx.data_ptr(), kps, self.cur.data_ptr(),
+                  stream_handle())
         torch.cuda.synchronize()
         for parity in (0, 1):
             g = torch.cuda.CUDAGraph()
@@ -372,12 +402,8 @@ class StepGraphs:
         size = self.mb.size
         cur = self.cur.data_ptr()
         new, prev = self.cbuf[p], self.cbuf[1 - p]
-        _lib.call("sg_keys_advance", self.table.data_ptr(), self.idx.data_ptr(), self.kps, cur, s)
+        # tables and keys of this visit are ready: the previous replay's finish built/advanced them
         _lib.call("sg_check_range", eng.pack.ref, self.obs.data_ptr(), self.ld, size, eng.err.ptr, s)
-        _lib.call("sg_build_tables", eng.pack.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(), eng.ftab.data_ptr(), s)
-        if eng.use_small:
-            _lib.call("sg_small_tables", eng.pack.ref, eng.pack.small_ref, eng.ftab.data_ptr(), eng.stab.data_ptr(), s)
-        new.zero_()
         S = cfg.sweeps_per_minibatch
         for sw in range(S):
             counts_ptr = new.data_ptr() if sw == S - 1 else None
@@ -392,13 +418,11 @@ class StepGraphs:
                           eng.err.ptr, s)
         if eng.comm is not None:
             eng.comm(new)
-        _lib.call("sg_accumulate", _lib.SG_ACC_MOVING, eng.total.data_ptr(), new.data_ptr(), prev.data_ptr(), 1.0,
-                  eng.pack.cells, s)
-        if cfg.map_estimate:
-            _lib.call("sg_mean_cpts", eng.pack.ref, eng.total.data_ptr(), eng.alpha.data_ptr(), eng.cpt.data_ptr(), s)
-        else:
-            _lib.call("sg_sample_cpts", eng.pack.ref, eng.total.data_ptr(), eng.alpha.data_ptr(), 0, cur + 8 * S,
-                      eng.cpt.data_ptr(), s)
+        # accumulate, CPT update, next tables, clear `prev` (the next replay's count buffer), advance keys
+        f = eng.finish_args(new, prev, 0, key_dev=cur + 8 * S, clear=prev,
+                            cursor=(self.table, self.idx, self.kps, self.cur))
+        self._finish_args.append(f)
+        _lib.call("sg_step_finish", eng.pack.ref, eng.small_ptr, f, s)
 
     def step(self, mb=None) -> None:
         """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
@@ -415,8 +439,8 @@ class StepGraphs:
 
     @property
     def launches_per_step(self) -> int:
-        n = 5 + self.eng.cfg.sweeps_per_minibatch + (1 if self.eng.use_small else 0)
-        return n
+        fused = self.eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
+        return 1 + self.eng.cfg.sweeps_per_minibatch + (1 if fused else 5 + (1 if self.eng.use_small else 0))
 
     def finish(self) -> None:
         """Hand the last visit's counts back to the engine's moving-sum bookkeeping."""
