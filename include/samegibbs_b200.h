@@ -245,7 +245,8 @@ int sg_forward_sample(const sg_net* net, const double* cpt, const int32_t* topo,
  * a uint8 word S; the conditional table of v is indexed by S & mbmask[v];
  * cases are bucketed by latent pattern so warps run one variable loop.
  * Draws and counters equal sg_sweep's FAST mode (same states and counts).
- *   lanes   uint8 [m][lane_ld]  lane words, slot order
+ *   lanes   uint8 [cases][lane_ld]  lane words, slot-major: lane (r, s) at
+ *                               s*lane_ld + r; lane_ld = 4, 8, 16 or 32 >= m
  *   pattern uint8 [cases]       latent-variable bit mask of each slot
  *   case_id int32 [cases]       minibatch case held by each slot
  */
@@ -262,7 +263,8 @@ typedef struct sg_small {
   int32_t width[SG_SMALL_MAXV];   /* bit width of v's field */
   uint32_t mbmask[SG_SMALL_MAXV]; /* lane-word bits of v's Markov blanket */
   int32_t card[SG_SMALL_MAXV];
-  int32_t toff[SG_SMALL_MAXV];    /* first word of v's sparse table ((card-1) words per S) */
+  int32_t toff[SG_SMALL_MAXV];    /* first word of v's sparse table */
+  int32_t tstride[SG_SMALL_MAXV]; /* words per lane-word entry: card-1 rounded up to 1, 2 or 4 (aligned) */
 } sg_small;
 
 /* Gather sg_build_tables' FAST thresholds into the sparse per-lane-word table

@@ -60,7 +60,7 @@ class SgSmall(ctypes.Structure):
     _fields_ = [("n", c_int32), ("bits", c_int32), ("tab_words", c_int32), ("pad_", c_int32)] + \
         [(name, ctypes.c_int32 * SMALL_MAXV) for name in ("order", "off", "width")] + \
         [("mbmask", ctypes.c_uint32 * SMALL_MAXV)] + \
-        [(name, ctypes.c_int32 * SMALL_MAXV) for name in ("card", "toff")]
+        [(name, ctypes.c_int32 * SMALL_MAXV) for name in ("card", "toff", "tstride")]
 
 
 class SgFinish(ctypes.Structure):

@@ -251,7 +251,7 @@ __device__ __forceinline__ void small_table_entry(const sg_net& net, const sg_sm
   const int v = i >> sp.bits;
   const uint32_t S = uint32_t(i & ((1 << sp.bits) - 1));
   const int card = sp.card[v];
-  uint32_t* out = stab + sp.toff[v] + S * (card - 1);
+  uint32_t* out = stab + sp.toff[v] + S * sp.tstride[v];
   bool valid = (S & ~sp.mbmask[v]) == 0u;
   int64_t e = 0;
   for (int k = __ldg(net.mb_start + v), ke = __ldg(net.mb_start + v + 1); k < ke && valid; ++k) {

@@ -2,23 +2,28 @@
 //
 // When every variable's state fits in a bit field and the whole lane fits in
 // one byte (sum of field widths <= 7; Koller: 1+1+1+2+1 = 6 bits), a lane is
-// a single uint8 word S.  Three consequences make the sweep cheap:
+// a single uint8 word S.  Consequences that make the sweep cheap:
 //
 //  * the full conditional of v is a function of (S & mbmask_v), so the
-//    conditional table is indexed by the masked lane word itself -- one LOP
-//    and one LDS per draw, no blanket arithmetic;
-//  * the latent pattern of a case (which variables are missing) is shared by
-//    its m replicas; cases are bucketed by pattern once per minibatch
-//    (counting sort, sg_small_prepare) so a warp's threads run the same
-//    variable loop -- no divergence, and only latent variables cost work;
+//    conditional table is indexed by the masked lane word itself;
+//  * the latent pattern of a case is shared by its m replicas; cases are
+//    bucketed by pattern once per minibatch (counting sort,
+//    sg_small_prepare) so a warp's threads run the same variable loop -- no
+//    divergence, and only latent variables cost work;
+//  * lane words are stored in quads: 32-bit word (q, s) holds replicas
+//    4q..4q+3 of slot s (one byte each), quad rows contiguous over slots.  A
+//    thread owns one (slot, quad) word -- coalesced 4-byte loads, few
+//    registers, full occupancy to hide the Philox round latency -- and works
+//    on its 4 lanes with byte-SIMD masking and bit insertion;
 //  * the tally histograms S directly (2^bits joint states, per-thread byte
 //    counters), expanded to CPT cells once per CTA.
 //
-// Layout (sg_small_batch): lanes uint8 [m][B] in bucketed slot order;
-// pattern uint8 [B]; case_id int32 [B] (slot -> case of the minibatch).
+// Layout: lanes uint32 [ceil(m/4)][lane_ld] (lane_ld >= cases words, slots in
+// bucketed order; lane (r, s) = byte r%4 of word (r/4, s)); pattern uint8
+// [cases]; case_id int32 [cases].
 // Counters and draws are identical to the generic kernel's FAST mode
 // (Philox4x32 on (case, variable, replica quad)), so both paths produce the
-// same states and counts from the same tables (tested).
+// same states and counts from the same tables (tests/test_gpu_small.py).
 #include "sg_device.cuh"
 
 namespace sg {
@@ -97,6 +102,7 @@ __global__ void __launch_bounds__(256) k_small_scatter(
     const int o = obs[int64_t(v) * ld + c];
     if (o >= 0) obsw |= uint32_t(o) << sp.off[v];
   }
+  uint32_t* out = reinterpret_cast<uint32_t*>(lanes);
   for (int q = 0; q < (m + 3) / 4; ++q) {
     uint32_t S[4] = {obsw, obsw, obsw, obsw};
     for (int v = 0; v < sp.n; ++v) {
@@ -106,22 +112,24 @@ __global__ void __launch_bounds__(256) k_small_scatter(
 #pragma unroll
       for (int j = 0; j < 4; ++j) S[j] |= uint32_t((uint64_t(ws[j]) * uint32_t(sp.card[v])) >> 32) << sp.off[v];
     }
-    for (int j = 0; j < 4 && q * 4 + j < m; ++j) lanes[int64_t(q * 4 + j) * lane_ld + s] = uint8_t(S[j]);
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) word |= (q * 4 + j < m ? (S[j] & 0xFFu) : 0u) << (8 * j);
+    out[int64_t(q) * lane_ld + s] = word;
   }
 }
 
-// Restore the lane words of already-bucketed slots from generic int8 lane
-// states (layout switch), and the reverse export.
+// Layout switches with generic int8 lane states.
 __global__ void k_small_import(const sg_small sp, const sg_batch bt, const int32_t* __restrict__ case_id,
                                uint8_t* __restrict__ lanes, int lane_ld) {
   const int64_t total = int64_t(bt.m) * bt.cases;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int r = int(i / bt.cases), s = int(i - int64_t(r) * bt.cases);
+    const int s = int(i / bt.m), r = int(i - int64_t(s) * bt.m);
     const int c = case_id[s];
     uint32_t S = 0;
     for (int v = 0; v < sp.n; ++v)
       S |= uint32_t(bt.states[(int64_t(v) * bt.m + r) * bt.pitch + c] & 0x7F) << sp.off[v];
-    lanes[int64_t(r) * lane_ld + s] = uint8_t(S);
+    lanes[(int64_t(r >> 2) * lane_ld + s) * 4 + (r & 3)] = uint8_t(S);
   }
 }
 
@@ -129,9 +137,9 @@ __global__ void k_small_export(const sg_small sp, const sg_batch bt, const int32
                                const uint8_t* __restrict__ pattern, const uint8_t* __restrict__ lanes, int lane_ld) {
   const int64_t total = int64_t(bt.m) * bt.cases;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int r = int(i / bt.cases), s = int(i - int64_t(r) * bt.cases);
+    const int s = int(i / bt.m), r = int(i - int64_t(s) * bt.m);
     const int c = case_id[s];
-    const uint32_t S = lanes[int64_t(r) * lane_ld + s];
+    const uint32_t S = lanes[(int64_t(r >> 2) * lane_ld + s) * 4 + (r & 3)];
     const uint32_t P = pattern[s];
     for (int v = 0; v < sp.n; ++v)
       bt.states[(int64_t(v) * bt.m + r) * bt.pitch + c] =
@@ -139,15 +147,114 @@ __global__ void k_small_export(const sg_small sp, const sg_batch bt, const int32
   }
 }
 
-// The sweep.  A thread owns slot s (one case) and walks its replica quads;
-// the four lanes of a quad live in registers as lane words.
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int j) { return __byte_perm(w, 0u, 0x4440 | j); }
+
+// u >= t as 0/1 for 31-bit u and thresholds t <= 2^31 (sentinel 0xFFFFFFFF never passes).
+__device__ __forceinline__ uint32_t ge(uint32_t u, uint32_t t) { return u >= t ? 1u : 0u; }
+
+// Per-thread constants of the sweep (the variable loop is unrolled over N
+// colour-ordered positions, every per-variable constant in registers).
+template <int N>
+struct SmallCtx {
+  int VAR[N], SH[N], K1[N];
+  uint32_t MSK[N], CLR[N];
+  const uint32_t* TV[N];
+  uint32_t* row;
+  const uint8_t* pattern;
+  const int32_t* case_id;
+  uint8_t* hist8;
+  int cases, num_real, q, nl, slot;
+  uint32_t valid4;
+  int64_t case_base;
+  uint64_t key;
+  bool counts;
+};
+
+// Walk this thread's (slot, quad) units.  ARMED: some table entry has no
+// support, so every draw checks for the sentinel (the reference raises
+// ZeroSupport only when a lane actually hits such a configuration).
+template <int N, bool ARMED>
+__device__ __forceinline__ bool small_units(const SmallCtx<N>& x) {
+  const int stride = gridDim.x * SG_THREADS;
+  bool zs = false;
+  int s = blockIdx.x * SG_THREADS + threadIdx.x;
+  uint32_t nw = 0, nP = 0;
+  int nc = 0;
+  if (s < x.cases) {
+    nw = x.row[s];
+    nP = x.pattern[s];
+    nc = x.case_id[s];
+  }
+  for (; s < x.cases; s += stride) {
+    uint32_t w = nw;
+    const uint32_t P = nP;
+    const int c = nc;
+    const int sn = s + stride;
+    if (sn < x.cases) {  // prefetch the next unit while this one computes
+      nw = x.row[sn];
+      nP = x.pattern[sn];
+      nc = x.case_id[sn];
+    }
+    const uint64_t gc = uint64_t(x.case_base + c);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (!((P >> x.VAR[i]) & 1u)) continue;  // warp-uniform: slots are bucketed by pattern
+      const u32x4 r = fast_block(x.key, gc, uint32_t(x.VAR[i]), uint32_t(x.q), 0u);
+      const uint32_t u[4] = {r.a >> 1, r.b >> 1, r.c >> 1, r.d >> 1};
+      const uint32_t wm = w & x.MSK[i];
+      uint32_t xs[4];
+      if (x.K1[i] == 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t t = x.TV[i][byte_of(wm, j)];
+          if (ARMED && j < x.nl && t == 0xFFFFFFFFu) zs = true;
+          xs[j] = ge(u[j], t);
+        }
+      } else if (x.K1[i] == 2) {
+        const uint2* t2 = reinterpret_cast<const uint2*>(x.TV[i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint2 t = t2[byte_of(wm, j)];
+          if (ARMED && j < x.nl && t.x == 0xFFFFFFFFu) zs = true;
+          xs[j] = ge(u[j], t.x) + ge(u[j], t.y);
+        }
+      } else {
+        const uint4* t4 = reinterpret_cast<const uint4*>(x.TV[i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint4 t = t4[byte_of(wm, j)];  // card 4: three thresholds + padding
+          if (ARMED && j < x.nl && t.x == 0xFFFFFFFFu) zs = true;
+          xs[j] = ge(u[j], t.x) + ge(u[j], t.y) + ge(u[j], t.z);
+        }
+      }
+      const uint32_t x4 = xs[0] | (xs[1] << 8) | (xs[2] << 16) | (xs[3] << 24);
+      w = (w & x.CLR[i]) | (x4 << x.SH[i]);
+    }
+    w &= x.valid4;
+    x.row[s] = w;
+    if (x.counts && c < x.num_real) {
+      if (x.nl == 4) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x.hist8[(byte_of(w, j) << 8) + x.slot] += 1;
+      } else {
+        for (int j = 0; j < x.nl; ++j) x.hist8[(byte_of(w, j) << 8) + x.slot] += 1;
+      }
+    }
+  }
+  return zs;
+}
+
+// The sweep.  Grid (x: slots, y: replica quad q).  A thread owns lane word
+// (q, s); per latent variable one Philox4x32 call gives the quad's 4
+// uniforms, each lane does one table lookup and compare, and the 4 new
+// states are inserted with one byte-SIMD mask/or.
+template <int N>
 __global__ void __launch_bounds__(SG_THREADS)
 k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint8_t* __restrict__ pattern,
-              const int32_t* __restrict__ case_id, uint8_t* __restrict__ lanes, int lane_ld, int cases, int num_real,
+              const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes, int lane_ld, int cases, int num_real,
               int m, int64_t case_base, uint64_t key, const uint64_t* __restrict__ key_dev,
               const int32_t* __restrict__ jcell, int cells, unsigned long long* __restrict__ counts,
               const uint32_t* __restrict__ zs_flag, int32_t* err) {
-  if (key_dev) key = __ldg(key_dev);
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* stab = reinterpret_cast<uint32_t*>(smem);
   uint8_t* hist8 = smem + ((sp.tab_words * 4 + 15) & ~15);
@@ -160,77 +267,40 @@ k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint
     for (int i = tid; i < cells; i += SG_THREADS) cellacc[i] = 0;
   }
   const bool armed = zs_flag && __ldg(zs_flag) != 0u;
-  __syncthreads();
-  const int slot = ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
-  const int Q = (m + 3) >> 2;
-  bool zs = false;
-  for (int s = blockIdx.x * SG_THREADS + tid; s < cases; s += gridDim.x * SG_THREADS) {
-    const uint32_t P = pattern[s];
-    const int c = case_id[s];
-    const bool real = counts && c < num_real;
-    uint32_t Po = 0;  // latent bits permuted into colour order
-    for (int i = 0; i < sp.n; ++i) Po |= ((P >> sp.order[i]) & 1u) << i;
-    for (int q = 0; q < Q; ++q) {
-      const int nl = min(4, m - q * 4);
-      uint8_t* lp = lanes + int64_t(q * 4) * lane_ld + s;
-      uint32_t S0 = lp[0];
-      uint32_t S1 = nl > 1 ? lp[lane_ld] : 0u;
-      uint32_t S2 = nl > 2 ? lp[2 * lane_ld] : 0u;
-      uint32_t S3 = nl > 3 ? lp[3 * lane_ld] : 0u;
-      for (uint32_t L = Po; L; L &= L - 1u) {  // latent variables, colour order
-        const int v = sp.order[__ffs(L) - 1];
-        const u32x4 w = fast_block(key, uint64_t(case_base + c), uint32_t(v), uint32_t(q), 0u);
-        const uint32_t msk = sp.mbmask[v];
-        const uint32_t* tv = stab + sp.toff[v];
-        const int sh = sp.off[v];
-        const uint32_t clear = ~(((1u << sp.width[v]) - 1u) << sh);
-        const int k1 = sp.card[v] - 1;
-        if (k1 == 1) {
-          const uint32_t t0 = tv[S0 & msk], t1 = tv[S1 & msk], t2 = tv[S2 & msk], t3 = tv[S3 & msk];
-          S0 = (S0 & clear) | (uint32_t((w.a >> 1) >= t0) << sh);
-          S1 = (S1 & clear) | (uint32_t((w.b >> 1) >= t1) << sh);
-          S2 = (S2 & clear) | (uint32_t((w.c >> 1) >= t2) << sh);
-          S3 = (S3 & clear) | (uint32_t((w.d >> 1) >= t3) << sh);
-          if (armed)
-            zs |= t0 == 0xFFFFFFFFu || (nl > 1 && t1 == 0xFFFFFFFFu) || (nl > 2 && t2 == 0xFFFFFFFFu) ||
-                  (nl > 3 && t3 == 0xFFFFFFFFu);
-        } else {
-          uint32_t Sx[4] = {S0, S1, S2, S3};
-          const uint32_t ws[4] = {w.a >> 1, w.b >> 1, w.c >> 1, w.d >> 1};
+  SmallCtx<N> x;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t* th = tv + (Sx[j] & msk) * k1;
-            if (armed && j < nl && th[0] == 0xFFFFFFFFu) zs = true;
-            uint32_t x = (ws[j] >= th[0]) + (ws[j] >= th[1]);
-            for (int t = 2; t < k1; ++t) x += ws[j] >= th[t];
-            Sx[j] = (Sx[j] & clear) | (x << sh);
-          }
-          S0 = Sx[0];
-          S1 = Sx[1];
-          S2 = Sx[2];
-          S3 = Sx[3];
-        }
-      }
-      lp[0] = uint8_t(S0);
-      if (nl > 1) lp[lane_ld] = uint8_t(S1);
-      if (nl > 2) lp[2 * lane_ld] = uint8_t(S2);
-      if (nl > 3) lp[3 * lane_ld] = uint8_t(S3);
-      if (real) {
-        hist8[(S0 << 8) + slot] += 1;
-        if (nl > 1) hist8[(S1 << 8) + slot] += 1;
-        if (nl > 2) hist8[(S2 << 8) + slot] += 1;
-        if (nl > 3) hist8[(S3 << 8) + slot] += 1;
-      }
-    }
+  for (int i = 0; i < N; ++i) {
+    const int v = sp.order[i];
+    x.VAR[i] = v;
+    x.SH[i] = sp.off[v];
+    x.K1[i] = sp.card[v] - 1;
+    x.MSK[i] = sp.mbmask[v] * 0x01010101u;
+    x.CLR[i] = ~((((1u << sp.width[v]) - 1u) << sp.off[v]) * 0x01010101u);
+    x.TV[i] = stab + sp.toff[v];
   }
+  x.q = blockIdx.y;
+  x.nl = min(4, m - 4 * x.q);  // real replicas in this quad
+  x.valid4 = x.nl >= 4 ? 0xFFFFFFFFu : ((1u << (8 * x.nl)) - 1u);
+  x.row = lanes + int64_t(x.q) * lane_ld;
+  x.pattern = pattern;
+  x.case_id = case_id;
+  x.hist8 = hist8;
+  x.cases = cases;
+  x.num_real = num_real;
+  x.slot = ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
+  x.case_base = case_base;
+  x.key = key_dev ? __ldg(key_dev) : key;
+  x.counts = counts != nullptr;
+  __syncthreads();
+  const bool zs = armed ? small_units<N, true>(x) : small_units<N, false>(x);
   if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
   if (!counts) return;
   __syncthreads();
   const int warp = tid >> 5, lane_id = tid & 31;
   for (int J = warp; J < (1 << sp.bits); J += SG_THREADS / 32) {
-    const uint32_t* row = reinterpret_cast<const uint32_t*>(hist8 + (J << 8));
-    int sum = __dp4a(int(row[lane_id]), 0x01010101, 0);
-    sum = __dp4a(int(row[lane_id + 32]), 0x01010101, sum);
+    const uint32_t* hrow = reinterpret_cast<const uint32_t*>(hist8 + (J << 8));
+    int sum = __dp4a(int(hrow[lane_id]), 0x01010101, 0);
+    sum = __dp4a(int(hrow[lane_id + 32]), 0x01010101, sum);
 #pragma unroll
     for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (sum && lane_id < sp.n) atomicAdd(cellacc + __ldg(jcell + J * sp.n + lane_id), uint32_t(sum));
@@ -238,6 +308,21 @@ k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint
   __syncthreads();
   for (int cell = tid; cell < cells; cell += SG_THREADS)
     if (cellacc[cell]) atomicAdd(counts + cell, (unsigned long long)cellacc[cell]);
+}
+
+template <int N>
+static void launch_small(const sg_small& sp, dim3 grid, size_t smem, cudaStream_t st, const uint32_t* stab,
+                         const uint8_t* pattern, const int32_t* case_id, uint32_t* lanes, int lane_ld, int cases,
+                         int num_real, int m, int64_t case_base, uint64_t key, const uint64_t* key_dev,
+                         const int32_t* jcell, int cells, uint64_t* counts, const uint32_t* zs_flag, int32_t* err) {
+  static size_t configured = 0;  // raise the opt-in once (keeps graph capture free of attribute calls)
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_small_sweep<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  k_small_sweep<N><<<grid, SG_THREADS, smem, st>>>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m,
+                                                   case_base, key, key_dev, jcell, cells,
+                                                   reinterpret_cast<unsigned long long*>(counts), zs_flag, err);
 }
 
 static size_t small_smem(const sg_small& sp, int cells) {
@@ -256,13 +341,15 @@ extern "C" int sg_small_tables(const sg_net* net, const sg_small* sp, const uint
   return check_launch("sg_small_tables");
 }
 
+static bool lane_ld_ok(int lane_ld, int cases) { return lane_ld >= cases && lane_ld % 4 == 0; }
+
 extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t ld_obs, int32_t cases, int32_t m,
                                 int64_t case_base, uint64_t init_key, int32_t init, int32_t* scratch,
                                 uint8_t* pattern, int32_t* case_id, uint8_t* lanes, int32_t lane_ld, void* stream) {
   using namespace sg;
   SG_REQUIRE(sp && obs && scratch && pattern && case_id && lanes, "sg_small_prepare: null argument");
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV, "sg_small_prepare: bad plan");
-  SG_REQUIRE(lane_ld >= cases && m >= 1, "sg_small_prepare: bad lane layout");
+  SG_REQUIRE(m >= 1 && lane_ld_ok(lane_ld, cases), "sg_small_prepare: lane_ld %d < cases %d", lane_ld, cases);
   if (cases == 0) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   int* hist = scratch;                                                  // [SMALL_PATTERNS]
@@ -285,23 +372,39 @@ extern "C" int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const ui
   SG_REQUIRE(sp && stab && pattern && case_id && lanes && err, "sg_small_sweep: null argument");
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV && sp->bits <= SG_SMALL_MAXBITS, "sg_small_sweep: bad plan");
   SG_REQUIRE(!counts || jcell, "sg_small_sweep: joint cell map required for the tally");
-  SG_REQUIRE(m <= 252, "sg_small_sweep: m=%d exceeds 252", m);
+  SG_REQUIRE(m >= 1 && lane_ld_ok(lane_ld, cases), "sg_small_sweep: lane_ld %d < cases %d", lane_ld, cases);
+  for (int v = 0; v < sp->n; ++v)
+    SG_REQUIRE(sp->card[v] <= 4 && sp->tstride[v] >= sp->card[v] - 1 && sp->toff[v] % sp->tstride[v] == 0,
+               "sg_small_sweep: variable %d needs card <= 4 and an aligned table", v);
   if (cases == 0) return SG_OK;
   const size_t smem = small_smem(*sp, cells);
-  // byte counters: at most 252 lanes per thread between flushes
-  const int64_t per_thread = std::max<int64_t>(1, 252 / m);
-  const int64_t need = (int64_t(cases) + int64_t(SG_THREADS) * per_thread - 1) / (int64_t(SG_THREADS) * per_thread);
+  // byte counters: at most 63 units (252 lanes) per thread before the per-CTA flush
+  const int Q = (m + 3) / 4;
+  const int64_t need = (int64_t(cases) + int64_t(SG_THREADS) * 63 - 1) / (int64_t(SG_THREADS) * 63);
   const int64_t fill = (int64_t(cases) + SG_THREADS - 1) / SG_THREADS;
-  int blocks = int(std::min<int64_t>(std::max<int64_t>(need, 148 * 4), fill));
-  if (blocks < 1) blocks = 1;
-  static size_t configured = 0;  // raise the opt-in once (keeps graph capture free of attribute calls)
-  if (smem > configured) {
-    cudaFuncSetAttribute(k_small_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
+  const int64_t want = std::max<int64_t>((148 * 8 + Q - 1) / Q, need);  // ~8 CTAs per SM in total
+  const int gx = int(std::max<int64_t>(1, std::min<int64_t>(want, fill)));
+  const dim3 grid(gx, Q);
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* lw = reinterpret_cast<uint32_t*>(lanes);
+#define SG_SMALL_CASE(NV)                                                                                     \
+  case NV:                                                                                                    \
+    launch_small<NV>(*sp, grid, smem, st, stab, pattern, case_id, lw, lane_ld, cases, num_real, m, case_base, \
+                     key, key_dev, jcell, cells, counts, zs_flag, err);                                       \
+    break;
+  switch (sp->n) {
+    SG_SMALL_CASE(1)
+    SG_SMALL_CASE(2)
+    SG_SMALL_CASE(3)
+    SG_SMALL_CASE(4)
+    SG_SMALL_CASE(5)
+    SG_SMALL_CASE(6)
+    SG_SMALL_CASE(7)
+    default:
+      set_error("sg_small_sweep: n=%d", sp->n);
+      return SG_EINVAL;
   }
-  k_small_sweep<<<blocks, SG_THREADS, smem, (cudaStream_t)stream>>>(
-      *sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m, case_base, key, key_dev, jcell, cells,
-      reinterpret_cast<unsigned long long*>(counts), zs_flag, err);
+#undef SG_SMALL_CASE
   return check_launch("sg_small_sweep");
 }
 
@@ -309,6 +412,7 @@ extern "C" int sg_small_import(const sg_small* sp, const sg_batch* batch, const 
                                int32_t lane_ld, void* stream) {
   using namespace sg;
   SG_REQUIRE(sp && batch && case_id && lanes, "sg_small_import: null argument");
+  SG_REQUIRE(lane_ld_ok(lane_ld, batch->cases), "sg_small_import: bad lane_ld");
   const int64_t total = int64_t(batch->m) * batch->cases;
   if (total == 0) return SG_OK;
   k_small_import<<<int(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, (cudaStream_t)stream>>>(
@@ -320,6 +424,7 @@ extern "C" int sg_small_export(const sg_small* sp, const sg_batch* batch, const 
                                const uint8_t* pattern, const uint8_t* lanes, int32_t lane_ld, void* stream) {
   using namespace sg;
   SG_REQUIRE(sp && batch && case_id && pattern && lanes, "sg_small_export: null argument");
+  SG_REQUIRE(lane_ld_ok(lane_ld, batch->cases), "sg_small_export: bad lane_ld");
   const int64_t total = int64_t(batch->m) * batch->cases;
   if (total == 0) return SG_OK;
   k_small_export<<<int(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, (cudaStream_t)stream>>>(

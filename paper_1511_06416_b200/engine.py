@@ -53,8 +53,8 @@ class SmallBatch:
 
     def __init__(self, n: int, m: int, cases: int, dev: torch.device):
         self.n, self.m, self.cases = n, m, cases
-        self.lane_ld = max(16, (cases + 15) // 16 * 16)
-        self.lanes = torch.empty((m, self.lane_ld), dtype=torch.uint8, device=dev)
+        self.lane_ld = max(4, (cases + 3) // 4 * 4)  # words per replica-quad row
+        self.lanes = torch.empty(((m + 3) // 4, self.lane_ld), dtype=torch.int32, device=dev)
         self.pattern = torch.empty(max(1, cases), dtype=torch.uint8, device=dev)
         self.case_id = torch.empty(max(1, cases), dtype=torch.int32, device=dev)
         self.scratch = torch.empty(128 + (cases + 3) // 4 + 1, dtype=torch.int32, device=dev)
@@ -110,7 +110,8 @@ class Engine:
         self.batch_bytes = 0
         self.sweep_events = None  # list -> (start, end, sweeps) CUDA events around each visit's sweeps
         # packed-lane path: FAST RNG and a lane state that fits one byte (sg_small.cu)
-        can_small = self.rng_mode == _lib.SG_RNG_FAST and self.pack.small is not None
+        max_m = cfg.same_m if isinstance(cfg.same_m, int) else max(mm for mm, _ in cfg.same_m)
+        can_small = self.rng_mode == _lib.SG_RNG_FAST and self.pack.small is not None and max_m <= 32
         self.use_small = can_small if small is None else (bool(small) and can_small)
         if self.use_small:
             self.stab = torch.empty(max(1, self.pack.small.tab_words), dtype=torch.int32, device=d)

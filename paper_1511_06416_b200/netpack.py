@@ -218,6 +218,8 @@ def small_plan(net: Network, lay: NetLayout):
     if n == 0 or n > SMALL_MAXV:
         return None
     cards = [int(k) for k in net.cardinalities]
+    if max(cards) > 4:  # one aligned LDS / LDS.64 / LDS.128 of thresholds per draw
+        return None
     width = [max(1, (k - 1).bit_length()) for k in cards]
     bits = sum(width)
     if bits > SMALL_MAXBITS:
@@ -230,10 +232,16 @@ def small_plan(net: Network, lay: NetLayout):
     sp = SgSmall()
     sp.n, sp.bits = n, bits
     order = [v for grp in lay.groups for v in grp]
-    toff, words = [], 0
+    # entries padded to 1, 2 or 4 words (card-1 thresholds) so a lookup is one
+    # aligned LDS / LDS.64 / LDS.128; tables aligned to their entry size
+    toff, tstride, words = [], [], 0
     for v in range(n):
+        k1 = cards[v] - 1
+        stride = 1 if k1 == 1 else 2 if k1 == 2 else 4 if k1 <= 4 else k1
+        words = (words + stride - 1) // stride * stride if stride in (2, 4) else words
         toff.append(words)
-        words += (1 << bits) * (cards[v] - 1)
+        tstride.append(stride)
+        words += (1 << bits) * stride
     sp.tab_words = words
     for v in range(n):
         sp.order[v] = order[v]
@@ -241,6 +249,7 @@ def small_plan(net: Network, lay: NetLayout):
         sp.width[v] = width[v]
         sp.card[v] = cards[v]
         sp.toff[v] = toff[v]
+        sp.tstride[v] = tstride[v]
         mask = 0
         for u in mb_var[mb_start[v]:mb_start[v + 1]]:
             mask |= ((1 << width[u]) - 1) << off[u]
