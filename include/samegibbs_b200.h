@@ -106,6 +106,14 @@ typedef struct sg_net {
      card, nmb (-1 = evaluate from CPTs), ftab offset, ptab offset,
      mb_var[SG_DESC_MB], mb_stride[SG_DESC_MB] */
   const int32_t* var_desc;    /* [n][SG_DESC_WORDS] */
+  /* Every int32 array above lives inside blob32 and every int64 array inside
+     blob64 (the pack is two contiguous buffers), so a kernel can stage the
+     whole structure in shared memory and rebase the pointers (NULL: not
+     packed that way). */
+  const int32_t* blob32;
+  int64_t blob32_words;
+  const int64_t* blob64;
+  int64_t blob64_words;
 } sg_net;
 
 #define SG_JOINT_MAX 128
@@ -283,13 +291,28 @@ int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t ld_obs,
 
 /* Sweep + tally on packed lanes.  jcell [dev] [2^bits][n]: CPT cell of each
    variable for each lane word; zs_flag = ftab + ftab_size (arms the
-   ZeroSupport check).  counts may be NULL. */
+   ZeroSupport check).  counts may be NULL.  obs (int8 [n][ld_obs], or NULL)
+   is the minibatch's observation block: its range check (sg_check_range)
+   runs inside the same launch. */
 int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern,
                    const int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
                    int32_t cases, int32_t num_real, int32_t m, int64_t case_base,
                    uint64_t key, const uint64_t* key_dev, const int32_t* jcell, int32_t cells,
-                   uint64_t* counts, const uint32_t* zs_flag, int32_t* err,
+                   uint64_t* counts, const uint32_t* zs_flag,
+                   const int8_t* obs, int32_t ld_obs, int32_t* err,
                    void* stream);
+
+/* sg_small_sweep + sg_step_finish in ONE launch: the last CTA to finish its
+   tally (device counter `done`, zero on entry and re-armed on exit) runs the
+   step tail for the whole grid.  The model must fit the single-CTA tail
+   (<= 4096 cells). */
+int sg_small_step(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern,
+                  const int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
+                  int32_t cases, int32_t num_real, int32_t m, int64_t case_base,
+                  uint64_t key, const uint64_t* key_dev, const int32_t* jcell, int32_t cells,
+                  uint64_t* counts, const uint32_t* zs_flag,
+                  const int8_t* obs, int32_t ld_obs, int32_t* err,
+                  const sg_net* net, const struct sg_finish* f, uint32_t* done, void* stream);
 
 /* Layout switches between packed lanes and sg_batch int8 lane states. */
 int sg_small_import(const sg_small* sp, const sg_batch* batch, const int32_t* case_id,

@@ -41,7 +41,8 @@ class SgNet(ctypes.Structure):
         ("cells", c_int64), ("rows", c_int64), ("ptab_size", c_int64), ("ftab_size", c_int64),
         ("table_entries", c_int64),
     ] + [(name, c_void_p) for name in NET_POINTERS] + [("joint_size", c_int64)] + \
-        [(name, c_void_p) for name in NET_POINTERS_TAIL]
+        [(name, c_void_p) for name in NET_POINTERS_TAIL] + \
+        [("blob32", c_void_p), ("blob32_words", c_int64), ("blob64", c_void_p), ("blob64_words", c_int64)]
 
 
 class SgBatch(ctypes.Structure):
@@ -97,9 +98,12 @@ _SIGNATURES = {
                           c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p], c_int32),
     "sg_small_sweep": ([POINTER(SgSmall), c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32,
                         c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
-                        c_void_p], c_int32),
+                        c_int32, c_void_p, c_void_p], c_int32),
     "sg_keys_advance": ([c_void_p, c_void_p, c_int32, c_void_p, c_void_p], c_int32),
     "sg_step_finish": ([POINTER(SgNet), c_void_p, POINTER(SgFinish), c_void_p], c_int32),
+    "sg_small_step": ([POINTER(SgSmall), c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32,
+                       c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
+                       c_int32, c_void_p, POINTER(SgNet), POINTER(SgFinish), c_void_p, c_void_p], c_int32),
     "sg_small_import": ([POINTER(SgSmall), POINTER(SgBatch), c_void_p, c_void_p, c_int32, c_void_p], c_int32),
     "sg_small_export": ([POINTER(SgSmall), POINTER(SgBatch), c_void_p, c_void_p, c_void_p, c_int32, c_void_p],
                         c_int32),
@@ -143,7 +147,7 @@ KERNELS_PER_CALL = {
     "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
     "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
-    "sg_keys_advance": 1, "sg_step_finish": 1,
+    "sg_keys_advance": 1, "sg_step_finish": 1, "sg_small_step": 1,
 }
 launch_count = 0
 

@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "../../include/samegibbs_b200.h"
@@ -124,34 +125,54 @@ __device__ __forceinline__ double np_pairwise_sum(const double* a, int n) {
 
 // CPT reads: through the read-only path when the CPTs are kernel inputs,
 // plain loads when the same kernel just wrote them (sg_step_finish).
-template <bool RO>
-__device__ __forceinline__ double cpt_load(const double* p) {
+template <bool RO, typename T>
+__device__ __forceinline__ T ro_load(const T* p) {
   if (RO) return __ldg(p);
   return *p;
+}
+template <bool RO>
+__device__ __forceinline__ double cpt_load(const double* p) {
+  return ro_load<RO>(p);
 }
 
 // Reference full-conditional weights of v given its Markov-blanket states
 // s[slot] (sampler.py:226-240): w = T_v[cfg, :], then for each child c in
 // ascending order w[t] *= T_c[cfg0_c + t*stride_vc, x_c].
-template <bool RO = true>
+// K > 0: the caller knows card == K at compile time, so w[] stays in
+// registers (K = 0: runtime card, w[] in local memory).
+template <bool RO = true, int K = 0>
 __device__ __forceinline__ void conditional_weights(const sg_net& net, int v, const int* s,
                                                     const double* cpt, double* w) {
-  const int card = __ldg(net.card + v);
+  const int card = K ? K : ro_load<RO>(net.card + v);
   int64_t cfg = 0;
-  for (int j = __ldg(net.par_start + v), e = __ldg(net.par_start + v + 1); j < e; ++j)
-    cfg += int64_t(s[__ldg(net.par_slot + j)]) * __ldg(net.par_stride + j);
-  const double* row = cpt + __ldg(net.cpt_off + v) + cfg * card;
-  for (int t = 0; t < card; ++t) w[t] = cpt_load<RO>(row + t);
-  for (int k = __ldg(net.chl_start + v), ke = __ldg(net.chl_start + v + 1); k < ke; ++k) {
-    const int c = __ldg(net.chl_var + k);
-    const int cc = __ldg(net.card + c);
-    const int xc = s[__ldg(net.chl_slot + k)];
+  for (int j = ro_load<RO>(net.par_start + v), e = ro_load<RO>(net.par_start + v + 1); j < e; ++j)
+    cfg += int64_t(s[ro_load<RO>(net.par_slot + j)]) * ro_load<RO>(net.par_stride + j);
+  const double* row = cpt + ro_load<RO>(net.cpt_off + v) + cfg * card;
+#pragma unroll
+  for (int t = 0; t < (K ? K : card); ++t) w[t] = cpt_load<RO>(row + t);
+  for (int k = ro_load<RO>(net.chl_start + v), ke = ro_load<RO>(net.chl_start + v + 1); k < ke; ++k) {
+    const int c = ro_load<RO>(net.chl_var + k);
+    const int cc = ro_load<RO>(net.card + c);
+    const int xc = s[ro_load<RO>(net.chl_slot + k)];
     int64_t cfg0 = 0;
-    for (int q = __ldg(net.chl_pstart + k), qe = __ldg(net.chl_pstart + k + 1); q < qe; ++q)
-      cfg0 += int64_t(s[__ldg(net.chl_pslot + q)]) * __ldg(net.chl_pstride + q);
-    const int64_t vs = __ldg(net.chl_vstride + k);
-    const double* tc = cpt + __ldg(net.cpt_off + c) + xc;
-    for (int t = 0; t < card; ++t) w[t] = __dmul_rn(w[t], cpt_load<RO>(tc + (cfg0 + t * vs) * cc));
+    for (int q = ro_load<RO>(net.chl_pstart + k), qe = ro_load<RO>(net.chl_pstart + k + 1); q < qe; ++q)
+      cfg0 += int64_t(s[ro_load<RO>(net.chl_pslot + q)]) * ro_load<RO>(net.chl_pstride + q);
+    const int64_t vs = ro_load<RO>(net.chl_vstride + k);
+    const double* tc = cpt + ro_load<RO>(net.cpt_off + c) + xc;
+#pragma unroll
+    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(w[t], cpt_load<RO>(tc + (cfg0 + t * vs) * cc));
+  }
+}
+
+// Call f(std::integral_constant<int, K>) with K = card for the common small
+// cardinalities (register-resident weight arrays), K = 0 otherwise.
+template <class F>
+__device__ __forceinline__ void with_card(int card, F&& f) {
+  switch (card) {
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    default: f(std::integral_constant<int, 0>{}); break;
   }
 }
 
@@ -208,31 +229,47 @@ __device__ __forceinline__ double log_gamma_draw(CellStream& rs, double a) {
 }
 
 // Normalise one row of log-gamma draws into Dirichlet probabilities.
+template <int K = 0>
 __device__ __forceinline__ void dirichlet_normalise(const double* lg, int card, double* out) {
+  if (K) card = K;
   double mx = -INFINITY;
-  for (int s = 0; s < card; ++s) mx = fmax(mx, lg[s]);
-  double e[SG_MAX_CARD];
+#pragma unroll
+  for (int s = 0; s < (K ? K : card); ++s) mx = fmax(mx, lg[s]);
+  double e[K ? K : SG_MAX_CARD];
   double sum = 0.0;
-  for (int s = 0; s < card; ++s) {
+#pragma unroll
+  for (int s = 0; s < (K ? K : card); ++s) {
     e[s] = exp(lg[s] - mx);
     sum += e[s];
   }
-  for (int s = 0; s < card; ++s) out[s] = e[s] / sum;
+#pragma unroll
+  for (int s = 0; s < (K ? K : card); ++s) out[s] = e[s] / sum;
 }
 
 // One conditional-table entry from the weights w[0..card) of a blanket
 // configuration: pe = cum[0..card-2], norm; fe = ceil(cum/norm * 2^31)
 // thresholds (0xFFFFFFFF in slot 0 and *zs_flag set when norm <= 0).
+template <int K = 0>
 __device__ __forceinline__ void table_entry(const double* w, int card, double* pe, uint32_t* fe,
                                             uint32_t* zs_flag) {
-  const double norm = np_pairwise_sum(w, card);
+  if (K) card = K;
+  double norm;
+  if (K && K < 8) {  // numpy's pairwise sum is sequential below 8 terms
+    norm = 0.0;
+#pragma unroll
+    for (int t = 0; t < (K ? K : 1); ++t) norm = __dadd_rn(norm, w[t]);
+  } else {
+    norm = np_pairwise_sum(w, card);
+  }
   const bool ok = norm > 0.0;
+  // FAST thresholds only need to be deterministic and monotone: scale by one reciprocal
+  const double scale = ok ? __ddiv_rn(2147483648.0, norm) : 0.0;
   double cum = 0.0;
-  for (int t = 0; t < card - 1; ++t) {
+#pragma unroll
+  for (int t = 0; t < (K ? K - 1 : card - 1); ++t) {
     cum = t ? __dadd_rn(cum, w[t]) : w[0];
     pe[t] = cum;
-    double q = ok ? ceil(__ddiv_rn(cum, norm) * 2147483648.0) : 0.0;
-    q = fmin(q, 2147483648.0);
+    const double q = fmin(ceil(__dmul_rn(cum, scale)), 2147483648.0);
     fe[t] = (t == 0 && !ok) ? 0xFFFFFFFFu : uint32_t(q);
   }
   pe[card - 1] = norm;
@@ -246,6 +283,7 @@ __device__ __forceinline__ int small_field(uint32_t S, const sg_small& sp, int v
 // Packed-lane table word(s) i = (v, S): the generic FAST thresholds of the
 // blanket configuration that lane word S encodes (0 for unused words).
 // Plain loads: ftab may have been written by the same kernel.
+template <bool RO = true>
 __device__ __forceinline__ void small_table_entry(const sg_net& net, const sg_small& sp, const uint32_t* ftab,
                                                   uint32_t* stab, int i) {
   const int v = i >> sp.bits;
@@ -254,24 +292,41 @@ __device__ __forceinline__ void small_table_entry(const sg_net& net, const sg_sm
   uint32_t* out = stab + sp.toff[v] + S * sp.tstride[v];
   bool valid = (S & ~sp.mbmask[v]) == 0u;
   int64_t e = 0;
-  for (int k = __ldg(net.mb_start + v), ke = __ldg(net.mb_start + v + 1); k < ke && valid; ++k) {
-    const int u = __ldg(net.mb_var + k);
+  for (int k = ro_load<RO>(net.mb_start + v), ke = ro_load<RO>(net.mb_start + v + 1); k < ke && valid; ++k) {
+    const int u = ro_load<RO>(net.mb_var + k);
     const int s = small_field(S, sp, u);
     valid = s < sp.card[u];
-    e += int64_t(s) * __ldg(net.mb_stride + k);
+    e += int64_t(s) * ro_load<RO>(net.mb_stride + k);
   }
-  const uint32_t* src = ftab + __ldg(net.ftab_off + v) + e * (card - 1);
+  const uint32_t* src = ftab + ro_load<RO>(net.ftab_off + v) + e * (card - 1);
   for (int t = 0; t < card - 1; ++t) out[t] = valid ? src[t] : 0u;
 }
 
 // Variable owning CPT cell `cell` (binary search over cpt_off).
+template <bool RO = true>
 __device__ __forceinline__ int cell_var(const sg_net& net, int64_t cell) {
   int lo = 0, hi = net.n;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (__ldg(net.cpt_off + mid) <= cell) lo = mid; else hi = mid;
+    if (ro_load<RO>(net.cpt_off + mid) <= cell) lo = mid; else hi = mid;
   }
   return lo;
+}
+
+// Copy of a two-blob network pack whose array pointers point into shared
+// memory copies s32 / s64 of the blobs (see sg_net.blob32).
+__device__ __forceinline__ sg_net rebase_net(const sg_net& g, const int32_t* s32, const int64_t* s64) {
+  sg_net n = g;
+#define SG_R32(f) n.f = g.f ? s32 + (g.f - g.blob32) : nullptr
+#define SG_R64(f) n.f = g.f ? s64 + (g.f - g.blob64) : nullptr
+  SG_R32(card); SG_R32(group_start); SG_R32(order); SG_R32(par_start); SG_R32(par_var); SG_R32(par_stride);
+  SG_R32(par_slot); SG_R32(mb_start); SG_R32(mb_var); SG_R32(mb_stride); SG_R32(chl_start); SG_R32(chl_var);
+  SG_R32(chl_vstride); SG_R32(chl_slot); SG_R32(chl_pstart); SG_R32(chl_pslot); SG_R32(chl_pstride);
+  SG_R32(row_var); SG_R32(joint_radix); SG_R32(joint_cell); SG_R32(var_desc);
+  SG_R64(cpt_off); SG_R64(row_off); SG_R64(tab_entries); SG_R64(tab_start); SG_R64(ptab_off); SG_R64(ftab_off);
+#undef SG_R32
+#undef SG_R64
+  return n;
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

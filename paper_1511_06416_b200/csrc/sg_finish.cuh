@@ -1,0 +1,187 @@
+// The model-sized tail of a minibatch step (accumulate -> CPT update ->
+// conditional tables -> packed tables -> clear next counts -> advance keys),
+// as a device function that one CTA runs.  Shared by k_step_finish
+// (sg_model.cu) and the fused packed sweep (sg_small.cu).
+#pragma once
+
+#include "sg_device.cuh"
+
+namespace sg {
+
+__device__ __forceinline__ double acc_cell(int mode, double t, double add, bool has_prev, double prev, double decay) {
+  if (mode == SG_ACC_MOVING) {
+    if (has_prev) t = __dadd_rn(t, __dmul_rn(-1.0, prev));
+    return __dadd_rn(t, add);
+  }
+  t = __dmul_rn(t, decay);
+  return __dadd_rn(t, add);
+}
+
+template <int K = 0>
+__device__ __forceinline__ void mean_row(const double* total, double a, int card, double* out) {
+  if (K) card = K;
+  double sh[K ? K : SG_MAX_CARD];
+#pragma unroll
+  for (int s = 0; s < (K ? K : card); ++s) sh[s] = __dadd_rn(total[s], a);
+  double sum;
+  if (K && K < 8) {  // numpy's pairwise sum is sequential below 8 terms
+    sum = 0.0;
+#pragma unroll
+    for (int s = 0; s < (K ? K : 1); ++s) sum = __dadd_rn(sum, sh[s]);
+  } else {
+    sum = np_pairwise_sum(sh, card);
+  }
+#pragma unroll
+  for (int s = 0; s < (K ? K : card); ++s) out[s] = __ddiv_rn(sh[s], sum);
+}
+
+struct FinishArgs {
+  int acc_mode, map_estimate;
+  double decay;
+  double* total;
+  const unsigned long long* new_counts;
+  const unsigned long long* prev_counts;
+  const double* alpha;
+  uint64_t key;
+  const uint64_t* key_dev;
+  double* cpt;
+  double* ptab;
+  uint32_t* ftab;
+  uint32_t* stab;
+  unsigned long long* clear_counts;
+  const uint64_t* key_table;
+  int32_t* key_index;
+  int kps;
+  uint64_t* key_current;
+  int has_small;
+  sg_small sp;
+};
+
+static constexpr int FINISH_THREADS = 512;
+static constexpr int FINISH_MAX_CELLS = 4096;
+static constexpr size_t FINISH_MAX_SMEM = 160 * 1024;
+
+__host__ __device__ inline size_t finish_smem(const sg_net& net) {
+  return size_t(net.cells) * 16 + size_t(net.blob64_words) * 8 + ((size_t(net.blob32_words) * 4 + 15) & ~size_t(15));
+}
+
+// The step tail, run by ONE CTA of `nt` threads (tid = threadIdx.x).  The
+// network pack (two blobs) and the CPTs are staged in shared memory `smem`
+// (finish_smem bytes) so the dependent index chains of the table build hit
+// on-chip memory instead of L2.  Used by k_step_finish and by the last CTA
+// of the fused packed sweep (sg_small_step).
+__device__ __forceinline__ void step_finish_body(const sg_net& gnet, const FinishArgs& f, unsigned char* smem,
+                                                 const int nt) {
+  double* lg = reinterpret_cast<double*>(smem);
+  double* cpt_s = lg + gnet.cells;
+  int64_t* b64 = reinterpret_cast<int64_t*>(cpt_s + gnet.cells);
+  int32_t* b32 = reinterpret_cast<int32_t*>(b64 + gnet.blob64_words);
+  const int tid = threadIdx.x;
+  const int cells = int(gnet.cells);
+  for (int i = tid; i < int(gnet.blob64_words); i += nt) b64[i] = __ldg(gnet.blob64 + i);
+  for (int i = tid; i < int(gnet.blob32_words); i += nt) b32[i] = __ldg(gnet.blob32 + i);
+  const uint64_t key = f.key_dev ? __ldg(f.key_dev) : f.key;
+  if (tid == 0 && gnet.table_entries > 0) f.ftab[gnet.ftab_size] = 0u;
+  __syncthreads();
+  const sg_net net = rebase_net(gnet, b32, b64);
+  // 1. accumulator (+ the cell's gamma draw)
+  for (int i = tid; i < cells; i += nt) {
+    const double t = acc_cell(f.acc_mode, f.total[i], double(f.new_counts[i]), f.prev_counts != nullptr,
+                              f.prev_counts ? double(f.prev_counts[i]) : 0.0, f.decay);
+    f.total[i] = t;
+    if (f.map_estimate) {
+      lg[i] = t;
+    } else {
+      const int v = cell_var<false>(net, i);
+      CellStream rs(key, uint64_t(i));
+      lg[i] = log_gamma_draw(rs, t + f.alpha[v]);
+    }
+  }
+  __syncthreads();
+  // 2. CPT update, one row per thread
+  for (int row = tid; row < int(net.rows); row += nt) {
+    const int v = net.row_var[row];
+    const int card = net.card[v];
+    const int64_t base = net.cpt_off[v] + (row - net.row_off[v]) * card;
+    with_card(card, [&](auto C) {
+      constexpr int K = decltype(C)::value;
+      if (f.map_estimate) mean_row<K>(lg + base, f.alpha[v], card, cpt_s + base);
+      else dirichlet_normalise<K>(lg + base, card, cpt_s + base);
+    });
+    for (int s2 = 0; s2 < card; ++s2) f.cpt[base + s2] = cpt_s[base + s2];
+  }
+  __syncthreads();
+  // 3. conditional tables from the new CPTs
+  for (int g = tid; g < int(net.table_entries); g += nt) {
+    int lo = 0, hi = net.n;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (net.tab_start[mid] <= g) lo = mid; else hi = mid;
+    }
+    const int v = lo;
+    const int64_t e = g - net.tab_start[v];
+    const int card = net.card[v];
+    int s[SG_MAX_MB];
+    const int m0 = net.mb_start[v], m1 = net.mb_start[v + 1];
+    for (int k = m0; k < m1; ++k) s[k - m0] = int((e / net.mb_stride[k]) % net.card[net.mb_var[k]]);
+    double* pe = f.ptab + net.ptab_off[v] + e * card;
+    uint32_t* fe = f.ftab + net.ftab_off[v] + e * (card - 1);
+    with_card(card, [&](auto C) {
+      constexpr int K = decltype(C)::value;
+      double w[K ? K : SG_MAX_CARD];
+      conditional_weights<false, K>(net, v, s, cpt_s, w);
+      table_entry<K>(w, card, pe, fe, f.ftab + net.ftab_size);
+    });
+  }
+  __syncthreads();
+  // 4. packed-lane tables
+  if (f.has_small) {
+    const sg_small& sp = f.sp;
+    for (int i = tid; i < (sp.n << sp.bits); i += nt) small_table_entry<false>(net, sp, f.ftab, f.stab, i);
+  }
+  // 5. clear the next visit's count buffer, advance the key cursor
+  if (f.clear_counts)
+    for (int i = tid; i < cells; i += nt) f.clear_counts[i] = 0ull;
+  if (f.key_table) {
+    __syncthreads();  // every thread has read this step's keys
+    const int idx = *f.key_index;
+    for (int k = tid; k < f.kps; k += nt) f.key_current[k] = f.key_table[int64_t(idx) * f.kps + k];
+    __syncthreads();
+    if (tid == 0) *f.key_index = idx + 1;
+  }
+}
+
+
+// Kernel-side copy of an sg_finish (+ optional packed plan).
+inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
+  FinishArgs a;
+  a.acc_mode = f->acc_mode;
+  a.map_estimate = f->map_estimate;
+  a.decay = f->decay;
+  a.total = f->total;
+  a.new_counts = reinterpret_cast<const unsigned long long*>(f->new_counts);
+  a.prev_counts = reinterpret_cast<const unsigned long long*>(f->prev_counts);
+  a.alpha = f->alpha;
+  a.key = f->key;
+  a.key_dev = f->key_dev;
+  a.cpt = f->cpt;
+  a.ptab = f->ptab;
+  a.ftab = f->ftab;
+  a.stab = f->stab;
+  a.clear_counts = reinterpret_cast<unsigned long long*>(f->clear_counts);
+  a.key_table = f->key_table;
+  a.key_index = f->key_index;
+  a.kps = f->kps;
+  a.key_current = f->key_current;
+  a.has_small = sp ? 1 : 0;
+  if (sp) a.sp = *sp;
+  return a;
+}
+
+// Whether the single-CTA tail can handle this model.
+inline bool finish_fits(const sg_net& net, const sg_small* sp) {
+  return net.blob32 && net.blob64 && net.cells <= FINISH_MAX_CELLS && finish_smem(net) <= FINISH_MAX_SMEM &&
+         net.table_entries <= 65536 && (!sp || (sp->n << sp->bits) <= 65536);
+}
+
+}  // namespace sg

@@ -13,18 +13,9 @@
 //    tables, next-count clearing, key advance) fused into ONE single-CTA
 //    kernel for model-sized networks -- a minibatch step is then check +
 //    sweep + finish.  Same arithmetic, same results as the separate calls.
-#include "sg_device.cuh"
+#include "sg_finish.cuh"
 
 namespace sg {
-
-__device__ __forceinline__ double acc_cell(int mode, double t, double add, bool has_prev, double prev, double decay) {
-  if (mode == SG_ACC_MOVING) {
-    if (has_prev) t = __dadd_rn(t, __dmul_rn(-1.0, prev));
-    return __dadd_rn(t, add);
-  }
-  t = __dmul_rn(t, decay);
-  return __dadd_rn(t, add);
-}
 
 __global__ void k_accumulate(int mode, double* __restrict__ total, const unsigned long long* __restrict__ nw,
                              const unsigned long long* __restrict__ prev, const double* __restrict__ nwf,
@@ -36,13 +27,6 @@ __global__ void k_accumulate(int mode, double* __restrict__ total, const unsigne
     const double pv = prev ? double(prev[i]) : (prevf ? prevf[i] : 0.0);
     total[i] = acc_cell(mode, total[i], add, hp, pv, decay);
   }
-}
-
-__device__ __forceinline__ void mean_row(const double* total, double a, int card, double* out) {
-  double sh[SG_MAX_CARD];
-  for (int s = 0; s < card; ++s) sh[s] = __dadd_rn(total[s], a);
-  const double sum = np_pairwise_sum(sh, card);
-  for (int s = 0; s < card; ++s) out[s] = __ddiv_rn(sh[s], sum);
 }
 
 __global__ void k_mean_cpts(const sg_net net, const double* __restrict__ total, const double* __restrict__ alpha,
@@ -78,94 +62,9 @@ __global__ void k_sample_cpts(const sg_net net, const double* __restrict__ total
   }
 }
 
-// ---------------------------------------------------------------- fused finish
-
-struct FinishArgs {
-  int acc_mode, map_estimate;
-  double decay;
-  double* total;
-  const unsigned long long* new_counts;
-  const unsigned long long* prev_counts;
-  const double* alpha;
-  uint64_t key;
-  const uint64_t* key_dev;
-  double* cpt;
-  double* ptab;
-  uint32_t* ftab;
-  uint32_t* stab;
-  unsigned long long* clear_counts;
-  const uint64_t* key_table;
-  int32_t* key_index;
-  int kps;
-  uint64_t* key_current;
-  int has_small;
-  sg_small sp;
-};
-
-static constexpr int FINISH_THREADS = 512;
-static constexpr int FINISH_MAX_CELLS = 4096;
-
-__global__ void __launch_bounds__(FINISH_THREADS) k_step_finish(const sg_net net, const FinishArgs f) {
-  __shared__ double lg[FINISH_MAX_CELLS];
-  const int tid = threadIdx.x;
-  const int cells = int(net.cells);
-  const uint64_t key = f.key_dev ? __ldg(f.key_dev) : f.key;
-  if (tid == 0 && net.table_entries > 0) f.ftab[net.ftab_size] = 0u;
-  // 1. accumulator
-  for (int i = tid; i < cells; i += FINISH_THREADS) {
-    const double t = acc_cell(f.acc_mode, f.total[i], double(f.new_counts[i]), f.prev_counts != nullptr,
-                              f.prev_counts ? double(f.prev_counts[i]) : 0.0, f.decay);
-    f.total[i] = t;
-    if (!f.map_estimate) {
-      const int v = cell_var(net, i);
-      CellStream rs(key, uint64_t(i));
-      lg[i] = log_gamma_draw(rs, t + f.alpha[v]);
-    }
-  }
-  __syncthreads();
-  // 2. CPT update, one row per thread
-  for (int row = tid; row < int(net.rows); row += FINISH_THREADS) {
-    const int v = __ldg(net.row_var + row);
-    const int card = __ldg(net.card + v);
-    const int64_t base = __ldg(net.cpt_off + v) + (row - __ldg(net.row_off + v)) * card;
-    if (f.map_estimate) mean_row(f.total + base, f.alpha[v], card, f.cpt + base);
-    else dirichlet_normalise(lg + base, card, f.cpt + base);
-  }
-  __syncthreads();
-  // 3. conditional tables from the new CPTs (plain loads: written above)
-  for (int g = tid; g < int(net.table_entries); g += FINISH_THREADS) {
-    int lo = 0, hi = net.n;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(net.tab_start + mid) <= g) lo = mid; else hi = mid;
-    }
-    const int v = lo;
-    const int64_t e = g - __ldg(net.tab_start + v);
-    const int card = __ldg(net.card + v);
-    int s[SG_MAX_MB];
-    const int m0 = __ldg(net.mb_start + v), m1 = __ldg(net.mb_start + v + 1);
-    for (int k = m0; k < m1; ++k) s[k - m0] = int((e / __ldg(net.mb_stride + k)) % __ldg(net.card + __ldg(net.mb_var + k)));
-    double w[SG_MAX_CARD];
-    conditional_weights<false>(net, v, s, f.cpt, w);
-    table_entry(w, card, f.ptab + __ldg(net.ptab_off + v) + e * card, f.ftab + __ldg(net.ftab_off + v) + e * (card - 1),
-                f.ftab + net.ftab_size);
-  }
-  __syncthreads();
-  // 4. packed-lane tables
-  if (f.has_small) {
-    const sg_small& sp = f.sp;
-    for (int i = tid; i < (sp.n << sp.bits); i += FINISH_THREADS) small_table_entry(net, sp, f.ftab, f.stab, i);
-  }
-  // 5. clear the next visit's count buffer, advance the key cursor
-  if (f.clear_counts)
-    for (int i = tid; i < cells; i += FINISH_THREADS) f.clear_counts[i] = 0ull;
-  if (f.key_table) {
-    __syncthreads();  // every thread has read this step's keys
-    const int idx = *f.key_index;
-    for (int k = tid; k < f.kps; k += FINISH_THREADS) f.key_current[k] = f.key_table[int64_t(idx) * f.kps + k];
-    __syncthreads();
-    if (tid == 0) *f.key_index = idx + 1;
-  }
+__global__ void __launch_bounds__(FINISH_THREADS) k_step_finish(const sg_net gnet, const FinishArgs f) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  step_finish_body(gnet, f, smem, FINISH_THREADS);
 }
 
 static int grid_for(int64_t work) {
@@ -226,29 +125,15 @@ extern "C" int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_fi
   if (sp) SG_REQUIRE(f->stab, "sg_step_finish: packed table required");
   if (f->key_table) SG_REQUIRE(f->key_index && f->key_current && f->kps > 0, "sg_step_finish: bad key cursor");
   cudaStream_t s = (cudaStream_t)stream;
-  if (net->cells <= FINISH_MAX_CELLS && net->table_entries <= 65536 && (!sp || (sp->n << sp->bits) <= 65536)) {
-    FinishArgs a;
-    a.acc_mode = f->acc_mode;
-    a.map_estimate = f->map_estimate;
-    a.decay = f->decay;
-    a.total = f->total;
-    a.new_counts = reinterpret_cast<const unsigned long long*>(f->new_counts);
-    a.prev_counts = reinterpret_cast<const unsigned long long*>(f->prev_counts);
-    a.alpha = f->alpha;
-    a.key = f->key;
-    a.key_dev = f->key_dev;
-    a.cpt = f->cpt;
-    a.ptab = f->ptab;
-    a.ftab = f->ftab;
-    a.stab = f->stab;
-    a.clear_counts = reinterpret_cast<unsigned long long*>(f->clear_counts);
-    a.key_table = f->key_table;
-    a.key_index = f->key_index;
-    a.kps = f->kps;
-    a.key_current = f->key_current;
-    a.has_small = sp ? 1 : 0;
-    if (sp) a.sp = *sp;
-    k_step_finish<<<1, FINISH_THREADS, 0, s>>>(*net, a);
+  if (finish_fits(*net, sp)) {
+    const FinishArgs a = make_finish_args(f, sp);
+    const size_t smem = finish_smem(*net);
+    static size_t configured = 0;  // raise the opt-in once (graph-capture friendly)
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaFuncSetAttribute(k_step_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      configured = smem;
+    }
+    k_step_finish<<<1, FINISH_THREADS, smem, s>>>(*net, a);
     return check_launch("sg_step_finish");
   }
   // large models: the same steps as separate grid-wide launches

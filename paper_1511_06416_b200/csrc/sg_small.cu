@@ -24,7 +24,7 @@
 // Counters and draws are identical to the generic kernel's FAST mode
 // (Philox4x32 on (case, variable, replica quad)), so both paths produce the
 // same states and counts from the same tables (tests/test_gpu_small.py).
-#include "sg_device.cuh"
+#include "sg_finish.cuh"
 
 namespace sg {
 
@@ -248,13 +248,14 @@ __device__ __forceinline__ bool small_units(const SmallCtx<N>& x) {
 // (q, s); per latent variable one Philox4x32 call gives the quad's 4
 // uniforms, each lane does one table lookup and compare, and the 4 new
 // states are inserted with one byte-SIMD mask/or.
-template <int N>
+template <int N, bool FUSE>
 __global__ void __launch_bounds__(SG_THREADS)
 k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint8_t* __restrict__ pattern,
               const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes, int lane_ld, int cases, int num_real,
               int m, int64_t case_base, uint64_t key, const uint64_t* __restrict__ key_dev,
               const int32_t* __restrict__ jcell, int cells, unsigned long long* __restrict__ counts,
-              const uint32_t* __restrict__ zs_flag, int32_t* err) {
+              const uint32_t* __restrict__ zs_flag, const int8_t* __restrict__ obs, int ld_obs, int32_t* err,
+              const sg_net fnet, const FinishArgs fin, unsigned int* done) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* stab = reinterpret_cast<uint32_t*>(smem);
   uint8_t* hist8 = smem + ((sp.tab_words * 4 + 15) & ~15);
@@ -294,6 +295,27 @@ k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint
   __syncthreads();
   const bool zs = armed ? small_units<N, true>(x) : small_units<N, false>(x);
   if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
+  if (obs) {  // the minibatch's range check (sampler.py:429-430), spread over the whole grid
+    const int chunks = (cases + 15) >> 4;
+    const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * SG_THREADS + tid;
+    const int gthreads = gridDim.x * gridDim.y * SG_THREADS;
+    unsigned bad = 0;
+    for (int i = gtid; i < N * chunks; i += gthreads) {
+      const int v = i / chunks, ch = i - v * chunks;
+      const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
+      const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
+      const uint32_t wv[4] = {uint32_t(qv.x), uint32_t(qv.y), uint32_t(qv.z), uint32_t(qv.w)};
+      const int left = cases - ch * 16;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t gt = __vcmpgts4(wv[k], lim);
+        const int valid = left - 4 * k;
+        if (valid < 4) gt &= valid <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - valid)));
+        bad |= gt;
+      }
+    }
+    if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
+  }
   if (!counts) return;
   __syncthreads();
   const int warp = tid >> 5, lane_id = tid & 31;
@@ -308,21 +330,36 @@ k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint
   __syncthreads();
   for (int cell = tid; cell < cells; cell += SG_THREADS)
     if (cellacc[cell]) atomicAdd(counts + cell, (unsigned long long)cellacc[cell]);
+  if (FUSE) {
+    // the last CTA to finish runs the step tail on the complete counts
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tid == 0) *done = 0u;  // re-armed for the next launch
+    step_finish_body(fnet, fin, smem, SG_THREADS);
+  }
 }
 
-template <int N>
+template <int N, bool FUSE>
 static void launch_small(const sg_small& sp, dim3 grid, size_t smem, cudaStream_t st, const uint32_t* stab,
                          const uint8_t* pattern, const int32_t* case_id, uint32_t* lanes, int lane_ld, int cases,
                          int num_real, int m, int64_t case_base, uint64_t key, const uint64_t* key_dev,
-                         const int32_t* jcell, int cells, uint64_t* counts, const uint32_t* zs_flag, int32_t* err) {
+                         const int32_t* jcell, int cells, uint64_t* counts, const uint32_t* zs_flag,
+                         const int8_t* obs, int ld_obs, int32_t* err, const sg_net& fnet, const FinishArgs& fin,
+                         unsigned int* done) {
   static size_t configured = 0;  // raise the opt-in once (keeps graph capture free of attribute calls)
   if (smem > configured) {
-    cudaFuncSetAttribute(k_small_sweep<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_small_sweep<N, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured = smem;
   }
-  k_small_sweep<N><<<grid, SG_THREADS, smem, st>>>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m,
-                                                   case_base, key, key_dev, jcell, cells,
-                                                   reinterpret_cast<unsigned long long*>(counts), zs_flag, err);
+  k_small_sweep<N, FUSE><<<grid, SG_THREADS, smem, st>>>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real,
+                                                         m, case_base, key, key_dev, jcell, cells,
+                                                         reinterpret_cast<unsigned long long*>(counts), zs_flag, obs,
+                                                         ld_obs, err, fnet, fin, done);
 }
 
 static size_t small_smem(const sg_small& sp, int cells) {
@@ -363,21 +400,42 @@ extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t l
   return check_launch("sg_small_prepare");
 }
 
-extern "C" int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern, const int32_t* case_id,
-                              uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real, int32_t m,
-                              int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell,
-                              int32_t cells, uint64_t* counts, const uint32_t* zs_flag, int32_t* err,
-                              void* stream) {
-  using namespace sg;
+namespace sg {
+template <bool FUSE>
+static int small_sweep_impl(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern, const int32_t* case_id,
+                            uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real, int32_t m,
+                            int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell,
+                            int32_t cells, uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs,
+                            int32_t ld_obs, int32_t* err, void* stream, const sg_net* fnet, const sg_finish* f,
+                            uint32_t* done) {
   SG_REQUIRE(sp && stab && pattern && case_id && lanes && err, "sg_small_sweep: null argument");
+  if (obs)
+    SG_REQUIRE(ld_obs % 16 == 0 && (reinterpret_cast<uintptr_t>(obs) & 15) == 0 && ld_obs >= cases,
+               "sg_small_sweep: obs rows must be 16-byte aligned");
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV && sp->bits <= SG_SMALL_MAXBITS, "sg_small_sweep: bad plan");
   SG_REQUIRE(!counts || jcell, "sg_small_sweep: joint cell map required for the tally");
   SG_REQUIRE(m >= 1 && lane_ld_ok(lane_ld, cases), "sg_small_sweep: lane_ld %d < cases %d", lane_ld, cases);
   for (int v = 0; v < sp->n; ++v)
     SG_REQUIRE(sp->card[v] <= 4 && sp->tstride[v] >= sp->card[v] - 1 && sp->toff[v] % sp->tstride[v] == 0,
                "sg_small_sweep: variable %d needs card <= 4 and an aligned table", v);
+  if (FUSE) {
+    SG_REQUIRE(fnet && f && done && counts, "sg_small_step: network, finish args, counter and counts required");
+    if (cases == 0 || !finish_fits(*fnet, sp)) {  // nothing to sweep / model too large to fuse: two launches
+      const int st = small_sweep_impl<false>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m,
+                                             case_base, key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs,
+                                             err, stream, nullptr, nullptr, nullptr);
+      return st ? st : sg_step_finish(fnet, sp, f, stream);
+    }
+  }
   if (cases == 0) return SG_OK;
-  const size_t smem = small_smem(*sp, cells);
+  size_t smem = small_smem(*sp, cells);
+  FinishArgs fin{};
+  sg_net fn{};
+  if (FUSE) {
+    fin = make_finish_args(f, sp);
+    fn = *fnet;
+    smem = std::max(smem, finish_smem(*fnet));
+  }
   // byte counters: at most 63 units (252 lanes) per thread before the per-CTA flush
   const int Q = (m + 3) / 4;
   const int64_t need = (int64_t(cases) + int64_t(SG_THREADS) * 63 - 1) / (int64_t(SG_THREADS) * 63);
@@ -389,8 +447,8 @@ extern "C" int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const ui
   uint32_t* lw = reinterpret_cast<uint32_t*>(lanes);
 #define SG_SMALL_CASE(NV)                                                                                     \
   case NV:                                                                                                    \
-    launch_small<NV>(*sp, grid, smem, st, stab, pattern, case_id, lw, lane_ld, cases, num_real, m, case_base, \
-                     key, key_dev, jcell, cells, counts, zs_flag, err);                                       \
+    launch_small<NV, FUSE>(*sp, grid, smem, st, stab, pattern, case_id, lw, lane_ld, cases, num_real, m, case_base, \
+                     key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err, fn, fin, done);           \
     break;
   switch (sp->n) {
     SG_SMALL_CASE(1)
@@ -405,7 +463,28 @@ extern "C" int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const ui
       return SG_EINVAL;
   }
 #undef SG_SMALL_CASE
-  return check_launch("sg_small_sweep");
+  return check_launch(FUSE ? "sg_small_step" : "sg_small_sweep");
+}
+}  // namespace sg
+
+extern "C" int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern, const int32_t* case_id,
+                              uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real, int32_t m,
+                              int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell,
+                              int32_t cells, uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs,
+                              int32_t ld_obs, int32_t* err, void* stream) {
+  return sg::small_sweep_impl<false>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m, case_base, key,
+                                     key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err, stream, nullptr, nullptr,
+                                     nullptr);
+}
+
+extern "C" int sg_small_step(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern, const int32_t* case_id,
+                             uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real, int32_t m,
+                             int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell,
+                             int32_t cells, uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs,
+                             int32_t ld_obs, int32_t* err, const sg_net* net, const sg_finish* f, uint32_t* done,
+                             void* stream) {
+  return sg::small_sweep_impl<true>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m, case_base, key,
+                                    key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err, stream, net, f, done);
 }
 
 extern "C" int sg_small_import(const sg_small* sp, const sg_batch* batch, const int32_t* case_id, uint8_t* lanes,

@@ -35,10 +35,14 @@ k_build_tables(const sg_net net, const double* __restrict__ cpt, double* __restr
       const int u = __ldg(net.mb_var + k);
       s[k - m0] = int((e / __ldg(net.mb_stride + k)) % __ldg(net.card + u));
     }
-    double w[SG_MAX_CARD];
-    conditional_weights(net, v, s, cpt, w);
-    table_entry(w, card, ptab + __ldg(net.ptab_off + v) + e * card, ftab + __ldg(net.ftab_off + v) + e * (card - 1),
-                ftab + net.ftab_size);
+    double* pe = ptab + __ldg(net.ptab_off + v) + e * card;
+    uint32_t* fe = ftab + __ldg(net.ftab_off + v) + e * (card - 1);
+    with_card(card, [&](auto C) {
+      constexpr int K = decltype(C)::value;
+      double w[K ? K : SG_MAX_CARD];
+      conditional_weights<true, K>(net, v, s, cpt, w);
+      table_entry<K>(w, card, pe, fe, ftab + net.ftab_size);
+    });
   }
 }
 

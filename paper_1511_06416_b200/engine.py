@@ -116,6 +116,9 @@ class Engine:
         if self.use_small:
             self.stab = torch.empty(max(1, self.pack.small.tab_words), dtype=torch.int32, device=d)
         self.tables_fresh = False  # conditional tables reflect self.cpt
+        # packed sweep + step tail in one launch (needs no count exchange between them)
+        self.fuse_step = self.use_small and comm is None
+        self.done = torch.zeros(1, dtype=torch.int32, device=d)  # last-CTA counter of sg_small_step
 
     # ------------------------------------------------------------ helpers
     def _upload_keys(self, seed: int, label: str, context: tuple) -> None:
@@ -176,7 +179,8 @@ class Engine:
         stored = self.latent.get(mb.index) if moving else None
         if stored is not None and not (stored.m == m and stored.cases == size):
             stored = None
-        _lib.call("sg_check_range", self.pack.ref, obs.data_ptr(), ld, size, self.err.ptr, s)
+        if not self.use_small:  # the packed sweep checks the block in its own launch
+            _lib.call("sg_check_range", self.pack.ref, obs.data_ptr(), ld, size, self.err.ptr, s)
         if self.use_small:
             db = stored if stored is not None else SmallBatch(self.n, m, size, self.dev)
             db.num_real = int(mb.num_real)
@@ -220,15 +224,26 @@ class Engine:
         if timing is not None:
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record()
+        prev = self.prev_counts.get(mb.index) if moving else None
+        key = 0 if cfg.map_estimate else derive_seed(derive_seed(cfg.seed, "cpt_update", pass_index, mb.index),
+                                                     "sample_cpts")
+        f = self.finish_args(new_counts, prev, key)
+        fused = False
         for sw in range(S):
             sweep_seed = derive_seed(cfg.seed, "sweep", pass_index, mb.index, sw)
-            counts_ptr = new_counts.data_ptr() if sw == S - 1 else None
+            last = sw == S - 1
+            counts_ptr = new_counts.data_ptr() if last else None
             if self.use_small:
-                _lib.call("sg_small_sweep", self.pack.small_ref, self.stab.data_ptr(), db.pattern.data_ptr(),
-                          db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m,
-                          self.case_base, sweep_seed, None, self.pack.small_jcell.data_ptr(), self.pack.cells,
-                          counts_ptr,
-                          self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"], self.err.ptr, s)
+                args = (self.pack.small_ref, self.stab.data_ptr(), db.pattern.data_ptr(), db.case_id.data_ptr(),
+                        db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m, self.case_base, sweep_seed, None,
+                        self.pack.small_jcell.data_ptr(), self.pack.cells, counts_ptr,
+                        self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"],
+                        obs.data_ptr() if last else None, ld, self.err.ptr)
+                if last and self.fuse_step and timing is None:
+                    _lib.call("sg_small_step", *args, self.pack.ref, f, self.done.data_ptr(), s)
+                    fused = True
+                else:
+                    _lib.call("sg_small_sweep", *args, s)
             elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
                 _lib.call("sg_sweep", self.pack.ref, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
@@ -241,13 +256,10 @@ class Engine:
         if timing is not None:
             ev1.record()
             timing.append((ev0, ev1, S))
-        if self.comm is not None:
-            self.comm(new_counts)
-        prev = self.prev_counts.get(mb.index) if moving else None
-        key = 0 if cfg.map_estimate else derive_seed(derive_seed(cfg.seed, "cpt_update", pass_index, mb.index),
-                                                     "sample_cpts")
-        f = self.finish_args(new_counts, prev, key)
-        _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
+        if not fused:
+            if self.comm is not None:
+                self.comm(new_counts)
+            _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
         if moving:
             self.prev_counts[mb.index] = new_counts
             self.latent[mb.index] = db
@@ -404,26 +416,36 @@ class StepGraphs:
         cur = self.cur.data_ptr()
         new, prev = self.cbuf[p], self.cbuf[1 - p]
         # tables and keys of this visit are ready: the previous replay's finish built/advanced them
-        _lib.call("sg_check_range", eng.pack.ref, self.obs.data_ptr(), self.ld, size, eng.err.ptr, s)
+        if not eng.use_small:  # the packed sweep checks the block in its own launch
+            _lib.call("sg_check_range", eng.pack.ref, self.obs.data_ptr(), self.ld, size, eng.err.ptr, s)
         S = cfg.sweeps_per_minibatch
+        # step tail: accumulate, CPT update, next tables, clear `prev` (the next
+        # replay's count buffer), advance the key cursor
+        f = eng.finish_args(new, prev, 0, key_dev=cur + 8 * S, clear=prev,
+                            cursor=(self.table, self.idx, self.kps, self.cur))
+        self._finish_args.append(f)
+        fuse = eng.fuse_step
         for sw in range(S):
-            counts_ptr = new.data_ptr() if sw == S - 1 else None
+            last = sw == S - 1
+            counts_ptr = new.data_ptr() if last else None
             if eng.use_small:
-                _lib.call("sg_small_sweep", eng.pack.small_ref, eng.stab.data_ptr(), db.pattern.data_ptr(),
-                          db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m,
-                          eng.case_base, 0, cur + 8 * sw, eng.pack.small_jcell.data_ptr(), eng.pack.cells,
-                          counts_ptr, eng.ftab.data_ptr() + 4 * eng.pack.layout.scalars["ftab_size"], eng.err.ptr, s)
+                args = (eng.pack.small_ref, eng.stab.data_ptr(), db.pattern.data_ptr(), db.case_id.data_ptr(),
+                        db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m, eng.case_base, 0, cur + 8 * sw,
+                        eng.pack.small_jcell.data_ptr(), eng.pack.cells, counts_ptr,
+                        eng.ftab.data_ptr() + 4 * eng.pack.layout.scalars["ftab_size"],
+                        self.obs.data_ptr() if last else None, self.ld, eng.err.ptr)
+                if fuse and last:  # sweep + tally + step tail in one launch
+                    _lib.call("sg_small_step", *args, eng.pack.ref, f, eng.done.data_ptr(), s)
+                else:
+                    _lib.call("sg_small_sweep", *args, s)
             else:
                 _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
                           eng.err.ptr, s)
-        if eng.comm is not None:
-            eng.comm(new)
-        # accumulate, CPT update, next tables, clear `prev` (the next replay's count buffer), advance keys
-        f = eng.finish_args(new, prev, 0, key_dev=cur + 8 * S, clear=prev,
-                            cursor=(self.table, self.idx, self.kps, self.cur))
-        self._finish_args.append(f)
-        _lib.call("sg_step_finish", eng.pack.ref, eng.small_ptr, f, s)
+        if not fuse:
+            if eng.comm is not None:
+                eng.comm(new)
+            _lib.call("sg_step_finish", eng.pack.ref, eng.small_ptr, f, s)
 
     def step(self, mb=None) -> None:
         """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
@@ -440,8 +462,12 @@ class StepGraphs:
 
     @property
     def launches_per_step(self) -> int:
-        fused = self.eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
-        return 1 + self.eng.cfg.sweeps_per_minibatch + (1 if fused else 5 + (1 if self.eng.use_small else 0))
+        eng = self.eng
+        one_cta = eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
+        if eng.fuse_step and one_cta:  # the last packed sweep runs the step tail in its last CTA
+            return eng.cfg.sweeps_per_minibatch
+        check = 0 if eng.use_small else 1  # the packed sweep folds in the range check
+        return check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
 
     def finish(self) -> None:
         """Hand the last visit's counts back to the engine's moving-sum bookkeeping."""

@@ -297,6 +297,8 @@ class NetPack:
                 setattr(s, k, self.buf32.data_ptr() + 4 * offs32[k])
             else:
                 setattr(s, k, self.buf64.data_ptr() + 8 * offs64[k])
+        s.blob32, s.blob32_words = self.buf32.data_ptr(), self.buf32.numel()
+        s.blob64, s.blob64_words = self.buf64.data_ptr(), self.buf64.numel()
         self.struct = s
         self.ref = ctypes.byref(self.struct)
         plan = small_plan(net, lay)
