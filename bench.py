@@ -215,6 +215,8 @@ def our_arm(args) -> None:
                                    case_base=rank * CASES)
     comm = (lambda c: dist.all_reduce(c)) if world > 1 else None
     eng = Engine(net, cfg, case_base=rank * CASES, comm=comm)
+    if args.fuse:
+        eng.fuse_step = eng.use_small and comm is None
     mb = next(iter(sg.DeviceSource(obs, CASES, CASES)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -228,7 +230,9 @@ def our_arm(args) -> None:
     graphs = None
     if not args.eager:
         total_replays = graph_warm + args.steps + 2 + e2e_steps
-        graphs = StepGraphs(eng, mb, M, range(first, first + total_replays), obs_buffer=obs)
+        # private double-buffered observation blocks: e2e steps upload the next block
+        # on a copy stream while the current visit runs
+        graphs = StepGraphs(eng, mb, M, range(first, first + total_replays))
         for _ in range(graph_warm):
             graphs.step()
         first += graph_warm
@@ -324,7 +328,8 @@ def our_arm(args) -> None:
             "vs_baseline": None, "dtype": "int8 states, u32 draws, f64 CPTs", "data": "synthetic",
             "config": workload_config(world, args.rng),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_sweep (sg_sweep)",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_small_sweep (sg_small_sweep)" if eng.use_small else "k_sweep (sg_sweep)",
                          "kernel_ms": sw, "algorithmic_bytes_per_launch": algo_bytes,
                          "bytes_per_node_sample": BYTES_PER_NODE_SAMPLE, "peak_source": peak_src,
                          "traffic_source": traffic_src, "sweep_share_of_step": sw / ms},
@@ -332,7 +337,8 @@ def our_arm(args) -> None:
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",
-            "kernel_path": "packed-lane sg_small_sweep" if eng.use_small else "generic sg_sweep",
+            "kernel_path": ("packed-lane sg_small_step (sweep + fused step tail)" if eng.fuse_step else
+                            "packed-lane sg_small_sweep + sg_step_finish") if eng.use_small else "generic sg_sweep",
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
@@ -352,6 +358,7 @@ def main() -> None:
     ap.add_argument("--rng", choices=["fast", "numpy"], default="fast")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch each visit eagerly instead of graph replay")
+    ap.add_argument("--fuse", action="store_true", help="run the step tail in the sweep's last CTA (sg_small_step)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -348,9 +348,15 @@ typedef struct sg_finish {
   const uint64_t* key_table;  /* [dev] [steps][kps] key cursor table, or NULL */
   int32_t* key_index;         /* [dev] cursor */
   int32_t kps;                /* keys per step */
-  int32_t pad_;
+  int32_t flags;              /* SG_FINISH_* bits */
   uint64_t* key_current;      /* [dev] [kps] */
 } sg_finish;
+
+/* sg_finish.flags: the packed table is the only consumer of this step's
+   conditional tables (sp != NULL, packed sweep): build it straight from the
+   new CPTs and leave ptab / ftab thresholds stale (the zero-support flag word
+   ftab[ftab_size] is still maintained).  Packed words are identical either way. */
+#define SG_FINISH_PACKED_ONLY 1
 
 int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_finish* f, void* stream);
 

@@ -21,6 +21,7 @@ SG_OK, SG_EINVAL, SG_ECUDA, SG_ECAPACITY = 0, 1, 2, 3
 SG_ERR_ZERO_SUPPORT, SG_ERR_STATE_RANGE, SG_ERR_REJECT_OVERFLOW = 1, 2, 4
 SG_RNG_FAST, SG_RNG_NUMPY, SG_RNG_INJECTED = 0, 1, 2
 SG_ACC_MOVING, SG_ACC_EXPONENTIAL = 0, 1
+SG_FINISH_PACKED_ONLY = 1
 REJ_SLACK = 64
 
 NET_POINTERS = (
@@ -70,7 +71,7 @@ class SgFinish(ctypes.Structure):
         ("total", c_void_p), ("new_counts", c_void_p), ("prev_counts", c_void_p), ("alpha", c_void_p),
         ("key", c_uint64), ("key_dev", c_void_p), ("cpt", c_void_p), ("ptab", c_void_p), ("ftab", c_void_p),
         ("stab", c_void_p), ("clear_counts", c_void_p), ("key_table", c_void_p), ("key_index", c_void_p),
-        ("kps", c_int32), ("pad_", c_int32), ("key_current", c_void_p),
+        ("kps", c_int32), ("flags", c_int32), ("key_current", c_void_p),
     ]
 
 

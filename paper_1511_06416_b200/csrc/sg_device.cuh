@@ -249,6 +249,7 @@ __device__ __forceinline__ void dirichlet_normalise(const double* lg, int card, 
 // One conditional-table entry from the weights w[0..card) of a blanket
 // configuration: pe = cum[0..card-2], norm; fe = ceil(cum/norm * 2^31)
 // thresholds (0xFFFFFFFF in slot 0 and *zs_flag set when norm <= 0).
+// pe may be NULL (thresholds only).
 template <int K = 0>
 __device__ __forceinline__ void table_entry(const double* w, int card, double* pe, uint32_t* fe,
                                             uint32_t* zs_flag) {
@@ -268,11 +269,11 @@ __device__ __forceinline__ void table_entry(const double* w, int card, double* p
 #pragma unroll
   for (int t = 0; t < (K ? K - 1 : card - 1); ++t) {
     cum = t ? __dadd_rn(cum, w[t]) : w[0];
-    pe[t] = cum;
+    if (pe) pe[t] = cum;
     const double q = fmin(ceil(__dmul_rn(cum, scale)), 2147483648.0);
     fe[t] = (t == 0 && !ok) ? 0xFFFFFFFFu : uint32_t(q);
   }
-  pe[card - 1] = norm;
+  if (pe) pe[card - 1] = norm;
   if (!ok) atomicOr(reinterpret_cast<int*>(zs_flag), 1);
 }
 

@@ -54,8 +54,38 @@ struct FinishArgs {
   int kps;
   uint64_t* key_current;
   int has_small;
+  int packed_only;  // SG_FINISH_PACKED_ONLY: skip ptab/ftab, build stab from the CPTs
   sg_small sp;
 };
+
+// Packed word(s) i = (v, S) straight from the CPTs: the weights and
+// thresholds table_entry computes for the blanket configuration S encodes,
+// i.e. exactly the words small_table_entry copies out of ftab.
+__device__ __forceinline__ void small_table_direct(const sg_net& net, const sg_small& sp, const double* cpt,
+                                                   uint32_t* stab, uint32_t* zs_flag, int i) {
+  const int v = i >> sp.bits;
+  const uint32_t S = uint32_t(i & ((1 << sp.bits) - 1));
+  const int card = sp.card[v];
+  uint32_t* out = stab + sp.toff[v] + S * sp.tstride[v];
+  bool valid = (S & ~sp.mbmask[v]) == 0u;
+  int s[SG_MAX_MB];
+  const int m0 = net.mb_start[v], m1 = net.mb_start[v + 1];
+  for (int k = m0; k < m1 && valid; ++k) {
+    const int u = net.mb_var[k];
+    s[k - m0] = small_field(S, sp, u);
+    valid = s[k - m0] < sp.card[u];
+  }
+  if (!valid) {
+    for (int t = 0; t < card - 1; ++t) out[t] = 0u;
+    return;
+  }
+  with_card(card, [&](auto C) {
+    constexpr int K = decltype(C)::value;
+    double w[K ? K : SG_MAX_CARD];
+    conditional_weights<false, K>(net, v, s, cpt, w);
+    table_entry<K>(w, card, nullptr, out, zs_flag);
+  });
+}
 
 static constexpr int FINISH_THREADS = 512;
 static constexpr int FINISH_MAX_CELLS = 4096;
@@ -111,8 +141,13 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     for (int s2 = 0; s2 < card; ++s2) f.cpt[base + s2] = cpt_s[base + s2];
   }
   __syncthreads();
-  // 3. conditional tables from the new CPTs
-  for (int g = tid; g < int(net.table_entries); g += nt) {
+  // 3. conditional tables from the new CPTs (packed-only: the packed words directly)
+  if (f.packed_only) {
+    const sg_small& sp = f.sp;
+    for (int i = tid; i < (sp.n << sp.bits); i += nt)
+      small_table_direct(net, sp, cpt_s, f.stab, f.ftab + net.ftab_size, i);
+  }
+  for (int g = f.packed_only ? int(net.table_entries) : tid; g < int(net.table_entries); g += nt) {
     int lo = 0, hi = net.n;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -135,7 +170,7 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
   }
   __syncthreads();
   // 4. packed-lane tables
-  if (f.has_small) {
+  if (f.has_small && !f.packed_only) {
     const sg_small& sp = f.sp;
     for (int i = tid; i < (sp.n << sp.bits); i += nt) small_table_entry<false>(net, sp, f.ftab, f.stab, i);
   }
@@ -174,6 +209,7 @@ inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
   a.kps = f->kps;
   a.key_current = f->key_current;
   a.has_small = sp ? 1 : 0;
+  a.packed_only = (sp && (f->flags & SG_FINISH_PACKED_ONLY)) ? 1 : 0;
   if (sp) a.sp = *sp;
   return a;
 }

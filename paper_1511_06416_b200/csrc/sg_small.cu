@@ -249,7 +249,7 @@ __device__ __forceinline__ bool small_units(const SmallCtx<N>& x) {
 // uniforms, each lane does one table lookup and compare, and the 4 new
 // states are inserted with one byte-SIMD mask/or.
 template <int N, bool FUSE>
-__global__ void __launch_bounds__(SG_THREADS)
+__global__ void __launch_bounds__(SG_THREADS, 4)
 k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint8_t* __restrict__ pattern,
               const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes, int lane_ld, int cases, int num_real,
               int m, int64_t case_base, uint64_t key, const uint64_t* __restrict__ key_dev,
@@ -344,8 +344,35 @@ k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint
   }
 }
 
+// Resident CTAs of one sweep instance on the whole device (one full wave).
 template <int N, bool FUSE>
-static void launch_small(const sg_small& sp, dim3 grid, size_t smem, cudaStream_t st, const uint32_t* stab,
+static int resident_ctas(size_t smem) {
+  static size_t cached_smem = ~size_t(0);
+  static int cached = 0;
+  if (smem != cached_smem) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_sweep<N, FUSE>, SG_THREADS, smem);
+    cached = sms * std::max(1, per_sm);
+    cached_smem = smem;
+  }
+  return cached;
+}
+
+// One wave of CTAs split over the Q replica quads (every CTA strides over the
+// pattern-sorted slots, so the units' cost is balanced across CTAs), but at
+// least enough CTAs that no thread's byte counters see more than 63 units.
+template <int N, bool FUSE>
+static dim3 small_grid(int cases, int Q, size_t smem) {
+  const int64_t need = (int64_t(cases) + int64_t(SG_THREADS) * 63 - 1) / (int64_t(SG_THREADS) * 63);
+  const int64_t fill = (int64_t(cases) + SG_THREADS - 1) / SG_THREADS;
+  const int64_t want = std::max<int64_t>(resident_ctas<N, FUSE>(smem) / Q, need);
+  return dim3(unsigned(std::max<int64_t>(1, std::min<int64_t>(want, fill))), unsigned(Q));
+}
+
+template <int N, bool FUSE>
+static void launch_small(const sg_small& sp, int Q, size_t smem, cudaStream_t st, const uint32_t* stab,
                          const uint8_t* pattern, const int32_t* case_id, uint32_t* lanes, int lane_ld, int cases,
                          int num_real, int m, int64_t case_base, uint64_t key, const uint64_t* key_dev,
                          const int32_t* jcell, int cells, uint64_t* counts, const uint32_t* zs_flag,
@@ -356,6 +383,7 @@ static void launch_small(const sg_small& sp, dim3 grid, size_t smem, cudaStream_
     cudaFuncSetAttribute(k_small_sweep<N, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured = smem;
   }
+  const dim3 grid = small_grid<N, FUSE>(cases, Q, smem);
   k_small_sweep<N, FUSE><<<grid, SG_THREADS, smem, st>>>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real,
                                                          m, case_base, key, key_dev, jcell, cells,
                                                          reinterpret_cast<unsigned long long*>(counts), zs_flag, obs,
@@ -436,18 +464,12 @@ static int small_sweep_impl(const sg_small* sp, const uint32_t* stab, const uint
     fn = *fnet;
     smem = std::max(smem, finish_smem(*fnet));
   }
-  // byte counters: at most 63 units (252 lanes) per thread before the per-CTA flush
   const int Q = (m + 3) / 4;
-  const int64_t need = (int64_t(cases) + int64_t(SG_THREADS) * 63 - 1) / (int64_t(SG_THREADS) * 63);
-  const int64_t fill = (int64_t(cases) + SG_THREADS - 1) / SG_THREADS;
-  const int64_t want = std::max<int64_t>((148 * 8 + Q - 1) / Q, need);  // ~8 CTAs per SM in total
-  const int gx = int(std::max<int64_t>(1, std::min<int64_t>(want, fill)));
-  const dim3 grid(gx, Q);
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t* lw = reinterpret_cast<uint32_t*>(lanes);
 #define SG_SMALL_CASE(NV)                                                                                     \
   case NV:                                                                                                    \
-    launch_small<NV, FUSE>(*sp, grid, smem, st, stab, pattern, case_id, lw, lane_ld, cases, num_real, m, case_base, \
+    launch_small<NV, FUSE>(*sp, Q, smem, st, stab, pattern, case_id, lw, lane_ld, cases, num_real, m, case_base, \
                      key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err, fn, fin, done);           \
     break;
   switch (sp->n) {

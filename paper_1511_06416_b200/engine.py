@@ -116,8 +116,11 @@ class Engine:
         if self.use_small:
             self.stab = torch.empty(max(1, self.pack.small.tab_words), dtype=torch.int32, device=d)
         self.tables_fresh = False  # conditional tables reflect self.cpt
-        # packed sweep + step tail in one launch (needs no count exchange between them)
-        self.fuse_step = self.use_small and comm is None
+        # sg_small_step: packed sweep + step tail in one launch (needs no count exchange
+        # between them).  Off by default: the tail then runs in one 256-thread CTA of a
+        # 64-register kernel, which measured slower on B200 than the separate
+        # 512-thread sg_step_finish launch (bench.py --fuse, profiles/README.md).
+        self.fuse_step = False
         self.done = torch.zeros(1, dtype=torch.int32, device=d)  # last-CTA counter of sg_small_step
 
     # ------------------------------------------------------------ helpers
@@ -285,6 +288,8 @@ class Engine:
         f.ftab = self.ftab.data_ptr()
         f.stab = self.stab.data_ptr() if self.use_small else None
         f.clear_counts = None if clear is None else clear.data_ptr()
+        # the packed sweep reads only the packed words: build them straight from the CPTs
+        f.flags = _lib.SG_FINISH_PACKED_ONLY if self.use_small else 0
         if cursor is not None:
             table, index, kps, current = cursor
             f.key_table, f.key_index, f.kps, f.key_current = table.data_ptr(), index.data_ptr(), kps, current.data_ptr()
@@ -388,12 +393,25 @@ class StepGraphs:
         prev = eng.prev_counts[mb.index]
         self.cbuf = [torch.zeros_like(prev), prev.clone()]
         if obs_buffer is None:
+            # two private buffers, one per graph parity: step(mb) uploads the next
+            # visit's block on a copy stream while the current visit runs
             src, _ = eng._obs_for(mb)
-            obs_buffer = torch.empty((eng.n, _pitch(mb.size)), dtype=torch.int8, device=d)
-            obs_buffer[:, :src.shape[1]].copy_(src[:, :obs_buffer.shape[1]])
-        if obs_buffer.stride(0) % 16 or obs_buffer.stride(1) != 1 or obs_buffer.data_ptr() % 16:
-            raise ValueError("obs_buffer must be an int8 (n, pitch) tensor with 16-byte aligned rows")
-        self.obs, self.ld = obs_buffer, obs_buffer.stride(0)
+            bufs = []
+            for _ in range(2):
+                b = torch.empty((eng.n, _pitch(mb.size)), dtype=torch.int8, device=d)
+                b[:, :src.shape[1]].copy_(src[:, :b.shape[1]])
+                bufs.append(b)
+            self.private_obs = True
+        else:
+            bufs = [obs_buffer, obs_buffer]
+            self.private_obs = False
+        for b in bufs:
+            if b.stride(0) % 16 or b.stride(1) != 1 or b.data_ptr() % 16:
+                raise ValueError("obs_buffer must be an int8 (n, pitch) tensor with 16-byte aligned rows")
+        self.obs_bufs, self.ld = bufs, bufs[0].stride(0)
+        self.obs = bufs[0]
+        self._copy_stream = None
+        self._buf_free: list = [None, None]  # event: the last replay reading buffer p has finished
         self.graphs = []
         self._finish_args = []
         if not eng.tables_fresh:
@@ -415,9 +433,10 @@ class StepGraphs:
         size = self.mb.size
         cur = self.cur.data_ptr()
         new, prev = self.cbuf[p], self.cbuf[1 - p]
+        obs = self.obs_bufs[p]
         # tables and keys of this visit are ready: the previous replay's finish built/advanced them
         if not eng.use_small:  # the packed sweep checks the block in its own launch
-            _lib.call("sg_check_range", eng.pack.ref, self.obs.data_ptr(), self.ld, size, eng.err.ptr, s)
+            _lib.call("sg_check_range", eng.pack.ref, obs.data_ptr(), self.ld, size, eng.err.ptr, s)
         S = cfg.sweeps_per_minibatch
         # step tail: accumulate, CPT update, next tables, clear `prev` (the next
         # replay's count buffer), advance the key cursor
@@ -433,7 +452,7 @@ class StepGraphs:
                         db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m, eng.case_base, 0, cur + 8 * sw,
                         eng.pack.small_jcell.data_ptr(), eng.pack.cells, counts_ptr,
                         eng.ftab.data_ptr() + 4 * eng.pack.layout.scalars["ftab_size"],
-                        self.obs.data_ptr() if last else None, self.ld, eng.err.ptr)
+                        obs.data_ptr() if last else None, self.ld, eng.err.ptr)
                 if fuse and last:  # sweep + tally + step tail in one launch
                     _lib.call("sg_small_step", *args, eng.pack.ref, f, eng.done.data_ptr(), s)
                 else:
@@ -451,12 +470,31 @@ class StepGraphs:
         """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
         if self.replayed >= self.planned:
             raise IndexError("all planned visits have been replayed")
+        p = self.replayed % 2
+        main = torch.cuda.current_stream()
         if mb is not None:
             vals = mb.values
-            if not (isinstance(vals, torch.Tensor) and vals.is_cuda and vals.data_ptr() == self.obs.data_ptr()):
+            buf = self.obs_bufs[p]
+            if not (isinstance(vals, torch.Tensor) and vals.is_cuda and vals.data_ptr() == buf.data_ptr()):
                 src = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(np.asarray(vals, dtype=np.int8))
-                self.obs[:, :mb.size].copy_(src, non_blocking=True)
-        self.graphs[self.replayed % 2].replay()
+                if not self.private_obs:
+                    buf[:, :mb.size].copy_(src, non_blocking=True)
+                else:
+                    # upload on the copy stream once the replay that last read this buffer is done,
+                    # so it overlaps the other parity's replay
+                    if self._copy_stream is None:
+                        self._copy_stream = torch.cuda.Stream()
+                    cs = self._copy_stream
+                    if self._buf_free[p] is not None:
+                        cs.wait_event(self._buf_free[p])
+                    with torch.cuda.stream(cs):
+                        buf[:, :mb.size].copy_(src, non_blocking=True)
+                    main.wait_stream(cs)
+        self.graphs[p].replay()
+        if self.private_obs:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self._buf_free[p] = ev
         self.replayed += 1
         _lib.launch_count += self.launches_per_step
 

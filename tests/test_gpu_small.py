@@ -85,6 +85,66 @@ def test_graph_replay_equals_eager_visits(koller, small):
                                   b.lane_states(0)[:, :, :cases].cpu().numpy())
 
 
+@pytest.mark.parametrize("map_estimate", [False, True])
+def test_packed_only_tables_equal_two_stage_build(koller, map_estimate):
+    """The step tail's packed words built straight from the CPTs
+    (SG_FINISH_PACKED_ONLY) equal sg_build_tables -> sg_small_tables."""
+    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200.device import stream_handle
+
+    net, truth = koller
+    cases, m = 10_000, 6
+    obs = sg.forward_sample_device(net, truth, cases, seed=41, hide_fraction=0.5, mask_seed=42)
+    cfg = sg.SamplerConfig(same_m=m, minibatch_size=cases, num_passes=1, seed=23, rng="fast",
+                           map_estimate=map_estimate)
+    a, _ = _engines(net, cfg)
+    mb = next(iter(sg.DeviceSource(obs, cases, cases)))
+    for p in range(3):
+        a.visit(mb, p, m)
+        ptab = torch.empty_like(a.ptab)
+        ftab = torch.empty_like(a.ftab)
+        stab = torch.zeros_like(a.stab)
+        s = stream_handle()
+        _lib.call("sg_build_tables", a.pack.ref, a.cpt.data_ptr(), ptab.data_ptr(), ftab.data_ptr(), s)
+        _lib.call("sg_small_tables", a.pack.ref, a.pack.small_ref, ftab.data_ptr(), stab.data_ptr(), s)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(a.stab.cpu().numpy(), stab.cpu().numpy())
+        assert int(a.ftab[-1]) == int(ftab[-1])
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_graph_host_uploads_equal_eager_visits(koller, fuse):
+    """Graph replays fed host minibatches (double-buffered copy-stream uploads),
+    with and without the fused step tail, match eager visits bit for bit."""
+    from paper_1511_06416_b200.engine import Engine, StepGraphs
+
+    net, truth = koller
+    cases, m = 30_000, 4
+    obs = sg.forward_sample_device(net, truth, cases, seed=31, hide_fraction=0.5, mask_seed=32)
+    cfg = sg.SamplerConfig(same_m=m, minibatch_size=cases, num_passes=1, seed=17, rng="fast")
+    mb = next(iter(sg.DeviceSource(obs, cases, cases)))
+    host = torch.empty((net.num_vars, cases), dtype=torch.int8, pin_memory=True)
+    host.copy_(obs[:, :cases])
+    hmb = sg.Minibatch(index=0, values=host, weights=np.ones(cases), num_real=cases)
+    a = Engine(net, cfg)
+    a.fuse_step = False
+    b = Engine(net, cfg)
+    b.fuse_step = fuse
+    for p in range(7):
+        a.visit(mb, p, m)
+    b.visit(mb, 0, m)
+    g = StepGraphs(b, mb, m, range(1, 7))
+    for _ in range(6):
+        g.step(hmb)
+    g.finish()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(a.cpt.cpu().numpy(), b.cpt.cpu().numpy())
+    np.testing.assert_array_equal(a.prev_counts[0].cpu().numpy(), b.prev_counts[0].cpu().numpy())
+    np.testing.assert_array_equal(a.lane_states(0)[:, :, :cases].cpu().numpy(),
+                                  b.lane_states(0)[:, :, :cases].cpu().numpy())
+    assert b.err.read() == 0
+
+
 def test_random_small_networks_packed_equals_generic():
     rng = np.random.default_rng(77)
     done = 0
