@@ -12,7 +12,7 @@ on the device.  node-samples per step = n_vars x cases x m (sampler.py:475).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Timing: per-step CUDA events on the launching stream, L2 flushed (256 MB
-write) between timed steps, max over ranks.  Prints ONE JSON line on rank 0.
+write + 256 MB read) between timed steps, max over ranks.  Prints ONE JSON line on rank 0.
 ``--impl reference`` times the CPU oracle (NumPy restatement of the reference,
 oracle/) on the host cores instead.
 """
@@ -51,7 +51,7 @@ def workload_config(n_gpus: int, rng: str) -> dict:
         "hidden_fraction": HIDE,
         "rng": rng,
         "parallelism": f"case-sharded x{n_gpus}, int64 count all-reduce" if n_gpus > 1 else "single GPU",
-        "l2": "flushed between timed steps (256 MB write outside the step events)",
+        "l2": "flushed between timed steps (256 MB write + 256 MB read, outside the step events)",
     }
 
 
@@ -215,10 +215,17 @@ def our_arm(args) -> None:
                                    case_base=rank * CASES)
     comm = (lambda c: dist.all_reduce(c)) if world > 1 else None
     eng = Engine(net, cfg, case_base=rank * CASES, comm=comm)
-    if args.fuse:
-        eng.fuse_step = eng.use_small and comm is None
     mb = next(iter(sg.DeviceSource(obs, CASES, CASES)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush_rd = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def flush_l2(k):
+        # evict the working set: write 256 MB (> 126 MB L2), then read another
+        # 256 MB so the flush's own dirty lines are written back here, outside
+        # the timed events, not during the next step
+        flush.fill_(k & 0xFF)
+        flush_rd.sum(dtype=torch.int64)
+
 
     # eager warm-up visits: the first one builds the resident lanes
     for w in range(args.warmup):
@@ -246,7 +253,7 @@ def our_arm(args) -> None:
     launches0 = _lib.launch_count
     with ClockSampler(local) as clk:
         for k in range(args.steps):
-            flush.fill_(k & 0xFF)
+            flush_l2(k)
             starts[k].record()
             if graphs is not None:
                 graphs.step()
@@ -266,7 +273,7 @@ def our_arm(args) -> None:
         probe.visit(mb, 0, M)
     probe.sweep_events = []
     for k in range(20):
-        flush.fill_(k & 0xFF)
+        flush_l2(k)
         probe.visit(mb, 1 + k, M)
     torch.cuda.synchronize()
     sweep_ms = [a.elapsed_time(b) / nsw for a, b, nsw in probe.sweep_events[2:]]
@@ -337,8 +344,8 @@ def our_arm(args) -> None:
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",
-            "kernel_path": ("packed-lane sg_small_step (sweep + fused step tail)" if eng.fuse_step else
-                            "packed-lane sg_small_sweep + sg_step_finish") if eng.use_small else "generic sg_sweep",
+            "kernel_path": "packed-lane sg_small_sweep + sg_step_finish" if eng.use_small else
+                           "generic sg_sweep + sg_step_finish",
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
@@ -358,7 +365,6 @@ def main() -> None:
     ap.add_argument("--rng", choices=["fast", "numpy"], default="fast")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch each visit eagerly instead of graph replay")
-    ap.add_argument("--fuse", action="store_true", help="run the step tail in the sweep's last CTA (sg_small_step)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -46,7 +46,10 @@ typedef enum sg_status {
 #define SG_ERR_REJECT_OVERFLOW 4u   /* too many Lemire rejections in one init stream */
 
 /* RNG modes of sg_sweep / sg_init_states */
-#define SG_RNG_FAST 0      /* Philox4x32-10, counters (case, var, replica quad) */
+#define SG_RNG_FAST 0      /* Philox4x32-10 under the fixed key (0x243F6A88, 0x85A308D3), counter
+                              (global case, var | quad << 16 | purpose << 28, key lo, key hi):
+                              purpose 0 = sweep draw, 1 = initial state; word j of the block is
+                              replica 4 * quad + j.  Global cases < 2^32, m <= 16384. */
 #define SG_RNG_NUMPY 1     /* numpy Philox4x64-10 stream per variable (bit-exact) */
 #define SG_RNG_INJECTED 2  /* caller-supplied fp64 uniforms, reference order */
 
@@ -289,11 +292,11 @@ int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t ld_obs,
                      uint8_t* pattern, int32_t* case_id, uint8_t* lanes,
                      int32_t lane_ld, void* stream);
 
-/* Sweep + tally on packed lanes.  jcell [dev] [2^bits][n]: CPT cell of each
-   variable for each lane word; zs_flag = ftab + ftab_size (arms the
-   ZeroSupport check).  counts may be NULL.  obs (int8 [n][ld_obs], or NULL)
-   is the minibatch's observation block: its range check (sg_check_range)
-   runs inside the same launch. */
+/* Sweep + tally on packed lanes (m <= 32, FAST stream).  jcell [dev]
+   [2^bits][n]: CPT cell of each variable for each lane word; zs_flag = ftab +
+   ftab_size (arms the ZeroSupport check).  counts may be NULL.  obs (int8
+   [n][ld_obs], or NULL) is the minibatch's observation block: its range check
+   (sg_check_range) runs inside the same launch. */
 int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern,
                    const int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
                    int32_t cases, int32_t num_real, int32_t m, int64_t case_base,
@@ -301,18 +304,6 @@ int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const uint8_t* patt
                    uint64_t* counts, const uint32_t* zs_flag,
                    const int8_t* obs, int32_t ld_obs, int32_t* err,
                    void* stream);
-
-/* sg_small_sweep + sg_step_finish in ONE launch: the last CTA to finish its
-   tally (device counter `done`, zero on entry and re-armed on exit) runs the
-   step tail for the whole grid.  The model must fit the single-CTA tail
-   (<= 4096 cells). */
-int sg_small_step(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern,
-                  const int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
-                  int32_t cases, int32_t num_real, int32_t m, int64_t case_base,
-                  uint64_t key, const uint64_t* key_dev, const int32_t* jcell, int32_t cells,
-                  uint64_t* counts, const uint32_t* zs_flag,
-                  const int8_t* obs, int32_t ld_obs, int32_t* err,
-                  const sg_net* net, const struct sg_finish* f, uint32_t* done, void* stream);
 
 /* Layout switches between packed lanes and sg_batch int8 lane states. */
 int sg_small_import(const sg_small* sp, const sg_batch* batch, const int32_t* case_id,

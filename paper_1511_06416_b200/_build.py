@@ -45,28 +45,34 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every .cu into libsamegibbs_b200.so (objects in csrc/build)."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines: tuple[str, ...] = (),
+          lib: Path | None = None) -> Path:
+    """Compile every .cu into libsamegibbs_b200.so (objects in csrc/build).
+
+    ``defines``/``lib``: a variant build (extra -D flags) into another path,
+    for A/B kernel experiments (load it with SAMEGIBBS_LIB=<path>)."""
+    target = Path(lib) if lib else LIB
+    if not force and not defines and lib is None and not _stale():
         return LIB
-    out = CSRC / "build"
+    out = CSRC / ("build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
     out.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = out / (Path(src).stem + ".o")
-        cmd = [nvcc(), *flags(), "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *flags(), *[f"-D{d}" for d in defines], "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = target.with_suffix(".so.tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
            "-Xcompiler", "-fPIC"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=True, defines=defs, lib=Path(outs[0]) if outs else None))

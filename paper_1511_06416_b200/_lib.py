@@ -10,12 +10,14 @@ machine has no CUDA device, every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_double, c_int32, c_int64, c_uint64, c_void_p
 from pathlib import Path
 
 from .errors import DeviceError
 
-LIB_PATH = Path(__file__).resolve().parent / "libsamegibbs_b200.so"
+# SAMEGIBBS_LIB overrides the in-tree library (variant builds for kernel A/B runs)
+LIB_PATH = Path(os.environ.get("SAMEGIBBS_LIB") or Path(__file__).resolve().parent / "libsamegibbs_b200.so")
 
 SG_OK, SG_EINVAL, SG_ECUDA, SG_ECAPACITY = 0, 1, 2, 3
 SG_ERR_ZERO_SUPPORT, SG_ERR_STATE_RANGE, SG_ERR_REJECT_OVERFLOW = 1, 2, 4
@@ -102,9 +104,6 @@ _SIGNATURES = {
                         c_int32, c_void_p, c_void_p], c_int32),
     "sg_keys_advance": ([c_void_p, c_void_p, c_int32, c_void_p, c_void_p], c_int32),
     "sg_step_finish": ([POINTER(SgNet), c_void_p, POINTER(SgFinish), c_void_p], c_int32),
-    "sg_small_step": ([POINTER(SgSmall), c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32,
-                       c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
-                       c_int32, c_void_p, POINTER(SgNet), POINTER(SgFinish), c_void_p, c_void_p], c_int32),
     "sg_small_import": ([POINTER(SgSmall), POINTER(SgBatch), c_void_p, c_void_p, c_int32, c_void_p], c_int32),
     "sg_small_export": ([POINTER(SgSmall), POINTER(SgBatch), c_void_p, c_void_p, c_void_p, c_int32, c_void_p],
                         c_int32),
@@ -148,7 +147,7 @@ KERNELS_PER_CALL = {
     "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
     "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
-    "sg_keys_advance": 1, "sg_step_finish": 1, "sg_small_step": 1,
+    "sg_keys_advance": 1, "sg_step_finish": 1,
 }
 launch_count = 0
 

@@ -256,6 +256,8 @@ extern "C" int sg_init_states(const sg_net* net, const sg_batch* batch, const in
   const int64_t per_var = int64_t(batch->m) * batch->pitch;
   const int gx = int(std::min<int64_t>((per_var + 255) / 256, 1024));
   if (rng_mode == SG_RNG_FAST) {
+    SG_REQUIRE(fast_cases_ok(batch->case_base, batch->cases) && batch->m <= 4 * 4096,
+               "sg_init_states: FAST counters need global cases < 2^32 and m <= 16384");
     k_init_states<SG_RNG_FAST><<<dim3(gx, net->n), 256, 0, s>>>(*net, *batch, obs, ld_obs, fast_key, nullptr,
                                                                 nullptr, err);
   } else {

@@ -88,11 +88,55 @@ __device__ __forceinline__ uint32_t np_word32(uint64_t j, uint64_t k0, uint64_t 
   return (j & 1) ? uint32_t(w >> 32) : uint32_t(w);
 }
 
-// Fast-mode counter for (case, variable, replica quad, purpose).
+// FAST-mode stream: Philox4x32-10 under a FIXED key, counter
+//   (global case, v | quad << 16 | purpose << 28, step key lo, step key hi)
+// for global case < 2^32, v < 2^16, quad < 2^12, purpose < 16 (checked by
+// the entry points).  The step key rides in the counter, so every round key
+// is a compile-time immediate, and the first round splits into a per-launch
+// part (FastKey, from the key words), a per-case part (FastCase, from the
+// case word) and one XOR with the (variable, quad) word -- the packed sweep
+// shares the first two across all of a case's draws.
+constexpr uint32_t FAST_K0 = 0x243F6A88u, FAST_K1 = 0x85A308D3u;
+constexpr uint32_t PHILOX_M0 = 0xD2511F53u, PHILOX_M1 = 0xCD9E8D57u;
+constexpr uint32_t PHILOX_W0 = 0x9E3779B9u, PHILOX_W1 = 0xBB67AE85u;
+
+struct FastKey {
+  uint32_t hk0, lo1, khi;  // umulhi(M1, key_lo) ^ K0, M1 * key_lo, key_hi ^ K1
+};
+struct FastCase {
+  uint32_t x0, x1, x2, x3;  // state after round 1, without the (v, quad) word
+};
+
+__device__ __forceinline__ FastKey fast_key(uint64_t key) {
+  const uint32_t lo = uint32_t(key);
+  return FastKey{__umulhi(PHILOX_M1, lo) ^ FAST_K0, PHILOX_M1 * lo, uint32_t(key >> 32) ^ FAST_K1};
+}
+__device__ __forceinline__ FastCase fast_case(const FastKey& k, uint32_t gcase) {
+  return FastCase{k.hk0, k.lo1, __umulhi(PHILOX_M0, gcase) ^ k.khi, PHILOX_M0 * gcase};
+}
+__device__ __forceinline__ uint32_t fast_word(uint32_t v, uint32_t quad, uint32_t purpose) {
+  return v | (quad << 16) | (purpose << 28);
+}
+// Rounds 2..10 after the shared first round.
+__device__ __forceinline__ u32x4 fast_draw(const FastCase& c, uint32_t word) {
+  u32x4 x{c.x0 ^ word, c.x1, c.x2, c.x3};
+#pragma unroll
+  for (int r = 1; r < 10; ++r) {
+    const uint32_t k0 = FAST_K0 + uint32_t(r) * PHILOX_W0, k1 = FAST_K1 + uint32_t(r) * PHILOX_W1;
+    const uint32_t lo0 = PHILOX_M0 * x.a, hi0 = __umulhi(PHILOX_M0, x.a);
+    const uint32_t lo1 = PHILOX_M1 * x.c, hi1 = __umulhi(PHILOX_M1, x.c);
+    x = u32x4{hi1 ^ x.b ^ k0, lo1, hi0 ^ x.d ^ k1, lo0};
+  }
+  return x;
+}
+// Host check of the FAST counter's case word: global case ids fit 32 bits.
+inline bool fast_cases_ok(int64_t case_base, int64_t cases) {
+  return case_base >= 0 && case_base + cases <= (int64_t(1) << 32);
+}
+// = philox4x32_10({gcase, fast_word(v, quad, purpose), key_lo, key_hi}, FAST_K0, FAST_K1)
 __device__ __forceinline__ u32x4 fast_block(uint64_t key, uint64_t gcase, uint32_t v,
                                             uint32_t quad, uint32_t purpose) {
-  return philox4x32_10(u32x4{uint32_t(gcase), v, quad, uint32_t(gcase >> 32) ^ (purpose << 24)},
-                       uint32_t(key), uint32_t(key >> 32));
+  return fast_draw(fast_case(fast_key(key), uint32_t(gcase)), fast_word(v, quad, purpose));
 }
 
 // ---------------------------------------------------------------- fp64

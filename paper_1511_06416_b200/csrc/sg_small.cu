@@ -24,7 +24,7 @@
 // Counters and draws are identical to the generic kernel's FAST mode
 // (Philox4x32 on (case, variable, replica quad)), so both paths produce the
 // same states and counts from the same tables (tests/test_gpu_small.py).
-#include "sg_finish.cuh"
+#include "sg_device.cuh"
 
 namespace sg {
 
@@ -149,118 +149,160 @@ __global__ void k_small_export(const sg_small sp, const sg_batch bt, const int32
 
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int j) { return __byte_perm(w, 0u, 0x4440 | j); }
 
+#ifndef SG_VAR_UNROLL
+#define SG_VAR_UNROLL 1
+#endif
+// Colour-position loop unrolling.  1 (a loop) measured faster on B200 than a
+// full unroll: the unrolled body (~8.3k SASS instructions for N=5, QG=3)
+// overflows the instruction cache; the loop (~3.4k) does not.
+constexpr int kVarUnroll = SG_VAR_UNROLL;
+
 // u >= t as 0/1 for 31-bit u and thresholds t <= 2^31 (sentinel 0xFFFFFFFF never passes).
 __device__ __forceinline__ uint32_t ge(uint32_t u, uint32_t t) { return u >= t ? 1u : 0u; }
 
-// Per-thread constants of the sweep (the variable loop is unrolled over N
-// colour-ordered positions, every per-variable constant in registers).
-template <int N>
-struct SmallCtx {
-  int VAR[N], SH[N], K1[N];
-  uint32_t MSK[N], CLR[N];
-  const uint32_t* TV[N];
-  uint32_t* row;
-  const uint8_t* pattern;
-  const int32_t* case_id;
-  uint8_t* hist8;
-  int cases, num_real, q, nl, slot;
-  uint32_t valid4;
-  int64_t case_base;
-  uint64_t key;
-  bool counts;
+// Per-variable constants in colour order, passed by value so that every use
+// is a constant-bank operand with an immediate offset (no dynamic indexing,
+// no registers held across the unit loop).
+struct SmallOrd {
+  uint32_t var[SG_SMALL_MAXV];   // variable at colour position i (its pattern bit, counter word)
+  uint32_t sh[SG_SMALL_MAXV];    // field offset
+  uint32_t k1[SG_SMALL_MAXV];    // card - 1 (1..3)
+  uint32_t msk[SG_SMALL_MAXV];   // blanket mask, replicated into the 4 bytes
+  uint32_t clr[SG_SMALL_MAXV];   // ~field mask, replicated
+  uint32_t toff[SG_SMALL_MAXV];  // table offset (words)
 };
 
-// Walk this thread's (slot, quad) units.  ARMED: some table entry has no
-// support, so every draw checks for the sentinel (the reference raises
-// ZeroSupport only when a lane actually hits such a configuration).
-template <int N, bool ARMED>
-__device__ __forceinline__ bool small_units(const SmallCtx<N>& x) {
+// Quad geometry of one thread: quads q0 .. q0 + QG - 1 of its slot.  Quads
+// past the last real one alias it (same word, same draws; never stored or
+// tallied); only the last real quad can have fewer than 4 real lanes.
+struct QuadSet {
+  uint32_t row0;    // word offset of quad q0's row
+  uint32_t ld;      // lane_ld (words between quad rows)
+  uint32_t q0w;     // q0 << 16 (counter word)
+  int last;         // index (0-based in the group) of the last real quad
+  int last_nl;      // real lanes of that quad (1..4)
+  uint32_t last_valid;
+};
+
+// One byte counter += 1 at shared address a (a thread's own slot: no races).
+__device__ __forceinline__ void hist_inc(uint32_t a) {
+  asm volatile("{\n\t.reg .u16 t;\n\tld.shared.u8 t, [%0];\n\tadd.u16 t, t, 1;\n\tst.shared.u8 [%0], t;\n\t}"
+               :: "r"(a));
+}
+
+// Walk this thread's slots: per latent variable (colour order), QG
+// independent Philox blocks (one per quad, sharing the case's first round),
+// then per quad 4 table lookups + compares and one byte-SIMD insert.
+template <int N, int QG, bool ARMED>
+__device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs, const uint32_t* stab,
+                                            uint32_t* lanes, const uint8_t* __restrict__ pattern,
+                                            const int32_t* __restrict__ case_id, uint32_t hist_a, int cases,
+                                            int num_real, int64_t case_base, const FastKey& fk, bool counts) {
   const int stride = gridDim.x * SG_THREADS;
   bool zs = false;
   int s = blockIdx.x * SG_THREADS + threadIdx.x;
-  uint32_t nw = 0, nP = 0;
+  uint32_t nw[QG], nP = 0;
   int nc = 0;
-  if (s < x.cases) {
-    nw = x.row[s];
-    nP = x.pattern[s];
-    nc = x.case_id[s];
+  uint32_t* rows = lanes + qs.row0;
+  if (s < cases) {
+#pragma unroll
+    for (int g = 0; g < QG; ++g) nw[g] = rows[min(g, qs.last) * qs.ld + s];
+    nP = pattern[s];
+    nc = case_id[s];
   }
-  for (; s < x.cases; s += stride) {
-    uint32_t w = nw;
+  for (; s < cases; s += stride) {
+    uint32_t w[QG];
+#pragma unroll
+    for (int g = 0; g < QG; ++g) w[g] = nw[g];
     const uint32_t P = nP;
     const int c = nc;
     const int sn = s + stride;
-    if (sn < x.cases) {  // prefetch the next unit while this one computes
-      nw = x.row[sn];
-      nP = x.pattern[sn];
-      nc = x.case_id[sn];
-    }
-    const uint64_t gc = uint64_t(x.case_base + c);
+    if (sn < cases) {  // prefetch the next slot while this one computes
 #pragma unroll
+      for (int g = 0; g < QG; ++g) nw[g] = rows[min(g, qs.last) * qs.ld + sn];
+      nP = pattern[sn];
+      nc = case_id[sn];
+    }
+    const FastCase fc = fast_case(fk, uint32_t(case_base + c));
+#pragma unroll kVarUnroll
     for (int i = 0; i < N; ++i) {
-      if (!((P >> x.VAR[i]) & 1u)) continue;  // warp-uniform: slots are bucketed by pattern
-      const u32x4 r = fast_block(x.key, gc, uint32_t(x.VAR[i]), uint32_t(x.q), 0u);
-      const uint32_t u[4] = {r.a >> 1, r.b >> 1, r.c >> 1, r.d >> 1};
-      const uint32_t wm = w & x.MSK[i];
-      uint32_t xs[4];
-      if (x.K1[i] == 1) {
+      if (!((P >> o.var[i]) & 1u)) continue;  // warp-uniform: slots are bucketed by pattern
+      u32x4 r[QG];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t t = x.TV[i][byte_of(wm, j)];
-          if (ARMED && j < x.nl && t == 0xFFFFFFFFu) zs = true;
-          xs[j] = ge(u[j], t);
-        }
-      } else if (x.K1[i] == 2) {
-        const uint2* t2 = reinterpret_cast<const uint2*>(x.TV[i]);
+      for (int g = 0; g < QG; ++g) r[g] = fast_draw(fc, o.var[i] | (qs.q0w + (uint32_t(min(g, qs.last)) << 16)));
+      const uint32_t* tv = stab + o.toff[i];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint2 t = t2[byte_of(wm, j)];
-          if (ARMED && j < x.nl && t.x == 0xFFFFFFFFu) zs = true;
-          xs[j] = ge(u[j], t.x) + ge(u[j], t.y);
-        }
-      } else {
-        const uint4* t4 = reinterpret_cast<const uint4*>(x.TV[i]);
+      for (int g = 0; g < QG; ++g) {
+        const uint32_t u[4] = {r[g].a >> 1, r[g].b >> 1, r[g].c >> 1, r[g].d >> 1};
+        const uint32_t wm = w[g] & o.msk[i];
+        const int nl = g < qs.last ? 4 : (g == qs.last ? qs.last_nl : 0);
+        uint32_t xs[4];
+        if (o.k1[i] == 1) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint4 t = t4[byte_of(wm, j)];  // card 4: three thresholds + padding
-          if (ARMED && j < x.nl && t.x == 0xFFFFFFFFu) zs = true;
-          xs[j] = ge(u[j], t.x) + ge(u[j], t.y) + ge(u[j], t.z);
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t t = tv[byte_of(wm, j)];
+            if (ARMED && j < nl && t == 0xFFFFFFFFu) zs = true;
+            xs[j] = ge(u[j], t);
+          }
+        } else if (o.k1[i] == 2) {
+          const uint2* t2 = reinterpret_cast<const uint2*>(tv);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint2 t = t2[byte_of(wm, j)];
+            if (ARMED && j < nl && t.x == 0xFFFFFFFFu) zs = true;
+            xs[j] = ge(u[j], t.x) + ge(u[j], t.y);
+          }
+        } else {
+          const uint4* t4 = reinterpret_cast<const uint4*>(tv);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 t = t4[byte_of(wm, j)];  // card 4: three thresholds + padding
+            if (ARMED && j < nl && t.x == 0xFFFFFFFFu) zs = true;
+            xs[j] = ge(u[j], t.x) + ge(u[j], t.y) + ge(u[j], t.z);
+          }
         }
+        const uint32_t x4 = __byte_perm(__byte_perm(xs[0], xs[1], 0x0040), __byte_perm(xs[2], xs[3], 0x0040), 0x5410);
+        w[g] = (w[g] & o.clr[i]) | (x4 << o.sh[i]);
       }
-      const uint32_t x4 = xs[0] | (xs[1] << 8) | (xs[2] << 16) | (xs[3] << 24);
-      w = (w & x.CLR[i]) | (x4 << x.SH[i]);
     }
-    w &= x.valid4;
-    x.row[s] = w;
-    if (x.counts && c < x.num_real) {
-      if (x.nl == 4) {
+    const bool tally = counts && c < num_real;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x.hist8[(byte_of(w, j) << 8) + x.slot] += 1;
-      } else {
-        for (int j = 0; j < x.nl; ++j) x.hist8[(byte_of(w, j) << 8) + x.slot] += 1;
+    for (int g = 0; g < QG; ++g) {
+      if (g > qs.last) break;  // aliases: nothing to store or count
+      const bool full = g < qs.last || qs.last_nl == 4;
+      const uint32_t wg = full ? w[g] : (w[g] & qs.last_valid);
+      rows[g * qs.ld + s] = wg;
+      if (tally) {
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) hist_inc(hist_a + (byte_of(wg, j) << 8));
+        } else {
+          for (int j = 0; j < qs.last_nl; ++j) hist_inc(hist_a + (byte_of(wg, j) << 8));
+        }
       }
     }
   }
   return zs;
 }
 
-// The sweep.  Grid (x: slots, y: replica quad q).  A thread owns lane word
-// (q, s); per latent variable one Philox4x32 call gives the quad's 4
-// uniforms, each lane does one table lookup and compare, and the 4 new
-// states are inserted with one byte-SIMD mask/or.
-template <int N, bool FUSE>
-__global__ void __launch_bounds__(SG_THREADS, 4)
-k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint8_t* __restrict__ pattern,
-              const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes, int lane_ld, int cases, int num_real,
-              int m, int64_t case_base, uint64_t key, const uint64_t* __restrict__ key_dev,
-              const int32_t* __restrict__ jcell, int cells, unsigned long long* __restrict__ counts,
-              const uint32_t* __restrict__ zs_flag, const int8_t* __restrict__ obs, int ld_obs, int32_t* err,
-              const sg_net fnet, const FinishArgs fin, unsigned int* done) {
+// The sweep.  Grid (x: slot blocks, y: quad groups of QG quads).  A thread
+// owns the QG lane words of a slot (QG x 4 replicas of one case).
+template <int N, int QG>
+__global__ void __launch_bounds__(SG_THREADS, QG <= 2 ? 4 : 3)
+k_small_sweep(const sg_small sp, const SmallOrd o, const uint32_t* __restrict__ stab_g,
+              const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes,
+              int lane_ld, int cases, int num_real, int m, int64_t case_base, uint64_t key,
+              const uint64_t* __restrict__ key_dev, const int32_t* __restrict__ jcell, int cells,
+              unsigned long long* __restrict__ counts, const uint32_t* __restrict__ zs_flag,
+              const int8_t* __restrict__ obs, int ld_obs, int32_t* err) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* stab = reinterpret_cast<uint32_t*>(smem);
   uint8_t* hist8 = smem + ((sp.tab_words * 4 + 15) & ~15);
   uint32_t* cellacc = reinterpret_cast<uint32_t*>(hist8 + (SG_THREADS << sp.bits));
   const int tid = threadIdx.x;
+  const int Q = (m + 3) >> 2;
+  const int q0 = blockIdx.y * QG;
+  const int last = min(QG - 1, Q - 1 - q0);
   for (int i = tid; i < sp.tab_words; i += SG_THREADS) stab[i] = __ldg(stab_g + i);
   if (counts) {
     uint32_t* h32 = reinterpret_cast<uint32_t*>(hist8);
@@ -268,32 +310,21 @@ k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint
     for (int i = tid; i < cells; i += SG_THREADS) cellacc[i] = 0;
   }
   const bool armed = zs_flag && __ldg(zs_flag) != 0u;
-  SmallCtx<N> x;
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const int v = sp.order[i];
-    x.VAR[i] = v;
-    x.SH[i] = sp.off[v];
-    x.K1[i] = sp.card[v] - 1;
-    x.MSK[i] = sp.mbmask[v] * 0x01010101u;
-    x.CLR[i] = ~((((1u << sp.width[v]) - 1u) << sp.off[v]) * 0x01010101u);
-    x.TV[i] = stab + sp.toff[v];
-  }
-  x.q = blockIdx.y;
-  x.nl = min(4, m - 4 * x.q);  // real replicas in this quad
-  x.valid4 = x.nl >= 4 ? 0xFFFFFFFFu : ((1u << (8 * x.nl)) - 1u);
-  x.row = lanes + int64_t(x.q) * lane_ld;
-  x.pattern = pattern;
-  x.case_id = case_id;
-  x.hist8 = hist8;
-  x.cases = cases;
-  x.num_real = num_real;
-  x.slot = ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
-  x.case_base = case_base;
-  x.key = key_dev ? __ldg(key_dev) : key;
-  x.counts = counts != nullptr;
+  QuadSet qs;
+  qs.row0 = uint32_t(q0) * uint32_t(lane_ld);
+  qs.ld = uint32_t(lane_ld);
+  qs.q0w = uint32_t(q0) << 16;
+  qs.last = last;
+  qs.last_nl = min(4, m - 4 * (q0 + qs.last));
+  qs.last_valid = qs.last_nl >= 4 ? 0xFFFFFFFFu : ((1u << (8 * qs.last_nl)) - 1u);
+  const int slot = ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
+  const uint32_t hist_a = uint32_t(__cvta_generic_to_shared(hist8)) + uint32_t(slot);
+  const FastKey fk = fast_key(key_dev ? __ldg(key_dev) : key);
   __syncthreads();
-  const bool zs = armed ? small_units<N, true>(x) : small_units<N, false>(x);
+  const bool zs = armed ? small_units<N, QG, true>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real,
+                                                   case_base, fk, counts != nullptr)
+                        : small_units<N, QG, false>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real,
+                                                    case_base, fk, counts != nullptr);
   if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
   if (obs) {  // the minibatch's range check (sampler.py:429-430), spread over the whole grid
     const int chunks = (cases + 15) >> 4;
@@ -324,28 +355,16 @@ k_small_sweep(const sg_small sp, const uint32_t* __restrict__ stab_g, const uint
     int sum = __dp4a(int(hrow[lane_id]), 0x01010101, 0);
     sum = __dp4a(int(hrow[lane_id + 32]), 0x01010101, sum);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int o2 = 16; o2; o2 >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o2);
     if (sum && lane_id < sp.n) atomicAdd(cellacc + __ldg(jcell + J * sp.n + lane_id), uint32_t(sum));
   }
   __syncthreads();
   for (int cell = tid; cell < cells; cell += SG_THREADS)
     if (cellacc[cell]) atomicAdd(counts + cell, (unsigned long long)cellacc[cell]);
-  if (FUSE) {
-    // the last CTA to finish runs the step tail on the complete counts
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (tid == 0) *done = 0u;  // re-armed for the next launch
-    step_finish_body(fnet, fin, smem, SG_THREADS);
-  }
 }
 
 // Resident CTAs of one sweep instance on the whole device (one full wave).
-template <int N, bool FUSE>
+template <int N, int QG>
 static int resident_ctas(size_t smem) {
   static size_t cached_smem = ~size_t(0);
   static int cached = 0;
@@ -353,46 +372,64 @@ static int resident_ctas(size_t smem) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_sweep<N, FUSE>, SG_THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_sweep<N, QG>, SG_THREADS, smem);
     cached = sms * std::max(1, per_sm);
     cached_smem = smem;
   }
   return cached;
 }
 
-// One wave of CTAs split over the Q replica quads (every CTA strides over the
-// pattern-sorted slots, so the units' cost is balanced across CTAs), but at
-// least enough CTAs that no thread's byte counters see more than 63 units.
-template <int N, bool FUSE>
-static dim3 small_grid(int cases, int Q, size_t smem) {
-  const int64_t need = (int64_t(cases) + int64_t(SG_THREADS) * 63 - 1) / (int64_t(SG_THREADS) * 63);
-  const int64_t fill = (int64_t(cases) + SG_THREADS - 1) / SG_THREADS;
-  const int64_t want = std::max<int64_t>(resident_ctas<N, FUSE>(smem) / Q, need);
-  return dim3(unsigned(std::max<int64_t>(1, std::min<int64_t>(want, fill))), unsigned(Q));
+// Quad groups: QG = the quads one thread carries (<= 4, registers), groups =
+// ceil(Q / QG) grid rows.
+static void quad_groups(int m, int* qg, int* groups) {
+  const int Q = (m + 3) / 4;
+  *groups = (Q + 3) / 4;
+  *qg = (Q + *groups - 1) / *groups;
 }
 
-template <int N, bool FUSE>
-static void launch_small(const sg_small& sp, int Q, size_t smem, cudaStream_t st, const uint32_t* stab,
-                         const uint8_t* pattern, const int32_t* case_id, uint32_t* lanes, int lane_ld, int cases,
-                         int num_real, int m, int64_t case_base, uint64_t key, const uint64_t* key_dev,
-                         const int32_t* jcell, int cells, uint64_t* counts, const uint32_t* zs_flag,
-                         const int8_t* obs, int ld_obs, int32_t* err, const sg_net& fnet, const FinishArgs& fin,
-                         unsigned int* done) {
+template <int N, int QG>
+static void launch_small(const sg_small& sp, const SmallOrd& o, int groups, size_t smem, cudaStream_t st,
+                         const uint32_t* stab, const uint8_t* pattern, const int32_t* case_id, uint32_t* lanes,
+                         int lane_ld, int cases, int num_real, int m, int64_t case_base, uint64_t key,
+                         const uint64_t* key_dev, const int32_t* jcell, int cells, uint64_t* counts,
+                         const uint32_t* zs_flag, const int8_t* obs, int ld_obs, int32_t* err) {
   static size_t configured = 0;  // raise the opt-in once (keeps graph capture free of attribute calls)
   if (smem > configured) {
-    cudaFuncSetAttribute(k_small_sweep<N, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_small_sweep<N, QG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured = smem;
   }
-  const dim3 grid = small_grid<N, FUSE>(cases, Q, smem);
-  k_small_sweep<N, FUSE><<<grid, SG_THREADS, smem, st>>>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real,
-                                                         m, case_base, key, key_dev, jcell, cells,
-                                                         reinterpret_cast<unsigned long long*>(counts), zs_flag, obs,
-                                                         ld_obs, err, fnet, fin, done);
+  // one wave over the quad groups (every CTA strides over the pattern-sorted
+  // slots, so unit costs balance), but enough CTAs that no thread's byte
+  // counters see more than 255 increments: <= 255 / (4 QG) slots per thread
+  const int64_t per_thread = 255 / (4 * QG);
+  const int64_t need = (int64_t(cases) + SG_THREADS * per_thread - 1) / (SG_THREADS * per_thread);
+  const int64_t fill = (int64_t(cases) + SG_THREADS - 1) / SG_THREADS;
+  const int64_t want = std::max<int64_t>(resident_ctas<N, QG>(smem) / groups, need);
+  const dim3 grid(unsigned(std::max<int64_t>(1, std::min<int64_t>(want, fill))), unsigned(groups));
+  k_small_sweep<N, QG><<<grid, SG_THREADS, smem, st>>>(sp, o, stab, pattern, case_id, lanes, lane_ld, cases,
+                                                       num_real, m, case_base, key, key_dev, jcell, cells,
+                                                       reinterpret_cast<unsigned long long*>(counts), zs_flag, obs,
+                                                       ld_obs, err);
 }
 
 static size_t small_smem(const sg_small& sp, int cells) {
   return size_t((sp.tab_words * 4 + 15) & ~15) + (size_t(SG_THREADS) << sp.bits) + size_t(cells) * 4 + 16;
 }
+
+static SmallOrd small_ord(const sg_small& sp) {
+  SmallOrd o{};
+  for (int i = 0; i < sp.n; ++i) {
+    const int v = sp.order[i];
+    o.var[i] = uint32_t(v);
+    o.sh[i] = uint32_t(sp.off[v]);
+    o.k1[i] = uint32_t(sp.card[v] - 1);
+    o.msk[i] = sp.mbmask[v] * 0x01010101u;
+    o.clr[i] = ~((((1u << sp.width[v]) - 1u) << sp.off[v]) * 0x01010101u);
+    o.toff[i] = uint32_t(sp.toff[v]);
+  }
+  return o;
+}
+
 
 }  // namespace sg
 
@@ -414,7 +451,9 @@ extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t l
   using namespace sg;
   SG_REQUIRE(sp && obs && scratch && pattern && case_id && lanes, "sg_small_prepare: null argument");
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV, "sg_small_prepare: bad plan");
-  SG_REQUIRE(m >= 1 && lane_ld_ok(lane_ld, cases), "sg_small_prepare: lane_ld %d < cases %d", lane_ld, cases);
+  SG_REQUIRE(m >= 1 && m <= 32 && lane_ld_ok(lane_ld, cases), "sg_small_prepare: m %d / lane_ld %d < cases %d", m,
+             lane_ld, cases);
+  SG_REQUIRE(fast_cases_ok(case_base, cases), "sg_small_prepare: global case index beyond 2^32");
   if (cases == 0) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   int* hist = scratch;                                                  // [SMALL_PATTERNS]
@@ -429,48 +468,45 @@ extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t l
 }
 
 namespace sg {
-template <bool FUSE>
 static int small_sweep_impl(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern, const int32_t* case_id,
                             uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real, int32_t m,
                             int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell,
                             int32_t cells, uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs,
-                            int32_t ld_obs, int32_t* err, void* stream, const sg_net* fnet, const sg_finish* f,
-                            uint32_t* done) {
+                            int32_t ld_obs, int32_t* err, void* stream) {
   SG_REQUIRE(sp && stab && pattern && case_id && lanes && err, "sg_small_sweep: null argument");
   if (obs)
     SG_REQUIRE(ld_obs % 16 == 0 && (reinterpret_cast<uintptr_t>(obs) & 15) == 0 && ld_obs >= cases,
                "sg_small_sweep: obs rows must be 16-byte aligned");
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV && sp->bits <= SG_SMALL_MAXBITS, "sg_small_sweep: bad plan");
   SG_REQUIRE(!counts || jcell, "sg_small_sweep: joint cell map required for the tally");
-  SG_REQUIRE(m >= 1 && lane_ld_ok(lane_ld, cases), "sg_small_sweep: lane_ld %d < cases %d", lane_ld, cases);
+  SG_REQUIRE(m >= 1 && m <= 32 && lane_ld_ok(lane_ld, cases), "sg_small_sweep: m %d / lane_ld %d < cases %d", m,
+             lane_ld, cases);
+  SG_REQUIRE(fast_cases_ok(case_base, cases), "sg_small_sweep: global case index beyond 2^32");
+  SG_REQUIRE(int64_t((m + 3) / 4) * lane_ld <= (int64_t(1) << 32), "sg_small_sweep: lane block beyond 2^32 words");
   for (int v = 0; v < sp->n; ++v)
-    SG_REQUIRE(sp->card[v] <= 4 && sp->tstride[v] >= sp->card[v] - 1 && sp->toff[v] % sp->tstride[v] == 0,
-               "sg_small_sweep: variable %d needs card <= 4 and an aligned table", v);
-  if (FUSE) {
-    SG_REQUIRE(fnet && f && done && counts, "sg_small_step: network, finish args, counter and counts required");
-    if (cases == 0 || !finish_fits(*fnet, sp)) {  // nothing to sweep / model too large to fuse: two launches
-      const int st = small_sweep_impl<false>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m,
-                                             case_base, key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs,
-                                             err, stream, nullptr, nullptr, nullptr);
-      return st ? st : sg_step_finish(fnet, sp, f, stream);
-    }
-  }
+    SG_REQUIRE(sp->card[v] >= 2 && sp->card[v] <= 4 && sp->tstride[v] >= sp->card[v] - 1 &&
+                   sp->toff[v] % sp->tstride[v] == 0,
+               "sg_small_sweep: variable %d needs 2 <= card <= 4 and an aligned table", v);
   if (cases == 0) return SG_OK;
-  size_t smem = small_smem(*sp, cells);
-  FinishArgs fin{};
-  sg_net fn{};
-  if (FUSE) {
-    fin = make_finish_args(f, sp);
-    fn = *fnet;
-    smem = std::max(smem, finish_smem(*fnet));
-  }
-  const int Q = (m + 3) / 4;
+  const size_t smem = small_smem(*sp, cells);
+  const SmallOrd o = small_ord(*sp);
+  int qg = 1, groups = 1;
+  quad_groups(m, &qg, &groups);
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t* lw = reinterpret_cast<uint32_t*>(lanes);
-#define SG_SMALL_CASE(NV)                                                                                     \
-  case NV:                                                                                                    \
-    launch_small<NV, FUSE>(*sp, Q, smem, st, stab, pattern, case_id, lw, lane_ld, cases, num_real, m, case_base, \
-                     key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err, fn, fin, done);           \
+#define SG_SMALL_QG(NV, G)                                                                                       \
+  case G:                                                                                                        \
+    launch_small<NV, G>(*sp, o, groups, smem, st, stab, pattern, case_id, lw, lane_ld, cases, num_real, m,      \
+                        case_base, key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err);               \
+    break;
+#define SG_SMALL_CASE(NV)    \
+  case NV:                   \
+    switch (qg) {            \
+      SG_SMALL_QG(NV, 1)     \
+      SG_SMALL_QG(NV, 2)     \
+      SG_SMALL_QG(NV, 3)     \
+      SG_SMALL_QG(NV, 4)     \
+    }                        \
     break;
   switch (sp->n) {
     SG_SMALL_CASE(1)
@@ -485,7 +521,8 @@ static int small_sweep_impl(const sg_small* sp, const uint32_t* stab, const uint
       return SG_EINVAL;
   }
 #undef SG_SMALL_CASE
-  return check_launch(FUSE ? "sg_small_step" : "sg_small_sweep");
+#undef SG_SMALL_QG
+  return check_launch("sg_small_sweep");
 }
 }  // namespace sg
 
@@ -494,20 +531,10 @@ extern "C" int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const ui
                               int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell,
                               int32_t cells, uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs,
                               int32_t ld_obs, int32_t* err, void* stream) {
-  return sg::small_sweep_impl<false>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m, case_base, key,
-                                     key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err, stream, nullptr, nullptr,
-                                     nullptr);
+  return sg::small_sweep_impl(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m, case_base, key, key_dev,
+                              jcell, cells, counts, zs_flag, obs, ld_obs, err, stream);
 }
 
-extern "C" int sg_small_step(const sg_small* sp, const uint32_t* stab, const uint8_t* pattern, const int32_t* case_id,
-                             uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real, int32_t m,
-                             int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell,
-                             int32_t cells, uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs,
-                             int32_t ld_obs, int32_t* err, const sg_net* net, const sg_finish* f, uint32_t* done,
-                             void* stream) {
-  return sg::small_sweep_impl<true>(sp, stab, pattern, case_id, lanes, lane_ld, cases, num_real, m, case_base, key,
-                                    key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err, stream, net, f, done);
-}
 
 extern "C" int sg_small_import(const sg_small* sp, const sg_batch* batch, const int32_t* case_id, uint8_t* lanes,
                                int32_t lane_ld, void* stream) {

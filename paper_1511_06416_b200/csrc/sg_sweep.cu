@@ -593,6 +593,9 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
              rng_mode);
   if (rng_mode != SG_RNG_FAST)
     SG_REQUIRE(batch->rank && batch->nmiss, "sg_sweep: rank/nmiss required for this rng mode");
+  else
+    SG_REQUIRE(fast_cases_ok(batch->case_base, batch->cases) && batch->m <= 4 * 4096,
+               "sg_sweep: FAST counters need global cases < 2^32 and m <= 16384");
   if (rng_mode == SG_RNG_NUMPY) SG_REQUIRE(keys, "sg_sweep: numpy keys required");
   if (rng_mode == SG_RNG_INJECTED) SG_REQUIRE(uniforms && inj_off, "sg_sweep: uniforms required");
   if (net->table_entries > 0) SG_REQUIRE(ptab && ftab, "sg_sweep: tables required");

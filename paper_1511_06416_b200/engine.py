@@ -116,12 +116,6 @@ class Engine:
         if self.use_small:
             self.stab = torch.empty(max(1, self.pack.small.tab_words), dtype=torch.int32, device=d)
         self.tables_fresh = False  # conditional tables reflect self.cpt
-        # sg_small_step: packed sweep + step tail in one launch (needs no count exchange
-        # between them).  Off by default: the tail then runs in one 256-thread CTA of a
-        # 64-register kernel, which measured slower on B200 than the separate
-        # 512-thread sg_step_finish launch (bench.py --fuse, profiles/README.md).
-        self.fuse_step = False
-        self.done = torch.zeros(1, dtype=torch.int32, device=d)  # last-CTA counter of sg_small_step
 
     # ------------------------------------------------------------ helpers
     def _upload_keys(self, seed: int, label: str, context: tuple) -> None:
@@ -231,7 +225,6 @@ class Engine:
         key = 0 if cfg.map_estimate else derive_seed(derive_seed(cfg.seed, "cpt_update", pass_index, mb.index),
                                                      "sample_cpts")
         f = self.finish_args(new_counts, prev, key)
-        fused = False
         for sw in range(S):
             sweep_seed = derive_seed(cfg.seed, "sweep", pass_index, mb.index, sw)
             last = sw == S - 1
@@ -242,11 +235,7 @@ class Engine:
                         self.pack.small_jcell.data_ptr(), self.pack.cells, counts_ptr,
                         self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"],
                         obs.data_ptr() if last else None, ld, self.err.ptr)
-                if last and self.fuse_step and timing is None:
-                    _lib.call("sg_small_step", *args, self.pack.ref, f, self.done.data_ptr(), s)
-                    fused = True
-                else:
-                    _lib.call("sg_small_sweep", *args, s)
+                _lib.call("sg_small_sweep", *args, s)
             elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
                 _lib.call("sg_sweep", self.pack.ref, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
@@ -259,10 +248,9 @@ class Engine:
         if timing is not None:
             ev1.record()
             timing.append((ev0, ev1, S))
-        if not fused:
-            if self.comm is not None:
-                self.comm(new_counts)
-            _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
+        if self.comm is not None:
+            self.comm(new_counts)
+        _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
         if moving:
             self.prev_counts[mb.index] = new_counts
             self.latent[mb.index] = db
@@ -443,7 +431,6 @@ class StepGraphs:
         f = eng.finish_args(new, prev, 0, key_dev=cur + 8 * S, clear=prev,
                             cursor=(self.table, self.idx, self.kps, self.cur))
         self._finish_args.append(f)
-        fuse = eng.fuse_step
         for sw in range(S):
             last = sw == S - 1
             counts_ptr = new.data_ptr() if last else None
@@ -453,18 +440,14 @@ class StepGraphs:
                         eng.pack.small_jcell.data_ptr(), eng.pack.cells, counts_ptr,
                         eng.ftab.data_ptr() + 4 * eng.pack.layout.scalars["ftab_size"],
                         obs.data_ptr() if last else None, self.ld, eng.err.ptr)
-                if fuse and last:  # sweep + tally + step tail in one launch
-                    _lib.call("sg_small_step", *args, eng.pack.ref, f, eng.done.data_ptr(), s)
-                else:
-                    _lib.call("sg_small_sweep", *args, s)
+                _lib.call("sg_small_sweep", *args, s)
             else:
                 _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
                           eng.err.ptr, s)
-        if not fuse:
-            if eng.comm is not None:
-                eng.comm(new)
-            _lib.call("sg_step_finish", eng.pack.ref, eng.small_ptr, f, s)
+        if eng.comm is not None:
+            eng.comm(new)
+        _lib.call("sg_step_finish", eng.pack.ref, eng.small_ptr, f, s)
 
     def step(self, mb=None) -> None:
         """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
@@ -502,8 +485,6 @@ class StepGraphs:
     def launches_per_step(self) -> int:
         eng = self.eng
         one_cta = eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
-        if eng.fuse_step and one_cta:  # the last packed sweep runs the step tail in its last CTA
-            return eng.cfg.sweeps_per_minibatch
         check = 0 if eng.use_small else 1  # the packed sweep folds in the range check
         return check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
 

@@ -218,7 +218,7 @@ def small_plan(net: Network, lay: NetLayout):
     if n == 0 or n > SMALL_MAXV:
         return None
     cards = [int(k) for k in net.cardinalities]
-    if max(cards) > 4:  # one aligned LDS / LDS.64 / LDS.128 of thresholds per draw
+    if max(cards) > 4 or min(cards) < 2:  # one aligned LDS / LDS.64 / LDS.128 of 1..3 thresholds per draw
         return None
     width = [max(1, (k - 1).bit_length()) for k in cards]
     bits = sum(width)

@@ -112,10 +112,9 @@ def test_packed_only_tables_equal_two_stage_build(koller, map_estimate):
         assert int(a.ftab[-1]) == int(ftab[-1])
 
 
-@pytest.mark.parametrize("fuse", [True, False])
-def test_graph_host_uploads_equal_eager_visits(koller, fuse):
-    """Graph replays fed host minibatches (double-buffered copy-stream uploads),
-    with and without the fused step tail, match eager visits bit for bit."""
+def test_graph_host_uploads_equal_eager_visits(koller):
+    """Graph replays fed host minibatches (double-buffered copy-stream uploads)
+    match eager visits bit for bit."""
     from paper_1511_06416_b200.engine import Engine, StepGraphs
 
     net, truth = koller
@@ -127,9 +126,7 @@ def test_graph_host_uploads_equal_eager_visits(koller, fuse):
     host.copy_(obs[:, :cases])
     hmb = sg.Minibatch(index=0, values=host, weights=np.ones(cases), num_real=cases)
     a = Engine(net, cfg)
-    a.fuse_step = False
     b = Engine(net, cfg)
-    b.fuse_step = fuse
     for p in range(7):
         a.visit(mb, p, m)
     b.visit(mb, 0, m)
