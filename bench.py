@@ -217,14 +217,14 @@ def our_arm(args) -> None:
     eng = Engine(net, cfg, case_base=rank * CASES, comm=comm)
     mb = next(iter(sg.DeviceSource(obs, CASES, CASES)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    flush_rd = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+    flush_rd = torch.ones(32 << 20, dtype=torch.int64, device="cuda")  # 256 MB
 
     def flush_l2(k):
         # evict the working set: write 256 MB (> 126 MB L2), then read another
         # 256 MB so the flush's own dirty lines are written back here, outside
         # the timed events, not during the next step
         flush.fill_(k & 0xFF)
-        flush_rd.sum(dtype=torch.int64)
+        flush_rd.sum()
 
 
     # eager warm-up visits: the first one builds the resident lanes
