@@ -130,6 +130,23 @@ def main():
     dd = mask(forward_sample(big, cp, 150, seed=71), 0.6, seed=72).to_dense()
     sweep_fixture("bigcard", big, cp, dd, 2, 73, 74)
 
+    # --- larger shapes of BASELINE configs C3/C4 (generators: paper_1511_06416_b200/netgen.py)
+    sys.path.insert(0, str(OUT.parents[1]))
+    from paper_1511_06416_b200 import netgen
+
+    def ref_net(n):
+        return build_network(list(n.cardinalities), [(p, c) for c in range(n.num_vars) for p in n.parents[c]])
+
+    dag = ref_net(netgen.random_dag_network(120, max_parents=4, min_card=2, max_card=4, seed=11))
+    cp = random_cpts(dag, np.random.default_rng(12), concentration=0.8)
+    dd = mask(forward_sample(dag, cp, 160, seed=13), 0.3, seed=14).to_dense()
+    sweep_fixture("dag120", dag, cp, dd, 2, 15, 16)
+    mooc = ref_net(netgen.mooc_network(10, 60, seed=3))
+    cp = random_cpts(mooc, np.random.default_rng(4), concentration=1.0)
+    dd = mask(forward_sample(mooc, cp, 150, seed=5), 0.7, seed=6).to_dense()
+    dd[:10] = -1  # concepts are never observed
+    sweep_fixture("mooc", mooc, cp, dd, 5, 7, 8)
+
     # --- init_latent
     mb = pad_block(0, dense[:, :64].astype(np.int32), 64)
     batch = replicate_minibatch(mb, 4)

@@ -30,5 +30,5 @@ def edges(d: dict) -> list:
     return [tuple(int(x) for x in e) for e in d["edges"]]
 
 
-SWEEPS = ["koller_m3", "koller_pad", "rand0", "rand1", "rand2", "rand3", "bigcard"]
+SWEEPS = ["koller_m3", "koller_pad", "rand0", "rand1", "rand2", "rand3", "bigcard", "dag120", "mooc"]
 RUNS_MAP = ["map_moving", "map_exp", "map_sweeps2"]

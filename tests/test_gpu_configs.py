@@ -1,0 +1,130 @@
+"""Parity at the network shapes of BASELINE configs C3 (MOOC-shaped) and C4
+(random DAG, 1000 nodes, in-degree <= 4, cards 2-4, 30 % missing).
+
+* numpy-RNG mode, bit-exact against the oracle (which tests/golden pins to the
+  reference, including the 120-node DAG and MOOC fixtures): one sweep of the
+  full-size networks on a case slice, and a MAP run over several minibatches
+  and passes on the 1000-node DAG -- the generic kernel, the direct
+  (untabulated) draw for large blankets and the multi-launch step tail of
+  models above the single-CTA size.
+* FAST mode at larger case counts: size-independent properties (tally mass,
+  observed cells untouched, CPT rows normalised).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+sg = pytest.importorskip("paper_1511_06416_b200")
+from paper_1511_06416_b200 import netgen  # noqa: E402
+
+
+def _oracle_net(net):
+    return O.make_net(list(net.cardinalities), [(p, c) for c in range(net.num_vars) for p in net.parents[c]])
+
+
+@pytest.fixture(scope="module")
+def c4():
+    net = netgen.random_dag_network(1000, max_parents=4, min_card=2, max_card=4, seed=4)
+    truth = netgen.dirichlet_cpts(net, 1.0, seed=5)
+    return net, truth
+
+
+@pytest.fixture(scope="module")
+def c3():
+    net = netgen.mooc_network(15, 319, seed=3)
+    truth = netgen.dirichlet_cpts(net, 1.0, seed=6)
+    return net, truth
+
+
+def _sweep_vs_oracle(net, cpts, dense, m, init_seed, sweep_seed):
+    onet = _oracle_net(net)
+    values, missing = O.replicate(dense, m)
+    O.init_latent(onet, values, missing, init_seed, 0, 0)
+    batch = sg.ReplicatedBatch(m=m, base_size=dense.shape[1], values=values.copy(),
+                               lane_weights=np.ones(values.shape[1]), missing_lanes=[x.copy() for x in missing])
+    counts = sg.sweep(net, sg.color_graph(sg.moralize(net)), cpts, batch, sweep_seed)
+    want = O.sweep(onet, O.greedy_coloring(onet), cpts.tables, values, missing, np.ones(values.shape[1]), sweep_seed)
+    np.testing.assert_array_equal(batch.values, values)
+    for a, b in zip(counts.tables, want):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_c4_colouring_matches_oracle(c4):
+    net, _ = c4
+    groups = sg.color_graph(sg.moralize(net)).groups
+    assert [list(g) for g in groups] == O.greedy_coloring(_oracle_net(net))
+
+
+def test_c4_sweep_bit_exact(c4):
+    net, truth = c4
+    obs = sg.forward_sample_device(net, truth, 1500, seed=104, hide_fraction=0.3, mask_seed=204)
+    dense = obs[:, :1500].cpu().numpy().astype(np.int32)
+    _sweep_vs_oracle(net, truth, dense, 1, 304, 9001)
+
+
+def test_c3_sweep_bit_exact(c3):
+    net, truth = c3
+    obs = netgen.mooc_observations(net, truth, 4000, 15, density=0.022, seed=103)
+    dense = obs[:, :4000].cpu().numpy().astype(np.int32)
+    assert (dense[:15] < 0).all()
+    _sweep_vs_oracle(net, truth, dense, 5, 303, 9002)
+
+
+def test_c4_map_run_bit_exact(c4):
+    """Three minibatches (last one padded), two passes, moving sum, posterior
+    mean: the 1000-node model (72k-cell class) exceeds the single-CTA tail, so
+    this exercises the multi-launch step tail."""
+    net, truth = c4
+    cases = 1300
+    obs = sg.forward_sample_device(net, truth, cases, seed=110, hide_fraction=0.3, mask_seed=210)
+    dense = obs[:, :cases].cpu().numpy().astype(np.int32)
+    cfg = sg.SamplerConfig(same_m=1, minibatch_size=500, num_passes=2, map_estimate=True, seed=310)
+    cpts, trace = sg.run(net, sg.DataMatrix.from_dense(dense), cfg, truth=truth)
+    res = O.run(_oracle_net(net), dense, same_m=1, minibatch_size=500, num_passes=2, map_estimate=True, seed=310,
+                truth=truth.tables)
+    for a, b in zip(cpts.tables, res.cpts):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal([r.kl_avg for r in trace.records], res.kl)
+
+
+def _fast_properties(net, obs, cases, m, mb_size):
+    from paper_1511_06416_b200.engine import Engine
+
+    cfg = sg.SamplerConfig(same_m=m, minibatch_size=mb_size, num_passes=1, seed=7, rng="fast")
+    eng = Engine(net, cfg)
+    src = sg.DeviceSource(obs, cases, mb_size)
+    for mb in src:
+        eng.visit(mb, 0, m)
+        torch.cuda.synchronize()
+        counts = eng.prev_counts[mb.index].cpu().numpy()
+        off = eng.pack.layout.cpt_off
+        for v in range(net.num_vars):
+            assert counts[off[v]:off[v + 1]].sum() == m * mb.num_real
+        st = eng.lane_states(mb.index)[:, :, :mb.num_real]
+        o = mb.values[:, :mb.num_real]
+        lat = st < 0
+        assert bool(((o >= 0).unsqueeze(1) == ~lat).all())
+        assert bool(((st & 0x7F) == o.clamp(min=0).unsqueeze(1))[~lat].all())
+    assert eng.err.read() == 0
+    cpt = eng.current_cpts()
+    for t in cpt.tables:
+        np.testing.assert_allclose(t.sum(axis=1), 1.0, atol=1e-12)
+
+
+def test_c3_fast_mode_properties(c3):
+    net, truth = c3
+    cases = 131_010  # 4,367 students x 30
+    obs = netgen.mooc_observations(net, truth, cases, 15, density=0.022, seed=113)
+    _fast_properties(net, obs, cases, 5, 65_536)
+
+
+def test_c4_fast_mode_properties(c4):
+    net, truth = c4
+    cases = 200_000
+    obs = sg.forward_sample_device(net, truth, cases, seed=114, hide_fraction=0.3, mask_seed=214)
+    _fast_properties(net, obs, cases, 1, 100_000)

@@ -63,7 +63,9 @@ def test_gibbs_pass_leaves_counts_alone_and_matches():
 
 def test_init_latent_bit_exact():
     d = load("init_koller")
-    net, _ = sg.io.load_network_file(sg.io.bundled_network_path("koller"))
+    from paper_1511_06416_b200.io import bundled_network_path, load_network_file
+
+    net, _ = load_network_file(bundled_network_path("koller"))
     mb = sg.pad_block(0, d["dense"].astype(np.int32), d["dense"].shape[1])
     batch = sg.replicate_minibatch(mb, int(d["m"]))
     sg.init_latent(net, batch, int(d["seed"]), *[int(x) for x in d["context"]])
