@@ -1,20 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the SAME Gibbs hot path (BASELINE.json metric: node-samples/s).
 
-Workload (BASELINE.json configs[1], "C2"): Koller student network, 1M cases per
-GPU, 50% of cells hidden, SAME m = 10, one minibatch of 1M cases, moving-sum
-accumulator, sampled Dirichlet CPT update, fast RNG mode.  One step = one
-minibatch visit = conditional tables + fused sweep/tally + accumulator +
-Dirichlet update (+ the count all-reduce when N > 1).  Synthetic data of that
-shape comes from the reference's own forward_sample/mask streams, generated
-on the device.  node-samples per step = n_vars x cases x m (sampler.py:475).
+Default workload (BASELINE.json configs[1], "C2"): Koller student network, 1M
+cases per GPU, 50% of cells hidden, SAME m = 10, one minibatch of 1M cases,
+moving-sum accumulator, sampled Dirichlet CPT update, fast RNG mode.  One step
+= one minibatch visit = sweep/tally + accumulator + Dirichlet update + next
+conditional tables (+ the count all-reduce when N > 1).  Synthetic data of
+that shape comes from the reference's own forward_sample/mask streams,
+generated on the device.  node-samples per step = n_vars x cases x m
+(sampler.py:475).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2|c3|c4]
+
+``--workload c3`` (MOOC-shaped, 334 variables, 131,010 cases, m = 5) and
+``c4`` (random DAG, 1000 nodes, 1.25M cases per GPU = 10M over 8, m = 1, 30%
+missing) measure the generic kernel on the other BASELINE shapes; C2 is the
+headline line.
 
 Timing: per-step CUDA events on the launching stream, L2 flushed (256 MB
-write + 256 MB read) between timed steps, max over ranks.  Prints ONE JSON line on rank 0.
-``--impl reference`` times the CPU oracle (NumPy restatement of the reference,
-oracle/) on the host cores instead.
+write + 256 MB read) between timed steps, max over ranks.  Prints ONE JSON
+line on rank 0.  ``--impl reference`` times the CPU oracle (NumPy restatement
+of the reference, oracle/) on the host cores instead.
 """
 
 from __future__ import annotations
@@ -31,45 +38,104 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-N_VARS = 5
-CASES = 1_000_000
-M = 10
-HIDE = 0.5
-BYTES_PER_NODE_SAMPLE = 1.5  # n*L*(1+f) int8 algorithmic bytes, f = 0.5
 METRIC = "node-samples/sec"
 UNIT = "node-samples/s"
 
 
-def workload_config(n_gpus: int, rng: str) -> dict:
-    return {
-        "workload": "C2: koller-student (5 vars), 1M cases/GPU, 50% hidden, SAME m=10, minibatch=1M, "
-                    "moving-sum, Dirichlet CPT update",
-        "network": "koller-student",
-        "cases_per_gpu": CASES,
-        "global_minibatch": CASES * n_gpus,
-        "m": M,
-        "hidden_fraction": HIDE,
-        "rng": rng,
-        "parallelism": f"case-sharded x{n_gpus}, int64 count all-reduce" if n_gpus > 1 else "single GPU",
-        "l2": "flushed between timed steps (256 MB write + 256 MB read, outside the step events)",
-    }
+class Workload:
+    """One BASELINE configuration: network, data shape, SAME factor."""
+
+    def __init__(self, key, title, cases, m, latent, cpu_cases):
+        self.key, self.title, self.cases, self.m = key, title, cases, m
+        self.latent = latent          # latent fraction f of the cells (SURVEY.md 8(d))
+        self.cpu_cases = cpu_cases    # case slice of one CPU oracle process
+
+    # -- network + generating CPTs (package types)
+    def network(self):
+        if self.key == "c2":
+            from paper_1511_06416_b200.io import bundled_network_path, load_network_file
+
+            return load_network_file(bundled_network_path("koller"))
+        from paper_1511_06416_b200 import netgen
+
+        if self.key == "c3":
+            net = netgen.mooc_network(15, 319, seed=3)
+            return net, netgen.dirichlet_cpts(net, 1.0, seed=6)
+        net = netgen.random_dag_network(1000, max_parents=4, min_card=2, max_card=4, seed=4)
+        return net, netgen.dirichlet_cpts(net, 1.0, seed=5)
+
+    # -- device observations of this rank's shard
+    def observations(self, net, truth, rank):
+        import paper_1511_06416_b200 as sg
+        from paper_1511_06416_b200 import netgen
+
+        base = rank * self.cases
+        if self.key == "c3":
+            return netgen.mooc_observations(net, truth, self.cases, 15, density=0.022, seed=103, case_base=base)
+        hide, seed = (0.5, 100) if self.key == "c2" else (0.3, 104)
+        return sg.forward_sample_device(net, truth, self.cases, seed=seed, hide_fraction=hide, mask_seed=seed + 100,
+                                        case_base=base)
+
+    # -- CPU oracle of the same shape (dense int32, -1 = missing)
+    def oracle_problem(self, cases, slice_id):
+        import numpy as np
+
+        import oracle as O
+
+        if self.key == "c2":
+            net, truth = O.koller()
+            dense = O.mask_dense(O.forward_sample(net, truth, cases, 100 + slice_id), 0.5, 200 + slice_id)
+            return net, dense
+        pnet, ptruth = self.network()
+        net = O.make_net(list(pnet.cardinalities),
+                         [(p, c) for c in range(pnet.num_vars) for p in pnet.parents[c]])
+        dense = O.forward_sample(net, ptruth.tables, cases, 100 + slice_id)
+        rng = np.random.default_rng(200 + slice_id)
+        if self.key == "c3":
+            dense = np.where(rng.random(dense.shape) < 0.022, dense, -1).astype(np.int32)
+            dense[:15] = -1
+        else:
+            dense = np.where(rng.random(dense.shape) < 0.3, -1, dense).astype(np.int32)
+        return net, dense
+
+    def config(self, n_gpus: int, rng: str, n_vars: int) -> dict:
+        return {
+            "workload": self.title, "network": {"c2": "koller-student", "c3": "mooc-shaped",
+                                                "c4": "random-dag-1000"}[self.key],
+            "n_vars": n_vars, "cases_per_gpu": self.cases, "global_minibatch": self.cases * n_gpus, "m": self.m,
+            "latent_fraction": round(self.latent, 4), "rng": rng,
+            "parallelism": f"case-sharded x{n_gpus}, int64 count all-reduce" if n_gpus > 1 else "single GPU",
+            "l2": "flushed between timed steps (256 MB write + 256 MB read, outside the step events)",
+        }
+
+
+WORKLOADS = {
+    "c2": Workload("c2", "C2: koller-student (5 vars), 1M cases/GPU, 50% hidden, SAME m=10, minibatch=1M, "
+                         "moving-sum, Dirichlet CPT update", 1_000_000, 10, 0.5, 100_000),
+    "c3": Workload("c3", "C3: MOOC-shaped (15 latent concepts + 319 questions), 131,010 cases, 2.2% of responses "
+                         "observed, SAME m=5, minibatch=all, moving-sum, Dirichlet CPT update", 131_010, 5, 0.978,
+                   8_000),
+    "c4": Workload("c4", "C4: random DAG, 1000 nodes, in-degree<=4, cards 2-4, 1.25M cases/GPU (10M over 8), "
+                         "30% missing, SAME m=1, minibatch=shard, moving-sum, Dirichlet CPT update", 1_250_000, 1,
+                   0.3, 4_000),
+}
 
 
 # ---------------------------------------------------------------- CPU oracle legs
 
 def _oracle_worker(args):
     """Time oracle steps (sweep + tally + moving sum + Dirichlet) on a case slice."""
-    cases, m, steps, budget_s, slice_id = args
+    key, cases, steps, budget_s, slice_id = args
     import numpy as np
 
     import oracle as O
 
-    net, truth = O.koller()
-    dense = O.mask_dense(O.forward_sample(net, truth, cases, 100 + slice_id), HIDE, 200 + slice_id)
+    wl = WORKLOADS[key]
+    net, dense = wl.oracle_problem(cases, slice_id)
     groups = O.greedy_coloring(net)
     cur = O.init_cpts(net, 300)
     total = [np.zeros((net.rows(v), net.cards[v])) for v in range(net.n)]
-    values, missing = O.replicate(dense, m)
+    values, missing = O.replicate(dense, wl.m)
     weights = np.ones(values.shape[1])
     O.init_latent(net, values, missing, 300, 0, 0)
     prev = None
@@ -87,42 +153,44 @@ def _oracle_worker(args):
     return times
 
 
-def cpu_baseline(budget_s: float = 12.0) -> dict:
-    """Single-core oracle on a 100k-case slice of the workload (rank 0, N=1)."""
-    cases = 100_000
-    times = _oracle_worker((cases, M, 1000, budget_s, 0))
+def cpu_baseline(wl: Workload, n_vars: int, budget_s: float = 12.0) -> dict:
+    """Single-core oracle on a case slice of the workload (rank 0, N=1)."""
+    cases = wl.cpu_cases
+    times = _oracle_worker((wl.key, cases, 1000, budget_s, 0))
     per = statistics.median(times[1:] if len(times) > 2 else times)
-    return {"value": N_VARS * cases * M / per, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"oracle (NumPy restatement of samegibbs) single process, 100k-case slice x m=10, "
+    return {"value": n_vars * cases * wl.m / per, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle (NumPy restatement of samegibbs) single process, {cases}-case slice x m={wl.m}, "
                       f"{len(times)} steps of sweep+tally+moving-sum+Dirichlet, median step {per * 1e3:.1f} ms"}
 
 
-def reference_arm(args) -> None:
+def reference_arm(args, wl: Workload) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import multiprocessing as mp
 
+    n_vars = wl.network()[0].num_vars
     procs = max(1, min(os.cpu_count() or 1, 64))
     total_steps = args.steps + args.warmup
-    # bound the run to roughly a minute of CPU time per process
-    cases = int(min(100_000, max(2_000, 60.0 / total_steps * 12e6 / (N_VARS * M))) // 1000 * 1000)
+    # bound the run to roughly a minute of CPU time per process (~1.2e7 node-samples/s per core)
+    cases = int(min(wl.cpu_cases, max(1_000, 60.0 / total_steps * 12e6 / (n_vars * wl.m))) // 500 * 500)
+    cases = max(cases, 500)
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(procs) as pool:
-        res = pool.map(_oracle_worker, [(cases, M, total_steps, 0, i) for i in range(procs)])
+        res = pool.map(_oracle_worker, [(wl.key, cases, total_steps, 0, i) for i in range(procs)])
     wall = time.perf_counter() - t0
     timed = [r[args.warmup:] for r in res]
     per_step = max(sum(t) for t in timed) / max(1, args.steps)  # slowest worker bounds the aggregate
-    value = procs * N_VARS * cases * M / per_step
+    value = procs * n_vars * cases * wl.m / per_step
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.gpus, "numpy"),
+        "config": wl.config(args.gpus, "numpy", n_vars),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                          "sample": f"{procs} independent single-threaded oracle processes, each on its own "
-                                   f"{cases}-case slice x m=10 (aggregate upper bound; the reference's own "
+                                   f"{cases}-case slice x m={wl.m} (aggregate upper bound; the reference's own "
                                    f"threads knob does not scale), wall {wall:.1f} s"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -180,19 +248,21 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- our arm
 
-def load_traffic():
+def load_traffic(wl: Workload, kernel: str):
     """Per-launch DRAM bytes of the sweep kernel from the committed ncu summary (or None)."""
     for p in sorted((ROOT / "profiles").glob("ncu_sweep_*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
-            if d.get("kernel") and d.get("cases") == CASES and d.get("m") == M:
+            base = d.get("kernel", "").split(" ")[0].split("<")[0]
+            if (d.get("workload", "c2") == wl.key and base == kernel.split(" ")[0]
+                    and d.get("cases") == wl.cases and d.get("m") == wl.m):
                 return d.get("dram_bytes_per_launch"), p.name
         except Exception:  # noqa: BLE001
             continue
     return None, None
 
 
-def our_arm(args) -> None:
+def our_arm(args, wl: Workload) -> None:
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -207,15 +277,16 @@ def our_arm(args) -> None:
     import paper_1511_06416_b200 as sg
     from paper_1511_06416_b200 import _lib
     from paper_1511_06416_b200.engine import Engine, StepGraphs
-    from paper_1511_06416_b200.io import bundled_network_path, load_network_file
 
-    net, truth = load_network_file(bundled_network_path("koller"))
+    CASES, M = wl.cases, wl.m
+    net, truth = wl.network()
+    n_vars = net.num_vars
     cfg = sg.SamplerConfig(same_m=M, minibatch_size=CASES, num_passes=1, seed=300, rng=args.rng)
-    obs = sg.forward_sample_device(net, truth, CASES, seed=100, hide_fraction=HIDE, mask_seed=200,
-                                   case_base=rank * CASES)
+    obs = wl.observations(net, truth, rank)
     comm = (lambda c: dist.all_reduce(c)) if world > 1 else None
     eng = Engine(net, cfg, case_base=rank * CASES, comm=comm)
     mb = next(iter(sg.DeviceSource(obs, CASES, CASES)))
+    latent = float((obs[:, :CASES] < 0).float().mean())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     flush_rd = torch.ones(32 << 20, dtype=torch.int64, device="cuda")  # 256 MB
 
@@ -225,7 +296,6 @@ def our_arm(args) -> None:
         # the timed events, not during the next step
         flush.fill_(k & 0xFF)
         flush_rd.sum()
-
 
     # eager warm-up visits: the first one builds the resident lanes
     for w in range(args.warmup):
@@ -283,11 +353,11 @@ def our_arm(args) -> None:
         t = torch.tensor([ms, sw], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, sw = float(t[0]), float(t[1])
-    node_samples = N_VARS * CASES * M  # per GPU per step
+    node_samples = n_vars * CASES * M  # per GPU per step
     value = world * node_samples / (ms * 1e-3)
 
     # ---- e2e through the public API: pinned host minibatch -> device, step, CPTs back to host
-    host_obs = torch.empty((N_VARS, CASES), dtype=torch.int8, pin_memory=True)
+    host_obs = torch.empty((n_vars, CASES), dtype=torch.int8, pin_memory=True)
     host_obs.copy_(obs[:, :CASES])
     hmb = sg.Minibatch(index=0, values=host_obs, weights=np.ones(CASES), num_real=CASES)
     cpt_host = torch.empty(eng.pack.cells, dtype=torch.float64, pin_memory=True)
@@ -318,29 +388,28 @@ def our_arm(args) -> None:
     e2e_value = world * node_samples / (e2e_ms * 1e-3)
 
     if rank == 0:
-        import json as _json
-
-        peaks = {}
         try:
-            peaks = _json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+            peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
             peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
         except Exception:  # noqa: BLE001
             peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
-        algo_bytes = BYTES_PER_NODE_SAMPLE * node_samples
+        bpns = 1.0 + latent
+        algo_bytes = bpns * node_samples
         achieved = algo_bytes / (sw * 1e-3) / 1e9
-        traffic, traffic_src = load_traffic()
+        kernel = "k_small_sweep (sg_small_sweep)" if eng.use_small else "k_sweep (sg_sweep)"
+        traffic, traffic_src = load_traffic(wl, kernel)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int8 states, u32 draws, f64 CPTs", "data": "synthetic",
-            "config": workload_config(world, args.rng),
+            "config": wl.config(world, args.rng, n_vars),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_small_sweep (sg_small_sweep)" if eng.use_small else "k_sweep (sg_sweep)",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": kernel,
                          "kernel_ms": sw, "algorithmic_bytes_per_launch": algo_bytes,
-                         "bytes_per_node_sample": BYTES_PER_NODE_SAMPLE, "peak_source": peak_src,
-                         "traffic_source": traffic_src, "sweep_share_of_step": sw / ms},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N_VARS * CASES,
+                         "bytes_per_node_sample": bpns, "peak_source": peak_src,
+                         "traffic_source": traffic_src, "sweep_share_of_step": sw / ms,
+                         "limiter": "instruction issue (Philox + table draws), not HBM: see DESIGN.md 6"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n_vars * CASES,
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",
@@ -349,7 +418,7 @@ def our_arm(args) -> None:
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline()
+            out["cpu_baseline"] = cpu_baseline(wl, n_vars)
         print(json.dumps(out))
     if world > 1:
         dist.barrier()
@@ -362,16 +431,18 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--rng", choices=["fast", "numpy"], default="fast")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch each visit eagerly instead of graph replay")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    wl = WORKLOADS[args.workload]
     if args.impl == "reference":
-        reference_arm(args)
+        reference_arm(args, wl)
     else:
-        our_arm(args)
+        our_arm(args, wl)
 
 
 if __name__ == "__main__":

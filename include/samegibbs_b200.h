@@ -109,6 +109,18 @@ typedef struct sg_net {
      card, nmb (-1 = evaluate from CPTs), ftab offset, ptab offset,
      mb_var[SG_DESC_MB], mb_stride[SG_DESC_MB] */
   const int32_t* var_desc;    /* [n][SG_DESC_WORDS] */
+  /* factored draw descriptor of v at fac_desc[fac_start[v]] (the weight
+     product of sampler.py:226-240 with pre-multiplied indices): card, npar,
+     nchl, cpt_off[v]; npar x (parent, stride*card); nchl x (child,
+     cpt_off[child], card[child], vstride*card[child], nq, nq x (other parent,
+     stride*card[child])) */
+  const int32_t* fac_start;   /* [n+1] */
+  const int32_t* fac_desc;
+  /* chunked tally (large models): variables split into runs of consecutive
+     variables whose cells fit a shared-memory histogram (SG_TALLY_CHUNK_CELLS);
+     a single variable above that gets a run of its own (global atomics) */
+  int64_t tally_chunks;
+  const int32_t* tally_chunk; /* [tally_chunks+1] first variable of each run */
   /* Every int32 array above lives inside blob32 and every int64 array inside
      blob64 (the pack is two contiguous buffers), so a kernel can stage the
      whole structure in shared memory and rebase the pointers (NULL: not
@@ -120,6 +132,7 @@ typedef struct sg_net {
 } sg_net;
 
 #define SG_JOINT_MAX 128
+#define SG_TALLY_CHUNK_CELLS 12288
 #define SG_DESC_MB 8
 #define SG_DESC_WORDS (4 + 2 * SG_DESC_MB)
 

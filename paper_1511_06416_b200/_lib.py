@@ -24,6 +24,7 @@ SG_ERR_ZERO_SUPPORT, SG_ERR_STATE_RANGE, SG_ERR_REJECT_OVERFLOW = 1, 2, 4
 SG_RNG_FAST, SG_RNG_NUMPY, SG_RNG_INJECTED = 0, 1, 2
 SG_ACC_MOVING, SG_ACC_EXPONENTIAL = 0, 1
 SG_FINISH_PACKED_ONLY = 1
+TALLY_CHUNK_CELLS = 12288
 REJ_SLACK = 64
 
 NET_POINTERS = (
@@ -34,7 +35,7 @@ NET_POINTERS = (
 )
 
 
-NET_POINTERS_TAIL = ("joint_radix", "joint_cell", "var_desc")
+NET_POINTERS_TAIL = ("joint_radix", "joint_cell", "var_desc", "fac_start", "fac_desc")
 
 
 class SgNet(ctypes.Structure):
@@ -45,6 +46,7 @@ class SgNet(ctypes.Structure):
         ("table_entries", c_int64),
     ] + [(name, c_void_p) for name in NET_POINTERS] + [("joint_size", c_int64)] + \
         [(name, c_void_p) for name in NET_POINTERS_TAIL] + \
+        [("tally_chunks", c_int64), ("tally_chunk", c_void_p)] + \
         [("blob32", c_void_p), ("blob32_words", c_int64), ("blob64", c_void_p), ("blob64_words", c_int64)]
 
 

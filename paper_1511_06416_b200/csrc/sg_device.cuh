@@ -367,7 +367,7 @@ __device__ __forceinline__ sg_net rebase_net(const sg_net& g, const int32_t* s32
   SG_R32(card); SG_R32(group_start); SG_R32(order); SG_R32(par_start); SG_R32(par_var); SG_R32(par_stride);
   SG_R32(par_slot); SG_R32(mb_start); SG_R32(mb_var); SG_R32(mb_stride); SG_R32(chl_start); SG_R32(chl_var);
   SG_R32(chl_vstride); SG_R32(chl_slot); SG_R32(chl_pstart); SG_R32(chl_pslot); SG_R32(chl_pstride);
-  SG_R32(row_var); SG_R32(joint_radix); SG_R32(joint_cell); SG_R32(var_desc);
+  SG_R32(row_var); SG_R32(joint_radix); SG_R32(joint_cell); SG_R32(var_desc); SG_R32(fac_start); SG_R32(fac_desc); SG_R32(tally_chunk);
   SG_R64(cpt_off); SG_R64(row_off); SG_R64(tab_entries); SG_R64(tab_start); SG_R64(ptab_off); SG_R64(ftab_off);
 #undef SG_R32
 #undef SG_R64

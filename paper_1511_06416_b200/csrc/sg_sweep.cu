@@ -12,23 +12,27 @@
 //      states in shared memory, splitting the latent flags (bit 7) into one
 //      32-case bit mask per variable (SAME replicas share the mask);
 //   2. per colour group, the latent (variable, case) cells are compacted,
-//      variable-major, into an item list (block scan over mask popcounts);
-//      an item carries all m replicas of its case, handled in quads of 4
-//      independent draws = one Philox4x32 call (FAST mode);
+//      variable-major, into an item list (block scan over mask popcounts), so
+//      a warp's 32 consecutive items mostly share one variable (broadcast
+//      descriptor loads, little divergence); an item carries all m replicas
+//      of its case, handled in quads of 4 independent draws = one Philox4x32
+//      call (FAST mode);
 //   3. a draw is a Markov-blanket index (one LDS.U8 + IMAD per member, the
 //      member count a template parameter) and a conditional-table read
 //      (sg_tables.cu) compared with the uniform, or the reference's weight
 //      product for variables without a table;
-//   4. the tally histograms the final lanes on-chip -- whole-lane joint
-//      states in per-thread byte counters for small networks (Koller: 48
-//      joint states), per-cell counters otherwise -- and flushes one atomic
-//      per touched CPT cell per CTA;
+//   4. small models tally the final lanes on-chip -- whole-lane joint states
+//      (Koller: 48) or CPT cells (<= 128) in per-thread byte counters -- and
+//      flush one atomic per touched cell per CTA; larger models are counted
+//      by k_tally_chunked after the sweep (shared-memory histograms per run of
+//      variables, one atomic per cell per CTA);
 //   5. one coalesced HBM write puts the tile back.
 #include "sg_device.cuh"
 
 namespace sg {
 
-enum TallyMode { TALLY_NONE = 0, TALLY_JOINT = 1, TALLY_CELL8 = 2, TALLY_SHARED = 3, TALLY_GLOBAL = 4 };
+// In-sweep tallies of small models; larger ones run k_tally_chunked after the sweep.
+enum TallyMode { TALLY_NONE = 0, TALLY_JOINT = 1, TALLY_CELL8 = 2 };
 
 struct SweepArgs {
   const double* cpt;
@@ -70,7 +74,6 @@ __host__ __device__ inline SmemLayout smem_layout(const sg_net& net, int m, int 
   L.hist = off;
   if (tally_mode == TALLY_JOINT) off += align16(size_t(net.joint_size) * SG_THREADS);
   else if (tally_mode == TALLY_CELL8) off += align16(size_t(net.cells) * SG_THREADS);
-  else if (tally_mode == TALLY_SHARED) off += align16(size_t(net.cells) * 4);
   L.cellacc = off;
   if (tally_mode == TALLY_JOINT) off += align16(size_t(net.cells) * 4 + 64);
   L.total = off;
@@ -118,25 +121,78 @@ __device__ __forceinline__ int block_scan(int x, int* s_warp, int* total) {
   return base + inc - x;
 }
 
-// Direct evaluation for variables without a table (blanket too large).
-__device__ __noinline__ int draw_direct(const sg_net& net, const double* cpt, const int8_t* st, int mtc, int roff,
-                                        int c, int v, double u, bool& zero_support) {
-  const int card = __ldg(net.card + v);
-  int s[SG_MAX_MB];
-  for (int k = __ldg(net.mb_start + v), k0 = k, e = __ldg(net.mb_start + v + 1); k < e; ++k)
-    s[k - k0] = st[__ldg(net.mb_var + k) * mtc + roff + c];
-  double w[SG_MAX_CARD];
-  conditional_weights(net, v, s, cpt, w);
-  const double norm = np_pairwise_sum(w, card);
-  if (!(norm > 0.0)) zero_support = true;
+// Direct evaluation for variables without a table (blanket too large): the
+// reference's weight product for one lane (sampler.py:226-240) from the
+// factored descriptor (sg_net.fac_desc) -- parent row, then each child's
+// factor in ascending child order, every product rounded as numpy rounds it
+// (no FMA) -- with the states read straight from the shared-memory tile by
+// variable id.  Children are taken two at a time so their loads overlap.
+template <int K>
+__device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, const double* __restrict__ cpt,
+                                               const int8_t* st, int mtc, int lane, double u, bool& zs) {
+  const int card = K ? K : fd[0];
+  const int npar = fd[1], nchl = fd[2];
+  int base = fd[3];
+  const int32_t* p = fd + 4;
+  for (int j = 0; j < npar; ++j, p += 2) base += int(st[p[0] * mtc + lane]) * p[1];
+  double w[K ? K : SG_MAX_CARD];
+#pragma unroll
+  for (int t = 0; t < (K ? K : card); ++t) w[t] = __ldg(cpt + base + t);
+  int k = 0;
+  for (; k + 1 < nchl; k += 2) {
+    int i0 = p[1] + int(st[p[0] * mtc + lane]);
+    const int s0 = p[3], n0 = p[4];
+    p += 5;
+    for (int q = 0; q < n0; ++q, p += 2) i0 += int(st[p[0] * mtc + lane]) * p[1];
+    int i1 = p[1] + int(st[p[0] * mtc + lane]);
+    const int s1 = p[3], n1 = p[4];
+    p += 5;
+    for (int q = 0; q < n1; ++q, p += 2) i1 += int(st[p[0] * mtc + lane]) * p[1];
+    double f0[K ? K : SG_MAX_CARD], f1[K ? K : SG_MAX_CARD];
+#pragma unroll
+    for (int t = 0; t < (K ? K : card); ++t) {
+      f0[t] = __ldg(cpt + i0 + t * s0);
+      f1[t] = __ldg(cpt + i1 + t * s1);
+    }
+#pragma unroll
+    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(__dmul_rn(w[t], f0[t]), f1[t]);
+  }
+  if (k < nchl) {
+    int i0 = p[1] + int(st[p[0] * mtc + lane]);
+    const int s0 = p[3], n0 = p[4];
+    p += 5;
+    for (int q = 0; q < n0; ++q, p += 2) i0 += int(st[p[0] * mtc + lane]) * p[1];
+#pragma unroll
+    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(w[t], __ldg(cpt + i0 + t * s0));
+  }
+  double norm;
+  if (K && K < 8) {  // numpy's pairwise sum is sequential below 8 terms
+    norm = 0.0;
+#pragma unroll
+    for (int t = 0; t < (K ? K : 1); ++t) norm = __dadd_rn(norm, w[t]);
+  } else {
+    norm = np_pairwise_sum(w, card);
+  }
+  if (!(norm > 0.0)) zs = true;
   const double au = __dmul_rn(u, norm);
   double cum = 0.0;
   int x = 0;
-  for (int t = 0; t < card - 1; ++t) {
+#pragma unroll
+  for (int t = 0; t < (K ? K - 1 : card - 1); ++t) {
     cum = t ? __dadd_rn(cum, w[t]) : w[0];
     x += (au > cum);
   }
   return x;
+}
+
+__device__ __forceinline__ int draw_factored(const int32_t* fd, const double* cpt, const int8_t* st, int mtc,
+                                             int lane, double u, bool& zs) {
+  switch (fd[0]) {
+    case 2: return draw_factored_k<2>(fd, cpt, st, mtc, lane, u, zs);
+    case 3: return draw_factored_k<3>(fd, cpt, st, mtc, lane, u, zs);
+    case 4: return draw_factored_k<4>(fd, cpt, st, mtc, lane, u, zs);
+    default: return draw_factored_k<0>(fd, cpt, st, mtc, lane, u, zs);
+  }
 }
 
 struct ItemCtx {
@@ -236,10 +292,11 @@ __device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, c
         xs[j] = s;
       }
     } else {
+      const int32_t* fd = net.fac_desc + __ldg(net.fac_start + v);
 #pragma unroll 1
       for (int j = 0; j < 4; ++j) {
         const int r = min(rq * 4 + j, m - 1);
-        xs[j] = draw_direct(net, a.cpt, x.st, mtc, r * tc, c, v, u[j], zs);
+        xs[j] = rq * 4 + j < m ? draw_factored(fd, a.cpt, x.st, mtc, r * tc + c, u[j], zs) : 0;
       }
     }
 #pragma unroll
@@ -316,6 +373,7 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
   const int row_step = SG_THREADS >> lg_row;
   const int row0 = tid >> lg_row;
   const int v0 = row0 / m, r0 = row0 - v0 * m;
+  const int step_v = row_step / m, step_r = row_step - step_v * m;  // (v, r) advance per row step
   {
     const int chunks = nload >> 4;
     const int ch = my_ch;
@@ -323,9 +381,10 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
     for (int row = row0; ch < chunks && row < n * m; row += row_step) {
       int4 val = __ldcs(reinterpret_cast<const int4*>(bt.states + int64_t(row) * bt.pitch + c0 + ch * 16));
       const bool first = r == 0;
-      r += row_step;
       const int vcur = v;
-      while (r >= m) {
+      r += step_r;
+      v += step_v;
+      if (r >= m) {
         r -= m;
         ++v;
       }
@@ -374,8 +433,6 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
       for (int i = tid; i < bytes / 4; i += SG_THREADS) hist32[i] = 0;
       if (a.tally_mode == TALLY_JOINT)
         for (int i = tid; i < int(net.cells); i += SG_THREADS) cellacc[i] = 0;
-    } else if (a.tally_mode == TALLY_SHARED) {
-      for (int i = tid; i < int(net.cells); i += SG_THREADS) hist32[i] = 0;
     }
   }
   __syncthreads();
@@ -464,14 +521,12 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
               cfg += int(lane_row[__ldg(net.par_var + p) * mtc + c]) * __ldg(net.par_stride + p);
             const int64_t cell =
                 __ldg(net.cpt_off + v) + int64_t(cfg) * __ldg(net.card + v) + lane_row[v * mtc + c];
-            if (a.tally_mode == TALLY_CELL8) hist8[cell * SG_THREADS + slot] += 1;
-            else if (a.tally_mode == TALLY_SHARED) atomicAdd(hist32 + cell, 1u);
-            else atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, 1ull);
+            hist8[cell * SG_THREADS + slot] += 1;
           }
         }
       }
       __syncthreads();
-      if (a.tally_mode == TALLY_CELL8) {
+      {
         const int warp = tid >> 5, lane_id = tid & 31;
         for (int cell = warp; cell < int(net.cells); cell += SG_THREADS / 32) {
           const uint32_t* row = reinterpret_cast<const uint32_t*>(hist8 + size_t(cell) * SG_THREADS);
@@ -482,10 +537,6 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
           if (sum && lane_id == 0)
             atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, (unsigned long long)sum);
         }
-      } else if (a.tally_mode == TALLY_SHARED) {
-        for (int cell = tid; cell < int(net.cells); cell += SG_THREADS)
-          if (hist32[cell])
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.counts) + cell, (unsigned long long)hist32[cell]);
       }
     }
   }
@@ -497,8 +548,9 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
     int v = v0, r = r0;
     for (int row = row0; ch < chunks && row < n * m; row += row_step) {
       const uint32_t bits = lat16[v * (words * 2) + ch];
-      r += row_step;
-      while (r >= m) {
+      r += step_r;
+      v += step_v;
+      if (r >= m) {
         r -= m;
         ++v;
       }
@@ -537,12 +589,86 @@ k_tally(const sg_net net, const sg_batch bt, unsigned long long* counts,
   }
 }
 
+// Chunked tally of a resident batch (large models).  blockIdx.y = a run of
+// consecutive variables whose cells fit a shared-memory histogram
+// (sg_net.tally_chunk), blockIdx.x = a slice of the cases.  For each variable
+// of its run a thread takes 4 consecutive cases of a replica row -- one
+// 32-bit load of the variable's row and of each parent's row -- and adds the
+// 4 cells to the histogram; the CTA then flushes every non-zero cell with one
+// global atomic.  A run holding a single oversized variable counts straight
+// into global memory.
+__global__ void __launch_bounds__(SG_THREADS)
+k_tally_chunked(const sg_net net, const sg_batch bt, unsigned long long* __restrict__ counts) {
+  extern __shared__ uint32_t hist[];
+  const int v0 = __ldg(net.tally_chunk + blockIdx.y), v1 = __ldg(net.tally_chunk + blockIdx.y + 1);
+  const int64_t cell0 = __ldg(net.cpt_off + v0);
+  const int64_t cell1 = v1 < net.n ? __ldg(net.cpt_off + v1) : net.cells;
+  const bool local = cell1 - cell0 <= SG_TALLY_CHUNK_CELLS;
+  const int ncell = int(cell1 - cell0);
+  if (local)
+    for (int i = threadIdx.x; i < ncell; i += SG_THREADS) hist[i] = 0;
+  __syncthreads();
+  const int quads = (bt.num_real + 3) >> 2;
+  const int per = (quads + gridDim.x - 1) / gridDim.x;
+  const int q0 = blockIdx.x * per, q1 = min(quads, q0 + per);
+  const int64_t vstride = int64_t(bt.m) * bt.pitch;
+  for (int v = v0; v < v1; ++v) {
+    const int card = __ldg(net.card + v);
+    const int ps = __ldg(net.par_start + v), pe = __ldg(net.par_start + v + 1);
+    const int64_t base = __ldg(net.cpt_off + v) - cell0;
+    for (int q = q0 + threadIdx.x; q < q1; q += SG_THREADS) {
+      const int c = q * 4;
+      const int nl = min(4, bt.num_real - c);
+      for (int r = 0; r < bt.m; ++r) {
+        const int8_t* col = bt.states + int64_t(r) * bt.pitch + c;
+        const uint32_t xv = __ldg(reinterpret_cast<const uint32_t*>(col + v * vstride)) & 0x7F7F7F7Fu;
+        int cfg[4] = {0, 0, 0, 0};
+        for (int p = ps; p < pe; ++p) {
+          const uint32_t xp =
+              __ldg(reinterpret_cast<const uint32_t*>(col + __ldg(net.par_var + p) * vstride)) & 0x7F7F7F7Fu;
+          const int st = __ldg(net.par_stride + p);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cfg[j] += int((xp >> (8 * j)) & 0xFF) * st;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j < nl) {
+            const int64_t cell = base + int64_t(cfg[j]) * card + int((xv >> (8 * j)) & 0xFF);
+            if (local) atomicAdd(hist + cell, 1u);
+            else atomicAdd(counts + cell0 + cell, 1ull);
+          }
+        }
+      }
+    }
+  }
+  if (!local) return;
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncell; i += SG_THREADS)
+    if (hist[i]) atomicAdd(counts + cell0 + i, (unsigned long long)hist[i]);
+}
+
+static int tally_chunked(const sg_net& net, const sg_batch& bt, uint64_t* counts, cudaStream_t s) {
+  const int quads = (bt.num_real + 3) / 4;
+  if (quads == 0 || net.tally_chunks == 0) return SG_OK;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_tally_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, SG_TALLY_CHUNK_CELLS * 4);
+    configured = true;
+  }
+  // ~4 CTAs per SM over all runs, each slice at least one thread-quad per thread
+  const int64_t want = std::max<int64_t>(1, (148 * 4 + net.tally_chunks - 1) / net.tally_chunks);
+  const int slices = int(std::min<int64_t>(want, (quads + SG_THREADS - 1) / SG_THREADS));
+  k_tally_chunked<<<dim3(std::max(1, slices), unsigned(net.tally_chunks)), SG_THREADS, SG_TALLY_CHUNK_CELLS * 4,
+                    s>>>(net, bt, reinterpret_cast<unsigned long long*>(counts));
+  return SG_OK;
+}
+
 static int choose_tile(const sg_net& net, int m, int cases, const SweepArgs& a, bool small, int* tc_out,
                        size_t* smem_out) {
   int best = 0;
   // largest power-of-two tile (<= 512 cases) whose shared memory leaves room
-  // for two CTAs per SM; fall back to one CTA of up to 200 KB.
-  for (int budget : {100 * 1024, 200 * 1024}) {
+  // for four CTAs per SM (latency hiding), else two, else one CTA of up to 200 KB.
+  for (int budget : {56 * 1024, 100 * 1024, 200 * 1024}) {
     for (int tc = 512; tc >= 32; tc >>= 1) {
       const SmemLayout L = smem_layout(net, m, tc, a.tally_mode, small, a.tab_bytes);
       if (L.total <= size_t(budget)) {
@@ -589,6 +715,7 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
   SG_REQUIRE(net->max_card <= SG_MAX_CARD && net->max_mb <= SG_MAX_MB,
              "sg_sweep: card/blanket capacity exceeded");
   SG_REQUIRE(net->var_desc, "sg_sweep: network pack has no variable descriptors");
+  if (net->direct_vars > 0) SG_REQUIRE(net->fac_start && net->fac_desc, "sg_sweep: no factored descriptors");
   SG_REQUIRE(rng_mode >= SG_RNG_FAST && rng_mode <= SG_RNG_INJECTED, "sg_sweep: bad rng mode %d",
              rng_mode);
   if (rng_mode != SG_RNG_FAST)
@@ -617,7 +744,7 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
   const int64_t tab_bytes = net->table_entries > 0
                                 ? (rng_mode == SG_RNG_FAST ? net->ftab_size * 4 : net->ptab_size * 8)
                                 : 0;
-  const bool small = net->n <= 256 && tab_bytes <= 32 * 1024;
+  const bool small = net->n <= 512 && tab_bytes <= 48 * 1024;
   a.tab_bytes = small ? tab_bytes : 0;
   // tally strategy; byte counters hold at most 255 lanes per thread
   const int max_lanes_per_thread = (batch->m * 512 + SG_THREADS - 1) / SG_THREADS;
@@ -627,8 +754,12 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
            net->joint_radix && net->joint_cell)
     a.tally_mode = TALLY_JOINT;
   else if (bytes_ok && net->cells <= 128) a.tally_mode = TALLY_CELL8;
-  else if (net->cells * 4 <= 48 * 1024) a.tally_mode = TALLY_SHARED;
-  else a.tally_mode = TALLY_GLOBAL;
+  else a.tally_mode = TALLY_NONE;  // large models: the chunked tally kernel after the sweep
+  const bool chunked = counts && a.tally_mode == TALLY_NONE;
+  if (chunked) {
+    SG_REQUIRE(net->tally_chunk && net->tally_chunks > 0, "sg_sweep: network pack has no tally runs");
+    a.counts = nullptr;  // the sweep itself counts nothing
+  }
   size_t smem = 0;
   int st = choose_tile(*net, batch->m, batch->cases, a, small, &a.tc, &smem);
   if (st != SG_OK) {
@@ -645,6 +776,7 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
     case 4: launch_sweep<SG_RNG_INJECTED, false>(*net, *batch, a, blocks, smem, s); break;
     default: launch_sweep<SG_RNG_INJECTED, true>(*net, *batch, a, blocks, smem, s); break;
   }
+  if (chunked) tally_chunked(*net, *batch, counts, s);
   return check_launch("sg_sweep");
 }
 
@@ -653,10 +785,9 @@ extern "C" int sg_tally(const sg_net* net, const sg_batch* batch, uint64_t* coun
   SG_REQUIRE(net && batch && counts && batch->states, "sg_tally: null argument");
   const int64_t lanes = int64_t(batch->m) * batch->num_real;
   if (lanes == 0) return SG_OK;
-  const int blocks = int((lanes + SG_THREADS - 1) / SG_THREADS < 148 * 32 ? (lanes + SG_THREADS - 1) / SG_THREADS
-                                                                          : 148 * 32);
-  k_tally<<<blocks, SG_THREADS, 0, (cudaStream_t)stream>>>(
-      *net, *batch, reinterpret_cast<unsigned long long*>(counts), nullptr, nullptr);
+  SG_REQUIRE(batch->pitch % 16 == 0, "sg_tally: row pitch must be a multiple of 16");
+  SG_REQUIRE(net->tally_chunk && net->tally_chunks > 0, "sg_tally: network pack has no tally runs");
+  tally_chunked(*net, *batch, counts, (cudaStream_t)stream);
   return check_launch("sg_tally");
 }
 

@@ -21,8 +21,14 @@ from .network import Coloring, Network, color_graph, moralize
 # A variable's full conditional is tabulated when its blanket has at most this
 # many configurations and the tables stay within the byte budget below; the
 # others are evaluated per lane from the CPTs ("direct" variables).
+# Conditional tables pay off only while the sweep can stage them in shared
+# memory (n <= TABLE_MAX_VARS, parity table <= TABLE_BUDGET_BYTES): tables read
+# from L2 lose to the factored weight product, and mixing the two draw kinds in
+# one large network costs instruction-cache misses (measured on B200, C4
+# shape: 39 ms factored-only vs 51 ms with 32 KB of tables vs 82 ms with 52 MB).
 TABLE_MAX_ENTRIES = 1 << 16
-TABLE_BUDGET_BYTES = 512 << 20
+TABLE_BUDGET_BYTES = 48 << 10
+TABLE_MAX_VARS = 512
 MAX_CARD = 64
 MAX_MB = 64
 JOINT_MAX = 128        # SG_JOINT_MAX
@@ -51,9 +57,11 @@ class NetLayout:
 
 
 def layout(net: Network, coloring: Coloring | None = None,
-           table_max_entries: int = TABLE_MAX_ENTRIES,
-           table_budget_bytes: int = TABLE_BUDGET_BYTES) -> NetLayout:
+           table_max_entries: int | None = None,
+           table_budget_bytes: int | None = None) -> NetLayout:
     n = net.num_vars
+    table_max_entries = TABLE_MAX_ENTRIES if table_max_entries is None else table_max_entries
+    table_budget_bytes = TABLE_BUDGET_BYTES if table_budget_bytes is None else table_budget_bytes
     if coloring is None:
         coloring = color_graph(moralize(net))
     cards = np.asarray(net.cardinalities, dtype=np.int64)
@@ -65,9 +73,6 @@ def layout(net: Network, coloring: Coloring | None = None,
     row_off = np.zeros(n + 1, dtype=np.int64)
     row_off[1:] = np.cumsum(rows)
 
-    order = [v for grp in coloring.groups for v in grp]
-    group_start = np.zeros(len(coloring.groups) + 1, dtype=np.int64)
-    group_start[1:] = np.cumsum([len(g) for g in coloring.groups])
 
     par_start, par_var, par_stride, par_slot = [0], [], [], []
     mb_start, mb_var, mb_stride = [0], [], []
@@ -120,7 +125,7 @@ def layout(net: Network, coloring: Coloring | None = None,
     # choose tabulated variables: smallest tables first under the byte budget
     tab_entries = np.zeros(n, dtype=np.int64)
     budget = table_budget_bytes
-    for v in sorted(range(n), key=lambda v: mb_confs[v]):
+    for v in sorted(range(n), key=lambda v: mb_confs[v]) if n <= TABLE_MAX_VARS else ():
         e = mb_confs[v]
         nbytes = e * int(cards[v]) * 8
         if e <= table_max_entries and nbytes <= budget:
@@ -128,6 +133,19 @@ def layout(net: Network, coloring: Coloring | None = None,
             budget -= nbytes
     tab_start = np.zeros(n + 1, dtype=np.int64)
     tab_start[1:] = np.cumsum(tab_entries)
+
+    # Inside a colour group the order is result-neutral (the members are
+    # conditionally independent and draw from per-variable streams).  The sweep
+    # compacts latent cells variable-major and a warp takes 32 consecutive
+    # items, so members with the same draw kind (table with k blanket members,
+    # or the factored product) sit together, costliest first.
+    def kind(v):
+        k = len(blankets[v]) if tab_entries[v] > 0 and len(blankets[v]) <= DESC_MB else DESC_MB + 1
+        return (k, -(len(net.children[v]) + len(net.parents[v])), v)
+
+    order = [v for grp in coloring.groups for v in sorted(grp, key=kind)]
+    group_start = np.zeros(len(coloring.groups) + 1, dtype=np.int64)
+    group_start[1:] = np.cumsum([len(g) for g in coloring.groups])
     ptab_len = tab_entries * cards
     ftab_len = tab_entries * (cards - 1)
     ptab_off = np.zeros(n, dtype=np.int64)
@@ -150,6 +168,43 @@ def layout(net: Network, coloring: Coloring | None = None,
             desc[v, 4 + DESC_MB:4 + DESC_MB + len(mb)] = mb_stride[mb_start[v]:mb_start[v + 1]]
         else:
             desc[v, 1] = -1
+    # factored draw descriptors (draw_factored, sg_sweep.cu): the reference's
+    # weight product (sampler.py:226-240) with every index pre-multiplied:
+    #   card, npar, nchl, cpt_off[v],
+    #   npar x (parent, stride * card),
+    #   nchl x (child, cpt_off[c], card[c], vstride * card[c], nq, nq x (other parent, stride * card[c]))
+    fac_start, fac = [0], []
+    for v in range(n):
+        card = int(cards[v])
+        ps = net.parent_strides(v)
+        fac += [card, len(net.parents[v]), len(net.children[v]), int(cpt_off[v])]
+        for j, p in enumerate(net.parents[v]):
+            fac += [p, int(ps[j]) * card]
+        for c in net.children[v]:
+            cps = net.parent_strides(c)
+            cc = int(cards[c])
+            j = net.parents[c].index(v)
+            others = [(p, int(cps[q]) * cc) for q, p in enumerate(net.parents[c]) if p != v]
+            fac += [c, int(cpt_off[c]), cc, int(cps[j]) * cc, len(others)]
+            for p, st in others:
+                fac += [p, st]
+        fac_start.append(len(fac))
+
+    # chunked tally: runs of consecutive variables whose cells fit one
+    # shared-memory histogram (SG_TALLY_CHUNK_CELLS)
+    from ._lib import TALLY_CHUNK_CELLS
+
+    tally_chunk = [0]
+    acc = 0
+    for v in range(n):
+        c = int(rows[v] * cards[v])
+        if acc and acc + c > TALLY_CHUNK_CELLS:
+            tally_chunk.append(v)
+            acc = 0
+        acc += c
+    if n:
+        tally_chunk.append(n)
+
     # joint-state tally tables (small networks)
     joint = int(np.prod(cards)) if n else 0
     if 0 < joint <= JOINT_MAX:
@@ -182,6 +237,7 @@ def layout(net: Network, coloring: Coloring | None = None,
         "chl_vstride": i32(chl_vstride), "chl_slot": i32(chl_slot), "chl_pstart": i32(chl_pstart),
         "chl_pslot": i32(chl_pslot), "chl_pstride": i32(chl_pstride), "row_var": i32(row_var),
         "joint_radix": i32(radix), "joint_cell": i32(jcell.ravel()), "var_desc": i32(desc.ravel()),
+        "fac_start": i32(fac_start), "fac_desc": i32(fac), "tally_chunk": i32(tally_chunk),
     }
     int64 = {
         "cpt_off": cpt_off[:n].copy(), "row_off": row_off, "tab_entries": tab_entries,
@@ -200,6 +256,7 @@ def layout(net: Network, coloring: Coloring | None = None,
         "ftab_size": int(ftab_len.sum()),
         "table_entries": int(tab_entries.sum()),
         "joint_size": joint,
+        "tally_chunks": len(tally_chunk) - 1,
     }
     return NetLayout(n=n, cards=cards, rows=rows, cpt_off=cpt_off, row_off=row_off,
                      groups=coloring.groups, topo=np.asarray(net.topo_order, dtype=np.int32),
@@ -292,7 +349,7 @@ class NetPack:
         s = SgNet()
         for k, v in lay.scalars.items():
             setattr(s, k, v)
-        for k in NET_POINTERS + NET_POINTERS_TAIL:
+        for k in NET_POINTERS + NET_POINTERS_TAIL + ("tally_chunk",):
             if k in offs32:
                 setattr(s, k, self.buf32.data_ptr() + 4 * offs32[k])
             else:

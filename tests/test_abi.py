@@ -50,8 +50,9 @@ def test_struct_layout_matches_header():
 #include <stddef.h>
 #include "samegibbs_b200.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(sg_net), offsetof(sg_net, cells), offsetof(sg_net, row_var),
-         sizeof(sg_batch), offsetof(sg_batch, case_base), offsetof(sg_batch, nmiss));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(sg_net), offsetof(sg_net, cells),
+         offsetof(sg_net, row_var), offsetof(sg_net, tally_chunk), sizeof(sg_batch), offsetof(sg_batch, case_base),
+         offsetof(sg_batch, nmiss), sizeof(sg_finish), offsetof(sg_finish, flags), sizeof(sg_small));
   return 0;
 }
 '''
@@ -64,7 +65,9 @@ int main(void) {
         subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
         got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     want = [ctypes.sizeof(_lib.SgNet), _lib.SgNet.cells.offset, _lib.SgNet.row_var.offset,
-            ctypes.sizeof(_lib.SgBatch), _lib.SgBatch.case_base.offset, _lib.SgBatch.nmiss.offset]
+            _lib.SgNet.tally_chunk.offset, ctypes.sizeof(_lib.SgBatch), _lib.SgBatch.case_base.offset,
+            _lib.SgBatch.nmiss.offset, ctypes.sizeof(_lib.SgFinish), _lib.SgFinish.flags.offset,
+            ctypes.sizeof(_lib.SgSmall)]
     assert got == want
 
 
