@@ -112,8 +112,8 @@ typedef struct sg_net {
   /* factored draw descriptor of v at fac_desc[fac_start[v]] (the weight
      product of sampler.py:226-240 with pre-multiplied indices): card, npar,
      nchl, cpt_off[v]; npar x (parent, stride*card); nchl x (child,
-     cpt_off[child], card[child], vstride*card[child], nq, nq x (other parent,
-     stride*card[child])) */
+     cpt_off[child], card[child], vstride*card[child], nq, 0, nq x (other
+     parent, stride*card[child])); every pair 8-byte aligned */
   const int32_t* fac_start;   /* [n+1] */
   const int32_t* fac_desc;
   /* chunked tally (large models): variables split into runs of consecutive

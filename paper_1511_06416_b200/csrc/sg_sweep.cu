@@ -134,7 +134,10 @@ __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, c
   const int npar = fd[1], nchl = fd[2];
   int base = fd[3];
   const int32_t* p = fd + 4;
-  for (int j = 0; j < npar; ++j, p += 2) base += int(st[p[0] * mtc + lane]) * p[1];
+  for (int j = 0; j < npar; ++j, p += 2) {
+    const int2 e = *reinterpret_cast<const int2*>(p);
+    base += int(st[e.x * mtc + lane]) * e.y;
+  }
   double w[K ? K : SG_MAX_CARD];
 #pragma unroll
   for (int t = 0; t < (K ? K : card); ++t) w[t] = __ldg(cpt + base + t);
@@ -142,12 +145,18 @@ __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, c
   for (; k + 1 < nchl; k += 2) {
     int i0 = p[1] + int(st[p[0] * mtc + lane]);
     const int s0 = p[3], n0 = p[4];
-    p += 5;
-    for (int q = 0; q < n0; ++q, p += 2) i0 += int(st[p[0] * mtc + lane]) * p[1];
+    p += 6;
+    for (int q = 0; q < n0; ++q, p += 2) {
+      const int2 e = *reinterpret_cast<const int2*>(p);
+      i0 += int(st[e.x * mtc + lane]) * e.y;
+    }
     int i1 = p[1] + int(st[p[0] * mtc + lane]);
     const int s1 = p[3], n1 = p[4];
-    p += 5;
-    for (int q = 0; q < n1; ++q, p += 2) i1 += int(st[p[0] * mtc + lane]) * p[1];
+    p += 6;
+    for (int q = 0; q < n1; ++q, p += 2) {
+      const int2 e = *reinterpret_cast<const int2*>(p);
+      i1 += int(st[e.x * mtc + lane]) * e.y;
+    }
     double f0[K ? K : SG_MAX_CARD], f1[K ? K : SG_MAX_CARD];
 #pragma unroll
     for (int t = 0; t < (K ? K : card); ++t) {
@@ -160,8 +169,11 @@ __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, c
   if (k < nchl) {
     int i0 = p[1] + int(st[p[0] * mtc + lane]);
     const int s0 = p[3], n0 = p[4];
-    p += 5;
-    for (int q = 0; q < n0; ++q, p += 2) i0 += int(st[p[0] * mtc + lane]) * p[1];
+    p += 6;
+    for (int q = 0; q < n0; ++q, p += 2) {
+      const int2 e = *reinterpret_cast<const int2*>(p);
+      i0 += int(st[e.x * mtc + lane]) * e.y;
+    }
 #pragma unroll
     for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(w[t], __ldg(cpt + i0 + t * s0));
   }
@@ -668,7 +680,10 @@ static int choose_tile(const sg_net& net, int m, int cases, const SweepArgs& a, 
   int best = 0;
   // largest power-of-two tile (<= 512 cases) whose shared memory leaves room
   // for four CTAs per SM (latency hiding), else two, else one CTA of up to 200 KB.
-  for (int budget : {56 * 1024, 100 * 1024, 200 * 1024}) {
+#ifndef SG_TILE_BUDGET0
+#define SG_TILE_BUDGET0 (56 * 1024)
+#endif
+  for (int budget : {SG_TILE_BUDGET0, 100 * 1024, 200 * 1024}) {
     for (int tc = 512; tc >= 32; tc >>= 1) {
       const SmemLayout L = smem_layout(net, m, tc, a.tally_mode, small, a.tab_bytes);
       if (L.total <= size_t(budget)) {

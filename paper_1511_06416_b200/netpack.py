@@ -172,7 +172,7 @@ def layout(net: Network, coloring: Coloring | None = None,
     # weight product (sampler.py:226-240) with every index pre-multiplied:
     #   card, npar, nchl, cpt_off[v],
     #   npar x (parent, stride * card),
-    #   nchl x (child, cpt_off[c], card[c], vstride * card[c], nq, nq x (other parent, stride * card[c]))
+    #   nchl x (child, cpt_off[c], card[c], vstride * card[c], nq, 0, nq x (other parent, stride * card[c]))
     fac_start, fac = [0], []
     for v in range(n):
         card = int(cards[v])
@@ -185,7 +185,7 @@ def layout(net: Network, coloring: Coloring | None = None,
             cc = int(cards[c])
             j = net.parents[c].index(v)
             others = [(p, int(cps[q]) * cc) for q, p in enumerate(net.parents[c]) if p != v]
-            fac += [c, int(cpt_off[c]), cc, int(cps[j]) * cc, len(others)]
+            fac += [c, int(cpt_off[c]), cc, int(cps[j]) * cc, len(others), 0]  # 6 words: pairs stay 8-byte aligned
             for p, st in others:
                 fac += [p, st]
         fac_start.append(len(fac))
@@ -335,9 +335,12 @@ class NetPack:
         parts32, parts64 = [], []
         pos = 0
         for k, a in lay.int32.items():
+            # every array starts on a 16-byte boundary (vector loads of descriptors)
+            a = a if len(a) else np.zeros(1, np.int32)
+            a = np.concatenate([a, np.zeros((-len(a)) % 4, np.int32)])
             offs32[k] = pos
-            pos += max(len(a), 1)
-            parts32.append(a if len(a) else np.zeros(1, np.int32))
+            pos += len(a)
+            parts32.append(a)
         pos64 = 0
         for k, a in lay.int64.items():
             offs64[k] = pos64
