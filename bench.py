@@ -11,12 +11,14 @@ generated on the device.  node-samples per step = n_vars x cases x m
 (sampler.py:475).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2|c3|c4]
+                  [--workload c2|c3|c4|c5]
 
 ``--workload c3`` (MOOC-shaped, 334 variables, 131,010 cases, m = 5) and
 ``c4`` (random DAG, 1000 nodes, 1.25M cases per GPU = 10M over 8, m = 1, 30%
-missing) measure the generic kernel on the other BASELINE shapes; C2 is the
-headline line.
+missing) measure the generic kernel on the other BASELINE shapes; ``c5``
+streams minibatches of the 1000-node network from pinned host memory
+(HostSource, copy stream one block ahead), m = 20, exponential accumulator.
+C2 is the headline line.
 
 Timing: per-step CUDA events on the launching stream, L2 flushed (256 MB
 write + 256 MB read) between timed steps, max over ranks.  Prints ONE JSON
@@ -62,7 +64,7 @@ class Workload:
             net = netgen.mooc_network(15, 319, seed=3)
             return net, netgen.dirichlet_cpts(net, 1.0, seed=6)
         net = netgen.random_dag_network(1000, max_parents=4, min_card=2, max_card=4, seed=4)
-        return net, netgen.dirichlet_cpts(net, 1.0, seed=5)
+        return net, netgen.dirichlet_cpts(net, 1.0, seed=5)  # C4 and C5 share the network
 
     # -- device observations of this rank's shard
     def observations(self, net, truth, rank):
@@ -101,7 +103,7 @@ class Workload:
     def config(self, n_gpus: int, rng: str, n_vars: int) -> dict:
         return {
             "workload": self.title, "network": {"c2": "koller-student", "c3": "mooc-shaped",
-                                                "c4": "random-dag-1000"}[self.key],
+                                                "c4": "random-dag-1000", "c5": "random-dag-1000"}[self.key],
             "n_vars": n_vars, "cases_per_gpu": self.cases, "global_minibatch": self.cases * n_gpus, "m": self.m,
             "latent_fraction": round(self.latent, 4), "rng": rng,
             "parallelism": f"case-sharded x{n_gpus}, int64 count all-reduce" if n_gpus > 1 else "single GPU",
@@ -118,7 +120,11 @@ WORKLOADS = {
     "c4": Workload("c4", "C4: random DAG, 1000 nodes, in-degree<=4, cards 2-4, 1.25M cases/GPU (10M over 8), "
                          "30% missing, SAME m=1, minibatch=shard, moving-sum, Dirichlet CPT update", 1_250_000, 1,
                    0.3, 4_000),
+    "c5": Workload("c5", "C5: out-of-core, random DAG 1000 nodes, 30% missing, SAME m=20, minibatches of 131,072 "
+                         "cases streamed from pinned host memory (8 host blocks = 1,048,576 cases per GPU, "
+                         "replayed), exponential accumulator, Dirichlet CPT update", 131_072, 20, 0.3, 500),
 }
+C5_HOST_BLOCKS = 8
 
 
 # ---------------------------------------------------------------- CPU oracle legs
@@ -425,6 +431,79 @@ def our_arm(args, wl: Workload) -> None:
         dist.destroy_process_group()
 
 
+def stream_arm(args, wl: Workload) -> None:
+    """C5: minibatches streamed from pinned host memory through HostSource."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1511_06416_b200 as sg
+    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200.engine import Engine
+
+    B, M = wl.cases, wl.m
+    host_cases = B * C5_HOST_BLOCKS
+    net, truth = wl.network()
+    n_vars = net.num_vars
+    obs = sg.forward_sample_device(net, truth, host_cases, seed=105, hide_fraction=0.3, mask_seed=205,
+                                   case_base=rank * host_cases)
+    latent = float((obs[:, :host_cases] < 0).float().mean())
+    steps = args.steps
+    cycle = (args.warmup + steps + C5_HOST_BLOCKS - 1) // C5_HOST_BLOCKS
+    src = sg.HostSource.from_dense(obs[:, :host_cases].cpu(), B, cycle=cycle)
+    del obs
+    cfg = sg.SamplerConfig(same_m=M, minibatch_size=B, num_passes=1, seed=300, rng=args.rng,
+                           accumulator_mode="exponential", exp_decay=0.9)
+    comm = (lambda c: dist.all_reduce(c)) if world > 1 else None
+    eng = Engine(net, cfg, case_base=rank * host_cases, comm=comm)
+    it = iter(src)
+    for _ in range(args.warmup):
+        eng.visit(next(it), 0, M)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    launches0 = _lib.launch_count
+    with ClockSampler(local) as clk:
+        marks[0].record()
+        for k in range(steps):
+            mb = next(it)  # the stream waits for this block's host->device copy
+            eng.visit(mb, 0, M)
+            marks[k + 1].record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count - launches0
+    if eng.err.read():
+        raise RuntimeError("device error word set")
+    ms = marks[0].elapsed_time(marks[steps]) / steps  # copy waits + visits, back to back
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    node_samples = n_vars * B * M
+    value = world * node_samples / (ms * 1e-3)
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int8 states, u32 draws, f64 CPTs", "data": "synthetic",
+            "config": dict(wl.config(world, args.rng, n_vars), latent_fraction=round(latent, 4),
+                           host_buffer_cases=host_cases, l2="inputs stream from host memory every step"),
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": n_vars * B, "d2h_bytes_per_step": 0,
+                    "note": "value is already end to end: every step's minibatch comes from pinned host memory"},
+            "gpu_launches": launches, "launch_mode": "eager, copy stream one minibatch ahead",
+            "kernel_path": "generic sg_sweep + chunked tally + step tail", "clocks": clk.summary(),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -441,6 +520,8 @@ def main() -> None:
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         reference_arm(args, wl)
+    elif wl.key == "c5":
+        stream_arm(args, wl)
     else:
         our_arm(args, wl)
 

@@ -46,6 +46,7 @@ struct SweepArgs {
   uint64_t* counts;
   int32_t* err;
   int tc;            // cases per tile (multiple of 32)
+  int mg;            // replicas per tile (replica groups: blockIdx.y)
   int tally_mode;
   int64_t tab_bytes; // bytes of the table this mode reads (staged when SMALL)
 };
@@ -209,7 +210,8 @@ __device__ __forceinline__ int draw_factored(const int32_t* fd, const double* cp
 
 struct ItemCtx {
   int8_t* st;
-  int mtc, tc, m;
+  int mtc, tc, m;  // m = replicas in this tile (local rows), r0 = global replica of local row 0
+  int r0;
   int64_t gcase0;  // global index of the tile's case 0
   int c0;
   uint64_t key;    // FAST key of this sweep
@@ -245,10 +247,19 @@ __device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, c
       ioff = __ldg(a.inj_off + v);
     }
   }
-  const int Q = (m + 3) >> 2;
-  for (int rq = 0; rq < Q; ++rq) {
+  // global replica quads overlapping this tile's replicas [r0, r0 + m)
+  const int q_lo = x.r0 >> 2, q_hi = (x.r0 + m - 1) >> 2;
+  for (int rq = q_lo; rq <= q_hi; ++rq) {
     uint32_t u31[4];
     double u[4];
+    int loc[4];  // local replica row of word j (clamped; `ok` tells whether it is ours)
+    bool ok[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int l = rq * 4 + j - x.r0;
+      ok[j] = l >= 0 && l < m;
+      loc[j] = min(max(l, 0), m - 1);
+    }
     if (MODE == SG_RNG_FAST) {
       const u32x4 w = fast_block(x.key, uint64_t(x.gcase0 + c), uint32_t(v), uint32_t(rq), 0u);
       u31[0] = w.a >> 1;
@@ -262,7 +273,7 @@ __device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, c
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int r = min(rq * 4 + j, m - 1);
+        const int r = x.r0 + loc[j];
         const int64_t idx = int64_t(r) * nmiss + rank;  // reference lane order (sampler.py:245)
         u[j] = MODE == SG_RNG_NUMPY ? np_uniform(uint64_t(idx), k0, k1) : __ldg(a.uniforms + ioff + idx);
         u31[j] = 0;
@@ -273,7 +284,7 @@ __device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, c
       int e[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int roff = min(rq * 4 + j, m - 1) * tc;
+        const int roff = loc[j] * tc;
         int acc = 0;
 #pragma unroll
         for (int k = 0; k < (K > 0 ? K : 0); ++k) acc += int(x.st[rows[k] + roff]) * strd[k];
@@ -285,7 +296,7 @@ __device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, c
         if (MODE == SG_RNG_FAST) {
           const uint32_t* th = tf + e[j] * (card - 1);
           const uint32_t t0 = th[0];
-          if (zs_armed && t0 == 0xFFFFFFFFu) zs = true;
+          if (zs_armed && ok[j] && t0 == 0xFFFFFFFFu) zs = true;
           s = u31[j] >= t0;
           if (card > 2) {
             s += u31[j] >= th[1];
@@ -297,7 +308,7 @@ __device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, c
         } else {
           const double* p = tp + int64_t(e[j]) * card;
           const double norm = p[card - 1];
-          if (!(norm > 0.0)) zs = true;
+          if (ok[j] && !(norm > 0.0)) zs = true;
           const double au = __dmul_rn(u[j], norm);
           for (int q = 0; q < card - 1; ++q) s += (au > p[q]);
         }
@@ -306,14 +317,11 @@ __device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, c
     } else {
       const int32_t* fd = net.fac_desc + __ldg(net.fac_start + v);
 #pragma unroll 1
-      for (int j = 0; j < 4; ++j) {
-        const int r = min(rq * 4 + j, m - 1);
-        xs[j] = rq * 4 + j < m ? draw_factored(fd, a.cpt, x.st, mtc, r * tc + c, u[j], zs) : 0;
-      }
+      for (int j = 0; j < 4; ++j) xs[j] = ok[j] ? draw_factored(fd, a.cpt, x.st, mtc, loc[j] * tc + c, u[j], zs) : 0;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (rq * 4 + j < m) out[(rq * 4 + j) * tc] = int8_t(xs[j]);
+      if (ok[j]) out[loc[j] * tc] = int8_t(xs[j]);
   }
 }
 
@@ -360,11 +368,12 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
   __shared__ int s_warp[SG_THREADS / 32];
   __shared__ int s_err;
   const int tc = a.tc;
-  const int m = bt.m;
+  const int rg0 = blockIdx.y * a.mg;              // first replica of this tile
+  const int m = min(a.mg, bt.m - rg0);            // replicas of this tile (local rows)
   const int n = net.n;
   const int mtc = m * tc;
   const int words = tc >> 5;  // flag words per variable
-  const SmemLayout L = smem_layout(net, m, tc, a.tally_mode, SMALL, a.tab_bytes);
+  const SmemLayout L = smem_layout(net, a.mg, tc, a.tally_mode, SMALL, a.tab_bytes);
   int8_t* st = reinterpret_cast<int8_t*>(smem + L.st);
   uint32_t* lat = reinterpret_cast<uint32_t*>(smem + L.lat);
   uint16_t* lat16 = reinterpret_cast<uint16_t*>(smem + L.lat);
@@ -391,8 +400,9 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
     const int ch = my_ch;
     int v = v0, r = r0;
     for (int row = row0; ch < chunks && row < n * m; row += row_step) {
-      int4 val = __ldcs(reinterpret_cast<const int4*>(bt.states + int64_t(row) * bt.pitch + c0 + ch * 16));
-      const bool first = r == 0;
+      int4 val = __ldcs(reinterpret_cast<const int4*>(bt.states + (int64_t(v) * bt.m + rg0 + r) * bt.pitch + c0 +
+                                                       ch * 16));
+      const bool first = r == 0;  // first replica of the tile (every replica carries the shared mask)
       const int vcur = v;
       r += step_r;
       v += step_v;
@@ -455,6 +465,7 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
   x.mtc = mtc;
   x.tc = tc;
   x.m = m;
+  x.r0 = rg0;
   x.gcase0 = bt.case_base + c0;
   x.key = a.fast_key_dev ? __ldg(a.fast_key_dev) : a.fast_key;
   x.c0 = c0;
@@ -560,6 +571,7 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
     int v = v0, r = r0;
     for (int row = row0; ch < chunks && row < n * m; row += row_step) {
       const uint32_t bits = lat16[v * (words * 2) + ch];
+      const int vcur = v, rcur = r;
       r += step_r;
       v += step_v;
       if (r >= m) {
@@ -571,7 +583,8 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
       val.y |= flags_to_bytes((bits >> 4) & 0xF);
       val.z |= flags_to_bytes((bits >> 8) & 0xF);
       val.w |= flags_to_bytes((bits >> 12) & 0xF);
-      __stcs(reinterpret_cast<int4*>(bt.states + int64_t(row) * bt.pitch + c0 + ch * 16), val);
+      __stcs(reinterpret_cast<int4*>(bt.states + (int64_t(vcur) * bt.m + rg0 + rcur) * bt.pitch + c0 + ch * 16),
+             val);
     }
   }
   __syncthreads();
@@ -676,33 +689,43 @@ static int tally_chunked(const sg_net& net, const sg_batch& bt, uint64_t* counts
 }
 
 static int choose_tile(const sg_net& net, int m, int cases, const SweepArgs& a, bool small, int* tc_out,
-                       size_t* smem_out) {
-  int best = 0;
-  // largest power-of-two tile (<= 512 cases) whose shared memory leaves room
-  // for four CTAs per SM (latency hiding), else two, else one CTA of up to 200 KB.
+                       int* mg_out, size_t* smem_out) {
+  // Largest power-of-two case tile (<= 512) holding all m replicas whose
+  // shared memory leaves room for four CTAs per SM (latency hiding), else
+  // two, else one of up to 200 KB.  When even 32 cases x m replicas do not
+  // fit (large n x m), the replicas split into groups (grid y): lanes never
+  // interact, so any tiling of (cases x replicas) is exact.
 #ifndef SG_TILE_BUDGET0
 #define SG_TILE_BUDGET0 (56 * 1024)
 #endif
+  int best = 0, mg = m;
   for (int budget : {SG_TILE_BUDGET0, 100 * 1024, 200 * 1024}) {
-    for (int tc = 512; tc >= 32; tc >>= 1) {
-      const SmemLayout L = smem_layout(net, m, tc, a.tally_mode, small, a.tab_bytes);
-      if (L.total <= size_t(budget)) {
-        best = tc;
+    for (int tc = 512; tc >= 32 && !best; tc >>= 1)
+      if (smem_layout(net, m, tc, a.tally_mode, small, a.tab_bytes).total <= size_t(budget)) best = tc;
+    if (best) break;
+  }
+  if (!best) {
+    // replica groups of 4 (one Philox quad), 2, 1 at the smallest tile
+    for (int g : {16, 12, 8, 4, 2, 1}) {
+      if (g >= m) continue;
+      if (smem_layout(net, g, 32, a.tally_mode, small, a.tab_bytes).total <= size_t(200 * 1024)) {
+        best = 32;
+        mg = g;
         break;
       }
     }
-    if (best) break;
   }
   if (!best) return SG_ECAPACITY;
   // do not make tiles much larger than the minibatch
   while (best > 32 && best / 2 >= cases) best >>= 1;
   *tc_out = best;
-  *smem_out = smem_layout(net, m, best, a.tally_mode, small, a.tab_bytes).total;
+  *mg_out = mg;
+  *smem_out = smem_layout(net, mg, best, a.tally_mode, small, a.tab_bytes).total;
   return SG_OK;
 }
 
 template <int MODE, bool SMALL>
-static void launch_sweep(const sg_net& net, const sg_batch& bt, const SweepArgs& a, int blocks, size_t smem,
+static void launch_sweep(const sg_net& net, const sg_batch& bt, const SweepArgs& a, dim3 blocks, size_t smem,
                          cudaStream_t s) {
   static size_t configured = 0;  // raise the opt-in once per instantiation (graph-capture friendly)
   if (smem > configured) {
@@ -756,6 +779,7 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
   a.counts = counts;
   a.err = err;
   a.tc = 0;
+  a.mg = 0;
   const int64_t tab_bytes = net->table_entries > 0
                                 ? (rng_mode == SG_RNG_FAST ? net->ftab_size * 4 : net->ptab_size * 8)
                                 : 0;
@@ -776,12 +800,12 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
     a.counts = nullptr;  // the sweep itself counts nothing
   }
   size_t smem = 0;
-  int st = choose_tile(*net, batch->m, batch->cases, a, small, &a.tc, &smem);
+  int st = choose_tile(*net, batch->m, batch->cases, a, small, &a.tc, &a.mg, &smem);
   if (st != SG_OK) {
     set_error("sg_sweep: tile of n=%d x m=%d does not fit in shared memory", net->n, batch->m);
     return st;
   }
-  const int blocks = (batch->cases + a.tc - 1) / a.tc;
+  const dim3 blocks((batch->cases + a.tc - 1) / a.tc, (batch->m + a.mg - 1) / a.mg);
   cudaStream_t s = (cudaStream_t)stream;
   switch (rng_mode * 2 + (small ? 1 : 0)) {
     case 0: launch_sweep<SG_RNG_FAST, false>(*net, *batch, a, blocks, smem, s); break;

@@ -67,6 +67,15 @@ def test_c4_sweep_bit_exact(c4):
     _sweep_vs_oracle(net, truth, dense, 1, 304, 9001)
 
 
+def test_c4_replica_groups_bit_exact(c4):
+    """n x m too large for one tile of all replicas (1000 x 10): the sweep
+    splits the replicas into groups (grid y) -- still bit-exact."""
+    net, truth = c4
+    obs = sg.forward_sample_device(net, truth, 700, seed=106, hide_fraction=0.3, mask_seed=206)
+    dense = obs[:, :700].cpu().numpy().astype(np.int32)
+    _sweep_vs_oracle(net, truth, dense, 10, 305, 9003)
+
+
 def test_c3_sweep_bit_exact(c3):
     net, truth = c3
     obs = netgen.mooc_observations(net, truth, 4000, 15, density=0.022, seed=103)
@@ -128,3 +137,38 @@ def test_c4_fast_mode_properties(c4):
     cases = 200_000
     obs = sg.forward_sample_device(net, truth, cases, seed=114, hide_fraction=0.3, mask_seed=214)
     _fast_properties(net, obs, cases, 1, 100_000)
+
+
+@pytest.mark.parametrize("acc", ["exponential", "moving_sum"])
+def test_host_source_streaming_equals_device_source(c4, acc):
+    """Out-of-core streaming (HostSource: pinned host blocks, copy stream one
+    minibatch ahead, replayed twice) gives exactly the run of a device-resident
+    source over the same (duplicated) data."""
+    net, truth = c4
+    cases, mb = 3_072, 1_024
+    obs = sg.forward_sample_device(net, truth, cases, seed=120, hide_fraction=0.3, mask_seed=220)
+    dense = obs[:, :cases].cpu()
+    host = sg.HostSource.from_dense(dense, mb, cycle=2)
+    # the device source sees the two replays as one matrix of twice the cases
+    devsrc = sg.DeviceSource(torch.cat([dense, dense], dim=1).cuda(), 2 * cases, mb)
+    cfg = sg.SamplerConfig(same_m=3, minibatch_size=mb, num_passes=2, seed=11, rng="fast",
+                           accumulator_mode=acc, exp_decay=0.9)
+    a, _ = sg.run(net, host, cfg)
+    b, _ = sg.run(net, devsrc, cfg)
+    for x, y in zip(a.tables, b.tables):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_host_source_padding_equals_matrix_source(c4):
+    """A final partial block (padded with missing cells of weight 0) streams
+    exactly like the reference-style host matrix source."""
+    net, truth = c4
+    cases, mb = 2_500, 1_024
+    obs = sg.forward_sample_device(net, truth, cases, seed=121, hide_fraction=0.3, mask_seed=221)
+    dense = obs[:, :cases].cpu().numpy()
+    cfg = sg.SamplerConfig(same_m=2, minibatch_size=mb, num_passes=2, seed=12, rng="fast",
+                           accumulator_mode="exponential", exp_decay=0.8)
+    a, _ = sg.run(net, sg.HostSource.from_dense(dense, mb), cfg)
+    b, _ = sg.run(net, sg.DataMatrix.from_dense(dense.astype(np.int32)), cfg)
+    for x, y in zip(a.tables, b.tables):
+        np.testing.assert_array_equal(x, y)
