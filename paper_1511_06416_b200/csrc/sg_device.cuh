@@ -13,6 +13,8 @@
 // FMA: the reference rounds each numpy operation separately.
 #pragma once
 
+#include <utility>
+
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -320,6 +322,31 @@ __device__ __forceinline__ void table_entry(const double* w, int card, double* p
   if (pe) pe[card - 1] = norm;
   if (!ok) atomicOr(reinterpret_cast<int*>(zs_flag), 1);
 }
+
+// Programmatic dependent launch (PDL).  A kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor in the stream is still running; pdl_wait() blocks until that
+// predecessor has completed and its writes are visible (a no-op without
+// PDL), pdl_trigger() lets this kernel's own dependent start its prologue.
+// Launch with programmatic stream serialization (PDL; see pdl_wait).
+template <typename... P, typename... A>
+static inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ int small_field(uint32_t S, const sg_small& sp, int v) {
   return int((S >> sp.off[v]) & ((1u << sp.width[v]) - 1u));

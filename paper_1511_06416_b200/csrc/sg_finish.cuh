@@ -8,6 +8,24 @@
 
 namespace sg {
 
+// Debug build only (-DSG_FINISH_TRACE): %globaltimer at the phase boundaries
+// of the step tail, read back with sg_debug_finish_trace (tools/trace_finish.py).
+#ifdef SG_FINISH_TRACE
+__device__ unsigned long long g_finish_trace[8];
+#define SG_TRACE(i)                                                                             \
+  do {                                                                                          \
+    if (threadIdx.x == 0) {                                                                     \
+      unsigned long long t;                                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                                     \
+      g_finish_trace[i] = t;                                                                    \
+    }                                                                                           \
+  } while (0)
+#else
+#define SG_TRACE(i) \
+  do {              \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double acc_cell(int mode, double t, double add, bool has_prev, double prev, double decay) {
   if (mode == SG_ACC_MOVING) {
     if (has_prev) t = __dadd_rn(t, __dmul_rn(-1.0, prev));
@@ -108,9 +126,15 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
   int32_t* b32 = reinterpret_cast<int32_t*>(b64 + gnet.blob64_words);
   const int tid = threadIdx.x;
   const int cells = int(gnet.cells);
+  SG_TRACE(7);
   for (int i = tid; i < int(gnet.blob64_words); i += nt) b64[i] = __ldg(gnet.blob64 + i);
   for (int i = tid; i < int(gnet.blob32_words); i += nt) b32[i] = __ldg(gnet.blob32 + i);
-  const uint64_t key = f.key_dev ? __ldg(f.key_dev) : f.key;
+  // Everything above reads the static network pack; from here on the inputs
+  // are the sweep's counts and the previous tail's key cursor (PDL).  Once
+  // they are complete the next sweep may start its own prologue.
+  pdl_wait();
+  pdl_trigger();
+  const uint64_t key = f.key_dev ? *f.key_dev : f.key;
   if (tid == 0 && gnet.table_entries > 0) f.ftab[gnet.ftab_size] = 0u;
   __syncthreads();
   const sg_net net = rebase_net(gnet, b32, b64);
@@ -128,6 +152,7 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     }
   }
   __syncthreads();
+  SG_TRACE(2);
   // 2. CPT update, one row per thread
   for (int row = tid; row < int(net.rows); row += nt) {
     const int v = net.row_var[row];
@@ -141,6 +166,7 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     for (int s2 = 0; s2 < card; ++s2) f.cpt[base + s2] = cpt_s[base + s2];
   }
   __syncthreads();
+  SG_TRACE(3);
   // 3. conditional tables from the new CPTs (packed-only: the packed words directly)
   if (f.packed_only) {
     const sg_small& sp = f.sp;
@@ -169,11 +195,13 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     });
   }
   __syncthreads();
+  SG_TRACE(4);
   // 4. packed-lane tables
   if (f.has_small && !f.packed_only) {
     const sg_small& sp = f.sp;
     for (int i = tid; i < (sp.n << sp.bits); i += nt) small_table_entry<false>(net, sp, f.ftab, f.stab, i);
   }
+  SG_TRACE(5);
   // 5. clear the next visit's count buffer, advance the key cursor
   if (f.clear_counts)
     for (int i = tid; i < cells; i += nt) f.clear_counts[i] = 0ull;
@@ -184,6 +212,7 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     __syncthreads();
     if (tid == 0) *f.key_index = idx + 1;
   }
+  SG_TRACE(6);
 }
 
 

@@ -133,7 +133,7 @@ extern "C" int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_fi
       cudaFuncSetAttribute(k_step_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       configured = smem;
     }
-    k_step_finish<<<1, FINISH_THREADS, smem, s>>>(*net, a);
+    launch_pdl(k_step_finish, dim3(1), dim3(FINISH_THREADS), smem, s, *net, a);  // staging overlaps the sweep
     return check_launch("sg_step_finish");
   }
   // large models: the same steps as separate grid-wide launches
@@ -152,3 +152,9 @@ extern "C" int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_fi
   if (f->key_table) return sg_keys_advance(f->key_table, f->key_index, f->kps, f->key_current, stream);
   return check_launch("sg_step_finish");
 }
+
+#ifdef SG_FINISH_TRACE
+extern "C" int sg_debug_finish_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, sg::g_finish_trace, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 2;
+}
+#endif

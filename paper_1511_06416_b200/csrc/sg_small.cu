@@ -197,19 +197,16 @@ template <int N, int QG, bool ARMED>
 __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs, const uint32_t* stab,
                                             uint32_t* lanes, const uint8_t* __restrict__ pattern,
                                             const int32_t* __restrict__ case_id, uint32_t hist_a, int cases,
-                                            int num_real, int64_t case_base, const FastKey& fk, bool counts) {
+                                            int num_real, int64_t case_base, const FastKey& fk, bool counts,
+                                            const uint32_t (&nw0)[QG], uint32_t nP0, int nc0) {
   const int stride = gridDim.x * SG_THREADS;
   bool zs = false;
   int s = blockIdx.x * SG_THREADS + threadIdx.x;
-  uint32_t nw[QG], nP = 0;
-  int nc = 0;
-  uint32_t* rows = lanes + qs.row0;
-  if (s < cases) {
+  uint32_t nw[QG], nP = nP0;
+  int nc = nc0;
 #pragma unroll
-    for (int g = 0; g < QG; ++g) nw[g] = rows[min(g, qs.last) * qs.ld + s];
-    nP = pattern[s];
-    nc = case_id[s];
-  }
+  for (int g = 0; g < QG; ++g) nw[g] = nw0[g];
+  uint32_t* rows = lanes + qs.row0;
   for (; s < cases; s += stride) {
     uint32_t w[QG];
 #pragma unroll
@@ -289,11 +286,11 @@ __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs
 // owns the QG lane words of a slot (QG x 4 replicas of one case).
 template <int N, int QG>
 __global__ void __launch_bounds__(SG_THREADS, QG <= 2 ? 4 : 3)
-k_small_sweep(const sg_small sp, const SmallOrd o, const uint32_t* __restrict__ stab_g,
+k_small_sweep(const sg_small sp, const SmallOrd o, const uint32_t* stab_g,
               const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes,
               int lane_ld, int cases, int num_real, int m, int64_t case_base, uint64_t key,
-              const uint64_t* __restrict__ key_dev, const int32_t* __restrict__ jcell, int cells,
-              unsigned long long* __restrict__ counts, const uint32_t* __restrict__ zs_flag,
+              const uint64_t* key_dev, const int32_t* __restrict__ jcell, int cells,
+              unsigned long long* __restrict__ counts, const uint32_t* zs_flag,
               const int8_t* __restrict__ obs, int ld_obs, int32_t* err) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* stab = reinterpret_cast<uint32_t*>(smem);
@@ -303,13 +300,32 @@ k_small_sweep(const sg_small sp, const SmallOrd o, const uint32_t* __restrict__ 
   const int Q = (m + 3) >> 2;
   const int q0 = blockIdx.y * QG;
   const int last = min(QG - 1, Q - 1 - q0);
-  for (int i = tid; i < sp.tab_words; i += SG_THREADS) stab[i] = __ldg(stab_g + i);
+  // PDL prologue: the step tail that follows may start staging its static
+  // data now; this kernel's own prologue (counters, first slot's lane words,
+  // pattern and case id -- none of them written by the preceding tail) runs
+  // before waiting for that tail's tables, key and cleared counts.
+  pdl_trigger();
   if (counts) {
     uint32_t* h32 = reinterpret_cast<uint32_t*>(hist8);
     for (int i = tid; i < (SG_THREADS << sp.bits) / 4; i += SG_THREADS) h32[i] = 0;
     for (int i = tid; i < cells; i += SG_THREADS) cellacc[i] = 0;
   }
-  const bool armed = zs_flag && __ldg(zs_flag) != 0u;
+  uint32_t nw0[QG] = {};
+  uint32_t nP0 = 0;
+  int nc0 = 0;
+  {
+    const int s0 = blockIdx.x * SG_THREADS + tid;
+    if (s0 < cases) {
+      const uint32_t* r0p = lanes + int64_t(q0) * lane_ld;
+#pragma unroll
+      for (int g = 0; g < QG; ++g) nw0[g] = r0p[int64_t(min(g, last)) * lane_ld + s0];
+      nP0 = pattern[s0];
+      nc0 = case_id[s0];
+    }
+  }
+  pdl_wait();
+  for (int i = tid; i < sp.tab_words; i += SG_THREADS) stab[i] = stab_g[i];
+  const bool armed = zs_flag && *zs_flag != 0u;
   QuadSet qs;
   qs.row0 = uint32_t(q0) * uint32_t(lane_ld);
   qs.ld = uint32_t(lane_ld);
@@ -319,12 +335,12 @@ k_small_sweep(const sg_small sp, const SmallOrd o, const uint32_t* __restrict__ 
   qs.last_valid = qs.last_nl >= 4 ? 0xFFFFFFFFu : ((1u << (8 * qs.last_nl)) - 1u);
   const int slot = ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
   const uint32_t hist_a = uint32_t(__cvta_generic_to_shared(hist8)) + uint32_t(slot);
-  const FastKey fk = fast_key(key_dev ? __ldg(key_dev) : key);
+  const FastKey fk = fast_key(key_dev ? *key_dev : key);
   __syncthreads();
   const bool zs = armed ? small_units<N, QG, true>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real,
-                                                   case_base, fk, counts != nullptr)
+                                                   case_base, fk, counts != nullptr, nw0, nP0, nc0)
                         : small_units<N, QG, false>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real,
-                                                    case_base, fk, counts != nullptr);
+                                                    case_base, fk, counts != nullptr, nw0, nP0, nc0);
   if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
   if (obs) {  // the minibatch's range check (sampler.py:429-430), spread over the whole grid
     const int chunks = (cases + 15) >> 4;
@@ -406,10 +422,10 @@ static void launch_small(const sg_small& sp, const SmallOrd& o, int groups, size
   const int64_t fill = (int64_t(cases) + SG_THREADS - 1) / SG_THREADS;
   const int64_t want = std::max<int64_t>(resident_ctas<N, QG>(smem) / groups, need);
   const dim3 grid(unsigned(std::max<int64_t>(1, std::min<int64_t>(want, fill))), unsigned(groups));
-  k_small_sweep<N, QG><<<grid, SG_THREADS, smem, st>>>(sp, o, stab, pattern, case_id, lanes, lane_ld, cases,
-                                                       num_real, m, case_base, key, key_dev, jcell, cells,
-                                                       reinterpret_cast<unsigned long long*>(counts), zs_flag, obs,
-                                                       ld_obs, err);
+  // PDL: the sweep's prologue overlaps the preceding step tail (pdl_wait)
+  launch_pdl(k_small_sweep<N, QG>, grid, dim3(SG_THREADS), smem, st, sp, o, stab, pattern, case_id, lanes, lane_ld,
+             cases, num_real, m, case_base, key, key_dev, jcell, cells, reinterpret_cast<unsigned long long*>(counts),
+             zs_flag, obs, ld_obs, err);
 }
 
 static size_t small_smem(const sg_small& sp, int cells) {
