@@ -1,0 +1,72 @@
+"""Host-side API behaviour that needs no GPU (reference tests/test_sampler.py
+and tests/test_network.py pin the same): annealing schedules, configuration
+validation, SAME replication of a minibatch, network validation and colouring."""
+
+import numpy as np
+import pytest
+
+import paper_1511_06416_b200 as sg
+from paper_1511_06416_b200.sampler import pad_block, replicate_minibatch
+
+
+def test_anneal_schedule_pieces():
+    assert sg.anneal_m(((1, 50), (5, 150)), 10) == 1
+    assert sg.anneal_m(((1, 50), (5, 150)), 60) == 5
+    assert sg.anneal_m(5, 123) == 5 and sg.anneal_m(((5, 10),), 3) == 5
+    assert sg.anneal_m(((1, 5), (7, 5)), 1000) == 7
+    with pytest.raises(ValueError):
+        sg.anneal_m((), 0)
+    with pytest.raises(ValueError):
+        sg.anneal_m(3, -1)
+
+
+@pytest.mark.parametrize("kw", [dict(accumulator_mode="exponential", exp_decay=0.0),
+                                dict(accumulator_mode="decaying"), dict(same_m=0), dict(same_m=[(1, 0)]),
+                                dict(rng="mersenne")])
+def test_config_validation(kw):
+    with pytest.raises(ValueError):
+        sg.SamplerConfig(**kw)
+
+
+def test_replication_shares_observed_cells():
+    dense = np.array([[0, 1, -1, 0], [-1, 2, 1, -1]], dtype=np.int32)
+    batch = replicate_minibatch(pad_block(0, dense, 4), 3)
+    assert batch.num_lanes == 12
+    for r in range(3):
+        lane = batch.values[:, r * 4:(r + 1) * 4]
+        np.testing.assert_array_equal(lane[dense >= 0], dense[dense >= 0])
+    for v in range(2):  # latent lanes listed in the reference's lane order r*B + c
+        want = [r * 4 + c for r in range(3) for c in range(4) if dense[v, c] < 0]
+        np.testing.assert_array_equal(batch.missing_lanes[v], want)
+    one = replicate_minibatch(pad_block(0, dense[:1], 4), 1)
+    np.testing.assert_array_equal(one.values, dense[:1])
+
+
+def test_padding_has_zero_weight():
+    mb = pad_block(2, np.array([[0, 1, 1]], dtype=np.int32), 8)
+    assert mb.size == 8 and mb.num_real == 3
+    np.testing.assert_array_equal(mb.weights, [1, 1, 1, 0, 0, 0, 0, 0])
+    assert (np.asarray(mb.values)[:, 3:] == -1).all()
+
+
+@pytest.mark.parametrize("cards,edges,err", [
+    ([2, 2], [(0, 1), (1, 0)], "CycleDetected"),
+    ([2, 2], [(0, 2)], "InvalidIndex"),
+    ([2, 2], [(0, 1), (0, 1)], "DuplicateEdge"),
+    ([1, 2], [(0, 1)], "CardinalityTooSmall"),
+])
+def test_network_validation_errors(cards, edges, err):
+    with pytest.raises(getattr(sg, err)):
+        sg.build_network(cards, edges)
+
+
+def test_colouring_is_proper_and_covers_every_variable():
+    from paper_1511_06416_b200 import netgen
+
+    net = netgen.random_dag_network(200, max_parents=4, seed=9)
+    g = sg.moralize(net)
+    col = sg.color_graph(g)
+    colour = {v: k for k, grp in enumerate(col.groups) for v in grp}
+    assert sorted(colour) == list(range(net.num_vars))
+    for a, b in g.edges:
+        assert colour[a] != colour[b]
