@@ -370,6 +370,13 @@ int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_finish* f, vo
 int sg_keys_advance(const uint64_t* table, int32_t* index, int32_t kps,
                     uint64_t* current, void* stream);
 
+/* 4-bit observation rows (.sgb nibble encoding, io.py) -> int8 rows:
+   byte j of a packed row holds cases 2j (low nibble) and 2j+1 (high);
+   15 = missing -> -1.  Replaces nothing in the reference (its data files
+   are text, io.py:105-153); it halves the bytes an out-of-core source moves. */
+int sg_unpack_nibbles(const uint8_t* packed, int64_t ld_packed, int8_t* out, int64_t ld_out,
+                      int32_t rows, int64_t cases, void* stream);
+
 /* Largest state of each variable's observed cells (range check, sampler.py:429-430). */
 int sg_check_range(const sg_net* net, const int8_t* obs, int32_t ld_obs,
                    int32_t cases, int32_t* err, void* stream);

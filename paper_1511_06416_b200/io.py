@@ -1,4 +1,5 @@
-"""Network / CPT JSON files (reference ``samegibbs/io.py:53-102``).
+"""Network / CPT JSON files (reference ``samegibbs/io.py:53-102``) and the
+binary ``.sgb`` observation format with its streaming source.
 
 A network file is a JSON object with ``cardinalities``, ``edges`` (list of
 [parent, child]) and optional ``cpts`` (one row-major list per variable, rows
@@ -9,10 +10,13 @@ schema with ``cpts`` present.
 from __future__ import annotations
 
 import json
+import struct
 from pathlib import Path
 
 import numpy as np
+import torch
 
+from .datagen import _BlockStream
 from .errors import IoError, ParseError
 from .model import CptSet
 from .network import Network, build_network
@@ -68,3 +72,118 @@ def write_network_file(path, net: Network, cpts: CptSet | None = None) -> None:
     if cpts is not None:
         obj["cpts"] = [np.asarray(t).ravel().tolist() for t in cpts.tables]
     Path(path).write_text(json.dumps(obj, indent=1) + "\n")
+
+
+# ---------------------------------------------------------------- binary observation files
+#
+# The reference's data files are text (io.py:105-153: CSV triples read through
+# pandas), which cannot feed a GPU at 10^8 cases x 1000 variables.  ``.sgb``
+# stores the observation matrix in the layout the device consumes, as
+# minibatch blocks:
+#
+#   header (64 bytes, little endian): b"SGB1", version u32 = 1, num_vars u32,
+#       num_cases u64, block_cases u32, pitch u32, encoding u32 (0 = int8,
+#       1 = 4-bit), zero padding
+#   blocks: ceil(num_cases / block_cases) x num_vars rows of `pitch` cases
+#       (case c of block b = case b * block_cases + c; columns past the data
+#       are missing).  int8: one byte per cell, -1 = missing.  4-bit: two
+#       cells per byte (case 2j in the low nibble), 15 = missing, so cards
+#       <= 15; decoded on the device by sg_unpack_nibbles.
+
+_SGB_MAGIC = b"SGB1"
+_SGB_HEADER = struct.Struct("<4sIIQIII")
+
+
+def write_binary(path, data, block_cases: int, encoding: str = "int8") -> None:
+    """Write a DataMatrix or a dense (num_vars, num_cases) int matrix (-1 = missing) as ``.sgb``."""
+    from .datagen import DataMatrix
+
+    if encoding not in ("int8", "nibble"):
+        raise ValueError(f"encoding must be 'int8' or 'nibble', got {encoding!r}")
+    if isinstance(data, DataMatrix):
+        dense = data.to_dense()
+    else:
+        dense = np.asarray(data.cpu() if hasattr(data, "cpu") else data)
+    n, cases = dense.shape
+    if cases == 0:
+        raise ValueError("no cases to write")
+    limit = 15 if encoding == "nibble" else 128
+    if dense.max(initial=-1) >= limit or dense.min(initial=0) < -1:
+        raise ValueError(f"states must lie in [-1, {limit - 1}] for the {encoding} encoding")
+    pitch = max(32, (block_cases + 31) // 32 * 32)
+    nb = (cases + block_cases - 1) // block_cases
+    with open(path, "wb") as f:
+        head = _SGB_HEADER.pack(_SGB_MAGIC, 1, n, cases, block_cases, pitch, 0 if encoding == "int8" else 1)
+        f.write(head + bytes(64 - len(head)))
+        for b in range(nb):
+            lo, hi = b * block_cases, min(cases, (b + 1) * block_cases)
+            blk = np.full((n, pitch), -1, dtype=np.int8)
+            blk[:, :hi - lo] = dense[:, lo:hi]
+            if encoding == "nibble":
+                u = np.where(blk < 0, 15, blk).astype(np.uint8)
+                blk = (u[:, 0::2] | (u[:, 1::2] << 4)).astype(np.uint8)
+            f.write(blk.tobytes())
+
+
+def read_binary_header(path) -> dict:
+    with open(path, "rb") as f:
+        raw = f.read(64)
+    if len(raw) < 64:
+        raise IoError(f"{path}: truncated header")
+    magic, version, n, cases, block, pitch, enc = _SGB_HEADER.unpack(raw[:_SGB_HEADER.size])
+    if magic != _SGB_MAGIC or version != 1 or enc not in (0, 1):
+        raise ParseError(f"{path}: not an .sgb v1 file")
+    return {"num_vars": n, "num_cases": cases, "block_cases": block, "pitch": pitch,
+            "encoding": "int8" if enc == 0 else "nibble"}
+
+
+class BinaryFileSource(_BlockStream):
+    """Minibatch source streaming an ``.sgb`` file from disk (reference source
+    protocol, sampler.py:393-398; ``FileSource`` io.py:156-240 for text).
+
+    Minibatches are the file's blocks.  Block i+1 is read from disk straight
+    into one of two pinned buffers and copied on a side stream while the
+    consumer works on block i (4-bit files are decoded on the device).
+    ``cycle`` replays the file that many times per pass.
+    """
+
+    def __init__(self, path, cycle: int = 1):
+        h = read_binary_header(path)
+        self.path = Path(path)
+        self.header = h
+        self.nibbles = h["encoding"] == "nibble"
+        self._row_bytes = h["pitch"] // 2 if self.nibbles else h["pitch"]
+        self._block_bytes = h["num_vars"] * self._row_bytes
+        self._nb = (h["num_cases"] + h["block_cases"] - 1) // h["block_cases"]
+        size = self.path.stat().st_size
+        if size < 64 + self._nb * self._block_bytes:
+            raise IoError(f"{path}: truncated ({size} bytes)")
+        self._setup(h["num_vars"], h["pitch"], h["num_cases"], h["block_cases"], cycle)
+        dt = torch.uint8 if self.nibbles else torch.int8
+        self._pinned = [torch.empty((h["num_vars"], self._row_bytes), dtype=dt).pin_memory() for _ in range(2)]
+        self._pinned_ev = [None, None]
+        self._turn = 0
+        self._pending = 0
+        self._file = None
+
+    def _num_blocks(self) -> int:
+        return self._nb
+
+    def _host_block(self, i: int) -> torch.Tensor:
+        k = self._turn
+        self._turn ^= 1
+        if self._pinned_ev[k] is not None:
+            self._pinned_ev[k].synchronize()  # the previous copy out of this buffer has drained
+        if self._file is None:
+            self._file = open(self.path, "rb", buffering=0)
+        self._file.seek(64 + i * self._block_bytes)
+        got = self._file.readinto(memoryview(self._pinned[k].numpy()).cast("B"))
+        if got != self._block_bytes:
+            raise IoError(f"{self.path}: short read of block {i}")
+        self._pending = k
+        return self._pinned[k]
+
+    def _copy(self, i: int, slot: int, after):
+        ev = super()._copy(i, slot, after)
+        self._pinned_ev[self._pending] = ev
+        return ev

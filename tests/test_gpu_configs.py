@@ -172,3 +172,40 @@ def test_host_source_padding_equals_matrix_source(c4):
     b, _ = sg.run(net, sg.DataMatrix.from_dense(dense.astype(np.int32)), cfg)
     for x, y in zip(a.tables, b.tables):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("encoding", ["int8", "nibble"])
+def test_binary_file_source_equals_matrix_source(tmp_path, koller, encoding):
+    """An .sgb file streamed from disk (4-bit rows decoded on the device)
+    drives exactly the run of the in-memory data, padding included."""
+    from paper_1511_06416_b200 import io
+
+    net, truth = koller
+    cases, mb = 5_000, 1_024
+    dense = sg.forward_sample_device(net, truth, cases, seed=130, hide_fraction=0.4, mask_seed=230)[:, :cases]
+    dense = dense.cpu().numpy().astype(np.int32)
+    path = tmp_path / "obs.sgb"
+    io.write_binary(path, dense, mb, encoding)
+    for rng in ("numpy", "fast"):
+        cfg = sg.SamplerConfig(same_m=3, minibatch_size=mb, num_passes=2, seed=13, rng=rng)
+        a, _ = sg.run(net, io.BinaryFileSource(path), cfg)
+        b, _ = sg.run(net, sg.DataMatrix.from_dense(dense), cfg)
+        for x, y in zip(a.tables, b.tables):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_unpack_nibbles_kernel():
+    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200.device import stream_handle
+
+    rng = np.random.default_rng(4)
+    rows, cases, ldp, ldo = 5, 1000, 512, 1024
+    vals = rng.integers(-1, 15, size=(rows, 2 * ldp)).astype(np.int64)
+    nib = np.where(vals < 0, 15, vals).astype(np.uint8)
+    packed = torch.from_numpy((nib[:, 0::2] | (nib[:, 1::2] << 4)).astype(np.uint8)).cuda()
+    out = torch.full((rows, ldo), 99, dtype=torch.int8, device="cuda")
+    _lib.call("sg_unpack_nibbles", packed.data_ptr(), ldp, out.data_ptr(), ldo, rows, cases, stream_handle())
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    np.testing.assert_array_equal(got[:, :cases], vals[:, :cases])
+    assert (got[:, cases:] == 99).all()

@@ -70,3 +70,34 @@ def test_colouring_is_proper_and_covers_every_variable():
     assert sorted(colour) == list(range(net.num_vars))
     for a, b in g.edges:
         assert colour[a] != colour[b]
+
+
+@pytest.mark.parametrize("encoding", ["int8", "nibble"])
+def test_sgb_writer_layout(tmp_path, encoding):
+    """.sgb blocks hold the dense matrix column-block by column-block
+    (4-bit: case 2j low nibble, 15 = missing)."""
+    from paper_1511_06416_b200 import io
+
+    rng = np.random.default_rng(3)
+    dense = rng.integers(-1, 4, size=(3, 70)).astype(np.int32)
+    path = tmp_path / "d.sgb"
+    io.write_binary(path, dense, 40, encoding)
+    h = io.read_binary_header(path)
+    assert (h["num_vars"], h["num_cases"], h["block_cases"], h["pitch"]) == (3, 70, 40, 64)
+    raw = np.fromfile(path, dtype=np.uint8, offset=64)
+    rb = 64 if encoding == "int8" else 32
+    blocks = raw.reshape(2, 3, rb)
+    for b in range(2):
+        want = np.full((3, 64), -1, dtype=np.int64)
+        seg = dense[:, b * 40:(b + 1) * 40]
+        want[:, :seg.shape[1]] = seg
+        if encoding == "int8":
+            got = blocks[b].view(np.int8).astype(np.int64)
+        else:
+            got = np.empty((3, 64), dtype=np.int64)
+            got[:, 0::2] = blocks[b] & 15
+            got[:, 1::2] = blocks[b] >> 4
+            got[got == 15] = -1
+        np.testing.assert_array_equal(got, want)
+    with pytest.raises(ValueError):
+        io.write_binary(tmp_path / "x.sgb", np.full((1, 4), 15), 4, "nibble")
