@@ -210,6 +210,93 @@ __device__ __forceinline__ void conditional_weights(const sg_net& net, int v, co
   }
 }
 
+// Direct evaluation for variables without a table (blanket too large): the
+// reference's weight product for one lane (sampler.py:226-240) from the
+// factored descriptor (sg_net.fac_desc) -- parent row, then each child's
+// factor in ascending child order, every product rounded as numpy rounds it
+// (no FMA).  `get(var)` returns the lane's current state of a variable
+// (shared-memory tile or packed column).  Children are taken two at a time
+// so their loads overlap.
+template <int K, class Get>
+__device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, const double* __restrict__ cpt,
+                                               Get get, double u, bool& zs) {
+  const int card = K ? K : fd[0];
+  const int npar = fd[1], nchl = fd[2];
+  int base = fd[3];
+  const int32_t* p = fd + 4;
+  for (int j = 0; j < npar; ++j, p += 2) {
+    const int2 e = *reinterpret_cast<const int2*>(p);
+    base += get(e.x) * e.y;
+  }
+  double w[K ? K : SG_MAX_CARD];
+#pragma unroll
+  for (int t = 0; t < (K ? K : card); ++t) w[t] = __ldg(cpt + base + t);
+  int k = 0;
+  for (; k + 1 < nchl; k += 2) {
+    int i0 = p[1] + get(p[0]);
+    const int s0 = p[3], n0 = p[4];
+    p += 6;
+    for (int q = 0; q < n0; ++q, p += 2) {
+      const int2 e = *reinterpret_cast<const int2*>(p);
+      i0 += get(e.x) * e.y;
+    }
+    int i1 = p[1] + get(p[0]);
+    const int s1 = p[3], n1 = p[4];
+    p += 6;
+    for (int q = 0; q < n1; ++q, p += 2) {
+      const int2 e = *reinterpret_cast<const int2*>(p);
+      i1 += get(e.x) * e.y;
+    }
+    double f0[K ? K : SG_MAX_CARD], f1[K ? K : SG_MAX_CARD];
+#pragma unroll
+    for (int t = 0; t < (K ? K : card); ++t) {
+      f0[t] = __ldg(cpt + i0 + t * s0);
+      f1[t] = __ldg(cpt + i1 + t * s1);
+    }
+#pragma unroll
+    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(__dmul_rn(w[t], f0[t]), f1[t]);
+  }
+  if (k < nchl) {
+    int i0 = p[1] + get(p[0]);
+    const int s0 = p[3], n0 = p[4];
+    p += 6;
+    for (int q = 0; q < n0; ++q, p += 2) {
+      const int2 e = *reinterpret_cast<const int2*>(p);
+      i0 += get(e.x) * e.y;
+    }
+#pragma unroll
+    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(w[t], __ldg(cpt + i0 + t * s0));
+  }
+  double norm;
+  if (K && K < 8) {  // numpy's pairwise sum is sequential below 8 terms
+    norm = 0.0;
+#pragma unroll
+    for (int t = 0; t < (K ? K : 1); ++t) norm = __dadd_rn(norm, w[t]);
+  } else {
+    norm = np_pairwise_sum(w, card);
+  }
+  if (!(norm > 0.0)) zs = true;
+  const double au = __dmul_rn(u, norm);
+  double cum = 0.0;
+  int x = 0;
+#pragma unroll
+  for (int t = 0; t < (K ? K - 1 : card - 1); ++t) {
+    cum = t ? __dadd_rn(cum, w[t]) : w[0];
+    x += (au > cum);
+  }
+  return x;
+}
+
+template <class Get>
+__device__ __forceinline__ int draw_factored(const int32_t* fd, const double* cpt, Get get, double u, bool& zs) {
+  switch (fd[0]) {
+    case 2: return draw_factored_k<2>(fd, cpt, get, u, zs);
+    case 3: return draw_factored_k<3>(fd, cpt, get, u, zs);
+    case 4: return draw_factored_k<4>(fd, cpt, get, u, zs);
+    default: return draw_factored_k<0>(fd, cpt, get, u, zs);
+  }
+}
+
 // Call f(std::integral_constant<int, K>) with K = card for the common small
 // cardinalities (register-resident weight arrays), K = 0 otherwise.
 template <class F>

@@ -122,92 +122,6 @@ __device__ __forceinline__ int block_scan(int x, int* s_warp, int* total) {
   return base + inc - x;
 }
 
-// Direct evaluation for variables without a table (blanket too large): the
-// reference's weight product for one lane (sampler.py:226-240) from the
-// factored descriptor (sg_net.fac_desc) -- parent row, then each child's
-// factor in ascending child order, every product rounded as numpy rounds it
-// (no FMA) -- with the states read straight from the shared-memory tile by
-// variable id.  Children are taken two at a time so their loads overlap.
-template <int K>
-__device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, const double* __restrict__ cpt,
-                                               const int8_t* st, int mtc, int lane, double u, bool& zs) {
-  const int card = K ? K : fd[0];
-  const int npar = fd[1], nchl = fd[2];
-  int base = fd[3];
-  const int32_t* p = fd + 4;
-  for (int j = 0; j < npar; ++j, p += 2) {
-    const int2 e = *reinterpret_cast<const int2*>(p);
-    base += int(st[e.x * mtc + lane]) * e.y;
-  }
-  double w[K ? K : SG_MAX_CARD];
-#pragma unroll
-  for (int t = 0; t < (K ? K : card); ++t) w[t] = __ldg(cpt + base + t);
-  int k = 0;
-  for (; k + 1 < nchl; k += 2) {
-    int i0 = p[1] + int(st[p[0] * mtc + lane]);
-    const int s0 = p[3], n0 = p[4];
-    p += 6;
-    for (int q = 0; q < n0; ++q, p += 2) {
-      const int2 e = *reinterpret_cast<const int2*>(p);
-      i0 += int(st[e.x * mtc + lane]) * e.y;
-    }
-    int i1 = p[1] + int(st[p[0] * mtc + lane]);
-    const int s1 = p[3], n1 = p[4];
-    p += 6;
-    for (int q = 0; q < n1; ++q, p += 2) {
-      const int2 e = *reinterpret_cast<const int2*>(p);
-      i1 += int(st[e.x * mtc + lane]) * e.y;
-    }
-    double f0[K ? K : SG_MAX_CARD], f1[K ? K : SG_MAX_CARD];
-#pragma unroll
-    for (int t = 0; t < (K ? K : card); ++t) {
-      f0[t] = __ldg(cpt + i0 + t * s0);
-      f1[t] = __ldg(cpt + i1 + t * s1);
-    }
-#pragma unroll
-    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(__dmul_rn(w[t], f0[t]), f1[t]);
-  }
-  if (k < nchl) {
-    int i0 = p[1] + int(st[p[0] * mtc + lane]);
-    const int s0 = p[3], n0 = p[4];
-    p += 6;
-    for (int q = 0; q < n0; ++q, p += 2) {
-      const int2 e = *reinterpret_cast<const int2*>(p);
-      i0 += int(st[e.x * mtc + lane]) * e.y;
-    }
-#pragma unroll
-    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(w[t], __ldg(cpt + i0 + t * s0));
-  }
-  double norm;
-  if (K && K < 8) {  // numpy's pairwise sum is sequential below 8 terms
-    norm = 0.0;
-#pragma unroll
-    for (int t = 0; t < (K ? K : 1); ++t) norm = __dadd_rn(norm, w[t]);
-  } else {
-    norm = np_pairwise_sum(w, card);
-  }
-  if (!(norm > 0.0)) zs = true;
-  const double au = __dmul_rn(u, norm);
-  double cum = 0.0;
-  int x = 0;
-#pragma unroll
-  for (int t = 0; t < (K ? K - 1 : card - 1); ++t) {
-    cum = t ? __dadd_rn(cum, w[t]) : w[0];
-    x += (au > cum);
-  }
-  return x;
-}
-
-__device__ __forceinline__ int draw_factored(const int32_t* fd, const double* cpt, const int8_t* st, int mtc,
-                                             int lane, double u, bool& zs) {
-  switch (fd[0]) {
-    case 2: return draw_factored_k<2>(fd, cpt, st, mtc, lane, u, zs);
-    case 3: return draw_factored_k<3>(fd, cpt, st, mtc, lane, u, zs);
-    case 4: return draw_factored_k<4>(fd, cpt, st, mtc, lane, u, zs);
-    default: return draw_factored_k<0>(fd, cpt, st, mtc, lane, u, zs);
-  }
-}
-
 struct ItemCtx {
   int8_t* st;
   int mtc, tc, m;  // m = replicas in this tile (local rows), r0 = global replica of local row 0
@@ -317,7 +231,10 @@ __device__ __forceinline__ void draw_cell(const ItemCtx& x, const sg_net& net, c
     } else {
       const int32_t* fd = net.fac_desc + __ldg(net.fac_start + v);
 #pragma unroll 1
-      for (int j = 0; j < 4; ++j) xs[j] = ok[j] ? draw_factored(fd, a.cpt, x.st, mtc, loc[j] * tc + c, u[j], zs) : 0;
+      for (int j = 0; j < 4; ++j) {
+        const int8_t* col = x.st + loc[j] * tc + c;
+        xs[j] = ok[j] ? draw_factored(fd, a.cpt, [&](int var) { return int(col[var * mtc]); }, u[j], zs) : 0;
+      }
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -614,6 +531,175 @@ k_tally(const sg_net net, const sg_batch bt, unsigned long long* counts,
   }
 }
 
+// ---------------------------------------------------------------- lane sweep
+//
+// Large networks (n > 32, card <= 16): one thread per lane (case c, replica r)
+// walks every variable in colour order, keeping its own column of states
+// bit-packed in shared memory (BITS per state) with one latent bit per
+// variable.  A single lane's sequential scan in colour order is exactly the
+// reference's group-by-group update of that lane (members of a group are
+// conditionally independent, lanes never interact), so there are no
+// colour-group barriers, no item compaction and no write races; the
+// variable is warp-uniform, so its descriptors are broadcast loads and the
+// draw kind never diverges.  A warp skips a variable no lane of it has
+// latent; otherwise only the latent lanes draw.  HBM traffic: every cell read
+// once, every latent cell written once (n * L * (1 + f) bytes).
+constexpr int LANE_T = 128;
+
+template <int BITS>
+struct LaneColumn {
+  uint32_t* st;  // state word w of this thread at st[w * LANE_T]
+  uint32_t* fl;  // latent word w at fl[w * LANE_T]
+  static constexpr int PER = 32 / BITS;
+  static constexpr uint32_t MASK = (1u << BITS) - 1u;
+  __device__ __forceinline__ int get(int v) const {
+    const uint32_t u = uint32_t(v);
+    return int((st[(u / PER) * LANE_T] >> ((u % PER) * BITS)) & MASK);
+  }
+  __device__ __forceinline__ void set(int v, int x) const {
+    const uint32_t u = uint32_t(v);
+    uint32_t& w = st[(u / PER) * LANE_T];
+    const uint32_t sh = (u % PER) * BITS;
+    w = (w & ~(MASK << sh)) | (uint32_t(x) << sh);
+  }
+  __device__ __forceinline__ bool latent(int v) const {
+    const uint32_t u = uint32_t(v);
+    return (fl[(u >> 5) * LANE_T] >> (u & 31)) & 1u;
+  }
+};
+
+template <int BITS>
+__host__ __device__ inline size_t lane_smem(int n) {
+  return size_t((n + 32 / BITS - 1) / (32 / BITS) + (n + 31) / 32) * LANE_T * 4;
+}
+
+template <int MODE, int BITS>
+__global__ void __launch_bounds__(LANE_T) k_sweep_lane(const sg_net net, const sg_batch bt, const SweepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_err;
+  const int n = net.n;
+  const int tid = threadIdx.x;
+  constexpr int PER = 32 / BITS;
+  const int sw = (n + PER - 1) / PER;
+  LaneColumn<BITS> col{reinterpret_cast<uint32_t*>(smem) + tid, reinterpret_cast<uint32_t*>(smem) + sw * LANE_T + tid};
+  // A warp holds G = min(m, 32) replicas of 32 / G consecutive cases (lane =
+  // case-in-warp * G + replica), so the replicas of a case -- which share the
+  // latent pattern -- sit together and a warp skips every variable none of
+  // its cases has latent.  Grid y = replica groups of G.
+  const int G = min(bt.m, 32), cpw = 32 / G;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int c = (blockIdx.x * (LANE_T / 32) + warp) * cpw + lane / G;
+  const int r = blockIdx.y * G + lane % G;
+  const bool active = lane < cpw * G && c < bt.cases && r < bt.m;
+  const int64_t vstride = int64_t(bt.m) * bt.pitch;
+  int8_t* base = bt.states + int64_t(active ? r : 0) * bt.pitch + (active ? c : 0);  // cell (v, r, c) at base[v * vstride]
+  if (tid == 0) s_err = 0;
+  // ---- stage this lane's column: states packed, latent flags as bits
+  if (active) {
+    for (int w0 = 0; w0 < n; w0 += 32) {
+      uint32_t flags = 0, lo = 0, hi = 0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const int v = w0 + k;
+        if (v < n) {
+          const uint32_t b = uint8_t(base[v * vstride]);
+          flags |= (b >> 7) << k;
+          const uint32_t x = b & 0x7Fu;
+          if (BITS == 2) {
+            if (k < 16) lo |= x << (2 * k);
+            else hi |= x << (2 * (k - 16));
+          } else {  // BITS == 4: 8 states per word, four words per 32 variables
+            col.st[((v) / PER) * LANE_T] = (k % PER == 0 ? 0u : col.st[(v / PER) * LANE_T]) | (x << ((v % PER) * 4));
+          }
+        }
+      }
+      if (BITS == 2) {
+        col.st[(w0 / 16) * LANE_T] = lo;
+        if (w0 + 16 < n) col.st[(w0 / 16 + 1) * LANE_T] = hi;
+      }
+      col.fl[(w0 >> 5) * LANE_T] = flags;
+    }
+  }
+  const uint64_t key = a.fast_key_dev ? __ldg(a.fast_key_dev) : a.fast_key;
+  const bool zs_armed = a.ftab && net.table_entries > 0 && __ldg(a.ftab + net.ftab_size) != 0u;
+  const uint64_t gcase = uint64_t(bt.case_base + c);
+  bool zs = false;
+  // ---- every variable in colour order
+  for (int i = 0; i < n; ++i) {
+    const int v = __ldg(net.order + i);
+    const bool lat = active && col.latent(v);
+    if (!__any_sync(0xffffffffu, lat)) continue;
+    if (!lat) continue;
+    double u;
+    uint32_t u31 = 0;
+    if (MODE == SG_RNG_FAST) {
+      const uint32_t w = pick(fast_block(key, gcase, uint32_t(v), uint32_t(r >> 2), 0u), r & 3);
+      u31 = w >> 1;
+      u = double(w) * 0x1.0p-32;
+    } else {
+      const int64_t idx = int64_t(r) * __ldg(bt.nmiss + v) + __ldg(bt.rank + int64_t(v) * bt.ld_rank + c);
+      u = MODE == SG_RNG_NUMPY ? np_uniform(uint64_t(idx), __ldg(a.keys + 2 * v), __ldg(a.keys + 2 * v + 1))
+                               : __ldg(a.uniforms + __ldg(a.inj_off + v) + idx);
+    }
+    const int32_t* dv = net.var_desc + v * SG_DESC_WORDS;
+    const int card = dv[0], nmb = dv[1];
+    int x = 0;
+    if (nmb >= 0) {  // conditional table indexed by the blanket configuration
+      int e = 0;
+      for (int k = 0; k < nmb; ++k) e += col.get(dv[4 + k]) * dv[4 + SG_DESC_MB + k];
+      if (MODE == SG_RNG_FAST) {
+        const uint32_t* th = a.ftab + dv[2] + e * (card - 1);
+        const uint32_t t0 = __ldg(th);
+        if (zs_armed && t0 == 0xFFFFFFFFu) zs = true;
+        x = u31 >= t0;
+        for (int q = 1; q < card - 1; ++q) x += u31 >= __ldg(th + q);
+      } else {
+        const double* p = a.ptab + dv[3] + int64_t(e) * card;
+        const double norm = __ldg(p + card - 1);
+        if (!(norm > 0.0)) zs = true;
+        const double au = __dmul_rn(u, norm);
+        for (int q = 0; q < card - 1; ++q) x += au > __ldg(p + q);
+      }
+    } else {
+      const int32_t* fd = net.fac_desc + __ldg(net.fac_start + v);
+      x = draw_factored(fd, a.cpt, [&](int var) { return col.get(var); }, u, zs);
+    }
+    col.set(v, x);
+  }
+  if (zs) atomicOr(&s_err, int(SG_ERR_ZERO_SUPPORT));
+  // ---- write back the latent cells (observed cells never change)
+  if (active) {
+    for (int v = 0; v < n; ++v)
+      if (col.latent(v)) base[v * vstride] = int8_t(0x80 | col.get(v));
+  }
+  __syncthreads();
+  if (tid == 0 && s_err) atomicOr(a.err, s_err);
+}
+
+template <int MODE, int BITS>
+static void launch_lane(const sg_net& net, const sg_batch& bt, const SweepArgs& a, cudaStream_t s) {
+  const size_t smem = lane_smem<BITS>(net.n);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_sweep_lane<MODE, BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  const int g = std::min(bt.m, 32), cases_per_cta = (LANE_T / 32) * (32 / g);
+  const dim3 grid((bt.cases + cases_per_cta - 1) / cases_per_cta, (bt.m + g - 1) / g);
+  k_sweep_lane<MODE, BITS><<<grid, LANE_T, smem, s>>>(net, bt, a);
+}
+
+// Whether a sweep takes the lane kernel: many variables, small cards, a
+// packed column that leaves room for several CTAs per SM, and SAME replicas
+// to fill the warps (with m = 1 a warp holds 32 cases and draws only where a
+// case is latent; the tile kernel's compaction measured faster there).
+static int lane_bits(const sg_net& net, int m) {
+  if (net.n <= 32 || net.max_card > 16 || m < 2) return 0;
+  const int bits = net.max_card <= 4 ? 2 : 4;
+  const size_t smem = bits == 2 ? lane_smem<2>(net.n) : lane_smem<4>(net.n);
+  return smem <= 100 * 1024 ? bits : 0;
+}
+
 // Chunked tally of a resident batch (large models).  blockIdx.y = a run of
 // consecutive variables whose cells fit a shared-memory histogram
 // (sg_net.tally_chunk), blockIdx.x = a slice of the cases.  For each variable
@@ -799,6 +885,25 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
     SG_REQUIRE(net->tally_chunk && net->tally_chunks > 0, "sg_sweep: network pack has no tally runs");
     a.counts = nullptr;  // the sweep itself counts nothing
   }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (const int bits = lane_bits(*net, batch->m)) {
+    // large network: lane-per-thread sweep, then the chunked tally
+    a.tally_mode = TALLY_NONE;
+    a.counts = nullptr;
+    switch (rng_mode * 2 + (bits == 2 ? 0 : 1)) {
+      case 0: launch_lane<SG_RNG_FAST, 2>(*net, *batch, a, s); break;
+      case 1: launch_lane<SG_RNG_FAST, 4>(*net, *batch, a, s); break;
+      case 2: launch_lane<SG_RNG_NUMPY, 2>(*net, *batch, a, s); break;
+      case 3: launch_lane<SG_RNG_NUMPY, 4>(*net, *batch, a, s); break;
+      case 4: launch_lane<SG_RNG_INJECTED, 2>(*net, *batch, a, s); break;
+      default: launch_lane<SG_RNG_INJECTED, 4>(*net, *batch, a, s); break;
+    }
+    if (counts) {
+      SG_REQUIRE(net->tally_chunk && net->tally_chunks > 0, "sg_sweep: network pack has no tally runs");
+      tally_chunked(*net, *batch, counts, s);
+    }
+    return check_launch("sg_sweep");
+  }
   size_t smem = 0;
   int st = choose_tile(*net, batch->m, batch->cases, a, small, &a.tc, &a.mg, &smem);
   if (st != SG_OK) {
@@ -806,7 +911,6 @@ extern "C" int sg_sweep(const sg_net* net, const sg_batch* batch, const double* 
     return st;
   }
   const dim3 blocks((batch->cases + a.tc - 1) / a.tc, (batch->m + a.mg - 1) / a.mg);
-  cudaStream_t s = (cudaStream_t)stream;
   switch (rng_mode * 2 + (small ? 1 : 0)) {
     case 0: launch_sweep<SG_RNG_FAST, false>(*net, *batch, a, blocks, smem, s); break;
     case 1: launch_sweep<SG_RNG_FAST, true>(*net, *batch, a, blocks, smem, s); break;
