@@ -7,6 +7,7 @@ both accumulator modes, and the posterior-mean limit of a fully observed run.
 
 import numpy as np
 import pytest
+import torch
 
 pytestmark = pytest.mark.gpu
 
@@ -169,3 +170,84 @@ def test_same_replication_shrinks_the_final_spread(rng):
         return float(np.std(np.stack(finals), axis=0).mean())
 
     assert spread(10) <= spread(1)
+
+
+def _zero_support_problem():
+    """A -> B with B = 1 impossible under every state of A: any latent A next
+    to an observed B = 1 has an all-zero full conditional (sampler.py:242-244)."""
+    net = sg.build_network([2, 2], [(0, 1)])
+    cpts = sg.CptSet([np.array([[0.5, 0.5]]), np.array([[1.0, 0.0], [1.0, 0.0]])])
+    dense = np.array([[0, -1, 1, -1], [0, 0, 0, 1]], dtype=np.int32)  # case 3: A latent, B = 1
+    return net, cpts, dense
+
+
+@pytest.mark.parametrize("rng", ["numpy", "fast"])
+@pytest.mark.parametrize("small", [True, False])
+def test_zero_support_is_flagged(rng, small):
+    """sg.sweep raises ZeroSupport like the reference; the engine's kernels
+    (generic and packed) set the device error word that run() turns into it."""
+    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200.engine import Engine
+
+    net, cpts, dense = _zero_support_problem()
+    if rng == "numpy" and not small:
+        batch = sg.replicate_minibatch(sg.pad_block(0, dense, 4), 2)
+        with pytest.raises(sg.ZeroSupport):
+            sg.sweep(net, sg.color_graph(sg.moralize(net)), cpts, batch, 7)
+    if rng == "numpy" and small:
+        pytest.skip("the packed-lane path is FAST-mode only")
+    # run() starts from Dirichlet(1) CPTs (full support), so plant the degenerate
+    # tables in an engine and sweep once
+    eng = Engine(net, sg.SamplerConfig(same_m=2, minibatch_size=4, num_passes=1, seed=1, rng=rng), small=small)
+    eng.cpt.copy_(torch.from_numpy(eng.pack.flatten(cpts.tables)))
+    eng.tables_fresh = False
+    eng.visit(sg.pad_block(0, dense, 4), 0, 2)
+    torch.cuda.synchronize()
+    assert eng.err.read() & _lib.SG_ERR_ZERO_SUPPORT
+
+
+def test_no_zero_support_when_the_impossible_case_is_observed():
+    """The reference raises only for latent lanes: the same CPTs with B = 1
+    never next to a latent A sweep cleanly."""
+    net, cpts, dense = _zero_support_problem()
+    dense = dense[:, :3].copy()
+    batch = sg.replicate_minibatch(sg.pad_block(0, dense, 3), 2)
+    counts = sg.sweep(net, sg.color_graph(sg.moralize(net)), cpts, batch, 7)
+    assert counts.tables[0].sum() == 6
+
+
+def test_large_cardinality_sweep_matches_oracle():
+    """Cards up to the device limit (64 states) go through the generic kernel
+    bit-exactly (numpy's 8-accumulator pairwise row sums for card >= 8)."""
+    import oracle as O
+
+    rng = np.random.default_rng(8)
+    cards, edges = [40, 3, 64, 5], [(0, 2), (1, 2), (2, 3)]
+    net = sg.build_network(cards, edges)
+    cpts = sg.CptSet([rng.dirichlet(np.full(c, 0.8), size=net.table_shape(v)[0]) for v, c in enumerate(cards)])
+    dense = np.stack([rng.integers(0, c, 300) for c in cards]).astype(np.int32)
+    dense[rng.random(dense.shape) < 0.5] = -1
+    onet = O.make_net(cards, edges)
+    values, missing = O.replicate(dense, 3)
+    O.init_latent(onet, values, missing, 5, 0, 0)
+    batch = sg.ReplicatedBatch(m=3, base_size=300, values=values.copy(), lane_weights=np.ones(900),
+                               missing_lanes=[x.copy() for x in missing])
+    counts = sg.sweep(net, sg.color_graph(sg.moralize(net)), cpts, batch, 123)
+    want = O.sweep(onet, O.greedy_coloring(onet), cpts.tables, values, missing, np.ones(900), 123)
+    np.testing.assert_array_equal(batch.values, values)
+    for a, b in zip(counts.tables, want):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("rng", ["numpy", "fast"])
+def test_all_observed_and_odd_sizes(koller, rng):
+    """No latent cells: the sweep changes nothing and counts the data; minibatch
+    sizes that are not multiples of 16 and a case count below the minibatch size."""
+    net, truth = koller
+    data = sg.forward_sample(net, truth, 37, seed=3)
+    cfg = sg.SamplerConfig(same_m=3, minibatch_size=50, num_passes=1, map_estimate=True,
+                           prior=sg.DirichletPrior(1e-12), seed=2, rng=rng)
+    cpts, trace = sg.run(net, data, cfg)
+    for a, b in zip(cpts.tables, _empirical(net, data.to_dense())):
+        np.testing.assert_allclose(a, b, atol=1e-9)
+    assert trace.records[0].vars_sampled == net.num_vars * 37 * 3
