@@ -147,7 +147,9 @@ typedef struct sg_batch {
   const int32_t* rank;      /* [dev] [n][ld_rank] latent rank of (v,c) among the
                                minibatch's latent cases of v (NUMPY / INJECTED) */
   int32_t ld_rank;
-  int32_t pad_;
+  int32_t latent_permille;  /* hint: latent share of the cells x 1000 (0 = unknown); large
+                               networks with dense latent cells (>= 800) and m >= 2 take the
+                               lane-per-thread sweep, the rest the big-tile sweep */
   const int64_t* nmiss;     /* [dev] [n] latent cases of v in the global minibatch */
 } sg_batch;
 

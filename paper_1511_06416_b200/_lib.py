@@ -54,7 +54,7 @@ class SgBatch(ctypes.Structure):
     _fields_ = [
         ("states", c_void_p), ("m", c_int32), ("cases", c_int32), ("pitch", c_int32),
         ("num_real", c_int32), ("case_base", c_int64), ("rank", c_void_p), ("ld_rank", c_int32),
-        ("pad_", c_int32), ("nmiss", c_void_p),
+        ("latent_permille", c_int32), ("nmiss", c_void_p),
     ]
 
 

@@ -116,6 +116,7 @@ class Engine:
         if self.use_small:
             self.stab = torch.empty(max(1, self.pack.small.tab_words), dtype=torch.int32, device=d)
         self.tables_fresh = False  # conditional tables reflect self.cpt
+        self._latent_hint = None   # latent share of the first generic minibatch (sg_batch.latent_permille)
 
     # ------------------------------------------------------------ helpers
     def _upload_keys(self, seed: int, label: str, context: tuple) -> None:
@@ -191,6 +192,10 @@ class Engine:
         else:
             db = stored if stored is not None else DeviceBatch(self.n, m, size, int(mb.num_real), self.dev,
                                                                self.case_base)
+            if stored is None:
+                if self._latent_hint is None:  # one host sync per engine: the sweep's kernel choice
+                    self._latent_hint = float((obs[:, :size] < 0).float().mean())
+                db.set_latent_hint(self._latent_hint)
             db.set_obs(obs)
             db.struct.num_real = int(mb.num_real)
             if self.rng_mode == _lib.SG_RNG_NUMPY:

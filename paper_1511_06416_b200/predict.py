@@ -33,8 +33,10 @@ def predict_missing(net, cpts, context, targets, num_samples: int, seed: int, bu
     t_cases = np.asarray([t[1] for t in targets], dtype=np.int64)
     cases = context.num_cases
     db = DeviceBatch(n, 1, cases, cases, dev)
+    dense = context.to_dense()
+    db.set_latent_hint((dense < 0).mean() if dense.size else 0.0)
     obs = torch.full((n, db.pitch), -1, dtype=torch.int8, device=dev)
-    obs[:, :cases] = torch.from_numpy(context.to_dense().astype(np.int8)).to(dev)
+    obs[:, :cases] = torch.from_numpy(dense.astype(np.int8)).to(dev)
     db.set_obs(obs)
     db.compute_ranks()
     s = stream_handle()

@@ -216,6 +216,10 @@ class DeviceBatch:
         self.struct = s
         self.ref = __import__("ctypes").byref(s)
 
+    def set_latent_hint(self, fraction: float) -> None:
+        """Latent share of the batch's cells (kernel choice for large networks, sg_batch.latent_permille)."""
+        self.struct.latent_permille = int(round(1000 * min(1.0, max(0.0, float(fraction)))))
+
     def set_obs(self, obs: torch.Tensor) -> None:
         """Attach the (n, pitch) int8 observation block the ranks refer to."""
         self.obs = obs
@@ -265,6 +269,7 @@ def _upload_lanes(values: np.ndarray, missing_lanes, m: int, cases: int, num_rea
     if missing_lanes is not None:
         for v, lanes in enumerate(missing_lanes):
             lat[v, np.asarray(lanes, dtype=np.int64)] = True
+    db.set_latent_hint(lat.mean() if lat.size else 0.0)
     st = np.zeros((n, m, db.pitch), dtype=np.int8)
     if (vals < 0).any() and missing_lanes is not None:
         # the reference samples cells listed in missing_lanes; any other cell must hold a state
