@@ -707,19 +707,38 @@ k_tally_chunked(const sg_net net, const sg_batch bt, unsigned long long* __restr
     const int card = __ldg(net.card + v);
     const int ps = __ldg(net.par_start + v), pe = __ldg(net.par_start + v + 1);
     const int64_t base = __ldg(net.cpt_off + v) - cell0;
+    // up to 4 parents in registers, so a quad's row loads are issued together
+    const int np4 = min(4, pe - ps);
+    int64_t poff[4] = {0, 0, 0, 0};
+    int pst[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < np4) {
+        poff[k] = int64_t(__ldg(net.par_var + ps + k)) * vstride;
+        pst[k] = __ldg(net.par_stride + ps + k);
+      }
+    const int64_t voff = int64_t(v) * vstride;
     for (int q = q0 + threadIdx.x; q < q1; q += SG_THREADS) {
       const int c = q * 4;
       const int nl = min(4, bt.num_real - c);
       for (int r = 0; r < bt.m; ++r) {
         const int8_t* col = bt.states + int64_t(r) * bt.pitch + c;
-        const uint32_t xv = __ldg(reinterpret_cast<const uint32_t*>(col + v * vstride)) & 0x7F7F7F7Fu;
+        const uint32_t xv = __ldg(reinterpret_cast<const uint32_t*>(col + voff)) & 0x7F7F7F7Fu;
+        uint32_t xp[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          xp[k] = k < np4 ? __ldg(reinterpret_cast<const uint32_t*>(col + poff[k])) & 0x7F7F7F7Fu : 0u;
         int cfg[4] = {0, 0, 0, 0};
-        for (int p = ps; p < pe; ++p) {
-          const uint32_t xp =
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cfg[j] += int((xp[k] >> (8 * j)) & 0xFF) * pst[k];
+        for (int p = ps + 4; p < pe; ++p) {  // parents beyond the fourth
+          const uint32_t x =
               __ldg(reinterpret_cast<const uint32_t*>(col + __ldg(net.par_var + p) * vstride)) & 0x7F7F7F7Fu;
           const int st = __ldg(net.par_stride + p);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) cfg[j] += int((xp >> (8 * j)) & 0xFF) * st;
+          for (int j = 0; j < 4; ++j) cfg[j] += int((x >> (8 * j)) & 0xFF) * st;
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
