@@ -149,6 +149,9 @@ __global__ void k_small_export(const sg_small sp, const sg_batch bt, const int32
 
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int j) { return __byte_perm(w, 0u, 0x4440 | j); }
 
+#ifndef SG_SMALL_MINB
+#define SG_SMALL_MINB(QG) ((QG) <= 3 ? 4 : 3)  // CTAs per SM the register budget targets (64 regs: no spills up to QG = 3)
+#endif
 #ifndef SG_VAR_UNROLL
 #define SG_VAR_UNROLL 1
 #endif
@@ -285,7 +288,7 @@ __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs
 // The sweep.  Grid (x: slot blocks, y: quad groups of QG quads).  A thread
 // owns the QG lane words of a slot (QG x 4 replicas of one case).
 template <int N, int QG>
-__global__ void __launch_bounds__(SG_THREADS, QG <= 2 ? 4 : 3)
+__global__ void __launch_bounds__(SG_THREADS, SG_SMALL_MINB(QG))
 k_small_sweep(const sg_small sp, const SmallOrd o, const uint32_t* stab_g,
               const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes,
               int lane_ld, int cases, int num_real, int m, int64_t case_base, uint64_t key,
