@@ -12,7 +12,7 @@
 // with n ~ 1000 variables an int8 tile of 512 cases would need 512 KB, so the
 // tile keeps the lane states bit-packed (BITS = 2 for cards <= 4, 4 for
 // <= 16) and the shared latent mask as one bit per (variable, case):
-// C4 (n = 1000, m = 1): ~450 cases in ~170 KB.  One CTA of 24 warps per SM;
+// C4 (n = 1000, m = 1): ~450 cases in ~170 KB.  One CTA of 32 warps per SM;
 // members of a colour group are handed to warps dynamically (their costs
 // differ) and the group ends with one CTA barrier.  Writes go to packed
 // words shared by 16 (8) cases of one variable row, i.e. by lanes of the
@@ -24,7 +24,13 @@
 namespace sg {
 
 #ifndef SG_BIG_T
-#define SG_BIG_T 768
+#define SG_BIG_T 1024      // threads per CTA
+#endif
+#ifndef SG_BIG_MINB
+#define SG_BIG_MINB 1      // CTAs per SM (register budget)
+#endif
+#ifndef SG_BIG_SMEM
+#define SG_BIG_SMEM (200 * 1024)  // tile budget (shared memory per CTA)
 #endif
 constexpr int BIG_T = SG_BIG_T;
 constexpr int BIG_W = BIG_T / 32;
@@ -64,7 +70,7 @@ __device__ __forceinline__ uint32_t flag_bits16(const int4 val) {
 }
 
 template <int MODE, int BITS>
-__global__ void __launch_bounds__(BIG_T, 1) k_sweep_big(const sg_net net, const sg_batch bt, const SweepArgs a) {
+__global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net net, const sg_batch bt, const SweepArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ int s_err;
   __shared__ int s_next;  // next colour-group member to hand out
@@ -240,7 +246,7 @@ static void launch_big(const sg_net& net, const sg_batch& bt, const SweepArgs& a
 bool sweep_big(const sg_net& net, const sg_batch& bt, const SweepArgs& a0, int rng_mode, cudaStream_t s) {
   if (net.n <= 32 || net.max_card > 16) return false;
   const int bits = net.max_card <= 4 ? 2 : 4;
-  constexpr size_t budget = 200 * 1024;
+  constexpr size_t budget = SG_BIG_SMEM;
   auto smem_of = [&](int mg, int tc) { return bits == 2 ? big_smem<2>(net.n, mg, tc) : big_smem<4>(net.n, mg, tc); };
   // widest tile (<= 1024 cases, multiple of 32) over all replicas; replica
   // groups only when even 64 cases do not fit
