@@ -54,7 +54,13 @@ def build(force: bool = False, verbose: bool = False, defines: tuple[str, ...] =
     target = Path(lib) if lib else LIB
     if not force and not defines and lib is None and not _stale():
         return LIB
-    out = CSRC / ("build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
+    if defines:  # variant objects under the repo-level build/ (git- and gpurun-ignored)
+        import hashlib
+
+        out = ROOT / "build" / ("obj_" + hashlib.sha1(" ".join(defines).encode()).hexdigest()[:10])
+        out.mkdir(parents=True, exist_ok=True)
+    else:
+        out = CSRC / "build"
     out.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:
