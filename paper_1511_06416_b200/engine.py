@@ -79,7 +79,7 @@ class SmallBatch:
 
 class Engine:
     def __init__(self, net: Network, cfg: SamplerConfig, case_base: int = 0, comm=None,
-                 small: bool | None = None):
+                 small: bool | None = None, exchange=None):
         self.net = net
         self.cfg = cfg
         self.dev = device()
@@ -88,6 +88,7 @@ class Engine:
         self.n = net.num_vars
         self.case_base = case_base
         self.comm = comm  # optional count all-reduce hook (multi-GPU, see parallel.py)
+        self.exchange = exchange  # NUMPY-mode sharding: global rank prefixes (parallel.rank_prefix_exchange)
         lay = self.pack.layout
         cells = self.pack.cells
         d = self.dev
@@ -200,6 +201,10 @@ class Engine:
             db.struct.num_real = int(mb.num_real)
             if self.rng_mode == _lib.SG_RNG_NUMPY:
                 db.compute_ranks()
+                if self.exchange is not None:  # ranks and counts over the global minibatch
+                    prefix, total = self.exchange(db.nmiss)
+                    db.rank += prefix.to(torch.int32)[:, None]
+                    db.nmiss.copy_(total)
             elif stored is None and moving:
                 db.compute_nmiss()  # latent counts for the memory accounting only
             if stored is None:

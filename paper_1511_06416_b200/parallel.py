@@ -38,6 +38,30 @@ def count_allreduce(group=None):
     return comm
 
 
+def rank_prefix_exchange(group=None):
+    """Engine ``exchange`` hook for NUMPY-mode sharding.
+
+    The reference draws lane (r, c) of variable v from position
+    ``r * nmiss_v + rank_v(c)`` of v's stream, with ranks and counts over the
+    GLOBAL minibatch.  Given this rank's latent counts per variable it returns
+    ``(prefix, total)``: the latent cases of v in lower-ranked shards (added
+    to the local ranks) and the global count -- so an N-rank run draws exactly
+    the uniforms of the 1-rank run over the same global minibatch."""
+
+    def exchange(nmiss: torch.Tensor):
+        world = dist.get_world_size(group)
+        parts = [torch.empty_like(nmiss) for _ in range(world)]
+        dist.all_gather(parts, nmiss, group=group)
+        me = dist.get_rank(group)
+        prefix = torch.zeros_like(nmiss)
+        for r in range(me):
+            prefix += parts[r]
+        total = torch.stack(parts).sum(dim=0)
+        return prefix, total
+
+    return exchange
+
+
 def init_from_env(backend: str = "nccl"):
     """Initialise torch.distributed from torchrun's environment; returns (rank, world, local_rank)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -65,4 +89,5 @@ def sharded_engine(net, cfg, num_cases: int, group=None):
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     lo, hi = shard_range(num_cases, world, rank)
     comm = count_allreduce(group) if world > 1 else None
-    return Engine(net, cfg, case_base=lo, comm=comm), lo, hi
+    exchange = rank_prefix_exchange(group) if world > 1 else None
+    return Engine(net, cfg, case_base=lo, comm=comm, exchange=exchange), lo, hi

@@ -33,13 +33,13 @@ def _problem(kind):
     return net, netgen.dirichlet_cpts(net, 1.0, seed=22), 3_000, 3
 
 
-def _run(kind, lo, hi, comm, passes=3):
+def _run(kind, rng, lo, hi, comm, exchange=None, passes=3):
     from paper_1511_06416_b200.engine import Engine
 
     net, truth, cases, m = _problem(kind)
     obs = sg.forward_sample_device(net, truth, hi - lo, seed=40, hide_fraction=0.4, mask_seed=41, case_base=lo)
-    cfg = sg.SamplerConfig(same_m=m, minibatch_size=hi - lo, num_passes=passes, seed=42, rng="fast")
-    eng = Engine(net, cfg, case_base=lo, comm=comm)
+    cfg = sg.SamplerConfig(same_m=m, minibatch_size=hi - lo, num_passes=passes, seed=42, rng=rng)
+    eng = Engine(net, cfg, case_base=lo, comm=comm, exchange=exchange)
     mb = next(iter(sg.DeviceSource(obs, hi - lo, hi - lo)))
     for p in range(passes):
         eng.visit(mb, p, m)
@@ -48,30 +48,33 @@ def _run(kind, lo, hi, comm, passes=3):
     return eng.cpt.cpu().numpy(), eng.prev_counts[0].cpu().numpy()
 
 
-def _worker(rank, world, port, kind, out):
+def _worker(rank, world, port, kind, rng, out):
     import torch.distributed as dist
 
-    from paper_1511_06416_b200.parallel import count_allreduce, shard_range
+    from paper_1511_06416_b200.parallel import count_allreduce, rank_prefix_exchange, shard_range
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     _, _, cases, _ = _problem(kind)
     lo, hi = shard_range(cases, world, rank)
-    out[rank] = _run(kind, lo, hi, count_allreduce())
+    out[rank] = _run(kind, rng, lo, hi, count_allreduce(), rank_prefix_exchange())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["koller", "dag200"])
-def test_two_ranks_equal_one_rank(kind):
+@pytest.mark.parametrize("kind,rng", [("koller", "fast"), ("dag200", "fast"), ("koller", "numpy"),
+                                      ("dag200", "numpy")])
+def test_two_ranks_equal_one_rank(kind, rng):
+    """NUMPY mode needs the global rank prefixes (parallel.rank_prefix_exchange):
+    with them the sharded run is bit-identical to the reference's own draws."""
     import torch.multiprocessing as mp
 
     _, _, cases, _ = _problem(kind)
     manager = mp.get_context("spawn").Manager()
     out = manager.dict()
-    mp.start_processes(_worker, args=(2, _free_port(), kind, out), nprocs=2, join=True, start_method="spawn")
-    cpt1, counts1 = _run(kind, 0, cases, None)
+    mp.start_processes(_worker, args=(2, _free_port(), kind, rng, out), nprocs=2, join=True, start_method="spawn")
+    cpt1, counts1 = _run(kind, rng, 0, cases, None)
     for r in (0, 1):
         cpt, counts = out[r]
         np.testing.assert_array_equal(counts, counts1)
