@@ -1,7 +1,6 @@
 // The model-sized tail of a minibatch step (accumulate -> CPT update ->
 // conditional tables -> packed tables -> clear next counts -> advance keys),
-// as a device function that one CTA runs.  Shared by k_step_finish
-// (sg_model.cu) and the fused packed sweep (sg_small.cu).
+// as a device function that one CTA runs (k_step_finish, sg_model.cu).
 #pragma once
 
 #include "sg_device.cuh"
@@ -116,8 +115,7 @@ __host__ __device__ inline size_t finish_smem(const sg_net& net) {
 // The step tail, run by ONE CTA of `nt` threads (tid = threadIdx.x).  The
 // network pack (two blobs) and the CPTs are staged in shared memory `smem`
 // (finish_smem bytes) so the dependent index chains of the table build hit
-// on-chip memory instead of L2.  Used by k_step_finish and by the last CTA
-// of the fused packed sweep (sg_small_step).
+// on-chip memory instead of L2.
 __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const FinishArgs& f, unsigned char* smem,
                                                  const int nt) {
   double* lg = reinterpret_cast<double*>(smem);

@@ -577,26 +577,21 @@ __global__ void __launch_bounds__(LANE_T) k_sweep_lane(const sg_net net, const s
   // ---- stage this lane's column: states packed, latent flags as bits
   if (active) {
     for (int w0 = 0; w0 < n; w0 += 32) {
-      uint32_t flags = 0, lo = 0, hi = 0;
-#pragma unroll 8
+      // 32 variables per step: their latent bits make one flag word and their
+      // states BITS packed words (16 or 8 states each)
+      uint32_t flags = 0, acc[BITS] = {};
+#pragma unroll
       for (int k = 0; k < 32; ++k) {
         const int v = w0 + k;
         if (v < n) {
           const uint32_t b = uint8_t(base[v * vstride]);
           flags |= (b >> 7) << k;
-          const uint32_t x = b & 0x7Fu;
-          if (BITS == 2) {
-            if (k < 16) lo |= x << (2 * k);
-            else hi |= x << (2 * (k - 16));
-          } else {  // BITS == 4: 8 states per word, four words per 32 variables
-            col.st[((v) / PER) * LANE_T] = (k % PER == 0 ? 0u : col.st[(v / PER) * LANE_T]) | (x << ((v % PER) * 4));
-          }
+          acc[k / PER] |= (b & 0x7Fu) << ((k % PER) * BITS);
         }
       }
-      if (BITS == 2) {
-        col.st[(w0 / 16) * LANE_T] = lo;
-        if (w0 + 16 < n) col.st[(w0 / 16 + 1) * LANE_T] = hi;
-      }
+#pragma unroll
+      for (int q = 0; q < BITS; ++q)
+        if (w0 + q * PER < n) col.st[(w0 / PER + q) * LANE_T] = acc[q];
       col.fl[(w0 >> 5) * LANE_T] = flags;
     }
   }

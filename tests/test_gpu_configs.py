@@ -209,3 +209,16 @@ def test_unpack_nibbles_kernel():
     got = out.cpu().numpy()
     np.testing.assert_array_equal(got[:, :cases], vals[:, :cases])
     assert (got[:, cases:] == 99).all()
+
+
+@pytest.mark.parametrize("hide,m", [(0.3, 1), (0.3, 6), (0.9, 3)])
+def test_four_bit_states_bit_exact(hide, m):
+    """Large networks with cards 5..8 keep 4-bit packed states: the big-tile
+    sweep (sparse latent cells) and the lane sweep (dense, m >= 2) stay
+    bit-exact against the oracle."""
+    net = netgen.random_dag_network(60, max_parents=3, min_card=2, max_card=8, seed=31)
+    assert max(net.cardinalities) > 4
+    truth = netgen.dirichlet_cpts(net, 1.0, seed=32)
+    obs = sg.forward_sample_device(net, truth, 900, seed=107, hide_fraction=hide, mask_seed=207)
+    dense = obs[:, :900].cpu().numpy().astype(np.int32)
+    _sweep_vs_oracle(net, truth, dense, m, 308, 9004)
