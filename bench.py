@@ -287,6 +287,10 @@ def our_arm(args, wl: Workload) -> None:
     CASES, M = wl.cases, wl.m
     net, truth = wl.network()
     n_vars = net.num_vars
+    if args.rng == "auto":
+        from paper_1511_06416_b200.device import netpack
+
+        args.rng = "joint" if netpack(net).joint is not None and M <= 32 else "fast"
     cfg = sg.SamplerConfig(same_m=M, minibatch_size=CASES, num_passes=1, seed=300, rng=args.rng)
     obs = wl.observations(net, truth, rank)
     comm = (lambda c: dist.all_reduce(c)) if world > 1 else None
@@ -402,7 +406,8 @@ def our_arm(args, wl: Workload) -> None:
         bpns = 1.0 + latent
         algo_bytes = bpns * node_samples
         achieved = algo_bytes / (sw * 1e-3) / 1e9
-        kernel = "k_small_sweep (sg_small_sweep)" if eng.use_small else "k_sweep (sg_sweep)"
+        kernel = ("k_joint_sweep (sg_joint_sweep)" if eng.joint else
+                  "k_small_sweep (sg_small_sweep)" if eng.use_small else "k_sweep (sg_sweep)")
         traffic, traffic_src = load_traffic(wl, kernel)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -419,8 +424,9 @@ def our_arm(args, wl: Workload) -> None:
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",
-            "kernel_path": "packed-lane sg_small_sweep + sg_step_finish" if eng.use_small else
-                           "generic sg_sweep + sg_step_finish",
+            "kernel_path": ("packed-lane sg_joint_sweep + sg_step_finish + sg_joint_tables" if eng.joint else
+                            "packed-lane sg_small_sweep + sg_step_finish" if eng.use_small else
+                            "generic sg_sweep + sg_step_finish"),
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
@@ -457,6 +463,8 @@ def stream_arm(args, wl: Workload) -> None:
     cycle = (args.warmup + steps + C5_HOST_BLOCKS - 1) // C5_HOST_BLOCKS
     src = sg.HostSource.from_dense(obs[:, :host_cases].cpu(), B, cycle=cycle)
     del obs
+    if args.rng == "auto":
+        args.rng = "fast"  # DAG-1000: no packed lane word
     cfg = sg.SamplerConfig(same_m=M, minibatch_size=B, num_passes=1, seed=300, rng=args.rng,
                            accumulator_mode="exponential", exp_decay=0.9)
     comm = (lambda c: dist.all_reduce(c)) if world > 1 else None
@@ -511,7 +519,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
-    ap.add_argument("--rng", choices=["fast", "numpy"], default="fast")
+    ap.add_argument("--rng", choices=["auto", "joint", "fast", "numpy"], default="auto",
+                    help="auto: joint (one draw per lane per sweep) when the network's lane word fits, else fast")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch each visit eagerly instead of graph replay")
     args = ap.parse_args()

@@ -320,6 +320,50 @@ int sg_small_sweep(const sg_small* sp, const uint32_t* stab, const uint8_t* patt
                    const int8_t* obs, int32_t ld_obs, int32_t* err,
                    void* stream);
 
+/* ---- joint sweep (rng = "joint") ------------------------------------------
+   The colour-ordered sweep of one packed lane as ONE draw from its sweep
+   transition kernel K_P(S -> S') (csrc/sg_small.cu, "joint sweep"): the
+   product, in colour-group order, of the full conditionals the reference's
+   gibbs_pass (sampler.py:251-284) draws from one variable at a time.  Same
+   Markov kernel, one uniform per lane per sweep.  Replaces
+   gibbs_pass + tally_counts (sampler.py:251-304, model.py:148-165) for
+   networks whose lane word has <= 6 bits.
+
+   Blob (uint32 [words], 16-byte aligned): a static header written once by
+   the host (netpack.joint_plan) -- [0,NP) byte offset of pattern P's rows,
+   [NP,2NP) B_P | keep_P << 8 | dep byte offset << 16, then dep_P[2^B_P]
+   (latent field bits of compact column j) -- and per pattern 2^bits rows of
+   2^B_P cumulative thresholds (2^31 scale) that sg_joint_tables rewrites
+   from the CPTs.  Rows are 2^B_P + 1 words apart (odd stride: the lanes of
+   a warp probing the same column of different rows hit different banks). */
+typedef struct sg_joint {
+  int32_t words;         /* uint32 words of the blob (multiple of 4) */
+  int32_t header_words;  /* static header words (multiple of 4) */
+  int32_t patterns;      /* NP = 2^n latent patterns */
+  int32_t max_b;         /* largest B_P (latent bits of one pattern) */
+} sg_joint;
+
+/* Rows of the joint blob from the CPTs (one CTA per pattern).  vprob: the
+   conditionals sg_step_finish wrote (sg_finish.vprob), or NULL to compute
+   them here from cpt. */
+int sg_joint_tables(const sg_net* net, const sg_small* sp, const sg_joint* jp,
+                    const double* cpt, const double* vprob, uint32_t* jblob, void* stream);
+
+/* Shared memory one joint-sweep CTA needs (eligibility: <= 227 KB). */
+int sg_joint_smem(const sg_small* sp, const sg_joint* jp, int32_t cells, int64_t* bytes);
+
+/* Sweep + tally on packed lanes with one uniform per lane (FAST Philox
+   counters with purpose 2, v = 0).  Arguments as sg_small_sweep plus the
+   joint plan and blob; when zs_flag is armed the per-variable path runs
+   instead (exact ZeroSupport semantics). */
+int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint32_t* stab,
+                   const uint32_t* jblob, const uint8_t* pattern, const int32_t* case_id,
+                   uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real,
+                   int32_t m, int64_t case_base, uint64_t key, const uint64_t* key_dev,
+                   const int32_t* jcell, int32_t cells, uint64_t* counts,
+                   const uint32_t* zs_flag, const int8_t* obs, int32_t ld_obs,
+                   int32_t* err, void* stream);
+
 /* Layout switches between packed lanes and sg_batch int8 lane states. */
 int sg_small_import(const sg_small* sp, const sg_batch* batch, const int32_t* case_id,
                     uint8_t* lanes, int32_t lane_ld, void* stream);
@@ -356,6 +400,8 @@ typedef struct sg_finish {
   int32_t kps;                /* keys per step */
   int32_t flags;              /* SG_FINISH_* bits */
   uint64_t* key_current;      /* [dev] [kps] */
+  double* vprob;              /* [dev] [n][2^bits][4] or NULL: the packed path's full conditionals
+                                 p_v(x | lane word) for sg_joint_tables (sp != NULL) */
 } sg_finish;
 
 /* sg_finish.flags: the packed table is the only consumer of this step's

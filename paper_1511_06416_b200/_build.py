@@ -62,14 +62,22 @@ def build(force: bool = False, verbose: bool = False, defines: tuple[str, ...] =
     else:
         out = CSRC / "build"
     out.mkdir(exist_ok=True)
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
+
+    cmds, objs = [], []
     for src in SOURCES:
         obj = out / (Path(src).stem + ".o")
-        cmd = [nvcc(), *flags(), *[f"-D{d}" for d in defines], "-c", str(CSRC / src), "-o", str(obj)]
+        cmds.append([nvcc(), *flags(), *[f"-D{d}" for d in defines], "-c", str(CSRC / src), "-o", str(obj)])
+        objs.append(str(obj))
+
+    def compile_one(cmd):
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-        objs.append(str(obj))
+
+    # translation units compile independently: one nvcc per source, in parallel
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        list(ex.map(compile_one, cmds))
     tmp = target.with_suffix(".so.tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
            "-Xcompiler", "-fPIC"]

@@ -69,13 +69,17 @@ class SgSmall(ctypes.Structure):
         [(name, ctypes.c_int32 * SMALL_MAXV) for name in ("card", "toff", "tstride")]
 
 
+class SgJoint(ctypes.Structure):
+    _fields_ = [("words", c_int32), ("header_words", c_int32), ("patterns", c_int32), ("max_b", c_int32)]
+
+
 class SgFinish(ctypes.Structure):
     _fields_ = [
         ("acc_mode", c_int32), ("map_estimate", c_int32), ("decay", c_double),
         ("total", c_void_p), ("new_counts", c_void_p), ("prev_counts", c_void_p), ("alpha", c_void_p),
         ("key", c_uint64), ("key_dev", c_void_p), ("cpt", c_void_p), ("ptab", c_void_p), ("ftab", c_void_p),
         ("stab", c_void_p), ("clear_counts", c_void_p), ("key_table", c_void_p), ("key_index", c_void_p),
-        ("kps", c_int32), ("flags", c_int32), ("key_current", c_void_p),
+        ("kps", c_int32), ("flags", c_int32), ("key_current", c_void_p), ("vprob", c_void_p),
     ]
 
 
@@ -104,6 +108,12 @@ _SIGNATURES = {
     "sg_small_sweep": ([POINTER(SgSmall), c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32,
                         c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
                         c_int32, c_void_p, c_void_p], c_int32),
+    "sg_joint_tables": ([POINTER(SgNet), POINTER(SgSmall), POINTER(SgJoint), c_void_p, c_void_p, c_void_p, c_void_p],
+                        c_int32),
+    "sg_joint_smem": ([POINTER(SgSmall), POINTER(SgJoint), c_int32, POINTER(ctypes.c_int64)], c_int32),
+    "sg_joint_sweep": ([POINTER(SgSmall), POINTER(SgJoint), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                        c_int32, c_int32, c_int32, c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32,
+                        c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p], c_int32),
     "sg_keys_advance": ([c_void_p, c_void_p, c_int32, c_void_p, c_void_p], c_int32),
     "sg_step_finish": ([POINTER(SgNet), c_void_p, POINTER(SgFinish), c_void_p], c_int32),
     "sg_unpack_nibbles": ([c_void_p, c_int64, c_void_p, c_int64, c_int32, c_int64, c_void_p], c_int32),
@@ -150,6 +160,7 @@ KERNELS_PER_CALL = {
     "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
     "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
+    "sg_joint_tables": 1, "sg_joint_sweep": 1,
     "sg_keys_advance": 1, "sg_step_finish": 1, "sg_unpack_nibbles": 1,
 }
 launch_count = 0

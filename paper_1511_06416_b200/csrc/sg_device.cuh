@@ -410,6 +410,16 @@ __device__ __forceinline__ void table_entry(const double* w, int card, double* p
   if (!ok) atomicOr(reinterpret_cast<int*>(zs_flag), 1);
 }
 
+// p_v(x | blanket) = w_x / norm for the joint sweep's transition tables
+// (sequential norm: cards <= 4), 0 where the blanket has no support.
+template <int K = 0>
+__device__ __forceinline__ void joint_conditional(const double* w, int card, double* out) {
+  if (K) card = K;
+  double norm = 0.0;
+  for (int t = 0; t < card; ++t) norm = __dadd_rn(norm, w[t]);
+  for (int t = 0; t < card; ++t) out[t] = norm > 0.0 ? __ddiv_rn(w[t], norm) : 0.0;
+}
+
 // Programmatic dependent launch (PDL).  A kernel launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization may start while its
 // predecessor in the stream is still running; pdl_wait() blocks until that

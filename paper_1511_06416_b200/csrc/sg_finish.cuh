@@ -70,6 +70,7 @@ struct FinishArgs {
   int32_t* key_index;
   int kps;
   uint64_t* key_current;
+  double* vprob;
   int has_small;
   int packed_only;  // SG_FINISH_PACKED_ONLY: skip ptab/ftab, build stab from the CPTs
   sg_small sp;
@@ -79,7 +80,7 @@ struct FinishArgs {
 // thresholds table_entry computes for the blanket configuration S encodes,
 // i.e. exactly the words small_table_entry copies out of ftab.
 __device__ __forceinline__ void small_table_direct(const sg_net& net, const sg_small& sp, const double* cpt,
-                                                   uint32_t* stab, uint32_t* zs_flag, int i) {
+                                                   uint32_t* stab, uint32_t* zs_flag, int i, double* vprob) {
   const int v = i >> sp.bits;
   const uint32_t S = uint32_t(i & ((1 << sp.bits) - 1));
   const int card = sp.card[v];
@@ -94,6 +95,8 @@ __device__ __forceinline__ void small_table_direct(const sg_net& net, const sg_s
   }
   if (!valid) {
     for (int t = 0; t < card - 1; ++t) out[t] = 0u;
+    if (vprob)
+      for (int t = 0; t < card; ++t) vprob[size_t(i) * 4 + t] = 0.0;
     return;
   }
   with_card(card, [&](auto C) {
@@ -101,6 +104,7 @@ __device__ __forceinline__ void small_table_direct(const sg_net& net, const sg_s
     double w[K ? K : SG_MAX_CARD];
     conditional_weights<false, K>(net, v, s, cpt, w);
     table_entry<K>(w, card, nullptr, out, zs_flag);
+    if (vprob) joint_conditional<K>(w, card, vprob + size_t(i) * 4);
   });
 }
 
@@ -169,7 +173,7 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
   if (f.packed_only) {
     const sg_small& sp = f.sp;
     for (int i = tid; i < (sp.n << sp.bits); i += nt)
-      small_table_direct(net, sp, cpt_s, f.stab, f.ftab + net.ftab_size, i);
+      small_table_direct(net, sp, cpt_s, f.stab, f.ftab + net.ftab_size, i, f.vprob);
   }
   for (int g = f.packed_only ? int(net.table_entries) : tid; g < int(net.table_entries); g += nt) {
     int lo = 0, hi = net.n;
@@ -235,6 +239,7 @@ inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
   a.key_index = f->key_index;
   a.kps = f->kps;
   a.key_current = f->key_current;
+  a.vprob = sp ? f->vprob : nullptr;
   a.has_small = sp ? 1 : 0;
   a.packed_only = (sp && (f->flags & SG_FINISH_PACKED_ONLY)) ? 1 : 0;
   if (sp) a.sp = *sp;

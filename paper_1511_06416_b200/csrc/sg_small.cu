@@ -196,15 +196,15 @@ __device__ __forceinline__ void hist_inc(uint32_t a) {
 // Walk this thread's slots: per latent variable (colour order), QG
 // independent Philox blocks (one per quad, sharing the case's first round),
 // then per quad 4 table lookups + compares and one byte-SIMD insert.
-template <int N, int QG, bool ARMED>
+template <int N, int QG, bool ARMED, int NT = SG_THREADS>
 __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs, const uint32_t* stab,
                                             uint32_t* lanes, const uint8_t* __restrict__ pattern,
                                             const int32_t* __restrict__ case_id, uint32_t hist_a, int cases,
                                             int num_real, int64_t case_base, const FastKey& fk, bool counts,
                                             const uint32_t (&nw0)[QG], uint32_t nP0, int nc0) {
-  const int stride = gridDim.x * SG_THREADS;
+  const int stride = gridDim.x * NT;
   bool zs = false;
-  int s = blockIdx.x * SG_THREADS + threadIdx.x;
+  int s = blockIdx.x * NT + threadIdx.x;
   uint32_t nw[QG], nP = nP0;
   int nc = nc0;
 #pragma unroll
@@ -275,14 +275,65 @@ __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs
       if (tally) {
         if (full) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) hist_inc(hist_a + (byte_of(wg, j) << 8));
+          for (int j = 0; j < 4; ++j) hist_inc(hist_a + byte_of(wg, j) * NT);
         } else {
-          for (int j = 0; j < qs.last_nl; ++j) hist_inc(hist_a + (byte_of(wg, j) << 8));
+          for (int j = 0; j < qs.last_nl; ++j) hist_inc(hist_a + byte_of(wg, j) * NT);
         }
       }
     }
   }
   return zs;
+}
+
+// The common end of both packed sweeps: ZeroSupport word, the minibatch's
+// range check (sampler.py:429-430) spread over the whole grid, and the
+// joint-state histogram (per-thread byte counters, hist8[J * NT + slot])
+// expanded to CPT cells through jcell and flushed with one global atomic per
+// touched cell.
+template <int N, int NT>
+__device__ __forceinline__ void small_epilogue(const sg_small& sp, bool zs, const uint8_t* hist8, uint32_t* cellacc,
+                                               const int32_t* __restrict__ jcell, int cells,
+                                               unsigned long long* __restrict__ counts,
+                                               const int8_t* __restrict__ obs, int ld_obs, int cases,
+                                               int32_t* err) {
+  const int tid = threadIdx.x;
+  if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
+  if (obs) {  // the minibatch's range check (sampler.py:429-430), spread over the whole grid
+    const int chunks = (cases + 15) >> 4;
+    const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + tid;
+    const int gthreads = gridDim.x * gridDim.y * NT;
+    unsigned bad = 0;
+    for (int i = gtid; i < N * chunks; i += gthreads) {
+      const int v = i / chunks, ch = i - v * chunks;
+      const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
+      const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
+      const uint32_t wv[4] = {uint32_t(qv.x), uint32_t(qv.y), uint32_t(qv.z), uint32_t(qv.w)};
+      const int left = cases - ch * 16;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t gt = __vcmpgts4(wv[k], lim);
+        const int valid = left - 4 * k;
+        if (valid < 4) gt &= valid <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - valid)));
+        bad |= gt;
+      }
+    }
+    if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
+  }
+  if (!counts) return;
+  __syncthreads();
+  const int warp = tid >> 5, lane_id = tid & 31;
+  for (int J = warp; J < (1 << sp.bits); J += NT / 32) {
+    const uint32_t* hrow = reinterpret_cast<const uint32_t*>(hist8 + J * NT);
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < NT / 128; ++k) sum = __dp4a(int(hrow[lane_id + 32 * k]), 0x01010101, sum);
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o2);
+    if (sum && lane_id < sp.n) atomicAdd(cellacc + __ldg(jcell + J * sp.n + lane_id), uint32_t(sum));
+  }
+  __syncthreads();
+  for (int cell = tid; cell < cells; cell += NT)
+    if (cellacc[cell]) atomicAdd(counts + cell, (unsigned long long)cellacc[cell]);
 }
 
 // The sweep.  Grid (x: slot blocks, y: quad groups of QG quads).  A thread
@@ -344,42 +395,7 @@ k_small_sweep(const sg_small sp, const SmallOrd o, const uint32_t* stab_g,
                                                    case_base, fk, counts != nullptr, nw0, nP0, nc0)
                         : small_units<N, QG, false>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real,
                                                     case_base, fk, counts != nullptr, nw0, nP0, nc0);
-  if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
-  if (obs) {  // the minibatch's range check (sampler.py:429-430), spread over the whole grid
-    const int chunks = (cases + 15) >> 4;
-    const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * SG_THREADS + tid;
-    const int gthreads = gridDim.x * gridDim.y * SG_THREADS;
-    unsigned bad = 0;
-    for (int i = gtid; i < N * chunks; i += gthreads) {
-      const int v = i / chunks, ch = i - v * chunks;
-      const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
-      const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
-      const uint32_t wv[4] = {uint32_t(qv.x), uint32_t(qv.y), uint32_t(qv.z), uint32_t(qv.w)};
-      const int left = cases - ch * 16;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint32_t gt = __vcmpgts4(wv[k], lim);
-        const int valid = left - 4 * k;
-        if (valid < 4) gt &= valid <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - valid)));
-        bad |= gt;
-      }
-    }
-    if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
-  }
-  if (!counts) return;
-  __syncthreads();
-  const int warp = tid >> 5, lane_id = tid & 31;
-  for (int J = warp; J < (1 << sp.bits); J += SG_THREADS / 32) {
-    const uint32_t* hrow = reinterpret_cast<const uint32_t*>(hist8 + (J << 8));
-    int sum = __dp4a(int(hrow[lane_id]), 0x01010101, 0);
-    sum = __dp4a(int(hrow[lane_id + 32]), 0x01010101, sum);
-#pragma unroll
-    for (int o2 = 16; o2; o2 >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o2);
-    if (sum && lane_id < sp.n) atomicAdd(cellacc + __ldg(jcell + J * sp.n + lane_id), uint32_t(sum));
-  }
-  __syncthreads();
-  for (int cell = tid; cell < cells; cell += SG_THREADS)
-    if (cellacc[cell]) atomicAdd(counts + cell, (unsigned long long)cellacc[cell]);
+  small_epilogue<N, SG_THREADS>(sp, zs, hist8, cellacc, jcell, cells, counts, obs, ld_obs, cases, err);
 }
 
 // Resident CTAs of one sweep instance on the whole device (one full wave).
@@ -449,6 +465,358 @@ static SmallOrd small_ord(const sg_small& sp) {
   return o;
 }
 
+
+
+// ============================================================ joint sweep
+//
+// rng = "joint" (SG_RNG_JOINT): the whole colour-ordered sweep of one lane
+// drawn with ONE uniform.  For a lane word S and latent pattern P the sweep
+// (reference gibbs_pass, sampler.py:251-284: colour groups in order, each
+// latent variable v drawn from its full conditional given the current
+// blanket) is a Markov kernel K_P(S -> S') over the 2^B_P values of the
+// latent fields, B_P = sum of the latent variables' field widths:
+//
+//   K_P(S -> S') = prod_{v latent, colour order} p_v(S'_v | cur_v),
+//   cur_v = S with the fields of the variables drawn before v replaced by S'.
+//
+// k_joint_tables tabulates every row (P, S) of K as 2^B_P cumulative
+// thresholds (2^31 scale, same quantisation as the per-variable FAST
+// tables); the sweep draws one 31-bit uniform per lane and binary-searches
+// its row in shared memory.  Same transition kernel as the per-variable
+// sweep (up to the 2^-31 threshold quantisation), 1 uniform per lane
+// instead of one per latent variable, B_P dependent shared loads instead of
+// 4 table lookups per latent variable.  When any conditional has zero
+// support (zs_flag armed) the kernel runs the per-variable path instead, so
+// ZeroSupport is detected exactly where the reference detects it.
+//
+// Blob (uint32 words, built on the host once -- netpack.joint_plan -- except
+// the rows, which k_joint_tables rewrites after every CPT update):
+//   [0, NP)        byte offset of row 0 of pattern P
+//   [NP, 2NP)      B_P | keep_P << 8 | (byte offset of dep_P) << 16
+//   dep_P[j]       latent field bits of compact column j (pdep(j, latent mask))
+//   rows_P[S][j]   thresholds, 2^bits rows of 2^B_P words per pattern
+
+#define SG_JOINT_THREADS 1024
+#define SG_JOINT_PURPOSE 2u
+#define SG_JOINT_MAXB 6
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "SG_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SG_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> this CTA's shared memory, completion on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Row search: the first entry j with u < row[j] (row[2^B - 1] is never read:
+// the last column takes the remaining mass).
+template <int B>
+__device__ __forceinline__ const uint32_t* joint_search(const uint32_t* row, uint32_t u) {
+  const uint32_t* p = row;
+#pragma unroll
+  for (int h = 1 << (B - 1); h >= 1; h >>= 1)
+    if (u >= p[h - 1]) p += h;
+  return p;
+}
+
+// The QG quads of one slot: per lane one uniform (word j of the quad's
+// Philox block), one row search, one dep lookup.  Straight-line over all
+// 4 x QG lanes (no per-lane branches) so the compiler interleaves the
+// independent search chains; lanes past m and alias quads compute garbage
+// that is never stored or tallied.
+template <int B, int QG>
+__device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[QG], const unsigned char* row0,
+                                            const unsigned char* dep0, uint32_t keep) {
+#pragma unroll
+  for (int g = 0; g < QG; ++g) {
+    const uint32_t u[4] = {r[g].a >> 1, r[g].b >> 1, r[g].c >> 1, r[g].d >> 1};
+    uint32_t xs[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t S = byte_of(w[g], j);
+      const unsigned char* row = row0 + (S << (B + 2)) + (S << 2);  // rows 2^B + 1 words apart
+      const uint32_t* p = joint_search<B>(reinterpret_cast<const uint32_t*>(row), u[j]);
+      const uint32_t lat = *reinterpret_cast<const uint32_t*>(dep0 + (reinterpret_cast<const unsigned char*>(p) - row));
+      xs[j] = (S & keep) | lat;
+    }
+    w[g] = __byte_perm(__byte_perm(xs[0], xs[1], 0x0040), __byte_perm(xs[2], xs[3], 0x0040), 0x5410);
+  }
+}
+
+// Per-lane byte counter += 1 without branches: lanes that must not count
+// (past m, alias quads, padding cases) increment a trash row instead.
+__device__ __forceinline__ void hist_inc_sel(bool ok, uint32_t a, uint32_t trash) { hist_inc(ok ? a : trash); }
+
+template <int QG, int NT>
+__device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned char* blob, int np, uint32_t* lanes,
+                                            const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id,
+                                            uint32_t hist_a, uint32_t trash_a, int cases, int num_real,
+                                            int64_t case_base, const FastKey& fk, bool counts,
+                                            const uint32_t (&nw0)[QG], uint32_t nP0, int nc0) {
+  const uint32_t* info = reinterpret_cast<const uint32_t*>(blob);
+  const int stride = gridDim.x * NT;
+  int s = blockIdx.x * NT + threadIdx.x;
+  uint32_t nw[QG], nP = nP0;
+  int nc = nc0;
+#pragma unroll
+  for (int g = 0; g < QG; ++g) nw[g] = nw0[g];
+  // lanes that exist: 4 per quad before the last, last_nl in the last, none in aliases
+  uint32_t real = 0;
+#pragma unroll
+  for (int g = 0; g < QG; ++g)
+    real |= (g < qs.last ? 0xFu : g == qs.last ? ((1u << qs.last_nl) - 1u) : 0u) << (4 * g);
+  uint32_t* rows = lanes + qs.row0;
+  for (; s < cases; s += stride) {
+    uint32_t w[QG];
+#pragma unroll
+    for (int g = 0; g < QG; ++g) w[g] = nw[g];
+    const uint32_t P = nP;
+    const int c = nc;
+    const int sn = s + stride;
+    if (sn < cases) {  // prefetch the next slot while this one computes
+#pragma unroll
+      for (int g = 0; g < QG; ++g) nw[g] = rows[min(g, qs.last) * qs.ld + sn];
+      nP = pattern[sn];
+      nc = case_id[sn];
+    }
+    const uint32_t meta = info[np + P];
+    const int B = int(meta & 0xFFu);
+    if (B) {  // warp-uniform: slots are bucketed by pattern
+      const FastCase fc = fast_case(fk, uint32_t(case_base + c));
+      u32x4 r[QG];
+#pragma unroll
+      for (int g = 0; g < QG; ++g)
+        r[g] = fast_draw(fc, (SG_JOINT_PURPOSE << 28) | (qs.q0w + (uint32_t(min(g, qs.last)) << 16)));
+      const unsigned char* row0 = blob + info[P];
+      const unsigned char* dep0 = blob + (meta >> 16);
+      const uint32_t keep = (meta >> 8) & 0xFFu;
+      switch (B) {
+        case 1: joint_quads<1, QG>(w, r, row0, dep0, keep); break;
+        case 2: joint_quads<2, QG>(w, r, row0, dep0, keep); break;
+        case 3: joint_quads<3, QG>(w, r, row0, dep0, keep); break;
+        case 4: joint_quads<4, QG>(w, r, row0, dep0, keep); break;
+        case 5: joint_quads<5, QG>(w, r, row0, dep0, keep); break;
+        default: joint_quads<6, QG>(w, r, row0, dep0, keep); break;
+      }
+    }
+    const uint32_t tally = (counts && c < num_real) ? real : 0u;
+#pragma unroll
+    for (int g = 0; g < QG; ++g) {
+      const uint32_t wg = w[g] & (g < qs.last ? 0xFFFFFFFFu : qs.last_valid);
+      if (g <= qs.last) rows[g * qs.ld + s] = wg;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) hist_inc_sel((tally >> (4 * g + j)) & 1u, hist_a + byte_of(wg, j) * NT, trash_a);
+    }
+  }
+}
+
+__host__ __device__ inline size_t joint_smem(const sg_small& sp, const sg_joint& jp, int cells) {
+  return size_t(jp.words) * 4 + size_t((sp.tab_words * 4 + 15) & ~15) +
+         ((size_t(1) << sp.bits) + 1) * SG_JOINT_THREADS + size_t((cells * 4 + 15) & ~15) + 16;
+}
+
+// One CTA per SM: the blob (Koller: 104 KB) + 1024 threads' byte counters.
+template <int N, int QG>
+__global__ void __launch_bounds__(SG_JOINT_THREADS, 1)
+k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint32_t* stab_g,
+              const uint32_t* __restrict__ jblob_g, const uint8_t* __restrict__ pattern,
+              const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes, int lane_ld, int cases, int num_real,
+              int m, int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* __restrict__ jcell,
+              int cells, unsigned long long* __restrict__ counts, const uint32_t* zs_flag,
+              const int8_t* __restrict__ obs, int ld_obs, int32_t* err) {
+  constexpr int NT = SG_JOINT_THREADS;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* blob = smem;
+  const uint32_t jbytes = uint32_t(jp.words) * 4u;
+  uint32_t* stab = reinterpret_cast<uint32_t*>(smem + jbytes);
+  uint8_t* hist8 = reinterpret_cast<uint8_t*>(stab) + ((sp.tab_words * 4 + 15) & ~15);
+  uint32_t* cellacc = reinterpret_cast<uint32_t*>(hist8 + ((1 << sp.bits) + 1) * NT);  // + trash row
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(cellacc) + ((cells * 4 + 15) & ~15));
+  const int tid = threadIdx.x;
+  const int Q = (m + 3) >> 2;
+  const int q0 = blockIdx.y * QG;
+  const int last = min(QG - 1, Q - 1 - q0);
+  pdl_trigger();
+  if (tid == 0) mbar_init(bar, 1);
+  if (counts) {
+    uint32_t* h32 = reinterpret_cast<uint32_t*>(hist8);
+    for (int i = tid; i < (NT << sp.bits) / 4; i += NT) h32[i] = 0;
+    for (int i = tid; i < cells; i += NT) cellacc[i] = 0;
+  }
+  uint32_t nw0[QG] = {};
+  uint32_t nP0 = 0;
+  int nc0 = 0;
+  {
+    const int s0 = blockIdx.x * NT + tid;
+    if (s0 < cases) {
+      const uint32_t* r0p = lanes + int64_t(q0) * lane_ld;
+#pragma unroll
+      for (int g = 0; g < QG; ++g) nw0[g] = r0p[int64_t(min(g, last)) * lane_ld + s0];
+      nP0 = pattern[s0];
+      nc0 = case_id[s0];
+    }
+  }
+  pdl_wait();  // the blob rows, tables, key and cleared counts of this step
+  if (tid == 0) {
+    mbar_expect_tx(bar, jbytes);
+    for (uint32_t o2 = 0; o2 < jbytes; o2 += 32768u)
+      bulk_g2s(blob + o2, reinterpret_cast<const unsigned char*>(jblob_g) + o2, min(32768u, jbytes - o2), bar);
+  }
+  for (int i = tid; i < sp.tab_words; i += NT) stab[i] = stab_g[i];
+  const bool armed = zs_flag && *zs_flag != 0u;
+  QuadSet qs;
+  qs.row0 = uint32_t(q0) * uint32_t(lane_ld);
+  qs.ld = uint32_t(lane_ld);
+  qs.q0w = uint32_t(q0) << 16;
+  qs.last = last;
+  qs.last_nl = min(4, m - 4 * (q0 + qs.last));
+  qs.last_valid = qs.last_nl >= 4 ? 0xFFFFFFFFu : ((1u << (8 * qs.last_nl)) - 1u);
+  const int slot = ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
+  const uint32_t hist_a = smem_u32(hist8) + uint32_t(slot);
+  const uint32_t trash_a = hist_a + (uint32_t(NT) << sp.bits);
+  const FastKey fk = fast_key(key_dev ? *key_dev : key);
+  __syncthreads();
+  mbar_wait(bar, 0);
+  bool zs = false;
+  if (armed)
+    zs = small_units<N, QG, true, NT>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
+                                      counts != nullptr, nw0, nP0, nc0);
+  else
+    joint_units<QG, NT>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, trash_a, cases, num_real,
+                        case_base, fk, counts != nullptr, nw0, nP0, nc0);
+  small_epilogue<N, NT>(sp, zs, hist8, cellacc, jcell, cells, counts, obs, ld_obs, cases, err);
+}
+
+// Rows of pattern P = blockIdx.x, lane words S of slice blockIdx.y, from the
+// current CPTs (see the blob comment).  fp64 in a fixed order, no FMA:
+// p_v = w / norm with the reference's weight product (conditional_weights)
+// and sequential norm; products in colour order; sequential row sums;
+// thresholds min(ceil(cum * (2^31 / total)), 2^31).
+#define SG_JOINT_TAB_SLICES 4
+__global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg_small sp, const sg_joint jp,
+                                                      const double* cpt, const double* vprob_g, uint32_t* jblob) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t lv[SG_SMALL_MAXV][4];  // latent variables of P in colour order: off|width<<8|card<<16, mbmask, fm, v
+  __shared__ int nlat;
+  const int P = blockIdx.x, tid = threadIdx.x;
+  pdl_trigger();
+  const uint32_t meta = jblob[jp.patterns + P];  // static header
+  const int B = int(meta & 0xFFu);
+  if (B == 0) return;
+  const uint32_t keep = (meta >> 8) & 0xFFu;
+  const uint32_t* dep = reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(jblob) + (meta >> 16));
+  uint32_t* rows = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(jblob) + jblob[P]);
+  const int R = 1 << sp.bits, K = 1 << B;
+  const int KS = K + 1;  // row stride (odd: no bank conflicts)
+  const int rows_per = R / SG_JOINT_TAB_SLICES, r0 = blockIdx.y * rows_per;
+  const int E = rows_per << B;
+  double* vprob = reinterpret_cast<double*>(smem);  // [n][R][4]
+  double* acc = vprob + sp.n * R * 4;               // [rows_per][KS]
+  double* scale = acc + rows_per * KS;              // [rows_per]
+  if (tid == 0) {
+    int k = 0;
+    for (int i = 0; i < sp.n; ++i) {
+      const int v = sp.order[i];
+      if (!((P >> v) & 1)) continue;
+      lv[k][0] = uint32_t(sp.off[v]) | (uint32_t(sp.width[v]) << 8) | (uint32_t(sp.card[v]) << 16);
+      lv[k][1] = sp.mbmask[v];
+      lv[k][2] = ((1u << sp.width[v]) - 1u) << sp.off[v];
+      lv[k][3] = uint32_t(v);
+      ++k;
+    }
+    nlat = k;
+  }
+  pdl_wait();  // this step's CPTs (and the tail's conditionals)
+  if (vprob_g) {  // written by the step tail (sg_finish.vprob): one coalesced copy
+    for (int i = tid; i < sp.n * R * 4; i += blockDim.x) vprob[i] = vprob_g[i];
+  } else {
+    for (int i = tid; i < sp.n * R; i += blockDim.x) {
+      const int v = i / R;
+      const uint32_t S = uint32_t(i - v * R);
+      if (!((P >> v) & 1) || (S & ~sp.mbmask[v])) continue;
+      int s[SG_MAX_MB];
+      bool valid = true;
+      const int m0 = net.mb_start[v], m1 = net.mb_start[v + 1];
+      for (int k = m0; k < m1 && valid; ++k) {
+        const int u = net.mb_var[k];
+        s[k - m0] = small_field(S, sp, u);
+        valid = s[k - m0] < sp.card[u];
+      }
+      double* out = vprob + size_t(i) * 4;
+      const int card = sp.card[v];
+      if (!valid) {
+        for (int t = 0; t < card; ++t) out[t] = 0.0;
+        continue;
+      }
+      with_card(card, [&](auto C) {
+        constexpr int KC = decltype(C)::value;
+        double w[KC ? KC : SG_MAX_CARD];
+        conditional_weights<false, KC>(net, v, s, cpt, w);
+        joint_conditional<KC>(w, card, out);
+      });
+    }
+  }
+  __syncthreads();
+  const int nl = nlat;
+  for (int e = tid; e < E; e += blockDim.x) {
+    const uint32_t S = uint32_t(r0 + (e >> B));
+    const uint32_t Sn = (S & keep) | dep[e & (K - 1)];
+    double p = 1.0;
+    uint32_t cur = S;
+    for (int k = 0; k < nl; ++k) {
+      const uint32_t d = lv[k][0];
+      const uint32_t x = (Sn >> (d & 0xFFu)) & ((1u << ((d >> 8) & 0xFFu)) - 1u);
+      if (x >= (d >> 16)) {
+        p = 0.0;
+        break;
+      }
+      p = __dmul_rn(p, vprob[(int(lv[k][3]) * R + int(cur & lv[k][1])) * 4 + int(x)]);
+      cur = (cur & ~lv[k][2]) | (Sn & lv[k][2]);
+    }
+    acc[(e >> B) * KS + (e & (K - 1))] = p;
+  }
+  __syncthreads();
+  for (int r = tid; r < rows_per; r += blockDim.x) {
+    double c = 0.0;
+    for (int j = 0; j < K; ++j) {
+      c = j ? __dadd_rn(c, acc[r * KS + j]) : acc[r * KS];
+      acc[r * KS + j] = c;
+    }
+    scale[r] = c > 0.0 ? __ddiv_rn(2147483648.0, c) : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int r = e >> B, j = e & (K - 1);
+    const double sc = scale[r];
+    uint32_t* row = rows + (r0 + r) * KS;
+    row[j] = (sc > 0.0 && j != K - 1) ? uint32_t(fmin(ceil(__dmul_rn(acc[r * KS + j], sc)), 2147483648.0))
+                                      : 0x80000000u;
+    if (j == K - 1) row[K] = 0x80000000u;  // stride padding
+  }
+}
+
+static size_t joint_tables_smem(const sg_small& sp, int maxb) {
+  const size_t R = size_t(1) << sp.bits;
+  const size_t rows = R / SG_JOINT_TAB_SLICES;
+  return (size_t(sp.n) * R * 4 + rows * ((size_t(1) << maxb) + 1) + rows) * sizeof(double);
+}
 
 }  // namespace sg
 
@@ -593,4 +961,126 @@ extern "C" int sg_keys_advance(const uint64_t* table, int32_t* index, int32_t kp
   SG_REQUIRE(table && index && current && kps > 0, "sg_keys_advance: bad argument");
   k_keys_advance<<<1, 32, 0, (cudaStream_t)stream>>>(table, index, kps, current);
   return check_launch("sg_keys_advance");
+}
+
+// ------------------------------------------------------------ joint C-ABI
+namespace sg {
+template <int N, int QG>
+static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& jp, int groups, size_t smem,
+                         cudaStream_t st, const uint32_t* stab, const uint32_t* jblob, const uint8_t* pattern,
+                         const int32_t* case_id, uint32_t* lanes, int lane_ld, int cases, int num_real, int m,
+                         int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell, int cells,
+                         uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs, int ld_obs, int32_t* err) {
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_joint_sweep<N, QG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // one CTA per SM (one wave), but no thread's byte counters past 255 increments
+  const int64_t per_thread = 255 / (4 * QG);
+  const int64_t need = (int64_t(cases) + SG_JOINT_THREADS * per_thread - 1) / (SG_JOINT_THREADS * per_thread);
+  const int64_t fill = (int64_t(cases) + SG_JOINT_THREADS - 1) / SG_JOINT_THREADS;
+  const int64_t want = std::max<int64_t>(std::max(1, sms / groups), need);
+  const dim3 grid(unsigned(std::max<int64_t>(1, std::min<int64_t>(want, fill))), unsigned(groups));
+  launch_pdl(k_joint_sweep<N, QG>, grid, dim3(SG_JOINT_THREADS), smem, st, sp, o, jp, stab, jblob, pattern, case_id,
+             lanes, lane_ld, cases, num_real, m, case_base, key, key_dev, jcell, cells,
+             reinterpret_cast<unsigned long long*>(counts), zs_flag, obs, ld_obs, err);
+}
+
+static bool joint_plan_ok(const sg_small& sp, const sg_joint& jp, int cells) {
+  return sp.bits >= 2 && sp.bits <= SG_JOINT_MAXB && jp.patterns == (1 << sp.n) && jp.words > 2 * jp.patterns &&
+         jp.words % 4 == 0 && jp.max_b >= 1 && jp.max_b <= sp.bits && joint_smem(sp, jp, cells) <= 227 * 1024;
+}
+}  // namespace sg
+
+extern "C" int sg_joint_smem(const sg_small* sp, const sg_joint* jp, int32_t cells, int64_t* bytes) {
+  using namespace sg;
+  SG_REQUIRE(sp && jp && bytes, "sg_joint_smem: null argument");
+  *bytes = int64_t(joint_smem(*sp, *jp, cells));
+  return SG_OK;
+}
+
+extern "C" int sg_joint_tables(const sg_net* net, const sg_small* sp, const sg_joint* jp, const double* cpt,
+                               const double* vprob, uint32_t* jblob, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(net && sp && jp && cpt && jblob, "sg_joint_tables: null argument");
+  SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV && sp->bits >= 2 && sp->bits <= SG_JOINT_MAXB &&
+                 jp->patterns == (1 << sp->n) && jp->max_b >= 1 && jp->max_b <= sp->bits,
+             "sg_joint_tables: bad plan (bits %d, patterns %d)", sp->bits, jp->patterns);
+  SG_REQUIRE(net->max_mb <= SG_MAX_MB, "sg_joint_tables: Markov blanket too large");
+  const size_t smem = joint_tables_smem(*sp, jp->max_b);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_joint_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  launch_pdl(k_joint_tables, dim3(jp->patterns, SG_JOINT_TAB_SLICES), dim3(256), smem, (cudaStream_t)stream, *net, *sp, *jp, cpt, vprob,
+             jblob);
+  return check_launch("sg_joint_tables");
+}
+
+extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint32_t* stab, const uint32_t* jblob,
+                              const uint8_t* pattern, const int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
+                              int32_t cases, int32_t num_real, int32_t m, int64_t case_base, uint64_t key,
+                              const uint64_t* key_dev, const int32_t* jcell, int32_t cells, uint64_t* counts,
+                              const uint32_t* zs_flag, const int8_t* obs, int32_t ld_obs, int32_t* err, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(sp && jp && stab && jblob && pattern && case_id && lanes && err, "sg_joint_sweep: null argument");
+  SG_REQUIRE((reinterpret_cast<uintptr_t>(jblob) & 15) == 0, "sg_joint_sweep: blob must be 16-byte aligned");
+  if (obs)
+    SG_REQUIRE(ld_obs % 16 == 0 && (reinterpret_cast<uintptr_t>(obs) & 15) == 0 && ld_obs >= cases,
+               "sg_joint_sweep: obs rows must be 16-byte aligned");
+  SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV, "sg_joint_sweep: bad plan");
+  SG_REQUIRE(joint_plan_ok(*sp, *jp, cells), "sg_joint_sweep: joint plan does not fit (bits %d, words %d)", sp->bits,
+             jp->words);
+  SG_REQUIRE(!counts || jcell, "sg_joint_sweep: joint cell map required for the tally");
+  SG_REQUIRE(m >= 1 && m <= 32 && lane_ld_ok(lane_ld, cases), "sg_joint_sweep: m %d / lane_ld %d < cases %d", m,
+             lane_ld, cases);
+  SG_REQUIRE(fast_cases_ok(case_base, cases), "sg_joint_sweep: global case index beyond 2^32");
+  SG_REQUIRE(int64_t((m + 3) / 4) * lane_ld <= (int64_t(1) << 32), "sg_joint_sweep: lane block beyond 2^32 words");
+  for (int v = 0; v < sp->n; ++v)
+    SG_REQUIRE(sp->card[v] >= 2 && sp->card[v] <= 4 && sp->tstride[v] >= sp->card[v] - 1 &&
+                   sp->toff[v] % sp->tstride[v] == 0,
+               "sg_joint_sweep: variable %d needs 2 <= card <= 4 and an aligned table", v);
+  if (cases == 0) return SG_OK;
+  const size_t smem = joint_smem(*sp, *jp, cells);
+  const SmallOrd o = small_ord(*sp);
+  int qg = 1, groups = 1;
+  quad_groups(m, &qg, &groups);
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* lw = reinterpret_cast<uint32_t*>(lanes);
+#define SG_JOINT_QG(NV, G)                                                                                     \
+  case G:                                                                                                      \
+    launch_joint<NV, G>(*sp, o, *jp, groups, smem, st, stab, jblob, pattern, case_id, lw, lane_ld, cases,      \
+                        num_real, m, case_base, key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err); \
+    break;
+#define SG_JOINT_CASE(NV) \
+  case NV:                \
+    switch (qg) {         \
+      SG_JOINT_QG(NV, 1)  \
+      SG_JOINT_QG(NV, 2)  \
+      SG_JOINT_QG(NV, 3)  \
+      SG_JOINT_QG(NV, 4)  \
+    }                     \
+    break;
+  switch (sp->n) {
+    SG_JOINT_CASE(1)
+    SG_JOINT_CASE(2)
+    SG_JOINT_CASE(3)
+    SG_JOINT_CASE(4)
+    SG_JOINT_CASE(5)
+    SG_JOINT_CASE(6)
+    default:
+      set_error("sg_joint_sweep: n=%d", sp->n);
+      return SG_EINVAL;
+  }
+#undef SG_JOINT_CASE
+#undef SG_JOINT_QG
+  return check_launch("sg_joint_sweep");
 }

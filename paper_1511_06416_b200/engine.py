@@ -114,8 +114,20 @@ class Engine:
         max_m = cfg.same_m if isinstance(cfg.same_m, int) else max(mm for mm, _ in cfg.same_m)
         can_small = self.rng_mode == _lib.SG_RNG_FAST and self.pack.small is not None and max_m <= 32
         self.use_small = can_small if small is None else (bool(small) and can_small)
+        # joint sweep (rng="joint"): one draw per lane from the sweep's transition kernel
+        self.joint = cfg.rng == "joint"
+        if self.joint and (not self.use_small or self.pack.joint is None):
+            raise ValueError("rng='joint' needs a network whose packed lane word has <= 6 bits "
+                             "(cards <= 4, n <= 6) and same_m <= 32; use rng='fast'")
         if self.use_small:
             self.stab = torch.empty(max(1, self.pack.small.tab_words), dtype=torch.int32, device=d)
+        if self.joint:
+            jp = self.pack.joint
+            blob = np.zeros(jp.words, dtype=np.uint32)
+            blob[:jp.header_words] = self.pack.joint_header
+            self.jblob = torch.from_numpy(blob.view(np.int32)).to(d)
+            # full conditionals p_v(x | lane word), written by the step tail for sg_joint_tables
+            self.vprob = torch.zeros(self.n * (4 << self.pack.small.bits), dtype=torch.float64, device=d)
         self.tables_fresh = False  # conditional tables reflect self.cpt
         self._latent_hint = None   # latent share of the first generic minibatch (sg_batch.latent_permille)
 
@@ -222,6 +234,7 @@ class Engine:
             if self.use_small:
                 _lib.call("sg_small_tables", self.pack.ref, self.pack.small_ref, self.ftab.data_ptr(),
                           self.stab.data_ptr(), s)
+            self.joint_tables(s, from_finish=False)
             self.tables_fresh = True
         new_counts = torch.zeros_like(self.counts) if moving else self.counts
         if not moving:
@@ -240,12 +253,7 @@ class Engine:
             last = sw == S - 1
             counts_ptr = new_counts.data_ptr() if last else None
             if self.use_small:
-                args = (self.pack.small_ref, self.stab.data_ptr(), db.pattern.data_ptr(), db.case_id.data_ptr(),
-                        db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m, self.case_base, sweep_seed, None,
-                        self.pack.small_jcell.data_ptr(), self.pack.cells, counts_ptr,
-                        self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"],
-                        obs.data_ptr() if last else None, ld, self.err.ptr)
-                _lib.call("sg_small_sweep", *args, s)
+                self.packed_sweep(db, size, m, sweep_seed, None, counts_ptr, obs.data_ptr() if last else None, ld, s)
             elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
                 _lib.call("sg_sweep", self.pack.ref, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
@@ -261,6 +269,7 @@ class Engine:
         if self.comm is not None:
             self.comm(new_counts)
         _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
+        self.joint_tables(s)
         if moving:
             self.prev_counts[mb.index] = new_counts
             self.latent[mb.index] = db
@@ -288,11 +297,31 @@ class Engine:
         f.clear_counts = None if clear is None else clear.data_ptr()
         # the packed sweep reads only the packed words: build them straight from the CPTs
         f.flags = _lib.SG_FINISH_PACKED_ONLY if self.use_small else 0
+        f.vprob = self.vprob.data_ptr() if self.joint else None
         if cursor is not None:
             table, index, kps, current = cursor
             f.key_table, f.key_index, f.kps, f.key_current = table.data_ptr(), index.data_ptr(), kps, current.data_ptr()
         self._finish_keepalive = f
         return f
+
+    def packed_sweep(self, db, size: int, m: int, key: int, key_dev, counts_ptr, obs_ptr, ld: int, s) -> None:
+        """Sweep + tally of a packed-lane minibatch: per-variable draws
+        (sg_small_sweep) or, with rng="joint", one draw per lane (sg_joint_sweep)."""
+        tail = (db.pattern.data_ptr(), db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m,
+                self.case_base, key, key_dev, self.pack.small_jcell.data_ptr(), self.pack.cells, counts_ptr,
+                self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"], obs_ptr, ld, self.err.ptr, s)
+        if self.joint:
+            _lib.call("sg_joint_sweep", self.pack.small_ref, self.pack.joint_ref, self.stab.data_ptr(),
+                      self.jblob.data_ptr(), *tail)
+        else:
+            _lib.call("sg_small_sweep", self.pack.small_ref, self.stab.data_ptr(), *tail)
+
+    def joint_tables(self, s, from_finish: bool = True) -> None:
+        """Joint-sweep rows from the current CPTs (after every CPT update);
+        ``from_finish``: the step tail has just written the conditionals."""
+        if self.joint:
+            _lib.call("sg_joint_tables", self.pack.ref, self.pack.small_ref, self.pack.joint_ref, self.cpt.data_ptr(),
+                      self.vprob.data_ptr() if from_finish else None, self.jblob.data_ptr(), s)
 
     @property
     def small_ptr(self):
@@ -445,12 +474,7 @@ class StepGraphs:
             last = sw == S - 1
             counts_ptr = new.data_ptr() if last else None
             if eng.use_small:
-                args = (eng.pack.small_ref, eng.stab.data_ptr(), db.pattern.data_ptr(), db.case_id.data_ptr(),
-                        db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m, eng.case_base, 0, cur + 8 * sw,
-                        eng.pack.small_jcell.data_ptr(), eng.pack.cells, counts_ptr,
-                        eng.ftab.data_ptr() + 4 * eng.pack.layout.scalars["ftab_size"],
-                        obs.data_ptr() if last else None, self.ld, eng.err.ptr)
-                _lib.call("sg_small_sweep", *args, s)
+                eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr, obs.data_ptr() if last else None, self.ld, s)
             else:
                 _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
@@ -458,6 +482,7 @@ class StepGraphs:
         if eng.comm is not None:
             eng.comm(new)
         _lib.call("sg_step_finish", eng.pack.ref, eng.small_ptr, f, s)
+        eng.joint_tables(s)
 
     def step(self, mb=None) -> None:
         """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
@@ -496,7 +521,8 @@ class StepGraphs:
         eng = self.eng
         one_cta = eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
         check = 0 if eng.use_small else 1  # the packed sweep folds in the range check
-        return check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
+        return (check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
+                + (1 if eng.joint else 0))
 
     def finish(self) -> None:
         """Hand the last visit's counts back to the engine's moving-sum bookkeeping."""

@@ -323,6 +323,67 @@ def small_plan(net: Network, lay: NetLayout):
     return sp, jcell.astype(np.int32)
 
 
+JOINT_MAXB = 6           # lane words of <= 6 bits (csrc/sg_small.cu SG_JOINT_MAXB)
+JOINT_THREADS = 1024     # SG_JOINT_THREADS
+JOINT_SMEM_LIMIT = 227 * 1024
+
+
+def joint_plan(sp, cells: int):
+    """Static header of the joint-sweep blob (include/samegibbs_b200.h sg_joint).
+
+    Patterns P (bit v = variable v latent, as sg_small_prepare buckets them):
+    B_P latent bits, keep_P = the observed bits of the lane word, dep_P[j] =
+    the lane bits of compact column j (bit i of j -> the i-th set bit of the
+    latent mask), 2^bits rows of 2^B_P thresholds, 2^B_P + 1 words apart.  Returns ``(SgJoint,
+    header uint32 array)`` or None when the network does not qualify or the
+    CTA's shared memory (blob + per-variable table + byte counters) does not
+    fit.
+    """
+    from ._lib import SgJoint
+
+    if sp is None or not 2 <= sp.bits <= JOINT_MAXB:
+        return None
+    n, bits = sp.n, sp.bits
+    NP = 1 << n
+    fmask = [((1 << sp.width[v]) - 1) << sp.off[v] for v in range(n)]
+    full = (1 << bits) - 1
+    lmask = [0] * NP
+    for P in range(NP):
+        for v in range(n):
+            if (P >> v) & 1:
+                lmask[P] |= fmask[v]
+    B = [bin(lm).count("1") for lm in lmask]
+    dep, dep_off = [], [0] * NP
+    for P in range(NP):
+        if not B[P]:
+            continue
+        dep_off[P] = 2 * NP + len(dep)
+        pos = [i for i in range(bits) if (lmask[P] >> i) & 1]
+        for j in range(1 << B[P]):
+            dep.append(sum(((j >> i) & 1) << pos[i] for i in range(B[P])))
+    header_words = (2 * NP + len(dep) + 3) // 4 * 4
+    row_off, words = [0] * NP, header_words
+    for P in range(NP):
+        if B[P]:  # rows 2^B + 1 words apart: odd stride, no bank conflicts between lanes
+            row_off[P] = words
+            words += (1 << bits) * ((1 << B[P]) + 1)
+    words = (words + 3) // 4 * 4
+    if max(dep_off) * 4 >= 1 << 16:
+        return None
+    head = np.zeros(header_words, dtype=np.uint32)
+    for P in range(NP):
+        head[P] = row_off[P] * 4
+        head[NP + P] = B[P] | ((full & ~lmask[P]) << 8) | ((dep_off[P] * 4) << 16)
+    head[2 * NP:2 * NP + len(dep)] = dep
+    jp = SgJoint()
+    jp.words, jp.header_words, jp.patterns, jp.max_b = words, header_words, NP, max(B)
+    smem = (words * 4 + ((sp.tab_words * 4 + 15) & ~15) + ((1 << bits) + 1) * JOINT_THREADS
+            + ((cells * 4 + 15) & ~15) + 16)
+    if smem > JOINT_SMEM_LIMIT:
+        return None
+    return jp, head
+
+
 class NetPack:
     """Device-resident ``sg_net``: two flat tensors plus the C struct of pointers."""
 
@@ -368,6 +429,11 @@ class NetPack:
             self.small = sp
             self.small_ref = ctypes.byref(sp)
             self.small_jcell = torch.from_numpy(jcell.ravel()).to(device)
+        self.joint = None
+        jplan = joint_plan(self.small, lay.cells)
+        if jplan is not None:
+            self.joint, self.joint_header = jplan
+            self.joint_ref = ctypes.byref(self.joint)
 
     @property
     def n(self) -> int:

@@ -18,8 +18,13 @@ RNG modes (``SamplerConfig.rng``):
   reference for the same site, so sweeps, tallies and MAP runs reproduce the
   reference bit for bit;
 * ``"fast"``: Philox4x32-10 with (case, variable, replica) counters --
-  statistically equivalent, independent of tiling and GPU count, and the
-  throughput mode.
+  statistically equivalent, independent of tiling and GPU count;
+* ``"joint"``: small networks only (packed lane word of <= 6 bits): each
+  lane's whole colour-ordered sweep is ONE draw from the sweep's transition
+  kernel (the product of the full conditionals gibbs_pass draws from, in
+  colour order), one Philox4x32 uniform per lane -- the same Markov chain as
+  ``"fast"`` with fewer random numbers and table lookups; the throughput
+  mode of the Koller configurations.
 
 ``threads`` is accepted for compatibility and, as in the reference, does not
 change results (the device decides its own parallelism).
@@ -47,7 +52,7 @@ from .rng import derive_seed, stream_key_ints
 MSchedule = Union[int, Sequence[tuple[int, int]]]
 
 ACCUMULATOR_MODES = ("moving_sum", "exponential")
-RNG_MODES = ("numpy", "fast")
+RNG_MODES = ("numpy", "fast", "joint")
 
 
 @dataclass

@@ -55,3 +55,135 @@ def fast_init_states(key: int, obs: np.ndarray, cards, m: int, case_base: int = 
             s = ((w * np.uint64(cards[v])) >> np.uint64(32)).astype(np.int16)
             out[v, r] = np.where(obs[v] >= 0, obs[v], 0x80 | s)
     return out.astype(np.uint8).view(np.int8)
+
+
+# ------------------------------------------------------------ joint sweep
+# rng = "joint" (csrc/sg_small.cu, "joint sweep"): one uniform per lane drawn
+# from the sweep's transition kernel K_P(S -> S'), the colour-ordered product
+# of the full conditionals (reference sampler.py:217-284).
+
+def lane_fields(cards):
+    """Field widths and bit offsets of the packed lane word (netpack.small_plan)."""
+    width = [max(1, (int(k) - 1).bit_length()) for k in cards]
+    off = [0] * len(cards)
+    for v in range(1, len(cards)):
+        off[v] = off[v - 1] + width[v - 1]
+    return width, off
+
+
+def _conditional(onet, cpts, v, a):
+    """Full conditional of v given assignment a: parent row, then children
+    ascending, fp64 left to right, sequential norm (sampler.py:226-242)."""
+    cfg = sum(int(a[p]) * st for p, st in zip(onet.parents[v], onet.strides(v)))
+    w = [float(x) for x in cpts[v][cfg]]
+    for c in onet.children[v]:
+        cs = onet.strides(c)
+        vst = cs[onet.parents[c].index(v)]
+        cfg0 = sum(int(a[p]) * st for p, st in zip(onet.parents[c], cs) if p != v)
+        for t in range(len(w)):
+            w[t] = w[t] * float(cpts[c][cfg0 + t * vst, int(a[c])])
+    norm = 0.0
+    for x in w:
+        norm = norm + x
+    return [x / norm if norm > 0.0 else 0.0 for x in w]
+
+
+def joint_tables(onet, cpts, order):
+    """{P: (B, keep, dep[K], rows uint32 (R, K))} for every pattern with latent bits."""
+    import math
+
+    n = onet.n
+    cards = onet.cards
+    width, off = lane_fields(cards)
+    bits = sum(width)
+    R = 1 << bits
+    fmask = [((1 << width[v]) - 1) << off[v] for v in range(n)]
+    mb = [set() for _ in range(n)]
+    for c in range(n):
+        ps = onet.parents[c]
+        for p in ps:
+            mb[c].add(p)
+            mb[p].add(c)
+            for q in ps:
+                if q != p:
+                    mb[p].add(q)
+
+    def fields(S):
+        return [(S >> off[v]) & ((1 << width[v]) - 1) for v in range(n)]
+
+    vprob = {}
+    for v in range(n):
+        for S in range(R):
+            a = fields(S)
+            if any(a[u] >= cards[u] for u in mb[v]):
+                vprob[v, S] = [0.0] * cards[v]
+            else:
+                vprob[v, S] = _conditional(onet, cpts, v, a)
+    out = {}
+    for P in range(1, 1 << n):
+        lm = 0
+        for v in range(n):
+            if (P >> v) & 1:
+                lm |= fmask[v]
+        pos = [i for i in range(bits) if (lm >> i) & 1]
+        B = len(pos)
+        K = 1 << B
+        dep = [sum(((j >> i) & 1) << pos[i] for i in range(B)) for j in range(K)]
+        keep = (R - 1) & ~lm
+        rows = np.zeros((R, K), dtype=np.uint32)
+        for S in range(R):
+            cum, c = [], 0.0
+            for j in range(K):
+                Sn = (S & keep) | dep[j]
+                a = fields(Sn)
+                cur = fields(S)
+                p = 1.0
+                for v in order:
+                    if not (P >> v) & 1:
+                        continue
+                    if a[v] >= cards[v]:
+                        p = 0.0
+                        break
+                    p = p * vprob[v, sum(cur[u] << off[u] for u in mb[v])][a[v]]
+                    cur[v] = a[v]
+                c = p if j == 0 else c + p
+                cum.append(c)
+            scale = 2147483648.0 / c if c > 0.0 else 0.0
+            for j in range(K):
+                if scale > 0.0 and j < K - 1:
+                    rows[S, j] = int(min(math.ceil(cum[j] * scale), 2147483648.0))
+                else:
+                    rows[S, j] = 0x80000000
+        out[P] = (B, keep, np.asarray(dep, dtype=np.int64), rows)
+    return out
+
+
+def joint_sweep(tabs, cards, lanes_in, latent, key, case_base=0):
+    """One joint sweep of generic lane states (n, m, cases) with latent mask
+    (n, cases): lane (r, c) draws word r % 4 of the FAST block (case, 0,
+    quad r // 4, purpose 2) >> 1 and takes the first column j whose threshold
+    exceeds it (the last column otherwise)."""
+    width, off = lane_fields(cards)
+    n, m, cases = lanes_in.shape
+    S = np.zeros((m, cases), dtype=np.int64)
+    for v in range(n):
+        S |= lanes_in[v].astype(np.int64) << off[v]
+    P = np.zeros(cases, dtype=np.int64)
+    for v in range(n):
+        P |= latent[v].astype(np.int64) << v
+    gc = np.arange(cases, dtype=np.uint64) + np.uint64(case_base)
+    out = S.copy()
+    for r in range(m):
+        u = (fast_block(key, gc, 0, r >> 2, 2)[:, r & 3] >> np.uint32(1)).astype(np.int64)
+        for p in np.unique(P):
+            if p == 0:
+                continue
+            B, keep, dep, rows = tabs[int(p)]
+            sel = np.flatnonzero(P == p)
+            t = rows[S[r, sel]][:, :-1].astype(np.int64)
+            j = (u[sel, None] >= t).sum(axis=1)
+            out[r, sel] = (S[r, sel] & keep) | dep[j]
+    res = np.zeros_like(lanes_in)
+    for v in range(n):
+        res[v] = (out >> off[v]) & ((1 << width[v]) - 1)
+    return res
