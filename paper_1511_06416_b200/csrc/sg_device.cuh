@@ -336,47 +336,81 @@ struct CellStream {
   }
 };
 
-// log of a Gamma(a, 1) draw, a > 0 (Marsaglia & Tsang 2000; a < 1 via
-// Gamma(a) = Gamma(a + 1) * U^(1/a), kept in log space so tiny shapes never
-// underflow -- the degenerate-row redraw of model.py:168-176 is not needed).
-__device__ __forceinline__ double log_gamma_draw(CellStream& rs, double a) {
+// Gamma(a, 1) draws (Marsaglia & Tsang 2000) from a cell's Philox stream.
+// Stream layout: words 0-1 the boost uniform (a < 1: Gamma(a) = Gamma(a + 1)
+// * U^(1/a)), words 2-5 the first attempt's normal, 6-7 its acceptance
+// uniform; later attempts continue from word 8 (normal, then uniform when
+// 1 + c x > 0).  The first attempt's variates do not depend on a, so a
+// kernel can draw them before the counts arrive (GammaPre).
+struct GammaPre {
+  double ub, x, u;
+};
+__device__ __forceinline__ GammaPre gamma_pre(CellStream& rs) {
+  GammaPre g;
+  g.ub = rs.uniform();
+  g.x = rs.normal();
+  g.u = rs.uniform();
+  return g;
+}
+
+// Returns the draw g itself when a >= 1, or log g when a < 1 (*in_log set):
+// tiny shapes are carried in log space so they never underflow (the
+// degenerate-row redraw of model.py:168-176 is not needed).
+__device__ __forceinline__ double gamma_draw(CellStream& rs, const GammaPre& pre, double a, bool* in_log) {
   double boost = 0.0;
-  if (a < 1.0) {
-    boost = log(rs.uniform()) / a;
+  const bool lg = a < 1.0;
+  if (lg) {
+    boost = log(pre.ub) / a;
     a += 1.0;
   }
+  *in_log = lg;
   const double d = a - 1.0 / 3.0;
   const double c = 1.0 / sqrt(9.0 * d);
-  for (;;) {
-    double x, v;
-    do {
-      x = rs.normal();
-      v = 1.0 + c * x;
-    } while (v <= 0.0);
+  for (int attempt = 0;; ++attempt) {
+    const double x = attempt ? rs.normal() : pre.x;
+    double v = 1.0 + c * x;
+    if (v <= 0.0) continue;
+    const double u = attempt ? rs.uniform() : pre.u;
     v = v * v * v;
-    const double u = rs.uniform();
     const double x2 = x * x;
     if (u < 1.0 - 0.0331 * x2 * x2 || log(u) < 0.5 * x2 + d * (1.0 - v + log(v)))
-      return log(d) + log(v) + boost;
+      return lg ? log(d) + log(v) + boost : d * v;
   }
 }
 
-// Normalise one row of log-gamma draws into Dirichlet probabilities.
+// Normalise one row of gamma draws (val[s] = g, or log g where in_log[s])
+// into Dirichlet probabilities: linear when no cell is in log space,
+// otherwise through exp(log g - max).
 template <int K = 0>
-__device__ __forceinline__ void dirichlet_normalise(const double* lg, int card, double* out) {
+__device__ __forceinline__ void dirichlet_row(const double* val, const uint8_t* in_log, int card, double* out) {
   if (K) card = K;
+  bool any = false;
+#pragma unroll
+  for (int s = 0; s < (K ? K : card); ++s) any |= in_log[s] != 0;
+  if (!any) {
+    double sum = 0.0;
+#pragma unroll
+    for (int s = 0; s < (K ? K : card); ++s) sum += val[s];
+    const double inv = 1.0 / sum;
+#pragma unroll
+    for (int s = 0; s < (K ? K : card); ++s) out[s] = val[s] * inv;
+    return;
+  }
+  double lv[K ? K : SG_MAX_CARD];
   double mx = -INFINITY;
 #pragma unroll
-  for (int s = 0; s < (K ? K : card); ++s) mx = fmax(mx, lg[s]);
-  double e[K ? K : SG_MAX_CARD];
+  for (int s = 0; s < (K ? K : card); ++s) {
+    lv[s] = in_log[s] ? val[s] : log(val[s]);
+    mx = fmax(mx, lv[s]);
+  }
   double sum = 0.0;
 #pragma unroll
   for (int s = 0; s < (K ? K : card); ++s) {
-    e[s] = exp(lg[s] - mx);
-    sum += e[s];
+    lv[s] = exp(lv[s] - mx);
+    sum += lv[s];
   }
 #pragma unroll
-  for (int s = 0; s < (K ? K : card); ++s) out[s] = e[s] / sum;
+  for (int s = 0; s < (K ? K : card); ++s) out[s] = lv[s] / sum;
 }
 
 // One conditional-table entry from the weights w[0..card) of a blanket
@@ -410,14 +444,15 @@ __device__ __forceinline__ void table_entry(const double* w, int card, double* p
   if (!ok) atomicOr(reinterpret_cast<int*>(zs_flag), 1);
 }
 
-// p_v(x | blanket) = w_x / norm for the joint sweep's transition tables
+// p_v(x | blanket) = w_x * (1 / norm) for the joint sweep's transition tables
 // (sequential norm: cards <= 4), 0 where the blanket has no support.
 template <int K = 0>
 __device__ __forceinline__ void joint_conditional(const double* w, int card, double* out) {
   if (K) card = K;
   double norm = 0.0;
   for (int t = 0; t < card; ++t) norm = __dadd_rn(norm, w[t]);
-  for (int t = 0; t < card; ++t) out[t] = norm > 0.0 ? __ddiv_rn(w[t], norm) : 0.0;
+  const double inv = norm > 0.0 ? __ddiv_rn(1.0, norm) : 0.0;
+  for (int t = 0; t < card; ++t) out[t] = __dmul_rn(w[t], inv);
 }
 
 // Programmatic dependent launch (PDL).  A kernel launched with

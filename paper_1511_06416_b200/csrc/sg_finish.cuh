@@ -72,6 +72,7 @@ struct FinishArgs {
   uint64_t* key_current;
   double* vprob;
   int has_small;
+  int early_inputs;  // the preceding sweep triggers only after its own wait: read total/prev/key before ours
   int packed_only;  // SG_FINISH_PACKED_ONLY: skip ptab/ftab, build stab from the CPTs
   sg_small sp;
 };
@@ -113,7 +114,8 @@ static constexpr int FINISH_MAX_CELLS = 4096;
 static constexpr size_t FINISH_MAX_SMEM = 160 * 1024;
 
 __host__ __device__ inline size_t finish_smem(const sg_net& net) {
-  return size_t(net.cells) * 16 + size_t(net.blob64_words) * 8 + ((size_t(net.blob32_words) * 4 + 15) & ~size_t(15));
+  return size_t(net.cells) * 16 + size_t(net.blob64_words) * 8 + ((size_t(net.blob32_words) * 4 + 15) & ~size_t(15)) +
+         ((size_t(net.cells) + 15) & ~size_t(15));
 }
 
 // The step tail, run by ONE CTA of `nt` threads (tid = threadIdx.x).  The
@@ -128,29 +130,79 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
   int32_t* b32 = reinterpret_cast<int32_t*>(b64 + gnet.blob64_words);
   const int tid = threadIdx.x;
   const int cells = int(gnet.cells);
+  uint8_t* inlog = reinterpret_cast<uint8_t*>(b32) + ((size_t(gnet.blob32_words) * 4 + 15) & ~size_t(15));
   SG_TRACE(7);
   for (int i = tid; i < int(gnet.blob64_words); i += nt) b64[i] = __ldg(gnet.blob64 + i);
   for (int i = tid; i < int(gnet.blob32_words); i += nt) b32[i] = __ldg(gnet.blob32 + i);
-  // Everything above reads the static network pack; from here on the inputs
-  // are the sweep's counts and the previous tail's key cursor (PDL).  Once
-  // they are complete the next sweep may start its own prologue.
+  // With early_inputs the preceding sweep has waited for the previous tail
+  // before letting this grid start, so the running total, this minibatch's
+  // previous counts and the Dirichlet key are final already: load them and
+  // draw each cell's first gamma attempt (independent of the counts) while
+  // the sweep is still running.
+  const bool early = f.early_inputs != 0;
+  double t_old = 0.0, t_prev = 0.0, a_cell = 0.0;
+  GammaPre pre{};
+  int my_cell = -1;  // early path: one cell per thread
+  uint64_t key = 0;
+  if (early && cells <= nt) {
+    key = f.key_dev ? *f.key_dev : f.key;
+    if (tid < cells) {
+      my_cell = tid;
+      t_old = f.total[tid];
+      t_prev = f.prev_counts ? double(f.prev_counts[tid]) : 0.0;
+      if (!f.map_estimate) {
+        int lo = 0, hi = gnet.n;  // cell_var on the global pack (blobs not yet synchronised)
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (__ldg(gnet.cpt_off + mid) <= tid) lo = mid; else hi = mid;
+        }
+        a_cell = f.alpha[lo];
+        CellStream rs(key, uint64_t(tid));
+        pre = gamma_pre(rs);
+      }
+    }
+  }
+  // Everything above reads data no kernel in flight writes; from here on the
+  // inputs are the sweep's counts (and, without early_inputs, the previous
+  // tail's key cursor).  Once they are complete the next sweep may start its
+  // own prologue.
+  SG_TRACE(0);
   pdl_wait();
   pdl_trigger();
-  const uint64_t key = f.key_dev ? *f.key_dev : f.key;
+  if (!(early && cells <= nt)) key = f.key_dev ? *f.key_dev : f.key;
   if (tid == 0 && gnet.table_entries > 0) f.ftab[gnet.ftab_size] = 0u;
   __syncthreads();
+  SG_TRACE(1);
   const sg_net net = rebase_net(gnet, b32, b64);
   // 1. accumulator (+ the cell's gamma draw)
-  for (int i = tid; i < cells; i += nt) {
-    const double t = acc_cell(f.acc_mode, f.total[i], double(f.new_counts[i]), f.prev_counts != nullptr,
-                              f.prev_counts ? double(f.prev_counts[i]) : 0.0, f.decay);
+  if (my_cell >= 0) {
+    const int i = my_cell;
+    const double t = acc_cell(f.acc_mode, t_old, double(f.new_counts[i]), f.prev_counts != nullptr, t_prev, f.decay);
     f.total[i] = t;
     if (f.map_estimate) {
       lg[i] = t;
     } else {
-      const int v = cell_var<false>(net, i);
       CellStream rs(key, uint64_t(i));
-      lg[i] = log_gamma_draw(rs, t + f.alpha[v]);
+      rs.call = 2;  // the first attempt's words (gamma_pre) are consumed
+      bool il;
+      lg[i] = gamma_draw(rs, pre, t + a_cell, &il);
+      inlog[i] = il;
+    }
+  } else if (!(early && cells <= nt)) {
+    for (int i = tid; i < cells; i += nt) {
+      const double t = acc_cell(f.acc_mode, f.total[i], double(f.new_counts[i]), f.prev_counts != nullptr,
+                                f.prev_counts ? double(f.prev_counts[i]) : 0.0, f.decay);
+      f.total[i] = t;
+      if (f.map_estimate) {
+        lg[i] = t;
+      } else {
+        const int v = cell_var<false>(net, i);
+        CellStream rs(key, uint64_t(i));
+        const GammaPre p0 = gamma_pre(rs);
+        bool il;
+        lg[i] = gamma_draw(rs, p0, t + f.alpha[v], &il);
+        inlog[i] = il;
+      }
     }
   }
   __syncthreads();
@@ -163,7 +215,7 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     with_card(card, [&](auto C) {
       constexpr int K = decltype(C)::value;
       if (f.map_estimate) mean_row<K>(lg + base, f.alpha[v], card, cpt_s + base);
-      else dirichlet_normalise<K>(lg + base, card, cpt_s + base);
+      else dirichlet_row<K>(lg + base, inlog + base, card, cpt_s + base);
     });
     for (int s2 = 0; s2 < card; ++s2) f.cpt[base + s2] = cpt_s[base + s2];
   }
@@ -240,6 +292,7 @@ inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
   a.kps = f->kps;
   a.key_current = f->key_current;
   a.vprob = sp ? f->vprob : nullptr;
+  a.early_inputs = 0;
   a.has_small = sp ? 1 : 0;
   a.packed_only = (sp && (f->flags & SG_FINISH_PACKED_ONLY)) ? 1 : 0;
   if (sp) a.sp = *sp;

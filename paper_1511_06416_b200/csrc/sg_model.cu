@@ -7,7 +7,7 @@
 //  * sg_sample_cpts: sample_cpts (model.py:179-185) draws each row from
 //    Dirichlet(c + alpha).  numpy's standard_gamma (ziggurat normals) is not
 //    reproduced; each cell draws a Marsaglia-Tsang gamma from its own Philox
-//    substream (sg_device.cuh), carried in log space so tiny shapes never
+//    substream (sg_device.cuh), shapes below 1 carried in log space so they never
 //    underflow (the reference's degenerate-row redraw, model.py:168-176).
 //  * sg_step_finish: accumulate + CPT update + conditional tables (+ packed
 //    tables, next-count clearing, key advance) fused into ONE single-CTA
@@ -44,6 +44,7 @@ __global__ void k_mean_cpts(const sg_net net, const double* __restrict__ total, 
 __global__ void k_sample_cpts(const sg_net net, const double* __restrict__ total, const double* __restrict__ alpha,
                               uint64_t key, const uint64_t* __restrict__ key_dev, double* __restrict__ out) {
   __shared__ double lg[8][SG_MAX_CARD];
+  __shared__ uint8_t inlog[8][SG_MAX_CARD];
   if (key_dev) key = __ldg(key_dev);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -54,10 +55,13 @@ __global__ void k_sample_cpts(const sg_net net, const double* __restrict__ total
     const double a = alpha[v];
     for (int s = lane; s < card; s += 32) {
       CellStream rs(key, uint64_t(base + s));
-      lg[warp][s] = log_gamma_draw(rs, total[base + s] + a);
+      const GammaPre pre = gamma_pre(rs);
+      bool il;
+      lg[warp][s] = gamma_draw(rs, pre, total[base + s] + a, &il);
+      inlog[warp][s] = il;
     }
     __syncwarp();
-    if (lane == 0) dirichlet_normalise(lg[warp], card, out + base);
+    if (lane == 0) dirichlet_row(lg[warp], inlog[warp], card, out + base);
     __syncwarp();
   }
 }

@@ -24,7 +24,7 @@
 // Counters and draws are identical to the generic kernel's FAST mode
 // (Philox4x32 on (case, variable, replica quad)), so both paths produce the
 // same states and counts from the same tables (tests/test_gpu_small.py).
-#include "sg_device.cuh"
+#include "sg_finish.cuh"
 
 namespace sg {
 
@@ -653,7 +653,6 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   const int Q = (m + 3) >> 2;
   const int q0 = blockIdx.y * QG;
   const int last = min(QG - 1, Q - 1 - q0);
-  pdl_trigger();
   if (tid == 0) mbar_init(bar, 1);
   if (counts) {
     uint32_t* h32 = reinterpret_cast<uint32_t*>(hist8);
@@ -674,6 +673,9 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
     }
   }
   pdl_wait();  // the blob rows, tables, key and cleared counts of this step
+  // Trigger only now: the step tail that follows may then read the previous
+  // tail's outputs (running total, key, previous counts) in its prologue.
+  pdl_trigger();
   if (tid == 0) {
     mbar_expect_tx(bar, jbytes);
     for (uint32_t o2 = 0; o2 < jbytes; o2 += 32768u)
@@ -710,22 +712,28 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
 // and sequential norm; products in colour order; sequential row sums;
 // thresholds min(ceil(cum * (2^31 / total)), 2^31).
 #define SG_JOINT_TAB_SLICES 4
-__global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg_small sp, const sg_joint jp,
-                                                      const double* cpt, const double* vprob_g, uint32_t* jblob) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// Slice `slice` (lane words S in [slice * R/4, (slice+1) * R/4)) of pattern
+// P's rows.  vprob_g: the step tail's conditionals [n][R][4] (L2-coherent
+// loads: written by another CTA of the same grid in the merged tail), or
+// NULL to compute them here from cpt.
+__device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& sp, const sg_joint& jp,
+                                            const double* cpt, const double* vprob_g, uint32_t* jblob, int P,
+                                            int slice, unsigned char* smem, bool wait_pdl) {
   __shared__ uint32_t lv[SG_SMALL_MAXV][4];  // latent variables of P in colour order: off|width<<8|card<<16, mbmask, fm, v
   __shared__ int nlat;
-  const int P = blockIdx.x, tid = threadIdx.x;
-  pdl_trigger();
+  const int tid = threadIdx.x, nt = blockDim.x;
   const uint32_t meta = jblob[jp.patterns + P];  // static header
   const int B = int(meta & 0xFFu);
-  if (B == 0) return;
+  if (B == 0) {
+    if (wait_pdl) pdl_wait();
+    return;
+  }
   const uint32_t keep = (meta >> 8) & 0xFFu;
   const uint32_t* dep = reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(jblob) + (meta >> 16));
   uint32_t* rows = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(jblob) + jblob[P]);
   const int R = 1 << sp.bits, K = 1 << B;
   const int KS = K + 1;  // row stride (odd: no bank conflicts)
-  const int rows_per = R / SG_JOINT_TAB_SLICES, r0 = blockIdx.y * rows_per;
+  const int rows_per = R / SG_JOINT_TAB_SLICES, r0 = slice * rows_per;
   const int E = rows_per << B;
   double* vprob = reinterpret_cast<double*>(smem);  // [n][R][4]
   double* acc = vprob + sp.n * R * 4;               // [rows_per][KS]
@@ -743,11 +751,11 @@ __global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg
     }
     nlat = k;
   }
-  pdl_wait();  // this step's CPTs (and the tail's conditionals)
-  if (vprob_g) {  // written by the step tail (sg_finish.vprob): one coalesced copy
-    for (int i = tid; i < sp.n * R * 4; i += blockDim.x) vprob[i] = vprob_g[i];
+  if (wait_pdl) pdl_wait();  // this step's CPTs (and the tail's conditionals)
+  if (vprob_g) {
+    for (int i = tid; i < sp.n * R * 4; i += nt) vprob[i] = __ldcg(vprob_g + i);
   } else {
-    for (int i = tid; i < sp.n * R; i += blockDim.x) {
+    for (int i = tid; i < sp.n * R; i += nt) {
       const int v = i / R;
       const uint32_t S = uint32_t(i - v * R);
       if (!((P >> v) & 1) || (S & ~sp.mbmask[v])) continue;
@@ -775,7 +783,7 @@ __global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg
   }
   __syncthreads();
   const int nl = nlat;
-  for (int e = tid; e < E; e += blockDim.x) {
+  for (int e = tid; e < E; e += nt) {
     const uint32_t S = uint32_t(r0 + (e >> B));
     const uint32_t Sn = (S & keep) | dep[e & (K - 1)];
     double p = 1.0;
@@ -793,7 +801,7 @@ __global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg
     acc[(e >> B) * KS + (e & (K - 1))] = p;
   }
   __syncthreads();
-  for (int r = tid; r < rows_per; r += blockDim.x) {
+  for (int r = tid; r < rows_per; r += nt) {
     double c = 0.0;
     for (int j = 0; j < K; ++j) {
       c = j ? __dadd_rn(c, acc[r * KS + j]) : acc[r * KS];
@@ -802,13 +810,85 @@ __global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg
     scale[r] = c > 0.0 ? __ddiv_rn(2147483648.0, c) : 0.0;
   }
   __syncthreads();
-  for (int e = tid; e < E; e += blockDim.x) {
+  for (int e = tid; e < E; e += nt) {
     const int r = e >> B, j = e & (K - 1);
     const double sc = scale[r];
     uint32_t* row = rows + (r0 + r) * KS;
     row[j] = (sc > 0.0 && j != K - 1) ? uint32_t(fmin(ceil(__dmul_rn(acc[r * KS + j], sc)), 2147483648.0))
                                       : 0x80000000u;
     if (j == K - 1) row[K] = 0x80000000u;  // stride padding
+  }
+}
+
+// Rows of pattern P = blockIdx.x, lane words of slice blockIdx.y, from the
+// current CPTs (see the blob comment).  fp64 in a fixed order, no FMA:
+// p_v = w / norm with the reference's weight product (conditional_weights)
+// and sequential norm; products in colour order; sequential row sums;
+// thresholds min(ceil(cum * (2^31 / total)), 2^31).
+__global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg_small sp, const sg_joint jp,
+                                                      const double* cpt, const double* vprob_g, uint32_t* jblob) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  pdl_trigger();
+  joint_slice(net, sp, jp, cpt, vprob_g, jblob, blockIdx.x, blockIdx.y, smem, true);
+}
+
+#ifdef SG_FINISH_TRACE
+__device__ unsigned long long g_tail_trace[4 * 160];
+extern "C" int sg_debug_tail_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tail_trace, sizeof(g_tail_trace)) == cudaSuccess ? 0 : 2;
+}
+#endif
+
+// The whole step tail of the joint path in ONE grid: CTA 0 runs the
+// single-CTA tail (accumulate, CPT update, packed tables, conditionals ->
+// f.vprob, count clearing, key advance) and releases `sync[0]`; CTAs 1.. wait
+// for it and build one slice of the joint rows each.  The last CTA to finish
+// re-arms the two sync words for the next step.  (Spinning is safe: CTA 0
+// needs one SM and the grid is far below the device's resident capacity.)
+__global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net gnet, const FinishArgs f,
+                                                                    const sg_small sp, const sg_joint jp,
+                                                                    uint32_t* jblob, uint32_t* sync) {
+  extern __shared__ __align__(16) unsigned char smem[];
+#ifdef SG_FINISH_TRACE
+  auto stamp = [](int k) {
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_tail_trace[blockIdx.x * 4 + k] = t;
+    }
+  };
+#else
+  auto stamp = [](int) {};
+#endif
+  stamp(0);
+  if (blockIdx.x == 0) {
+    step_finish_body(gnet, f, smem, FINISH_THREADS);
+    stamp(1);
+    __threadfence();  // this thread's conditionals (f.vprob) are visible device-wide ...
+    __syncthreads();  // ... for every thread of the CTA before the release
+    if (threadIdx.x == 0) {
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sync), "r"(1u) : "memory");
+    }
+    return;
+  }
+  pdl_trigger();
+  pdl_wait();  // the sweep has finished reading the blob rows this grid overwrites
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(sync) : "memory");
+      if (r) break;
+    }
+  }
+  __syncthreads();
+  stamp(1);
+  const int b = blockIdx.x - 1;
+  joint_slice(gnet, sp, jp, nullptr, f.vprob, jblob, b / SG_JOINT_TAB_SLICES, b % SG_JOINT_TAB_SLICES, smem, false);
+  __syncthreads();
+  stamp(2);
+  if (threadIdx.x == 0 && atomicAdd(sync + 1, 1u) == gridDim.x - 2) {
+    sync[1] = 0u;
+    sync[0] = 0u;
   }
 }
 
@@ -982,11 +1062,13 @@ static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // one CTA per SM (one wave), but no thread's byte counters past 255 increments
+  // one CTA per SM (one wave) but one SM left free, where the step tail's
+  // first CTA starts early (PDL) and loads its inputs while the sweep runs;
+  // no thread's byte counters past 255 increments
   const int64_t per_thread = 255 / (4 * QG);
   const int64_t need = (int64_t(cases) + SG_JOINT_THREADS * per_thread - 1) / (SG_JOINT_THREADS * per_thread);
   const int64_t fill = (int64_t(cases) + SG_JOINT_THREADS - 1) / SG_JOINT_THREADS;
-  const int64_t want = std::max<int64_t>(std::max(1, sms / groups), need);
+  const int64_t want = std::max<int64_t>(std::max(1, (sms - 1) / groups), need);
   const dim3 grid(unsigned(std::max<int64_t>(1, std::min<int64_t>(want, fill))), unsigned(groups));
   launch_pdl(k_joint_sweep<N, QG>, grid, dim3(SG_JOINT_THREADS), smem, st, sp, o, jp, stab, jblob, pattern, case_id,
              lanes, lane_ld, cases, num_real, m, case_base, key, key_dev, jcell, cells,
@@ -1083,4 +1165,29 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
 #undef SG_JOINT_CASE
 #undef SG_JOINT_QG
   return check_launch("sg_joint_sweep");
+}
+
+extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const sg_finish* f, const sg_joint* jp,
+                                  uint32_t* jblob, uint32_t* sync, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(net && sp && f && jp && jblob && sync && f->vprob && f->stab, "sg_step_tail_joint: null argument");
+  SG_REQUIRE(f->acc_mode == SG_ACC_MOVING || f->acc_mode == SG_ACC_EXPONENTIAL, "sg_step_tail_joint: bad mode");
+  SG_REQUIRE(net->max_card <= SG_MAX_CARD && net->max_mb <= SG_MAX_MB, "sg_step_tail_joint: capacity exceeded");
+  SG_REQUIRE(finish_fits(*net, sp), "sg_step_tail_joint: model too large for the single-CTA tail");
+  SG_REQUIRE(sp->bits >= 2 && sp->bits <= SG_JOINT_MAXB && jp->patterns == (1 << sp->n) && jp->max_b >= 1,
+             "sg_step_tail_joint: bad joint plan");
+  if (net->table_entries > 0) SG_REQUIRE(f->ptab && f->ftab, "sg_step_tail_joint: tables required");
+  if (f->key_table) SG_REQUIRE(f->key_index && f->key_current && f->kps > 0, "sg_step_tail_joint: bad key cursor");
+  FinishArgs a = make_finish_args(f, sp);
+  a.early_inputs = 1;  // k_joint_sweep triggers after its own wait
+  const size_t smem = std::max(finish_smem(*net), joint_tables_smem(*sp, jp->max_b));
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  const dim3 grid(1 + jp->patterns * SG_JOINT_TAB_SLICES);
+  launch_pdl(k_step_tail_joint, grid, dim3(FINISH_THREADS), smem, (cudaStream_t)stream, *net, a, *sp, *jp, jblob,
+             sync);
+  return check_launch("sg_step_tail_joint");
 }

@@ -128,6 +128,7 @@ class Engine:
             self.jblob = torch.from_numpy(blob.view(np.int32)).to(d)
             # full conditionals p_v(x | lane word), written by the step tail for sg_joint_tables
             self.vprob = torch.zeros(self.n * (4 << self.pack.small.bits), dtype=torch.float64, device=d)
+            self.jsync = torch.zeros(2, dtype=torch.int32, device=d)  # sg_step_tail_joint's hand-off words
         self.tables_fresh = False  # conditional tables reflect self.cpt
         self._latent_hint = None   # latent share of the first generic minibatch (sg_batch.latent_permille)
 
@@ -268,8 +269,7 @@ class Engine:
             timing.append((ev0, ev1, S))
         if self.comm is not None:
             self.comm(new_counts)
-        _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
-        self.joint_tables(s)
+        self.step_tail(f, s)
         if moving:
             self.prev_counts[mb.index] = new_counts
             self.latent[mb.index] = db
@@ -315,6 +315,15 @@ class Engine:
                       self.jblob.data_ptr(), *tail)
         else:
             _lib.call("sg_small_sweep", self.pack.small_ref, self.stab.data_ptr(), *tail)
+
+    def step_tail(self, f, s) -> None:
+        """Accumulate, CPT update and the next visit's tables: one single-CTA
+        launch, or with rng="joint" one grid that also builds the joint rows."""
+        if self.joint:
+            _lib.call("sg_step_tail_joint", self.pack.ref, self.pack.small_ref, f, self.pack.joint_ref,
+                      self.jblob.data_ptr(), self.jsync.data_ptr(), s)
+        else:
+            _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
 
     def joint_tables(self, s, from_finish: bool = True) -> None:
         """Joint-sweep rows from the current CPTs (after every CPT update);
@@ -481,8 +490,7 @@ class StepGraphs:
                           eng.err.ptr, s)
         if eng.comm is not None:
             eng.comm(new)
-        _lib.call("sg_step_finish", eng.pack.ref, eng.small_ptr, f, s)
-        eng.joint_tables(s)
+        eng.step_tail(f, s)
 
     def step(self, mb=None) -> None:
         """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
@@ -521,8 +529,7 @@ class StepGraphs:
         eng = self.eng
         one_cta = eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
         check = 0 if eng.use_small else 1  # the packed sweep folds in the range check
-        return (check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
-                + (1 if eng.joint else 0))
+        return check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
 
     def finish(self) -> None:
         """Hand the last visit's counts back to the engine's moving-sum bookkeeping."""

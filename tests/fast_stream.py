@@ -72,8 +72,9 @@ def lane_fields(cards):
 
 
 def _conditional(onet, cpts, v, a):
-    """Full conditional of v given assignment a: parent row, then children
-    ascending, fp64 left to right, sequential norm (sampler.py:226-242)."""
+    """Full conditional of v given assignment a: the weights of
+    sampler.py:226-242 (parent row, then children ascending, fp64 left to
+    right), sequential norm, times one reciprocal of the norm."""
     cfg = sum(int(a[p]) * st for p, st in zip(onet.parents[v], onet.strides(v)))
     w = [float(x) for x in cpts[v][cfg]]
     for c in onet.children[v]:
@@ -85,7 +86,8 @@ def _conditional(onet, cpts, v, a):
     norm = 0.0
     for x in w:
         norm = norm + x
-    return [x / norm if norm > 0.0 else 0.0 for x in w]
+    inv = 1.0 / norm if norm > 0.0 else 0.0  # one reciprocal, then products (csrc joint_conditional)
+    return [x * inv for x in w]
 
 
 def joint_tables(onet, cpts, order):

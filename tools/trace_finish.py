@@ -22,9 +22,14 @@ lib.sg_debug_finish_trace.argtypes = [ctypes.c_void_p]
 net, truth = load_network_file(bundled_network_path("koller"))
 cases = 1_000_000
 obs = sg.forward_sample_device(net, truth, cases, seed=1, hide_fraction=0.5, mask_seed=2)
-names = ["stage blobs", "accumulate + gamma", "rows (Dirichlet)", "tables", "small tables", "clear + keys"]
+names = ["stage blobs", "wait + key", "accumulate + gamma", "rows (Dirichlet)", "tables", "small tables",
+         "clear + keys"]
+cold = "cold" in sys.argv
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush_rd = torch.ones(32 << 20, dtype=torch.int64, device="cuda")
+rng = "joint" if "joint" in sys.argv else "fast"
 for map_est in (False, True):
-    cfg = sg.SamplerConfig(same_m=10, minibatch_size=cases, seed=3, rng="fast", map_estimate=map_est)
+    cfg = sg.SamplerConfig(same_m=10, minibatch_size=cases, seed=3, rng=rng, map_estimate=map_est)
     eng = Engine(net, cfg)
     mb = next(iter(sg.DeviceSource(obs, cases, cases)))
     eng.visit(mb, 0, 10)
@@ -32,12 +37,15 @@ for map_est in (False, True):
     f = eng.finish_args(new, eng.prev_counts[0], 12345)
     rows = []
     for k in range(30):
+        if cold:
+            flush.fill_(k & 0xFF)
+            flush_rd.sum()
         _lib.call("sg_step_finish", eng.pack.ref, eng.small_ptr, f, stream_handle())
         torch.cuda.synchronize()
         t = (ctypes.c_ulonglong * 8)()
         lib.sg_debug_finish_trace(ctypes.cast(t, ctypes.c_void_p))
-        order = [t[7], t[0], t[2], t[3], t[4], t[5], t[6]]
+        order = [t[7], t[0], t[1], t[2], t[3], t[4], t[5], t[6]]
         rows.append([b - a for a, b in zip(order, order[1:])])
-    med = [statistics.median(r[i] for r in rows[5:]) for i in range(6)]
-    print("map" if map_est else "sampled", " | ".join(f"{n} {v / 1e3:.2f}" for n, v in zip(names, med)),
+    med = [statistics.median(r[i] for r in rows[5:]) for i in range(7)]
+    print(rng, "cold" if cold else "warm", "map" if map_est else "sampled", " | ".join(f"{n} {v / 1e3:.2f}" for n, v in zip(names, med)),
           f"| total {sum(med) / 1e3:.2f} us")
