@@ -193,10 +193,19 @@ __device__ __forceinline__ void hist_inc(uint32_t a) {
                :: "r"(a));
 }
 
+// Tally of the joint sweep: per-warp u32 histograms (65 bins: 64 lane
+// states + a trash bin) updated with shared-memory reductions.  Lanes that
+// must not count (past m, alias quads, padding cases) carry state 64 in
+// their tally byte, so the update needs no branch.
+__device__ __forceinline__ void joint_count(uint32_t base, uint32_t state) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + state * 4u) : "memory");
+}
+static constexpr int kJointBins = 65;
+
 // Walk this thread's slots: per latent variable (colour order), QG
 // independent Philox blocks (one per quad, sharing the case's first round),
 // then per quad 4 table lookups + compares and one byte-SIMD insert.
-template <int N, int QG, bool ARMED, int NT = SG_THREADS>
+template <int N, int QG, bool ARMED, int NT = SG_THREADS, bool RED = false>
 __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs, const uint32_t* stab,
                                             uint32_t* lanes, const uint8_t* __restrict__ pattern,
                                             const int32_t* __restrict__ case_id, uint32_t hist_a, int cases,
@@ -275,9 +284,15 @@ __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs
       if (tally) {
         if (full) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) hist_inc(hist_a + byte_of(wg, j) * NT);
+          for (int j = 0; j < 4; ++j) {
+            if (RED) joint_count(hist_a, byte_of(wg, j));
+            else hist_inc(hist_a + byte_of(wg, j) * NT);
+          }
         } else {
-          for (int j = 0; j < qs.last_nl; ++j) hist_inc(hist_a + byte_of(wg, j) * NT);
+          for (int j = 0; j < qs.last_nl; ++j) {
+            if (RED) joint_count(hist_a, byte_of(wg, j));
+            else hist_inc(hist_a + byte_of(wg, j) * NT);
+          }
         }
       }
     }
@@ -525,25 +540,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// Row search: the first entry j with u < row[j] (row[2^B - 1] is never read:
-// the last column takes the remaining mass).
+// Row search: the byte address (shared window) of the first entry j with
+// u < row[j] (row[2^B - 1] is never read: the last column takes the
+// remaining mass).  One LDS with an immediate offset, one compare and one
+// predicated add per level.
+template <int H>
+__device__ __forceinline__ void joint_step(uint32_t& a, uint32_t u) {
+  uint32_t t;
+  asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(t) : "r"(a), "n"((H - 1) * 4));
+  asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}" : "+r"(a) : "r"(u), "r"(t), "n"(H * 4));
+  if constexpr (H > 1) joint_step<H / 2>(a, u);
+}
 template <int B>
-__device__ __forceinline__ const uint32_t* joint_search(const uint32_t* row, uint32_t u) {
-  const uint32_t* p = row;
-#pragma unroll
-  for (int h = 1 << (B - 1); h >= 1; h >>= 1)
-    if (u >= p[h - 1]) p += h;
-  return p;
+__device__ __forceinline__ uint32_t joint_search(uint32_t a, uint32_t u) {
+  joint_step<1 << (B - 1)>(a, u);
+  return a;
 }
 
 // The QG quads of one slot: per lane one uniform (word j of the quad's
 // Philox block), one row search, one dep lookup.  Straight-line over all
 // 4 x QG lanes (no per-lane branches) so the compiler interleaves the
 // independent search chains; lanes past m and alias quads compute garbage
-// that is never stored or tallied.
+// that is never stored or tallied.  row0 / dep0: shared-window addresses.
 template <int B, int QG>
-__device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[QG], const unsigned char* row0,
-                                            const unsigned char* dep0, uint32_t keep) {
+__device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[QG], uint32_t row0, uint32_t dep0,
+                                            uint32_t keep) {
+  constexpr uint32_t kRowBytes = ((1u << B) + 1u) * 4u;  // rows 2^B + 1 words apart
 #pragma unroll
   for (int g = 0; g < QG; ++g) {
     const uint32_t u[4] = {r[g].a >> 1, r[g].b >> 1, r[g].c >> 1, r[g].d >> 1};
@@ -551,23 +573,20 @@ __device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t S = byte_of(w[g], j);
-      const unsigned char* row = row0 + (S << (B + 2)) + (S << 2);  // rows 2^B + 1 words apart
-      const uint32_t* p = joint_search<B>(reinterpret_cast<const uint32_t*>(row), u[j]);
-      const uint32_t lat = *reinterpret_cast<const uint32_t*>(dep0 + (reinterpret_cast<const unsigned char*>(p) - row));
+      const uint32_t row = row0 + S * kRowBytes;
+      const uint32_t hit = joint_search<B>(row, u[j]);
+      uint32_t lat;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lat) : "r"(hit - row + dep0));
       xs[j] = (S & keep) | lat;
     }
     w[g] = __byte_perm(__byte_perm(xs[0], xs[1], 0x0040), __byte_perm(xs[2], xs[3], 0x0040), 0x5410);
   }
 }
 
-// Per-lane byte counter += 1 without branches: lanes that must not count
-// (past m, alias quads, padding cases) increment a trash row instead.
-__device__ __forceinline__ void hist_inc_sel(bool ok, uint32_t a, uint32_t trash) { hist_inc(ok ? a : trash); }
-
 template <int QG, int NT>
 __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned char* blob, int np, uint32_t* lanes,
                                             const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id,
-                                            uint32_t hist_a, uint32_t trash_a, int cases, int num_real,
+                                            uint32_t hist_a, int cases, int num_real,
                                             int64_t case_base, const FastKey& fk, bool counts,
                                             const uint32_t (&nw0)[QG], uint32_t nP0, int nc0) {
   const uint32_t* info = reinterpret_cast<const uint32_t*>(blob);
@@ -578,10 +597,11 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
 #pragma unroll
   for (int g = 0; g < QG; ++g) nw[g] = nw0[g];
   // lanes that exist: 4 per quad before the last, last_nl in the last, none in aliases
-  uint32_t real = 0;
+  // per quad: 0x40 in the bytes of lanes that do not exist (tally -> trash row 64)
+  uint32_t trash[QG];
 #pragma unroll
   for (int g = 0; g < QG; ++g)
-    real |= (g < qs.last ? 0xFu : g == qs.last ? ((1u << qs.last_nl) - 1u) : 0u) << (4 * g);
+    trash[g] = g < qs.last ? 0u : g == qs.last ? (0x40404040u & ~qs.last_valid) : 0x40404040u;
   uint32_t* rows = lanes + qs.row0;
   for (; s < cases; s += stride) {
     uint32_t w[QG];
@@ -604,8 +624,8 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
 #pragma unroll
       for (int g = 0; g < QG; ++g)
         r[g] = fast_draw(fc, (SG_JOINT_PURPOSE << 28) | (qs.q0w + (uint32_t(min(g, qs.last)) << 16)));
-      const unsigned char* row0 = blob + info[P];
-      const unsigned char* dep0 = blob + (meta >> 16);
+      const uint32_t row0 = smem_u32(blob) + info[P];
+      const uint32_t dep0 = smem_u32(blob) + (meta >> 16);
       const uint32_t keep = (meta >> 8) & 0xFFu;
       switch (B) {
         case 1: joint_quads<1, QG>(w, r, row0, dep0, keep); break;
@@ -616,20 +636,23 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
         default: joint_quads<6, QG>(w, r, row0, dep0, keep); break;
       }
     }
-    const uint32_t tally = (counts && c < num_real) ? real : 0u;
+    const bool real_case = c < num_real;
 #pragma unroll
     for (int g = 0; g < QG; ++g) {
       const uint32_t wg = w[g] & (g < qs.last ? 0xFFFFFFFFu : qs.last_valid);
       if (g <= qs.last) rows[g * qs.ld + s] = wg;
+      if (counts) {
+        const uint32_t wt = wg | (real_case ? trash[g] : 0x40404040u);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) hist_inc_sel((tally >> (4 * g + j)) & 1u, hist_a + byte_of(wg, j) * NT, trash_a);
+        for (int j = 0; j < 4; ++j) joint_count(hist_a, byte_of(wt, j));
+      }
     }
   }
 }
 
 __host__ __device__ inline size_t joint_smem(const sg_small& sp, const sg_joint& jp, int cells) {
-  return size_t(jp.words) * 4 + size_t((sp.tab_words * 4 + 15) & ~15) +
-         ((size_t(1) << sp.bits) + 1) * SG_JOINT_THREADS + size_t((cells * 4 + 15) & ~15) + 16;
+  return size_t(jp.words) * 4 + size_t((sp.tab_words * 4 + 15) & ~15) + size_t(SG_JOINT_THREADS / 32) * 65 * 4 +
+         size_t((cells * 4 + 15) & ~15) + 16;
 }
 
 // One CTA per SM: the blob (Koller: 104 KB) + 1024 threads' byte counters.
@@ -647,7 +670,7 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   const uint32_t jbytes = uint32_t(jp.words) * 4u;
   uint32_t* stab = reinterpret_cast<uint32_t*>(smem + jbytes);
   uint8_t* hist8 = reinterpret_cast<uint8_t*>(stab) + ((sp.tab_words * 4 + 15) & ~15);
-  uint32_t* cellacc = reinterpret_cast<uint32_t*>(hist8 + ((1 << sp.bits) + 1) * NT);  // + trash row
+  uint32_t* cellacc = reinterpret_cast<uint32_t*>(hist8 + (NT / 32) * kJointBins * 4);
   uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(cellacc) + ((cells * 4 + 15) & ~15));
   const int tid = threadIdx.x;
   const int Q = (m + 3) >> 2;
@@ -656,7 +679,7 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   if (tid == 0) mbar_init(bar, 1);
   if (counts) {
     uint32_t* h32 = reinterpret_cast<uint32_t*>(hist8);
-    for (int i = tid; i < (NT << sp.bits) / 4; i += NT) h32[i] = 0;
+    for (int i = tid; i < (NT / 32) * kJointBins; i += NT) h32[i] = 0;
     for (int i = tid; i < cells; i += NT) cellacc[i] = 0;
   }
   uint32_t nw0[QG] = {};
@@ -691,19 +714,32 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   qs.last_nl = min(4, m - 4 * (q0 + qs.last));
   qs.last_valid = qs.last_nl >= 4 ? 0xFFFFFFFFu : ((1u << (8 * qs.last_nl)) - 1u);
   const int slot = ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
-  const uint32_t hist_a = smem_u32(hist8) + uint32_t(slot);
-  const uint32_t trash_a = hist_a + (uint32_t(NT) << sp.bits);
+  const uint32_t hist_a = smem_u32(hist8) + uint32_t(tid >> 5) * kJointBins * 4u;  // this warp's bins
   const FastKey fk = fast_key(key_dev ? *key_dev : key);
   __syncthreads();
   mbar_wait(bar, 0);
   bool zs = false;
   if (armed)
-    zs = small_units<N, QG, true, NT>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
+    zs = small_units<N, QG, true, NT, true>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
                                       counts != nullptr, nw0, nP0, nc0);
   else
-    joint_units<QG, NT>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, trash_a, cases, num_real,
-                        case_base, fk, counts != nullptr, nw0, nP0, nc0);
-  small_epilogue<N, NT>(sp, zs, hist8, cellacc, jcell, cells, counts, obs, ld_obs, cases, err);
+    joint_units<QG, NT>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
+                        counts != nullptr, nw0, nP0, nc0);
+  // per-warp bins -> CPT cells (jcell) -> one global atomic per touched cell
+  small_epilogue<N, NT>(sp, zs, hist8, cellacc, jcell, cells, nullptr, obs, ld_obs, cases, err);
+  if (!counts) return;
+  __syncthreads();
+  const uint32_t* wh = reinterpret_cast<const uint32_t*>(hist8);
+  for (int J = tid; J < (1 << sp.bits); J += NT) {
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (int w2 = 0; w2 < NT / 32; ++w2) sum += wh[w2 * kJointBins + J];
+    if (sum)
+      for (int v = 0; v < sp.n; ++v) atomicAdd(cellacc + __ldg(jcell + J * sp.n + v), sum);
+  }
+  __syncthreads();
+  for (int cell = tid; cell < cells; cell += NT)
+    if (cellacc[cell]) atomicAdd(counts + cell, (unsigned long long)cellacc[cell]);
 }
 
 // Rows of pattern P = blockIdx.x, lane words S of slice blockIdx.y, from the
@@ -734,10 +770,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
   const int R = 1 << sp.bits, K = 1 << B;
   const int KS = K + 1;  // row stride (odd: no bank conflicts)
   const int rows_per = R / SG_JOINT_TAB_SLICES, r0 = slice * rows_per;
-  const int E = rows_per << B;
   double* vprob = reinterpret_cast<double*>(smem);  // [n][R][4]
-  double* acc = vprob + sp.n * R * 4;               // [rows_per][KS]
-  double* scale = acc + rows_per * KS;              // [rows_per]
   if (tid == 0) {
     int k = 0;
     for (int i = 0; i < sp.n; ++i) {
@@ -782,41 +815,47 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
     }
   }
   __syncthreads();
+  // One warp per row S: lanes hold columns (2l, 2l+1) when K = 64, column l
+  // when K <= 32; products in colour order, a Kogge-Stone scan across lanes
+  // for the cumulative sums (tests/fast_stream.py restates this order).
   const int nl = nlat;
-  for (int e = tid; e < E; e += nt) {
-    const uint32_t S = uint32_t(r0 + (e >> B));
-    const uint32_t Sn = (S & keep) | dep[e & (K - 1)];
+  const int warp = tid >> 5, lane = tid & 31;
+  const bool two = K == 64;
+  auto prod = [&](uint32_t S, int j) {
+    const uint32_t Sn = (S & keep) | dep[j];
     double p = 1.0;
     uint32_t cur = S;
     for (int k = 0; k < nl; ++k) {
       const uint32_t d = lv[k][0];
       const uint32_t x = (Sn >> (d & 0xFFu)) & ((1u << ((d >> 8) & 0xFFu)) - 1u);
-      if (x >= (d >> 16)) {
-        p = 0.0;
-        break;
-      }
+      if (x >= (d >> 16)) return 0.0;
       p = __dmul_rn(p, vprob[(int(lv[k][3]) * R + int(cur & lv[k][1])) * 4 + int(x)]);
       cur = (cur & ~lv[k][2]) | (Sn & lv[k][2]);
     }
-    acc[(e >> B) * KS + (e & (K - 1))] = p;
-  }
-  __syncthreads();
-  for (int r = tid; r < rows_per; r += nt) {
-    double c = 0.0;
-    for (int j = 0; j < K; ++j) {
-      c = j ? __dadd_rn(c, acc[r * KS + j]) : acc[r * KS];
-      acc[r * KS + j] = c;
+    return p;
+  };
+  for (int r = warp; r < rows_per; r += nt >> 5) {
+    const uint32_t S = uint32_t(r0 + r);
+    const int j0 = two ? 2 * lane : lane;
+    const double a = j0 < K ? prod(S, j0) : 0.0;
+    const double b2 = two ? prod(S, j0 + 1) : 0.0;
+    double x = two ? __dadd_rn(a, b2) : a;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x = __dadd_rn(x, y);
     }
-    scale[r] = c > 0.0 ? __ddiv_rn(2147483648.0, c) : 0.0;
-  }
-  __syncthreads();
-  for (int e = tid; e < E; e += nt) {
-    const int r = e >> B, j = e & (K - 1);
-    const double sc = scale[r];
-    uint32_t* row = rows + (r0 + r) * KS;
-    row[j] = (sc > 0.0 && j != K - 1) ? uint32_t(fmin(ceil(__dmul_rn(acc[r * KS + j], sc)), 2147483648.0))
-                                      : 0x80000000u;
-    if (j == K - 1) row[K] = 0x80000000u;  // stride padding
+    const double left = __shfl_up_sync(0xffffffffu, x, 1);
+    const double total = __shfl_sync(0xffffffffu, x, two ? 31 : K - 1);
+    const double c0 = two ? (lane ? __dadd_rn(left, a) : a) : x;
+    const double sc = total > 0.0 ? __ddiv_rn(2147483648.0, total) : 0.0;
+    auto thr = [&](double c, int j) -> uint32_t {
+      return (sc > 0.0 && j != K - 1) ? uint32_t(fmin(ceil(__dmul_rn(c, sc)), 2147483648.0)) : 0x80000000u;
+    };
+    uint32_t* row = rows + S * KS;
+    if (j0 < K) row[j0] = thr(c0, j0);
+    if (two) row[j0 + 1] = thr(x, j0 + 1);
+    if (lane == 0) row[K] = 0x80000000u;  // stride padding
   }
 }
 
@@ -836,6 +875,9 @@ __global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg
 __device__ unsigned long long g_tail_trace[4 * 160];
 extern "C" int sg_debug_tail_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_tail_trace, sizeof(g_tail_trace)) == cudaSuccess ? 0 : 2;
+}
+extern "C" int sg_debug_tail_finish_trace(unsigned long long* out) {  // this TU's copy of g_finish_trace
+  return cudaMemcpyFromSymbol(out, g_finish_trace, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 2;
 }
 #endif
 
@@ -894,8 +936,8 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
 
 static size_t joint_tables_smem(const sg_small& sp, int maxb) {
   const size_t R = size_t(1) << sp.bits;
-  const size_t rows = R / SG_JOINT_TAB_SLICES;
-  return (size_t(sp.n) * R * 4 + rows * ((size_t(1) << maxb) + 1) + rows) * sizeof(double);
+  (void)maxb;
+  return size_t(sp.n) * R * 4 * sizeof(double);
 }
 
 }  // namespace sg

@@ -336,7 +336,7 @@ def joint_plan(sp, cells: int):
     the lane bits of compact column j (bit i of j -> the i-th set bit of the
     latent mask), 2^bits rows of 2^B_P thresholds, 2^B_P + 1 words apart.  Returns ``(SgJoint,
     header uint32 array)`` or None when the network does not qualify or the
-    CTA's shared memory (blob + per-variable table + byte counters) does not
+    CTA's shared memory (blob + per-variable table + per-warp tally bins) does not
     fit.
     """
     from ._lib import SgJoint
@@ -377,7 +377,7 @@ def joint_plan(sp, cells: int):
     head[2 * NP:2 * NP + len(dep)] = dep
     jp = SgJoint()
     jp.words, jp.header_words, jp.patterns, jp.max_b = words, header_words, NP, max(B)
-    smem = (words * 4 + ((sp.tab_words * 4 + 15) & ~15) + ((1 << bits) + 1) * JOINT_THREADS
+    smem = (words * 4 + ((sp.tab_words * 4 + 15) & ~15) + (JOINT_THREADS // 32) * 65 * 4
             + ((cells * 4 + 15) & ~15) + 16)
     if smem > JOINT_SMEM_LIMIT:
         return None

@@ -90,6 +90,26 @@ def _conditional(onet, cpts, v, a):
     return [x * inv for x in w]
 
 
+def warp_scan(p):
+    """Cumulative sums of one row in the device's order (csrc joint_slice):
+    K <= 32 -- one column per lane, Kogge-Stone over the lanes; K = 64 --
+    lane l holds (2l, 2l+1): its pair sum is scanned, then column 2l = the
+    left neighbour's inclusive sum + p[2l], column 2l+1 = its own."""
+    K = len(p)
+    x = p.copy() if K <= 32 else p[0::2] + p[1::2]
+    d = 1
+    while d < 32:
+        x[d:] = x[d:] + x[:-d]
+        d *= 2
+    if K <= 32:
+        return x
+    out = np.empty(K)
+    out[1::2] = x
+    out[0] = p[0]
+    out[2::2] = x[:-1] + p[2::2]
+    return out
+
+
 def joint_tables(onet, cpts, order):
     """{P: (B, keep, dep[K], rows uint32 (R, K))} for every pattern with latent bits."""
     import math
@@ -134,7 +154,7 @@ def joint_tables(onet, cpts, order):
         keep = (R - 1) & ~lm
         rows = np.zeros((R, K), dtype=np.uint32)
         for S in range(R):
-            cum, c = [], 0.0
+            prods = []
             for j in range(K):
                 Sn = (S & keep) | dep[j]
                 a = fields(Sn)
@@ -148,8 +168,9 @@ def joint_tables(onet, cpts, order):
                         break
                     p = p * vprob[v, sum(cur[u] << off[u] for u in mb[v])][a[v]]
                     cur[v] = a[v]
-                c = p if j == 0 else c + p
-                cum.append(c)
+                prods.append(p)
+            cum = warp_scan(np.asarray(prods, dtype=np.float64))
+            c = float(cum[-1])
             scale = 2147483648.0 / c if c > 0.0 else 0.0
             for j in range(K):
                 if scale > 0.0 and j < K - 1:

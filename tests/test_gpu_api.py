@@ -181,7 +181,7 @@ def _zero_support_problem():
     return net, cpts, dense
 
 
-@pytest.mark.parametrize("rng", ["numpy", "fast"])
+@pytest.mark.parametrize("rng", ["numpy", "fast", "joint"])
 @pytest.mark.parametrize("small", [True, False])
 def test_zero_support_is_flagged(rng, small):
     """sg.sweep raises ZeroSupport like the reference; the engine's kernels
@@ -196,6 +196,8 @@ def test_zero_support_is_flagged(rng, small):
             sg.sweep(net, sg.color_graph(sg.moralize(net)), cpts, batch, 7)
     if rng == "numpy" and small:
         pytest.skip("the packed-lane path is FAST-mode only")
+    if rng == "joint" and not small:
+        pytest.skip("the joint sweep runs on packed lanes only")
     # run() starts from Dirichlet(1) CPTs (full support), so plant the degenerate
     # tables in an engine and sweep once
     eng = Engine(net, sg.SamplerConfig(same_m=2, minibatch_size=4, num_passes=1, seed=1, rng=rng), small=small)

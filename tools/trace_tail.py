@@ -19,7 +19,7 @@ from paper_1511_06416_b200.io import bundled_network_path, load_network_file
 
 lib = _lib.load()
 lib.sg_debug_tail_trace.argtypes = [ctypes.c_void_p]
-lib.sg_debug_finish_trace.argtypes = [ctypes.c_void_p]
+lib.sg_debug_tail_finish_trace.argtypes = [ctypes.c_void_p]
 net, truth = load_network_file(bundled_network_path("koller"))
 cases = 1_000_000
 obs = sg.forward_sample_device(net, truth, cases, seed=1, hide_fraction=0.5, mask_seed=2)
@@ -43,7 +43,7 @@ for k in range(20):
     t = (ctypes.c_ulonglong * 640)()
     lib.sg_debug_tail_trace(ctypes.cast(t, ctypes.c_void_p))
     ft = (ctypes.c_ulonglong * 8)()
-    lib.sg_debug_finish_trace(ctypes.cast(ft, ctypes.c_void_p))
+    lib.sg_debug_tail_finish_trace(ctypes.cast(ft, ctypes.c_void_p))
     t0 = min(t[4 * b] for b in range(G))
     lead_start, lead_end = t[0] - t0, t[1] - t0
     starts = [t[4 * b] - t0 for b in range(1, G)]
