@@ -319,7 +319,8 @@ def our_arm(args, wl: Workload) -> None:
         total_replays = graph_warm + args.steps + 2 + e2e_steps
         # private double-buffered observation blocks: e2e steps upload the next block
         # on a copy stream while the current visit runs
-        graphs = StepGraphs(eng, mb, M, range(first, first + total_replays))
+        # joint path: observation blocks travel in the 4-bit .sgb form (half the PCIe bytes)
+        graphs = StepGraphs(eng, mb, M, range(first, first + total_replays), nibbles=eng.joint)
         for _ in range(graph_warm):
             graphs.step()
         first += graph_warm
@@ -367,17 +368,31 @@ def our_arm(args, wl: Workload) -> None:
     value = world * node_samples / (ms * 1e-3)
 
     # ---- e2e through the public API: pinned host minibatch -> device, step, CPTs back to host
-    host_obs = torch.empty((n_vars, CASES), dtype=torch.int8, pin_memory=True)
-    host_obs.copy_(obs[:, :CASES])
+    if graphs is not None and graphs.nibbles:
+        from paper_1511_06416_b200.io import pack_nibbles
+
+        pitch4 = graphs.obs_bufs[0].shape[1] * 2
+        host_obs = torch.empty((n_vars, pitch4 // 2), dtype=torch.uint8, pin_memory=True)
+        host_obs.copy_(pack_nibbles(obs[:, :CASES], pitch4).cpu())  # the minibatch as an .sgb 4-bit block
+    else:
+        host_obs = torch.empty((n_vars, CASES), dtype=torch.int8, pin_memory=True)
+        host_obs.copy_(obs[:, :CASES])
     hmb = sg.Minibatch(index=0, values=host_obs, weights=np.ones(CASES), num_real=CASES)
     cpt_host = torch.empty(eng.pack.cells, dtype=torch.float64, pin_memory=True)
+    e2e_graphs = None
+    if graphs is not None:
+        # host-fed step graphs: each replay uploads the next visit's pinned block on a
+        # side branch overlapped with the sweep, and reads the CPTs back at its end
+        graphs.finish()
+        e2e_graphs = StepGraphs(eng, mb, M, range(first + args.steps + 10, first + args.steps + 20 + e2e_steps),
+                                nibbles=graphs.nibbles, host_block=host_obs, readback=[(eng.cpt, cpt_host)])
 
     def e2e_step(k):
-        if graphs is not None:
-            graphs.step(hmb)  # H2D of the minibatch into the graph's observation buffer, then replay
+        if e2e_graphs is not None:
+            e2e_graphs.step()  # one graph launch: H2D of the next block || sweep -> tail -> CPTs to host
         else:
             eng.visit(hmb, 20_000 + k, M)
-        cpt_host.copy_(eng.cpt, non_blocking=True)
+            cpt_host.copy_(eng.cpt, non_blocking=True)
 
     for w in range(2):
         e2e_step(w)
@@ -385,12 +400,26 @@ def our_arm(args, wl: Workload) -> None:
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dbg = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)] if os.environ.get("SG_E2E_DEBUG") else None
     e0.record()
     for k in range(e2e_steps):
         e2e_step(k)
+        if dbg:
+            dbg[k].record()
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dbg:
+        print("e2e per-step us:", [round((dbg[k].elapsed_time(dbg[k + 1])) * 1e3, 1) for k in range(e2e_steps - 1)],
+              file=sys.stderr)
+        dst = torch.empty_like(host_obs, device="cuda")
+        for rep in range(3):
+            e0.record()
+            for _ in range(20):
+                dst.copy_(host_obs, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"H2D alone: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us for {host_obs.numel()} B", file=sys.stderr)
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -420,7 +449,8 @@ def our_arm(args, wl: Workload) -> None:
                          "bytes_per_node_sample": bpns, "peak_source": peak_src,
                          "traffic_source": traffic_src, "sweep_share_of_step": sw / ms,
                          "limiter": "instruction issue (Philox + table draws), not HBM: see DESIGN.md 6"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n_vars * CASES,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_obs.numel()),
+                    "host_format": "4-bit .sgb block" if host_obs.dtype == torch.uint8 else "int8 block",
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",

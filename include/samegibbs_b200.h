@@ -156,6 +156,14 @@ typedef struct sg_batch {
 /* Version of this ABI (SG_ABI_VERSION). */
 int sg_abi_version(void);
 
+/* Stream-ordered copy (cudaMemcpyDefault: pinned host <-> device), recorded
+   as a memcpy node when `stream` is capturing a CUDA graph. */
+int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* Small stream-ordered copy done by a kernel (8-byte aligned); dst may be
+   pinned host memory (mapped through unified addressing). */
+int sg_copy_small(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* Text of the last failing call on this host thread ("" if none). */
 const char* sg_last_error(void);
 
@@ -355,14 +363,16 @@ int sg_joint_smem(const sg_small* sp, const sg_joint* jp, int32_t cells, int64_t
 /* Sweep + tally on packed lanes with one uniform per lane (FAST Philox
    counters with purpose 2, v = 0).  Arguments as sg_small_sweep plus the
    joint plan and blob; when zs_flag is armed the per-variable path runs
-   instead (exact ZeroSupport semantics). */
+   instead (exact ZeroSupport semantics).  obs_nibbles != 0: obs is the 4-bit
+   block of an .sgb file (ld_obs bytes per row, two cases per byte, case 2j
+   in the low nibble, 15 = missing) and is range-checked in that form. */
 int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint32_t* stab,
                    const uint32_t* jblob, const uint8_t* pattern, const int32_t* case_id,
                    uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real,
                    int32_t m, int64_t case_base, uint64_t key, const uint64_t* key_dev,
                    const int32_t* jcell, int32_t cells, uint64_t* counts,
                    const uint32_t* zs_flag, const int8_t* obs, int32_t ld_obs,
-                   int32_t* err, void* stream);
+                   int32_t obs_nibbles, int32_t* err, void* stream);
 
 /* Layout switches between packed lanes and sg_batch int8 lane states. */
 int sg_small_import(const sg_small* sp, const sg_batch* batch, const int32_t* case_id,

@@ -1,4 +1,5 @@
 // Error reporting of the C-ABI: a thread-local message plus sg_status codes.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 
@@ -29,3 +30,39 @@ int check_launch(const char* what) {
 extern "C" int sg_abi_version(void) { return SG_ABI_VERSION; }
 
 extern "C" const char* sg_last_error(void) { return sg::g_last_error; }
+
+// Stream-ordered copy between any two of host (pinned) / device memory; it
+// is captured as a memcpy node when the stream is capturing a CUDA graph
+// (StepGraphs: the next minibatch's upload inside the step graph).
+extern "C" int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(dst && src && bytes >= 0, "sg_copy_async: bad argument");
+  if (bytes == 0) return SG_OK;
+  const cudaError_t e = cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    set_error("sg_copy_async: %s", cudaGetErrorString(e));
+    return SG_ECUDA;
+  }
+  return SG_OK;
+}
+
+// Small copy as a kernel (graph kernel nodes launch faster than memcpy
+// nodes): dst may be pinned host memory, which unified addressing maps into
+// the device's address space -- the step graph's CPT read-back.
+__global__ void k_copy_words(unsigned long long* dst, const unsigned long long* src, int64_t words) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < words; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+extern "C" int sg_copy_small(void* dst, const void* src, int64_t bytes, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(dst && src && bytes >= 0 && bytes % 8 == 0 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0 &&
+                 (reinterpret_cast<uintptr_t>(src) & 7) == 0,
+             "sg_copy_small: 8-byte aligned pointers and sizes required");
+  if (bytes == 0) return SG_OK;
+  const int64_t words = bytes / 8;
+  const int blocks = int(std::min<int64_t>((words + 255) / 256, 64));
+  k_copy_words<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<unsigned long long*>(dst),
+                                                        static_cast<const unsigned long long*>(src), words);
+  return check_launch("sg_copy_small");
+}

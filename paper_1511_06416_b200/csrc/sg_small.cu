@@ -310,10 +310,35 @@ __device__ __forceinline__ void small_epilogue(const sg_small& sp, bool zs, cons
                                                const int32_t* __restrict__ jcell, int cells,
                                                unsigned long long* __restrict__ counts,
                                                const int8_t* __restrict__ obs, int ld_obs, int cases,
-                                               int32_t* err) {
+                                               int32_t* err, int nib = 0) {
   const int tid = threadIdx.x;
   if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
-  if (obs) {  // the minibatch's range check (sampler.py:429-430), spread over the whole grid
+  if (obs && nib) {  // 4-bit observations (io.py .sgb): two cases per byte, 15 = missing
+    const int chunks = (cases + 31) >> 5;
+    const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + tid;
+    const int gthreads = gridDim.x * gridDim.y * NT;
+    unsigned bad = 0;
+    for (int i = gtid; i < N * chunks; i += gthreads) {
+      const int v = i / chunks, ch = i - v * chunks;
+      const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
+      const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
+      const uint32_t wv[4] = {uint32_t(qv.x), uint32_t(qv.y), uint32_t(qv.z), uint32_t(qv.w)};
+      const int left = cases - ch * 32;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // low nibbles: even cases, high nibbles: odd cases
+          const uint32_t x = (wv[k] >> (4 * h)) & 0x0F0F0F0Fu;
+          uint32_t gt = __vcmpgtu4(x, lim) & ~__vcmpeq4(x, 0x0F0F0F0Fu);
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (8 * k + 2 * b + h >= left) gt &= ~(0xFFu << (8 * b));
+          bad |= gt;
+        }
+      }
+    }
+    if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
+  } else if (obs) {  // the minibatch's range check (sampler.py:429-430), spread over the whole grid
     const int chunks = (cases + 15) >> 4;
     const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + tid;
     const int gthreads = gridDim.x * gridDim.y * NT;
@@ -663,7 +688,7 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
               const int32_t* __restrict__ case_id, uint32_t* __restrict__ lanes, int lane_ld, int cases, int num_real,
               int m, int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* __restrict__ jcell,
               int cells, unsigned long long* __restrict__ counts, const uint32_t* zs_flag,
-              const int8_t* __restrict__ obs, int ld_obs, int32_t* err) {
+              const int8_t* __restrict__ obs, int ld_obs, int obs_nib, int32_t* err) {
   constexpr int NT = SG_JOINT_THREADS;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* blob = smem;
@@ -726,7 +751,7 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
     joint_units<QG, NT>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
                         counts != nullptr, nw0, nP0, nc0);
   // per-warp bins -> CPT cells (jcell) -> one global atomic per touched cell
-  small_epilogue<N, NT>(sp, zs, hist8, cellacc, jcell, cells, nullptr, obs, ld_obs, cases, err);
+  small_epilogue<N, NT>(sp, zs, hist8, cellacc, jcell, cells, nullptr, obs, ld_obs, cases, err, obs_nib);
   if (!counts) return;
   __syncthreads();
   const uint32_t* wh = reinterpret_cast<const uint32_t*>(hist8);
@@ -1092,7 +1117,8 @@ static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& 
                          cudaStream_t st, const uint32_t* stab, const uint32_t* jblob, const uint8_t* pattern,
                          const int32_t* case_id, uint32_t* lanes, int lane_ld, int cases, int num_real, int m,
                          int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell, int cells,
-                         uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs, int ld_obs, int32_t* err) {
+                         uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs, int ld_obs, int obs_nib,
+                         int32_t* err) {
   static size_t configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(k_joint_sweep<N, QG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -1114,7 +1140,7 @@ static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& 
   const dim3 grid(unsigned(std::max<int64_t>(1, std::min<int64_t>(want, fill))), unsigned(groups));
   launch_pdl(k_joint_sweep<N, QG>, grid, dim3(SG_JOINT_THREADS), smem, st, sp, o, jp, stab, jblob, pattern, case_id,
              lanes, lane_ld, cases, num_real, m, case_base, key, key_dev, jcell, cells,
-             reinterpret_cast<unsigned long long*>(counts), zs_flag, obs, ld_obs, err);
+             reinterpret_cast<unsigned long long*>(counts), zs_flag, obs, ld_obs, obs_nib, err);
 }
 
 static bool joint_plan_ok(const sg_small& sp, const sg_joint& jp, int cells) {
@@ -1153,13 +1179,17 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
                               const uint8_t* pattern, const int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
                               int32_t cases, int32_t num_real, int32_t m, int64_t case_base, uint64_t key,
                               const uint64_t* key_dev, const int32_t* jcell, int32_t cells, uint64_t* counts,
-                              const uint32_t* zs_flag, const int8_t* obs, int32_t ld_obs, int32_t* err, void* stream) {
+                              const uint32_t* zs_flag, const int8_t* obs, int32_t ld_obs, int32_t obs_nibbles,
+                              int32_t* err, void* stream) {
   using namespace sg;
   SG_REQUIRE(sp && jp && stab && jblob && pattern && case_id && lanes && err, "sg_joint_sweep: null argument");
   SG_REQUIRE((reinterpret_cast<uintptr_t>(jblob) & 15) == 0, "sg_joint_sweep: blob must be 16-byte aligned");
   if (obs)
-    SG_REQUIRE(ld_obs % 16 == 0 && (reinterpret_cast<uintptr_t>(obs) & 15) == 0 && ld_obs >= cases,
+    SG_REQUIRE(ld_obs % 16 == 0 && (reinterpret_cast<uintptr_t>(obs) & 15) == 0 &&
+                   int64_t(ld_obs) * (obs_nibbles ? 2 : 1) >= cases,
                "sg_joint_sweep: obs rows must be 16-byte aligned");
+  if (obs_nibbles)
+    for (int v = 0; v < sp->n; ++v) SG_REQUIRE(sp->card[v] <= 15, "sg_joint_sweep: 4-bit observations need cards <= 15");
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV, "sg_joint_sweep: bad plan");
   SG_REQUIRE(joint_plan_ok(*sp, *jp, cells), "sg_joint_sweep: joint plan does not fit (bits %d, words %d)", sp->bits,
              jp->words);
@@ -1182,7 +1212,8 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
 #define SG_JOINT_QG(NV, G)                                                                                     \
   case G:                                                                                                      \
     launch_joint<NV, G>(*sp, o, *jp, groups, smem, st, stab, jblob, pattern, case_id, lw, lane_ld, cases,      \
-                        num_real, m, case_base, key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs, err); \
+                        num_real, m, case_base, key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs,      \
+                        obs_nibbles, err);                                                                     \
     break;
 #define SG_JOINT_CASE(NV) \
   case NV:                \

@@ -23,6 +23,7 @@ from . import _lib
 from .device import ErrorWord, device, netpack, stream_handle
 from .errors import ValidationError
 from .metrics import kl_avg
+from .io import pack_nibbles
 from .model import CptSet, init_cpts
 from .network import Network, color_graph, moralize
 from .rng import derive_seed, stream_key_ints
@@ -304,17 +305,21 @@ class Engine:
         self._finish_keepalive = f
         return f
 
-    def packed_sweep(self, db, size: int, m: int, key: int, key_dev, counts_ptr, obs_ptr, ld: int, s) -> None:
+    def packed_sweep(self, db, size: int, m: int, key: int, key_dev, counts_ptr, obs_ptr, ld: int, s,
+                     obs_nibbles: bool = False) -> None:
         """Sweep + tally of a packed-lane minibatch: per-variable draws
-        (sg_small_sweep) or, with rng="joint", one draw per lane (sg_joint_sweep)."""
-        tail = (db.pattern.data_ptr(), db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m,
+        (sg_small_sweep) or, with rng="joint", one draw per lane (sg_joint_sweep;
+        ``obs_nibbles``: the range-checked block is 4-bit, ``ld`` bytes per row)."""
+        head = (db.pattern.data_ptr(), db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m,
                 self.case_base, key, key_dev, self.pack.small_jcell.data_ptr(), self.pack.cells, counts_ptr,
-                self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"], obs_ptr, ld, self.err.ptr, s)
+                self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"], obs_ptr, ld)
         if self.joint:
             _lib.call("sg_joint_sweep", self.pack.small_ref, self.pack.joint_ref, self.stab.data_ptr(),
-                      self.jblob.data_ptr(), *tail)
+                      self.jblob.data_ptr(), *head, 1 if obs_nibbles else 0, self.err.ptr, s)
         else:
-            _lib.call("sg_small_sweep", self.pack.small_ref, self.stab.data_ptr(), *tail)
+            if obs_nibbles:
+                raise ValueError("4-bit observation blocks are range-checked by the joint sweep only")
+            _lib.call("sg_small_sweep", self.pack.small_ref, self.stab.data_ptr(), *head, self.err.ptr, s)
 
     def step_tail(self, f, s) -> None:
         """Accumulate, CPT update and the next visit's tables: one single-CTA
@@ -400,11 +405,22 @@ class StepGraphs:
     so results equal eager visits bit for bit (FAST RNG mode).
     """
 
-    def __init__(self, eng: Engine, mb, m: int, pass_indices, obs_buffer: torch.Tensor | None = None):
+    def __init__(self, eng: Engine, mb, m: int, pass_indices, obs_buffer: torch.Tensor | None = None,
+                 nibbles: bool = False, host_block: torch.Tensor | None = None, readback=()):
         """``obs_buffer``: device int8 (n, pitch) tensor the graphs read the
         minibatch's observations from; the caller keeps it filled (e.g. a
         device-resident source).  Default: a private buffer that
-        :meth:`step` refills from the minibatch passed to it."""
+        :meth:`step` refills from the minibatch passed to it.  ``nibbles``
+        (joint sweep, private buffers): :meth:`step` takes the minibatch in
+        the 4-bit .sgb block form (uint8 (n, pitch // 2), io.py), half the
+        host-to-device bytes, range-checked in that form on the device.
+
+        ``host_block`` (pinned, the private buffers' layout): every replay
+        also uploads this block into the OTHER parity's buffer -- the next
+        visit's input -- on a side branch of the graph, overlapped with the
+        sweep, so a host-fed step is one graph launch.  ``readback``: pairs
+        (device tensor, pinned host tensor) copied back at the end of each
+        replay (e.g. the CPTs)."""
         cfg = eng.cfg
         if eng.rng_mode != _lib.SG_RNG_FAST or cfg.accumulator_mode != "moving_sum":
             raise ValueError("graph replay needs the fast RNG and the moving-sum accumulator")
@@ -428,14 +444,21 @@ class StepGraphs:
         self.replayed = 0
         prev = eng.prev_counts[mb.index]
         self.cbuf = [torch.zeros_like(prev), prev.clone()]
+        self.nibbles = bool(nibbles)
+        if self.nibbles and (obs_buffer is not None or not eng.joint):
+            raise ValueError("4-bit uploads need the joint sweep and private observation buffers")
         if obs_buffer is None:
             # two private buffers, one per graph parity: step(mb) uploads the next
             # visit's block on a copy stream while the current visit runs
             src, _ = eng._obs_for(mb)
             bufs = []
+            shape, dt = self.obs_geometry(eng.n, mb.size, self.nibbles)
             for _ in range(2):
-                b = torch.empty((eng.n, _pitch(mb.size)), dtype=torch.int8, device=d)
-                b[:, :src.shape[1]].copy_(src[:, :b.shape[1]])
+                b = torch.empty(shape, dtype=dt, device=d)
+                if self.nibbles:
+                    b.copy_(pack_nibbles(src[:, :mb.size], shape[1] * 2))
+                else:
+                    b[:, :src.shape[1]].copy_(src[:, :b.shape[1]])
                 bufs.append(b)
             self.private_obs = True
         else:
@@ -446,6 +469,18 @@ class StepGraphs:
                 raise ValueError("obs_buffer must be an int8 (n, pitch) tensor with 16-byte aligned rows")
         self.obs_bufs, self.ld = bufs, bufs[0].stride(0)
         self.obs = bufs[0]
+        self.host_block = host_block
+        self.readback = list(readback)
+        if host_block is not None:
+            if obs_buffer is not None or not host_block.is_pinned() or host_block.dtype != bufs[0].dtype \
+                    or tuple(host_block.shape) != tuple(bufs[0].shape) or not host_block.is_contiguous():
+                raise ValueError(f"host_block must be a pinned contiguous {bufs[0].dtype} {tuple(bufs[0].shape)}")
+            for b in bufs:
+                b.copy_(host_block)
+            self._side = torch.cuda.Stream()
+        for dev_t, host_t in self.readback:
+            if not host_t.is_pinned() or host_t.numel() * host_t.element_size() < dev_t.numel() * dev_t.element_size():
+                raise ValueError("readback targets must be pinned host tensors large enough")
         self._copy_stream = None
         self._buf_free: list = [None, None]  # event: the last replay reading buffer p has finished
         self.graphs = []
@@ -463,6 +498,15 @@ class StepGraphs:
             self.graphs.append(g)
         torch.cuda.synchronize()
 
+    @staticmethod
+    def obs_geometry(n: int, size: int, nibbles: bool = False):
+        """(shape, dtype) of the private observation buffers (and of a host_block)."""
+        pitch = _pitch(size)
+        if nibbles:
+            pitch = max(32, (pitch + 31) // 32 * 32)
+            return (n, pitch // 2), torch.uint8
+        return (n, pitch), torch.int8
+
     def _record(self, p: int) -> None:
         eng, db, m, cfg = self.eng, self.db, self.m, self.eng.cfg
         s = stream_handle()
@@ -470,6 +514,14 @@ class StepGraphs:
         cur = self.cur.data_ptr()
         new, prev = self.cbuf[p], self.cbuf[1 - p]
         obs = self.obs_bufs[p]
+        main = torch.cuda.current_stream()
+        if self.host_block is not None:  # fork: upload the next visit's block beside the sweep
+            fork = torch.cuda.Event()
+            fork.record(main)
+            self._side.wait_event(fork)
+            nxt = self.obs_bufs[1 - p]
+            _lib.call("sg_copy_async", nxt.data_ptr(), self.host_block.data_ptr(),
+                      nxt.numel() * nxt.element_size(), self._side.cuda_stream)
         # tables and keys of this visit are ready: the previous replay's finish built/advanced them
         if not eng.use_small:  # the packed sweep checks the block in its own launch
             _lib.call("sg_check_range", eng.pack.ref, obs.data_ptr(), self.ld, size, eng.err.ptr, s)
@@ -483,7 +535,8 @@ class StepGraphs:
             last = sw == S - 1
             counts_ptr = new.data_ptr() if last else None
             if eng.use_small:
-                eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr, obs.data_ptr() if last else None, self.ld, s)
+                eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr, obs.data_ptr() if last else None, self.ld, s,
+                                 obs_nibbles=self.nibbles)
             else:
                 _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
@@ -491,6 +544,16 @@ class StepGraphs:
         if eng.comm is not None:
             eng.comm(new)
         eng.step_tail(f, s)
+        for dev_t, host_t in self.readback:  # a kernel node (faster than a D2H memcpy node) into mapped pinned memory
+            nbytes = dev_t.numel() * dev_t.element_size()
+            if nbytes % 8 == 0 and dev_t.data_ptr() % 8 == 0 and host_t.data_ptr() % 8 == 0:
+                _lib.call("sg_copy_small", host_t.data_ptr(), dev_t.data_ptr(), nbytes, s)
+            else:
+                _lib.call("sg_copy_async", host_t.data_ptr(), dev_t.data_ptr(), nbytes, s)
+        if self.host_block is not None:  # join the upload branch (the read-back above overlaps its tail)
+            join = torch.cuda.Event()
+            join.record(self._side)
+            main.wait_event(join)
 
     def step(self, mb=None) -> None:
         """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
@@ -498,11 +561,15 @@ class StepGraphs:
             raise IndexError("all planned visits have been replayed")
         p = self.replayed % 2
         main = torch.cuda.current_stream()
+        if mb is not None and self.host_block is not None:
+            raise ValueError("this graph uploads its own host block; call step() without a minibatch")
         if mb is not None:
             vals = mb.values
             buf = self.obs_bufs[p]
             if not (isinstance(vals, torch.Tensor) and vals.is_cuda and vals.data_ptr() == buf.data_ptr()):
                 src = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(np.asarray(vals, dtype=np.int8))
+                if self.nibbles and (src.dtype != torch.uint8 or tuple(src.shape) != tuple(buf.shape)):
+                    raise ValueError(f"expected a 4-bit block uint8 {tuple(buf.shape)} (io.pack_nibbles)")
                 if not self.private_obs:
                     buf[:, :mb.size].copy_(src, non_blocking=True)
                 else:
@@ -514,7 +581,10 @@ class StepGraphs:
                     if self._buf_free[p] is not None:
                         cs.wait_event(self._buf_free[p])
                     with torch.cuda.stream(cs):
-                        buf[:, :mb.size].copy_(src, non_blocking=True)
+                        if self.nibbles:
+                            buf.copy_(src, non_blocking=True)
+                        else:
+                            buf[:, :mb.size].copy_(src, non_blocking=True)
                     main.wait_stream(cs)
         self.graphs[p].replay()
         if self.private_obs:
@@ -527,9 +597,11 @@ class StepGraphs:
     @property
     def launches_per_step(self) -> int:
         eng = self.eng
+        readback = len(self.readback)
         one_cta = eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
         check = 0 if eng.use_small else 1  # the packed sweep folds in the range check
-        return check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
+        return (check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
+                + readback)
 
     def finish(self) -> None:
         """Hand the last visit's counts back to the engine's moving-sum bookkeeping."""

@@ -94,6 +94,24 @@ _SGB_MAGIC = b"SGB1"
 _SGB_HEADER = struct.Struct("<4sIIQIII")
 
 
+def pack_nibbles(block, pitch: int):
+    """(n, cases) observation block (int, -1 = missing, states <= 14) -> the
+    4-bit .sgb form: uint8 (n, pitch // 2), case 2j in the low nibble, 15 =
+    missing (also for the padding columns up to ``pitch``, a multiple of 32).
+    Works on numpy arrays and on (host or device) torch tensors."""
+    if pitch % 32 or pitch < block.shape[1]:
+        raise ValueError("pitch must be a multiple of 32 covering the block")
+    if isinstance(block, torch.Tensor):
+        u = torch.full((block.shape[0], pitch), 15, dtype=torch.uint8, device=block.device)
+        b = block.to(torch.int16)
+        u[:, :block.shape[1]] = torch.where(b < 0, 15, b).to(torch.uint8)
+        return u[:, 0::2] | (u[:, 1::2] << 4)
+    arr = np.asarray(block)
+    u = np.full((arr.shape[0], pitch), 15, dtype=np.uint8)
+    u[:, :arr.shape[1]] = np.where(arr < 0, 15, arr).astype(np.uint8)
+    return (u[:, 0::2] | (u[:, 1::2] << 4)).astype(np.uint8)
+
+
 def write_binary(path, data, block_cases: int, encoding: str = "int8") -> None:
     """Write a DataMatrix or a dense (num_vars, num_cases) int matrix (-1 = missing) as ``.sgb``."""
     from .datagen import DataMatrix
@@ -120,8 +138,7 @@ def write_binary(path, data, block_cases: int, encoding: str = "int8") -> None:
             blk = np.full((n, pitch), -1, dtype=np.int8)
             blk[:, :hi - lo] = dense[:, lo:hi]
             if encoding == "nibble":
-                u = np.where(blk < 0, 15, blk).astype(np.uint8)
-                blk = (u[:, 0::2] | (u[:, 1::2] << 4)).astype(np.uint8)
+                blk = pack_nibbles(blk, pitch)
             f.write(blk.tobytes())
 
 

@@ -101,3 +101,19 @@ def test_sgb_writer_layout(tmp_path, encoding):
         np.testing.assert_array_equal(got, want)
     with pytest.raises(ValueError):
         io.write_binary(tmp_path / "x.sgb", np.full((1, 4), 15), 4, "nibble")
+
+
+def test_pack_nibbles_matches_sgb_blocks(tmp_path):
+    """io.pack_nibbles (numpy and torch) is the 4-bit .sgb block layout."""
+    import numpy as np
+    import torch
+
+    from paper_1511_06416_b200 import io
+
+    rng = np.random.default_rng(3)
+    dense = rng.integers(-1, 5, size=(4, 45)).astype(np.int32)
+    io.write_binary(tmp_path / "a.sgb", dense, block_cases=45, encoding="nibble")
+    h = io.read_binary_header(tmp_path / "a.sgb")
+    raw = np.fromfile(tmp_path / "a.sgb", dtype=np.uint8)[64:].reshape(4, h["pitch"] // 2)
+    np.testing.assert_array_equal(io.pack_nibbles(dense, h["pitch"]), raw)
+    np.testing.assert_array_equal(io.pack_nibbles(torch.from_numpy(dense), h["pitch"]).numpy(), raw)
