@@ -387,13 +387,26 @@ def our_arm(args, wl: Workload) -> None:
         e2e_graphs = StepGraphs(eng, mb, M, range(first + args.steps + 10, first + args.steps + 20 + e2e_steps),
                                 nibbles=graphs.nibbles, host_block=host_obs, readback=[(eng.cpt, cpt_host)])
 
+    ready = [torch.cuda.Event(), torch.cuda.Event()]
+
     def e2e_step(k):
         if e2e_graphs is not None:
-            e2e_graphs.step()  # one graph launch: H2D of the next block || sweep -> tail -> CPTs to host
+            e2e_graphs.step()  # H2D of the next block (copy stream) || replay: sweep -> tail -> CPTs to host
         else:
             eng.visit(hmb, 20_000 + k, M)
             cpt_host.copy_(eng.cpt, non_blocking=True)
+        ready[k % 2].record()  # the host may read this step's CPTs once it has completed
 
+    # The PCIe link drops to a low-power state while the device-only steps run;
+    # bring it back to full speed (~25 ms of uploads) before the e2e region, as
+    # a streaming pipeline would keep it.
+    scratch = torch.empty_like(host_obs, device="cuda")
+    t_warm = time.perf_counter()
+    while time.perf_counter() - t_warm < 0.025:
+        for _ in range(8):
+            scratch.copy_(host_obs, non_blocking=True)
+        torch.cuda.synchronize()
+    del scratch
     for w in range(2):
         e2e_step(w)
     torch.cuda.synchronize()
@@ -401,25 +414,19 @@ def our_arm(args, wl: Workload) -> None:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dbg = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)] if os.environ.get("SG_E2E_DEBUG") else None
-    e0.record()
-    for k in range(e2e_steps):
-        e2e_step(k)
-        if dbg:
-            dbg[k].record()
-    e1.record()
-    torch.cuda.synchronize()
+    with ClockSampler(local) as e2e_clk:
+        e0.record()
+        for k in range(e2e_steps):
+            e2e_step(k)
+            if dbg:
+                dbg[k].record()
+        e1.record()
+        torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if dbg:
         print("e2e per-step us:", [round((dbg[k].elapsed_time(dbg[k + 1])) * 1e3, 1) for k in range(e2e_steps - 1)],
               file=sys.stderr)
-        dst = torch.empty_like(host_obs, device="cuda")
-        for rep in range(3):
-            e0.record()
-            for _ in range(20):
-                dst.copy_(host_obs, non_blocking=True)
-            e1.record()
-            torch.cuda.synchronize()
-            print(f"H2D alone: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us for {host_obs.numel()} B", file=sys.stderr)
+        print("e2e clocks:", e2e_clk.summary(), file=sys.stderr)
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -448,7 +455,9 @@ def our_arm(args, wl: Workload) -> None:
                          "kernel_ms": sw, "algorithmic_bytes_per_launch": algo_bytes,
                          "bytes_per_node_sample": bpns, "peak_source": peak_src,
                          "traffic_source": traffic_src, "sweep_share_of_step": sw / ms,
-                         "limiter": "instruction issue (Philox + table draws), not HBM: see DESIGN.md 6"},
+                         "limiter": ("shared-memory row searches (bank conflicts) + Philox issue, not HBM: "
+                                     "see DESIGN.md 6" if eng.joint else
+                                     "instruction issue (Philox + table draws), not HBM: see DESIGN.md 6")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_obs.numel()),
                     "host_format": "4-bit .sgb block" if host_obs.dtype == torch.uint8 else "int8 block",
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},

@@ -415,10 +415,10 @@ class StepGraphs:
         the 4-bit .sgb block form (uint8 (n, pitch // 2), io.py), half the
         host-to-device bytes, range-checked in that form on the device.
 
-        ``host_block`` (pinned, the private buffers' layout): every replay
+        ``host_block`` (pinned, the private buffers' layout): every step()
         also uploads this block into the OTHER parity's buffer -- the next
-        visit's input -- on a side branch of the graph, overlapped with the
-        sweep, so a host-fed step is one graph launch.  ``readback``: pairs
+        visit's input -- on a copy stream (a copy engine), overlapped with
+        the replay, ordered by events.  ``readback``: pairs
         (device tensor, pinned host tensor) copied back at the end of each
         replay (e.g. the CPTs)."""
         cfg = eng.cfg
@@ -477,7 +477,13 @@ class StepGraphs:
                 raise ValueError(f"host_block must be a pinned contiguous {bufs[0].dtype} {tuple(bufs[0].shape)}")
             for b in bufs:
                 b.copy_(host_block)
-            self._side = torch.cuda.Stream()
+            # uploads run on a copy stream outside the graphs (a copy engine,
+            # never SM time), ordered by events against the replays
+            self._up_stream = torch.cuda.Stream()
+            self._uploaded = [torch.cuda.Event(), torch.cuda.Event()]
+            self._up_pending = [False, False]
+            self._read_done = [torch.cuda.Event(), torch.cuda.Event()]
+            self._read_pending = [False, False]
         for dev_t, host_t in self.readback:
             if not host_t.is_pinned() or host_t.numel() * host_t.element_size() < dev_t.numel() * dev_t.element_size():
                 raise ValueError("readback targets must be pinned host tensors large enough")
@@ -514,14 +520,6 @@ class StepGraphs:
         cur = self.cur.data_ptr()
         new, prev = self.cbuf[p], self.cbuf[1 - p]
         obs = self.obs_bufs[p]
-        main = torch.cuda.current_stream()
-        if self.host_block is not None:  # fork: upload the next visit's block beside the sweep
-            fork = torch.cuda.Event()
-            fork.record(main)
-            self._side.wait_event(fork)
-            nxt = self.obs_bufs[1 - p]
-            _lib.call("sg_copy_async", nxt.data_ptr(), self.host_block.data_ptr(),
-                      nxt.numel() * nxt.element_size(), self._side.cuda_stream)
         # tables and keys of this visit are ready: the previous replay's finish built/advanced them
         if not eng.use_small:  # the packed sweep checks the block in its own launch
             _lib.call("sg_check_range", eng.pack.ref, obs.data_ptr(), self.ld, size, eng.err.ptr, s)
@@ -550,10 +548,6 @@ class StepGraphs:
                 _lib.call("sg_copy_small", host_t.data_ptr(), dev_t.data_ptr(), nbytes, s)
             else:
                 _lib.call("sg_copy_async", host_t.data_ptr(), dev_t.data_ptr(), nbytes, s)
-        if self.host_block is not None:  # join the upload branch (the read-back above overlaps its tail)
-            join = torch.cuda.Event()
-            join.record(self._side)
-            main.wait_event(join)
 
     def step(self, mb=None) -> None:
         """Replay the next planned visit; ``mb`` (optional) refills the observation buffer first."""
@@ -563,6 +557,26 @@ class StepGraphs:
         main = torch.cuda.current_stream()
         if mb is not None and self.host_block is not None:
             raise ValueError("this graph uploads its own host block; call step() without a minibatch")
+        if self.host_block is not None:
+            # upload the NEXT visit's block into the other buffer while this replay runs
+            q = 1 - p
+            up = self._up_stream
+            if self._read_pending[q]:
+                up.wait_event(self._read_done[q])  # the replay that last read buffer q has finished
+            nxt = self.obs_bufs[q]
+            _lib.call("sg_copy_async", nxt.data_ptr(), self.host_block.data_ptr(), nxt.numel() * nxt.element_size(),
+                      up.cuda_stream)
+            self._uploaded[q].record(up)
+            self._up_pending[q] = True
+            if self._up_pending[p]:
+                main.wait_event(self._uploaded[p])
+                self._up_pending[p] = False
+            self.graphs[p].replay()
+            self._read_done[p].record(main)
+            self._read_pending[p] = True
+            self.replayed += 1
+            _lib.launch_count += self.launches_per_step
+            return
         if mb is not None:
             vals = mb.values
             buf = self.obs_bufs[p]

@@ -14,8 +14,8 @@ if $L > $O/plain_launch_$R.log 2>&1; then
 fi
 F="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --eager"
 if $F > $O/plain_full_$R.log 2>&1; then
-  ncu --set full --clock-control none --import-source on -k regex:k_small_sweep --launch-skip 4 --launch-count 1 \
-    -o $O/sweep_$R -f $F > $O/ncu_full_$R.log 2>&1; echo "ncu sweep rc=$?"
-  ncu --set full --clock-control none --import-source on -k regex:k_step_finish --launch-skip 4 --launch-count 1 \
-    -o $O/finish_$R -f $F > $O/ncu_finish_$R.log 2>&1; echo "ncu finish rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:${SWEEP_K:-k_joint_sweep} --launch-skip 4 \
+    --launch-count 1 -o $O/sweep_$R -f $F > $O/ncu_full_$R.log 2>&1; echo "ncu sweep rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:${TAIL_K:-k_step_tail_joint} --launch-skip 4 \
+    --launch-count 1 -o $O/finish_$R -f $F > $O/ncu_finish_$R.log 2>&1; echo "ncu finish rc=$?"
 fi

@@ -54,8 +54,8 @@ if src.exists():
         f.write(f"{'count':>5} {'mean us':>9} {'total us':>10} {'share':>6}  kernel\n")
         for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
             f.write(f"{len(v):5d} {sum(v) / len(v):9.2f} {sum(v):10.1f} {sum(v) / total:6.1%}  {k}\n")
-        sw = per.get("void sg::k_small_sweep<5, 3>", [])
-        fin = per.get("sg::k_step_finish", [])
+        sw = per.get("void sg::k_joint_sweep<5, 3>", []) or per.get("void sg::k_small_sweep<5, 3>", [])
+        fin = per.get("sg::k_step_tail_joint", []) or per.get("sg::k_step_finish", [])
         if sw and fin:
             a, b = sum(sw) / len(sw), sum(fin) / len(fin)
             f.write(f"\nper step (graph replay = 1 sweep + 1 step tail): sweep {a:.1f} us + tail {b:.1f} us; "
@@ -77,8 +77,12 @@ if rep.exists():
     rd *= scale.get(m["dram__bytes_read.sum"][1], 1)
     wr *= scale.get(m["dram__bytes_write.sum"][1], 1)
     dur = num(m["gpu__time_duration.sum"][0]) * (1e-3 if m["gpu__time_duration.sum"][1] == "nsecond" else 1)
+    kname = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv", "--metrics", "gpu__time_duration.sum"],
+                           capture_output=True, text=True).stdout
+    kernel = ("k_joint_sweep<5, 3> (sg_joint_sweep)" if "k_joint_sweep" in kname else
+              "k_small_sweep<5, 3> (sg_small_sweep)")
     (P / f"ncu_sweep_{R}.json").write_text(json.dumps({
-        "kernel": "k_small_sweep<5, 3> (sg_small_sweep)", "cases": 1_000_000, "m": 10,
+        "kernel": kernel, "cases": 1_000_000, "m": 10,
         "command": "python bench.py --steps 5 --warmup 3 --no-cpu-baseline --eager",
         "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
         "duration_us_under_ncu": dur, "algorithmic_bytes_per_launch": 75_000_000,
