@@ -63,7 +63,7 @@ def _worker(rank, world, port, kind, rng, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,rng", [("koller", "fast"), ("dag200", "fast"), ("koller", "numpy"),
+@pytest.mark.parametrize("kind,rng", [("koller", "fast"), ("koller", "joint"), ("dag200", "fast"), ("koller", "numpy"),
                                       ("dag200", "numpy")])
 def test_two_ranks_equal_one_rank(kind, rng):
     """NUMPY mode needs the global rank prefixes (parallel.rank_prefix_exchange):
