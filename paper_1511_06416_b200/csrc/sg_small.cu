@@ -318,7 +318,7 @@ __device__ __forceinline__ void small_epilogue(const sg_small& sp, bool zs, cons
     const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + tid;
     const int gthreads = gridDim.x * gridDim.y * NT;
     unsigned bad = 0;
-    for (int i = gtid; i < N * chunks; i += gthreads) {
+    for (int i = gtid; i < sp.n * chunks; i += gthreads) {
       const int v = i / chunks, ch = i - v * chunks;
       const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
       const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
@@ -343,7 +343,7 @@ __device__ __forceinline__ void small_epilogue(const sg_small& sp, bool zs, cons
     const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + tid;
     const int gthreads = gridDim.x * gridDim.y * NT;
     unsigned bad = 0;
-    for (int i = gtid; i < N * chunks; i += gthreads) {
+    for (int i = gtid; i < sp.n * chunks; i += gthreads) {
       const int v = i / chunks, ch = i - v * chunks;
       const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
       const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
@@ -493,6 +493,7 @@ static size_t small_smem(const sg_small& sp, int cells) {
 
 static SmallOrd small_ord(const sg_small& sp) {
   SmallOrd o{};
+  for (int i = sp.n; i < SG_SMALL_MAXV; ++i) o.var[i] = 31u;  // padding: never a latent-pattern bit
   for (int i = 0; i < sp.n; ++i) {
     const int v = sp.order[i];
     o.var[i] = uint32_t(v);
@@ -536,7 +537,9 @@ static SmallOrd small_ord(const sg_small& sp) {
 //   dep_P[j]       latent field bits of compact column j (pdep(j, latent mask))
 //   rows_P[S][j]   thresholds, 2^bits rows of 2^B_P words per pattern
 
+#ifndef SG_JOINT_THREADS
 #define SG_JOINT_THREADS 1024
+#endif
 #define SG_JOINT_PURPOSE 2u
 #define SG_JOINT_MAXB 6
 
@@ -587,16 +590,17 @@ __device__ __forceinline__ uint32_t joint_search(uint32_t a, uint32_t u) {
 // 4 x QG lanes (no per-lane branches) so the compiler interleaves the
 // independent search chains; lanes past m and alias quads compute garbage
 // that is never stored or tallied.  row0 / dep0: shared-window addresses.
-template <int B, int QG>
+template <int B, int QG, int NL>
 __device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[QG], uint32_t row0, uint32_t dep0,
                                             uint32_t keep) {
   constexpr uint32_t kRowBytes = ((1u << B) + 1u) * 4u;  // rows 2^B + 1 words apart
 #pragma unroll
   for (int g = 0; g < QG; ++g) {
     const uint32_t u[4] = {r[g].a >> 1, r[g].b >> 1, r[g].c >> 1, r[g].d >> 1};
-    uint32_t xs[4];
+    uint32_t xs[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      if (g == QG - 1 && j >= NL) continue;  // compile time: lanes past m in the last quad
       const uint32_t S = byte_of(w[g], j);
       const uint32_t row = row0 + S * kRowBytes;
       const uint32_t hit = joint_search<B>(row, u[j]);
@@ -608,7 +612,9 @@ __device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[
   }
 }
 
-template <int QG, int NT>
+// NL: lanes of quad QG-1 (m - 4 * (Q - 1) when this CTA row holds the last
+// quad, else 4); lanes past it are neither drawn nor tallied.
+template <int QG, int NT, int NL>
 __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned char* blob, int np, uint32_t* lanes,
                                             const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id,
                                             uint32_t hist_a, int cases, int num_real,
@@ -653,12 +659,12 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
       const uint32_t dep0 = smem_u32(blob) + (meta >> 16);
       const uint32_t keep = (meta >> 8) & 0xFFu;
       switch (B) {
-        case 1: joint_quads<1, QG>(w, r, row0, dep0, keep); break;
-        case 2: joint_quads<2, QG>(w, r, row0, dep0, keep); break;
-        case 3: joint_quads<3, QG>(w, r, row0, dep0, keep); break;
-        case 4: joint_quads<4, QG>(w, r, row0, dep0, keep); break;
-        case 5: joint_quads<5, QG>(w, r, row0, dep0, keep); break;
-        default: joint_quads<6, QG>(w, r, row0, dep0, keep); break;
+        case 1: joint_quads<1, QG, NL>(w, r, row0, dep0, keep); break;
+        case 2: joint_quads<2, QG, NL>(w, r, row0, dep0, keep); break;
+        case 3: joint_quads<3, QG, NL>(w, r, row0, dep0, keep); break;
+        case 4: joint_quads<4, QG, NL>(w, r, row0, dep0, keep); break;
+        case 5: joint_quads<5, QG, NL>(w, r, row0, dep0, keep); break;
+        default: joint_quads<6, QG, NL>(w, r, row0, dep0, keep); break;
       }
     }
     const bool real_case = c < num_real;
@@ -669,7 +675,7 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
       if (counts) {
         const uint32_t wt = wg | (real_case ? trash[g] : 0x40404040u);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) joint_count(hist_a, byte_of(wt, j));
+        for (int j = 0; j < (g == QG - 1 ? NL : 4); ++j) joint_count(hist_a, byte_of(wt, j));
       }
     }
   }
@@ -680,8 +686,10 @@ __host__ __device__ inline size_t joint_smem(const sg_small& sp, const sg_joint&
          size_t((cells * 4 + 15) & ~15) + 16;
 }
 
-// One CTA per SM: the blob (Koller: 104 KB) + 1024 threads' byte counters.
-template <int N, int QG>
+// One CTA per SM (1024 threads: the register file) with the blob (Koller:
+// 109 KB) and per-warp tally bins in shared memory.  NL: lanes of the final
+// quad (m - 4 * (Q - 1)).
+template <int QG, int NL>
 __global__ void __launch_bounds__(SG_JOINT_THREADS, 1)
 k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint32_t* stab_g,
               const uint32_t* __restrict__ jblob_g, const uint8_t* __restrict__ pattern,
@@ -744,14 +752,18 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   __syncthreads();
   mbar_wait(bar, 0);
   bool zs = false;
-  if (armed)
-    zs = small_units<N, QG, true, NT, true>(o, qs, stab, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
-                                      counts != nullptr, nw0, nP0, nc0);
-  else
-    joint_units<QG, NT>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
-                        counts != nullptr, nw0, nP0, nc0);
+  if (armed) {  // padded SmallOrd entries (variable 31) are never latent: any n <= SG_SMALL_MAXV
+    zs = small_units<SG_SMALL_MAXV, QG, true, NT, true>(o, qs, stab, lanes, pattern, case_id, hist_a, cases,
+                                                        num_real, case_base, fk, counts != nullptr, nw0, nP0, nc0);
+  } else if (NL < 4 && last == QG - 1 && q0 + QG == Q) {  // this row holds the partial final quad
+    joint_units<QG, NT, NL>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
+                            counts != nullptr, nw0, nP0, nc0);
+  } else {
+    joint_units<QG, NT, 4>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
+                           counts != nullptr, nw0, nP0, nc0);
+  }
   // per-warp bins -> CPT cells (jcell) -> one global atomic per touched cell
-  small_epilogue<N, NT>(sp, zs, hist8, cellacc, jcell, cells, nullptr, obs, ld_obs, cases, err, obs_nib);
+  small_epilogue<SG_SMALL_MAXV, NT>(sp, zs, hist8, cellacc, jcell, cells, nullptr, obs, ld_obs, cases, err, obs_nib);
   if (!counts) return;
   __syncthreads();
   const uint32_t* wh = reinterpret_cast<const uint32_t*>(hist8);
@@ -1112,7 +1124,7 @@ extern "C" int sg_keys_advance(const uint64_t* table, int32_t* index, int32_t kp
 
 // ------------------------------------------------------------ joint C-ABI
 namespace sg {
-template <int N, int QG>
+template <int QG, int NL>
 static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& jp, int groups, size_t smem,
                          cudaStream_t st, const uint32_t* stab, const uint32_t* jblob, const uint8_t* pattern,
                          const int32_t* case_id, uint32_t* lanes, int lane_ld, int cases, int num_real, int m,
@@ -1121,7 +1133,7 @@ static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& 
                          int32_t* err) {
   static size_t configured = 0;
   if (smem > configured) {
-    cudaFuncSetAttribute(k_joint_sweep<N, QG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_joint_sweep<QG, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured = smem;
   }
   static int sms = 0;
@@ -1138,7 +1150,7 @@ static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& 
   const int64_t fill = (int64_t(cases) + SG_JOINT_THREADS - 1) / SG_JOINT_THREADS;
   const int64_t want = std::max<int64_t>(std::max(1, (sms - 1) / groups), need);
   const dim3 grid(unsigned(std::max<int64_t>(1, std::min<int64_t>(want, fill))), unsigned(groups));
-  launch_pdl(k_joint_sweep<N, QG>, grid, dim3(SG_JOINT_THREADS), smem, st, sp, o, jp, stab, jblob, pattern, case_id,
+  launch_pdl(k_joint_sweep<QG, NL>, grid, dim3(SG_JOINT_THREADS), smem, st, sp, o, jp, stab, jblob, pattern, case_id,
              lanes, lane_ld, cases, num_real, m, case_base, key, key_dev, jcell, cells,
              reinterpret_cast<unsigned long long*>(counts), zs_flag, obs, ld_obs, obs_nib, err);
 }
@@ -1209,33 +1221,32 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
   quad_groups(m, &qg, &groups);
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t* lw = reinterpret_cast<uint32_t*>(lanes);
-#define SG_JOINT_QG(NV, G)                                                                                     \
-  case G:                                                                                                      \
-    launch_joint<NV, G>(*sp, o, *jp, groups, smem, st, stab, jblob, pattern, case_id, lw, lane_ld, cases,      \
-                        num_real, m, case_base, key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs,      \
-                        obs_nibbles, err);                                                                     \
+  const int nl = m - 4 * ((m + 3) / 4 - 1);  // lanes of the final quad
+#define SG_JOINT_NL(G, L)                                                                                     \
+  case L:                                                                                                     \
+    launch_joint<G, L>(*sp, o, *jp, groups, smem, st, stab, jblob, pattern, case_id, lw, lane_ld, cases,      \
+                       num_real, m, case_base, key, key_dev, jcell, cells, counts, zs_flag, obs, ld_obs,      \
+                       obs_nibbles, err);                                                                     \
     break;
-#define SG_JOINT_CASE(NV) \
-  case NV:                \
-    switch (qg) {         \
-      SG_JOINT_QG(NV, 1)  \
-      SG_JOINT_QG(NV, 2)  \
-      SG_JOINT_QG(NV, 3)  \
-      SG_JOINT_QG(NV, 4)  \
-    }                     \
+#define SG_JOINT_QG(G)   \
+  case G:                \
+    switch (nl) {        \
+      SG_JOINT_NL(G, 1)  \
+      SG_JOINT_NL(G, 2)  \
+      SG_JOINT_NL(G, 3)  \
+      SG_JOINT_NL(G, 4)  \
+    }                    \
     break;
-  switch (sp->n) {
-    SG_JOINT_CASE(1)
-    SG_JOINT_CASE(2)
-    SG_JOINT_CASE(3)
-    SG_JOINT_CASE(4)
-    SG_JOINT_CASE(5)
-    SG_JOINT_CASE(6)
+  switch (qg) {
+    SG_JOINT_QG(1)
+    SG_JOINT_QG(2)
+    SG_JOINT_QG(3)
+    SG_JOINT_QG(4)
     default:
-      set_error("sg_joint_sweep: n=%d", sp->n);
+      set_error("sg_joint_sweep: quad group %d", qg);
       return SG_EINVAL;
   }
-#undef SG_JOINT_CASE
+#undef SG_JOINT_NL
 #undef SG_JOINT_QG
   return check_launch("sg_joint_sweep");
 }
