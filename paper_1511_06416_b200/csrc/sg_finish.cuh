@@ -71,6 +71,7 @@ struct FinishArgs {
   int kps;
   uint64_t* key_current;
   double* vprob;
+  uint32_t* release_sync;  // != NULL: release this word (st.release.gpu) once the new CPTs are in f.cpt
   int has_small;
   int early_inputs;  // the preceding sweep triggers only after its own wait: read total/prev/key before ours
   int packed_only;  // SG_FINISH_PACKED_ONLY: skip ptab/ftab, build stab from the CPTs
@@ -144,6 +145,14 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
   GammaPre pre{};
   int my_cell = -1;  // early path: one cell per thread
   uint64_t key = 0;
+  // early path: the next visit's keys (static table) and the cursor, stored right after the wait
+  const bool early_keys = early && f.key_table && f.kps <= nt;
+  uint64_t next_key = 0;
+  int key_idx = 0;
+  if (early_keys) {
+    key_idx = *f.key_index;
+    if (tid < f.kps) next_key = f.key_table[int64_t(key_idx) * f.kps + tid];
+  }
   if (early && cells <= nt) {
     key = f.key_dev ? *f.key_dev : f.key;
     if (tid < cells) {
@@ -171,6 +180,12 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
   pdl_trigger();
   if (!(early && cells <= nt)) key = f.key_dev ? *f.key_dev : f.key;
   if (tid == 0 && gnet.table_entries > 0) f.ftab[gnet.ftab_size] = 0u;
+  const bool early_clear = early && cells <= nt && f.clear_counts;  // prev counts already in registers
+  if (early_clear && tid < cells) f.clear_counts[tid] = 0ull;
+  if (early_keys) {  // every reader of this step's keys has them (the sweep finished, ours are in registers)
+    if (tid < f.kps) f.key_current[tid] = next_key;
+    if (tid == 0) *f.key_index = key_idx + 1;
+  }
   __syncthreads();
   SG_TRACE(1);
   const sg_net net = rebase_net(gnet, b32, b64);
@@ -219,7 +234,10 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     });
     for (int s2 = 0; s2 < card; ++s2) f.cpt[base + s2] = cpt_s[base + s2];
   }
-  __syncthreads();
+  if (f.release_sync) __threadfence();  // this thread's CPT rows are visible device-wide ...
+  __syncthreads();                      // ... for every thread before the release
+  if (f.release_sync && tid == 0)
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.release_sync), "r"(1u) : "memory");
   SG_TRACE(3);
   // 3. conditional tables from the new CPTs (packed-only: the packed words directly)
   if (f.packed_only) {
@@ -257,9 +275,9 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
   }
   SG_TRACE(5);
   // 5. clear the next visit's count buffer, advance the key cursor
-  if (f.clear_counts)
+  if (f.clear_counts && !early_clear)
     for (int i = tid; i < cells; i += nt) f.clear_counts[i] = 0ull;
-  if (f.key_table) {
+  if (f.key_table && !early_keys) {
     __syncthreads();  // every thread has read this step's keys
     const int idx = *f.key_index;
     for (int k = tid; k < f.kps; k += nt) f.key_current[k] = f.key_table[int64_t(idx) * f.kps + k];
@@ -293,6 +311,7 @@ inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
   a.key_current = f->key_current;
   a.vprob = sp ? f->vprob : nullptr;
   a.early_inputs = 0;
+  a.release_sync = nullptr;
   a.has_small = sp ? 1 : 0;
   a.packed_only = (sp && (f->flags & SG_FINISH_PACKED_ONLY)) ? 1 : 0;
   if (sp) a.sp = *sp;

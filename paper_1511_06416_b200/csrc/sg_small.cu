@@ -689,6 +689,25 @@ __host__ __device__ inline size_t joint_smem(const sg_small& sp, const sg_joint&
 // One CTA per SM (1024 threads: the register file) with the blob (Koller:
 // 109 KB) and per-warp tally bins in shared memory.  NL: lanes of the final
 // quad (m - 4 * (Q - 1)).
+#ifdef SG_FINISH_TRACE
+__device__ unsigned long long g_sweep_trace[2 * 160];
+extern "C" int sg_debug_sweep_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_sweep_trace, sizeof(g_sweep_trace)) == cudaSuccess ? 0 : 2;
+}
+#define SG_SWEEP_STAMP(k)                                                 \
+  do {                                                                    \
+    if (threadIdx.x == 0 && blockIdx.y == 0) {                            \
+      unsigned long long t_;                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
+      g_sweep_trace[blockIdx.x * 2 + (k)] = t_;                           \
+    }                                                                     \
+  } while (0)
+#else
+#define SG_SWEEP_STAMP(k) \
+  do {                    \
+  } while (0)
+#endif
+
 template <int QG, int NL>
 __global__ void __launch_bounds__(SG_JOINT_THREADS, 1)
 k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint32_t* stab_g,
@@ -698,6 +717,7 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
               int cells, unsigned long long* __restrict__ counts, const uint32_t* zs_flag,
               const int8_t* __restrict__ obs, int ld_obs, int obs_nib, int32_t* err) {
   constexpr int NT = SG_JOINT_THREADS;
+  SG_SWEEP_STAMP(0);
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* blob = smem;
   const uint32_t jbytes = uint32_t(jp.words) * 4u;
@@ -777,6 +797,7 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   __syncthreads();
   for (int cell = tid; cell < cells; cell += NT)
     if (cellacc[cell]) atomicAdd(counts + cell, (unsigned long long)cellacc[cell]);
+  SG_SWEEP_STAMP(1);
 }
 
 // Rows of pattern P = blockIdx.x, lane words S of slice blockIdx.y, from the
@@ -940,19 +961,24 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   auto stamp = [](int) {};
 #endif
   stamp(0);
-  if (blockIdx.x == 0) {
+  if (blockIdx.x == 0) {  // releases sync[0] as soon as the new CPTs are written (f.release_sync)
     step_finish_body(gnet, f, smem, FINISH_THREADS);
     stamp(1);
-    __threadfence();  // this thread's conditionals (f.vprob) are visible device-wide ...
-    __syncthreads();  // ... for every thread of the CTA before the release
-    if (threadIdx.x == 0) {
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sync), "r"(1u) : "memory");
-    }
     return;
   }
+  // Slices: stage the network pack while the sweep and CTA 0 run, then wait
+  // for the CPTs and build this slice's conditionals and rows.
+  const int tid = threadIdx.x;
+  int64_t* b64 = reinterpret_cast<int64_t*>(smem);
+  int32_t* b32 = reinterpret_cast<int32_t*>(b64 + gnet.blob64_words);
+  double* cpt_s = reinterpret_cast<double*>(
+      reinterpret_cast<unsigned char*>(b32) + ((size_t(gnet.blob32_words) * 4 + 15) & ~size_t(15)));
+  unsigned char* work = reinterpret_cast<unsigned char*>(cpt_s + ((gnet.cells + 1) & ~int64_t(1)));
   pdl_trigger();
+  for (int i = tid; i < int(gnet.blob64_words); i += blockDim.x) b64[i] = __ldg(gnet.blob64 + i);
+  for (int i = tid; i < int(gnet.blob32_words); i += blockDim.x) b32[i] = __ldg(gnet.blob32 + i);
   pdl_wait();  // the sweep has finished reading the blob rows this grid overwrites
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     uint32_t r = 0;
     for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(sync) : "memory");
@@ -961,8 +987,11 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   }
   __syncthreads();
   stamp(1);
+  for (int i = tid; i < int(gnet.cells); i += blockDim.x) cpt_s[i] = __ldcg(f.cpt + i);
+  __syncthreads();
+  const sg_net net = rebase_net(gnet, b32, b64);
   const int b = blockIdx.x - 1;
-  joint_slice(gnet, sp, jp, nullptr, f.vprob, jblob, b / SG_JOINT_TAB_SLICES, b % SG_JOINT_TAB_SLICES, smem, false);
+  joint_slice(net, sp, jp, cpt_s, nullptr, jblob, b / SG_JOINT_TAB_SLICES, b % SG_JOINT_TAB_SLICES, work, false);
   __syncthreads();
   stamp(2);
   if (threadIdx.x == 0 && atomicAdd(sync + 1, 1u) == gridDim.x - 2) {
@@ -1254,7 +1283,7 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
 extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const sg_finish* f, const sg_joint* jp,
                                   uint32_t* jblob, uint32_t* sync, void* stream) {
   using namespace sg;
-  SG_REQUIRE(net && sp && f && jp && jblob && sync && f->vprob && f->stab, "sg_step_tail_joint: null argument");
+  SG_REQUIRE(net && sp && f && jp && jblob && sync && f->stab, "sg_step_tail_joint: null argument");
   SG_REQUIRE(f->acc_mode == SG_ACC_MOVING || f->acc_mode == SG_ACC_EXPONENTIAL, "sg_step_tail_joint: bad mode");
   SG_REQUIRE(net->max_card <= SG_MAX_CARD && net->max_mb <= SG_MAX_MB, "sg_step_tail_joint: capacity exceeded");
   SG_REQUIRE(finish_fits(*net, sp), "sg_step_tail_joint: model too large for the single-CTA tail");
@@ -1263,8 +1292,12 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
   if (net->table_entries > 0) SG_REQUIRE(f->ptab && f->ftab, "sg_step_tail_joint: tables required");
   if (f->key_table) SG_REQUIRE(f->key_index && f->key_current && f->kps > 0, "sg_step_tail_joint: bad key cursor");
   FinishArgs a = make_finish_args(f, sp);
-  a.early_inputs = 1;  // k_joint_sweep triggers after its own wait
-  const size_t smem = std::max(finish_smem(*net), joint_tables_smem(*sp, jp->max_b));
+  a.early_inputs = 1;    // k_joint_sweep triggers after its own wait
+  a.vprob = nullptr;     // the slices derive their conditionals from the CPTs themselves
+  a.release_sync = sync;  // ... as soon as CTA 0 has written them
+  const size_t slice_smem = size_t(net->blob64_words) * 8 + ((size_t(net->blob32_words) * 4 + 15) & ~size_t(15)) +
+                            size_t((net->cells + 1) & ~int64_t(1)) * 8 + joint_tables_smem(*sp, jp->max_b);
+  const size_t smem = std::max(finish_smem(*net), slice_smem);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

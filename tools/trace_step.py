@@ -1,0 +1,71 @@
+"""Dev tool: globaltimer timeline of graph-replayed joint steps (debug build
+-DSG_FINISH_TRACE): sweep CTAs, the tail's CTA 0 phases, the row slices.
+
+  python paper_1511_06416_b200/_build.py -DSG_FINISH_TRACE --out=paper_1511_06416_b200/lib_variant_trace.so
+  SAMEGIBBS_LIB=$PWD/paper_1511_06416_b200/lib_variant_trace.so python tools/trace_step.py [cold]
+"""
+import ctypes
+import statistics
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+
+import paper_1511_06416_b200 as sg
+from paper_1511_06416_b200 import _lib
+from paper_1511_06416_b200.engine import Engine, StepGraphs
+from paper_1511_06416_b200.io import bundled_network_path, load_network_file
+
+lib = _lib.load()
+for f in ("sg_debug_tail_trace", "sg_debug_tail_finish_trace", "sg_debug_sweep_trace"):
+    getattr(lib, f).argtypes = [ctypes.c_void_p]
+net, truth = load_network_file(bundled_network_path("koller"))
+cases, m = 1_000_000, 10
+obs = sg.forward_sample_device(net, truth, cases, seed=1, hide_fraction=0.5, mask_seed=2)
+cold = "cold" in sys.argv
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush_rd = torch.ones(32 << 20, dtype=torch.int64, device="cuda")
+cfg = sg.SamplerConfig(same_m=10, minibatch_size=cases, seed=3, rng="joint")
+eng = Engine(net, cfg)
+mb = next(iter(sg.DeviceSource(obs, cases, cases)))
+for p in range(3):
+    eng.visit(mb, p, 10)
+g = StepGraphs(eng, mb, 10, range(3, 40))
+rows = []
+for k in range(12):
+    if cold:
+        flush.fill_(k & 0xFF)
+        flush_rd.sum()
+    torch.cuda.synchronize()
+    g.step()
+    torch.cuda.synchronize()
+    sw = (ctypes.c_ulonglong * 320)()
+    lib.sg_debug_sweep_trace(ctypes.cast(sw, ctypes.c_void_p))
+    tt = (ctypes.c_ulonglong * 640)()
+    lib.sg_debug_tail_trace(ctypes.cast(tt, ctypes.c_void_p))
+    ft = (ctypes.c_ulonglong * 8)()
+    lib.sg_debug_tail_finish_trace(ctypes.cast(ft, ctypes.c_void_p))
+    nsw = 147
+    t0 = min(sw[2 * b] for b in range(nsw))
+    r = {
+        "sweep first start": 0,
+        "sweep last start": max(sw[2 * b] for b in range(nsw)) - t0,
+        "sweep first end": min(sw[2 * b + 1] for b in range(nsw)) - t0,
+        "sweep last end": max(sw[2 * b + 1] for b in range(nsw)) - t0,
+        "tail CTA0 start": tt[0] - t0,
+        "tail: early inputs done": ft[0] - t0,
+        "tail: wait+key": ft[1] - t0,
+        "tail: acc+gamma": ft[2] - t0,
+        "tail: rows": ft[3] - t0,
+        "tail: tables": ft[4] - t0,
+        "tail: clear+keys": ft[6] - t0,
+        "tail CTA0 end": tt[1] - t0,
+        "slices last start": max(tt[4 * b] for b in range(1, 129)) - t0,
+        "slices flag seen (median)": statistics.median(tt[4 * b + 1] for b in range(1, 129)) - t0,
+        "slices last end": max(tt[4 * b + 2] for b in range(1, 129)) - t0,
+    }
+    rows.append(r)
+print("cold" if cold else "warm", "(us from the first sweep CTA's start, median of steps 2..11)")
+for key in rows[0]:
+    print(f"  {key:28s} {statistics.median(r[key] for r in rows[2:]) / 1e3:8.2f}")
