@@ -193,6 +193,13 @@ __device__ __forceinline__ void hist_inc(uint32_t a) {
                :: "r"(a));
 }
 
+// First slot of this thread in the joint sweep: warp-major across the CTAs
+// ((warp * grid + cta) * 32 + lane, stride grid * NT), so the ragged last
+// wave of 32-slot chunks is spread over every CTA instead of the first ones.
+__device__ __forceinline__ int joint_first_slot() {
+  return int(((threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32u + (threadIdx.x & 31u));
+}
+
 // Tally of the joint sweep: per-warp u32 histograms (65 bins: 64 lane
 // states + a trash bin) updated with shared-memory reductions.  Lanes that
 // must not count (past m, alias quads, padding cases) carry state 64 in
@@ -213,7 +220,7 @@ __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs
                                             const uint32_t (&nw0)[QG], uint32_t nP0, int nc0) {
   const int stride = gridDim.x * NT;
   bool zs = false;
-  int s = blockIdx.x * NT + threadIdx.x;
+  int s = RED ? joint_first_slot() : int(blockIdx.x * NT + threadIdx.x);
   uint32_t nw[QG], nP = nP0;
   int nc = nc0;
 #pragma unroll
@@ -622,7 +629,7 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
                                             const uint32_t (&nw0)[QG], uint32_t nP0, int nc0) {
   const uint32_t* info = reinterpret_cast<const uint32_t*>(blob);
   const int stride = gridDim.x * NT;
-  int s = blockIdx.x * NT + threadIdx.x;
+  int s = joint_first_slot();
   uint32_t nw[QG], nP = nP0;
   int nc = nc0;
 #pragma unroll
@@ -739,7 +746,7 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   uint32_t nP0 = 0;
   int nc0 = 0;
   {
-    const int s0 = blockIdx.x * NT + tid;
+    const int s0 = joint_first_slot();
     if (s0 < cases) {
       const uint32_t* r0p = lanes + int64_t(q0) * lane_ld;
 #pragma unroll
