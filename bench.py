@@ -320,7 +320,10 @@ def our_arm(args, wl: Workload) -> None:
         # private double-buffered observation blocks: e2e steps upload the next block
         # on a copy stream while the current visit runs
         # joint path: observation blocks travel in the 4-bit .sgb form (half the PCIe bytes)
-        graphs = StepGraphs(eng, mb, M, range(first, first + total_replays), nibbles=eng.joint)
+        obs_bits = 8
+        if eng.joint:  # the observation block travels packed: 2 bits/cell when every card <= 3, else 4
+            obs_bits = 2 if max(net.cardinalities) <= 3 else 4
+        graphs = StepGraphs(eng, mb, M, range(first, first + total_replays), obs_bits=obs_bits)
         for _ in range(graph_warm):
             graphs.step()
         first += graph_warm
@@ -369,11 +372,16 @@ def our_arm(args, wl: Workload) -> None:
 
     # ---- e2e through the public API: pinned host minibatch -> device, step, CPTs back to host
     if graphs is not None and graphs.nibbles:
-        from paper_1511_06416_b200.io import pack_nibbles
+        from paper_1511_06416_b200.io import pack_bits
 
-        pitch4 = graphs.obs_bufs[0].shape[1] * 2
-        host_obs = torch.empty((n_vars, pitch4 // 2), dtype=torch.uint8, pin_memory=True)
-        host_obs.copy_(pack_nibbles(obs[:, :CASES], pitch4).cpu())  # the minibatch as an .sgb 4-bit block
+        shape, _ = StepGraphs.obs_geometry(n_vars, CASES, graphs.obs_bits)
+        host_obs = torch.empty(shape, dtype=torch.uint8, pin_memory=True)
+        # the minibatch as a packed .sgb block
+        host_obs.copy_(pack_bits(obs[:, :CASES], shape[1] * 8 // graphs.obs_bits, graphs.obs_bits).cpu())
+    elif graphs is not None:  # int8 block in the graphs' buffer layout (missing-padded to the row pitch)
+        shape, _ = StepGraphs.obs_geometry(n_vars, CASES)
+        host_obs = torch.full(shape, -1, dtype=torch.int8).pin_memory()
+        host_obs[:, :CASES].copy_(obs[:, :CASES])
     else:
         host_obs = torch.empty((n_vars, CASES), dtype=torch.int8, pin_memory=True)
         host_obs.copy_(obs[:, :CASES])
@@ -385,7 +393,7 @@ def our_arm(args, wl: Workload) -> None:
         # side branch overlapped with the sweep, and reads the CPTs back at its end
         graphs.finish()
         e2e_graphs = StepGraphs(eng, mb, M, range(first + args.steps + 10, first + args.steps + 20 + e2e_steps),
-                                nibbles=graphs.nibbles, host_block=host_obs, readback=[(eng.cpt, cpt_host)])
+                                obs_bits=graphs.obs_bits, host_block=host_obs, readback=[(eng.cpt, cpt_host)])
 
     ready = [torch.cuda.Event(), torch.cuda.Event()]
 
@@ -459,7 +467,8 @@ def our_arm(args, wl: Workload) -> None:
                                      "see DESIGN.md 6" if eng.joint else
                                      "instruction issue (Philox + table draws), not HBM: see DESIGN.md 6")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_obs.numel()),
-                    "host_format": "4-bit .sgb block" if host_obs.dtype == torch.uint8 else "int8 block",
+                    "host_format": (f"{graphs.obs_bits}-bit .sgb block" if graphs is not None and graphs.nibbles
+                                    else "int8 block"),
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",

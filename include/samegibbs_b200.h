@@ -363,16 +363,17 @@ int sg_joint_smem(const sg_small* sp, const sg_joint* jp, int32_t cells, int64_t
 /* Sweep + tally on packed lanes with one uniform per lane (FAST Philox
    counters with purpose 2, v = 0).  Arguments as sg_small_sweep plus the
    joint plan and blob; when zs_flag is armed the per-variable path runs
-   instead (exact ZeroSupport semantics).  obs_nibbles != 0: obs is the 4-bit
-   block of an .sgb file (ld_obs bytes per row, two cases per byte, case 2j
-   in the low nibble, 15 = missing) and is range-checked in that form. */
+   instead (exact ZeroSupport semantics).  obs_bits 4 or 2: obs is a packed
+   .sgb block (ld_obs bytes per row, 8 / obs_bits cases per byte, case
+   k * (8 / obs_bits) + h in bits [h * obs_bits, (h + 1) * obs_bits) of byte
+   k, all-ones = missing) and is range-checked in that form; 0 or 8: int8. */
 int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint32_t* stab,
                    const uint32_t* jblob, const uint8_t* pattern, const int32_t* case_id,
                    uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real,
                    int32_t m, int64_t case_base, uint64_t key, const uint64_t* key_dev,
                    const int32_t* jcell, int32_t cells, uint64_t* counts,
                    const uint32_t* zs_flag, const int8_t* obs, int32_t ld_obs,
-                   int32_t obs_nibbles, int32_t* err, void* stream);
+                   int32_t obs_bits, int32_t* err, void* stream);
 
 /* Layout switches between packed lanes and sg_batch int8 lane states. */
 int sg_small_import(const sg_small* sp, const sg_batch* batch, const int32_t* case_id,
@@ -443,6 +444,11 @@ int sg_keys_advance(const uint64_t* table, int32_t* index, int32_t kps,
    are text, io.py:105-153); it halves the bytes an out-of-core source moves. */
 int sg_unpack_nibbles(const uint8_t* packed, int64_t ld_packed, int8_t* out, int64_t ld_out,
                       int32_t rows, int64_t cases, void* stream);
+
+/* 2-bit .sgb blocks (encoding "crumb", cards <= 3): four cases per byte, case
+   4j + h in bits [2h, 2h + 2), 3 = missing -> int8 (-1 = missing). */
+int sg_unpack_crumbs(const uint8_t* packed, int64_t ld_packed, int8_t* out, int64_t ld_out,
+                     int32_t rows, int64_t cases, void* stream);
 
 /* Largest state of each variable's observed cells (range check, sampler.py:429-430). */
 int sg_check_range(const sg_net* net, const int8_t* obs, int32_t ld_obs,

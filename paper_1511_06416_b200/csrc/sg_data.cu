@@ -108,3 +108,32 @@ extern "C" int sg_unpack_nibbles(const uint8_t* packed, int64_t ld_packed, int8_
   k_unpack_nibbles<<<blocks, 256, 0, (cudaStream_t)stream>>>(packed, ld_packed, out, ld_out, rows, cases);
   return check_launch("sg_unpack_nibbles");
 }
+
+// 2-bit blocks: one thread per output byte group of 4 cases (simple; the
+// file-streaming path decodes one minibatch per visit).
+__global__ void k_unpack_crumbs(const uint8_t* __restrict__ packed, int64_t ld_packed, int8_t* __restrict__ out,
+                                int64_t ld_out, int rows, int64_t cases) {
+  const int64_t per_row = (cases + 3) / 4;
+  const int64_t total = per_row * rows;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(i / per_row);
+    const int64_t k = i - int64_t(r) * per_row;
+    const uint32_t b = packed[int64_t(r) * ld_packed + k];
+    for (int h = 0; h < 4 && k * 4 + h < cases; ++h) {
+      const uint32_t x = (b >> (2 * h)) & 3u;
+      out[int64_t(r) * ld_out + k * 4 + h] = x == 3u ? int8_t(-1) : int8_t(x);
+    }
+  }
+}
+
+extern "C" int sg_unpack_crumbs(const uint8_t* packed, int64_t ld_packed, int8_t* out, int64_t ld_out, int32_t rows,
+                                int64_t cases, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(packed && out, "sg_unpack_crumbs: null argument");
+  SG_REQUIRE(rows >= 0 && cases >= 0 && ld_packed * 4 >= cases && ld_out >= cases, "sg_unpack_crumbs: bad shape");
+  const int64_t work = int64_t(rows) * ((cases + 3) / 4);
+  if (work == 0) return SG_OK;
+  const int blocks = int(std::min<int64_t>((work + 255) / 256, 148 * 16));
+  k_unpack_crumbs<<<blocks, 256, 0, (cudaStream_t)stream>>>(packed, ld_packed, out, ld_out, rows, cases);
+  return check_launch("sg_unpack_crumbs");
+}

@@ -320,8 +320,11 @@ __device__ __forceinline__ void small_epilogue(const sg_small& sp, bool zs, cons
                                                int32_t* err, int nib = 0) {
   const int tid = threadIdx.x;
   if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
-  if (obs && nib) {  // 4-bit observations (io.py .sgb): two cases per byte, 15 = missing
-    const int chunks = (cases + 31) >> 5;
+  if (obs && (nib == 4 || nib == 2)) {  // packed observations (io.py .sgb): 8/nib cases per byte, all-ones = missing
+    const int per_byte = 8 / nib;
+    const int chunk_cases = 16 * per_byte;
+    const uint32_t fmask = nib == 4 ? 0x0F0F0F0Fu : 0x03030303u;
+    const int chunks = (cases + chunk_cases - 1) / chunk_cases;
     const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + tid;
     const int gthreads = gridDim.x * gridDim.y * NT;
     unsigned bad = 0;
@@ -330,16 +333,15 @@ __device__ __forceinline__ void small_epilogue(const sg_small& sp, bool zs, cons
       const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
       const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
       const uint32_t wv[4] = {uint32_t(qv.x), uint32_t(qv.y), uint32_t(qv.z), uint32_t(qv.w)};
-      const int left = cases - ch * 32;
+      const int left = cases - ch * chunk_cases;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
+        for (int h = 0; h < per_byte; ++h) {  // field h of byte b = case (4k + b) * per_byte + h
+          const uint32_t x = (wv[k] >> (nib * h)) & fmask;
+          uint32_t gt = __vcmpgtu4(x, lim) & ~__vcmpeq4(x, fmask);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // low nibbles: even cases, high nibbles: odd cases
-          const uint32_t x = (wv[k] >> (4 * h)) & 0x0F0F0F0Fu;
-          uint32_t gt = __vcmpgtu4(x, lim) & ~__vcmpeq4(x, 0x0F0F0F0Fu);
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if (8 * k + 2 * b + h >= left) gt &= ~(0xFFu << (8 * b));
+          for (int b2 = 0; b2 < 4; ++b2)
+            if ((4 * k + b2) * per_byte + h >= left) gt &= ~(0xFFu << (8 * b2));
           bad |= gt;
         }
       }
@@ -1227,17 +1229,23 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
                               const uint8_t* pattern, const int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
                               int32_t cases, int32_t num_real, int32_t m, int64_t case_base, uint64_t key,
                               const uint64_t* key_dev, const int32_t* jcell, int32_t cells, uint64_t* counts,
-                              const uint32_t* zs_flag, const int8_t* obs, int32_t ld_obs, int32_t obs_nibbles,
+                              const uint32_t* zs_flag, const int8_t* obs, int32_t ld_obs, int32_t obs_bits,
                               int32_t* err, void* stream) {
   using namespace sg;
   SG_REQUIRE(sp && jp && stab && jblob && pattern && case_id && lanes && err, "sg_joint_sweep: null argument");
   SG_REQUIRE((reinterpret_cast<uintptr_t>(jblob) & 15) == 0, "sg_joint_sweep: blob must be 16-byte aligned");
+  SG_REQUIRE(obs_bits == 0 || obs_bits == 8 || obs_bits == 4 || obs_bits == 2,
+             "sg_joint_sweep: obs_bits must be 0/8 (int8), 4 or 2");
+  const int per_byte = (obs_bits == 4 || obs_bits == 2) ? 8 / obs_bits : 1;
   if (obs)
     SG_REQUIRE(ld_obs % 16 == 0 && (reinterpret_cast<uintptr_t>(obs) & 15) == 0 &&
-                   int64_t(ld_obs) * (obs_nibbles ? 2 : 1) >= cases,
+                   int64_t(ld_obs) * per_byte >= cases,
                "sg_joint_sweep: obs rows must be 16-byte aligned");
-  if (obs_nibbles)
-    for (int v = 0; v < sp->n; ++v) SG_REQUIRE(sp->card[v] <= 15, "sg_joint_sweep: 4-bit observations need cards <= 15");
+  if (per_byte > 1)
+    for (int v = 0; v < sp->n; ++v)
+      SG_REQUIRE(sp->card[v] < (1 << obs_bits), "sg_joint_sweep: %d-bit observations need cards < %d", obs_bits,
+                 1 << obs_bits);
+  const int obs_nibbles = per_byte > 1 ? obs_bits : 0;
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV, "sg_joint_sweep: bad plan");
   SG_REQUIRE(joint_plan_ok(*sp, *jp, cells), "sg_joint_sweep: joint plan does not fit (bits %d, words %d)", sp->bits,
              jp->words);

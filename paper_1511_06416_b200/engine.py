@@ -23,7 +23,7 @@ from . import _lib
 from .device import ErrorWord, device, netpack, stream_handle
 from .errors import ValidationError
 from .metrics import kl_avg
-from .io import pack_nibbles
+from .io import pack_bits
 from .model import CptSet, init_cpts
 from .network import Network, color_graph, moralize
 from .rng import derive_seed, stream_key_ints
@@ -306,19 +306,19 @@ class Engine:
         return f
 
     def packed_sweep(self, db, size: int, m: int, key: int, key_dev, counts_ptr, obs_ptr, ld: int, s,
-                     obs_nibbles: bool = False) -> None:
+                     obs_bits: int = 8) -> None:
         """Sweep + tally of a packed-lane minibatch: per-variable draws
         (sg_small_sweep) or, with rng="joint", one draw per lane (sg_joint_sweep;
-        ``obs_nibbles``: the range-checked block is 4-bit, ``ld`` bytes per row)."""
+        ``obs_bits`` 4 / 2: the range-checked block is packed, ``ld`` bytes per row)."""
         head = (db.pattern.data_ptr(), db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld, size, db.num_real, m,
                 self.case_base, key, key_dev, self.pack.small_jcell.data_ptr(), self.pack.cells, counts_ptr,
                 self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"], obs_ptr, ld)
         if self.joint:
             _lib.call("sg_joint_sweep", self.pack.small_ref, self.pack.joint_ref, self.stab.data_ptr(),
-                      self.jblob.data_ptr(), *head, 1 if obs_nibbles else 0, self.err.ptr, s)
+                      self.jblob.data_ptr(), *head, obs_bits if obs_bits < 8 else 0, self.err.ptr, s)
         else:
-            if obs_nibbles:
-                raise ValueError("4-bit observation blocks are range-checked by the joint sweep only")
+            if obs_bits < 8:
+                raise ValueError("packed observation blocks are range-checked by the joint sweep only")
             _lib.call("sg_small_sweep", self.pack.small_ref, self.stab.data_ptr(), *head, self.err.ptr, s)
 
     def step_tail(self, f, s) -> None:
@@ -406,14 +406,15 @@ class StepGraphs:
     """
 
     def __init__(self, eng: Engine, mb, m: int, pass_indices, obs_buffer: torch.Tensor | None = None,
-                 nibbles: bool = False, host_block: torch.Tensor | None = None, readback=()):
+                 nibbles: bool = False, host_block: torch.Tensor | None = None, readback=(), obs_bits: int = 8):
         """``obs_buffer``: device int8 (n, pitch) tensor the graphs read the
         minibatch's observations from; the caller keeps it filled (e.g. a
         device-resident source).  Default: a private buffer that
-        :meth:`step` refills from the minibatch passed to it.  ``nibbles``
-        (joint sweep, private buffers): :meth:`step` takes the minibatch in
-        the 4-bit .sgb block form (uint8 (n, pitch // 2), io.py), half the
-        host-to-device bytes, range-checked in that form on the device.
+        :meth:`step` refills from the minibatch passed to it.  ``obs_bits``
+        4 or 2 (``nibbles=True`` = 4; joint sweep, private buffers): the
+        observation blocks travel in the packed .sgb form (io.pack_bits;
+        1/2 or 1/4 of the host-to-device bytes) and are range-checked in that
+        form on the device.
 
         ``host_block`` (pinned, the private buffers' layout): every step()
         also uploads this block into the OTHER parity's buffer -- the next
@@ -444,19 +445,22 @@ class StepGraphs:
         self.replayed = 0
         prev = eng.prev_counts[mb.index]
         self.cbuf = [torch.zeros_like(prev), prev.clone()]
-        self.nibbles = bool(nibbles)
+        self.obs_bits = 4 if nibbles else int(obs_bits)
+        if self.obs_bits not in (8, 4, 2):
+            raise ValueError("obs_bits must be 8, 4 or 2")
+        self.nibbles = self.obs_bits < 8  # packed blocks (4- or 2-bit)
         if self.nibbles and (obs_buffer is not None or not eng.joint):
-            raise ValueError("4-bit uploads need the joint sweep and private observation buffers")
+            raise ValueError("packed uploads need the joint sweep and private observation buffers")
         if obs_buffer is None:
             # two private buffers, one per graph parity: step(mb) uploads the next
             # visit's block on a copy stream while the current visit runs
             src, _ = eng._obs_for(mb)
             bufs = []
-            shape, dt = self.obs_geometry(eng.n, mb.size, self.nibbles)
+            shape, dt = self.obs_geometry(eng.n, mb.size, self.obs_bits)
             for _ in range(2):
                 b = torch.empty(shape, dtype=dt, device=d)
                 if self.nibbles:
-                    b.copy_(pack_nibbles(src[:, :mb.size], shape[1] * 2))
+                    b.copy_(pack_bits(src[:, :mb.size], shape[1] * 8 // self.obs_bits, self.obs_bits))
                 else:
                     b[:, :src.shape[1]].copy_(src[:, :b.shape[1]])
                 bufs.append(b)
@@ -505,12 +509,14 @@ class StepGraphs:
         torch.cuda.synchronize()
 
     @staticmethod
-    def obs_geometry(n: int, size: int, nibbles: bool = False):
-        """(shape, dtype) of the private observation buffers (and of a host_block)."""
+    def obs_geometry(n: int, size: int, obs_bits=8):
+        """(shape, dtype) of the private observation buffers (and of a host_block):
+        ``obs_bits`` 8 (int8), 4 or 2 (packed rows of a 64-case multiple; True = 4)."""
+        bits = 4 if obs_bits is True else (8 if obs_bits is False else int(obs_bits))
         pitch = _pitch(size)
-        if nibbles:
-            pitch = max(32, (pitch + 31) // 32 * 32)
-            return (n, pitch // 2), torch.uint8
+        if bits < 8:
+            pitch = max(64, (pitch + 63) // 64 * 64)
+            return (n, pitch * bits // 8), torch.uint8
         return (n, pitch), torch.int8
 
     def _record(self, p: int) -> None:
@@ -534,7 +540,7 @@ class StepGraphs:
             counts_ptr = new.data_ptr() if last else None
             if eng.use_small:
                 eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr, obs.data_ptr() if last else None, self.ld, s,
-                                 obs_nibbles=self.nibbles)
+                                 obs_bits=self.obs_bits)
             else:
                 _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
@@ -583,7 +589,7 @@ class StepGraphs:
             if not (isinstance(vals, torch.Tensor) and vals.is_cuda and vals.data_ptr() == buf.data_ptr()):
                 src = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(np.asarray(vals, dtype=np.int8))
                 if self.nibbles and (src.dtype != torch.uint8 or tuple(src.shape) != tuple(buf.shape)):
-                    raise ValueError(f"expected a 4-bit block uint8 {tuple(buf.shape)} (io.pack_nibbles)")
+                    raise ValueError(f"expected a packed block uint8 {tuple(buf.shape)} (io.pack_bits)")
                 if not self.private_obs:
                     buf[:, :mb.size].copy_(src, non_blocking=True)
                 else:

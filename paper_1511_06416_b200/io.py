@@ -88,36 +88,60 @@ def write_network_file(path, net: Network, cpts: CptSet | None = None) -> None:
 #       (case c of block b = case b * block_cases + c; columns past the data
 #       are missing).  int8: one byte per cell, -1 = missing.  4-bit: two
 #       cells per byte (case 2j in the low nibble), 15 = missing, so cards
-#       <= 15; decoded on the device by sg_unpack_nibbles.
+#       <= 15; decoded on the device by sg_unpack_nibbles.  2-bit ("crumb",
+#       encoding 2): four cells per byte (case 4j + h in bits 2h..2h+1), 3 =
+#       missing, cards <= 3; decoded by sg_unpack_crumbs.
 
 _SGB_MAGIC = b"SGB1"
+_SGB_ENCODINGS = {"int8": 0, "nibble": 1, "crumb": 2}
 _SGB_HEADER = struct.Struct("<4sIIQIII")
 
 
-def pack_nibbles(block, pitch: int):
-    """(n, cases) observation block (int, -1 = missing, states <= 14) -> the
-    4-bit .sgb form: uint8 (n, pitch // 2), case 2j in the low nibble, 15 =
-    missing (also for the padding columns up to ``pitch``, a multiple of 32).
-    Works on numpy arrays and on (host or device) torch tensors."""
-    if pitch % 32 or pitch < block.shape[1]:
-        raise ValueError("pitch must be a multiple of 32 covering the block")
+def pack_bits(block, pitch: int, bits: int):
+    """(n, cases) observation block (int, -1 = missing) -> the packed .sgb
+    form with ``bits`` = 4 or 2 bits per cell: uint8 (n, pitch * bits / 8),
+    case k * (8 / bits) + h in bits [h * bits, (h + 1) * bits) of byte k, the
+    all-ones value = missing (also for the padding columns up to ``pitch``, a
+    multiple of 64).  Works on numpy arrays and on (host or device) tensors."""
+    if bits not in (4, 2):
+        raise ValueError("bits must be 4 or 2")
+    per = 8 // bits
+    miss = (1 << bits) - 1
+    if pitch % 64 or pitch < block.shape[1]:
+        raise ValueError("pitch must be a multiple of 64 covering the block")
     if isinstance(block, torch.Tensor):
-        u = torch.full((block.shape[0], pitch), 15, dtype=torch.uint8, device=block.device)
+        u = torch.full((block.shape[0], pitch), miss, dtype=torch.uint8, device=block.device)
         b = block.to(torch.int16)
-        u[:, :block.shape[1]] = torch.where(b < 0, 15, b).to(torch.uint8)
-        return u[:, 0::2] | (u[:, 1::2] << 4)
+        u[:, :block.shape[1]] = torch.where(b < 0, miss, b).to(torch.uint8)
+        out = u[:, 0::per].clone()
+        for h in range(1, per):
+            out |= u[:, h::per] << (bits * h)
+        return out
     arr = np.asarray(block)
-    u = np.full((arr.shape[0], pitch), 15, dtype=np.uint8)
-    u[:, :arr.shape[1]] = np.where(arr < 0, 15, arr).astype(np.uint8)
-    return (u[:, 0::2] | (u[:, 1::2] << 4)).astype(np.uint8)
+    u = np.full((arr.shape[0], pitch), miss, dtype=np.uint8)
+    u[:, :arr.shape[1]] = np.where(arr < 0, miss, arr).astype(np.uint8)
+    out = u[:, 0::per].copy()
+    for h in range(1, per):
+        out |= (u[:, h::per] << (bits * h)).astype(np.uint8)
+    return out
+
+
+def pack_nibbles(block, pitch: int):
+    """The 4-bit .sgb form (:func:`pack_bits` with bits = 4)."""
+    return pack_bits(block, pitch, 4)
+
+
+def pack_crumbs(block, pitch: int):
+    """The 2-bit .sgb form (:func:`pack_bits` with bits = 2; cards <= 3)."""
+    return pack_bits(block, pitch, 2)
 
 
 def write_binary(path, data, block_cases: int, encoding: str = "int8") -> None:
     """Write a DataMatrix or a dense (num_vars, num_cases) int matrix (-1 = missing) as ``.sgb``."""
     from .datagen import DataMatrix
 
-    if encoding not in ("int8", "nibble"):
-        raise ValueError(f"encoding must be 'int8' or 'nibble', got {encoding!r}")
+    if encoding not in _SGB_ENCODINGS:
+        raise ValueError(f"encoding must be one of {tuple(_SGB_ENCODINGS)}, got {encoding!r}")
     if isinstance(data, DataMatrix):
         dense = data.to_dense()
     else:
@@ -125,20 +149,20 @@ def write_binary(path, data, block_cases: int, encoding: str = "int8") -> None:
     n, cases = dense.shape
     if cases == 0:
         raise ValueError("no cases to write")
-    limit = 15 if encoding == "nibble" else 128
+    limit = {"int8": 128, "nibble": 15, "crumb": 3}[encoding]
     if dense.max(initial=-1) >= limit or dense.min(initial=0) < -1:
         raise ValueError(f"states must lie in [-1, {limit - 1}] for the {encoding} encoding")
-    pitch = max(32, (block_cases + 31) // 32 * 32)
+    pitch = max(64, (block_cases + 63) // 64 * 64)
     nb = (cases + block_cases - 1) // block_cases
     with open(path, "wb") as f:
-        head = _SGB_HEADER.pack(_SGB_MAGIC, 1, n, cases, block_cases, pitch, 0 if encoding == "int8" else 1)
+        head = _SGB_HEADER.pack(_SGB_MAGIC, 1, n, cases, block_cases, pitch, _SGB_ENCODINGS[encoding])
         f.write(head + bytes(64 - len(head)))
         for b in range(nb):
             lo, hi = b * block_cases, min(cases, (b + 1) * block_cases)
             blk = np.full((n, pitch), -1, dtype=np.int8)
             blk[:, :hi - lo] = dense[:, lo:hi]
-            if encoding == "nibble":
-                blk = pack_nibbles(blk, pitch)
+            if encoding != "int8":
+                blk = pack_bits(blk, pitch, 4 if encoding == "nibble" else 2)
             f.write(blk.tobytes())
 
 
@@ -148,10 +172,10 @@ def read_binary_header(path) -> dict:
     if len(raw) < 64:
         raise IoError(f"{path}: truncated header")
     magic, version, n, cases, block, pitch, enc = _SGB_HEADER.unpack(raw[:_SGB_HEADER.size])
-    if magic != _SGB_MAGIC or version != 1 or enc not in (0, 1):
+    names = {v: k for k, v in _SGB_ENCODINGS.items()}
+    if magic != _SGB_MAGIC or version != 1 or enc not in names:
         raise ParseError(f"{path}: not an .sgb v1 file")
-    return {"num_vars": n, "num_cases": cases, "block_cases": block, "pitch": pitch,
-            "encoding": "int8" if enc == 0 else "nibble"}
+    return {"num_vars": n, "num_cases": cases, "block_cases": block, "pitch": pitch, "encoding": names[enc]}
 
 
 class BinaryFileSource(_BlockStream):
@@ -168,15 +192,15 @@ class BinaryFileSource(_BlockStream):
         h = read_binary_header(path)
         self.path = Path(path)
         self.header = h
-        self.nibbles = h["encoding"] == "nibble"
-        self._row_bytes = h["pitch"] // 2 if self.nibbles else h["pitch"]
+        self.bits = {"int8": 8, "nibble": 4, "crumb": 2}[h["encoding"]]
+        self._row_bytes = h["pitch"] * self.bits // 8
         self._block_bytes = h["num_vars"] * self._row_bytes
         self._nb = (h["num_cases"] + h["block_cases"] - 1) // h["block_cases"]
         size = self.path.stat().st_size
         if size < 64 + self._nb * self._block_bytes:
             raise IoError(f"{path}: truncated ({size} bytes)")
         self._setup(h["num_vars"], h["pitch"], h["num_cases"], h["block_cases"], cycle)
-        dt = torch.uint8 if self.nibbles else torch.int8
+        dt = torch.uint8 if self.bits < 8 else torch.int8
         self._pinned = [torch.empty((h["num_vars"], self._row_bytes), dtype=dt).pin_memory() for _ in range(2)]
         self._pinned_ev = [None, None]
         self._turn = 0

@@ -174,9 +174,9 @@ def test_host_source_padding_equals_matrix_source(c4):
         np.testing.assert_array_equal(x, y)
 
 
-@pytest.mark.parametrize("encoding", ["int8", "nibble"])
+@pytest.mark.parametrize("encoding", ["int8", "nibble", "crumb"])
 def test_binary_file_source_equals_matrix_source(tmp_path, koller, encoding):
-    """An .sgb file streamed from disk (4-bit rows decoded on the device)
+    """An .sgb file streamed from disk (4-/2-bit rows decoded on the device)
     drives exactly the run of the in-memory data, padding included."""
     from paper_1511_06416_b200 import io
 

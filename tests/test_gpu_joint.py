@@ -199,13 +199,14 @@ def test_joint_stream_samples_the_posterior(koller):
     assert tv <= 0.02, tv
 
 
-def test_joint_graph_with_4bit_uploads_equals_eager(koller):
+@pytest.mark.parametrize("bits", [4, 2])
+def test_joint_graph_with_4bit_uploads_equals_eager(koller, bits):
     """StepGraphs fed 4-bit host blocks (.sgb form, half the PCIe bytes) ==
     eager visits on the int8 block, bit for bit; a state >= card in the 4-bit
     block is flagged like the int8 range check (sampler.py:429-430)."""
     from paper_1511_06416_b200 import _lib
     from paper_1511_06416_b200.engine import Engine, StepGraphs
-    from paper_1511_06416_b200.io import pack_nibbles
+    from paper_1511_06416_b200.io import pack_bits
 
     net, truth = koller
     cases, m = 30_001, 10
@@ -216,10 +217,10 @@ def test_joint_graph_with_4bit_uploads_equals_eager(koller):
     for p in range(5):
         a.visit(mb, p, m)
     b.visit(mb, 0, m)
-    g = StepGraphs(b, mb, m, range(1, 6), nibbles=True)
-    pitch4 = g.obs_bufs[0].shape[1] * 2
-    host = torch.empty((net.num_vars, pitch4 // 2), dtype=torch.uint8, pin_memory=True)
-    host.copy_(torch.from_numpy(pack_nibbles(obs[:, :cases].cpu().numpy(), pitch4)))
+    g = StepGraphs(b, mb, m, range(1, 6), obs_bits=bits)
+    pitch4 = g.obs_bufs[0].shape[1] * 8 // bits
+    host = torch.empty(tuple(g.obs_bufs[0].shape), dtype=torch.uint8, pin_memory=True)
+    host.copy_(torch.from_numpy(pack_bits(obs[:, :cases].cpu().numpy(), pitch4, bits)))
     hmb = sg.Minibatch(index=0, values=host, weights=np.ones(cases), num_real=cases)
     for _ in range(4):
         g.step(hmb)
@@ -229,20 +230,20 @@ def test_joint_graph_with_4bit_uploads_equals_eager(koller):
     np.testing.assert_array_equal(a.lane_states(0)[:, :, :cases].cpu().numpy(),
                                   b.lane_states(0)[:, :, :cases].cpu().numpy())
     bad = obs[:, :cases].cpu().numpy().copy()
-    bad[3, cases - 1] = 7  # grade has 3 states
-    host.copy_(torch.from_numpy(pack_nibbles(bad, pitch4)))
+    bad[0, cases - 1] = 2  # variable 0 has 2 states (2 is representable in 2 and 4 bits)
+    host.copy_(torch.from_numpy(pack_bits(bad, pitch4, bits)))
     g.step(hmb)
     torch.cuda.synchronize()
     assert b.err.read() & _lib.SG_ERR_STATE_RANGE
 
 
-@pytest.mark.parametrize("rng,nibbles", [("joint", True), ("joint", False), ("fast", False)])
-def test_host_fed_step_graphs_equal_eager(koller, rng, nibbles):
+@pytest.mark.parametrize("rng,bits", [("joint", 4), ("joint", 2), ("joint", 8), ("fast", 8)])
+def test_host_fed_step_graphs_equal_eager(koller, rng, bits):
     """StepGraphs(host_block=...): each replay uploads the next visit's pinned
     block beside the sweep and reads the CPTs back -- same results as eager
     visits, and the read-back CPTs are the engine's."""
     from paper_1511_06416_b200.engine import Engine, StepGraphs
-    from paper_1511_06416_b200.io import pack_nibbles
+    from paper_1511_06416_b200.io import pack_bits
 
     net, truth = koller
     cases, m = 20_000, 10
@@ -253,15 +254,15 @@ def test_host_fed_step_graphs_equal_eager(koller, rng, nibbles):
     for p in range(5):
         a.visit(mb, p, m)
     b.visit(mb, 0, m)
-    shape, dt = StepGraphs.obs_geometry(net.num_vars, cases, nibbles)
+    shape, dt = StepGraphs.obs_geometry(net.num_vars, cases, bits)
     host = torch.empty(shape, dtype=dt, pin_memory=True)
-    if nibbles:
-        host.copy_(torch.from_numpy(pack_nibbles(obs[:, :cases].cpu().numpy(), shape[1] * 2)))
+    if bits < 8:
+        host.copy_(torch.from_numpy(pack_bits(obs[:, :cases].cpu().numpy(), shape[1] * 8 // bits, bits)))
     else:
         host.fill_(-1)
         host[:, :cases].copy_(obs[:, :cases])
     cpt_host = torch.empty(b.pack.cells, dtype=torch.float64, pin_memory=True)
-    g = StepGraphs(b, mb, m, range(1, 5), nibbles=nibbles, host_block=host, readback=[(b.cpt, cpt_host)])
+    g = StepGraphs(b, mb, m, range(1, 5), obs_bits=bits, host_block=host, readback=[(b.cpt, cpt_host)])
     for _ in range(4):
         g.step()
     g.finish()

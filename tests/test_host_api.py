@@ -117,3 +117,21 @@ def test_pack_nibbles_matches_sgb_blocks(tmp_path):
     raw = np.fromfile(tmp_path / "a.sgb", dtype=np.uint8)[64:].reshape(4, h["pitch"] // 2)
     np.testing.assert_array_equal(io.pack_nibbles(dense, h["pitch"]), raw)
     np.testing.assert_array_equal(io.pack_nibbles(torch.from_numpy(dense), h["pitch"]).numpy(), raw)
+
+
+def test_pack_crumbs_matches_sgb_blocks(tmp_path):
+    """io.pack_crumbs (2-bit) is the crumb .sgb block layout; the header round-trips."""
+    import numpy as np
+
+    from paper_1511_06416_b200 import io
+
+    rng = np.random.default_rng(4)
+    dense = rng.integers(-1, 3, size=(3, 70)).astype(np.int32)
+    io.write_binary(tmp_path / "c.sgb", dense, block_cases=70, encoding="crumb")
+    h = io.read_binary_header(tmp_path / "c.sgb")
+    assert h["encoding"] == "crumb" and h["pitch"] == 128
+    raw = np.fromfile(tmp_path / "c.sgb", dtype=np.uint8)[64:].reshape(3, h["pitch"] // 4)
+    np.testing.assert_array_equal(io.pack_crumbs(dense, h["pitch"]), raw)
+    x = raw[:, :18].astype(np.int64)  # decode by hand
+    dec = np.stack([(x >> (2 * k)) & 3 for k in range(4)], axis=-1).reshape(3, -1)[:, :70]
+    np.testing.assert_array_equal(np.where(dec == 3, -1, dec), dense)

@@ -33,13 +33,16 @@ for p in range(3):
     eng.visit(mb, p, 10)
 g = StepGraphs(eng, mb, 10, range(3, 40))
 rows = []
+prev_end = None
 for k in range(12):
     if cold:
         flush.fill_(k & 0xFF)
         flush_rd.sum()
-    torch.cuda.synchronize()
+    if cold:
+        torch.cuda.synchronize()
     g.step()
-    torch.cuda.synchronize()
+    if cold or k % 2 == 1:
+        torch.cuda.synchronize()
     sw = (ctypes.c_ulonglong * 320)()
     lib.sg_debug_sweep_trace(ctypes.cast(sw, ctypes.c_void_p))
     tt = (ctypes.c_ulonglong * 640)()
@@ -65,6 +68,8 @@ for k in range(12):
         "slices flag seen (median)": statistics.median(tt[4 * b + 1] for b in range(1, 129)) - t0,
         "slices last end": max(tt[4 * b + 2] for b in range(1, 129)) - t0,
     }
+    r["gap: prev tail end -> sweep start"] = (t0 - prev_end) if (prev_end and not cold) else 0
+    prev_end = max(tt[4 * b + 2] for b in range(1, 129))
     rows.append(r)
 print("cold" if cold else "warm", "(us from the first sweep CTA's start, median of steps 2..11)")
 for key in rows[0]:
