@@ -358,6 +358,9 @@ def our_arm(args, wl: Workload) -> None:
     probe.sweep_events = []
     for k in range(20):
         flush_l2(k)
+        # keep the device busy (a spin kernel, no memory traffic) while the host enqueues the
+        # visit, so the events around the sweep time the kernel, not the host's launch latency
+        torch.cuda._sleep(200_000)
         probe.visit(mb, 1 + k, M)
     torch.cuda.synchronize()
     sweep_ms = [a.elapsed_time(b) / nsw for a, b, nsw in probe.sweep_events[2:]]

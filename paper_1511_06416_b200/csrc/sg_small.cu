@@ -590,8 +590,12 @@ __device__ __forceinline__ void joint_step(uint32_t& a, uint32_t u) {
 }
 template <int B>
 __device__ __forceinline__ uint32_t joint_search(uint32_t a, uint32_t u) {
+#ifdef SG_EXP_NOSEARCH  // timing experiment only: direct column, no search (wrong results)
+  return a + ((u >> (31 - B)) << 2);
+#else
   joint_step<1 << (B - 1)>(a, u);
   return a;
+#endif
 }
 
 // The QG quads of one slot: per lane one uniform (word j of the quad's
@@ -662,8 +666,14 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
       const FastCase fc = fast_case(fk, uint32_t(case_base + c));
       u32x4 r[QG];
 #pragma unroll
-      for (int g = 0; g < QG; ++g)
+      for (int g = 0; g < QG; ++g) {
+#ifdef SG_EXP_NOPHILOX  // timing experiment only: a cheap hash instead of Philox (wrong stream)
+        const uint32_t h0 = (fc.x2 ^ (uint32_t(g) * 0x9E3779B9u)) * 0x85EBCA6Bu;
+        r[g] = u32x4{h0, h0 * 0xC2B2AE35u, h0 ^ 0x27D4EB2Fu, h0 * 0x165667B1u};
+#else
         r[g] = fast_draw(fc, (SG_JOINT_PURPOSE << 28) | (qs.q0w + (uint32_t(min(g, qs.last)) << 16)));
+#endif
+      }
       const uint32_t row0 = smem_u32(blob) + info[P];
       const uint32_t dep0 = smem_u32(blob) + (meta >> 16);
       const uint32_t keep = (meta >> 8) & 0xFFu;
@@ -683,8 +693,10 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
       if (g <= qs.last) rows[g * qs.ld + s] = wg;
       if (counts) {
         const uint32_t wt = wg | (real_case ? trash[g] : 0x40404040u);
+#ifndef SG_EXP_NOTALLY  // timing experiment only: no tally
 #pragma unroll
         for (int j = 0; j < (g == QG - 1 ? NL : 4); ++j) joint_count(hist_a, byte_of(wt, j));
+#endif
       }
     }
   }
@@ -1172,6 +1184,9 @@ static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& 
   static size_t configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(k_joint_sweep<QG, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    // the step tail prefers the same carveout: no L1/shared reconfiguration between the two kernels
+    cudaFuncSetAttribute(k_joint_sweep<QG, NL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         int(cudaSharedmemCarveoutMaxShared));
     configured = smem;
   }
   static int sms = 0;
@@ -1314,8 +1329,12 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
                             size_t((net->cells + 1) & ~int64_t(1)) * 8 + joint_tables_smem(*sp, jp->max_b);
   const size_t smem = std::max(finish_smem(*net), slice_smem);
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (smem > configured) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    // same carveout as k_joint_sweep (no L1/shared reconfiguration between sweep and tail)
+    cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         int(cudaSharedmemCarveoutMaxShared));
     configured = smem;
   }
   const dim3 grid(1 + jp->patterns * SG_JOINT_TAB_SLICES);

@@ -54,7 +54,8 @@ if src.exists():
         f.write(f"{'count':>5} {'mean us':>9} {'total us':>10} {'share':>6}  kernel\n")
         for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
             f.write(f"{len(v):5d} {sum(v) / len(v):9.2f} {sum(v):10.1f} {sum(v) / total:6.1%}  {k}\n")
-        sw = per.get("void sg::k_joint_sweep<5, 3>", []) or per.get("void sg::k_small_sweep<5, 3>", [])
+        sw = next((v for k, v in per.items() if "k_joint_sweep" in k), None) or \
+            per.get("void sg::k_small_sweep<5, 3>", [])
         fin = per.get("sg::k_step_tail_joint", []) or per.get("sg::k_step_finish", [])
         if sw and fin:
             a, b = sum(sw) / len(sw), sum(fin) / len(fin)
@@ -79,7 +80,7 @@ if rep.exists():
     dur = num(m["gpu__time_duration.sum"][0]) * (1e-3 if m["gpu__time_duration.sum"][1] == "nsecond" else 1)
     kname = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv", "--metrics", "gpu__time_duration.sum"],
                            capture_output=True, text=True).stdout
-    kernel = ("k_joint_sweep<5, 3> (sg_joint_sweep)" if "k_joint_sweep" in kname else
+    kernel = ("k_joint_sweep<3, 2> (sg_joint_sweep)" if "k_joint_sweep" in kname else
               "k_small_sweep<5, 3> (sg_small_sweep)")
     (P / f"ncu_sweep_{R}.json").write_text(json.dumps({
         "kernel": kernel, "cases": 1_000_000, "m": 10,
