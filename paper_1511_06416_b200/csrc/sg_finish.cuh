@@ -234,7 +234,7 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     });
     for (int s2 = 0; s2 < card; ++s2) f.cpt[base + s2] = cpt_s[base + s2];
   }
-  if (f.release_sync) __threadfence();  // this thread's CPT rows are visible device-wide ...
+  if (f.release_sync && tid < int(net.rows)) __threadfence();  // this thread's CPT rows are visible device-wide ...
   __syncthreads();                      // ... for every thread before the release
   if (f.release_sync && tid == 0)
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.release_sync), "r"(1u) : "memory");

@@ -826,6 +826,19 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
 // p_v = w / norm with the reference's weight product (conditional_weights)
 // and sequential norm; products in colour order; sequential row sums;
 // thresholds min(ceil(cum * (2^31 / total)), 2^31).
+#ifdef SG_FINISH_TRACE
+__device__ unsigned long long g_tail_trace[4 * 160];
+__device__ __forceinline__ void tail_stamp(int k) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tail_trace[blockIdx.x * 4 + k] = t;
+  }
+}
+#else
+__device__ __forceinline__ void tail_stamp(int) {}
+#endif
+
 #define SG_JOINT_TAB_SLICES 4
 // Slice `slice` (lane words S in [slice * R/4, (slice+1) * R/4)) of pattern
 // P's rows.  vprob_g: the step tail's conditionals [n][R][4] (L2-coherent
@@ -894,6 +907,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
     }
   }
   __syncthreads();
+  tail_stamp(3);
   // One warp per row S: lanes hold columns (2l, 2l+1) when K = 64, column l
   // when K <= 32; products in colour order, a Kogge-Stone scan across lanes
   // for the cumulative sums (tests/fast_stream.py restates this order).
@@ -951,7 +965,6 @@ __global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg
 }
 
 #ifdef SG_FINISH_TRACE
-__device__ unsigned long long g_tail_trace[4 * 160];
 extern "C" int sg_debug_tail_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_tail_trace, sizeof(g_tail_trace)) == cudaSuccess ? 0 : 2;
 }

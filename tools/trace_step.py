@@ -66,11 +66,18 @@ for k in range(12):
         "tail CTA0 end": tt[1] - t0,
         "slices last start": max(tt[4 * b] for b in range(1, 129)) - t0,
         "slices flag seen (median)": statistics.median(tt[4 * b + 1] for b in range(1, 129)) - t0,
+        "slices conditionals done (median)": statistics.median(tt[4 * b + 3] for b in range(1, 129)) - t0,
+        "slices median end": statistics.median(tt[4 * b + 2] for b in range(1, 129)) - t0,
         "slices last end": max(tt[4 * b + 2] for b in range(1, 129)) - t0,
+        "slice rows phase max": max(tt[4 * b + 2] - tt[4 * b + 3] for b in range(1, 129)),
+        "slice rows phase median": statistics.median(tt[4 * b + 2] - tt[4 * b + 3] for b in range(1, 129)),
+        "slice cond phase max": max(tt[4 * b + 3] - tt[4 * b + 1] for b in range(1, 129)),
+        "slowest slice (P*4+slice)": max(range(1, 129), key=lambda b: tt[4 * b + 2]) - 1 + 0.0,
     }
     r["gap: prev tail end -> sweep start"] = (t0 - prev_end) if (prev_end and not cold) else 0
     prev_end = max(tt[4 * b + 2] for b in range(1, 129))
     rows.append(r)
 print("cold" if cold else "warm", "(us from the first sweep CTA's start, median of steps 2..11)")
 for key in rows[0]:
-    print(f"  {key:28s} {statistics.median(r[key] for r in rows[2:]) / 1e3:8.2f}")
+    v = statistics.median(r[key] for r in rows[2:])
+    print(f"  {key:34s} {v / 1e3 if 'slowest' not in key else v:8.2f}")
