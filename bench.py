@@ -268,6 +268,42 @@ def load_traffic(wl: Workload, kernel: str):
     return None, None
 
 
+def event_floor_ms(eng, flush_l2) -> float | None:
+    """Events-around-an-empty-kernel time (the sweep's launch shape, in a graph)."""
+    import ctypes
+
+    import torch
+
+    from paper_1511_06416_b200 import _lib
+
+    if not getattr(eng, "joint", False):
+        return None
+    ev = []
+    for _ in range(2):
+        h = ctypes.c_uint64()
+        _lib.call("sg_event_create", ctypes.byref(h))
+        ev.append(h.value)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        s = torch.cuda.current_stream().cuda_stream
+        _lib.call("sg_event_record", ev[0], s)
+        _lib.call("sg_noop", sms - 1, 1024, 120 * 1024, s)
+        _lib.call("sg_event_record", ev[1], s)
+    out = []
+    for k in range(15):
+        flush_l2(k)
+        g.replay()
+        torch.cuda.synchronize()
+        ms = ctypes.c_float()
+        _lib.call("sg_event_elapsed", ev[0], ev[1], ctypes.byref(ms))
+        if k >= 3:
+            out.append(ms.value)
+    for h in ev:
+        _lib.call("sg_event_destroy", h)
+    return statistics.mean(out)
+
+
 def our_arm(args, wl: Workload) -> None:
     import numpy as np
     import torch
@@ -351,20 +387,37 @@ def our_arm(args, wl: Workload) -> None:
     if err:
         raise RuntimeError(f"device error word {err}")
     ms = statistics.mean(step_ms)
-    # the sweep kernel alone: events around its launch in eager visits (same kernel, L2 flushed)
-    probe = eng if graphs is None else Engine(net, cfg, case_base=rank * CASES, small=eng.use_small)
-    if probe is not eng:
-        probe.visit(mb, 0, M)
-    probe.sweep_events = []
-    for k in range(20):
-        flush_l2(k)
-        # keep the device busy (a spin kernel, no memory traffic) while the host enqueues the
-        # visit, so the events around the sweep time the kernel, not the host's launch latency
-        torch.cuda._sleep(200_000)
-        probe.visit(mb, 1 + k, M)
-    torch.cuda.synchronize()
-    sweep_ms = [a.elapsed_time(b) / nsw for a, b, nsw in probe.sweep_events[2:]]
-    probe.sweep_events = None
+    # the sweep kernel alone, L2 flushed before every step: with graph replay, external timing
+    # events recorded inside the step graph around the sweep node (the kernel as it runs in
+    # the replayed step); eager mode: events around its launch in eager visits
+    t_first = first + args.steps + 40 + e2e_steps
+    if graphs is not None:
+        graphs.finish()
+        tg = StepGraphs(eng, mb, M, range(t_first, t_first + 25), obs_bits=graphs.obs_bits, timing=True)
+        sweep_ms = []
+        for k in range(25):
+            flush_l2(k)
+            tg.step()
+            torch.cuda.synchronize()
+            if k >= 3:
+                sweep_ms.append(tg.sweep_ms() / cfg.sweeps_per_minibatch)
+        tg.finish()
+        graphs.finish = lambda: None  # the engine's moving-sum state already holds the timing visits
+        # timing floor of this method: an EMPTY kernel of the sweep's launch shape, bracketed by
+        # the same external events inside a captured graph, L2 flushed before each replay
+        floor_ms = event_floor_ms(eng, flush_l2)
+    else:
+        eng.sweep_events = []
+        for k in range(20):
+            flush_l2(k)
+            # keep the device busy (a spin kernel, no memory traffic) while the host enqueues the
+            # visit, so the events around the sweep time the kernel, not the host's launch latency
+            torch.cuda._sleep(200_000)
+            eng.visit(mb, t_first + k, M)
+        torch.cuda.synchronize()
+        sweep_ms = [a.elapsed_time(b) / nsw for a, b, nsw in eng.sweep_events[2:]]
+        eng.sweep_events = None
+        floor_ms = None
     sw = statistics.mean(sweep_ms)
     if world > 1:
         t = torch.tensor([ms, sw], dtype=torch.float64, device="cuda")
@@ -466,6 +519,12 @@ def our_arm(args, wl: Workload) -> None:
                          "kernel_ms": sw, "algorithmic_bytes_per_launch": algo_bytes,
                          "bytes_per_node_sample": bpns, "peak_source": peak_src,
                          "traffic_source": traffic_src, "sweep_share_of_step": sw / ms,
+                         "timing": ("external events around the sweep node inside the replayed step graph, "
+                                    "L2 flushed before each step" if floor_ms is not None else
+                                    "events around the sweep launch in eager visits, L2 flushed"),
+                         "event_floor_ms": floor_ms,
+                         "frac_above_event_floor": (algo_bytes / ((sw - floor_ms) * 1e-3) / 1e9 / peak
+                                                    if floor_ms is not None and sw > floor_ms else None),
                          "limiter": ("shared-memory row searches (bank conflicts) + Philox issue, not HBM: "
                                      "see DESIGN.md 6" if eng.joint else
                                      "instruction issue (Philox + table draws), not HBM: see DESIGN.md 6")},

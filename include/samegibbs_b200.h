@@ -164,6 +164,18 @@ int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
    pinned host memory (mapped through unified addressing). */
 int sg_copy_small(void* dst, const void* src, int64_t bytes, void* stream);
 
+/* Timing events usable inside CUDA-graph capture (recorded as external
+   event nodes while the stream is capturing): create / record / elapsed
+   milliseconds / destroy.  Handles are cudaEvent_t values. */
+int sg_event_create(uint64_t* ev);
+int sg_event_record(uint64_t ev, void* stream);
+int sg_event_elapsed(uint64_t start, uint64_t end, float* ms);
+int sg_event_destroy(uint64_t ev);
+
+/* Empty kernel of the given launch shape (timing-floor calibration of the
+   bench's event measurements). */
+int sg_noop(int32_t ctas, int32_t threads, int32_t smem_bytes, void* stream);
+
 /* Text of the last failing call on this host thread ("" if none). */
 const char* sg_last_error(void);
 

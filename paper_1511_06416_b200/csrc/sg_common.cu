@@ -66,3 +66,72 @@ extern "C" int sg_copy_small(void* dst, const void* src, int64_t bytes, void* st
                                                         static_cast<const unsigned long long*>(src), words);
   return check_launch("sg_copy_small");
 }
+
+// Timing events that can be recorded inside a CUDA graph (external event
+// record nodes): StepGraphs(timing=True) brackets the sweep node with them so
+// the bench times the kernel as it runs in the replayed step.
+extern "C" int sg_event_create(uint64_t* ev) {
+  using namespace sg;
+  SG_REQUIRE(ev, "sg_event_create: null argument");
+  cudaEvent_t e;
+  const cudaError_t st = cudaEventCreate(&e);
+  if (st != cudaSuccess) {
+    set_error("sg_event_create: %s", cudaGetErrorString(st));
+    return SG_ECUDA;
+  }
+  *ev = reinterpret_cast<uint64_t>(e);
+  return SG_OK;
+}
+
+extern "C" int sg_event_record(uint64_t ev, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(ev, "sg_event_record: null event");
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing((cudaStream_t)stream, &cs);
+  const cudaError_t st =
+      cs == cudaStreamCaptureStatusActive
+          ? cudaEventRecordWithFlags(reinterpret_cast<cudaEvent_t>(ev), (cudaStream_t)stream, cudaEventRecordExternal)
+          : cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), (cudaStream_t)stream);
+  if (st != cudaSuccess) {
+    set_error("sg_event_record: %s", cudaGetErrorString(st));
+    return SG_ECUDA;
+  }
+  return SG_OK;
+}
+
+extern "C" int sg_event_elapsed(uint64_t start, uint64_t end, float* ms) {
+  using namespace sg;
+  SG_REQUIRE(start && end && ms, "sg_event_elapsed: null argument");
+  const cudaError_t st =
+      cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(start), reinterpret_cast<cudaEvent_t>(end));
+  if (st != cudaSuccess) {
+    set_error("sg_event_elapsed: %s", cudaGetErrorString(st));
+    return SG_ECUDA;
+  }
+  return SG_OK;
+}
+
+extern "C" int sg_event_destroy(uint64_t ev) {
+  if (ev) cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev));
+  return SG_OK;
+}
+
+// An empty kernel of a given launch shape: the bench times it exactly like
+// the sweep (events around it inside a step-shaped graph) to report the
+// timing floor of the event method next to the sweep time.
+__global__ void k_noop(int* never) {
+  extern __shared__ int sm_noop[];
+  if (never != nullptr && threadIdx.x == 0) never[0] = sm_noop[0];
+}
+
+extern "C" int sg_noop(int32_t ctas, int32_t threads, int32_t smem_bytes, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(ctas > 0 && threads > 0 && threads <= 1024 && smem_bytes >= 0, "sg_noop: bad shape");
+  static int configured = 0;
+  if (smem_bytes > 48 * 1024 && smem_bytes > configured) {
+    cudaFuncSetAttribute(k_noop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    configured = smem_bytes;
+  }
+  k_noop<<<ctas, threads, smem_bytes, (cudaStream_t)stream>>>(nullptr);
+  return check_launch("sg_noop");
+}

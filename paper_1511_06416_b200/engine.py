@@ -14,6 +14,7 @@ device; the running total is fp64 and follows the reference's rounding.
 
 from __future__ import annotations
 
+import ctypes
 import time
 
 import numpy as np
@@ -406,7 +407,8 @@ class StepGraphs:
     """
 
     def __init__(self, eng: Engine, mb, m: int, pass_indices, obs_buffer: torch.Tensor | None = None,
-                 nibbles: bool = False, host_block: torch.Tensor | None = None, readback=(), obs_bits: int = 8):
+                 nibbles: bool = False, host_block: torch.Tensor | None = None, readback=(), obs_bits: int = 8,
+                 timing: bool = False):
         """``obs_buffer``: device int8 (n, pitch) tensor the graphs read the
         minibatch's observations from; the caller keeps it filled (e.g. a
         device-resident source).  Default: a private buffer that
@@ -421,7 +423,9 @@ class StepGraphs:
         visit's input -- on a copy stream (a copy engine), overlapped with
         the replay, ordered by events.  ``readback``: pairs
         (device tensor, pinned host tensor) copied back at the end of each
-        replay (e.g. the CPTs)."""
+        replay (e.g. the CPTs).  ``timing``: external timing events bracket the
+        sweep node(s) inside each graph; :meth:`sweep_ms` reads the last
+        replay's sweep duration (call after synchronising)."""
         cfg = eng.cfg
         if eng.rng_mode != _lib.SG_RNG_FAST or cfg.accumulator_mode != "moving_sum":
             raise ValueError("graph replay needs the fast RNG and the moving-sum accumulator")
@@ -495,6 +499,13 @@ class StepGraphs:
         self._buf_free: list = [None, None]  # event: the last replay reading buffer p has finished
         self.graphs = []
         self._finish_args = []
+        self._tev = None
+        if timing:
+            self._tev = []
+            for _ in range(4):
+                h = ctypes.c_uint64()
+                _lib.call("sg_event_create", ctypes.byref(h))
+                self._tev.append(h.value)
         if not eng.tables_fresh:
             raise ValueError("engine tables are stale")
         # keys of the first replayed visit; every replay's finish advances the cursor
@@ -507,6 +518,15 @@ class StepGraphs:
                 self._record(parity)
             self.graphs.append(g)
         torch.cuda.synchronize()
+
+    def sweep_ms(self) -> float:
+        """Sweep time (ms, all sweeps of the visit) of the last replay (timing=True)."""
+        if self._tev is None or not self.replayed:
+            raise ValueError("no timed replay")
+        p = (self.replayed - 1) % 2
+        ms = ctypes.c_float()
+        _lib.call("sg_event_elapsed", self._tev[2 * p], self._tev[2 * p + 1], ctypes.byref(ms))
+        return float(ms.value)
 
     @staticmethod
     def obs_geometry(n: int, size: int, obs_bits=8):
@@ -535,6 +555,8 @@ class StepGraphs:
         f = eng.finish_args(new, prev, 0, key_dev=cur + 8 * S, clear=prev,
                             cursor=(self.table, self.idx, self.kps, self.cur))
         self._finish_args.append(f)
+        if self._tev is not None:
+            _lib.call("sg_event_record", self._tev[2 * p], s)
         for sw in range(S):
             last = sw == S - 1
             counts_ptr = new.data_ptr() if last else None
@@ -545,6 +567,8 @@ class StepGraphs:
                 _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
                           eng.err.ptr, s)
+        if self._tev is not None:
+            _lib.call("sg_event_record", self._tev[2 * p + 1], s)
         if eng.comm is not None:
             eng.comm(new)
         eng.step_tail(f, s)
