@@ -347,7 +347,7 @@ def our_arm(args, wl: Workload) -> None:
     for w in range(args.warmup):
         eng.visit(mb, w, M)
     torch.cuda.synchronize()
-    e2e_steps = max(3, min(args.steps, 50))
+    e2e_steps = max(3, min(args.steps, 200))  # long enough that one host hiccup does not dominate
     graph_warm = 3
     first = args.warmup
     graphs = None
@@ -480,17 +480,19 @@ def our_arm(args, wl: Workload) -> None:
     dbg = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)] if os.environ.get("SG_E2E_DEBUG") else None
     with ClockSampler(local) as e2e_clk:
         e0.record()
+        h0 = time.perf_counter()
         for k in range(e2e_steps):
             e2e_step(k)
             if dbg:
                 dbg[k].record()
         e1.record()
+        host_enqueue_us = (time.perf_counter() - h0) * 1e6 / e2e_steps
         torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if dbg:
         print("e2e per-step us:", [round((dbg[k].elapsed_time(dbg[k + 1])) * 1e3, 1) for k in range(e2e_steps - 1)],
               file=sys.stderr)
-        print("e2e clocks:", e2e_clk.summary(), file=sys.stderr)
+        print("e2e clocks:", e2e_clk.summary(), "host enqueue us/step:", round(host_enqueue_us, 1), file=sys.stderr)
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -531,7 +533,8 @@ def our_arm(args, wl: Workload) -> None:
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_obs.numel()),
                     "host_format": (f"{graphs.obs_bits}-bit .sgb block" if graphs is not None and graphs.nibbles
                                     else "int8 block"),
-                    "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms},
+                    "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms,
+                    "host_enqueue_us_per_step": host_enqueue_us},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",
             "kernel_path": ("packed-lane sg_joint_sweep + sg_step_finish + sg_joint_tables" if eng.joint else
