@@ -1,6 +1,6 @@
-"""Dev tool: does the L1/shared carveout switch after the L2-flush kernels cost the sweep time?
-Times the joint sweep (eager events, L2 flushed) with and without a tiny max-shared kernel
-launched between the flush and the visit."""
+"""Dev tool: does the L1/shared carveout switch after the L2-flush kernels cost the step / sweep time?
+Replays timed step graphs (external events around the sweep node) after a torch L2 flush, with and
+without an empty max-shared kernel (sg_noop, the sweep's launch shape) between the flush and the step."""
 import statistics
 import sys
 from pathlib import Path
@@ -10,8 +10,7 @@ import torch
 
 import paper_1511_06416_b200 as sg
 from paper_1511_06416_b200 import _lib
-from paper_1511_06416_b200.device import stream_handle
-from paper_1511_06416_b200.engine import Engine
+from paper_1511_06416_b200.engine import Engine, StepGraphs
 from paper_1511_06416_b200.io import bundled_network_path, load_network_file
 
 net, truth = load_network_file(bundled_network_path("koller"))
@@ -21,15 +20,28 @@ cfg = sg.SamplerConfig(same_m=10, minibatch_size=cases, seed=3, rng="joint")
 eng = Engine(net, cfg)
 mb = next(iter(sg.DeviceSource(obs, cases, cases)))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-eng.visit(mb, 0, 10)
+flush_rd = torch.ones(32 << 20, dtype=torch.int64, device="cuda")
+for w in range(3):
+    eng.visit(mb, w, 10)
+torch.cuda.synchronize()
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+base = 10
 for prime in (False, True, False, True):
-    eng.sweep_events = []
-    for k in range(20):
+    tg = StepGraphs(eng, mb, 10, range(base, base + 30), obs_bits=2, timing=True)
+    base += 40
+    sw, st = [], []
+    for k in range(30):
         flush.fill_(k & 0xFF)
-        if prime:  # the step tail kernel (max-shared carveout) on a dummy sync pair: re-primes the SMs' carveout
-            _lib.call("sg_copy_small", eng.vprob.data_ptr(), eng.vprob.data_ptr(), 8, stream_handle())
-        torch.cuda._sleep(100_000)
-        eng.visit(mb, 1 + k + (100 if prime else 0), 10)
-    torch.cuda.synchronize()
-    t = [a.elapsed_time(b) * 1e3 for a, b, _ in eng.sweep_events[3:]]
-    print(f"prime={prime}: sweep {statistics.mean(t):.1f} us")
+        flush_rd.sum()
+        if prime:
+            _lib.call("sg_noop", sms, 1024, 120 * 1024, torch.cuda.current_stream().cuda_stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        tg.step()
+        b.record()
+        torch.cuda.synchronize()
+        if k >= 3:
+            sw.append(tg.sweep_ms() * 1e3)
+            st.append(a.elapsed_time(b) * 1e3)
+    tg.finish()
+    print(f"prime={prime}: sweep {statistics.mean(sw):.1f} us  step {statistics.mean(st):.1f} us")
