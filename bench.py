@@ -462,14 +462,28 @@ def our_arm(args, wl: Workload) -> None:
         ready[k % 2].record()  # the host may read this step's CPTs once it has completed
 
     # The PCIe link drops to a low-power state while the device-only steps run;
-    # bring it back to full speed (~25 ms of uploads) before the e2e region, as
-    # a streaming pipeline would keep it.
+    # bring it back to full speed before the e2e region, as a streaming
+    # pipeline would keep it: upload blocks until three consecutive rounds
+    # reach >= 85 % of the best H2D rate seen (at least 25 ms, at most 1 s).
     scratch = torch.empty_like(host_obs, device="cuda")
     t_warm = time.perf_counter()
-    while time.perf_counter() - t_warm < 0.025:
+    best, good, rates = 0.0, 0, []
+    ew0, ew1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    while True:
+        ew0.record()
         for _ in range(8):
             scratch.copy_(host_obs, non_blocking=True)
+        ew1.record()
         torch.cuda.synchronize()
+        rate = 8 * host_obs.numel() * host_obs.element_size() / (ew0.elapsed_time(ew1) * 1e-3) / 1e9
+        rates.append(rate)
+        best = max(best, rate)
+        good = good + 1 if rate >= 0.85 * best else 0
+        el = time.perf_counter() - t_warm
+        if (el >= 0.025 and good >= 3) or el >= 1.0:
+            break
+    h2d_warm = {"gbs_last": round(rates[-1], 1), "gbs_best": round(best, 1), "rounds": len(rates),
+                "ms": round((time.perf_counter() - t_warm) * 1e3, 1)}
     del scratch
     for w in range(2):
         e2e_step(w)
@@ -478,6 +492,8 @@ def our_arm(args, wl: Workload) -> None:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dbg = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)] if os.environ.get("SG_E2E_DEBUG") else None
+    if dbg and e2e_graphs is not None:
+        e2e_graphs.debug_events = []
     with ClockSampler(local) as e2e_clk:
         e0.record()
         h0 = time.perf_counter()
@@ -492,6 +508,11 @@ def our_arm(args, wl: Workload) -> None:
     if dbg:
         print("e2e per-step us:", [round((dbg[k].elapsed_time(dbg[k + 1])) * 1e3, 1) for k in range(e2e_steps - 1)],
               file=sys.stderr)
+        if e2e_graphs is not None and e2e_graphs.debug_events:
+            for k, ev in enumerate(e2e_graphs.debug_events[10:16]):
+                print(f"step {k + 10}: upload {e0.elapsed_time(ev[0]) * 1e3:8.1f} -> {e0.elapsed_time(ev[1]) * 1e3:8.1f}"
+                      f"  replay {e0.elapsed_time(ev[2]) * 1e3:8.1f} -> {e0.elapsed_time(ev[3]) * 1e3:8.1f} us",
+                      file=sys.stderr)
         print("e2e clocks:", e2e_clk.summary(), "host enqueue us/step:", round(host_enqueue_us, 1), file=sys.stderr)
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
@@ -534,7 +555,7 @@ def our_arm(args, wl: Workload) -> None:
                     "host_format": (f"{graphs.obs_bits}-bit .sgb block" if graphs is not None and graphs.nibbles
                                     else "int8 block"),
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms,
-                    "host_enqueue_us_per_step": host_enqueue_us},
+                    "host_enqueue_us_per_step": host_enqueue_us, "h2d_warmup": h2d_warm},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",
             "kernel_path": ("packed-lane sg_joint_sweep + sg_step_finish + sg_joint_tables" if eng.joint else

@@ -500,6 +500,7 @@ class StepGraphs:
         self.graphs = []
         self._finish_args = []
         self._tev = None
+        self.debug_events = None  # a list: per host-fed step, events (upload start, end, replay start, end)
         if timing:
             self._tev = []
             for _ in range(4):
@@ -594,14 +595,25 @@ class StepGraphs:
             if self._read_pending[q]:
                 up.wait_event(self._read_done[q])  # the replay that last read buffer q has finished
             nxt = self.obs_bufs[q]
+            dbg = self.debug_events
+            if dbg is not None:
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                ev[0].record(up)
             _lib.call("sg_copy_async", nxt.data_ptr(), self.host_block.data_ptr(), nxt.numel() * nxt.element_size(),
                       up.cuda_stream)
+            if dbg is not None:
+                ev[1].record(up)
             self._uploaded[q].record(up)
             self._up_pending[q] = True
             if self._up_pending[p]:
                 main.wait_event(self._uploaded[p])
                 self._up_pending[p] = False
+            if dbg is not None:
+                ev[2].record(main)
             self.graphs[p].replay()
+            if dbg is not None:
+                ev[3].record(main)
+                dbg.append(ev)
             self._read_done[p].record(main)
             self._read_pending[p] = True
             self.replayed += 1

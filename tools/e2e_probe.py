@@ -29,23 +29,21 @@ def timed(g, steps=50):
     return e0.elapsed_time(e1) / steps * 1e3
 
 
-for nib in (True, False):
+from paper_1511_06416_b200.io import pack_bits
+
+for rep in range(2):
     cfg = sg.SamplerConfig(same_m=m, minibatch_size=cases, num_passes=1, seed=300, rng="joint")
     eng = Engine(net, cfg)
     for w in range(3):
         eng.visit(mb, w, m)
-    shape, dt = StepGraphs.obs_geometry(5, cases, nib)
+    shape, dt = StepGraphs.obs_geometry(5, cases, 2)
     host = torch.empty(shape, dtype=dt, pin_memory=True)
-    if nib:
-        host.copy_(pack_nibbles(obs[:, :cases], shape[1] * 2).cpu())
-    else:
-        host.fill_(-1)
-        host[:, :cases].copy_(obs[:, :cases])
+    host.copy_(pack_bits(obs[:, :cases], shape[1] * 4, 2).cpu())
     cpt_host = torch.empty(eng.pack.cells, dtype=torch.float64, pin_memory=True)
     base = 3
     for label, kw in [("plain", {}), ("host_block", {"host_block": host}),
                       ("host_block+readback", {"host_block": host, "readback": [(eng.cpt, cpt_host)]})]:
-        g = StepGraphs(eng, mb, m, range(base, base + 40), nibbles=nib, **kw)
-        print(f"nibbles={nib} {label:22s} {timed(g):7.1f} us/step")
+        g = StepGraphs(eng, mb, m, range(base, base + 60), obs_bits=2, **kw)
+        print(f"rep {rep} {label:22s} {timed(g):7.1f} us/step", flush=True)
         g.finish()
-        base += 50
+        base += 70
