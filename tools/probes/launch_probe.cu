@@ -20,7 +20,7 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  struct Shape { int ctas, threads, smem_kb; } shapes[] = {{147, 1024, 0}, {147, 1024, 123}, {148, 256, 18},
+  struct Shape { int ctas, threads, smem_kb; } shapes[] = {{1, 32, 0}, {148, 32, 0}, {147, 1024, 0}, {147, 1024, 123}, {148, 256, 18},
                                                              {147, 1024, 123}, {592, 256, 18}, {129, 512, 17}};
   for (int flush = 0; flush < 2; ++flush)
     for (auto sh : shapes) {
