@@ -436,9 +436,11 @@ typedef struct sg_finish {
 int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_finish* f, void* stream);
 
 /* The whole step tail of the joint path as ONE grid: sg_step_finish (CTA 0;
-   f->stab required, f->vprob ignored), which releases sync[0] as soon as the
-   new CPTs are written, and sg_joint_tables (CTAs 1.., which wait for that
-   release and derive the conditionals of their rows from the CPTs).  sync:
+   f->stab required), which releases sync[0] as soon as the new CPTs are
+   written, and sg_joint_tables (CTAs 1.., which wait for that release and
+   derive the conditionals of their rows from the CPTs).  f->vprob, when not
+   NULL, is scratch for an earlier hand-off: CTA 0 releases the cells' gamma
+   draws and every slice normalises the CPT rows itself.  sync:
    [dev] 2 uint32, zero before the first call; the kernel re-arms them. */
 int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const sg_finish* f,
                        const sg_joint* jp, uint32_t* jblob, uint32_t* sync, void* stream);

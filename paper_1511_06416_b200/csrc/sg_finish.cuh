@@ -72,6 +72,10 @@ struct FinishArgs {
   uint64_t* key_current;
   double* vprob;
   uint32_t* release_sync;  // != NULL: release this word (st.release.gpu) once the new CPTs are in f.cpt
+  // != NULL (with release_sync): release right after phase 1 instead, with the
+  // cells' gamma draws (MAP: totals) in release_lg[0..cells) and their in-log
+  // flags in the bytes after them; the readers normalise the rows themselves
+  double* release_lg;
   int has_small;
   int early_inputs;  // the preceding sweep triggers only after its own wait: read total/prev/key before ours
   int packed_only;  // SG_FINISH_PACKED_ONLY: skip ptab/ftab, build stab from the CPTs
@@ -220,7 +224,24 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
       }
     }
   }
-  __syncthreads();
+  if (f.release_sync && f.release_lg) {  // hand the draws over now: the slices build their rows from them
+    uint8_t* il_out = reinterpret_cast<uint8_t*>(f.release_lg + cells);
+    if (my_cell >= 0) {
+      f.release_lg[my_cell] = lg[my_cell];
+      il_out[my_cell] = f.map_estimate ? 0 : inlog[my_cell];
+      __threadfence();
+    } else if (!(early && cells <= nt)) {
+      for (int i = tid; i < cells; i += nt) {
+        f.release_lg[i] = lg[i];
+        il_out[i] = f.map_estimate ? 0 : inlog[i];
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.release_sync), "r"(1u) : "memory");
+  } else {
+    __syncthreads();
+  }
   SG_TRACE(2);
   // 2. CPT update, one row per thread
   for (int row = tid; row < int(net.rows); row += nt) {
@@ -234,9 +255,10 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     });
     for (int s2 = 0; s2 < card; ++s2) f.cpt[base + s2] = cpt_s[base + s2];
   }
-  if (f.release_sync && tid < int(net.rows)) __threadfence();  // this thread's CPT rows are visible device-wide ...
+  const bool release_cpts = f.release_sync && !f.release_lg;
+  if (release_cpts && tid < int(net.rows)) __threadfence();  // this thread's CPT rows are visible device-wide ...
   __syncthreads();                      // ... for every thread before the release
-  if (f.release_sync && tid == 0)
+  if (release_cpts && tid == 0)
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.release_sync), "r"(1u) : "memory");
   SG_TRACE(3);
   // 3. conditional tables from the new CPTs (packed-only: the packed words directly)
@@ -312,6 +334,7 @@ inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
   a.vprob = sp ? f->vprob : nullptr;
   a.early_inputs = 0;
   a.release_sync = nullptr;
+  a.release_lg = nullptr;
   a.has_small = sp ? 1 : 0;
   a.packed_only = (sp && (f->flags & SG_FINISH_PACKED_ONLY)) ? 1 : 0;
   if (sp) a.sp = *sp;

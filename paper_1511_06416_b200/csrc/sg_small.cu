@@ -1003,11 +1003,16 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   // Slices: stage the network pack while the sweep and CTA 0 run, then wait
   // for the CPTs and build this slice's conditionals and rows.
   const int tid = threadIdx.x;
+  const int cells = int(gnet.cells);
+  const int64_t cells2 = (gnet.cells + 1) & ~int64_t(1);
+  const bool from_lg = f.release_lg != nullptr;  // CTA 0 hands over the gamma draws, not the CPTs
   int64_t* b64 = reinterpret_cast<int64_t*>(smem);
   int32_t* b32 = reinterpret_cast<int32_t*>(b64 + gnet.blob64_words);
   double* cpt_s = reinterpret_cast<double*>(
       reinterpret_cast<unsigned char*>(b32) + ((size_t(gnet.blob32_words) * 4 + 15) & ~size_t(15)));
-  unsigned char* work = reinterpret_cast<unsigned char*>(cpt_s + ((gnet.cells + 1) & ~int64_t(1)));
+  double* lg = cpt_s + cells2;
+  uint8_t* inlog = reinterpret_cast<uint8_t*>(lg + (from_lg ? cells2 : 0));
+  unsigned char* work = inlog + (from_lg ? ((size_t(cells) + 15) & ~size_t(15)) : 0);
   pdl_trigger();
   for (int i = tid; i < int(gnet.blob64_words); i += blockDim.x) b64[i] = __ldg(gnet.blob64 + i);
   for (int i = tid; i < int(gnet.blob32_words); i += blockDim.x) b32[i] = __ldg(gnet.blob32 + i);
@@ -1021,9 +1026,28 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   }
   __syncthreads();
   stamp(1);
-  for (int i = tid; i < int(gnet.cells); i += blockDim.x) cpt_s[i] = __ldcg(f.cpt + i);
-  __syncthreads();
   const sg_net net = rebase_net(gnet, b32, b64);
+  if (from_lg) {  // the Dirichlet rows from CTA 0's draws (the same code and rounding as CTA 0's own rows)
+    const uint8_t* il_g = reinterpret_cast<const uint8_t*>(f.release_lg + cells);
+    for (int i = tid; i < cells; i += blockDim.x) {
+      lg[i] = __ldcg(f.release_lg + i);
+      inlog[i] = __ldcg(il_g + i);
+    }
+    __syncthreads();
+    for (int row = tid; row < int(net.rows); row += blockDim.x) {
+      const int v = net.row_var[row];
+      const int card = net.card[v];
+      const int64_t base = net.cpt_off[v] + (row - net.row_off[v]) * card;
+      with_card(card, [&](auto C) {
+        constexpr int K = decltype(C)::value;
+        if (f.map_estimate) mean_row<K>(lg + base, f.alpha[v], card, cpt_s + base);
+        else dirichlet_row<K>(lg + base, inlog + base, card, cpt_s + base);
+      });
+    }
+  } else {
+    for (int i = tid; i < cells; i += blockDim.x) cpt_s[i] = __ldcg(f.cpt + i);
+  }
+  __syncthreads();
   const int b = blockIdx.x - 1;
   joint_slice(net, sp, jp, cpt_s, nullptr, jblob, b / SG_JOINT_TAB_SLICES, b % SG_JOINT_TAB_SLICES, work, false);
   __syncthreads();
@@ -1338,8 +1362,15 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
   a.early_inputs = 1;    // k_joint_sweep triggers after its own wait
   a.vprob = nullptr;     // the slices derive their conditionals from the CPTs themselves
   a.release_sync = sync;  // ... as soon as CTA 0 has written them
+  // With f->vprob as scratch (n * 2^bits * 4 doubles), CTA 0 releases the cells' gamma draws right
+  // after drawing them and every slice normalises the rows itself: CTA 0's row phase and its fence
+  // leave the critical path.
+  const size_t cells2 = size_t((net->cells + 1) & ~int64_t(1));
+  const bool from_lg = f->vprob && size_t(sp->n) * (size_t(4) << sp->bits) * 8 >= size_t(net->cells) * 9;
+  a.release_lg = from_lg ? f->vprob : nullptr;
   const size_t slice_smem = size_t(net->blob64_words) * 8 + ((size_t(net->blob32_words) * 4 + 15) & ~size_t(15)) +
-                            size_t((net->cells + 1) & ~int64_t(1)) * 8 + joint_tables_smem(*sp, jp->max_b);
+                            cells2 * 8 + (from_lg ? cells2 * 8 + ((size_t(net->cells) + 15) & ~size_t(15)) : 0) +
+                            joint_tables_smem(*sp, jp->max_b);
   const size_t smem = std::max(finish_smem(*net), slice_smem);
   static size_t configured = 0;
   if (smem > configured) {
