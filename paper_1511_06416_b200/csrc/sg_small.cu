@@ -846,7 +846,8 @@ __device__ __forceinline__ void tail_stamp(int) {}
 // NULL to compute them here from cpt.
 __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& sp, const sg_joint& jp,
                                             const double* cpt, const double* vprob_g, uint32_t* jblob, int P,
-                                            int slice, unsigned char* smem, bool wait_pdl) {
+                                            int slice, unsigned char* smem, bool wait_pdl,
+                                            bool vprob_ready = false) {
   __shared__ uint32_t lv[SG_SMALL_MAXV][4];  // latent variables of P in colour order: off|width<<8|card<<16, mbmask, fm, v
   __shared__ int nlat;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -877,7 +878,9 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
     nlat = k;
   }
   if (wait_pdl) pdl_wait();  // this step's CPTs (and the tail's conditionals)
-  if (vprob_g) {
+  if (vprob_ready) {
+    // the caller has filled vprob (joint_cond_apply)
+  } else if (vprob_g) {
     for (int i = tid; i < sp.n * R * 4; i += nt) vprob[i] = __ldcg(vprob_g + i);
   } else {
     for (int i = tid; i < sp.n * R; i += nt) {
@@ -952,6 +955,84 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
   }
 }
 
+// The conditionals p_v(x | lane word S) a slice of pattern P needs, split in
+// two: joint_cond_plan (before the new CPTs exist) resolves every CPT index
+// of conditional_weights -- the parent row, then each child's factor in
+// ascending child order, as (first cell, cell step per state of v) -- and
+// joint_cond_apply (once they exist) only gathers, multiplies in that same
+// order and normalises (joint_conditional): the same products as the direct
+// path, without the dependent index chains on the critical path.
+#define SG_JOINT_MAXF (1 + SG_SMALL_MAXV)
+__device__ __forceinline__ void joint_cond_plan(const sg_net& net, const sg_small& sp, int P, int2* plan,
+                                                int8_t* nf) {
+  const int R = 1 << sp.bits;
+  for (int i = threadIdx.x; i < sp.n * R; i += blockDim.x) {
+    const int v = i / R;
+    const uint32_t S = uint32_t(i - v * R);
+    if (!((P >> v) & 1) || (S & ~sp.mbmask[v])) {  // never read by this pattern's rows
+      nf[i] = -1;
+      continue;
+    }
+    int st[SG_MAX_MB];
+    bool valid = true;
+    const int m0 = net.mb_start[v], m1 = net.mb_start[v + 1];
+    for (int k = m0; k < m1 && valid; ++k) {
+      const int u = net.mb_var[k];
+      st[k - m0] = small_field(S, sp, u);
+      valid = st[k - m0] < sp.card[u];
+    }
+    if (!valid) {
+      nf[i] = 0;
+      continue;
+    }
+    int2* pl = plan + size_t(i) * SG_JOINT_MAXF;
+    const int card = net.card[v];
+    int64_t cfg = 0;
+    for (int j = net.par_start[v], e = net.par_start[v + 1]; j < e; ++j)
+      cfg += int64_t(st[net.par_slot[j]]) * net.par_stride[j];
+    pl[0] = make_int2(int(net.cpt_off[v] + cfg * card), 1);
+    int f = 1;
+    for (int k = net.chl_start[v], ke = net.chl_start[v + 1]; k < ke; ++k, ++f) {
+      const int c = net.chl_var[k];
+      const int cc = net.card[c];
+      int64_t cfg0 = 0;
+      for (int q = net.chl_pstart[k], qe = net.chl_pstart[k + 1]; q < qe; ++q)
+        cfg0 += int64_t(st[net.chl_pslot[q]]) * net.chl_pstride[q];
+      pl[f] = make_int2(int(net.cpt_off[c] + st[net.chl_slot[k]] + cfg0 * cc), int(net.chl_vstride[k] * cc));
+    }
+    nf[i] = int8_t(f);
+  }
+}
+
+__device__ __forceinline__ void joint_cond_apply(const sg_net& net, const sg_small& sp, const int2* plan,
+                                                 const int8_t* nf, const double* cpt, double* vprob) {
+  const int R = 1 << sp.bits;
+  for (int i = threadIdx.x; i < sp.n * R; i += blockDim.x) {
+    const int n_f = nf[i];
+    if (n_f < 0) continue;
+    const int card = net.card[i / R];
+    double* out = vprob + size_t(i) * 4;
+    if (n_f == 0) {
+      for (int t = 0; t < card; ++t) out[t] = 0.0;
+      continue;
+    }
+    const int2* pl = plan + size_t(i) * SG_JOINT_MAXF;
+    with_card(card, [&](auto C) {
+      constexpr int KC = decltype(C)::value;
+      double w[KC ? KC : SG_MAX_CARD];
+      const int2 p0 = pl[0];
+#pragma unroll
+      for (int t = 0; t < (KC ? KC : card); ++t) w[t] = cpt[p0.x + t];
+      for (int f = 1; f < n_f; ++f) {
+        const int2 pf = pl[f];
+#pragma unroll
+        for (int t = 0; t < (KC ? KC : card); ++t) w[t] = __dmul_rn(w[t], cpt[pf.x + t * pf.y]);
+      }
+      joint_conditional<KC>(w, card, out);
+    });
+  }
+}
+
 // Rows of pattern P = blockIdx.x, lane words of slice blockIdx.y, from the
 // current CPTs (see the blob comment).  fp64 in a fixed order, no FMA:
 // p_v = w / norm with the reference's weight product (conditional_weights)
@@ -1013,9 +1094,19 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   double* lg = cpt_s + cells2;
   uint8_t* inlog = reinterpret_cast<uint8_t*>(lg + (from_lg ? cells2 : 0));
   unsigned char* work = inlog + (from_lg ? ((size_t(cells) + 15) & ~size_t(15)) : 0);
+  // after the slice's conditionals (work: n * 2^bits * 4 doubles): their gather plan
+  const int nr = sp.n << sp.bits;
+  int2* plan = reinterpret_cast<int2*>(work + size_t(nr) * 4 * sizeof(double));
+  int8_t* plan_nf = reinterpret_cast<int8_t*>(plan + size_t(nr) * SG_JOINT_MAXF);
+  const int b = blockIdx.x - 1;
+  const int P = b / SG_JOINT_TAB_SLICES;
   pdl_trigger();
   for (int i = tid; i < int(gnet.blob64_words); i += blockDim.x) b64[i] = __ldg(gnet.blob64 + i);
   for (int i = tid; i < int(gnet.blob32_words); i += blockDim.x) b32[i] = __ldg(gnet.blob32 + i);
+  __syncthreads();
+  const sg_net net = rebase_net(gnet, b32, b64);
+  // every CPT index of this pattern's conditionals, while the sweep / CTA 0 still run
+  if (jblob[jp.patterns + P] & 0xFFu) joint_cond_plan(net, sp, P, plan, plan_nf);
   pdl_wait();  // the sweep has finished reading the blob rows this grid overwrites
   if (tid == 0) {
     uint32_t r = 0;
@@ -1026,7 +1117,6 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   }
   __syncthreads();
   stamp(1);
-  const sg_net net = rebase_net(gnet, b32, b64);
   if (from_lg) {  // the Dirichlet rows from CTA 0's draws (the same code and rounding as CTA 0's own rows)
     const uint8_t* il_g = reinterpret_cast<const uint8_t*>(f.release_lg + cells);
     for (int i = tid; i < cells; i += blockDim.x) {
@@ -1048,8 +1138,10 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
     for (int i = tid; i < cells; i += blockDim.x) cpt_s[i] = __ldcg(f.cpt + i);
   }
   __syncthreads();
-  const int b = blockIdx.x - 1;
-  joint_slice(net, sp, jp, cpt_s, nullptr, jblob, b / SG_JOINT_TAB_SLICES, b % SG_JOINT_TAB_SLICES, work, false);
+  const bool live = (jblob[jp.patterns + P] & 0xFFu) != 0;
+  if (live) joint_cond_apply(net, sp, plan, plan_nf, cpt_s, reinterpret_cast<double*>(work));
+  __syncthreads();
+  joint_slice(net, sp, jp, cpt_s, nullptr, jblob, P, b % SG_JOINT_TAB_SLICES, work, false, true);
   __syncthreads();
   stamp(2);
   if (threadIdx.x == 0 && atomicAdd(sync + 1, 1u) == gridDim.x - 2) {
@@ -1370,7 +1462,8 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
   a.release_lg = from_lg ? f->vprob : nullptr;
   const size_t slice_smem = size_t(net->blob64_words) * 8 + ((size_t(net->blob32_words) * 4 + 15) & ~size_t(15)) +
                             cells2 * 8 + (from_lg ? cells2 * 8 + ((size_t(net->cells) + 15) & ~size_t(15)) : 0) +
-                            joint_tables_smem(*sp, jp->max_b);
+                            joint_tables_smem(*sp, jp->max_b) +
+                            (size_t(sp->n) << sp->bits) * (SG_JOINT_MAXF * sizeof(int2) + 1);
   const size_t smem = std::max(finish_smem(*net), slice_smem);
   static size_t configured = 0;
   if (smem > configured) {
