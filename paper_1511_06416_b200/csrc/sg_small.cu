@@ -847,7 +847,11 @@ __device__ __forceinline__ void tail_stamp(int) {}
 __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& sp, const sg_joint& jp,
                                             const double* cpt, const double* vprob_g, uint32_t* jblob, int P,
                                             int slice, unsigned char* smem, bool wait_pdl,
-                                            bool vprob_ready = false) {
+                                            bool vprob_ready = false, int part = 0, uint16_t* pidx = nullptr) {
+  // part 0: everything; 1: only the static preparation -- the pattern's
+  // latent-variable list and, with pidx, every row entry's list of vprob
+  // indices (a caller runs it early); 2: everything but that (part 1 ran
+  // before).  pidx: [rows_per][K][SG_SMALL_MAXV] u16, 0xFFFF = zero entry.
   __shared__ uint32_t lv[SG_SMALL_MAXV][4];  // latent variables of P in colour order: off|width<<8|card<<16, mbmask, fm, v
   __shared__ int nlat;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -864,7 +868,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
   const int KS = K + 1;  // row stride (odd: no bank conflicts)
   const int rows_per = R / SG_JOINT_TAB_SLICES, r0 = slice * rows_per;
   double* vprob = reinterpret_cast<double*>(smem);  // [n][R][4]
-  if (tid == 0) {
+  if (tid == 0 && part != 2) {
     int k = 0;
     for (int i = 0; i < sp.n; ++i) {
       const int v = sp.order[i];
@@ -876,6 +880,30 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
       ++k;
     }
     nlat = k;
+  }
+  if (part == 1) {
+    if (pidx) {
+      __syncthreads();
+      const int nl1 = nlat;
+      for (int e = tid; e < rows_per * K; e += nt) {
+        const int j = e % K;
+        const uint32_t S = uint32_t(r0 + e / K);
+        const uint32_t Sn = (S & keep) | dep[j];
+        uint16_t* out = pidx + size_t(e) * SG_SMALL_MAXV;
+        uint32_t cur = S;
+        for (int k = 0; k < nl1; ++k) {
+          const uint32_t d = lv[k][0];
+          const uint32_t x = (Sn >> (d & 0xFFu)) & ((1u << ((d >> 8) & 0xFFu)) - 1u);
+          if (x >= (d >> 16)) {
+            out[0] = 0xFFFFu;
+            break;
+          }
+          out[k] = uint16_t((int(lv[k][3]) * R + int(cur & lv[k][1])) * 4 + int(x));
+          cur = (cur & ~lv[k][2]) | (Sn & lv[k][2]);
+        }
+      }
+    }
+    return;
   }
   if (wait_pdl) pdl_wait();  // this step's CPTs (and the tail's conditionals)
   if (vprob_ready) {
@@ -918,6 +946,13 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
   const int warp = tid >> 5, lane = tid & 31;
   const bool two = K == 64;
   auto prod = [&](uint32_t S, int j) {
+    if (pidx) {  // the indices part 1 resolved: the same products in the same order
+      const uint16_t* ix = pidx + size_t((int(S) - r0) * K + j) * SG_SMALL_MAXV;
+      if (nl > 0 && ix[0] == 0xFFFFu) return 0.0;
+      double p = 1.0;
+      for (int k = 0; k < nl; ++k) p = __dmul_rn(p, vprob[ix[k]]);
+      return p;
+    }
     const uint32_t Sn = (S & keep) | dep[j];
     double p = 1.0;
     uint32_t cur = S;
@@ -1098,6 +1133,7 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   const int nr = sp.n << sp.bits;
   int2* plan = reinterpret_cast<int2*>(work + size_t(nr) * 4 * sizeof(double));
   int8_t* plan_nf = reinterpret_cast<int8_t*>(plan + size_t(nr) * SG_JOINT_MAXF);
+  uint16_t* pidx = reinterpret_cast<uint16_t*>(plan_nf + ((size_t(nr) + 15) & ~size_t(15)));
   const int b = blockIdx.x - 1;
   const int P = b / SG_JOINT_TAB_SLICES;
   pdl_trigger();
@@ -1106,7 +1142,10 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   __syncthreads();
   const sg_net net = rebase_net(gnet, b32, b64);
   // every CPT index of this pattern's conditionals, while the sweep / CTA 0 still run
-  if (jblob[jp.patterns + P] & 0xFFu) joint_cond_plan(net, sp, P, plan, plan_nf);
+  if (jblob[jp.patterns + P] & 0xFFu) {
+    joint_cond_plan(net, sp, P, plan, plan_nf);
+    joint_slice(net, sp, jp, nullptr, nullptr, jblob, P, b % SG_JOINT_TAB_SLICES, work, false, true, 1, pidx);
+  }
   pdl_wait();  // the sweep has finished reading the blob rows this grid overwrites
   if (tid == 0) {
     uint32_t r = 0;
@@ -1141,7 +1180,7 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   const bool live = (jblob[jp.patterns + P] & 0xFFu) != 0;
   if (live) joint_cond_apply(net, sp, plan, plan_nf, cpt_s, reinterpret_cast<double*>(work));
   __syncthreads();
-  joint_slice(net, sp, jp, cpt_s, nullptr, jblob, P, b % SG_JOINT_TAB_SLICES, work, false, true);
+  joint_slice(net, sp, jp, cpt_s, nullptr, jblob, P, b % SG_JOINT_TAB_SLICES, work, false, true, 2, pidx);
   __syncthreads();
   stamp(2);
   if (threadIdx.x == 0 && atomicAdd(sync + 1, 1u) == gridDim.x - 2) {
@@ -1463,7 +1502,9 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
   const size_t slice_smem = size_t(net->blob64_words) * 8 + ((size_t(net->blob32_words) * 4 + 15) & ~size_t(15)) +
                             cells2 * 8 + (from_lg ? cells2 * 8 + ((size_t(net->cells) + 15) & ~size_t(15)) : 0) +
                             joint_tables_smem(*sp, jp->max_b) +
-                            (size_t(sp->n) << sp->bits) * (SG_JOINT_MAXF * sizeof(int2) + 1);
+                            (size_t(sp->n) << sp->bits) * SG_JOINT_MAXF * sizeof(int2) +
+                            (((size_t(sp->n) << sp->bits) + 15) & ~size_t(15)) +
+                            (size_t(1) << sp->bits) / SG_JOINT_TAB_SLICES * (size_t(1) << jp->max_b) * SG_SMALL_MAXV * 2;
   const size_t smem = std::max(finish_smem(*net), slice_smem);
   static size_t configured = 0;
   if (smem > configured) {
