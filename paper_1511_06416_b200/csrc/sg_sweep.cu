@@ -683,6 +683,99 @@ static int lane_bits(const sg_net& net, int m) {
 // 4 cells to the histogram; the CTA then flushes every non-zero cell with one
 // global atomic.  A run holding a single oversized variable counts straight
 // into global memory.
+//
+// V16 (states 16-byte aligned, run histogram local): a thread takes 16
+// consecutive cases -- one 16-byte load per row -- and evaluates the cell
+// indices two cases per 32-bit word: bytes 0/2 and 1/3 of a state word are
+// spread into the 16-bit halves of two words and multiplied by the parent's
+// cell stride (stride x card), so each parent costs 5 integer ops per 4 cases
+// instead of 4 byte extractions and 4 multiply-adds.  No half can carry into
+// its neighbour: every partial sum is <= the variable's last cell index
+// < SG_TALLY_CHUNK_CELLS < 2^16.  The ragged last unit of a slice (cases past
+// num_real hold padding) takes the per-case path.
+__device__ __forceinline__ void tally_add4(uint32_t* hist, int base, uint32_t lo, uint32_t hi) {
+  atomicAdd(hist + base + int(lo & 0xFFFFu), 1u);
+  atomicAdd(hist + base + int(hi & 0xFFFFu), 1u);
+  atomicAdd(hist + base + int(lo >> 16), 1u);
+  atomicAdd(hist + base + int(hi >> 16), 1u);
+}
+
+__device__ __forceinline__ void tally_spread(uint32_t x, uint32_t& lo, uint32_t& hi) {
+  lo = x & 0x007F007Fu;
+  hi = (x >> 8) & 0x007F007Fu;
+}
+
+__device__ __forceinline__ void tally_run_v16(const sg_net& net, const sg_batch& bt, uint32_t* hist, int v0,
+                                              int v1, int64_t cell0) {
+  // work items = (replica row, 16-case unit), replica-major so consecutive
+  // threads read consecutive 16-byte columns of one row
+  const int units = (bt.num_real + 15) >> 4;
+  const int full = bt.num_real >> 4;  // units whose 16 cases are all real
+  const int items = units * bt.m;
+  const int per = (items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * per, i1 = min(items, i0 + per);
+  const int64_t vstride = int64_t(bt.m) * bt.pitch;
+  for (int v = v0; v < v1; ++v) {
+    const int card = __ldg(net.card + v);
+    const int ps = __ldg(net.par_start + v), pe = __ldg(net.par_start + v + 1);
+    const int base = int(__ldg(net.cpt_off + v) - cell0);
+    const int np4 = min(4, pe - ps);
+    int64_t poff[4] = {0, 0, 0, 0};
+    uint32_t pst[4] = {0, 0, 0, 0};  // parent cell strides: row stride x card
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < np4) {
+        poff[k] = int64_t(__ldg(net.par_var + ps + k)) * vstride;
+        pst[k] = uint32_t(__ldg(net.par_stride + ps + k) * card);
+      }
+    const int64_t voff = int64_t(v) * vstride;
+    for (int i = i0 + threadIdx.x; i < i1; i += SG_THREADS) {
+      const int r = i / units, u = i - r * units;
+      const int c = u * 16;
+      {
+        const int8_t* col = bt.states + int64_t(r) * bt.pitch + c;
+        if (u < full) {
+          const uint4 xv = __ldg(reinterpret_cast<const uint4*>(col + voff));
+          uint32_t lo[4], hi[4];
+          tally_spread(xv.x, lo[0], hi[0]);
+          tally_spread(xv.y, lo[1], hi[1]);
+          tally_spread(xv.z, lo[2], hi[2]);
+          tally_spread(xv.w, lo[3], hi[3]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < np4) {
+              const uint4 xp = __ldg(reinterpret_cast<const uint4*>(col + poff[k]));
+              uint32_t a, b;
+              tally_spread(xp.x, a, b); lo[0] += a * pst[k]; hi[0] += b * pst[k];
+              tally_spread(xp.y, a, b); lo[1] += a * pst[k]; hi[1] += b * pst[k];
+              tally_spread(xp.z, a, b); lo[2] += a * pst[k]; hi[2] += b * pst[k];
+              tally_spread(xp.w, a, b); lo[3] += a * pst[k]; hi[3] += b * pst[k];
+            }
+          for (int p = ps + 4; p < pe; ++p) {  // parents beyond the fourth
+            const uint4 xp = __ldg(reinterpret_cast<const uint4*>(col + int64_t(__ldg(net.par_var + p)) * vstride));
+            const uint32_t st = uint32_t(__ldg(net.par_stride + p) * card);
+            uint32_t a, b;
+            tally_spread(xp.x, a, b); lo[0] += a * st; hi[0] += b * st;
+            tally_spread(xp.y, a, b); lo[1] += a * st; hi[1] += b * st;
+            tally_spread(xp.z, a, b); lo[2] += a * st; hi[2] += b * st;
+            tally_spread(xp.w, a, b); lo[3] += a * st; hi[3] += b * st;
+          }
+#pragma unroll
+          for (int w = 0; w < 4; ++w) tally_add4(hist, base, lo[w], hi[w]);
+        } else {
+          for (int j = 0; c + j < bt.num_real; ++j) {  // ragged last unit
+            int cell = col[voff + j] & 0x7F;
+            for (int p = ps; p < pe; ++p)
+              cell += (col[int64_t(__ldg(net.par_var + p)) * vstride + j] & 0x7F) * __ldg(net.par_stride + p) * card;
+            atomicAdd(hist + base + cell, 1u);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <bool V16>
 __global__ void __launch_bounds__(SG_THREADS)
 k_tally_chunked(const sg_net net, const sg_batch bt, unsigned long long* __restrict__ counts) {
   extern __shared__ uint32_t hist[];
@@ -694,6 +787,13 @@ k_tally_chunked(const sg_net net, const sg_batch bt, unsigned long long* __restr
   if (local)
     for (int i = threadIdx.x; i < ncell; i += SG_THREADS) hist[i] = 0;
   __syncthreads();
+  if (V16 && local) {
+    tally_run_v16(net, bt, hist, v0, v1, cell0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncell; i += SG_THREADS)
+      if (hist[i]) atomicAdd(counts + cell0 + i, (unsigned long long)hist[i]);
+    return;
+  }
   const int quads = (bt.num_real + 3) >> 2;
   const int per = (quads + gridDim.x - 1) / gridDim.x;
   const int q0 = blockIdx.x * per, q1 = min(quads, q0 + per);
@@ -757,14 +857,23 @@ static int tally_chunked(const sg_net& net, const sg_batch& bt, uint64_t* counts
   if (quads == 0 || net.tally_chunks == 0) return SG_OK;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_tally_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, SG_TALLY_CHUNK_CELLS * 4);
+    cudaFuncSetAttribute(k_tally_chunked<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SG_TALLY_CHUNK_CELLS * 4);
+    cudaFuncSetAttribute(k_tally_chunked<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SG_TALLY_CHUNK_CELLS * 4);
     configured = true;
   }
-  // ~4 CTAs per SM over all runs, each slice at least one thread-quad per thread
+  // 16-case units when every row is 16-byte aligned (pitch % 16 == 0 is part
+  // of the sg_batch contract), else 4-case quads
+  const bool v16 = (reinterpret_cast<uintptr_t>(bt.states) & 15) == 0 && bt.pitch % 16 == 0;
+  const int work = v16 ? (bt.num_real + 15) / 16 * bt.m : quads;
+  // ~4 CTAs per SM over all runs, each slice at least one work item per thread
   const int64_t want = std::max<int64_t>(1, (148 * 4 + net.tally_chunks - 1) / net.tally_chunks);
-  const int slices = int(std::min<int64_t>(want, (quads + SG_THREADS - 1) / SG_THREADS));
-  k_tally_chunked<<<dim3(std::max(1, slices), unsigned(net.tally_chunks)), SG_THREADS, SG_TALLY_CHUNK_CELLS * 4,
-                    s>>>(net, bt, reinterpret_cast<unsigned long long*>(counts));
+  const int slices = std::max(1, int(std::min<int64_t>(want, (work + SG_THREADS - 1) / SG_THREADS)));
+  const dim3 grid(slices, unsigned(net.tally_chunks));
+  auto cp = reinterpret_cast<unsigned long long*>(counts);
+  if (v16)
+    k_tally_chunked<true><<<grid, SG_THREADS, SG_TALLY_CHUNK_CELLS * 4, s>>>(net, bt, cp);
+  else
+    k_tally_chunked<false><<<grid, SG_THREADS, SG_TALLY_CHUNK_CELLS * 4, s>>>(net, bt, cp);
   return SG_OK;
 }
 
