@@ -729,44 +729,62 @@ __device__ __forceinline__ void tally_run_v16(const sg_net& net, const sg_batch&
         pst[k] = uint32_t(__ldg(net.par_stride + ps + k) * card);
       }
     const int64_t voff = int64_t(v) * vstride;
-    for (int i = i0 + threadIdx.x; i < i1; i += SG_THREADS) {
-      const int r = i / units, u = i - r * units;
-      const int c = u * 16;
-      {
-        const int8_t* col = bt.states + int64_t(r) * bt.pitch + c;
-        if (u < full) {
-          const uint4 xv = __ldg(reinterpret_cast<const uint4*>(col + voff));
+    // two items per thread per iteration: both items' row loads are in flight
+    // before either item's cell arithmetic and histogram atomics
+    for (int i = i0 + threadIdx.x; i < i1; i += 2 * SG_THREADS) {
+      const int8_t* col[2];
+      bool vec[2], rag[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ih = i + h * SG_THREADS;
+        const int r = ih / units, u = ih - r * units;
+        col[h] = bt.states + int64_t(r) * bt.pitch + u * 16;
+        vec[h] = ih < i1 && u < full;
+        rag[h] = ih < i1 && u >= full;
+      }
+      uint4 xv[2], xp[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (vec[h]) xv[h] = __ldg(reinterpret_cast<const uint4*>(col[h] + voff));
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (k < np4 && vec[h]) xp[h][k] = __ldg(reinterpret_cast<const uint4*>(col[h] + poff[k]));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (vec[h]) {
           uint32_t lo[4], hi[4];
-          tally_spread(xv.x, lo[0], hi[0]);
-          tally_spread(xv.y, lo[1], hi[1]);
-          tally_spread(xv.z, lo[2], hi[2]);
-          tally_spread(xv.w, lo[3], hi[3]);
+          tally_spread(xv[h].x, lo[0], hi[0]);
+          tally_spread(xv[h].y, lo[1], hi[1]);
+          tally_spread(xv[h].z, lo[2], hi[2]);
+          tally_spread(xv[h].w, lo[3], hi[3]);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if (k < np4) {
-              const uint4 xp = __ldg(reinterpret_cast<const uint4*>(col + poff[k]));
               uint32_t a, b;
-              tally_spread(xp.x, a, b); lo[0] += a * pst[k]; hi[0] += b * pst[k];
-              tally_spread(xp.y, a, b); lo[1] += a * pst[k]; hi[1] += b * pst[k];
-              tally_spread(xp.z, a, b); lo[2] += a * pst[k]; hi[2] += b * pst[k];
-              tally_spread(xp.w, a, b); lo[3] += a * pst[k]; hi[3] += b * pst[k];
+              tally_spread(xp[h][k].x, a, b); lo[0] += a * pst[k]; hi[0] += b * pst[k];
+              tally_spread(xp[h][k].y, a, b); lo[1] += a * pst[k]; hi[1] += b * pst[k];
+              tally_spread(xp[h][k].z, a, b); lo[2] += a * pst[k]; hi[2] += b * pst[k];
+              tally_spread(xp[h][k].w, a, b); lo[3] += a * pst[k]; hi[3] += b * pst[k];
             }
           for (int p = ps + 4; p < pe; ++p) {  // parents beyond the fourth
-            const uint4 xp = __ldg(reinterpret_cast<const uint4*>(col + int64_t(__ldg(net.par_var + p)) * vstride));
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(col[h] + int64_t(__ldg(net.par_var + p)) * vstride));
             const uint32_t st = uint32_t(__ldg(net.par_stride + p) * card);
             uint32_t a, b;
-            tally_spread(xp.x, a, b); lo[0] += a * st; hi[0] += b * st;
-            tally_spread(xp.y, a, b); lo[1] += a * st; hi[1] += b * st;
-            tally_spread(xp.z, a, b); lo[2] += a * st; hi[2] += b * st;
-            tally_spread(xp.w, a, b); lo[3] += a * st; hi[3] += b * st;
+            tally_spread(x.x, a, b); lo[0] += a * st; hi[0] += b * st;
+            tally_spread(x.y, a, b); lo[1] += a * st; hi[1] += b * st;
+            tally_spread(x.z, a, b); lo[2] += a * st; hi[2] += b * st;
+            tally_spread(x.w, a, b); lo[3] += a * st; hi[3] += b * st;
           }
 #pragma unroll
           for (int w = 0; w < 4; ++w) tally_add4(hist, base, lo[w], hi[w]);
-        } else {
-          for (int j = 0; c + j < bt.num_real; ++j) {  // ragged last unit
-            int cell = col[voff + j] & 0x7F;
+        } else if (rag[h]) {
+          const int c = int(col[h] - bt.states) % bt.pitch;  // ragged last unit: per case
+          for (int j = 0; c + j < bt.num_real; ++j) {
+            int cell = col[h][voff + j] & 0x7F;
             for (int p = ps; p < pe; ++p)
-              cell += (col[int64_t(__ldg(net.par_var + p)) * vstride + j] & 0x7F) * __ldg(net.par_stride + p) * card;
+              cell += (col[h][int64_t(__ldg(net.par_var + p)) * vstride + j] & 0x7F) * __ldg(net.par_stride + p) * card;
             atomicAdd(hist + base + cell, 1u);
           }
         }
@@ -776,7 +794,7 @@ __device__ __forceinline__ void tally_run_v16(const sg_net& net, const sg_batch&
 }
 
 template <bool V16>
-__global__ void __launch_bounds__(SG_THREADS)
+__global__ void __launch_bounds__(SG_THREADS, 4)
 k_tally_chunked(const sg_net net, const sg_batch bt, unsigned long long* __restrict__ counts) {
   extern __shared__ uint32_t hist[];
   const int v0 = __ldg(net.tally_chunk + blockIdx.y), v1 = __ldg(net.tally_chunk + blockIdx.y + 1);
