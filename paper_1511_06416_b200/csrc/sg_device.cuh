@@ -217,7 +217,11 @@ __device__ __forceinline__ void conditional_weights(const sg_net& net, int v, co
 // (no FMA).  `get(var)` returns the lane's current state of a variable
 // (shared-memory tile or packed column).  Children are taken two at a time
 // so their loads overlap.
-template <int K, class Get>
+// KMAX > 0 (K = 0): one code path for every card <= KMAX -- fixed-size arrays,
+// the entries t >= card predicated off -- so warps drawing variables of
+// different cardinalities share one instruction stream (fewer i-cache misses);
+// the arithmetic on the entries t < card is exactly that of K = card.
+template <int K, class Get, int KMAX = 0>
 __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, const double* __restrict__ cpt,
                                                Get get, double u, bool& zs) {
   const int card = K ? K : fd[0];
@@ -228,9 +232,10 @@ __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, c
     const int2 e = *reinterpret_cast<const int2*>(p);
     base += get(e.x) * e.y;
   }
-  double w[K ? K : SG_MAX_CARD];
+  constexpr int NT = K ? K : (KMAX ? KMAX : SG_MAX_CARD);
+  double w[NT];
 #pragma unroll
-  for (int t = 0; t < (K ? K : card); ++t) w[t] = __ldg(cpt + base + t);
+  for (int t = 0; t < (K || KMAX ? NT : card); ++t) w[t] = (K || t < card) ? __ldg(cpt + base + t) : 0.0;
   int k = 0;
   for (; k + 1 < nchl; k += 2) {
     int i0 = p[1] + get(p[0]);
@@ -247,14 +252,14 @@ __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, c
       const int2 e = *reinterpret_cast<const int2*>(p);
       i1 += get(e.x) * e.y;
     }
-    double f0[K ? K : SG_MAX_CARD], f1[K ? K : SG_MAX_CARD];
+    double f0[NT], f1[NT];
 #pragma unroll
-    for (int t = 0; t < (K ? K : card); ++t) {
-      f0[t] = __ldg(cpt + i0 + t * s0);
-      f1[t] = __ldg(cpt + i1 + t * s1);
+    for (int t = 0; t < (K || KMAX ? NT : card); ++t) {
+      f0[t] = (K || t < card) ? __ldg(cpt + i0 + t * s0) : 0.0;
+      f1[t] = (K || t < card) ? __ldg(cpt + i1 + t * s1) : 0.0;
     }
 #pragma unroll
-    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(__dmul_rn(w[t], f0[t]), f1[t]);
+    for (int t = 0; t < (K || KMAX ? NT : card); ++t) w[t] = __dmul_rn(__dmul_rn(w[t], f0[t]), f1[t]);
   }
   if (k < nchl) {
     int i0 = p[1] + get(p[0]);
@@ -265,13 +270,19 @@ __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, c
       i0 += get(e.x) * e.y;
     }
 #pragma unroll
-    for (int t = 0; t < (K ? K : card); ++t) w[t] = __dmul_rn(w[t], __ldg(cpt + i0 + t * s0));
+    for (int t = 0; t < (K || KMAX ? NT : card); ++t)
+      if (K || t < card) w[t] = __dmul_rn(w[t], __ldg(cpt + i0 + t * s0));
   }
   double norm;
   if (K && K < 8) {  // numpy's pairwise sum is sequential below 8 terms
     norm = 0.0;
 #pragma unroll
     for (int t = 0; t < (K ? K : 1); ++t) norm = __dadd_rn(norm, w[t]);
+  } else if (KMAX && KMAX < 8) {
+    norm = 0.0;
+#pragma unroll
+    for (int t = 0; t < (KMAX ? KMAX : 1); ++t)
+      if (t < card) norm = __dadd_rn(norm, w[t]);
   } else {
     norm = np_pairwise_sum(w, card);
   }
@@ -280,15 +291,26 @@ __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, c
   double cum = 0.0;
   int x = 0;
 #pragma unroll
-  for (int t = 0; t < (K ? K - 1 : card - 1); ++t) {
-    cum = t ? __dadd_rn(cum, w[t]) : w[0];
-    x += (au > cum);
+  for (int t = 0; t < (K ? K - 1 : (KMAX ? KMAX - 1 : card - 1)); ++t) {
+    if (K || !KMAX || t < card - 1) {
+      cum = t ? __dadd_rn(cum, w[t]) : w[0];
+      x += (au > cum);
+    }
   }
   return x;
 }
 
-template <class Get>
+// UNIFIED: cards 2..4 share one code path (k_sweep_big: its 32 warps draw
+// variables of mixed cardinality side by side, and the unified path cut its
+// instruction-fetch stalls -- C4 sweep 15.9 -> 11.4 ms); the lane and tile
+// kernels keep one specialisation per card (C3, mostly binary: 3.35 ms vs
+// 3.80 ms unified).
+template <bool UNIFIED = false, class Get>
 __device__ __forceinline__ int draw_factored(const int32_t* fd, const double* cpt, Get get, double u, bool& zs) {
+  if (UNIFIED) {
+    if (fd[0] <= 4) return draw_factored_k<0, Get, 4>(fd, cpt, get, u, zs);
+    return draw_factored_k<0>(fd, cpt, get, u, zs);
+  }
   switch (fd[0]) {
     case 2: return draw_factored_k<2>(fd, cpt, get, u, zs);
     case 3: return draw_factored_k<3>(fd, cpt, get, u, zs);
