@@ -357,7 +357,9 @@ def our_arm(args, wl: Workload) -> None:
         # on a copy stream while the current visit runs
         # joint path: observation blocks travel in the 4-bit .sgb form (half the PCIe bytes)
         obs_bits = 8
-        if eng.joint:  # the observation block travels packed: 2 bits/cell when every card <= 3, else 4
+        # the observation block travels packed: 2 bits/cell when every card <= 3, else 4
+        # (joint sweep: read packed; generic sweep: unpacked + range-checked in the graph)
+        if (eng.joint or not eng.use_small) and max(net.cardinalities) <= 15:
             obs_bits = 2 if max(net.cardinalities) <= 3 else 4
         graphs = StepGraphs(eng, mb, M, range(first, first + total_replays), obs_bits=obs_bits)
         for _ in range(graph_warm):

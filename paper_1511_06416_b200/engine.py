@@ -453,8 +453,13 @@ class StepGraphs:
         if self.obs_bits not in (8, 4, 2):
             raise ValueError("obs_bits must be 8, 4 or 2")
         self.nibbles = self.obs_bits < 8  # packed blocks (4- or 2-bit)
-        if self.nibbles and (obs_buffer is not None or not eng.joint):
-            raise ValueError("packed uploads need the joint sweep and private observation buffers")
+        if self.nibbles and (obs_buffer is not None or (eng.use_small and not eng.joint)):
+            raise ValueError("packed uploads need private observation buffers and the joint or generic sweep")
+        # generic sweep: a packed block is unpacked into one int8 block inside
+        # the graph and range-checked there (the joint sweep reads it packed)
+        self._unpacked = None
+        if self.nibbles and not eng.use_small:
+            self._unpacked = torch.empty((eng.n, _pitch(mb.size)), dtype=torch.int8, device=eng.dev)
         if obs_buffer is None:
             # two private buffers, one per graph parity: step(mb) uploads the next
             # visit's block on a copy stream while the current visit runs
@@ -549,7 +554,13 @@ class StepGraphs:
         obs = self.obs_bufs[p]
         # tables and keys of this visit are ready: the previous replay's finish built/advanced them
         if not eng.use_small:  # the packed sweep checks the block in its own launch
-            _lib.call("sg_check_range", eng.pack.ref, obs.data_ptr(), self.ld, size, eng.err.ptr, s)
+            if self._unpacked is not None:
+                u = self._unpacked
+                _lib.call("sg_unpack_nibbles" if self.obs_bits == 4 else "sg_unpack_crumbs", obs.data_ptr(),
+                          obs.stride(0), u.data_ptr(), u.stride(0), eng.n, size, s)
+                _lib.call("sg_check_range", eng.pack.ref, u.data_ptr(), u.stride(0), size, eng.err.ptr, s)
+            else:
+                _lib.call("sg_check_range", eng.pack.ref, obs.data_ptr(), self.ld, size, eng.err.ptr, s)
         S = cfg.sweeps_per_minibatch
         # step tail: accumulate, CPT update, next tables, clear `prev` (the next
         # replay's count buffer), advance the key cursor
@@ -655,7 +666,8 @@ class StepGraphs:
         eng = self.eng
         readback = len(self.readback)
         one_cta = eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
-        check = 0 if eng.use_small else 1  # the packed sweep folds in the range check
+        # the packed sweep folds in the range check; a packed block on the generic path is unpacked first
+        check = 0 if eng.use_small else (2 if self._unpacked is not None else 1)
         return (check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
                 + readback)
 

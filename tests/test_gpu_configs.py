@@ -222,3 +222,45 @@ def test_four_bit_states_bit_exact(hide, m):
     obs = sg.forward_sample_device(net, truth, 900, seed=107, hide_fraction=hide, mask_seed=207)
     dense = obs[:, :900].cpu().numpy().astype(np.int32)
     _sweep_vs_oracle(net, truth, dense, m, 308, 9004)
+
+
+@pytest.mark.parametrize("bits,max_card", [(4, 4), (2, 3)])
+def test_generic_graph_with_packed_uploads_equals_eager(bits, max_card):
+    """Generic-sweep StepGraphs fed packed host blocks (.sgb 4- / 2-bit form:
+    unpacked + range-checked inside the graph) == eager visits on the int8
+    block, bit for bit; an out-of-range state is still flagged
+    (sampler.py:429-430)."""
+    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200.engine import Engine, StepGraphs
+    from paper_1511_06416_b200.io import pack_bits
+
+    net = netgen.random_dag_network(40, max_parents=4, min_card=2, max_card=max_card, seed=31)
+    truth = netgen.dirichlet_cpts(net, 1.0, seed=32)
+    cases, m = 20_001, 2
+    obs = sg.forward_sample_device(net, truth, cases, seed=33, hide_fraction=0.3, mask_seed=34)
+    cfg = sg.SamplerConfig(same_m=m, minibatch_size=cases, num_passes=1, seed=35, rng="fast")
+    mb = next(iter(sg.DeviceSource(obs, cases, cases)))
+    a, b = Engine(net, cfg), Engine(net, cfg)
+    assert not b.use_small
+    for p in range(5):
+        a.visit(mb, p, m)
+    b.visit(mb, 0, m)
+    g = StepGraphs(b, mb, m, range(1, 6), obs_bits=bits)
+    pitchp = g.obs_bufs[0].shape[1] * 8 // bits
+    host = torch.empty(tuple(g.obs_bufs[0].shape), dtype=torch.uint8, pin_memory=True)
+    host.copy_(torch.from_numpy(pack_bits(obs[:, :cases].cpu().numpy(), pitchp, bits)))
+    hmb = sg.Minibatch(index=0, values=host, weights=np.ones(cases), num_real=cases)
+    for _ in range(4):
+        g.step(hmb)
+    torch.cuda.synchronize()
+    assert b.err.read() == 0
+    np.testing.assert_array_equal(a.cpt.cpu().numpy(), b.cpt.cpu().numpy())
+    np.testing.assert_array_equal(a.lane_states(0)[:, :, :cases].cpu().numpy(),
+                                  b.lane_states(0)[:, :, :cases].cpu().numpy())
+    bad = obs[:, :cases].cpu().numpy().copy()
+    v2 = [v for v in range(net.num_vars) if net.cardinalities[v] == 2][0]
+    bad[v2, cases - 1] = 2
+    host.copy_(torch.from_numpy(pack_bits(bad, pitchp, bits)))
+    g.step(hmb)
+    torch.cuda.synchronize()
+    assert b.err.read() & _lib.SG_ERR_STATE_RANGE
