@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
                 for (int q = 0; q < card - 1; ++q) x += au > __ldg(p + q);
               }
             } else {
-              x = draw_factored<true>(fd, a.cpt, get, u01, zs);
+              x = draw_factored<4>(fd, a.cpt, get, u01, zs);
             }
             uint32_t* wp = st + (size_t(v) * a.mg + l) * wpr + cw;
             atomicAnd(wp, ~(MASK << csh));

@@ -305,10 +305,11 @@ __device__ __forceinline__ int draw_factored_k(const int32_t* __restrict__ fd, c
 // instruction-fetch stalls -- C4 sweep 15.9 -> 11.4 ms); the lane and tile
 // kernels keep one specialisation per card (C3, mostly binary: 3.35 ms vs
 // 3.80 ms unified).
-template <bool UNIFIED = false, class Get>
+template <int UNIFIED = 0, class Get>
 __device__ __forceinline__ int draw_factored(const int32_t* fd, const double* cpt, Get get, double u, bool& zs) {
   if (UNIFIED) {
-    if (fd[0] <= 4) return draw_factored_k<0, Get, 4>(fd, cpt, get, u, zs);
+    if (fd[0] <= UNIFIED) return draw_factored_k<0, Get, (UNIFIED ? UNIFIED : 1)>(fd, cpt, get, u, zs);
+    if (UNIFIED < 4 && fd[0] == 4) return draw_factored_k<4>(fd, cpt, get, u, zs);
     return draw_factored_k<0>(fd, cpt, get, u, zs);
   }
   switch (fd[0]) {

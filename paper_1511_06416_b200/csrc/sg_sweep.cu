@@ -29,6 +29,12 @@
 //   5. one coalesced HBM write puts the tile back.
 #include "sg_sweep.cuh"
 
+// draw_factored variant of the lane kernel: cards <= SG_LANE_UNIFIED share one path (0 = per card;
+// measured on C3: per card 3.40 ms, unified <= 3 3.78 ms, unified <= 4 3.80 ms)
+#ifndef SG_LANE_UNIFIED
+#define SG_LANE_UNIFIED 0
+#endif
+
 namespace sg {
 
 struct SmemLayout {
@@ -637,7 +643,7 @@ __global__ void __launch_bounds__(LANE_T) k_sweep_lane(const sg_net net, const s
       }
     } else {
       const int32_t* fd = net.fac_desc + __ldg(net.fac_start + v);
-      x = draw_factored(fd, a.cpt, [&](int var) { return col.get(var); }, u, zs);
+      x = draw_factored<SG_LANE_UNIFIED>(fd, a.cpt, [&](int var) { return col.get(var); }, u, zs);
     }
     col.set(v, x);
   }
