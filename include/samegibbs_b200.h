@@ -176,6 +176,11 @@ int sg_event_destroy(uint64_t ev);
    bench's event measurements). */
 int sg_noop(int32_t ctas, int32_t threads, int32_t smem_bytes, void* stream);
 
+/* L2 flush for benchmarks: writes `bytes` of wbuf, then reads `bytes` of
+   rbuf [dev] (both > L2), with the sweep's max-shared carveout preference
+   (no L1/shared reconfiguration in front of the next timed step). */
+int sg_flush_l2(void* wbuf, void* rbuf, int64_t bytes, uint32_t tag, void* stream);
+
 /* Text of the last failing call on this host thread ("" if none). */
 const char* sg_last_error(void);
 
@@ -467,6 +472,28 @@ int sg_unpack_crumbs(const uint8_t* packed, int64_t ld_packed, int8_t* out, int6
 /* Largest state of each variable's observed cells (range check, sampler.py:429-430). */
 int sg_check_range(const sg_net* net, const int8_t* obs, int32_t ld_obs,
                    int32_t cases, int32_t* err, void* stream);
+
+/* Site keys on the device (replaces rng.stream_key, rng.py:16-20, at its
+   per-variable call sites sampler.py:211 and :245, metrics.py:135):
+   keys[2i], keys[2i+1] = blake2b-128 of the text
+       [decimal(*seed_dev)] prefix decimal(first + i)
+   read as two little-endian uint64, for i in [0, count).  seed_dev [dev]
+   may be NULL (the caller then formats the seed into prefix), e.g.
+   seed_dev = the sweep seed, prefix ":var:" -> stream_key(seed, "var", v). */
+#define SG_SITE_TEXT_MAX 88
+int sg_site_keys(const uint64_t* seed_dev, const char* prefix, int32_t prefix_len, int64_t first,
+                 int32_t count, uint64_t* keys, void* stream);
+
+/* The same BLAKE2b-128 evaluated on the host (no device needed; tests pin it
+   to hashlib): out[0..1] = digest words of text[0..len), len <= 128. */
+int sg_site_key_host(const char* text, int32_t len, uint64_t* out);
+
+/* predict_missing frequency tally (metrics.py:133-137, np.add.at):
+   freq[t][states[t_var[t] * var_stride + t_case[t]] & 0x7F] += 1 for every
+   target t; freq int64 [targets][max_card]. */
+int sg_predict_tally(const int8_t* states, int64_t var_stride, const int32_t* t_var,
+                     const int32_t* t_case, int32_t targets, int32_t max_card, int64_t* freq,
+                     int32_t* err, void* stream);
 
 #ifdef __cplusplus
 }

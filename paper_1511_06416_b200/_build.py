@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsamegibbs_b200.so"
-SOURCES = ["sg_common.cu", "sg_tables.cu", "sg_sweep.cu", "sg_big.cu", "sg_batch.cu", "sg_model.cu", "sg_data.cu", "sg_small.cu"]
+SOURCES = ["sg_common.cu", "sg_tables.cu", "sg_sweep.cu", "sg_big.cu", "sg_batch.cu", "sg_model.cu", "sg_data.cu", "sg_small.cu", "sg_aux.cu"]
 HEADERS = ["sg_device.cuh", "sg_finish.cuh", "sg_sweep.cuh"]
 ROOT = PKG.parent
 

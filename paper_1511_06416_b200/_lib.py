@@ -102,6 +102,10 @@ _SIGNATURES = {
     "sg_forward_sample": ([POINTER(SgNet), c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64,
                            c_double, c_uint64, c_uint64, c_void_p], c_int32),
     "sg_check_range": ([POINTER(SgNet), c_void_p, c_int32, c_int32, c_void_p, c_void_p], c_int32),
+    "sg_site_keys": ([c_void_p, ctypes.c_char_p, c_int32, c_int64, c_int32, c_void_p, c_void_p], c_int32),
+    "sg_site_key_host": ([ctypes.c_char_p, c_int32, c_void_p], c_int32),
+    "sg_predict_tally": ([c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p],
+                         c_int32),
     "sg_small_tables": ([POINTER(SgNet), POINTER(SgSmall), c_void_p, c_void_p, c_void_p], c_int32),
     "sg_small_prepare": ([POINTER(SgSmall), c_void_p, c_int32, c_int32, c_int32, c_int64, c_uint64, c_int32,
                           c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p], c_int32),
@@ -124,6 +128,7 @@ _SIGNATURES = {
     "sg_event_elapsed": ([c_uint64, c_uint64, POINTER(ctypes.c_float)], c_int32),
     "sg_event_destroy": ([c_uint64], c_int32),
     "sg_noop": ([c_int32, c_int32, c_int32, c_void_p], c_int32),
+    "sg_flush_l2": ([c_void_p, c_void_p, c_int64, ctypes.c_uint32, c_void_p], c_int32),
     "sg_step_finish": ([POINTER(SgNet), c_void_p, POINTER(SgFinish), c_void_p], c_int32),
     "sg_unpack_nibbles": ([c_void_p, c_int64, c_void_p, c_int64, c_int32, c_int64, c_void_p], c_int32),
     "sg_unpack_crumbs": ([c_void_p, c_int64, c_void_p, c_int64, c_int32, c_int64, c_void_p], c_int32),
@@ -171,7 +176,7 @@ KERNELS_PER_CALL = {
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
     "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
     "sg_joint_tables": 1, "sg_joint_sweep": 1, "sg_step_tail_joint": 1, "sg_copy_small": 1, "sg_noop": 1,
-    "sg_keys_advance": 1, "sg_step_finish": 1, "sg_unpack_nibbles": 1, "sg_unpack_crumbs": 1,
+    "sg_keys_advance": 1, "sg_step_finish": 1, "sg_site_keys": 1, "sg_predict_tally": 1, "sg_unpack_nibbles": 1, "sg_unpack_crumbs": 1,
 }
 launch_count = 0
 

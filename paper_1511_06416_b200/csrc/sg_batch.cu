@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(256) k_init_states(const sg_net net, const sg_
     if (c < bt.cases) {
       const int o = obs[int64_t(v) * ld_obs + c];
       if (o >= 0) {
-        out = int8_t(o);
+        // an out-of-range observation never becomes an index: state 0 + error bit
+        out = o < card ? int8_t(o) : int8_t(0);
         bad |= o >= card;
       } else if (MODE == SG_RNG_FAST) {
         const uint32_t w = pick(fast_block(fast_key, uint64_t(bt.case_base + c), uint32_t(v), uint32_t(r >> 2), 1u), r & 3);

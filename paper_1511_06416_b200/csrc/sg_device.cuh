@@ -13,6 +13,7 @@
 // FMA: the reference rounds each numpy operation separately.
 #pragma once
 
+#include <cstdlib>
 #include <utility>
 
 #include <cstdint>
@@ -496,7 +497,8 @@ static inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const int pdl_off = std::getenv("SG_NO_PDL") != nullptr;  // debugging: plain stream order
+  cfg.numAttrs = pdl_off ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
 }
 

@@ -100,7 +100,9 @@ __global__ void __launch_bounds__(256) k_small_scatter(
   uint32_t obsw = 0;
   for (int v = 0; v < sp.n; ++v) {
     const int o = obs[int64_t(v) * ld + c];
-    if (o >= 0) obsw |= uint32_t(o) << sp.off[v];
+    // out of range -> field 0 (the sweep's range check of this block raises
+    // SG_ERR_STATE_RANGE); it never spills into a neighbouring field
+    if (o >= 0 && o < sp.card[v]) obsw |= uint32_t(o) << sp.off[v];
   }
   uint32_t* out = reinterpret_cast<uint32_t*>(lanes);
   for (int q = 0; q < (m + 3) / 4; ++q) {
@@ -692,7 +694,9 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
       const uint32_t wg = w[g] & (g < qs.last ? 0xFFFFFFFFu : qs.last_valid);
       if (g <= qs.last) rows[g * qs.ld + s] = wg;
       if (counts) {
-        const uint32_t wt = wg | (real_case ? trash[g] : 0x40404040u);
+        // padded cases (c >= num_real) and alias quads (g > last): every lane to the trash
+        // bin 64 (OR-ing 0x40 into a lane word would index bins 64..127, past this warp's 65)
+        const uint32_t wt = (real_case && g <= qs.last) ? (wg | trash[g]) : 0x40404040u;
 #ifndef SG_EXP_NOTALLY  // timing experiment only: no tally
 #pragma unroll
         for (int j = 0; j < (g == QG - 1 ? NL : 4); ++j) joint_count(hist_a, byte_of(wt, j));

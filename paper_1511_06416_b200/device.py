@@ -66,3 +66,39 @@ class ErrorWord:
         self.host.copy_(self.dev, non_blocking=False)
         return int(self.host.item())
 
+
+
+def site_keys(out: torch.Tensor, prefix: str, count: int, seed_dev: torch.Tensor | int | None = None,
+              first: int = 0) -> torch.Tensor:
+    """Device ``stream_key`` of ``count`` consecutive sites into ``out`` (int64 [count, 2]).
+
+    Site i's text is ``[str(*seed_dev)] + prefix + str(first + i)`` (rng.py:16-20):
+    ``site_keys(k, ":var:", n, seed_dev=cursor)`` = ``stream_key(seed, "var", v)``
+    for v < n with the seed word read from device memory at replay time;
+    ``site_keys(k, f"{seed}:latent_init:{p}:{mb}:", n)`` has the seed in the text.
+    ``seed_dev`` is a device tensor (its first uint64) or a raw device pointer."""
+    text = prefix.encode()
+    ptr = None if seed_dev is None else (seed_dev if isinstance(seed_dev, int) else seed_dev.data_ptr())
+    _lib.call("sg_site_keys", ptr, text, len(text), first, count, out.data_ptr(), stream_handle())
+    return out
+
+
+def var_keys(out: torch.Tensor | None, seed: int, label: str, context: tuple, n: int) -> torch.Tensor:
+    """``stream_key(seed, label, *context, v)`` for v < n on the device (int64 [n, 2]).
+
+    Hashed by ``sg_site_keys`` (one thread per variable); a site text that does
+    not fit one BLAKE2b block (seeds beyond 64 bits) is hashed on the host."""
+    if out is None:
+        out = torch.empty((max(1, n), 2), dtype=torch.int64, device=device())
+    prefix = ":".join([str(int(seed)), label, *(str(int(i)) for i in context)]) + ":"
+    if len(prefix) <= 88:
+        return site_keys(out, prefix, n)
+    import numpy as np
+
+    from .rng import stream_key_ints
+
+    host = np.empty((n, 2), dtype=np.uint64)
+    for v in range(n):
+        host[v] = stream_key_ints(seed, label, *context, v)
+    out[:n].copy_(torch.from_numpy(host.view(np.int64)))
+    return out

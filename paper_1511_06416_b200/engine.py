@@ -21,13 +21,13 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import ErrorWord, device, netpack, stream_handle
+from .device import ErrorWord, device, netpack, site_keys, stream_handle, var_keys
 from .errors import ValidationError
 from .metrics import kl_avg
 from .io import pack_bits
 from .model import CptSet, init_cpts
 from .network import Network, color_graph, moralize
-from .rng import derive_seed, stream_key_ints
+from .rng import derive_seed
 from .sampler import (DeviceBatch, MemoryStats, SamplerConfig, Trace, TraceRecord, _pitch, _raise_errors,
                       anneal_m)
 
@@ -106,7 +106,6 @@ class Engine:
         self.latent: dict[int, DeviceBatch] = {}   # moving-sum: resident lane states per minibatch
         self.nmiss_host: dict[int, np.ndarray] = {}
         self.keys = torch.empty((self.n, 2), dtype=torch.int64, device=d)
-        self._keys_ring = PinnedRing((self.n, 2), torch.int64)
         self.rej = torch.empty(self.n * (_lib.REJ_SLACK + 2), dtype=torch.int64, device=d)
         self._obs_cache: dict[int, torch.Tensor] = {}
         self._obs_rings: dict[int, PinnedRing] = {}
@@ -132,16 +131,13 @@ class Engine:
             self.vprob = torch.zeros(self.n * (4 << self.pack.small.bits), dtype=torch.float64, device=d)
             self.jsync = torch.zeros(2, dtype=torch.int32, device=d)  # sg_step_tail_joint's hand-off words
         self.tables_fresh = False  # conditional tables reflect self.cpt
+        self.graph_replay = True   # run(): replay steady-state visits as CUDA graphs
         self._latent_hint = None   # latent share of the first generic minibatch (sg_batch.latent_permille)
 
     # ------------------------------------------------------------ helpers
     def _upload_keys(self, seed: int, label: str, context: tuple) -> None:
-        host, done = self._keys_ring.slot()
-        kh = host.numpy().view(np.uint64)
-        for v in range(self.n):
-            kh[v] = stream_key_ints(seed, label, *context, v)
-        self.keys.copy_(host, non_blocking=True)
-        done.record()
+        """Per-variable site keys of one sweep / latent init, hashed on the device."""
+        var_keys(self.keys, seed, label, context, self.n)
 
     def _obs_for(self, mb) -> tuple[torch.Tensor, int]:
         """Device (n, pitch) int8 observation block of a minibatch."""
@@ -164,11 +160,13 @@ class Engine:
             buf.copy_(vals, non_blocking=True)
             return buf, pitch
         host = vals.numpy() if isinstance(vals, torch.Tensor) else np.asarray(vals)
-        if host.dtype != np.int8:
-            cards = np.asarray(self.net.cardinalities)[:, None]
-            if ((host >= cards) & (host >= 0)).any():
-                raise ValidationError("data contains a state >= its variable's cardinality")
-            host = host.astype(np.int8)
+        # host blocks of any dtype are range-checked before the upload (sampler.py:429-430);
+        # device and pinned blocks are checked on the device, and an out-of-range state is
+        # written as state 0 + the error bit, never used as an index
+        cards = np.asarray(self.net.cardinalities)[:, None]
+        if ((host >= cards) | (host < -1)).any():
+            raise ValidationError("data contains a state >= its variable's cardinality")
+        host = host.astype(np.int8)
         buf = self._obs_cache.get(pitch)
         if buf is None:
             buf = self._obs_cache[pitch] = torch.empty((self.n, pitch), dtype=torch.int8, device=self.dev)
@@ -256,6 +254,8 @@ class Engine:
             last = sw == S - 1
             counts_ptr = new_counts.data_ptr() if last else None
             if self.use_small:
+                if sw:
+                    self.sweep_fence(s)
                 self.packed_sweep(db, size, m, sweep_seed, None, counts_ptr, obs.data_ptr() if last else None, ld, s)
             elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
@@ -322,6 +322,15 @@ class Engine:
                 raise ValueError("packed observation blocks are range-checked by the joint sweep only")
             _lib.call("sg_small_sweep", self.pack.small_ref, self.stab.data_ptr(), *head, self.err.ptr, s)
 
+    @staticmethod
+    def sweep_fence(s) -> None:
+        """Before the 2nd..S-th packed sweep of a visit: a plain (non-PDL) launch.
+        The packed sweeps load their first slot's lane words before their PDL
+        wait -- safe after the step tail, which never writes lanes, but not
+        right after another sweep; an ordinary launch in between starts only
+        when that sweep has completed."""
+        _lib.call("sg_noop", 1, 32, 0, s)
+
     def step_tail(self, f, s) -> None:
         """Accumulate, CPT update and the next visit's tables: one single-CTA
         launch, or with rng="joint" one grid that also builds the joint rows."""
@@ -356,28 +365,83 @@ class Engine:
     def current_cpts(self) -> CptSet:
         return CptSet(self.pack.split(self.cpt.cpu().numpy()))
 
+    def graphs_ok(self) -> bool:
+        """Steady-state visits may be graph-replayed: moving sum (resident lanes)
+        and no host collective inside the step (NCCL all-reduces are capturable)."""
+        if self.cfg.accumulator_mode != "moving_sum" or not self.graph_replay:
+            return False
+        return self.comm is None or getattr(self.comm, "capturable", False)
+
     def run(self, source, truth: CptSet | None = None):
+        """All passes of ``run()`` (sampler.py:385-495) without a host round trip per visit.
+
+        The first visit of a minibatch (and the first after the SAME factor
+        changes) runs eagerly and leaves its lanes resident; the following
+        visits of that minibatch replay two captured step graphs
+        (:class:`StepGraphs`: same kernels, same keys, bit-identical results).
+        Per pass the engine records a CUDA event and, with ``truth``, a device
+        snapshot of the CPTs; the host synchronises once at the end, checks
+        the error word and builds the trace (pass times from the events,
+        ``kl_avg`` from the snapshots in the reference's fp64 arithmetic)."""
         cfg = self.cfg
         trace = Trace()
         cell_bytes = self.pack.cells * 8
-        trace.memory.model_bytes = cell_bytes
-        trace.memory.accumulator_bytes = cell_bytes
         torch.cuda.synchronize()
-        start = time.perf_counter()
+        start = torch.cuda.Event(enable_timing=True)
+        start.record()
+        marks, snaps = [], []
+        snap_all = truth is not None and cfg.num_passes * cell_bytes <= (1 << 30)
+        graphs: dict[int, StepGraphs] = {}
+        use_graphs = self.graphs_ok()
+        sched = [anneal_m(cfg.same_m, p) for p in range(cfg.num_passes)]
+        host_t0 = time.perf_counter()
+        kls = []
         for pass_index in range(cfg.num_passes):
-            pass_start = time.perf_counter()
-            m = anneal_m(cfg.same_m, pass_index)
+            m = sched[pass_index]
+            end_same = pass_index
+            while end_same < cfg.num_passes and sched[end_same] == m:
+                end_same += 1
             for mb in source:
+                g = graphs.get(mb.index)
+                if g is not None and (g.m != m or not g.accepts(mb)):
+                    g.finish()
+                    del graphs[mb.index]
+                    g = None
+                if g is not None:
+                    g.step(mb)
+                    continue
                 self.visit(mb, pass_index, m)
-            word = self.err.read()  # synchronises the stream
-            _raise_errors(word)
-            now = time.perf_counter()
-            secs = now - pass_start
-            sampled = self.n * source.num_cases * m * cfg.sweeps_per_minibatch
-            kl = kl_avg(truth, self.current_cpts()) if truth is not None else None
-            trace.records.append(TraceRecord(pass_index=pass_index + 1, seconds=now - start, kl_avg=kl,
+                if use_graphs and pass_index + 1 < end_same:
+                    graphs[mb.index] = StepGraphs(self, mb, m, range(pass_index + 1, end_same),
+                                                  obs_buffer=StepGraphs.view_of(mb))
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append(ev)
+            if truth is not None:
+                if snap_all:
+                    snaps.append(self.cpt.clone())
+                else:  # very large models: one CPT read-back per pass
+                    _raise_errors(self.err.read())
+                    kls.append(kl_avg(truth, self.current_cpts()))
+        for g in graphs.values():
+            g.finish()
+        torch.cuda.synchronize()
+        host_secs = time.perf_counter() - host_t0
+        _raise_errors(self.err.read())
+        if snap_all and snaps:
+            stacked = torch.stack(snaps).cpu().numpy()
+            kls = [kl_avg(truth, CptSet(self.pack.split(row))) for row in stacked]
+        prev_s = 0.0
+        for pass_index, ev in enumerate(marks):
+            now = start.elapsed_time(ev) * 1e-3
+            secs = now - prev_s
+            prev_s = now
+            sampled = self.n * source.num_cases * sched[pass_index] * cfg.sweeps_per_minibatch
+            trace.records.append(TraceRecord(pass_index=pass_index + 1, seconds=now,
+                                             kl_avg=kls[pass_index] if truth is not None else None,
                                              vars_per_sec=sampled / secs if secs > 0 else None,
                                              vars_sampled=sampled))
+        self.host_seconds = host_secs
         mem = trace.memory
         mem.accumulator_bytes = cell_bytes * (1 + len(self.prev_counts))
         latent = 0
@@ -403,7 +467,8 @@ class StepGraphs:
     that ``sg_keys_advance`` steps through at the head of each replay, and the
     new/previous count buffers alternate between two graphs.  Replays run
     exactly the kernels ``Engine.visit`` launches with exactly the same keys,
-    so results equal eager visits bit for bit (FAST RNG mode).
+    so results equal eager visits bit for bit (every RNG mode: in numpy mode
+    each replay hashes its per-variable sweep keys on the device).
     """
 
     def __init__(self, eng: Engine, mb, m: int, pass_indices, obs_buffer: torch.Tensor | None = None,
@@ -427,8 +492,8 @@ class StepGraphs:
         sweep node(s) inside each graph; :meth:`sweep_ms` reads the last
         replay's sweep duration (call after synchronising)."""
         cfg = eng.cfg
-        if eng.rng_mode != _lib.SG_RNG_FAST or cfg.accumulator_mode != "moving_sum":
-            raise ValueError("graph replay needs the fast RNG and the moving-sum accumulator")
+        if cfg.accumulator_mode != "moving_sum":
+            raise ValueError("graph replay of resident minibatches needs the moving-sum accumulator")
         db = eng.latent.get(mb.index)
         if db is None or db.m != m or db.cases != mb.size:
             raise ValueError("visit the minibatch once (eagerly) before capturing its graph")
@@ -525,6 +590,20 @@ class StepGraphs:
             self.graphs.append(g)
         torch.cuda.synchronize()
 
+    @staticmethod
+    def view_of(mb):
+        """The minibatch's device int8 block when the graphs can read it in place
+        (16-byte aligned rows), else None (private buffers refilled by step())."""
+        v = mb.values
+        if isinstance(v, torch.Tensor) and v.is_cuda and v.dtype == torch.int8 and v.stride(1) == 1 \
+                and v.stride(0) % 16 == 0 and v.data_ptr() % 16 == 0:
+            return v
+        return None
+
+    def accepts(self, mb) -> bool:
+        """``mb`` can be replayed by these graphs (same minibatch shape, visits left)."""
+        return self.replayed < self.planned and mb.size == self.mb.size and int(mb.num_real) == int(self.db.num_real)
+
     def sweep_ms(self) -> float:
         """Sweep time (ms, all sweeps of the visit) of the last replay (timing=True)."""
         if self._tev is None or not self.replayed:
@@ -573,8 +652,17 @@ class StepGraphs:
             last = sw == S - 1
             counts_ptr = new.data_ptr() if last else None
             if eng.use_small:
+                if sw:
+                    eng.sweep_fence(s)
                 eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr, obs.data_ptr() if last else None, self.ld, s,
                                  obs_bits=self.obs_bits)
+            elif eng.rng_mode == _lib.SG_RNG_NUMPY:
+                # numpy stream: stream_key(sweep_seed, "var", v) hashed on the device from the
+                # cursor's sweep seed (sampler.py:245, rng.py:16-20), then the bit-exact sweep
+                site_keys(eng.keys, ":var:", eng.n, seed_dev=cur + 8 * sw)
+                _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
+                          eng.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, None, eng.keys.data_ptr(), None, None, counts_ptr,
+                          eng.err.ptr, s)
             else:
                 _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
@@ -634,11 +722,23 @@ class StepGraphs:
             vals = mb.values
             buf = self.obs_bufs[p]
             if not (isinstance(vals, torch.Tensor) and vals.is_cuda and vals.data_ptr() == buf.data_ptr()):
-                src = vals if isinstance(vals, torch.Tensor) else torch.from_numpy(np.asarray(vals, dtype=np.int8))
+                if isinstance(vals, torch.Tensor) and vals.is_cuda:
+                    src = vals
+                else:  # host block: range-checked before the int8 conversion (as _obs_for does)
+                    host = vals.numpy() if isinstance(vals, torch.Tensor) else np.asarray(vals)
+                    if not self.nibbles:
+                        cards = np.asarray(self.eng.net.cardinalities)[:, None]
+                        if ((host >= cards) | (host < -1)).any():
+                            raise ValidationError("data contains a state >= its variable's cardinality")
+                    src = torch.from_numpy(np.ascontiguousarray(host.astype(np.uint8 if self.nibbles else np.int8)))
                 if self.nibbles and (src.dtype != torch.uint8 or tuple(src.shape) != tuple(buf.shape)):
                     raise ValueError(f"expected a packed block uint8 {tuple(buf.shape)} (io.pack_bits)")
-                if not self.private_obs:
-                    buf[:, :mb.size].copy_(src, non_blocking=True)
+                if not self.private_obs or src.is_cuda:
+                    # device blocks are produced on this stream: copy in stream order
+                    if self.nibbles:
+                        buf.copy_(src, non_blocking=True)
+                    else:
+                        buf[:, :mb.size].copy_(src, non_blocking=True)
                 else:
                     # upload on the copy stream once the replay that last read this buffer is done,
                     # so it overlaps the other parity's replay
@@ -668,7 +768,10 @@ class StepGraphs:
         one_cta = eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
         # the packed sweep folds in the range check; a packed block on the generic path is unpacked first
         check = 0 if eng.use_small else (2 if self._unpacked is not None else 1)
-        return (check + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
+        keys = eng.cfg.sweeps_per_minibatch if eng.rng_mode == _lib.SG_RNG_NUMPY else 0
+        if eng.use_small:
+            keys += eng.cfg.sweeps_per_minibatch - 1  # sweep fences
+        return (check + keys + eng.cfg.sweeps_per_minibatch + (1 if one_cta else 5 + (1 if eng.use_small else 0))
                 + readback)
 
     def finish(self) -> None:

@@ -167,7 +167,7 @@ def tally_counts(net: Network, values, weights) -> CountSet:
     if vals.ndim != 2 or vals.shape[0] != net.num_vars or w.shape != (vals.shape[1],):
         raise ShapeMismatch("values must be (num_vars, lanes) with one weight per lane")
     lanes = vals.shape[1]
-    batch = _upload_lanes(vals, None, m=1, cases=lanes, num_real=lanes, dev=dev)
+    batch = _upload_lanes(vals, None, m=1, cases=lanes, num_real=lanes, dev=dev, cards=net.cardinalities)
     binary = bool(np.all((w == 0.0) | (w == 1.0)))
     if binary and np.all(w[:int(w.sum())] == 1.0):  # a prefix of ones: plain integer tally
         batch.struct.num_real = int(w.sum())

@@ -35,6 +35,9 @@ def count_allreduce(group=None):
     def comm(counts: torch.Tensor) -> None:
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
 
+    # an NCCL all-reduce can be captured inside the step graphs (Engine.run replays them);
+    # a gloo all-reduce is a host collective and keeps the visits eager
+    comm.capturable = dist.is_initialized() and dist.get_backend(group) == "nccl"
     return comm
 
 

@@ -47,7 +47,7 @@ from .errors import (DimensionMismatch, EmptyData, ShapeMismatch, ValidationErro
                      DeviceError)
 from .model import CountSet, CptSet, DirichletPrior, init_cpts, zero_counts
 from .network import Coloring, Network, color_graph, moralize
-from .rng import derive_seed, stream_key_ints
+from .rng import derive_seed
 
 MSchedule = Union[int, Sequence[tuple[int, int]]]
 
@@ -263,8 +263,11 @@ def _obs_from_values(vals_rep0: np.ndarray, latent: np.ndarray, pitch: int, dev)
 
 
 def _upload_lanes(values: np.ndarray, missing_lanes, m: int, cases: int, num_real: int, dev,
-                  ) -> DeviceBatch:
-    """Host (n, m*cases) int values + latent lane lists -> DeviceBatch (flags in bit 7)."""
+                  cards=None) -> DeviceBatch:
+    """Host (n, m*cases) int values + latent lane lists -> DeviceBatch (flags in bit 7).
+
+    ``cards``: per-variable cardinalities; every cell must hold a state below
+    its card (checked here, before any device index is formed)."""
     vals = np.asarray(values)
     n = vals.shape[0]
     if vals.shape[1] != m * cases:
@@ -280,6 +283,12 @@ def _upload_lanes(values: np.ndarray, missing_lanes, m: int, cases: int, num_rea
         # the reference samples cells listed in missing_lanes; any other cell must hold a state
         if (vals[~lat] < 0).any():
             raise ValidationError("a non-latent cell holds no state")
+    if missing_lanes is None and (vals < 0).any():
+        raise ValidationError("values must be complete assignments (a cell holds no state)")
+    if cards is not None and vals.size:
+        top = np.asarray(cards, dtype=np.int64)[:, None]
+        if (vals >= top).any():
+            raise ValidationError("data contains a state >= its variable's cardinality")
     cell = np.where(vals < 0, 0, vals).astype(np.int64)
     if cell.size and cell.max() > 127:
         raise ValueError("states above 127 are not supported by the int8 lane layout")
@@ -296,10 +305,9 @@ def _upload_lanes(values: np.ndarray, missing_lanes, m: int, cases: int, num_rea
 
 
 def _var_keys(seed: int, label: str, context: tuple, n: int, dev) -> torch.Tensor:
-    keys = np.empty((n, 2), dtype=np.uint64)
-    for v in range(n):
-        keys[v] = stream_key_ints(seed, label, *context, v)
-    return torch.from_numpy(keys.view(np.int64)).to(dev)
+    from .device import var_keys
+
+    return var_keys(None, seed, label, context, n)
 
 
 def _download_states(db: DeviceBatch, batch: ReplicatedBatch) -> None:
@@ -336,7 +344,7 @@ def _device_pass(net: Network, coloring: Coloring, cpts: CptSet, batch: Replicat
     n = net.num_vars
     num_real = _batch_num_real(batch) if tally else batch.base_size
     db = _upload_lanes(batch.values, batch.missing_lanes, batch.m, batch.base_size,
-                       num_real if num_real is not None else batch.base_size, dev)
+                       num_real if num_real is not None else batch.base_size, dev, net.cardinalities)
     db.compute_ranks()
     cpt = torch.from_numpy(pack.flatten(cpts.tables)).to(dev)
     ptab = torch.empty(max(1, pack.layout.scalars["ptab_size"]), dtype=torch.float64, device=dev)
@@ -409,7 +417,8 @@ def init_latent(net: Network, batch: ReplicatedBatch, seed: int, *context: int) 
     dev = device()
     pack = netpack(net)
     n = net.num_vars
-    db = _upload_lanes(batch.values, batch.missing_lanes, batch.m, batch.base_size, batch.base_size, dev)
+    db = _upload_lanes(batch.values, batch.missing_lanes, batch.m, batch.base_size, batch.base_size, dev,
+                       net.cardinalities)
     db.compute_ranks()
     keys = _var_keys(seed, "latent_init", tuple(context), n, dev)
     rej = torch.empty(n * (_lib.REJ_SLACK + 2), dtype=torch.int64, device=dev)

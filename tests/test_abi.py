@@ -83,3 +83,31 @@ def test_no_cpu_fallback_without_gpu():
     net = sg.build_network([2, 2], [(0, 1)])
     with pytest.raises(DeviceError):
         sg.tally_counts(net, [[0, 1], [1, 1]], [1.0, 1.0])
+
+
+def test_device_site_key_hash_matches_hashlib():
+    """sg_site_keys' BLAKE2b-128 (evaluated on the host through sg_site_key_host,
+    the same __host__ __device__ code) equals rng.stream_key (hashlib), rng.py:16-20."""
+    import hashlib
+
+    import numpy as np
+
+    from paper_1511_06416_b200 import _build, _lib
+    from paper_1511_06416_b200.rng import stream_key_ints
+
+    _build.build()
+    lib = _lib.load()
+    texts = [b"", b"a", b"0:sweep:0:0:0", b"18446744073709551615:var:999", b"-7:latent_init:3:1:2",
+             b"x" * 127, b"y" * 128, b"300:cpt_update:1:2"]
+    out = (ctypes.c_uint64 * 2)()
+    for t in texts:
+        assert lib.sg_site_key_host(t, len(t), out) == 0
+        d = hashlib.blake2b(t, digest_size=16).digest()
+        assert (out[0], out[1]) == (int.from_bytes(d[:8], "little"), int.from_bytes(d[8:], "little")), t
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        seed = int(rng.integers(0, 2**63)) * int(rng.integers(1, 3))
+        v = int(rng.integers(0, 10**6))
+        t = f"{seed}:var:{v}".encode()
+        assert lib.sg_site_key_host(t, len(t), out) == 0
+        assert (out[0], out[1]) == stream_key_ints(seed, "var", v)

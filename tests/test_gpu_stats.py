@@ -122,21 +122,6 @@ def test_koller_protocol_fast_stream_median():
     assert float(np.median([r[1] for r in res])) <= 0.005
     assert max(r[0] for r in res) <= 0.015
 
-
-def test_sampled_run_close_to_reference(koller):
-    """Sampled-Dirichlet run vs the reference's own (fixture) at equal sweeps:
-    final CPT max-abs difference and KL to the truth within tolerance."""
-    from golden_io import load, tables
-
-    d = load("run_sampled")
-    net, truth = koller
-    cfg = sg.SamplerConfig(same_m=5, minibatch_size=200, num_passes=20, seed=7)
-    kls = []
-    for seed in range(4):
-        cfg.seed = seed
-        cpts, trace = sg.run(net, sg.DataMatrix.from_dense(d["dense"]), cfg, truth=truth)
-        kls.append(trace.records[-1].kl_avg)
-        ref = tables(d, "cpt")
-        assert max(np.abs(a - b).max() for a, b in zip(cpts.tables, ref)) < 0.25
-    # the reference's final KL (one seed) sits inside the spread of ours
-    assert min(kls) / 3 <= float(d["kl"][-1]) <= 3 * max(kls)
+# The sampled-run comparison against the reference lives in test_gpu_acceptance.py:
+# the Koller protocol (15 runs), the sampler spread (24 seeds per m, Welch t) and the
+# C2-scale trajectories, each against the reference's own runs with stated tolerances.
