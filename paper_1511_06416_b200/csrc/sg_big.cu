@@ -234,11 +234,9 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
 
 template <int MODE, int BITS>
 static void launch_big(const sg_net& net, const sg_batch& bt, const SweepArgs& a, size_t smem, cudaStream_t s) {
-  static size_t configured = 0;
-  if (smem > configured) {
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, smem))
     cudaFuncSetAttribute(k_sweep_big<MODE, BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
-  }
   const dim3 grid((bt.cases + a.tc - 1) / a.tc, (bt.m + a.mg - 1) / a.mg);
   k_sweep_big<MODE, BITS><<<grid, BIG_T, smem, s>>>(net, bt, a);
 }

@@ -127,11 +127,9 @@ __global__ void k_noop(int* never) {
 extern "C" int sg_noop(int32_t ctas, int32_t threads, int32_t smem_bytes, void* stream) {
   using namespace sg;
   SG_REQUIRE(ctas > 0 && threads > 0 && threads <= 1024 && smem_bytes >= 0, "sg_noop: bad shape");
-  static int configured = 0;
-  if (smem_bytes > 48 * 1024 && smem_bytes > configured) {
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, size_t(smem_bytes)))
     cudaFuncSetAttribute(k_noop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    configured = smem_bytes;
-  }
   k_noop<<<ctas, threads, smem_bytes, (cudaStream_t)stream>>>(nullptr);
   return check_launch("sg_noop");
 }
@@ -159,16 +157,15 @@ __global__ void __launch_bounds__(512) k_flush_read(const uint4* __restrict__ sr
 extern "C" int sg_flush_l2(void* wbuf, void* rbuf, int64_t bytes, uint32_t tag, void* stream) {
   using namespace sg;
   SG_REQUIRE(wbuf && rbuf && bytes >= 16 && bytes % 16 == 0, "sg_flush_l2: bad argument");
-  static int configured[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !configured[dev]) {
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, 1)) {
     cudaFuncSetAttribute(k_flush_write, cudaFuncAttributePreferredSharedMemoryCarveout,
                          int(cudaSharedmemCarveoutMaxShared));
     cudaFuncSetAttribute(k_flush_read, cudaFuncAttributePreferredSharedMemoryCarveout,
                          int(cudaSharedmemCarveoutMaxShared));
-    configured[dev] = 1;
   }
+  int dev = 0;
+  cudaGetDevice(&dev);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n16 = bytes / 16;

@@ -26,6 +26,7 @@
 #define SG_MAX_CARD 64      // states per variable (int8 lane state keeps 7 bits)
 #define SG_MAX_MB 64        // Markov-blanket members gathered per draw
 #define SG_REJ_SLACK 64     // Lemire rejections tolerated per init stream
+#define SG_MAX_DEVICES 64   // per-device caches of kernel attribute opt-ins
 
 namespace sg {
 
@@ -500,6 +501,19 @@ static inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block
   static const int pdl_off = std::getenv("SG_NO_PDL") != nullptr;  // debugging: plain stream order
   cfg.numAttrs = pdl_off ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+
+// Kernel attribute opt-ins are per device context: each launch site keeps the
+// largest shared-memory size it has opted in to, per device, and raises the
+// attribute only when a launch needs more (so graph capture sees no
+// attribute calls after the first launch on each device).
+static inline bool optin_needed(size_t* configured /* [SG_MAX_DEVICES] */, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= SG_MAX_DEVICES) return true;
+  if (bytes <= configured[dev]) return false;
+  configured[dev] = bytes;
+  return true;
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

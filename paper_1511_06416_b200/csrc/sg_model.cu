@@ -132,11 +132,9 @@ extern "C" int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_fi
   if (finish_fits(*net, sp)) {
     const FinishArgs a = make_finish_args(f, sp);
     const size_t smem = finish_smem(*net);
-    static size_t configured = 0;  // raise the opt-in once (graph-capture friendly)
-    if (smem > 48 * 1024 && smem > configured) {
+    static size_t configured[SG_MAX_DEVICES] = {};  // raise the opt-in once per device (graph-capture friendly)
+    if (optin_needed(configured, smem))
       cudaFuncSetAttribute(k_step_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      configured = smem;
-    }
     launch_pdl(k_step_finish, dim3(1), dim3(FINISH_THREADS), smem, s, *net, a);  // staging overlaps the sweep
     return check_launch("sg_step_finish");
   }

@@ -309,6 +309,67 @@ __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs
   return zs;
 }
 
+// The minibatch's range check (sampler.py:429-430) spread over the whole
+// grid, one 16-byte load per thread and row at a time (no divisions): int8
+// rows (-1 = missing; bytes compared as signed SIMD lanes against card - 1)
+// or packed .sgb rows (nib = 4 / 2 bits per case, all-ones = missing).
+// Sets SG_ERR_STATE_RANGE.
+__device__ __forceinline__ uint32_t packed_invalid(uint32_t w, int card, int nib) {
+  if (nib == 2) {  // crumbs: 3 = missing; only 2 can be out of range (binary variables)
+    return card >= 3 ? 0u : ((w >> 1) & ~w & 0x55555555u);
+  }
+  const uint32_t lim = 0x01010101u * uint32_t(card - 1);  // nibbles: 15 = missing
+  const uint32_t xe = w & 0x0F0F0F0Fu, xo = (w >> 4) & 0x0F0F0F0Fu;
+  return (__vcmpgtu4(xe, lim) & ~__vcmpeq4(xe, 0x0F0F0F0Fu)) | (__vcmpgtu4(xo, lim) & ~__vcmpeq4(xo, 0x0F0F0F0Fu));
+}
+
+template <int NT>
+__device__ __forceinline__ void obs_range_check(const sg_small& sp, const int8_t* __restrict__ obs, int ld_obs,
+                                                int cases, int32_t* err, int nib) {
+  if (!obs || cases <= 0) return;
+  const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + threadIdx.x;
+  const int gthreads = gridDim.x * gridDim.y * NT;
+  const bool packed = nib == 4 || nib == 2;
+  const int per_word = packed ? 32 / nib : 4;  // cases per 32-bit word
+  const int words = (cases + per_word - 1) / per_word;
+  const int vecs = (words + 3) >> 2;
+  unsigned bad = 0;
+  for (int i = gtid; i < sp.n * vecs; i += gthreads) {
+    int v = 0, q = i;  // (row, vector): n <= 7 subtractions instead of a division
+    while (q >= vecs) {
+      q -= vecs;
+      ++v;
+    }
+    const int card = sp.card[v];
+    const uint4* row = reinterpret_cast<const uint4*>(obs + int64_t(v) * ld_obs);
+    const uint32_t lim = 0x01010101u * uint32_t(card - 1);
+    {
+      const uint4 x = __ldcs(row + q);
+      const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int first = (4 * q + k) * per_word;  // first case of this word
+        if (first >= cases) break;
+        uint32_t b = packed ? packed_invalid(wv[k], card, nib) : __vcmpgts4(wv[k], lim);
+        const int valid = cases - first;
+        if (valid < per_word) {  // the row's last word: cases past the minibatch do not count
+          const int field_bits = packed ? nib : 8;
+          if (packed && nib == 4) {  // planes: byte b of the even plane is case 2b, of the odd plane 2b + 1
+            uint32_t keep = 0;
+            for (int j = 0; j < valid; ++j) keep |= 0xFu << (4 * j);
+            const uint32_t we = wv[k] | ~keep;  // cases past `valid` read as missing (15)
+            b = packed_invalid(we, card, nib);
+          } else {
+            b &= valid * field_bits >= 32 ? 0xFFFFFFFFu : ((1u << (valid * field_bits)) - 1u);
+          }
+        }
+        bad |= b;
+      }
+    }
+  }
+  if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
+}
+
 // The common end of both packed sweeps: ZeroSupport word, the minibatch's
 // range check (sampler.py:429-430) spread over the whole grid, and the
 // joint-state histogram (per-thread byte counters, hist8[J * NT + slot])
@@ -322,54 +383,7 @@ __device__ __forceinline__ void small_epilogue(const sg_small& sp, bool zs, cons
                                                int32_t* err, int nib = 0) {
   const int tid = threadIdx.x;
   if (zs) atomicOr(err, int(SG_ERR_ZERO_SUPPORT));
-  if (obs && (nib == 4 || nib == 2)) {  // packed observations (io.py .sgb): 8/nib cases per byte, all-ones = missing
-    const int per_byte = 8 / nib;
-    const int chunk_cases = 16 * per_byte;
-    const uint32_t fmask = nib == 4 ? 0x0F0F0F0Fu : 0x03030303u;
-    const int chunks = (cases + chunk_cases - 1) / chunk_cases;
-    const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + tid;
-    const int gthreads = gridDim.x * gridDim.y * NT;
-    unsigned bad = 0;
-    for (int i = gtid; i < sp.n * chunks; i += gthreads) {
-      const int v = i / chunks, ch = i - v * chunks;
-      const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
-      const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
-      const uint32_t wv[4] = {uint32_t(qv.x), uint32_t(qv.y), uint32_t(qv.z), uint32_t(qv.w)};
-      const int left = cases - ch * chunk_cases;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        for (int h = 0; h < per_byte; ++h) {  // field h of byte b = case (4k + b) * per_byte + h
-          const uint32_t x = (wv[k] >> (nib * h)) & fmask;
-          uint32_t gt = __vcmpgtu4(x, lim) & ~__vcmpeq4(x, fmask);
-#pragma unroll
-          for (int b2 = 0; b2 < 4; ++b2)
-            if ((4 * k + b2) * per_byte + h >= left) gt &= ~(0xFFu << (8 * b2));
-          bad |= gt;
-        }
-      }
-    }
-    if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
-  } else if (obs) {  // the minibatch's range check (sampler.py:429-430), spread over the whole grid
-    const int chunks = (cases + 15) >> 4;
-    const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + tid;
-    const int gthreads = gridDim.x * gridDim.y * NT;
-    unsigned bad = 0;
-    for (int i = gtid; i < sp.n * chunks; i += gthreads) {
-      const int v = i / chunks, ch = i - v * chunks;
-      const uint32_t lim = 0x01010101u * uint32_t(sp.card[v] - 1);
-      const int4 qv = __ldcs(reinterpret_cast<const int4*>(obs + int64_t(v) * ld_obs + ch * 16));
-      const uint32_t wv[4] = {uint32_t(qv.x), uint32_t(qv.y), uint32_t(qv.z), uint32_t(qv.w)};
-      const int left = cases - ch * 16;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint32_t gt = __vcmpgts4(wv[k], lim);
-        const int valid = left - 4 * k;
-        if (valid < 4) gt &= valid <= 0 ? 0u : (0xFFFFFFFFu >> (8 * (4 - valid)));
-        bad |= gt;
-      }
-    }
-    if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
-  }
+  obs_range_check<NT>(sp, obs, ld_obs, cases, err, nib);
   if (!counts) return;
   __syncthreads();
   const int warp = tid >> 5, lane_id = tid & 31;
@@ -386,6 +400,7 @@ __device__ __forceinline__ void small_epilogue(const sg_small& sp, bool zs, cons
   for (int cell = tid; cell < cells; cell += NT)
     if (cellacc[cell]) atomicAdd(counts + cell, (unsigned long long)cellacc[cell]);
 }
+
 
 // The sweep.  Grid (x: slot blocks, y: quad groups of QG quads).  A thread
 // owns the QG lane words of a slot (QG x 4 replicas of one case).
@@ -479,11 +494,9 @@ static void launch_small(const sg_small& sp, const SmallOrd& o, int groups, size
                          int lane_ld, int cases, int num_real, int m, int64_t case_base, uint64_t key,
                          const uint64_t* key_dev, const int32_t* jcell, int cells, uint64_t* counts,
                          const uint32_t* zs_flag, const int8_t* obs, int ld_obs, int32_t* err) {
-  static size_t configured = 0;  // raise the opt-in once (keeps graph capture free of attribute calls)
-  if (smem > configured) {
+  static size_t configured[SG_MAX_DEVICES] = {};  // once per device (keeps graph capture free of attribute calls)
+  if (optin_needed(configured, smem))
     cudaFuncSetAttribute(k_small_sweep<N, QG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
-  }
   // one wave over the quad groups (every CTA strides over the pattern-sorted
   // slots, so unit costs balance), but enough CTAs that no thread's byte
   // counters see more than 255 increments: <= 255 / (4 QG) slots per thread
@@ -531,13 +544,15 @@ static SmallOrd small_ord(const sg_small& sp) {
 //   K_P(S -> S') = prod_{v latent, colour order} p_v(S'_v | cur_v),
 //   cur_v = S with the fields of the variables drawn before v replaced by S'.
 //
-// k_joint_tables tabulates every row (P, S) of K as 2^B_P cumulative
-// thresholds (2^31 scale, same quantisation as the per-variable FAST
-// tables); the sweep draws one 31-bit uniform per lane and binary-searches
-// its row in shared memory.  Same transition kernel as the per-variable
-// sweep (up to the 2^-31 threshold quantisation), 1 uniform per lane
-// instead of one per latent variable, B_P dependent shared loads instead of
-// 4 table lookups per latent variable.  When any conditional has zero
+// k_joint_tables tabulates every row (P, S) of K as an alias table of 2^B_P
+// entries (joint_alias_row: integer column masses summing to 2^32); the
+// sweep draws one 32-bit uniform per lane and reads ONE entry of its row in
+// shared memory (column = top B_P bits, primary-or-alias on the rest) plus
+// the column's latent field bits.  Same transition kernel as the
+// per-variable sweep up to the 2^-32 quantisation of the row's cumulative
+// sums, 1 uniform per lane instead of one per latent variable, 2 dependent
+// shared loads instead of 4 table lookups per latent variable (or the
+// B_P-level binary search of a cumulative row).  When any conditional has zero
 // support (zs_flag armed) the kernel runs the per-variable path instead, so
 // ZeroSupport is detected exactly where the reference detects it.
 //
@@ -546,7 +561,7 @@ static SmallOrd small_ord(const sg_small& sp) {
 //   [0, NP)        byte offset of row 0 of pattern P
 //   [NP, 2NP)      B_P | keep_P << 8 | (byte offset of dep_P) << 16
 //   dep_P[j]       latent field bits of compact column j (pdep(j, latent mask))
-//   rows_P[S][j]   thresholds, 2^bits rows of 2^B_P words per pattern
+//   rows_P[S][j]   alias entries (primary << B_P | alias), 2^bits rows of 2^B_P + 1 words
 
 #ifndef SG_JOINT_THREADS
 #define SG_JOINT_THREADS 1024
@@ -579,48 +594,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// Row search: the byte address (shared window) of the first entry j with
-// u < row[j] (row[2^B - 1] is never read: the last column takes the
-// remaining mass).  One LDS with an immediate offset, one compare and one
-// predicated add per level.
-template <int H>
-__device__ __forceinline__ void joint_step(uint32_t& a, uint32_t u) {
-  uint32_t t;
-  asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(t) : "r"(a), "n"((H - 1) * 4));
-  asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}" : "+r"(a) : "r"(u), "r"(t), "n"(H * 4));
-  if constexpr (H > 1) joint_step<H / 2>(a, u);
-}
+// Alias draw from a row (joint_alias_row): column i = top B bits of the
+// 32-bit uniform; keep it when the low 32 - B bits are below its primary
+// mass, else take its alias.  One LDS of the entry, one of the column's
+// latent field bits (dep): two dependent shared loads per lane.
 template <int B>
-__device__ __forceinline__ uint32_t joint_search(uint32_t a, uint32_t u) {
-#ifdef SG_EXP_NOSEARCH  // timing experiment only: direct column, no search (wrong results)
-  return a + ((u >> (31 - B)) << 2);
-#else
-  joint_step<1 << (B - 1)>(a, u);
-  return a;
-#endif
+__device__ __forceinline__ uint32_t joint_alias_col(uint32_t row, uint32_t u) {
+  const uint32_t i = u >> (32 - B);
+  uint32_t e;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(row + (i << 2)));
+  const uint32_t f = u << B;                 // the low 32 - B bits, left-aligned
+  const uint32_t thr = e & ~((1u << B) - 1u);  // primary << B
+  return f < thr ? i : (e & ((1u << B) - 1u));
 }
 
-// The QG quads of one slot: per lane one uniform (word j of the quad's
-// Philox block), one row search, one dep lookup.  Straight-line over all
-// 4 x QG lanes (no per-lane branches) so the compiler interleaves the
-// independent search chains; lanes past m and alias quads compute garbage
-// that is never stored or tallied.  row0 / dep0: shared-window addresses.
+// The QG quads of one slot: per lane one 32-bit uniform (word j of the
+// quad's Philox block), one alias draw, one dep lookup.  Straight-line over
+// all 4 x QG lanes (no per-lane branches) so the compiler interleaves the
+// independent chains; lanes past m and alias quads compute garbage that is
+// never stored or tallied.  row0 / dep0: shared-window addresses.
 template <int B, int QG, int NL>
 __device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[QG], uint32_t row0, uint32_t dep0,
                                             uint32_t keep) {
   constexpr uint32_t kRowBytes = ((1u << B) + 1u) * 4u;  // rows 2^B + 1 words apart
 #pragma unroll
   for (int g = 0; g < QG; ++g) {
-    const uint32_t u[4] = {r[g].a >> 1, r[g].b >> 1, r[g].c >> 1, r[g].d >> 1};
+    const uint32_t u[4] = {r[g].a, r[g].b, r[g].c, r[g].d};
     uint32_t xs[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (g == QG - 1 && j >= NL) continue;  // compile time: lanes past m in the last quad
       const uint32_t S = byte_of(w[g], j);
-      const uint32_t row = row0 + S * kRowBytes;
-      const uint32_t hit = joint_search<B>(row, u[j]);
+#ifdef SG_EXP_NOSEARCH  // timing experiment only: the column straight from the uniform (wrong results)
+      const uint32_t col = u[j] >> (32 - B);
+#else
+      const uint32_t col = joint_alias_col<B>(row0 + S * kRowBytes, u[j]);
+#endif
       uint32_t lat;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lat) : "r"(hit - row + dep0));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lat) : "r"(dep0 + (col << 2)));
       xs[j] = (S & keep) | lat;
     }
     w[g] = __byte_perm(__byte_perm(xs[0], xs[1], 0x0040), __byte_perm(xs[2], xs[3], 0x0040), 0x5410);
@@ -648,7 +659,11 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
 #pragma unroll
   for (int g = 0; g < QG; ++g)
     trash[g] = g < qs.last ? 0u : g == qs.last ? (0x40404040u & ~qs.last_valid) : 0x40404040u;
-  uint32_t* rows = lanes + qs.row0;
+  // word offset of each quad's row (alias quads read the last real one): 32-bit
+  // indices, so every access is one add + one IMAD.WIDE.U32
+  uint32_t roff[QG];
+#pragma unroll
+  for (int g = 0; g < QG; ++g) roff[g] = qs.row0 + uint32_t(min(g, qs.last)) * qs.ld;
   for (; s < cases; s += stride) {
     uint32_t w[QG];
 #pragma unroll
@@ -657,10 +672,11 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
     const int c = nc;
     const int sn = s + stride;
     if (sn < cases) {  // prefetch the next slot while this one computes
+      const uint32_t usn = uint32_t(sn);
 #pragma unroll
-      for (int g = 0; g < QG; ++g) nw[g] = rows[min(g, qs.last) * qs.ld + sn];
-      nP = pattern[sn];
-      nc = case_id[sn];
+      for (int g = 0; g < QG; ++g) nw[g] = lanes[roff[g] + usn];
+      nP = pattern[usn];
+      nc = case_id[usn];
     }
     const uint32_t meta = info[np + P];
     const int B = int(meta & 0xFFu);
@@ -692,7 +708,7 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
 #pragma unroll
     for (int g = 0; g < QG; ++g) {
       const uint32_t wg = w[g] & (g < qs.last ? 0xFFFFFFFFu : qs.last_valid);
-      if (g <= qs.last) rows[g * qs.ld + s] = wg;
+      if (g <= qs.last) lanes[roff[g] + uint32_t(s)] = wg;
       if (counts) {
         // padded cases (c >= num_real) and alias quads (g > last): every lane to the trash
         // bin 64 (OR-ing 0x40 into a lane word would index bins 64..127, past this warp's 65)
@@ -794,6 +810,9 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   const int slot = ((tid & 31) << 2) | ((tid >> 5) & 3) | ((tid >> 7) << 7);
   const uint32_t hist_a = smem_u32(hist8) + uint32_t(tid >> 5) * kJointBins * 4u;  // this warp's bins
   const FastKey fk = fast_key(key_dev ? *key_dev : key);
+  // the minibatch's range check while the blob is in flight (no kernel of this
+  // step writes the observation block)
+  obs_range_check<NT>(sp, obs, ld_obs, cases, err, obs_nib);
   __syncthreads();
   mbar_wait(bar, 0);
   bool zs = false;
@@ -808,7 +827,7 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
                            counts != nullptr, nw0, nP0, nc0);
   }
   // per-warp bins -> CPT cells (jcell) -> one global atomic per touched cell
-  small_epilogue<SG_SMALL_MAXV, NT>(sp, zs, hist8, cellacc, jcell, cells, nullptr, obs, ld_obs, cases, err, obs_nib);
+  small_epilogue<SG_SMALL_MAXV, NT>(sp, zs, hist8, cellacc, jcell, cells, nullptr, nullptr, 0, cases, err);
   if (!counts) return;
   __syncthreads();
   const uint32_t* wh = reinterpret_cast<const uint32_t*>(hist8);
@@ -844,6 +863,99 @@ __device__ __forceinline__ void tail_stamp(int) {}
 #endif
 
 #define SG_JOINT_TAB_SLICES 4
+#define SG_JOINT_ROW_WARPS (FINISH_THREADS / 32)
+
+// first index in a[0..n) with a[i] > v (a non-decreasing; n <= 64)
+__device__ __forceinline__ int upper_bound_u32(const uint32_t* a, int n, uint32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] > v) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+// first index in a[0..n) with a[i] >= v
+__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] >= v) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// One transition row as an alias table (one warp; K = 2^B columns, lane l
+// holds column l, or columns 2l, 2l+1 when K = 64).  Input: the inclusive fp64
+// cumulative sums of the row's products (c_own at the lane's first column,
+// c_hi at its second when `two`) and the row total.  Integer column masses
+// w_j = C_j - C_{j-1} with C_j = min(ceil(cum_j * 2^32 / total), 2^32) and
+// C_{K-1} = 2^32 sum to exactly 2^32; with T = 2^(32-B):
+//   light (w < T): deficit T - w; heavy (w > T): surplus w - T; full (w = T).
+// Lights in column order cover [D_{k-1}, D_k) of the deficit line, heavies
+// [E_{h-1}, E_h) of the surplus line (both end at the same total).
+//   light: primary w, alias = the heavy whose interval holds D_{k-1};
+//   heavy: X = first light end >= E_h; overshoot X - E_h > 0 -> primary
+//          T - overshoot, alias = the next heavy; else full;
+//   full:  primary everything (alias = itself).
+// Every column's probability is then exactly w_j / 2^32 (a draw picks column
+// u >> (32 - B), keeps it when (u mod T) < primary, else takes the alias).
+// Entry = primary << B | alias.  tests/fast_stream.py restates this rule.
+__device__ __forceinline__ void joint_alias_row(uint32_t* row, int B, bool two, int lane, double c_own, double c_hi,
+                                                double total, uint32_t* sd, uint32_t* se) {
+  const int K = 1 << B;
+  const uint64_t ONE = 1ull << 32;
+  const uint64_t T = ONE >> B;
+  const double sc = total > 0.0 ? __ddiv_rn(4294967296.0, total) : 0.0;
+  auto quant = [&](double c, int j) -> uint64_t {
+    if (j >= K - 1) return ONE;
+    return uint64_t(fmin(ceil(__dmul_rn(c, sc)), 4294967296.0));
+  };
+  const int j0 = two ? 2 * lane : lane;
+  const bool act = j0 < K;
+  const uint64_t C0 = act ? quant(c_own, j0) : ONE;
+  const uint64_t C1 = two ? quant(c_hi, j0 + 1) : C0;
+  const uint64_t up = __shfl_up_sync(0xffffffffu, C1, 1);
+  const uint64_t prev = lane ? up : 0ull;
+  const uint64_t w0 = act ? C0 - prev : T;
+  const uint64_t w1 = two ? C1 - C0 : T;
+  const uint32_t d0 = w0 < T ? uint32_t(T - w0) : 0u, d1 = w1 < T ? uint32_t(T - w1) : 0u;
+  const uint32_t e0 = w0 > T ? uint32_t(w0 - T) : 0u, e1 = w1 > T ? uint32_t(w1 - T) : 0u;
+  // inclusive warp scans of the lane sums (every partial sum < 2^32)
+  uint32_t dl = d0 + d1, el = e0 + e1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t dy = __shfl_up_sync(0xffffffffu, dl, o), ey = __shfl_up_sync(0xffffffffu, el, o);
+    if (lane >= o) {
+      dl += dy;
+      el += ey;
+    }
+  }
+  const uint32_t D0 = dl - d1, E0 = el - e1;  // inclusive at the lane's first column
+  if (act) {
+    sd[j0] = D0;
+    se[j0] = E0;
+    if (two) {
+      sd[j0 + 1] = dl;
+      se[j0 + 1] = el;
+    }
+  }
+  __syncwarp();
+  auto entry = [&](int j, uint64_t w, uint32_t d, uint32_t Dinc, uint32_t Einc) -> uint32_t {
+    if (w < T) return (uint32_t(w) << B) | uint32_t(upper_bound_u32(se, K, Dinc - d));
+    if (w > T) {
+      const uint32_t X = sd[lower_bound_u32(sd, K, Einc)];
+      const uint32_t ov = X - Einc;
+      if (ov) return (uint32_t(T - ov) << B) | uint32_t(upper_bound_u32(se, K, Einc));
+    }
+    return uint32_t(j);
+  };
+  if (act) {
+    row[j0] = entry(j0, w0, d0, D0, E0);
+    if (two) row[j0 + 1] = entry(j0 + 1, w1, d1, dl, el);
+  }
+  if (lane == 0) row[K] = 0u;  // stride padding
+  __syncwarp();
+}
 // Slice `slice` (lane words S in [slice * R/4, (slice+1) * R/4)) of pattern
 // P's rows.  vprob_g: the step tail's conditionals [n][R][4] (L2-coherent
 // loads: written by another CTA of the same grid in the merged tail), or
@@ -857,6 +969,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
   // indices (a caller runs it early); 2: everything but that (part 1 ran
   // before).  pidx: [rows_per][K][SG_SMALL_MAXV] u16, 0xFFFF = zero entry.
   __shared__ uint32_t lv[SG_SMALL_MAXV][4];  // latent variables of P in colour order: off|width<<8|card<<16, mbmask, fm, v
+  __shared__ uint32_t alias_sd[SG_JOINT_ROW_WARPS][64], alias_se[SG_JOINT_ROW_WARPS][64];  // per-warp alias scans
   __shared__ int nlat;
   const int tid = threadIdx.x, nt = blockDim.x;
   const uint32_t meta = jblob[jp.patterns + P];  // static header
@@ -983,14 +1096,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
     const double left = __shfl_up_sync(0xffffffffu, x, 1);
     const double total = __shfl_sync(0xffffffffu, x, two ? 31 : K - 1);
     const double c0 = two ? (lane ? __dadd_rn(left, a) : a) : x;
-    const double sc = total > 0.0 ? __ddiv_rn(2147483648.0, total) : 0.0;
-    auto thr = [&](double c, int j) -> uint32_t {
-      return (sc > 0.0 && j != K - 1) ? uint32_t(fmin(ceil(__dmul_rn(c, sc)), 2147483648.0)) : 0x80000000u;
-    };
-    uint32_t* row = rows + S * KS;
-    if (j0 < K) row[j0] = thr(c0, j0);
-    if (two) row[j0 + 1] = thr(x, j0 + 1);
-    if (lane == 0) row[K] = 0x80000000u;  // stride padding
+    joint_alias_row(rows + S * KS, B, two, lane, j0 < K ? c0 : 0.0, x, total, alias_sd[warp], alias_se[warp]);
   }
 }
 
@@ -1075,8 +1181,8 @@ __device__ __forceinline__ void joint_cond_apply(const sg_net& net, const sg_sma
 // Rows of pattern P = blockIdx.x, lane words of slice blockIdx.y, from the
 // current CPTs (see the blob comment).  fp64 in a fixed order, no FMA:
 // p_v = w / norm with the reference's weight product (conditional_weights)
-// and sequential norm; products in colour order; sequential row sums;
-// thresholds min(ceil(cum * (2^31 / total)), 2^31).
+// and sequential norm; products in colour order; warp-scan row sums;
+// alias entries from min(ceil(cum * (2^32 / total)), 2^32) (joint_alias_row).
 __global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg_small sp, const sg_joint jp,
                                                       const double* cpt, const double* vprob_g, uint32_t* jblob) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1353,13 +1459,12 @@ static void launch_joint(const sg_small& sp, const SmallOrd& o, const sg_joint& 
                          int64_t case_base, uint64_t key, const uint64_t* key_dev, const int32_t* jcell, int cells,
                          uint64_t* counts, const uint32_t* zs_flag, const int8_t* obs, int ld_obs, int obs_nib,
                          int32_t* err) {
-  static size_t configured = 0;
-  if (smem > configured) {
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, smem)) {
     cudaFuncSetAttribute(k_joint_sweep<QG, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     // the step tail prefers the same carveout: no L1/shared reconfiguration between the two kernels
     cudaFuncSetAttribute(k_joint_sweep<QG, NL>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          int(cudaSharedmemCarveoutMaxShared));
-    configured = smem;
   }
   static int sms = 0;
   if (!sms) {
@@ -1402,11 +1507,9 @@ extern "C" int sg_joint_tables(const sg_net* net, const sg_small* sp, const sg_j
              "sg_joint_tables: bad plan (bits %d, patterns %d)", sp->bits, jp->patterns);
   SG_REQUIRE(net->max_mb <= SG_MAX_MB, "sg_joint_tables: Markov blanket too large");
   const size_t smem = joint_tables_smem(*sp, jp->max_b);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, smem))
     cudaFuncSetAttribute(k_joint_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
-  }
   launch_pdl(k_joint_tables, dim3(jp->patterns, SG_JOINT_TAB_SLICES), dim3(256), smem, (cudaStream_t)stream, *net, *sp, *jp, cpt, vprob,
              jblob);
   return check_launch("sg_joint_tables");
@@ -1510,14 +1613,13 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
                             (((size_t(sp->n) << sp->bits) + 15) & ~size_t(15)) +
                             (size_t(1) << sp->bits) / SG_JOINT_TAB_SLICES * (size_t(1) << jp->max_b) * SG_SMALL_MAXV * 2;
   const size_t smem = std::max(finish_smem(*net), slice_smem);
-  static size_t configured = 0;
-  if (smem > configured) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, smem)) {
+    // opted in at any size: dynamic + the static alias scratch may pass 48 KB
+    cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     // same carveout as k_joint_sweep (no L1/shared reconfiguration between sweep and tail)
     cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributePreferredSharedMemoryCarveout,
                          int(cudaSharedmemCarveoutMaxShared));
-    configured = smem;
   }
   const dim3 grid(1 + jp->patterns * SG_JOINT_TAB_SLICES);
   launch_pdl(k_step_tail_joint, grid, dim3(FINISH_THREADS), smem, (cudaStream_t)stream, *net, a, *sp, *jp, jblob,

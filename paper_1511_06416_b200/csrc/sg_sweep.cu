@@ -660,11 +660,9 @@ __global__ void __launch_bounds__(LANE_T) k_sweep_lane(const sg_net net, const s
 template <int MODE, int BITS>
 static void launch_lane(const sg_net& net, const sg_batch& bt, const SweepArgs& a, cudaStream_t s) {
   const size_t smem = lane_smem<BITS>(net.n);
-  static size_t configured = 0;
-  if (smem > configured) {
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, smem))
     cudaFuncSetAttribute(k_sweep_lane<MODE, BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
-  }
   const int g = std::min(bt.m, 32), cases_per_cta = (LANE_T / 32) * (32 / g);
   const dim3 grid((bt.cases + cases_per_cta - 1) / cases_per_cta, (bt.m + g - 1) / g);
   k_sweep_lane<MODE, BITS><<<grid, LANE_T, smem, s>>>(net, bt, a);
@@ -879,11 +877,10 @@ k_tally_chunked(const sg_net net, const sg_batch bt, unsigned long long* __restr
 static int tally_chunked(const sg_net& net, const sg_batch& bt, uint64_t* counts, cudaStream_t s) {
   const int quads = (bt.num_real + 3) / 4;
   if (quads == 0 || net.tally_chunks == 0) return SG_OK;
-  static bool configured = false;
-  if (!configured) {
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, SG_TALLY_CHUNK_CELLS * 4)) {
     cudaFuncSetAttribute(k_tally_chunked<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SG_TALLY_CHUNK_CELLS * 4);
     cudaFuncSetAttribute(k_tally_chunked<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SG_TALLY_CHUNK_CELLS * 4);
-    configured = true;
   }
   // 16-case units when every row is 16-byte aligned (pitch % 16 == 0 is part
   // of the sg_batch contract), else 4-case quads
@@ -940,11 +937,9 @@ static int choose_tile(const sg_net& net, int m, int cases, const SweepArgs& a, 
 template <int MODE, bool SMALL>
 static void launch_sweep(const sg_net& net, const sg_batch& bt, const SweepArgs& a, dim3 blocks, size_t smem,
                          cudaStream_t s) {
-  static size_t configured = 0;  // raise the opt-in once per instantiation (graph-capture friendly)
-  if (smem > configured) {
+  static size_t configured[SG_MAX_DEVICES] = {};  // once per instantiation and device (graph-capture friendly)
+  if (optin_needed(configured, smem))
     cudaFuncSetAttribute(k_sweep<MODE, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
-  }
   k_sweep<MODE, SMALL><<<blocks, SG_THREADS, smem, s>>>(net, bt, a);
 }
 

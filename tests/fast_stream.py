@@ -170,22 +170,67 @@ def joint_tables(onet, cpts, order):
                     cur[v] = a[v]
                 prods.append(p)
             cum = warp_scan(np.asarray(prods, dtype=np.float64))
-            c = float(cum[-1])
-            scale = 2147483648.0 / c if c > 0.0 else 0.0
-            for j in range(K):
-                if scale > 0.0 and j < K - 1:
-                    rows[S, j] = int(min(math.ceil(cum[j] * scale), 2147483648.0))
-                else:
-                    rows[S, j] = 0x80000000
+            rows[S] = alias_row(cum, B)
         out[P] = (B, keep, np.asarray(dep, dtype=np.int64), rows)
     return out
 
 
+def alias_row(cum, B):
+    """Alias entries of one row (csrc joint_alias_row): integer masses
+    w_j = C_j - C_{j-1}, C_j = min(ceil(cum_j * 2^32 / total), 2^32), C_{K-1} = 2^32;
+    T = 2^(32-B); lights (w < T) and heavies (w > T) laid out in column order
+    on a deficit and a surplus line; light: primary w, alias = the heavy whose
+    surplus interval holds the light's start; heavy: overshoot = first light
+    end >= its end E_h, minus E_h; primary T - overshoot and alias = next heavy
+    when the overshoot is positive, else full; full columns alias themselves.
+    Entry = primary << B | alias."""
+    import math
+
+    K = 1 << B
+    total = float(cum[-1])
+    sc = 4294967296.0 / total if total > 0.0 else 0.0
+    def quant(c):  # fmin(ceil(c * sc), 2^32) as the device rounds it (NaN / inf -> 2^32)
+        x = c * sc
+        return 4294967296 if (math.isnan(x) or x >= 4294967296.0) else math.ceil(x)
+
+    C = [quant(float(cum[j])) if j < K - 1 else 4294967296 for j in range(K)]
+    w = [C[j] - (C[j - 1] if j else 0) for j in range(K)]
+    T = 1 << (32 - B)
+    d = [T - x if x < T else 0 for x in w]
+    e = [x - T if x > T else 0 for x in w]
+    Dinc = np.cumsum(d).tolist()
+    Einc = np.cumsum(e).tolist()
+    out = np.zeros(K, dtype=np.uint32)
+    for j in range(K):
+        if w[j] < T:
+            alias = int(np.searchsorted(Einc, Dinc[j] - d[j], side="right"))
+            out[j] = (w[j] << B) | alias
+        elif w[j] > T:
+            X = Dinc[int(np.searchsorted(Dinc, Einc[j], side="left"))]
+            ov = X - Einc[j]
+            out[j] = ((T - ov) << B) | int(np.searchsorted(Einc, Einc[j], side="right")) if ov else j
+        else:
+            out[j] = j
+    return out
+
+
+def alias_probs(entries, B):
+    """Column probabilities an alias row encodes (x 2^32, exact integers)."""
+    K = 1 << B
+    T = 1 << (32 - B)
+    p = [0] * K
+    for i, e in enumerate(int(x) for x in entries):
+        thr, al = e >> B, e & (K - 1)
+        p[i] += thr
+        p[al] += T - thr
+    return p
+
+
 def joint_sweep(tabs, cards, lanes_in, latent, key, case_base=0):
     """One joint sweep of generic lane states (n, m, cases) with latent mask
-    (n, cases): lane (r, c) draws word r % 4 of the FAST block (case, 0,
-    quad r // 4, purpose 2) >> 1 and takes the first column j whose threshold
-    exceeds it (the last column otherwise)."""
+    (n, cases): lane (r, c) draws word u = r % 4 of the FAST block (case, 0,
+    quad r // 4, purpose 2) and reads entry i = u >> (32 - B) of its alias
+    row: column i when (u mod 2^(32-B)) < the entry's primary, else its alias."""
     width, off = lane_fields(cards)
     n, m, cases = lanes_in.shape
     S = np.zeros((m, cases), dtype=np.int64)
@@ -197,14 +242,16 @@ def joint_sweep(tabs, cards, lanes_in, latent, key, case_base=0):
     gc = np.arange(cases, dtype=np.uint64) + np.uint64(case_base)
     out = S.copy()
     for r in range(m):
-        u = (fast_block(key, gc, 0, r >> 2, 2)[:, r & 3] >> np.uint32(1)).astype(np.int64)
+        u = fast_block(key, gc, 0, r >> 2, 2)[:, r & 3].astype(np.int64)
         for p in np.unique(P):
             if p == 0:
                 continue
             B, keep, dep, rows = tabs[int(p)]
             sel = np.flatnonzero(P == p)
-            t = rows[S[r, sel]][:, :-1].astype(np.int64)
-            j = (u[sel, None] >= t).sum(axis=1)
+            i = u[sel] >> (32 - B)
+            e = rows[S[r, sel], i].astype(np.int64)
+            f = u[sel] & ((1 << (32 - B)) - 1)
+            j = np.where(f < (e >> B), i, e & ((1 << B) - 1))
             out[r, sel] = (S[r, sel] & keep) | dep[j]
     res = np.zeros_like(lanes_in)
     for v in range(n):

@@ -3,7 +3,7 @@
 tests/fast_stream.py restates the joint tables (the colour-ordered product of
 the reference's full conditionals, sampler.py:217-284, tabulated per latent
 pattern and lane word) and the draw (one FAST Philox word per lane, first
-threshold above it).  The device must match both bit for bit: the blob rows
+alias entry of its row, csrc joint_alias_row).  The device must match both bit for bit: the blob rows
 after every CPT update, the lane states after a sweep, and the count tables
 (the tally of the new states, model.py:148-165).
 """
@@ -33,7 +33,7 @@ def _blob_rows(eng, P):
     off = int(head[P]) // 4
     R, K = 1 << eng.pack.small.bits, 1 << B
     rows = blob[off:off + R * (K + 1)].reshape(R, K + 1)  # odd row stride: one padding word
-    assert np.all(rows[:, K] == 0x80000000)
+    assert np.all(rows[:, K] == 0)
     return rows[:, :K]
 
 
@@ -217,7 +217,7 @@ def test_joint_graph_with_4bit_uploads_equals_eager(koller, bits):
     for p in range(5):
         a.visit(mb, p, m)
     b.visit(mb, 0, m)
-    g = StepGraphs(b, mb, m, range(1, 6), obs_bits=bits)
+    g = StepGraphs(b, mb, m, range(1, 7), obs_bits=bits)
     pitch4 = g.obs_bufs[0].shape[1] * 8 // bits
     host = torch.empty(tuple(g.obs_bufs[0].shape), dtype=torch.uint8, pin_memory=True)
     host.copy_(torch.from_numpy(pack_bits(obs[:, :cases].cpu().numpy(), pitch4, bits)))
@@ -229,6 +229,14 @@ def test_joint_graph_with_4bit_uploads_equals_eager(koller, bits):
     np.testing.assert_array_equal(a.cpt.cpu().numpy(), b.cpt.cpu().numpy())
     np.testing.assert_array_equal(a.lane_states(0)[:, :, :cases].cpu().numpy(),
                                   b.lane_states(0)[:, :, :cases].cpu().numpy())
+    # a bad state in the padding past the last case is not part of the minibatch
+    pad = np.full((obs.shape[0], cases + 7), -1, dtype=np.int64)
+    pad[:, :cases] = obs[:, :cases].cpu().numpy()
+    pad[0, cases:] = 2
+    host.copy_(torch.from_numpy(pack_bits(pad, pitch4, bits)))
+    g.step(hmb)
+    torch.cuda.synchronize()
+    assert b.err.read() == 0
     bad = obs[:, :cases].cpu().numpy().copy()
     bad[0, cases - 1] = 2  # variable 0 has 2 states (2 is representable in 2 and 4 bits)
     host.copy_(torch.from_numpy(pack_bits(bad, pitch4, bits)))

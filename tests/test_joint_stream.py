@@ -5,7 +5,7 @@ The joint sweep replaces the per-variable draws of one sweep by one draw from
 the sweep's transition kernel K.  K must be the composition of the
 reference's per-variable Gibbs kernels (sampler.py:217-284), so the
 posterior of the latent fields given the observed ones is stationary under
-it: pi K = pi.  The thresholds quantise K to 2^-31.
+it: pi K = pi.  The alias rows quantise K to 2^-32.
 """
 
 import itertools
@@ -18,9 +18,8 @@ import oracle as O
 
 
 def _kernel(rows):
-    t = rows.astype(np.float64) / 2.0 ** 31
-    t[:, -1] = 1.0
-    return np.diff(np.concatenate([np.zeros((t.shape[0], 1)), t], axis=1), axis=1)
+    B = int(rows.shape[1]).bit_length() - 1
+    return np.asarray([F.alias_probs(r, B) for r in rows], dtype=np.float64) / 2.0 ** 32
 
 
 def _posterior(onet, cpts, P, obs_word, width, off, dep, keep):
@@ -141,3 +140,32 @@ def test_joint_rng_needs_a_joint_plan():
     assert cfg.rng == "joint"
     with pytest.raises(ValueError):
         sg.SamplerConfig(rng="bogus")
+
+
+@pytest.mark.parametrize("B", [1, 2, 3, 5, 6])
+def test_alias_rows_encode_the_quantised_masses_exactly(B):
+    """alias_row (the restatement of csrc joint_alias_row): the column masses the
+    entries encode are exactly w_j = C_j - C_{j-1} (C = the 2^32-scaled ceil of
+    the cumulative sums), for random, sparse, single-column and uniform rows."""
+    import math
+
+    rng = np.random.default_rng(B)
+    K = 1 << B
+    rows = [rng.random(K), rng.random(K) ** 8, np.eye(K)[0], np.eye(K)[K - 1], np.ones(K),
+            np.where(rng.random(K) < 0.5, 0.0, rng.random(K)), np.full(K, 1e-300)]
+    for p in rows:
+        if p.sum() == 0:
+            p[0] = 1.0
+        cum = F.warp_scan(np.asarray(p, dtype=np.float64))
+        ent = F.alias_row(cum, B)
+        sc = 4294967296.0 / float(cum[-1])
+
+        def quant(c):
+            x = c * sc
+            return 4294967296 if (math.isnan(x) or x >= 4294967296.0) else math.ceil(x)
+
+        C = [quant(float(cum[j])) if j < K - 1 else 4294967296 for j in range(K)]
+        w = [C[j] - (C[j - 1] if j else 0) for j in range(K)]
+        assert F.alias_probs(ent, B) == w
+        assert sum(w) == 1 << 32
+        assert np.all((ent & (K - 1)) < K)

@@ -47,7 +47,7 @@ with torch.cuda.graph(g):
     _lib.call("sg_noop", sms - 1, 1024, 120 * 1024, s())
     _lib.call("sg_event_record", ev[1], s())
 p0 = 10
-for kind in ("torch", "sg", "none"):
+for kind in (sys.argv[2].split(",") if len(sys.argv) > 2 else ("torch", "sg", "none")):
     fl = []
     for k in range(20):
         flush(kind, k)
@@ -57,7 +57,7 @@ for kind in ("torch", "sg", "none"):
         _lib.call("sg_event_elapsed", ev[0], ev[1], ctypes.byref(ms))
         if k >= 3:
             fl.append(ms.value * 1e3)
-    tg = StepGraphs(eng, mb, 10, range(p0, p0 + 30), timing=True)
+    tg = StepGraphs(eng, mb, 10, range(p0, p0 + 30), timing=True, obs_bits=int(sys.argv[1]) if len(sys.argv) > 1 else 8)
     p0 += 40
     sw, st = [], []
     for k in range(30):
