@@ -159,14 +159,57 @@ def _oracle_worker(args):
     return times
 
 
+REF_DIR = ROOT / "oracle" / "_ref"  # the unmodified reference, installed by oracle/build_ref.sh
+
+
+def have_reference() -> bool:
+    return (REF_DIR / "samegibbs" / "__init__.py").exists()
+
+
+def _reference_worker(args):
+    """Time the UNMODIFIED reference's own ``samegibbs.run(threads=1)`` (oracle/_ref)
+    on a case slice of the workload: one pass = one minibatch visit (sweep +
+    tally + accumulator + Dirichlet update); per-pass times from its trace."""
+    key, cases, passes, slice_id = args
+    sys.path.insert(0, str(REF_DIR))
+    import samegibbs as R
+
+    wl = WORKLOADS[key]
+    onet, dense = wl.oracle_problem(cases, slice_id)  # the same data the port times (bit-exact generators)
+    net = R.build_network(list(onet.cards), [(p, c) for c in range(onet.n) for p in onet.parents[c]])
+    data = R.DataMatrix.from_dense(dense)
+    mode = "exponential" if key == "c5" else "moving_sum"
+    cfg = R.SamplerConfig(same_m=wl.m, minibatch_size=cases, num_passes=passes, seed=300, accumulator_mode=mode,
+                          exp_decay=0.9 if mode == "exponential" else 1.0)
+    _, trace = R.run(net, data, cfg, threads=1)
+    secs = [r.seconds for r in trace.records]
+    return [b - a for a, b in zip([0.0] + secs[:-1], secs)]
+
+
+def _cpu_times(key, cases, steps, slice_id):
+    if have_reference():
+        return _reference_worker((key, cases, steps, slice_id)), "reference"
+    return _oracle_worker((key, cases, steps, 0, slice_id)), "port"
+
+
 def cpu_baseline(wl: Workload, n_vars: int, budget_s: float = 12.0) -> dict:
-    """Single-core oracle on a case slice of the workload (rank 0, N=1)."""
+    """Single core, rank 0, N=1: the reference's own run() (oracle/_ref) on a case
+    slice of the workload, else the oracle port."""
     cases = wl.cpu_cases
-    times = _oracle_worker((wl.key, cases, 1000, budget_s, 0))
+    # about budget_s of CPU time at ~1e7 node-samples/s
+    passes = int(max(4, min(40, budget_s * 1e7 / (n_vars * cases * wl.m))))
+    times, kind = _cpu_times(wl.key, cases, passes, 0)
     per = statistics.median(times[1:] if len(times) > 2 else times)
-    return {"value": n_vars * cases * wl.m / per, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"oracle (NumPy restatement of samegibbs) single process, {cases}-case slice x m={wl.m}, "
-                      f"{len(times)} steps of sweep+tally+moving-sum+Dirichlet, median step {per * 1e3:.1f} ms"}
+    what = ("samegibbs.run(threads=1) of the unmodified reference (oracle/_ref)" if kind == "reference" else
+            "oracle (NumPy restatement of samegibbs), sweep+tally+moving-sum+Dirichlet per step")
+    return {"value": n_vars * cases * wl.m / per, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{what}, single process, {cases}-case slice x m={wl.m}, {len(times)} passes of one "
+                      f"minibatch, median pass {per * 1e3:.1f} ms"}
+
+
+def _arm_worker(args):
+    key, cases, steps, slice_id = args
+    return _cpu_times(key, cases, steps, slice_id)[0]
 
 
 def reference_arm(args, wl: Workload) -> None:
@@ -178,26 +221,29 @@ def reference_arm(args, wl: Workload) -> None:
     n_vars = wl.network()[0].num_vars
     procs = max(1, min(os.cpu_count() or 1, 64))
     total_steps = args.steps + args.warmup
-    # bound the run to roughly a minute of CPU time per process (~1.2e7 node-samples/s per core)
-    cases = int(min(wl.cpu_cases, max(1_000, 60.0 / total_steps * 12e6 / (n_vars * wl.m))) // 500 * 500)
+    # bound the run to roughly a minute of CPU time per process (~1e7 node-samples/s per core)
+    cases = int(min(wl.cpu_cases, max(1_000, 60.0 / total_steps * 1e7 / (n_vars * wl.m))) // 500 * 500)
     cases = max(cases, 500)
+    kind = "reference" if have_reference() else "port"
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(procs) as pool:
-        res = pool.map(_oracle_worker, [(wl.key, cases, total_steps, 0, i) for i in range(procs)])
+        res = pool.map(_arm_worker, [(wl.key, cases, total_steps, i) for i in range(procs)])
     wall = time.perf_counter() - t0
     timed = [r[args.warmup:] for r in res]
     per_step = max(sum(t) for t in timed) / max(1, args.steps)  # slowest worker bounds the aggregate
     value = procs * n_vars * cases * wl.m / per_step
+    what = ("the unmodified reference's samegibbs.run(threads=1) (oracle/_ref, built by oracle/build_ref.sh)"
+            if kind == "reference" else "the oracle port (NumPy restatement)")
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": wl.config(args.gpus, "numpy", n_vars),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{procs} independent single-threaded oracle processes, each on its own "
-                                   f"{cases}-case slice x m={wl.m} (aggregate upper bound; the reference's own "
-                                   f"threads knob does not scale), wall {wall:.1f} s"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": kind,
+                         "sample": f"{procs} independent single-threaded processes of {what}, each on its own "
+                                   f"{cases}-case slice x m={wl.m}, one minibatch visit per step (aggregate upper "
+                                   f"bound; the reference's own threads knob does not scale), wall {wall:.1f} s"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
