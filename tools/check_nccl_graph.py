@@ -41,7 +41,23 @@ t = b.cpt.clone()
 dist.broadcast(t, 0)
 same = bool(torch.equal(t, b.cpt))
 tot = a.prev_counts[0].sum().item()
+# run(): the capturable NCCL hook (parallel.count_allreduce) lets Engine.run replay its
+# steady-state visits as graphs with the all-reduce inside; equal to eager visits
+from paper_1511_06416_b200 import parallel  # noqa: E402
+
+comm = parallel.count_allreduce()
+cfg2 = sg.SamplerConfig(same_m=m, minibatch_size=cases // 2, num_passes=4, seed=301, rng="joint")
+res = []
+for graphs in (False, True):
+    eng = Engine(net, cfg2, case_base=rank * cases, comm=comm)
+    eng.graph_replay = graphs
+    cp, _ = eng.run(sg.DeviceSource(obs, cases, cases // 2))
+    res.append(cp)
+    if graphs:
+        used = eng.graphs_ok()
+run_ok = all(np.array_equal(x, y) for x, y in zip(res[0].tables, res[1].tables))
 if rank == 0:
-    print("OK" if ok and same else "MISMATCH", "graph==eager", ok, "ranks agree", same,
-          "count mass", tot, "expected", net.num_vars * m * cases * world)
+    print("OK" if ok and same and run_ok and used else "MISMATCH", "graph==eager", ok, "ranks agree", same,
+          "run graphs==eager", run_ok, "graphs used", used, "count mass", tot, "expected",
+          net.num_vars * m * cases * world, flush=True)
 dist.destroy_process_group()
