@@ -16,8 +16,9 @@ generated on the device.  node-samples per step = n_vars x cases x m
 ``--workload c3`` (MOOC-shaped, 334 variables, 131,010 cases, m = 5) and
 ``c4`` (random DAG, 1000 nodes, 1.25M cases per GPU = 10M over 8, m = 1, 30%
 missing) measure the generic kernel on the other BASELINE shapes; ``c5``
-streams minibatches of the 1000-node network from pinned host memory
-(HostSource, copy stream one block ahead), m = 20, exponential accumulator.
+streams a 10^7-case 4-bit .sgb file of the 1000-node network per GPU
+(BinaryFileSource: disk -> pinned -> device one block ahead), m = 20,
+exponential accumulator, one full pass timed.
 C2 is the headline line.
 
 Timing: per-step CUDA events on the launching stream, L2 flushed (256 MB
@@ -120,11 +121,10 @@ WORKLOADS = {
     "c4": Workload("c4", "C4: random DAG, 1000 nodes, in-degree<=4, cards 2-4, 1.25M cases/GPU (10M over 8), "
                          "30% missing, SAME m=1, minibatch=shard, moving-sum, Dirichlet CPT update", 1_250_000, 1,
                    0.3, 4_000),
-    "c5": Workload("c5", "C5: out-of-core, random DAG 1000 nodes, 30% missing, SAME m=20, minibatches of 131,072 "
-                         "cases streamed from pinned host memory (8 host blocks = 1,048,576 cases per GPU, "
-                         "replayed), exponential accumulator, Dirichlet CPT update", 131_072, 20, 0.3, 500),
+    "c5": Workload("c5", "C5: out-of-core, random DAG 1000 nodes, 30% missing, SAME m=20, one pass over a 4-bit "
+                         ".sgb file of 10^7 cases per GPU (minibatches of 131,072 cases, disk -> pinned -> device), "
+                         "exponential accumulator, Dirichlet CPT update", 131_072, 20, 0.3, 500),
 }
-C5_HOST_BLOCKS = 8
 
 
 # ---------------------------------------------------------------- CPU oracle legs
@@ -625,7 +625,14 @@ def our_arm(args, wl: Workload) -> None:
 
 
 def stream_arm(args, wl: Workload) -> None:
-    """C5: minibatches streamed from pinned host memory through HostSource."""
+    """C5: a pass over an on-disk 4-bit .sgb file of ``--c5-cases`` cases per GPU
+    (default 10^7), streamed through BinaryFileSource: disk -> pinned buffer ->
+    device on a copy stream one minibatch ahead, decoded on the device.  The
+    timed region is the whole pass (every minibatch of the file, after a
+    separate warm-up pass over the first ``--warmup`` blocks); a step is one
+    minibatch visit."""
+    import tempfile
+
     import torch
     import torch.distributed as dist
 
@@ -636,64 +643,97 @@ def stream_arm(args, wl: Workload) -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1511_06416_b200 as sg
-    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200 import _lib, io
     from paper_1511_06416_b200.engine import Engine
 
     B, M = wl.cases, wl.m
-    host_cases = B * C5_HOST_BLOCKS
+    cases = int(args.c5_cases)
     net, truth = wl.network()
     n_vars = net.num_vars
-    obs = sg.forward_sample_device(net, truth, host_cases, seed=105, hide_fraction=0.3, mask_seed=205,
-                                   case_base=rank * host_cases)
-    latent = float((obs[:, :host_cases] < 0).float().mean())
-    steps = args.steps
-    cycle = (args.warmup + steps + C5_HOST_BLOCKS - 1) // C5_HOST_BLOCKS
-    src = sg.HostSource.from_dense(obs[:, :host_cases].cpu(), B, cycle=cycle)
-    del obs
+    base = rank * cases  # this rank's shard of the global data set
+    tmpdir = tempfile.mkdtemp(prefix="sg_c5_", dir=os.environ.get("SG_C5_DIR") or None)
+    path = os.path.join(tmpdir, f"c5_rank{rank}.sgb")
+    latent_cells = [0, 0]
+
+    def block(lo, hi):
+        obs = sg.forward_sample_device(net, truth, hi - lo, seed=105, hide_fraction=0.3, mask_seed=205,
+                                       case_base=base + lo)[:, :hi - lo]
+        latent_cells[0] += int((obs < 0).sum())
+        latent_cells[1] += obs.numel()
+        return obs
+
+    t_w = time.perf_counter()
+    io.write_binary_blocks(path, n_vars, cases, B, block, "nibble")
+    write_s = time.perf_counter() - t_w
+    latent = latent_cells[0] / max(1, latent_cells[1])
+    src = io.BinaryFileSource(path)
+    nblocks = (cases + B - 1) // B
     if args.rng == "auto":
         args.rng = "fast"  # DAG-1000: no packed lane word
     cfg = sg.SamplerConfig(same_m=M, minibatch_size=B, num_passes=1, seed=300, rng=args.rng,
                            accumulator_mode="exponential", exp_decay=0.9)
     comm = (lambda c: dist.all_reduce(c)) if world > 1 else None
-    eng = Engine(net, cfg, case_base=rank * host_cases, comm=comm)
-    it = iter(src)
-    for _ in range(args.warmup):
-        eng.visit(next(it), 0, M)
+    eng = Engine(net, cfg, case_base=base, comm=comm)
+    for k, mb in enumerate(src):  # warm-up: the first blocks of the file
+        if k >= args.warmup:
+            break
+        eng.visit(mb, 0, M)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    marks = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(nblocks + 1)]
     launches0 = _lib.launch_count
+    h0 = time.perf_counter()
     with ClockSampler(local) as clk:
         marks[0].record()
-        for k in range(steps):
-            mb = next(it)  # the stream waits for this block's host->device copy
-            eng.visit(mb, 0, M)
+        for k, mb in enumerate(src):  # the whole file: every step's block is read, uploaded and decoded
+            eng.visit(mb, 1, M)
             marks[k + 1].record()
         torch.cuda.synchronize()
+    wall = time.perf_counter() - h0
     launches = _lib.launch_count - launches0
     if eng.err.read():
         raise RuntimeError("device error word set")
-    ms = marks[0].elapsed_time(marks[steps]) / steps  # copy waits + visits, back to back
+    ms = marks[0].elapsed_time(marks[nblocks]) / nblocks  # reads + copies + visits, back to back
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
-    node_samples = n_vars * B * M
+    node_samples = n_vars * cases * M / nblocks  # per GPU per step (mean over the pass)
     value = world * node_samples / (ms * 1e-3)
+    h2d = n_vars * src.header["pitch"] // 2  # 4-bit block bytes per step
     if rank == 0:
+        try:
+            peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        except Exception:  # noqa: BLE001
+            peak = 6650.0
+        bpns = 1.0 + latent
+        hbm_gbs = bpns * node_samples / (ms * 1e-3) / 1e9
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": nblocks,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int8 states, u32 draws, f64 CPTs", "data": "synthetic",
             "config": dict(wl.config(world, args.rng, n_vars), latent_fraction=round(latent, 4),
-                           host_buffer_cases=host_cases, l2="inputs stream from host memory every step"),
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": n_vars * B, "d2h_bytes_per_step": 0,
-                    "note": "value is already end to end: every step's minibatch comes from pinned host memory"},
+                           cases_per_gpu=cases, file=f"4-bit .sgb, {os.path.getsize(path) / 1e9:.2f} GB per GPU",
+                           l2="inputs stream from disk / host memory every step"),
+            "roofline": {"bound": "hbm", "achieved": hbm_gbs, "peak": peak, "unit": "GB/s", "frac": hbm_gbs / peak,
+                         "traffic": None, "note": "whole step (sweep + tally + tail + decode), algorithmic bytes "
+                                                   "n x B x m x (1 + f) per step"},
+            "pcie": {"h2d_gbs": h2d / (ms * 1e-3) / 1e9, "h2d_bytes_per_step": h2d,
+                     "frac_of_50gbs": h2d / (ms * 1e-3) / 50e9},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 0,
+                    "note": "value is already end to end: every step's minibatch is read from the .sgb file, "
+                            "copied from pinned host memory and decoded on the device"},
             "gpu_launches": launches, "launch_mode": "eager, copy stream one minibatch ahead",
-            "kernel_path": "generic sg_sweep + chunked tally + step tail", "clocks": clk.summary(),
+            "kernel_path": "BinaryFileSource + sg_unpack_nibbles + generic big-tile sweep + chunked tally + step tail",
+            "file_write_s": round(write_s, 1), "pass_wall_s": round(wall, 2), "clocks": clk.summary(),
         }
         print(json.dumps(out))
+    try:
+        os.remove(path)
+        os.rmdir(tmpdir)
+    except OSError:
+        pass
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -710,6 +750,7 @@ def main() -> None:
                     help="auto: joint (one draw per lane per sweep) when the network's lane word fits, else fast")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch each visit eagerly instead of graph replay")
+    ap.add_argument("--c5-cases", type=int, default=10_000_000, help="C5: cases per GPU in the streamed .sgb file")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -446,7 +446,8 @@ int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_finish* f, vo
    derive the conditionals of their rows from the CPTs).  f->vprob, when not
    NULL, is scratch for an earlier hand-off: CTA 0 releases the cells' gamma
    draws and every slice normalises the CPT rows itself.  sync:
-   [dev] 2 uint32, zero before the first call; the kernel re-arms them. */
+   [dev] 4 uint32 (hand-off flag, finish count, role ticket, spare), zero
+   before the first call; the kernel re-arms them. */
 int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const sg_finish* f,
                        const sg_joint* jp, uint32_t* jblob, uint32_t* sync, void* stream);
 

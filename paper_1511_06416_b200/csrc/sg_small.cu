@@ -1199,29 +1199,36 @@ extern "C" int sg_debug_tail_finish_trace(unsigned long long* out) {  // this TU
 }
 #endif
 
-// The whole step tail of the joint path in ONE grid: CTA 0 runs the
-// single-CTA tail (accumulate, CPT update, packed tables, conditionals ->
-// f.vprob, count clearing, key advance) and releases `sync[0]`; CTAs 1.. wait
-// for it and build one slice of the joint rows each.  The last CTA to finish
-// re-arms the two sync words for the next step.  (Spinning is safe: CTA 0
-// needs one SM and the grid is far below the device's resident capacity.)
+// The whole step tail of the joint path in ONE grid.  Roles come from a
+// ticket (sync[2]): the first CTA to run takes role 0 and runs the single-CTA
+// tail (accumulate, CPT update, packed tables, count clearing, key advance),
+// releasing sync[0] once the slices can proceed; every later CTA takes the
+// next row slice and spins on sync[0].  The spinning CTAs therefore only ever
+// wait on a CTA that is already resident, whatever order or subset of CTAs
+// the hardware schedules first (no reliance on CTA 0 being dispatched first
+// or on co-residency of the whole grid).  The last slice to finish re-arms
+// the sync words for the next step.
 __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net gnet, const FinishArgs f,
                                                                     const sg_small sp, const sg_joint jp,
                                                                     uint32_t* jblob, uint32_t* sync) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_role;
+  if (threadIdx.x == 0) s_role = int(atomicAdd(sync + 2, 1u));
+  __syncthreads();
+  const int role = s_role;  // 0: the model update; r >= 1: row slice r - 1
 #ifdef SG_FINISH_TRACE
-  auto stamp = [](int k) {
+  auto stamp = [role](int k) {
     if (threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      g_tail_trace[blockIdx.x * 4 + k] = t;
+      g_tail_trace[role * 4 + k] = t;
     }
   };
 #else
   auto stamp = [](int) {};
 #endif
   stamp(0);
-  if (blockIdx.x == 0) {  // releases sync[0] as soon as the new CPTs are written (f.release_sync)
+  if (role == 0) {  // releases sync[0] as soon as the new CPTs are written (f.release_sync)
     step_finish_body(gnet, f, smem, FINISH_THREADS);
     stamp(1);
     return;
@@ -1244,7 +1251,7 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   int2* plan = reinterpret_cast<int2*>(work + size_t(nr) * 4 * sizeof(double));
   int8_t* plan_nf = reinterpret_cast<int8_t*>(plan + size_t(nr) * SG_JOINT_MAXF);
   uint16_t* pidx = reinterpret_cast<uint16_t*>(plan_nf + ((size_t(nr) + 15) & ~size_t(15)));
-  const int b = blockIdx.x - 1;
+  const int b = role - 1;
   const int P = b / SG_JOINT_TAB_SLICES;
   pdl_trigger();
   for (int i = tid; i < int(gnet.blob64_words); i += blockDim.x) b64[i] = __ldg(gnet.blob64 + i);
@@ -1296,6 +1303,7 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   if (threadIdx.x == 0 && atomicAdd(sync + 1, 1u) == gridDim.x - 2) {
     sync[1] = 0u;
     sync[0] = 0u;
+    sync[2] = 0u;  // every CTA has taken its ticket
   }
 }
 

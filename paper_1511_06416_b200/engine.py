@@ -129,7 +129,7 @@ class Engine:
             self.jblob = torch.from_numpy(blob.view(np.int32)).to(d)
             # full conditionals p_v(x | lane word), written by the step tail for sg_joint_tables
             self.vprob = torch.zeros(self.n * (4 << self.pack.small.bits), dtype=torch.float64, device=d)
-            self.jsync = torch.zeros(2, dtype=torch.int32, device=d)  # sg_step_tail_joint's hand-off words
+            self.jsync = torch.zeros(4, dtype=torch.int32, device=d)  # sg_step_tail_joint's hand-off + ticket words
         self.tables_fresh = False  # conditional tables reflect self.cpt
         self.graph_replay = True   # run(): replay steady-state visits as CUDA graphs
         self._latent_hint = None   # latent share of the first generic minibatch (sg_batch.latent_permille)

@@ -166,6 +166,49 @@ def write_binary(path, data, block_cases: int, encoding: str = "int8") -> None:
             f.write(blk.tobytes())
 
 
+def write_binary_blocks(path, num_vars: int, num_cases: int, block_cases: int, block_fn,
+                        encoding: str = "nibble") -> None:
+    """Stream an ``.sgb`` file block by block: ``block_fn(lo, hi)`` returns the
+    (num_vars, hi - lo) observations of cases [lo, hi) (-1 = missing; a host
+    array or a device tensor, packed on its own device).  Lets a generator
+    write files far larger than host memory (BASELINE C5)."""
+    import torch
+
+    if encoding not in _SGB_ENCODINGS:
+        raise ValueError(f"encoding must be one of {tuple(_SGB_ENCODINGS)}, got {encoding!r}")
+    if num_cases <= 0:
+        raise ValueError("no cases to write")
+    limit = {"int8": 128, "nibble": 15, "crumb": 3}[encoding]
+    pitch = max(64, (block_cases + 63) // 64 * 64)
+    nb = (num_cases + block_cases - 1) // block_cases
+    with open(path, "wb") as f:
+        head = _SGB_HEADER.pack(_SGB_MAGIC, 1, num_vars, num_cases, block_cases, pitch, _SGB_ENCODINGS[encoding])
+        f.write(head + bytes(64 - len(head)))
+        for b in range(nb):
+            lo, hi = b * block_cases, min(num_cases, (b + 1) * block_cases)
+            blk = block_fn(lo, hi)
+            if tuple(blk.shape) != (num_vars, hi - lo):
+                raise ValueError(f"block {b}: expected shape {(num_vars, hi - lo)}, got {tuple(blk.shape)}")
+            if isinstance(blk, torch.Tensor):
+                if int(blk.max()) >= limit or int(blk.min()) < -1:
+                    raise ValueError(f"states must lie in [-1, {limit - 1}] for the {encoding} encoding")
+                if encoding == "int8":
+                    out = torch.full((num_vars, pitch), -1, dtype=torch.int8, device=blk.device)
+                    out[:, :hi - lo] = blk
+                else:
+                    out = pack_bits(blk, pitch, 4 if encoding == "nibble" else 2)
+                f.write(out.cpu().numpy().tobytes())
+            else:
+                arr = np.asarray(blk)
+                if arr.max(initial=-1) >= limit or arr.min(initial=0) < -1:
+                    raise ValueError(f"states must lie in [-1, {limit - 1}] for the {encoding} encoding")
+                out = np.full((num_vars, pitch), -1, dtype=np.int8)
+                out[:, :hi - lo] = arr
+                if encoding != "int8":
+                    out = pack_bits(out, pitch, 4 if encoding == "nibble" else 2)
+                f.write(out.tobytes())
+
+
 def read_binary_header(path) -> dict:
     with open(path, "rb") as f:
         raw = f.read(64)
