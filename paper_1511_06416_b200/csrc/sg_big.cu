@@ -152,55 +152,53 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
           ioff = __ldg(a.inj_off + v);
         }
       }
+      const int rs = a.mg * wpr;  // words between variable rows of the tile (32-bit offsets throughout)
       for (int it = lane; it < total; it += 32) {
         const int c = wl[it];
         const int cw = c / PER, csh = (c % PER) * BITS;
         int64_t rank = 0;
         if (MODE != SG_RNG_FAST) rank = __ldg(bt.rank + int64_t(v) * bt.ld_rank + c0 + c);
-        // all replicas of this tile for (v, c), in global quads (one Philox block each)
-        const int q_lo = rg0 >> 2, q_hi = (rg0 + mg - 1) >> 2;
-        for (int rq = q_lo; rq <= q_hi; ++rq) {
-          u32x4 blk{0u, 0u, 0u, 0u};
-          if (MODE == SG_RNG_FAST) blk = fast_block(key, uint64_t(bt.case_base + c0 + c), uint32_t(v), uint32_t(rq), 0u);
-          for (int j = 0; j < 4; ++j) {
-            const int l = rq * 4 + j - rg0;  // local replica
-            if (l < 0 || l >= mg) continue;
-            const uint32_t* rowbase = st + size_t(l) * wpr + cw;  // + u * a.mg * wpr selects variable u
-            auto get = [&](int u) { return int((rowbase[size_t(u) * a.mg * wpr] >> csh) & MASK); };
-            double u01;
-            uint32_t u31 = 0;
-            if (MODE == SG_RNG_FAST) {
-              const uint32_t wv = pick(blk, j);
-              u31 = wv >> 1;
-              u01 = double(wv) * 0x1.0p-32;
-            } else {
-              const int64_t ui = int64_t(rg0 + l) * nmiss + rank;  // reference lane order (sampler.py:245)
-              u01 = MODE == SG_RNG_NUMPY ? np_uniform(uint64_t(ui), k0, k1) : __ldg(a.uniforms + ioff + ui);
-            }
-            int x = 0;
-            if (nmb >= 0) {  // conditional table of the blanket configuration
-              int e = 0;
-              for (int q = 0; q < nmb; ++q) e += get(dv[4 + q]) * dv[4 + SG_DESC_MB + q];
-              if (MODE == SG_RNG_FAST) {
-                const uint32_t* th = a.ftab + dv[2] + e * (card - 1);
-                const uint32_t t0 = __ldg(th);
-                if (zs_armed && t0 == 0xFFFFFFFFu) zs = true;
-                x = u31 >= t0;
-                for (int q = 1; q < card - 1; ++q) x += u31 >= __ldg(th + q);
-              } else {
-                const double* p = a.ptab + dv[3] + int64_t(e) * card;
-                const double norm = __ldg(p + card - 1);
-                if (!(norm > 0.0)) zs = true;
-                const double au = __dmul_rn(u01, norm);
-                for (int q = 0; q < card - 1; ++q) x += au > __ldg(p + q);
-              }
-            } else {
-              x = draw_factored<4>(fd, a.cpt, get, u01, zs);
-            }
-            uint32_t* wp = st + (size_t(v) * a.mg + l) * wpr + cw;
-            atomicAnd(wp, ~(MASK << csh));
-            atomicOr(wp, uint32_t(x) << csh);
+        const uint64_t gcase = uint64_t(bt.case_base + c0 + c);
+        // the tile's replicas of (v, c): replica r takes word r % 4 of the Philox block of its
+        // global quad (FAST counters); the block is recomputed per replica so that no block
+        // state stays live across the draw (register pressure: 64 registers at 1024 threads)
+        for (int l = 0; l < mg; ++l) {
+          const int r = rg0 + l;
+          const int roff = l * wpr + cw;  // + u * rs selects variable u
+          auto get = [&](int u) { return int((st[u * rs + roff] >> csh) & MASK); };
+          double u01;
+          uint32_t u31 = 0;
+          if (MODE == SG_RNG_FAST) {
+            const uint32_t wv = pick(fast_block(key, gcase, uint32_t(v), uint32_t(r >> 2), 0u), r & 3);
+            u31 = wv >> 1;
+            u01 = double(wv) * 0x1.0p-32;
+          } else {
+            const int64_t ui = int64_t(r) * nmiss + rank;  // reference lane order (sampler.py:245)
+            u01 = MODE == SG_RNG_NUMPY ? np_uniform(uint64_t(ui), k0, k1) : __ldg(a.uniforms + ioff + ui);
           }
+          int x = 0;
+          if (nmb >= 0) {  // conditional table of the blanket configuration
+            int e = 0;
+            for (int q = 0; q < nmb; ++q) e += get(dv[4 + q]) * dv[4 + SG_DESC_MB + q];
+            if (MODE == SG_RNG_FAST) {
+              const uint32_t* th = a.ftab + dv[2] + e * (card - 1);
+              const uint32_t t0 = __ldg(th);
+              if (zs_armed && t0 == 0xFFFFFFFFu) zs = true;
+              x = u31 >= t0;
+              for (int q = 1; q < card - 1; ++q) x += u31 >= __ldg(th + q);
+            } else {
+              const double* p = a.ptab + dv[3] + int64_t(e) * card;
+              const double norm = __ldg(p + card - 1);
+              if (!(norm > 0.0)) zs = true;
+              const double au = __dmul_rn(u01, norm);
+              for (int q = 0; q < card - 1; ++q) x += au > __ldg(p + q);
+            }
+          } else {
+            x = draw_factored<4>(fd, a.cpt, get, u01, zs);
+          }
+          uint32_t* wp = st + v * rs + roff;
+          atomicAnd(wp, ~(MASK << csh));
+          atomicOr(wp, uint32_t(x) << csh);
         }
       }
       __syncwarp();
