@@ -271,3 +271,83 @@ class BinaryFileSource(_BlockStream):
         ev = super()._copy(i, slot, after)
         self._pinned_ev[self._pending] = ev
         return ev
+
+
+# ------------------------------------------------------------------ text formats of the reference CLI
+# (io.py:105-153 coordinate data, io.py:243-270 trace CSV, io.py:273-280 manifest):
+# read so that `train` can consume the reference's own files.
+
+def write_data(path, data) -> None:
+    """Coordinate triples, case-major, 1-based (reference io.py:105-116)."""
+    with open(path, "w") as fh:
+        fh.write(f"{data.num_vars} {data.num_cases} {data.nnz}\n")
+        trip = np.stack([data.var_idx + 1, data.case_idx + 1, data.values.astype(np.int64) + 1], axis=1)
+        np.savetxt(fh, trip, fmt="%d", delimiter=" ")
+
+
+def read_data(path):
+    """A whole coordinate file as a DataMatrix (reference io.py:119-153)."""
+    from .datagen import DataMatrix
+
+    path = Path(path)
+    if not path.exists():
+        raise IoError(f"file not found: {path}")
+    with open(path) as fh:
+        header = fh.readline()
+        try:
+            num_vars, num_cases, nnz = (int(tok) for tok in header.split())
+        except ValueError as exc:
+            raise ParseError(f"{path}:1: bad header {header.strip()!r}") from exc
+        body = fh.read()
+    try:
+        trip = np.array(body.split(), dtype=np.int64).reshape(-1, 3) if body.strip() else np.zeros((0, 3), np.int64)
+    except ValueError as exc:
+        raise ParseError(f"{path}: bad triple row: {exc}") from exc
+    if len(trip) != nnz:
+        raise ParseError(f"{path}: header promises {nnz} entries, found {len(trip)}")
+    try:
+        return DataMatrix(num_vars=num_vars, num_cases=num_cases, var_idx=trip[:, 0] - 1, case_idx=trip[:, 1] - 1,
+                          values=trip[:, 2] - 1)
+    except ValueError as exc:
+        raise ParseError(f"{path}: {exc}") from exc
+
+
+def write_trace(path, trace) -> None:
+    """pass,seconds,kl_avg,vars_per_sec rows (reference io.py:243-249)."""
+    with open(path, "w") as fh:
+        fh.write("pass,seconds,kl_avg,vars_per_sec\n")
+        for r in trace.records:
+            kl = "" if r.kl_avg is None else repr(r.kl_avg)
+            vps = "" if r.vars_per_sec is None else repr(r.vars_per_sec)
+            fh.write(f"{r.pass_index},{r.seconds!r},{kl},{vps}\n")
+
+
+def read_trace(path):
+    from .sampler import Trace, TraceRecord
+
+    trace = Trace()
+    with open(path) as fh:
+        if fh.readline().strip() != "pass,seconds,kl_avg,vars_per_sec":
+            raise ParseError(f"{path}:1: unexpected trace header")
+        for line in fh:
+            pass_ix, seconds, kl, vps = line.rstrip("\n").split(",")
+            trace.records.append(TraceRecord(pass_index=int(pass_ix), seconds=float(seconds),
+                                             kl_avg=float(kl) if kl else None,
+                                             vars_per_sec=float(vps) if vps else None, vars_sampled=0))
+    return trace
+
+
+def write_manifest(path, manifest: dict) -> None:
+    with open(path, "w") as fh:
+        json.dump(manifest, fh, indent=1, sort_keys=True)
+        fh.write("\n")
+
+
+def read_manifest(path) -> dict:
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except FileNotFoundError as exc:
+        raise IoError(f"file not found: {path}") from exc
+    except json.JSONDecodeError as exc:
+        raise ParseError(f"{path}: {exc}") from exc
