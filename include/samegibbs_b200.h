@@ -449,7 +449,17 @@ int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_finish* f, vo
    [dev] 4 uint32 (hand-off flag, finish count, role ticket, spare), zero
    before the first call; the kernel re-arms them. */
 int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const sg_finish* f,
-                       const sg_joint* jp, uint32_t* jblob, uint32_t* sync, void* stream);
+                       const sg_joint* jp, uint32_t* jblob, uint32_t* sync, const void* prep,
+                       void* stream);
+
+/* The step tail's static per-slice preparation (the conditionals' gather
+   plan and every row entry's index list; they depend only on the network):
+   sg_joint_prep fills `prep` [dev] (sg_joint_prep_bytes bytes, 16-byte
+   aligned) once, after the blob header is in jblob; sg_step_tail_joint then
+   bulk-copies each slice's part instead of building it (prep = NULL: build). */
+int sg_joint_prep_bytes(const sg_small* sp, const sg_joint* jp, int64_t* bytes);
+int sg_joint_prep(const sg_net* net, const sg_small* sp, const sg_joint* jp, const uint32_t* jblob,
+                  void* prep, void* stream);
 
 
 /* Device key cursor for CUDA-graph replay of minibatch steps:

@@ -115,7 +115,9 @@ _SIGNATURES = {
     "sg_joint_tables": ([POINTER(SgNet), POINTER(SgSmall), POINTER(SgJoint), c_void_p, c_void_p, c_void_p, c_void_p],
                         c_int32),
     "sg_step_tail_joint": ([POINTER(SgNet), POINTER(SgSmall), POINTER(SgFinish), POINTER(SgJoint), c_void_p,
-                            c_void_p, c_void_p], c_int32),
+                            c_void_p, c_void_p, c_void_p], c_int32),
+    "sg_joint_prep_bytes": ([POINTER(SgSmall), POINTER(SgJoint), POINTER(ctypes.c_int64)], c_int32),
+    "sg_joint_prep": ([POINTER(SgNet), POINTER(SgSmall), POINTER(SgJoint), c_void_p, c_void_p, c_void_p], c_int32),
     "sg_joint_smem": ([POINTER(SgSmall), POINTER(SgJoint), c_int32, POINTER(ctypes.c_int64)], c_int32),
     "sg_joint_sweep": ([POINTER(SgSmall), POINTER(SgJoint), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                         c_int32, c_int32, c_int32, c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32,
@@ -175,7 +177,7 @@ KERNELS_PER_CALL = {
     "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
     "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
-    "sg_joint_tables": 1, "sg_joint_sweep": 1, "sg_step_tail_joint": 1, "sg_copy_small": 1, "sg_noop": 1,
+    "sg_joint_tables": 1, "sg_joint_sweep": 1, "sg_step_tail_joint": 1, "sg_joint_prep": 1, "sg_copy_small": 1, "sg_noop": 1,
     "sg_keys_advance": 1, "sg_step_finish": 1, "sg_site_keys": 1, "sg_predict_tally": 1, "sg_unpack_nibbles": 1, "sg_unpack_crumbs": 1,
 }
 launch_count = 0

@@ -10,7 +10,7 @@ namespace sg {
 // Debug build only (-DSG_FINISH_TRACE): %globaltimer at the phase boundaries
 // of the step tail, read back with sg_debug_finish_trace (tools/trace_finish.py).
 #ifdef SG_FINISH_TRACE
-__device__ unsigned long long g_finish_trace[8];
+__device__ unsigned long long g_finish_trace[12];
 #define SG_TRACE(i)                                                                             \
   do {                                                                                          \
     if (threadIdx.x == 0) {                                                                     \
@@ -196,7 +196,9 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
   // 1. accumulator (+ the cell's gamma draw)
   if (my_cell >= 0) {
     const int i = my_cell;
-    const double t = acc_cell(f.acc_mode, t_old, double(f.new_counts[i]), f.prev_counts != nullptr, t_prev, f.decay);
+    const double nc = double(f.new_counts[i]);
+    SG_TRACE(8);
+    const double t = acc_cell(f.acc_mode, t_old, nc, f.prev_counts != nullptr, t_prev, f.decay);
     f.total[i] = t;
     if (f.map_estimate) {
       lg[i] = t;
@@ -207,6 +209,7 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
       lg[i] = gamma_draw(rs, pre, t + a_cell, &il);
       inlog[i] = il;
     }
+    SG_TRACE(9);
   } else if (!(early && cells <= nt)) {
     for (int i = tid; i < cells; i += nt) {
       const double t = acc_cell(f.acc_mode, f.total[i], double(f.new_counts[i]), f.prev_counts != nullptr,
@@ -225,17 +228,19 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
     }
   }
   if (f.release_sync && f.release_lg) {  // hand the draws over now: the slices build their rows from them
+    // Publication without a per-thread fence: every thread's stores happen
+    // before the CTA barrier, the barrier before tid 0's st.release.gpu, and
+    // a release is cumulative over what happens before it -- a slice that
+    // reads the flag with ld.acquire.gpu sees all of them.
     uint8_t* il_out = reinterpret_cast<uint8_t*>(f.release_lg + cells);
     if (my_cell >= 0) {
       f.release_lg[my_cell] = lg[my_cell];
       il_out[my_cell] = f.map_estimate ? 0 : inlog[my_cell];
-      __threadfence();
     } else if (!(early && cells <= nt)) {
       for (int i = tid; i < cells; i += nt) {
         f.release_lg[i] = lg[i];
         il_out[i] = f.map_estimate ? 0 : inlog[i];
       }
-      __threadfence();
     }
     __syncthreads();
     if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.release_sync), "r"(1u) : "memory");

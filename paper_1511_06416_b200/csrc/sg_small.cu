@@ -844,18 +844,15 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   SG_SWEEP_STAMP(1);
 }
 
-// Rows of pattern P = blockIdx.x, lane words S of slice blockIdx.y, from the
-// current CPTs (see the blob comment).  fp64 in a fixed order, no FMA:
-// p_v = w / norm with the reference's weight product (conditional_weights)
-// and sequential norm; products in colour order; sequential row sums;
-// thresholds min(ceil(cum * (2^31 / total)), 2^31).
+// Trace stamps of the step tail's CTAs (debug builds, -DSG_FINISH_TRACE).
 #ifdef SG_FINISH_TRACE
-__device__ unsigned long long g_tail_trace[4 * 160];
+__device__ unsigned long long g_tail_trace[8 * 160];
+__device__ int g_tail_trace_role[160];
 __device__ __forceinline__ void tail_stamp(int k) {
   if (threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_tail_trace[blockIdx.x * 4 + k] = t;
+    g_tail_trace[blockIdx.x * 8 + k] = t;
   }
 }
 #else
@@ -863,26 +860,11 @@ __device__ __forceinline__ void tail_stamp(int) {}
 #endif
 
 #define SG_JOINT_TAB_SLICES 4
+// The merged step tail splits a pattern whose rows have 2^B = 64 columns
+// (two per lane) into twice as many slices: its per-CTA static preparation
+// and rows then cost what a 32-column pattern's do (it was the straggler).
+__host__ __device__ __forceinline__ int joint_tail_slices(int B) { return B >= 6 ? 2 * SG_JOINT_TAB_SLICES : SG_JOINT_TAB_SLICES; }
 #define SG_JOINT_ROW_WARPS (FINISH_THREADS / 32)
-
-// first index in a[0..n) with a[i] > v (a non-decreasing; n <= 64)
-__device__ __forceinline__ int upper_bound_u32(const uint32_t* a, int n, uint32_t v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] > v) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
-// first index in a[0..n) with a[i] >= v
-__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] >= v) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
 
 // One transition row as an alias table (one warp; K = 2^B columns, lane l
 // holds column l, or columns 2l, 2l+1 when K = 64).  Input: the inclusive fp64
@@ -931,22 +913,36 @@ __device__ __forceinline__ void joint_alias_row(uint32_t* row, int B, bool two, 
     }
   }
   const uint32_t D0 = dl - d1, E0 = el - e1;  // inclusive at the lane's first column
-  if (act) {
+  // both scans as 64-entry arrays, padded past K with values above any query
+  // (0xFFFFFFFF), so every search below is the same 6-step branch-free loop
+  if (two) {
     sd[j0] = D0;
     se[j0] = E0;
-    if (two) {
-      sd[j0 + 1] = dl;
-      se[j0 + 1] = el;
-    }
+    sd[j0 + 1] = dl;
+    se[j0 + 1] = el;
+  } else {
+    sd[lane] = act ? D0 : 0xFFFFFFFFu;
+    se[lane] = act ? E0 : 0xFFFFFFFFu;
+    sd[lane + 32] = 0xFFFFFFFFu;
+    se[lane + 32] = 0xFFFFFFFFu;
   }
   __syncwarp();
+  // light: primary w, alias = the heavy holding the light's start D - d on the
+  // surplus line; heavy: overshoot = first light end >= E, minus E; primary
+  // T - overshoot, alias = the next heavy (the same count-of-E<=q search with
+  // q = E).  Both searches run for every lane (no divergence).
   auto entry = [&](int j, uint64_t w, uint32_t d, uint32_t Dinc, uint32_t Einc) -> uint32_t {
-    if (w < T) return (uint32_t(w) << B) | uint32_t(upper_bound_u32(se, K, Dinc - d));
-    if (w > T) {
-      const uint32_t X = sd[lower_bound_u32(sd, K, Einc)];
-      const uint32_t ov = X - Einc;
-      if (ov) return (uint32_t(T - ov) << B) | uint32_t(upper_bound_u32(se, K, Einc));
+    const bool light = w < T, heavy = w > T;
+    const uint32_t q = light ? Dinc - d : Einc;
+    int al = 0, xi = 0;
+#pragma unroll
+    for (int step = 32; step; step >>= 1) {
+      if (se[al + step - 1] <= q) al += step;    // #{E <= q}: upper bound
+      if (sd[xi + step - 1] < Einc) xi += step;  // #{D < E}: lower bound
     }
+    const uint32_t ov = sd[min(xi, 63)] - Einc;
+    if (light) return (uint32_t(w) << B) | uint32_t(al);
+    if (heavy && ov) return (uint32_t(T - ov) << B) | uint32_t(al);
     return uint32_t(j);
   };
   if (act) {
@@ -963,7 +959,8 @@ __device__ __forceinline__ void joint_alias_row(uint32_t* row, int B, bool two, 
 __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& sp, const sg_joint& jp,
                                             const double* cpt, const double* vprob_g, uint32_t* jblob, int P,
                                             int slice, unsigned char* smem, bool wait_pdl,
-                                            bool vprob_ready = false, int part = 0, uint16_t* pidx = nullptr) {
+                                            bool vprob_ready = false, int part = 0, uint16_t* pidx = nullptr,
+                                            int slices = SG_JOINT_TAB_SLICES) {
   // part 0: everything; 1: only the static preparation -- the pattern's
   // latent-variable list and, with pidx, every row entry's list of vprob
   // indices (a caller runs it early); 2: everything but that (part 1 ran
@@ -983,7 +980,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
   uint32_t* rows = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(jblob) + jblob[P]);
   const int R = 1 << sp.bits, K = 1 << B;
   const int KS = K + 1;  // row stride (odd: no bank conflicts)
-  const int rows_per = R / SG_JOINT_TAB_SLICES, r0 = slice * rows_per;
+  const int rows_per = R / slices, r0 = slice * rows_per;
   double* vprob = reinterpret_cast<double*>(smem);  // [n][R][4]
   if (tid == 0 && part != 2) {
     int k = 0;
@@ -1082,6 +1079,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
     }
     return p;
   };
+  tail_stamp(4);
   for (int r = warp; r < rows_per; r += nt >> 5) {
     const uint32_t S = uint32_t(r0 + r);
     const int j0 = two ? 2 * lane : lane;
@@ -1096,7 +1094,9 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
     const double left = __shfl_up_sync(0xffffffffu, x, 1);
     const double total = __shfl_sync(0xffffffffu, x, two ? 31 : K - 1);
     const double c0 = two ? (lane ? __dadd_rn(left, a) : a) : x;
+    if (r == 0) tail_stamp(5);
     joint_alias_row(rows + S * KS, B, two, lane, j0 < K ? c0 : 0.0, x, total, alias_sd[warp], alias_se[warp]);
+    if (r == 0) tail_stamp(6);
   }
 }
 
@@ -1192,10 +1192,15 @@ __global__ void __launch_bounds__(256) k_joint_tables(const sg_net net, const sg
 
 #ifdef SG_FINISH_TRACE
 extern "C" int sg_debug_tail_trace(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, g_tail_trace, sizeof(g_tail_trace)) == cudaSuccess ? 0 : 2;
+  // 8 stamps per CTA (by blockIdx.x), then the CTA -> role map as 160 more words
+  if (cudaMemcpyFromSymbol(out, g_tail_trace, sizeof(g_tail_trace)) != cudaSuccess) return 2;
+  int roles[160];
+  if (cudaMemcpyFromSymbol(roles, g_tail_trace_role, sizeof(roles)) != cudaSuccess) return 2;
+  for (int i = 0; i < 160; ++i) out[8 * 160 + i] = (unsigned long long)roles[i];
+  return 0;
 }
 extern "C" int sg_debug_tail_finish_trace(unsigned long long* out) {  // this TU's copy of g_finish_trace
-  return cudaMemcpyFromSymbol(out, g_finish_trace, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 2;
+  return cudaMemcpyFromSymbol(out, g_finish_trace, sizeof(unsigned long long) * 12) == cudaSuccess ? 0 : 2;
 }
 #endif
 
@@ -1210,20 +1215,17 @@ extern "C" int sg_debug_tail_finish_trace(unsigned long long* out) {  // this TU
 // the sync words for the next step.
 __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net gnet, const FinishArgs f,
                                                                     const sg_small sp, const sg_joint jp,
-                                                                    uint32_t* jblob, uint32_t* sync) {
+                                                                    uint32_t* jblob, uint32_t* sync,
+                                                                    const unsigned char* __restrict__ prep,
+                                                                    int64_t prep_bytes) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_role;
   if (threadIdx.x == 0) s_role = int(atomicAdd(sync + 2, 1u));
   __syncthreads();
   const int role = s_role;  // 0: the model update; r >= 1: row slice r - 1
 #ifdef SG_FINISH_TRACE
-  auto stamp = [role](int k) {
-    if (threadIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      g_tail_trace[role * 4 + k] = t;
-    }
-  };
+  if (threadIdx.x == 0) g_tail_trace_role[blockIdx.x] = role;
+  auto stamp = [](int k) { tail_stamp(k); };
 #else
   auto stamp = [](int) {};
 #endif
@@ -1251,18 +1253,38 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   int2* plan = reinterpret_cast<int2*>(work + size_t(nr) * 4 * sizeof(double));
   int8_t* plan_nf = reinterpret_cast<int8_t*>(plan + size_t(nr) * SG_JOINT_MAXF);
   uint16_t* pidx = reinterpret_cast<uint16_t*>(plan_nf + ((size_t(nr) + 15) & ~size_t(15)));
-  const int b = role - 1;
-  const int P = b / SG_JOINT_TAB_SLICES;
+  // role -> (pattern, slice): patterns in order, joint_tail_slices(B_P) slices each
+  int P = 0, slice = role - 1, nsl = SG_JOINT_TAB_SLICES;
+  for (; P < jp.patterns; ++P) {
+    nsl = joint_tail_slices(int(jblob[jp.patterns + P] & 0xFFu));
+    if (slice < nsl) break;
+    slice -= nsl;
+  }
   pdl_trigger();
+  __shared__ __align__(8) uint64_t prep_bar;
+  const bool live = (jblob[jp.patterns + P] & 0xFFu) != 0;
+  // the static gather plan and row index lists of this slice: precomputed once
+  // (sg_joint_prep) and brought in with one TMA bulk copy, or built here
+  const bool prepped = prep != nullptr && live;
+  if (prepped && tid == 0) {
+    mbar_init(&prep_bar, 1);
+    mbar_expect_tx(&prep_bar, uint32_t(prep_bytes));
+    const unsigned char* src = prep + int64_t(role - 1) * prep_bytes;
+    for (int64_t o2 = 0; o2 < prep_bytes; o2 += 32768)
+      bulk_g2s(reinterpret_cast<unsigned char*>(plan) + o2, src + o2, uint32_t(prep_bytes - o2 < 32768 ? prep_bytes - o2 : 32768),
+               &prep_bar);
+  }
   for (int i = tid; i < int(gnet.blob64_words); i += blockDim.x) b64[i] = __ldg(gnet.blob64 + i);
   for (int i = tid; i < int(gnet.blob32_words); i += blockDim.x) b32[i] = __ldg(gnet.blob32 + i);
   __syncthreads();
   const sg_net net = rebase_net(gnet, b32, b64);
   // every CPT index of this pattern's conditionals, while the sweep / CTA 0 still run
-  if (jblob[jp.patterns + P] & 0xFFu) {
-    joint_cond_plan(net, sp, P, plan, plan_nf);
-    joint_slice(net, sp, jp, nullptr, nullptr, jblob, P, b % SG_JOINT_TAB_SLICES, work, false, true, 1, pidx);
+  if (live) {
+    if (!prepped) joint_cond_plan(net, sp, P, plan, plan_nf);
+    joint_slice(net, sp, jp, nullptr, nullptr, jblob, P, slice, work, false, true, 1, prepped ? nullptr : pidx, nsl);
+    if (prepped) mbar_wait(&prep_bar, 0);
   }
+  stamp(7);
   pdl_wait();  // the sweep has finished reading the blob rows this grid overwrites
   if (tid == 0) {
     uint32_t r = 0;
@@ -1294,10 +1316,9 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
     for (int i = tid; i < cells; i += blockDim.x) cpt_s[i] = __ldcg(f.cpt + i);
   }
   __syncthreads();
-  const bool live = (jblob[jp.patterns + P] & 0xFFu) != 0;
   if (live) joint_cond_apply(net, sp, plan, plan_nf, cpt_s, reinterpret_cast<double*>(work));
   __syncthreads();
-  joint_slice(net, sp, jp, cpt_s, nullptr, jblob, P, b % SG_JOINT_TAB_SLICES, work, false, true, 2, pidx);
+  joint_slice(net, sp, jp, cpt_s, nullptr, jblob, P, slice, work, false, true, 2, pidx, nsl);
   __syncthreads();
   stamp(2);
   if (threadIdx.x == 0 && atomicAdd(sync + 1, 1u) == gridDim.x - 2) {
@@ -1305,6 +1326,61 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
     sync[0] = 0u;
     sync[2] = 0u;  // every CTA has taken its ticket
   }
+}
+
+// Static preparation of every row slice of the merged tail, once per
+// network (it depends only on the network and the latent patterns): the
+// gather plan of the slice's conditionals and every row entry's vprob index
+// list, exactly as the slice would build them, stored per slice (role) so
+// that k_step_tail_joint loads them with one bulk copy instead of building
+// them on its critical path.
+__global__ void __launch_bounds__(FINISH_THREADS) k_joint_prep(const sg_net gnet, const sg_small sp,
+                                                               const sg_joint jp, const uint32_t* jblob,
+                                                               unsigned char* __restrict__ prep, int64_t prep_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x;
+  int64_t* b64 = reinterpret_cast<int64_t*>(smem);
+  int32_t* b32 = reinterpret_cast<int32_t*>(b64 + gnet.blob64_words);
+  unsigned char* work = reinterpret_cast<unsigned char*>(b32) + ((size_t(gnet.blob32_words) * 4 + 15) & ~size_t(15));
+  const int nr = sp.n << sp.bits;
+  int2* plan = reinterpret_cast<int2*>(work + size_t(nr) * 4 * sizeof(double));
+  int8_t* plan_nf = reinterpret_cast<int8_t*>(plan + size_t(nr) * SG_JOINT_MAXF);
+  uint16_t* pidx = reinterpret_cast<uint16_t*>(plan_nf + ((size_t(nr) + 15) & ~size_t(15)));
+  int P = 0, slice = blockIdx.x, nsl = SG_JOINT_TAB_SLICES;
+  for (; P < jp.patterns; ++P) {
+    nsl = joint_tail_slices(int(jblob[jp.patterns + P] & 0xFFu));
+    if (slice < nsl) break;
+    slice -= nsl;
+  }
+  if (P >= jp.patterns || !(jblob[jp.patterns + P] & 0xFFu)) return;
+  for (int i = tid; i < int(gnet.blob64_words); i += blockDim.x) b64[i] = __ldg(gnet.blob64 + i);
+  for (int i = tid; i < int(gnet.blob32_words); i += blockDim.x) b32[i] = __ldg(gnet.blob32 + i);
+  __syncthreads();
+  const sg_net net = rebase_net(gnet, b32, b64);
+  joint_cond_plan(net, sp, P, plan, plan_nf);
+  joint_slice(net, sp, jp, nullptr, nullptr, const_cast<uint32_t*>(jblob), P, slice, work, false, true, 1, pidx, nsl);
+  __syncthreads();
+  const unsigned char* src = reinterpret_cast<const unsigned char*>(plan);
+  unsigned char* dst = prep + int64_t(blockIdx.x) * prep_bytes;
+  for (int64_t i = tid; i < prep_bytes; i += blockDim.x) dst[i] = src[i];
+}
+
+// bytes of one slice's prep region (plan, plan_nf, pidx; the slice smem layout)
+static int64_t joint_prep_slice_bytes(const sg_small& sp, const sg_joint& jp) {
+  const int64_t nr = int64_t(sp.n) << sp.bits;
+  const int64_t pidx = (int64_t(1) << sp.bits) / SG_JOINT_TAB_SLICES * (int64_t(1) << jp.max_b) * SG_SMALL_MAXV * 2;
+  return (nr * SG_JOINT_MAXF * 8 + ((nr + 15) & ~int64_t(15)) + pidx + 15) & ~int64_t(15);
+}
+
+static int joint_tail_slice_count(const sg_small& sp, const sg_joint& jp) {
+  int slices = 0;
+  for (int P = 0; P < jp.patterns; ++P) {  // B_P = the latent variables' field widths (the blob header's B)
+    int B = 0;
+    for (int v = 0; v < sp.n; ++v)
+      if ((P >> v) & 1) B += sp.width[v];
+    slices += joint_tail_slices(B);
+  }
+  return slices;
 }
 
 static size_t joint_tables_smem(const sg_small& sp, int maxb) {
@@ -1593,8 +1669,35 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
   return check_launch("sg_joint_sweep");
 }
 
+extern "C" int sg_joint_prep_bytes(const sg_small* sp, const sg_joint* jp, int64_t* bytes) {
+  using namespace sg;
+  SG_REQUIRE(sp && jp && bytes, "sg_joint_prep_bytes: null argument");
+  *bytes = joint_prep_slice_bytes(*sp, *jp) * joint_tail_slice_count(*sp, *jp);
+  return SG_OK;
+}
+
+extern "C" int sg_joint_prep(const sg_net* net, const sg_small* sp, const sg_joint* jp, const uint32_t* jblob,
+                             void* prep, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(net && sp && jp && jblob && prep, "sg_joint_prep: null argument");
+  SG_REQUIRE(sp->bits >= 2 && sp->bits <= SG_JOINT_MAXB && jp->patterns == (1 << sp->n) && jp->max_b >= 1,
+             "sg_joint_prep: bad joint plan");
+  SG_REQUIRE(net->blob32 && net->blob64 && net->max_mb <= SG_MAX_MB, "sg_joint_prep: network pack not blobbed");
+  const int64_t per = joint_prep_slice_bytes(*sp, *jp);
+  const int slices = joint_tail_slice_count(*sp, *jp);
+  const int64_t nr = int64_t(sp->n) << sp->bits;
+  const size_t smem = size_t(net->blob64_words) * 8 + ((size_t(net->blob32_words) * 4 + 15) & ~size_t(15)) +
+                      size_t(nr) * 4 * sizeof(double) + size_t(per);
+  static size_t configured[SG_MAX_DEVICES] = {};
+  if (optin_needed(configured, smem))
+    cudaFuncSetAttribute(k_joint_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_joint_prep<<<slices, FINISH_THREADS, smem, (cudaStream_t)stream>>>(*net, *sp, *jp, jblob,
+                                                                      static_cast<unsigned char*>(prep), per);
+  return check_launch("sg_joint_prep");
+}
+
 extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const sg_finish* f, const sg_joint* jp,
-                                  uint32_t* jblob, uint32_t* sync, void* stream) {
+                                  uint32_t* jblob, uint32_t* sync, const void* prep, void* stream) {
   using namespace sg;
   SG_REQUIRE(net && sp && f && jp && jblob && sync && f->stab, "sg_step_tail_joint: null argument");
   SG_REQUIRE(f->acc_mode == SG_ACC_MOVING || f->acc_mode == SG_ACC_EXPONENTIAL, "sg_step_tail_joint: bad mode");
@@ -1629,8 +1732,10 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
     cudaFuncSetAttribute(k_step_tail_joint, cudaFuncAttributePreferredSharedMemoryCarveout,
                          int(cudaSharedmemCarveoutMaxShared));
   }
-  const dim3 grid(1 + jp->patterns * SG_JOINT_TAB_SLICES);
+  // one CTA for the model update + the row slices (joint_tail_slices per pattern)
+  const dim3 grid(1 + joint_tail_slice_count(*sp, *jp));
+  SG_REQUIRE(!prep || (reinterpret_cast<uintptr_t>(prep) & 15) == 0, "sg_step_tail_joint: prep must be 16-byte aligned");
   launch_pdl(k_step_tail_joint, grid, dim3(FINISH_THREADS), smem, (cudaStream_t)stream, *net, a, *sp, *jp, jblob,
-             sync);
+             sync, static_cast<const unsigned char*>(prep), joint_prep_slice_bytes(*sp, *jp));
   return check_launch("sg_step_tail_joint");
 }

@@ -130,6 +130,12 @@ class Engine:
             # full conditionals p_v(x | lane word), written by the step tail for sg_joint_tables
             self.vprob = torch.zeros(self.n * (4 << self.pack.small.bits), dtype=torch.float64, device=d)
             self.jsync = torch.zeros(4, dtype=torch.int32, device=d)  # sg_step_tail_joint's hand-off + ticket words
+            # the tail slices' static preparation, built once (sg_joint_prep)
+            nb = ctypes.c_int64()
+            _lib.call("sg_joint_prep_bytes", self.pack.small_ref, self.pack.joint_ref, ctypes.byref(nb))
+            self.jprep = torch.empty(max(16, nb.value), dtype=torch.uint8, device=d)
+            _lib.call("sg_joint_prep", self.pack.ref, self.pack.small_ref, self.pack.joint_ref, self.jblob.data_ptr(),
+                      self.jprep.data_ptr(), stream_handle())
         self.tables_fresh = False  # conditional tables reflect self.cpt
         self.graph_replay = True   # run(): replay steady-state visits as CUDA graphs
         self._latent_hint = None   # latent share of the first generic minibatch (sg_batch.latent_permille)
@@ -336,7 +342,7 @@ class Engine:
         launch, or with rng="joint" one grid that also builds the joint rows."""
         if self.joint:
             _lib.call("sg_step_tail_joint", self.pack.ref, self.pack.small_ref, f, self.pack.joint_ref,
-                      self.jblob.data_ptr(), self.jsync.data_ptr(), s)
+                      self.jblob.data_ptr(), self.jsync.data_ptr(), self.jprep.data_ptr(), s)
         else:
             _lib.call("sg_step_finish", self.pack.ref, self.small_ptr, f, s)
 

@@ -45,39 +45,54 @@ for k in range(12):
         torch.cuda.synchronize()
     sw = (ctypes.c_ulonglong * 320)()
     lib.sg_debug_sweep_trace(ctypes.cast(sw, ctypes.c_void_p))
-    tt = (ctypes.c_ulonglong * 640)()
+    tt = (ctypes.c_ulonglong * (8 * 160 + 160))()
     lib.sg_debug_tail_trace(ctypes.cast(tt, ctypes.c_void_p))
-    ft = (ctypes.c_ulonglong * 8)()
+    ft = (ctypes.c_ulonglong * 12)()
     lib.sg_debug_tail_finish_trace(ctypes.cast(ft, ctypes.c_void_p))
     nsw = 147
     t0 = min(sw[2 * b] for b in range(nsw))
+    roles = [int(tt[8 * 160 + b]) for b in range(129)]
+    c0 = roles.index(0)
+    sl = [b for b in range(129) if roles[b] >= 1]
+    T = lambda b, k: tt[8 * b + k]  # noqa: E731
     r = {
         "sweep first start": 0,
         "sweep last start": max(sw[2 * b] for b in range(nsw)) - t0,
         "sweep first end": min(sw[2 * b + 1] for b in range(nsw)) - t0,
         "sweep last end": max(sw[2 * b + 1] for b in range(nsw)) - t0,
-        "tail CTA0 start": tt[0] - t0,
+        "tail CTA0 start": T(c0, 0) - t0,
         "tail: early inputs done": ft[0] - t0,
         "tail: wait+key": ft[1] - t0,
+        "tail: counts loaded": ft[8] - t0,
+        "tail: gamma drawn": ft[9] - t0,
         "tail: acc+gamma": ft[2] - t0,
         "tail: rows": ft[3] - t0,
         "tail: tables": ft[4] - t0,
         "tail: clear+keys": ft[6] - t0,
-        "tail CTA0 end": tt[1] - t0,
-        "slices last start": max(tt[4 * b] for b in range(1, 129)) - t0,
-        "slices flag seen (median)": statistics.median(tt[4 * b + 1] for b in range(1, 129)) - t0,
-        "slices conditionals done (median)": statistics.median(tt[4 * b + 3] for b in range(1, 129)) - t0,
-        "slices median end": statistics.median(tt[4 * b + 2] for b in range(1, 129)) - t0,
-        "slices last end": max(tt[4 * b + 2] for b in range(1, 129)) - t0,
-        "slice rows phase max": max(tt[4 * b + 2] - tt[4 * b + 3] for b in range(1, 129)),
-        "slice rows phase median": statistics.median(tt[4 * b + 2] - tt[4 * b + 3] for b in range(1, 129)),
-        "slice cond phase max": max(tt[4 * b + 3] - tt[4 * b + 1] for b in range(1, 129)),
-        "slowest slice (P*4+slice)": max(range(1, 129), key=lambda b: tt[4 * b + 2]) - 1 + 0.0,
+        "tail CTA0 end": T(c0, 1) - t0,
+        "slices last start": max(T(b, 0) for b in sl) - t0,
+        "slices prep done (median)": statistics.median(T(b, 7) for b in sl) - t0,
+        "slices prep done (last)": max(T(b, 7) for b in sl) - t0,
+        "slices flag seen (median)": statistics.median(T(b, 1) for b in sl) - t0,
+        "slices conditionals done (median)": statistics.median(T(b, 3) for b in sl) - t0,
+        "slices rows loop start (median)": statistics.median(T(b, 4) for b in sl) - t0,
+        "slices warp0 scan done (median)": statistics.median(T(b, 5) for b in sl) - t0,
+        "slices warp0 alias done (median)": statistics.median(T(b, 6) for b in sl) - t0,
+        "slices median end": statistics.median(T(b, 2) for b in sl) - t0,
+        "slices last end": max(T(b, 2) for b in sl) - t0,
+        "slowest slice role": float(roles[max(sl, key=lambda b: T(b, 2))]),
+        "slowest: start": T(max(sl, key=lambda b: T(b, 2)), 0) - t0,
+        "slowest: prep done": T(max(sl, key=lambda b: T(b, 2)), 7) - t0,
+        "slowest: flag seen": T(max(sl, key=lambda b: T(b, 2)), 1) - t0,
+        "slowest: cond done": T(max(sl, key=lambda b: T(b, 2)), 3) - t0,
+        "slowest: rows start": T(max(sl, key=lambda b: T(b, 2)), 4) - t0,
+        "slowest: warp0 scan": T(max(sl, key=lambda b: T(b, 2)), 5) - t0,
+        "slowest: warp0 alias": T(max(sl, key=lambda b: T(b, 2)), 6) - t0,
     }
     r["gap: prev tail end -> sweep start"] = (t0 - prev_end) if (prev_end and not cold) else 0
-    prev_end = max(tt[4 * b + 2] for b in range(1, 129))
+    prev_end = max(T(b, 2) for b in sl)
     rows.append(r)
 print("cold" if cold else "warm", "(us from the first sweep CTA's start, median of steps 2..11)")
 for key in rows[0]:
     v = statistics.median(r[key] for r in rows[2:])
-    print(f"  {key:34s} {v / 1e3 if 'slowest' not in key else v:8.2f}")
+    print(f"  {key:34s} {v / 1e3 if 'role' not in key else v:8.2f}")
