@@ -601,7 +601,7 @@ def our_arm(args, wl: Workload) -> None:
                          "event_floor_ms": floor_ms,
                          "frac_above_event_floor": (algo_bytes / ((sw - floor_ms) * 1e-3) / 1e9 / peak
                                                     if floor_ms is not None and sw > floor_ms else None),
-                         "limiter": ("shared-memory row searches (bank conflicts) + Philox issue, not HBM: "
+                         "limiter": ("instruction issue (ALU pipe: Philox, alias draws, tally), not HBM: "
                                      "see DESIGN.md 6" if eng.joint else
                                      "instruction issue (Philox + table draws), not HBM: see DESIGN.md 6")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(host_obs.numel()),

@@ -84,7 +84,7 @@ if rep.exists():
               "k_small_sweep<5, 3> (sg_small_sweep)")
     (P / f"ncu_sweep_{R}.json").write_text(json.dumps({
         "kernel": kernel, "cases": 1_000_000, "m": 10,
-        "command": "python bench.py --steps 5 --warmup 3 --no-cpu-baseline --eager",
+        "command": "python bench.py --steps 5 --warmup 3 --no-cpu-baseline (step graph replay, 2-bit observation block)",
         "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
         "duration_us_under_ncu": dur, "algorithmic_bytes_per_launch": 75_000_000,
         "note": "traffic = dram__bytes_read.sum + dram__bytes_write.sum of one launch; the lane words, pattern "
@@ -92,7 +92,19 @@ if rep.exists():
                 "written back (writes land in L2 and are not evicted within the launch).",
     }, indent=1) + "\n")
 
-for src, dst in ((f"bench_{R}.json", f"{R}_bench.json"), (f"bench_ref_{R}.json", f"{R}_bench_reference.json")):
+for name in ("big",):
+    rep = G / f"{name}_{R}.ncu-rep"
+    if rep.exists():
+        txt = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), str(rep), "20"],
+                             capture_output=True, text=True).stdout
+        (P / f"{R}_sweep_big_ncu_summary.txt").write_text(
+            f"# ncu --set full --clock-control none --import-source on, one k_sweep_big launch on C4 ({rep.name})\n"
+            + txt)
+if (G / f"pytest_gpu_{R}.log").exists():
+    shutil.copy(G / f"pytest_gpu_{R}.log", P / f"{R}_pytest_gpu.log")
+for src, dst in ((f"bench_{R}.json", f"{R}_bench.json"), (f"bench_ref_{R}.json", f"{R}_bench_reference.json"),
+                 (f"bench_numpy_{R}.json", f"{R}_bench_numpy.json"), (f"bench_c3_{R}.json", f"{R}_bench_c3.json"),
+                 (f"bench_c4_{R}.json", f"{R}_bench_c4.json"), (f"bench_c5_{R}.json", f"{R}_bench_c5.json")):
     if (G / src).exists():
         lines = [l for l in (G / src).read_text().splitlines() if l.startswith("{")]
         if lines:
