@@ -561,7 +561,7 @@ static SmallOrd small_ord(const sg_small& sp) {
 //   [0, NP)        byte offset of row 0 of pattern P
 //   [NP, 2NP)      B_P | keep_P << 8 | (byte offset of dep_P) << 16
 //   dep_P[j]       latent field bits of compact column j (pdep(j, latent mask))
-//   rows_P[S][j]   alias entries (primary << B_P | alias), 2^bits rows of 2^B_P + 1 words
+//   rows_P[S][j]   alias entries (primary << B_P | alias), 2^bits rows of 2^B_P words
 
 #ifndef SG_JOINT_THREADS
 #define SG_JOINT_THREADS 1024
@@ -616,7 +616,7 @@ __device__ __forceinline__ uint32_t joint_alias_col(uint32_t row, uint32_t u) {
 template <int B, int QG, int NL>
 __device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[QG], uint32_t row0, uint32_t dep0,
                                             uint32_t keep) {
-  constexpr uint32_t kRowBytes = ((1u << B) + 1u) * 4u;  // rows 2^B + 1 words apart
+  constexpr uint32_t kRowBytes = (1u << B) * 4u;  // rows 2^B words apart
 #pragma unroll
   for (int g = 0; g < QG; ++g) {
     const uint32_t u[4] = {r[g].a, r[g].b, r[g].c, r[g].d};
@@ -731,7 +731,7 @@ __host__ __device__ inline size_t joint_smem(const sg_small& sp, const sg_joint&
 // 109 KB) and per-warp tally bins in shared memory.  NL: lanes of the final
 // quad (m - 4 * (Q - 1)).
 #ifdef SG_FINISH_TRACE
-__device__ unsigned long long g_sweep_trace[2 * 160];
+__device__ unsigned long long g_sweep_trace[8 * 160];
 extern "C" int sg_debug_sweep_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_sweep_trace, sizeof(g_sweep_trace)) == cudaSuccess ? 0 : 2;
 }
@@ -740,7 +740,7 @@ extern "C" int sg_debug_sweep_trace(unsigned long long* out) {
     if (threadIdx.x == 0 && blockIdx.y == 0) {                            \
       unsigned long long t_;                                              \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
-      g_sweep_trace[blockIdx.x * 2 + (k)] = t_;                           \
+      g_sweep_trace[blockIdx.x * 8 + (k)] = t_;                           \
     }                                                                     \
   } while (0)
 #else
@@ -798,8 +798,9 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
     for (uint32_t o2 = 0; o2 < jbytes; o2 += 32768u)
       bulk_g2s(blob + o2, reinterpret_cast<const unsigned char*>(jblob_g) + o2, min(32768u, jbytes - o2), bar);
   }
-  for (int i = tid; i < sp.tab_words; i += NT) stab[i] = stab_g[i];
   const bool armed = zs_flag && *zs_flag != 0u;
+  if (armed)  // the per-variable tables are read only by the zero-support fallback
+    for (int i = tid; i < sp.tab_words; i += NT) stab[i] = stab_g[i];
   QuadSet qs;
   qs.row0 = uint32_t(q0) * uint32_t(lane_ld);
   qs.ld = uint32_t(lane_ld);
@@ -813,8 +814,10 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   // the minibatch's range check while the blob is in flight (no kernel of this
   // step writes the observation block)
   obs_range_check<NT>(sp, obs, ld_obs, cases, err, obs_nib);
+  SG_SWEEP_STAMP(2);  // prologue issued (blob copy in flight, range check done)
   __syncthreads();
   mbar_wait(bar, 0);
+  SG_SWEEP_STAMP(3);  // blob landed: the draws start
   bool zs = false;
   if (armed) {  // padded SmallOrd entries (variable 31) are never latent: any n <= SG_SMALL_MAXV
     zs = small_units<SG_SMALL_MAXV, QG, true, NT, true>(o, qs, stab, lanes, pattern, case_id, hist_a, cases,
@@ -949,7 +952,6 @@ __device__ __forceinline__ void joint_alias_row(uint32_t* row, int B, bool two, 
     row[j0] = entry(j0, w0, d0, D0, E0);
     if (two) row[j0 + 1] = entry(j0 + 1, w1, d1, dl, el);
   }
-  if (lane == 0) row[K] = 0u;  // stride padding
   __syncwarp();
 }
 // Slice `slice` (lane words S in [slice * R/4, (slice+1) * R/4)) of pattern
@@ -979,7 +981,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
   const uint32_t* dep = reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(jblob) + (meta >> 16));
   uint32_t* rows = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(jblob) + jblob[P]);
   const int R = 1 << sp.bits, K = 1 << B;
-  const int KS = K + 1;  // row stride (odd: no bank conflicts)
+  const int KS = K;  // row stride (alias columns are uniform: no structural bank conflicts)
   const int rows_per = R / slices, r0 = slice * rows_per;
   double* vprob = reinterpret_cast<double*>(smem);  // [n][R][4]
   if (tid == 0 && part != 2) {

@@ -43,23 +43,26 @@ for k in range(12):
     g.step()
     if cold or k % 2 == 1:
         torch.cuda.synchronize()
-    sw = (ctypes.c_ulonglong * 320)()
+    sw = (ctypes.c_ulonglong * 1280)()
     lib.sg_debug_sweep_trace(ctypes.cast(sw, ctypes.c_void_p))
     tt = (ctypes.c_ulonglong * (8 * 160 + 160))()
     lib.sg_debug_tail_trace(ctypes.cast(tt, ctypes.c_void_p))
     ft = (ctypes.c_ulonglong * 12)()
     lib.sg_debug_tail_finish_trace(ctypes.cast(ft, ctypes.c_void_p))
     nsw = 147
-    t0 = min(sw[2 * b] for b in range(nsw))
+    t0 = min(sw[8 * b] for b in range(nsw))
     roles = [int(tt[8 * 160 + b]) for b in range(129)]
     c0 = roles.index(0)
     sl = [b for b in range(129) if roles[b] >= 1]
     T = lambda b, k: tt[8 * b + k]  # noqa: E731
     r = {
         "sweep first start": 0,
-        "sweep last start": max(sw[2 * b] for b in range(nsw)) - t0,
-        "sweep first end": min(sw[2 * b + 1] for b in range(nsw)) - t0,
-        "sweep last end": max(sw[2 * b + 1] for b in range(nsw)) - t0,
+        "sweep last start": max(sw[8 * b] for b in range(nsw)) - t0,
+        "sweep prologue issued (median)": statistics.median(sw[8 * b + 2] for b in range(nsw)) - t0,
+        "sweep draws start (median)": statistics.median(sw[8 * b + 3] for b in range(nsw)) - t0,
+        "sweep draws start (last)": max(sw[8 * b + 3] for b in range(nsw)) - t0,
+        "sweep first end": min(sw[8 * b + 1] for b in range(nsw)) - t0,
+        "sweep last end": max(sw[8 * b + 1] for b in range(nsw)) - t0,
         "tail CTA0 start": T(c0, 0) - t0,
         "tail: early inputs done": ft[0] - t0,
         "tail: wait+key": ft[1] - t0,
