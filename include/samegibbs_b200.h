@@ -324,13 +324,15 @@ int sg_small_tables(const sg_net* net, const sg_small* sp, const uint32_t* ftab,
                     uint32_t* stab, void* stream);
 
 /* Bucket the minibatch's cases by latent pattern and (init != 0) build their
-   lane words with FAST initial draws (same draws as sg_init_states).
+   lane words with FAST initial draws (same draws as sg_init_states; key
+   derive_seed(seed, "latent_init", pass, mb), sampler.py:211 -- read from
+   init_key_dev [dev] when it is not NULL, e.g. a CUDA-graph key cursor).
    scratch: [dev] int32 of 128 + ceil(cases / 4) words. */
 int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t ld_obs,
                      int32_t cases, int32_t m, int64_t case_base,
                      uint64_t init_key, int32_t init, int32_t* scratch,
                      uint8_t* pattern, int32_t* case_id, uint8_t* lanes,
-                     int32_t lane_ld, void* stream);
+                     int32_t lane_ld, const uint64_t* init_key_dev, void* stream);
 
 /* Sweep + tally on packed lanes (m <= 32, FAST stream).  jcell [dev]
    [2^bits][n]: CPT cell of each variable for each lane word; zs_flag = ftab +

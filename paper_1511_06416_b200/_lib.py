@@ -108,7 +108,7 @@ _SIGNATURES = {
                          c_int32),
     "sg_small_tables": ([POINTER(SgNet), POINTER(SgSmall), c_void_p, c_void_p, c_void_p], c_int32),
     "sg_small_prepare": ([POINTER(SgSmall), c_void_p, c_int32, c_int32, c_int32, c_int64, c_uint64, c_int32,
-                          c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p], c_int32),
+                          c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p], c_int32),
     "sg_small_sweep": ([POINTER(SgSmall), c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32,
                         c_int32, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
                         c_int32, c_void_p, c_void_p], c_int32),

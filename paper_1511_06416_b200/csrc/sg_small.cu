@@ -76,8 +76,10 @@ __global__ void k_small_scan(int* hist) {
 __global__ void __launch_bounds__(256) k_small_scatter(
     const sg_small sp, const int8_t* __restrict__ obs, int ld, int cases, int m, int64_t case_base,
     uint64_t init_key, const uint8_t* __restrict__ pattern_of_case, int* __restrict__ cursor,
-    uint8_t* __restrict__ pattern, int32_t* __restrict__ case_id, uint8_t* __restrict__ lanes, int lane_ld, int init) {
+    uint8_t* __restrict__ pattern, int32_t* __restrict__ case_id, uint8_t* __restrict__ lanes, int lane_ld, int init,
+    const uint64_t* __restrict__ init_key_dev) {
   __shared__ int cnt[SMALL_PATTERNS];
+  if (init_key_dev) init_key = *init_key_dev;  // graph replay: the key cursor's init key
   __shared__ int base[SMALL_PATTERNS];
   for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
@@ -1407,7 +1409,8 @@ static bool lane_ld_ok(int lane_ld, int cases) { return lane_ld >= cases && lane
 
 extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t ld_obs, int32_t cases, int32_t m,
                                 int64_t case_base, uint64_t init_key, int32_t init, int32_t* scratch,
-                                uint8_t* pattern, int32_t* case_id, uint8_t* lanes, int32_t lane_ld, void* stream) {
+                                uint8_t* pattern, int32_t* case_id, uint8_t* lanes, int32_t lane_ld,
+                                const uint64_t* init_key_dev, void* stream) {
   using namespace sg;
   SG_REQUIRE(sp && obs && scratch && pattern && case_id && lanes, "sg_small_prepare: null argument");
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV, "sg_small_prepare: bad plan");
@@ -1423,7 +1426,7 @@ extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t l
   k_small_count<<<blocks, 256, 0, s>>>(*sp, obs, ld_obs, cases, poc, hist);
   k_small_scan<<<1, 32, 0, s>>>(hist);
   k_small_scatter<<<(cases + 255) / 256, 256, 0, s>>>(*sp, obs, ld_obs, cases, m, case_base, init_key, poc, hist,
-                                                       pattern, case_id, lanes, lane_ld, init);
+                                                       pattern, case_id, lanes, lane_ld, init, init_key_dev);
   return check_launch("sg_small_prepare");
 }
 

@@ -206,7 +206,7 @@ class Engine:
                 key = derive_seed(cfg.seed, "latent_init", pass_index, mb.index)
                 _lib.call("sg_small_prepare", self.pack.small_ref, obs.data_ptr(), ld, size, m, self.case_base,
                           key, 1, db.scratch.data_ptr(), db.pattern.data_ptr(), db.case_id.data_ptr(),
-                          db.lanes.data_ptr(), db.lane_ld, s)
+                          db.lanes.data_ptr(), db.lane_ld, None, s)
                 if moving:
                     db.count_latent(obs, ld)
         else:
@@ -400,6 +400,13 @@ class Engine:
         graphs: dict[int, StepGraphs] = {}
         use_graphs = self.graphs_ok()
         sched = [anneal_m(cfg.same_m, p) for p in range(cfg.num_passes)]
+        # exponential accumulator on the packed / joint path: fresh visits replayed as stream graphs
+        # (every full minibatch; the first visit and a padded last block run eagerly)
+        full = source.num_cases // cfg.minibatch_size
+        stream_ok = (cfg.accumulator_mode == "exponential" and self.use_small and self.graph_replay
+                     and isinstance(cfg.same_m, int) and full >= 1
+                     and (self.comm is None or getattr(self.comm, "capturable", False)))
+        stream: StreamGraphs | None = None
         host_t0 = time.perf_counter()
         kls = []
         for pass_index in range(cfg.num_passes):
@@ -408,6 +415,12 @@ class Engine:
             while end_same < cfg.num_passes and sched[end_same] == m:
                 end_same += 1
             for mb in source:
+                if stream_ok and mb.index < full and (pass_index, mb.index) != (0, 0) and mb.size == cfg.minibatch_size:
+                    if stream is None:
+                        visits = [(p, i) for p in range(cfg.num_passes) for i in range(full) if (p, i) != (0, 0)]
+                        stream = StreamGraphs(self, cfg.minibatch_size, m, visits)
+                    stream.step(mb)
+                    continue
                 g = graphs.get(mb.index)
                 if g is not None and (g.m != m or not g.accepts(mb)):
                     g.finish()
@@ -784,3 +797,148 @@ class StepGraphs:
         """Hand the last visit's counts back to the engine's moving-sum bookkeeping."""
         if self.replayed:
             self.eng.prev_counts[self.mb.index] = self.cbuf[(self.replayed - 1) % 2].clone()
+
+
+class StreamGraphs:
+    """CUDA-graph replay of FRESH minibatch visits: the out-of-core mode of the
+    packed and joint paths (exponential accumulator, sampler.py:346-351 and
+    :434-441 -- every visit re-initialises its latents).
+
+    One replay = [decode of a packed .sgb block] + ``sg_small_prepare`` (cases
+    bucketed by latent pattern, observed fields from the block, FAST initial
+    latents keyed derive_seed(seed, "latent_init", pass, mb) read from the
+    key cursor) + the sweep(s) + the step tail.  The block is the graph's
+    private buffer (two, alternating), refilled by :meth:`step` from each
+    streamed minibatch, so every replay samples the minibatch it was given.
+    ``visits``: the planned (pass, minibatch) sequence of full minibatches;
+    replays equal eager visits bit for bit."""
+
+    def __init__(self, eng: Engine, size: int, m: int, visits, obs_bits: int = 8, readback=()):
+        cfg = eng.cfg
+        if cfg.accumulator_mode != "exponential" or not eng.use_small:
+            raise ValueError("stream graphs replay fresh visits of the packed / joint path (exponential accumulator)")
+        if obs_bits not in (8, 4, 2):
+            raise ValueError("obs_bits must be 8, 4 or 2")
+        if obs_bits < 8 and not eng.joint:
+            raise ValueError("packed observation blocks are range-checked by the joint sweep only")
+        if not eng.tables_fresh:
+            raise ValueError("engine tables are stale: run one eager visit first")
+        self.eng, self.size, self.m = eng, size, m
+        self.obs_bits = int(obs_bits)
+        S = cfg.sweeps_per_minibatch
+        self.kps = kps = S + 2  # sweep keys, Dirichlet key, latent-init key
+        visits = list(visits)
+        table = np.empty((len(visits), kps), dtype=np.uint64)
+        for i, (p, b) in enumerate(visits):
+            for sw in range(S):
+                table[i, sw] = derive_seed(cfg.seed, "sweep", p, b, sw)
+            table[i, S] = derive_seed(derive_seed(cfg.seed, "cpt_update", p, b), "sample_cpts")
+            table[i, S + 1] = derive_seed(cfg.seed, "latent_init", p, b)
+        d = eng.dev
+        self.visits = visits
+        self.table = torch.from_numpy(table.view(np.int64)).to(d)
+        self.idx = torch.zeros(1, dtype=torch.int32, device=d)
+        self.cur = torch.zeros(kps, dtype=torch.int64, device=d)
+        self.planned, self.replayed = len(visits), 0
+        self.db = SmallBatch(eng.n, m, size, d)
+        self.db.num_real = size
+        self.cbuf = [torch.zeros_like(eng.counts), torch.zeros_like(eng.counts)]
+        shape, dt = StepGraphs.obs_geometry(eng.n, size, self.obs_bits)
+        self.obs_bufs = [torch.full(shape, -1 if dt == torch.int8 else 0xFF, dtype=dt, device=d) for _ in range(2)]
+        self.ld = self.obs_bufs[0].stride(0)
+        self._int8 = None
+        if self.obs_bits < 8:  # the prepare step reads int8 rows
+            self._int8 = torch.empty((eng.n, _pitch(size)), dtype=torch.int8, device=d)
+        self.readback = list(readback)
+        self._buf_free = [None, None]
+        self._copy_stream = None
+        _lib.call("sg_keys_advance", self.table.data_ptr(), self.idx.data_ptr(), kps, self.cur.data_ptr(),
+                  stream_handle())
+        torch.cuda.synchronize()
+        self.graphs = []
+        for parity in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._record(parity)
+            self.graphs.append(g)
+        torch.cuda.synchronize()
+
+    def _record(self, p: int) -> None:
+        eng, db, m, S = self.eng, self.db, self.m, self.eng.cfg.sweeps_per_minibatch
+        s = stream_handle()
+        cur = self.cur.data_ptr()
+        obs = self.obs_bufs[p]
+        prep, prep_ld = obs, self.ld
+        if self._int8 is not None:
+            u = self._int8
+            _lib.call("sg_unpack_nibbles" if self.obs_bits == 4 else "sg_unpack_crumbs", obs.data_ptr(), obs.stride(0),
+                      u.data_ptr(), u.stride(0), eng.n, self.size, s)
+            prep, prep_ld = u, u.stride(0)
+        _lib.call("sg_small_prepare", eng.pack.small_ref, prep.data_ptr(), prep_ld, self.size, m, eng.case_base, 0, 1,
+                  db.scratch.data_ptr(), db.pattern.data_ptr(), db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld,
+                  cur + 8 * (S + 1), s)
+        new = self.cbuf[p]
+        f = eng.finish_args(new, None, 0, key_dev=cur + 8 * S, clear=self.cbuf[1 - p],
+                            cursor=(self.table, self.idx, self.kps, self.cur))
+        self._f = getattr(self, "_f", []) + [f]
+        for sw in range(S):
+            last = sw == S - 1
+            if sw:
+                eng.sweep_fence(s)
+            eng.packed_sweep(db, self.size, m, 0, cur + 8 * sw, new.data_ptr() if last else None,
+                             obs.data_ptr() if last else None, self.ld, s, obs_bits=self.obs_bits)
+        if eng.comm is not None:
+            eng.comm(new)
+        eng.step_tail(f, s)
+        for dev_t, host_t in self.readback:
+            _lib.call("sg_copy_small", host_t.data_ptr(), dev_t.data_ptr(), dev_t.numel() * dev_t.element_size(), s)
+
+    def step(self, mb) -> None:
+        """Replay the next planned visit on minibatch ``mb`` (its block is copied into the graph's buffer:
+        device blocks in stream order, host blocks on a copy stream after the buffer's last reader)."""
+        if self.replayed >= self.planned:
+            raise IndexError("all planned visits have been replayed")
+        if mb.size != self.size or int(mb.num_real) != self.size:
+            raise ValueError("stream graphs replay full minibatches of the captured size")
+        p = self.replayed % 2
+        buf = self.obs_bufs[p]
+        vals = mb.values
+        main = torch.cuda.current_stream()
+        if isinstance(vals, torch.Tensor) and vals.is_cuda:
+            if self.obs_bits < 8 and (vals.dtype != torch.uint8 or tuple(vals.shape) != tuple(buf.shape)):
+                from .io import pack_bits
+
+                vals = pack_bits(vals, buf.shape[1] * 8 // self.obs_bits, self.obs_bits)
+            if self.obs_bits < 8:
+                buf.copy_(vals, non_blocking=True)
+            else:
+                buf[:, :self.size].copy_(vals, non_blocking=True)
+        else:
+            host = vals.numpy() if isinstance(vals, torch.Tensor) else np.asarray(vals)
+            if self.obs_bits == 8:
+                cards = np.asarray(self.eng.net.cardinalities)[:, None]
+                if ((host >= cards) | (host < -1)).any():
+                    raise ValidationError("data contains a state >= its variable's cardinality")
+            src = torch.from_numpy(np.ascontiguousarray(host.astype(np.uint8 if self.obs_bits < 8 else np.int8)))
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream()
+            cs = self._copy_stream
+            if self._buf_free[p] is not None:
+                cs.wait_event(self._buf_free[p])
+            with torch.cuda.stream(cs):
+                if self.obs_bits < 8:
+                    buf.copy_(src, non_blocking=True)
+                else:
+                    buf[:, :self.size].copy_(src, non_blocking=True)
+            main.wait_stream(cs)
+        self.graphs[p].replay()
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self._buf_free[p] = ev
+        self.replayed += 1
+        _lib.launch_count += self.launches_per_step
+
+    @property
+    def launches_per_step(self) -> int:
+        S = self.eng.cfg.sweeps_per_minibatch
+        return (1 if self._int8 is not None else 0) + 3 + (S - 1) + S + 1 + len(self.readback)

@@ -92,3 +92,57 @@ def test_trace_times_are_device_events(koller):
     assert all(b >= a for a, b in zip(secs, secs[1:])) and secs[0] > 0
     assert all(r.vars_per_sec and r.vars_per_sec > 0 for r in trace.records)
     assert sg.throughput(trace).overall > 0
+
+
+@pytest.mark.parametrize("rng,src", [("joint", "device"), ("joint", "host"), ("fast", "device"), ("joint", "sgb")])
+def test_stream_graphs_equal_eager(koller, tmp_path, rng, src):
+    """Exponential accumulator on the packed / joint path: fresh visits replayed as
+    stream graphs (prepare + sweep + tail per replay, the block copied into the
+    graph each visit) equal eager visits bit for bit -- device, pinned-host and
+    .sgb (2-bit, disk) sources, with a padded last block run eagerly."""
+    from paper_1511_06416_b200 import io
+
+    net, truth = koller
+    cases = 5000
+    obs = sg.forward_sample_device(net, truth, cases, seed=15, hide_fraction=0.5, mask_seed=16)
+    cfg = sg.SamplerConfig(same_m=10, minibatch_size=1024, num_passes=4, seed=19, rng=rng,
+                           accumulator_mode="exponential", exp_decay=0.9)
+
+    def source():
+        if src == "device":
+            return sg.DeviceSource(obs, cases, 1024)
+        if src == "host":
+            return sg.HostSource.from_dense(obs[:, :cases].cpu(), 1024)
+        path = tmp_path / "c.sgb"
+        if not path.exists():
+            io.write_binary(path, obs[:, :cases].cpu().numpy().astype(np.int32), 1024, "crumb")
+        return io.BinaryFileSource(path)
+
+    a, ta, _ = _run(net, source(), cfg, truth, False)
+    b, tb, _ = _run(net, source(), cfg, truth, True)
+    for x, y in zip(a.tables, b.tables):
+        np.testing.assert_array_equal(x, y)
+    assert [r.kl_avg for r in ta.records] == [r.kl_avg for r in tb.records]
+
+
+def test_stream_graphs_sample_the_streamed_blocks(koller):
+    """Every replay samples the block it was given: two different data sets through
+    the same stream graphs give the runs of those data sets."""
+    from paper_1511_06416_b200.engine import Engine, StreamGraphs
+
+    net, truth = koller
+    cfg = sg.SamplerConfig(same_m=4, minibatch_size=2048, num_passes=1, seed=3, rng="joint",
+                           accumulator_mode="exponential", exp_decay=0.5)
+    d1 = sg.forward_sample_device(net, truth, 2048, seed=1, hide_fraction=0.4, mask_seed=2)
+    d2 = sg.forward_sample_device(net, truth, 2048, seed=7, hide_fraction=0.4, mask_seed=8)
+    mbs = [next(iter(sg.DeviceSource(d, 2048, 2048))) for d in (d1, d2, d1)]
+    eager = Engine(net, cfg)
+    for k, mb in enumerate(mbs):
+        eager.visit(mb, k, 4)
+    graphed = Engine(net, cfg)
+    graphed.visit(mbs[0], 0, 4)
+    g = StreamGraphs(graphed, 2048, 4, [(1, 0), (2, 0)])
+    g.step(mbs[1])
+    g.step(mbs[2])
+    torch.cuda.synchronize()
+    assert torch.equal(eager.cpt, graphed.cpt) and torch.equal(eager.total, graphed.total)
