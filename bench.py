@@ -739,21 +739,98 @@ def stream_arm(args, wl: Workload) -> None:
         dist.destroy_process_group()
 
 
+def stream_small_arm(args, wl: Workload) -> None:
+    """C2 streamed (``--workload c2s``): the Koller workload of C2 (m = 10, 1M-case
+    minibatches, 50 % hidden, joint stream) over ``--c2s-cases`` cases per GPU
+    (default 10^8) held as 2-bit .sgb blocks in pinned host memory, driven
+    through the public API: ``run(net, HostSource(...), cfg)`` with the
+    exponential accumulator, i.e. every step copies its minibatch host ->
+    device, decodes it and replays a stream graph (prepare + sweep + tail)
+    that samples it.  Two passes; the second (pure steady state: graph
+    capture and the first eager visit are in pass 1) is reported, timed by
+    run()'s own per-pass CUDA events."""
+    import torch
+
+    import paper_1511_06416_b200 as sg
+    from paper_1511_06416_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:  # independent replicas: every rank streams its own shard, no collective in this line
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B, M = 1_000_000, 10
+    cases = int(args.c2s_cases)
+    net, truth = WORKLOADS["c2"].network()
+    base = rank * cases
+    t0 = time.perf_counter()
+    src = sg.HostSource.from_device_blocks(
+        lambda lo, hi: sg.forward_sample_device(net, truth, hi - lo, seed=100, hide_fraction=0.5, mask_seed=200,
+                                                case_base=base + lo)[:, :hi - lo], net.num_vars, cases, B, bits=2)
+    build_s = time.perf_counter() - t0
+    cfg = sg.SamplerConfig(same_m=M, minibatch_size=B, num_passes=2, seed=300, rng="joint",
+                           accumulator_mode="exponential", exp_decay=0.9)
+    launches0 = _lib.launch_count
+    with ClockSampler(local) as clk:
+        _, trace = sg.run(net, src, cfg, engine_hook=lambda e: setattr(e, "case_base", base))
+    launches = _lib.launch_count - launches0
+    rec = trace.records[1]
+    secs = rec.seconds - trace.records[0].seconds
+    steps = (cases + B - 1) // B
+    value = world * rec.vars_sampled / secs
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        value = world * rec.vars_sampled / float(t[0])
+        dist.destroy_process_group()
+    if rank == 0:
+        h2d = net.num_vars * max(64, (B + 63) // 64 * 64) // 4
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": steps,
+            "ms_per_step": secs / steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 states, u32 draws, f64 CPTs", "data": "synthetic",
+            "config": {"workload": f"C2 streamed: koller-student, {cases} cases per GPU as 2-bit .sgb blocks in pinned "
+                                   "host memory, minibatch 1M, SAME m=10, 50% hidden, exponential accumulator "
+                                   "(decay 0.9), rng=joint, pass 2 of 2 reported",
+                       "network": "koller-student", "cases_per_gpu": cases, "m": M, "rng": "joint",
+                       "api": "run(net, HostSource.from_device_blocks(..., bits=2), cfg)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 0,
+                    "note": "already end to end: every step's minibatch is copied from pinned host memory, decoded "
+                            "and sampled; CPTs stay on the device until the end of the run"},
+            "pcie": {"h2d_gbs": h2d / (secs / steps) / 1e9},
+            "gpu_launches": launches, "launch_mode": "stream graphs (one replay per minibatch)",
+            "host_blocks_build_s": round(build_s, 1), "clocks": clk.summary(),
+        }
+        print(json.dumps(out))
+
+
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["c2s"], default="c2")
     ap.add_argument("--rng", choices=["auto", "joint", "fast", "numpy"], default="auto",
                     help="auto: joint (one draw per lane per sweep) when the network's lane word fits, else fast")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch each visit eagerly instead of graph replay")
     ap.add_argument("--c5-cases", type=int, default=10_000_000, help="C5: cases per GPU in the streamed .sgb file")
+    ap.add_argument("--c2s-cases", type=int, default=100_000_000, help="c2s: cases per GPU streamed from host memory")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.workload == "c2s":
+        if args.impl == "reference":
+            args.workload = "c2"  # the reference arm of the same C2 workload
+        else:
+            stream_small_arm(args, None)
+            return
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         reference_arm(args, wl)

@@ -327,7 +327,7 @@ int sg_small_tables(const sg_net* net, const sg_small* sp, const uint32_t* ftab,
    lane words with FAST initial draws (same draws as sg_init_states; key
    derive_seed(seed, "latent_init", pass, mb), sampler.py:211 -- read from
    init_key_dev [dev] when it is not NULL, e.g. a CUDA-graph key cursor).
-   scratch: [dev] int32 of 128 + ceil(cases / 4) words. */
+   scratch: [dev] int32 of 128 * 296 + ceil(cases / 2) words. */
 int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t ld_obs,
                      int32_t cases, int32_t m, int64_t case_base,
                      uint64_t init_key, int32_t init, int32_t* scratch,

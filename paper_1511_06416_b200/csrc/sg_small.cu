@@ -39,87 +39,128 @@ __global__ void k_small_tables(const sg_net net, const sg_small sp, const uint32
     small_table_entry(net, sp, ftab, stab, i);
 }
 
-// Pattern histogram of the minibatch's cases.
-__global__ void k_small_count(const sg_small sp, const int8_t* __restrict__ obs, int ld, int cases,
-                              uint8_t* __restrict__ pattern_of_case, int* __restrict__ hist) {
+// Cases are bucketed by latent pattern with a deterministic block partition
+// (no hot global atomics): block b of SMALL_PREP_BLOCKS owns the cases
+// [b * chunk, (b + 1) * chunk); k_small_count writes its per-pattern counts
+// cnt[P][b], k_small_scan turns them into each (pattern, block) bucket's
+// first slot, and k_small_scatter places the block's cases from there (the
+// order inside a block's share of a bucket is irrelevant: results depend on
+// case ids only).
+#define SMALL_PREP_BLOCKS 296
+__device__ __forceinline__ void small_chunk(int cases, int blocks, int b, int& lo, int& hi) {
+  const int chunk = ((cases + blocks - 1) / blocks + 255) & ~255;
+  lo = min(cases, b * chunk);
+  hi = min(cases, lo + chunk);
+}
+
+__global__ void __launch_bounds__(256) k_small_count(const sg_small sp, const int8_t* __restrict__ obs, int ld,
+                                                     int cases, uint8_t* __restrict__ pattern_of_case,
+                                                     uint8_t* __restrict__ obsw_of_case, int* __restrict__ cnt) {
   __shared__ int h[SMALL_PATTERNS];
   for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cases; c += gridDim.x * blockDim.x) {
-    uint32_t P = 0;
-    for (int v = 0; v < sp.n; ++v) P |= uint32_t(obs[int64_t(v) * ld + c] < 0) << v;
-    pattern_of_case[c] = uint8_t(P);
-    atomicAdd(&h[P], 1);
+  int lo, hi;
+  small_chunk(cases, gridDim.x, blockIdx.x, lo, hi);
+  for (int c0 = lo; c0 < hi; c0 += blockDim.x) {  // whole warps iterate (warp-aggregated counts below)
+    const int c = c0 + int(threadIdx.x);
+    uint32_t P = 0xFFFFFFFFu, obsw = 0;
+    if (c < hi) {
+      P = 0;
+      for (int v = 0; v < sp.n; ++v) {
+        const int o = obs[int64_t(v) * ld + c];
+        P |= uint32_t(o < 0) << v;
+        // observed fields of the lane word; out of range -> field 0 (the sweep's range
+        // check of this block raises SG_ERR_STATE_RANGE), never a neighbouring field
+        if (o >= 0 && o < sp.card[v]) obsw |= uint32_t(o) << sp.off[v];
+      }
+      pattern_of_case[c] = uint8_t(P);
+      obsw_of_case[c] = uint8_t(obsw);
+    }
+    // one shared-memory atomic per distinct pattern in the warp
+    const uint32_t peers = __match_any_sync(0xffffffffu, P);
+    if (P != 0xFFFFFFFFu && (threadIdx.x & 31) == uint32_t(__ffs(peers) - 1)) atomicAdd(&h[P], __popc(peers));
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x)
-    if (h[i]) atomicAdd(hist + i, h[i]);
+  for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x) cnt[i * gridDim.x + blockIdx.x] = h[i];
 }
 
-__global__ void k_small_scan(int* hist) {
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int i = 0; i < SMALL_PATTERNS; ++i) {
-      const int x = hist[i];
-      hist[i] = run;
-      run += x;
+// Warp w scans patterns w, w + 32, ...: the exclusive scan of each pattern's
+// per-block counts, then the pattern offsets (exclusive over the pattern
+// totals) are added to every entry.
+__global__ void __launch_bounds__(1024) k_small_scan(int* __restrict__ cnt, int blocks, int patterns) {
+  __shared__ int total[SMALL_PATTERNS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int P = warp; P < patterns; P += 32) {
+    int* row = cnt + P * blocks;
+    int carry = 0;
+    for (int b0 = 0; b0 < blocks; b0 += 32) {
+      const int b = b0 + lane;
+      const int x = b < blocks ? row[b] : 0;
+      int inc = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (b < blocks) row[b] = carry + inc - x;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
+    if (lane == 0) total[P] = carry;
+  }
+  __syncthreads();
+  for (int P = warp; P < patterns; P += 32) {
+    int off = 0;
+    for (int q = 0; q < P; ++q) off += total[q];
+    int* row = cnt + P * blocks;
+    for (int b = lane; b < blocks; b += 32) row[b] += off;
   }
 }
 
-// Scatter cases into pattern buckets and build their lanes: observed fields
+// Place the cases into their pattern buckets (pattern[s], case_id[s]).
+__global__ void __launch_bounds__(256) k_small_scatter(const int cases, const uint8_t* __restrict__ pattern_of_case,
+                                                       const int* __restrict__ cursor, uint8_t* __restrict__ pattern,
+                                                       int32_t* __restrict__ case_id) {
+  __shared__ int cnt[SMALL_PATTERNS];
+  for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x) cnt[i] = cursor[i * gridDim.x + blockIdx.x];
+  __syncthreads();
+  int lo, hi;
+  small_chunk(cases, gridDim.x, blockIdx.x, lo, hi);
+  for (int c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+    const uint32_t P = pattern_of_case[c];
+    const int s = atomicAdd(&cnt[P], 1);
+    pattern[s] = uint8_t(P);
+    case_id[s] = c;
+  }
+}
+
+// Build the lanes of every slot (in bucket order, so a warp's slots share a
+// latent pattern and its variable loop does not diverge): observed fields
 // from the data, latent fields from the FAST init stream (same draw as
 // k_init_states: Philox4x32(key, (case, v, r/4, purpose 1))[r%4] * card >> 32).
-// Slots are claimed per block (shared-memory ranks, one global atomic per
-// pattern per block); the order inside a bucket is irrelevant to the
-// results, which depend on case ids only.
-__global__ void __launch_bounds__(256) k_small_scatter(
-    const sg_small sp, const int8_t* __restrict__ obs, int ld, int cases, int m, int64_t case_base,
-    uint64_t init_key, const uint8_t* __restrict__ pattern_of_case, int* __restrict__ cursor,
-    uint8_t* __restrict__ pattern, int32_t* __restrict__ case_id, uint8_t* __restrict__ lanes, int lane_ld, int init,
-    const uint64_t* __restrict__ init_key_dev) {
-  __shared__ int cnt[SMALL_PATTERNS];
+__global__ void __launch_bounds__(256) k_small_init_lanes(
+    const sg_small sp, const uint8_t* __restrict__ obsw_of_case, int cases, int m, int64_t case_base,
+    uint64_t init_key, const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id,
+    uint8_t* __restrict__ lanes, int lane_ld, const uint64_t* __restrict__ init_key_dev) {
   if (init_key_dev) init_key = *init_key_dev;  // graph replay: the key cursor's init key
-  __shared__ int base[SMALL_PATTERNS];
-  for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x) cnt[i] = 0;
-  __syncthreads();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t P = 0;
-  int local = 0;
-  if (c < cases) {
-    P = pattern_of_case[c];
-    local = atomicAdd(&cnt[P], 1);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x)
-    base[i] = cnt[i] ? atomicAdd(cursor + i, cnt[i]) : 0;
-  __syncthreads();
-  if (c >= cases) return;
-  const int s = base[P] + local;
-  pattern[s] = uint8_t(P);
-  case_id[s] = c;
-  if (!init) return;
-  uint32_t obsw = 0;
-  for (int v = 0; v < sp.n; ++v) {
-    const int o = obs[int64_t(v) * ld + c];
-    // out of range -> field 0 (the sweep's range check of this block raises
-    // SG_ERR_STATE_RANGE); it never spills into a neighbouring field
-    if (o >= 0 && o < sp.card[v]) obsw |= uint32_t(o) << sp.off[v];
-  }
   uint32_t* out = reinterpret_cast<uint32_t*>(lanes);
-  for (int q = 0; q < (m + 3) / 4; ++q) {
-    uint32_t S[4] = {obsw, obsw, obsw, obsw};
-    for (int v = 0; v < sp.n; ++v) {
-      if (!((P >> v) & 1u)) continue;
-      const u32x4 w = fast_block(init_key, uint64_t(case_base + c), uint32_t(v), uint32_t(q), 1u);
-      const uint32_t ws[4] = {w.a, w.b, w.c, w.d};
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < cases; s += gridDim.x * blockDim.x) {
+    const uint32_t P = pattern[s];
+    const int c = case_id[s];
+    const uint32_t obsw = obsw_of_case[c];
+    for (int q = 0; q < (m + 3) / 4; ++q) {
+      uint32_t S[4] = {obsw, obsw, obsw, obsw};
+      for (int v = 0; v < sp.n; ++v) {
+        if (!((P >> v) & 1u)) continue;
+        const u32x4 w = fast_block(init_key, uint64_t(case_base + c), uint32_t(v), uint32_t(q), 1u);
+        const uint32_t ws[4] = {w.a, w.b, w.c, w.d};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) S[j] |= uint32_t((uint64_t(ws[j]) * uint32_t(sp.card[v])) >> 32) << sp.off[v];
+        for (int j = 0; j < 4; ++j) S[j] |= uint32_t((uint64_t(ws[j]) * uint32_t(sp.card[v])) >> 32) << sp.off[v];
+      }
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) word |= (q * 4 + j < m ? (S[j] & 0xFFu) : 0u) << (8 * j);
+      out[int64_t(q) * lane_ld + s] = word;
     }
-    uint32_t word = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) word |= (q * 4 + j < m ? (S[j] & 0xFFu) : 0u) << (8 * j);
-    out[int64_t(q) * lane_ld + s] = word;
   }
 }
 
@@ -1419,14 +1460,16 @@ extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t l
   SG_REQUIRE(fast_cases_ok(case_base, cases), "sg_small_prepare: global case index beyond 2^32");
   if (cases == 0) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  int* hist = scratch;                                                  // [SMALL_PATTERNS]
-  uint8_t* poc = reinterpret_cast<uint8_t*>(scratch + SMALL_PATTERNS);  // [cases]
-  cudaMemsetAsync(hist, 0, sizeof(int) * SMALL_PATTERNS, s);
-  const int blocks = std::min((cases + 255) / 256, 148 * 8);
-  k_small_count<<<blocks, 256, 0, s>>>(*sp, obs, ld_obs, cases, poc, hist);
-  k_small_scan<<<1, 32, 0, s>>>(hist);
-  k_small_scatter<<<(cases + 255) / 256, 256, 0, s>>>(*sp, obs, ld_obs, cases, m, case_base, init_key, poc, hist,
-                                                       pattern, case_id, lanes, lane_ld, init, init_key_dev);
+  const int blocks = std::min((cases + 255) / 256, SMALL_PREP_BLOCKS);
+  int* cnt = scratch;                                                                     // [SMALL_PATTERNS][blocks]
+  uint8_t* poc = reinterpret_cast<uint8_t*>(scratch + SMALL_PATTERNS * SMALL_PREP_BLOCKS);  // [cases] patterns
+  uint8_t* ow = poc + cases;                                                               // [cases] observed fields
+  k_small_count<<<blocks, 256, 0, s>>>(*sp, obs, ld_obs, cases, poc, ow, cnt);
+  k_small_scan<<<1, 1024, 0, s>>>(cnt, blocks, 1 << sp->n);
+  k_small_scatter<<<blocks, 256, 0, s>>>(cases, poc, cnt, pattern, case_id);
+  if (init)
+    k_small_init_lanes<<<std::min((cases + 255) / 256, 148 * 8), 256, 0, s>>>(
+        *sp, ow, cases, m, case_base, init_key, pattern, case_id, lanes, lane_ld, init_key_dev);
   return check_launch("sg_small_prepare");
 }
 

@@ -59,7 +59,8 @@ class SmallBatch:
         self.lanes = torch.empty(((m + 3) // 4, self.lane_ld), dtype=torch.int32, device=dev)
         self.pattern = torch.empty(max(1, cases), dtype=torch.uint8, device=dev)
         self.case_id = torch.empty(max(1, cases), dtype=torch.int32, device=dev)
-        self.scratch = torch.empty(128 + (cases + 3) // 4 + 1, dtype=torch.int32, device=dev)
+        # sg_small_prepare: per-(pattern, block) bucket counts + the pattern of each case
+        self.scratch = torch.empty(128 * 296 + (cases + 1) // 2 + 1, dtype=torch.int32, device=dev)
         self.nmiss = torch.zeros(n, dtype=torch.int64, device=dev)
         self.num_real = cases
         self.dev = dev
@@ -941,4 +942,4 @@ class StreamGraphs:
     @property
     def launches_per_step(self) -> int:
         S = self.eng.cfg.sweeps_per_minibatch
-        return (1 if self._int8 is not None else 0) + 3 + (S - 1) + S + 1 + len(self.readback)
+        return (1 if self._int8 is not None else 0) + 4 + (S - 1) + S + 1 + len(self.readback)
