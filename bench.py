@@ -608,6 +608,9 @@ def our_arm(args, wl: Workload) -> None:
                     "host_format": (f"{graphs.obs_bits}-bit .sgb block" if graphs is not None and graphs.nibbles
                                     else "int8 block"),
                     "d2h_bytes_per_step": eng.pack.cells * 8, "ms_per_step": e2e_ms,
+                    "mode": ("the C2 minibatch (moving sum, lanes resident) re-uploaded from pinned memory and "
+                             "range-checked every step, CPTs read back every step; `--workload c2s` streams "
+                             "different minibatches that each step samples"),
                     "host_enqueue_us_per_step": host_enqueue_us, "h2d_warmup": h2d_warm},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",

@@ -506,7 +506,14 @@ class StepGraphs:
         ``host_block`` (pinned, the private buffers' layout): every step()
         also uploads this block into the OTHER parity's buffer -- the next
         visit's input -- on a copy stream (a copy engine), overlapped with
-        the replay, ordered by events.  ``readback``: pairs
+        the replay, ordered by events.  The copy is asynchronous: a caller
+        that refills ``host_block`` between steps must first wait for
+        :attr:`upload_done` (the event of the last upload).  With the moving
+        sum the replayed minibatch keeps its lanes resident, so the uploaded
+        block is range-checked each visit but its observed values are the
+        resident ones (the reference re-reads the same data every pass); a
+        stream of different minibatches is replayed by :class:`StreamGraphs`,
+        which samples each uploaded block.  ``readback``: pairs
         (device tensor, pinned host tensor) copied back at the end of each
         replay (e.g. the CPTs).  ``timing``: external timing events bracket the
         sweep node(s) inside each graph; :meth:`sweep_ms` reads the last
@@ -723,6 +730,7 @@ class StepGraphs:
             if dbg is not None:
                 ev[1].record(up)
             self._uploaded[q].record(up)
+            self.upload_done = self._uploaded[q]
             self._up_pending[q] = True
             if self._up_pending[p]:
                 main.wait_event(self._uploaded[p])
