@@ -593,6 +593,7 @@ class StepGraphs:
             if not host_t.is_pinned() or host_t.numel() * host_t.element_size() < dev_t.numel() * dev_t.element_size():
                 raise ValueError("readback targets must be pinned host tensors large enough")
         self._copy_stream = None
+        self.upload_done = None  # event of the last host_block upload (see the docstring)
         self._buf_free: list = [None, None]  # event: the last replay reading buffer p has finished
         self.graphs = []
         self._finish_args = []
