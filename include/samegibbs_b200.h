@@ -129,6 +129,21 @@ typedef struct sg_net {
   int64_t blob32_words;
   const int64_t* blob64;
   int64_t blob64_words;
+  /* Blanket factor tables of the big-tile sweep (n > 32, cards <= 4; outside
+     the blobs; bft_rows = 0: not built).  Row r holds 4 doubles, the CPT cells
+     bft_src[2r] + t * (bft_src[2r+1] & (2^26 - 1)) for t < bft_src[2r+1] >> 26
+     (zero padded): one factor of a weight product (sampler.py:226-240) as v
+     runs over its states.  The program of v at bft_desc[bft_start[v]] (int4
+     records): [card, npar, nchl, own row base], ceil(npar/2) x [u, stride, u,
+     stride], per child [c, row base, nrec, 0] + nrec x [u, stride, u, stride]
+     (child row = base + x_c + sum x_u * stride).  bft is device scratch that
+     every large-network sg_sweep rewrites from its cpt argument (one stream
+     per pack at a time). */
+  int64_t bft_rows;
+  const int32_t* bft_start;  /* [n+1] */
+  const int32_t* bft_desc;
+  const int32_t* bft_src;    /* [bft_rows][2] */
+  double* bft;               /* [dev] [bft_rows][4] */
 } sg_net;
 
 #define SG_JOINT_MAX 128

@@ -47,7 +47,9 @@ class SgNet(ctypes.Structure):
     ] + [(name, c_void_p) for name in NET_POINTERS] + [("joint_size", c_int64)] + \
         [(name, c_void_p) for name in NET_POINTERS_TAIL] + \
         [("tally_chunks", c_int64), ("tally_chunk", c_void_p)] + \
-        [("blob32", c_void_p), ("blob32_words", c_int64), ("blob64", c_void_p), ("blob64_words", c_int64)]
+        [("blob32", c_void_p), ("blob32_words", c_int64), ("blob64", c_void_p), ("blob64_words", c_int64)] + \
+        [("bft_rows", c_int64), ("bft_start", c_void_p), ("bft_desc", c_void_p), ("bft_src", c_void_p),
+         ("bft", c_void_p)]
 
 
 class SgBatch(ctypes.Structure):

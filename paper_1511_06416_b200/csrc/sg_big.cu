@@ -69,6 +69,195 @@ __device__ __forceinline__ uint32_t flag_bits16(const int4 val) {
   return f;
 }
 
+// ---- blanket factor tables (sg_net.bft, cards <= 4)
+// Row r = the CPT cells src[2r] + t * step, t < k (zero padded to 4): one
+// factor of the weight product as v runs over its states.  Rebuilt from the
+// CPTs before every big-tile sweep (3.5 MB on C4: a few microseconds).
+__global__ void __launch_bounds__(256) k_build_bft(const sg_net net, const double* __restrict__ cpt) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < net.bft_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int2 s = __ldg(reinterpret_cast<const int2*>(net.bft_src) + r);
+    const int step = s.y & ((1 << 26) - 1), k = s.y >> 26;
+    double f[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) f[t] = t < k ? __ldg(cpt + s.x + int64_t(t) * step) : 0.0;
+    double2* o = reinterpret_cast<double2*>(net.bft) + 2 * r;
+    o[0] = make_double2(f[0], f[1]);
+    o[1] = make_double2(f[2], f[3]);
+  }
+}
+
+__device__ __forceinline__ void bft_row(const double* __restrict__ bft, int row, double (&f)[4]) {
+  const double2* p = reinterpret_cast<const double2*>(bft) + 2 * row;
+  const double2 a = __ldg(p), b = __ldg(p + 1);
+  f[0] = a.x;
+  f[1] = a.y;
+  f[2] = b.x;
+  f[3] = b.y;
+}
+
+// Row index of one child factor: base + x_c + sum x_u * stride over the
+// child's other parents (records of two; an unused half has stride 0).
+template <class Get>
+__device__ __forceinline__ int bft_child(const int4*& p, Get get) {
+  const int4 c = __ldg(p++);
+  int i = c.y + get(c.x);
+#pragma unroll 1
+  for (int q = 0; q < c.z; ++q, ++p) {
+    const int4 r = __ldg(p);
+    i += get(r.x) * r.y;
+    if (r.w) i += get(r.z) * r.w;
+  }
+  return i;
+}
+
+// The factored draw (draw_factored: sampler.py:226-247) over the blanket
+// factor tables: one 32-byte row per factor, products in the reference's
+// order (own row, then children in order), numpy's sequential sum, the
+// cumulative comparisons.  Zero padding leaves every result bit-identical to
+// draw_factored for cards 2..4: padded weights add exact zeros and their
+// comparisons are never true (u * norm <= norm).
+template <class Get>
+__device__ __forceinline__ int draw_bft(const int4* __restrict__ prog, const double* __restrict__ bft, Get get,
+                                        double u, bool& zs) {
+  const int4 h = __ldg(prog);  // card, npar, nchl, own row base
+  const int4* p = prog + 1;
+  int row = h.w;
+#pragma unroll 1
+  for (int j = 0; j < h.y; j += 2, ++p) {
+    const int4 r = __ldg(p);
+    row += get(r.x) * r.y;
+    if (r.w) row += get(r.z) * r.w;
+  }
+  double w[4];
+  bft_row(bft, row, w);
+  int k = 0;
+#pragma unroll 1
+  for (; k + 1 < h.z; k += 2) {  // two children per step: both gathers in flight
+    const int i0 = bft_child(p, get);
+    const int i1 = bft_child(p, get);
+    double f0[4], f1[4];
+    bft_row(bft, i0, f0);
+    bft_row(bft, i1, f1);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) w[t] = __dmul_rn(__dmul_rn(w[t], f0[t]), f1[t]);
+  }
+  if (k < h.z) {
+    const int i0 = bft_child(p, get);
+    double f0[4];
+    bft_row(bft, i0, f0);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) w[t] = __dmul_rn(w[t], f0[t]);
+  }
+  const double norm = __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1]), w[2]), w[3]);
+  if (!(norm > 0.0)) zs = true;
+  const double au = __dmul_rn(u, norm);
+  double cum = w[0];
+  int x = au > cum;
+  cum = __dadd_rn(cum, w[1]);
+  x += au > cum;
+  cum = __dadd_rn(cum, w[2]);
+  x += au > cum;
+  return x;
+}
+
+// 2-bit tiles: whole-word bit tricks instead of per-case shifts.  A product
+// (x & 0x03030303) * 0x01041040 carries no bits (its partial products occupy
+// distinct positions) and leaves the four 2-bit fields of x in byte 3;
+// (x & 0x80808080) * 0x00204081 leaves the four flag bits in bits 28..31.
+__device__ __forceinline__ uint32_t crumb_word(const int4 val) {
+  const uint32_t p0 = (uint32_t(val.x) & 0x03030303u) * 0x01041040u;
+  const uint32_t p1 = (uint32_t(val.y) & 0x03030303u) * 0x01041040u;
+  const uint32_t p2 = (uint32_t(val.z) & 0x03030303u) * 0x01041040u;
+  const uint32_t p3 = (uint32_t(val.w) & 0x03030303u) * 0x01041040u;
+  return __byte_perm(__byte_perm(p0, p1, 0x0073), __byte_perm(p2, p3, 0x0073), 0x5410);
+}
+__device__ __forceinline__ uint32_t flag_word16(const int4 val) {
+  const uint32_t g0 = (uint32_t(val.x) & 0x80808080u) * 0x00204081u;
+  const uint32_t g1 = (uint32_t(val.y) & 0x80808080u) * 0x00204081u;
+  const uint32_t g2 = (uint32_t(val.z) & 0x80808080u) * 0x00204081u;
+  const uint32_t g3 = (uint32_t(val.w) & 0x80808080u) * 0x00204081u;
+  return (g0 >> 28) | ((g1 >> 24) & 0xF0u) | ((g2 >> 20) & 0xF00u) | ((g3 >> 16) & 0xF000u);
+}
+// Inverse: 4 cases (byte k of the crumb word, flag nibble k) -> 4 int8 states
+// (fields spread to bytes with two shifted ORs; flags by a carry-free product).
+__device__ __forceinline__ uint32_t state_bytes4(uint32_t crumbs, uint32_t flags, int k) {
+  uint32_t x = __byte_perm(crumbs, 0u, 0x4440u | uint32_t(k));
+  x |= x << 6;
+  x = (x | (x << 12)) & 0x03030303u;
+  return x | ((((flags >> (4 * k)) & 0xFu) * 0x10204080u) & 0x80808080u);
+}
+
+// Two latent cases of the same variable drawn in lockstep (2-bit tiles): one
+// pass over v's program serves both, and both cases' factor rows are in flight
+// together.  Tile word offsets ra / rb and field shifts sa / sb locate the
+// cases; per case the arithmetic is draw_bft's.
+__device__ __forceinline__ int2 get2(const uint32_t* st, int o, int ra, int rb, int sa, int sb) {
+  return make_int2(int((st[o + ra] >> sa) & 3u), int((st[o + rb] >> sb) & 3u));
+}
+__device__ __forceinline__ int bft_finish(const double (&w)[4], double u, bool& zs) {
+  const double norm = __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1]), w[2]), w[3]);
+  if (!(norm > 0.0)) zs = true;
+  const double au = __dmul_rn(u, norm);
+  double cum = w[0];
+  int x = au > cum;
+  cum = __dadd_rn(cum, w[1]);
+  x += au > cum;
+  cum = __dadd_rn(cum, w[2]);
+  x += au > cum;
+  return x;
+}
+__device__ __forceinline__ int2 draw_bft2(const int4* __restrict__ prog, const double* __restrict__ bft,
+                                          const uint32_t* st, int rs, int ra, int rb, int sa, int sb, double ua,
+                                          double ub, bool& zs) {
+  const int4 h = __ldg(prog);  // card, npar, nchl, own row base
+  const int4* p = prog + 1;
+  int ia = h.w, ib = h.w;
+#pragma unroll 1
+  for (int j = 0; j < h.y; j += 2, ++p) {
+    const int4 r = __ldg(p);
+    int2 g = get2(st, r.x * rs, ra, rb, sa, sb);
+    ia += g.x * r.y;
+    ib += g.y * r.y;
+    if (r.w) {
+      g = get2(st, r.z * rs, ra, rb, sa, sb);
+      ia += g.x * r.w;
+      ib += g.y * r.w;
+    }
+  }
+  double wa[4], wb[4];
+  bft_row(bft, ia, wa);
+  bft_row(bft, ib, wb);
+#pragma unroll 1
+  for (int k = 0; k < h.z; ++k) {
+    const int4 c = __ldg(p++);
+    int2 g = get2(st, c.x * rs, ra, rb, sa, sb);
+    ia = c.y + g.x;
+    ib = c.y + g.y;
+#pragma unroll 1
+    for (int q = 0; q < c.z; ++q, ++p) {
+      const int4 r = __ldg(p);
+      g = get2(st, r.x * rs, ra, rb, sa, sb);
+      ia += g.x * r.y;
+      ib += g.y * r.y;
+      if (r.w) {
+        g = get2(st, r.z * rs, ra, rb, sa, sb);
+        ia += g.x * r.w;
+        ib += g.y * r.w;
+      }
+    }
+    double fa[4], fb[4];
+    bft_row(bft, ia, fa);
+    bft_row(bft, ib, fb);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      wa[t] = __dmul_rn(wa[t], fa[t]);
+      wb[t] = __dmul_rn(wb[t], fb[t]);
+    }
+  }
+  return make_int2(bft_finish(wa, ua, zs), bft_finish(wb, ub, zs));
+}
+
 template <int MODE, int BITS>
 __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net net, const sg_batch bt, const SweepArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -88,30 +277,39 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
   const int cpr = tc >> 4;  // 16-case chunks per row
   if (tid == 0) s_err = 0;
 
-  // ---- stage the tile: one int4 (16 cases) per thread step, packed on the fly
-  for (int i = tid; i < n * mg * cpr; i += BIG_T) {
-    const int row = i / cpr, ch = i - row * cpr;
-    const int v = row / mg, r = row - v * mg;
-    int4 val = make_int4(0, 0, 0, 0);
-    if (ch * 16 < nload)
-      val = __ldcs(reinterpret_cast<const int4*>(bt.states + (int64_t(v) * bt.m + rg0 + r) * bt.pitch + c0 + ch * 16));
-    if (r == 0) {  // every replica carries the shared latent mask
-      uint32_t f = flag_bits16(val);
-      const int cc = ch * 16;
-      if (cc + 16 > ncase) f &= cc >= ncase ? 0u : ((1u << (ncase - cc)) - 1u);
-      fl16[v * cpr + ch] = uint16_t(f);
+  // ---- stage the tile: a warp per variable row, one int4 (16 cases) per lane step
+  for (int v = warp; v < n; v += BIG_W) {
+    for (int r = 0; r < mg; ++r) {
+      for (int ch = lane; ch < cpr; ch += 32) {
+        int4 val = make_int4(0, 0, 0, 0);
+        if (ch * 16 < nload)
+          val = __ldcs(reinterpret_cast<const int4*>(bt.states + (int64_t(v) * bt.m + rg0 + r) * bt.pitch + c0 +
+                                                     ch * 16));
+        if (r == 0) {  // every replica carries the shared latent mask
+          uint32_t f = BITS == 2 ? flag_word16(val) : flag_bits16(val);
+          const int cc = ch * 16;
+          if (cc + 16 > ncase) f &= cc >= ncase ? 0u : ((1u << (ncase - cc)) - 1u);
+          fl16[v * cpr + ch] = uint16_t(f);
+        }
+        uint32_t* dst = st + size_t(v * a.mg + r) * wpr + ch * (16 / PER);
+        if constexpr (BITS == 2) {
+          dst[0] = crumb_word(val);
+        } else {
+          val.x &= 0x7F7F7F7F;
+          val.y &= 0x7F7F7F7F;
+          val.z &= 0x7F7F7F7F;
+          val.w &= 0x7F7F7F7F;
+          pack16<BITS>(val, dst);
+        }
+      }
     }
-    val.x &= 0x7F7F7F7F;
-    val.y &= 0x7F7F7F7F;
-    val.z &= 0x7F7F7F7F;
-    val.w &= 0x7F7F7F7F;
-    pack16<BITS>(val, st + size_t(v * a.mg + r) * wpr + ch * (16 / PER));
   }
   const uint32_t* fl = reinterpret_cast<const uint32_t*>(fl16);  // [n][tc / 32]
   const int fw = tc >> 5;
   uint16_t* wl = reinterpret_cast<uint16_t*>(sm + size_t(n) * a.mg * wpr + size_t(n) * fw) + warp * tc;
   const uint64_t key = a.fast_key_dev ? __ldg(a.fast_key_dev) : a.fast_key;
   const bool zs_armed = a.ftab && net.table_entries > 0 && __ldg(a.ftab + net.ftab_size) != 0u;
+  constexpr bool use_bft = BITS == 2;  // 2-bit tiles draw from the blanket factor tables (sweep_big)
   bool zs = false;
   __syncthreads();
 
@@ -140,7 +338,8 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
       __syncwarp();
       const int32_t* dv = net.var_desc + v * SG_DESC_WORDS;
       const int card = dv[0], nmb = dv[1];
-      const int32_t* fd = nmb < 0 ? net.fac_desc + __ldg(net.fac_start + v) : nullptr;
+      const int32_t* fd = !use_bft && nmb < 0 ? net.fac_desc + __ldg(net.fac_start + v) : nullptr;
+      const int4* prog = use_bft ? reinterpret_cast<const int4*>(net.bft_desc + __ldg(net.bft_start + v)) : nullptr;
       int64_t nmiss = 0, ioff = 0;
       uint64_t k0 = 0, k1 = 0;
       if (MODE != SG_RNG_FAST) {
@@ -153,15 +352,59 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
         }
       }
       const int rs = a.mg * wpr;  // words between variable rows of the tile (32-bit offsets throughout)
+      if constexpr (use_bft) {
+        if (nmb < 0) {
+          // two cases per lane: it and it + 32 of the warp's 64-entry stride
+          for (int it = lane; it < total; it += 64) {
+            const bool two = it + 32 < total;
+            const int ca = wl[it], cb = wl[two ? it + 32 : it];
+            const int cwa = ca / PER, sa = (ca % PER) * BITS, cwb = cb / PER, sb = (cb % PER) * BITS;
+            int64_t rka = 0, rkb = 0;
+            if (MODE != SG_RNG_FAST) {
+              rka = __ldg(bt.rank + int64_t(v) * bt.ld_rank + c0 + ca);
+              rkb = __ldg(bt.rank + int64_t(v) * bt.ld_rank + c0 + cb);
+            }
+            const uint64_t ga = uint64_t(bt.case_base + c0 + ca), gb = uint64_t(bt.case_base + c0 + cb);
+            for (int l = 0; l < mg; ++l) {
+              const int r = rg0 + l;
+              double ua, ub;
+              if (MODE == SG_RNG_FAST) {
+                ua = double(pick(fast_block(key, ga, uint32_t(v), uint32_t(r >> 2), 0u), r & 3)) * 0x1.0p-32;
+                ub = double(pick(fast_block(key, gb, uint32_t(v), uint32_t(r >> 2), 0u), r & 3)) * 0x1.0p-32;
+              } else if (MODE == SG_RNG_NUMPY) {
+                ua = np_uniform(uint64_t(int64_t(r) * nmiss + rka), k0, k1);
+                ub = np_uniform(uint64_t(int64_t(r) * nmiss + rkb), k0, k1);
+              } else {
+                ua = __ldg(a.uniforms + ioff + int64_t(r) * nmiss + rka);
+                ub = __ldg(a.uniforms + ioff + int64_t(r) * nmiss + rkb);
+              }
+              const int2 x = draw_bft2(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs);
+              uint32_t* wa = st + v * rs + l * wpr + cwa;
+              const uint32_t da = ((*wa >> sa) ^ uint32_t(x.x)) & MASK;
+              if (da) atomicXor(wa, da << sa);
+              if (two) {
+                uint32_t* wb = st + v * rs + l * wpr + cwb;
+                const uint32_t db = ((*wb >> sb) ^ uint32_t(x.y)) & MASK;
+                if (db) atomicXor(wb, db << sb);
+              }
+            }
+          }
+          __syncwarp();
+          int nx = 0;
+          if (lane == 0) nx = atomicAdd(&s_next, 1);
+          vi = __shfl_sync(0xffffffffu, nx, 0);
+          continue;
+        }
+      }
       for (int it = lane; it < total; it += 32) {
         const int c = wl[it];
         const int cw = c / PER, csh = (c % PER) * BITS;
         int64_t rank = 0;
         if (MODE != SG_RNG_FAST) rank = __ldg(bt.rank + int64_t(v) * bt.ld_rank + c0 + c);
         const uint64_t gcase = uint64_t(bt.case_base + c0 + c);
+        u32x4 blk{};
         // the tile's replicas of (v, c): replica r takes word r % 4 of the Philox block of its
-        // global quad (FAST counters); the block is recomputed per replica so that no block
-        // state stays live across the draw (register pressure: 64 registers at 1024 threads)
+        // global quad (FAST counters), one block per quad of the tile's replicas
         for (int l = 0; l < mg; ++l) {
           const int r = rg0 + l;
           const int roff = l * wpr + cw;  // + u * rs selects variable u
@@ -169,7 +412,8 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
           double u01;
           uint32_t u31 = 0;
           if (MODE == SG_RNG_FAST) {
-            const uint32_t wv = pick(fast_block(key, gcase, uint32_t(v), uint32_t(r >> 2), 0u), r & 3);
+            if (l == 0 || (r & 3) == 0) blk = fast_block(key, gcase, uint32_t(v), uint32_t(r >> 2), 0u);
+            const uint32_t wv = pick(blk, r & 3);
             u31 = wv >> 1;
             u01 = double(wv) * 0x1.0p-32;
           } else {
@@ -193,12 +437,15 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
               const double au = __dmul_rn(u01, norm);
               for (int q = 0; q < card - 1; ++q) x += au > __ldg(p + q);
             }
+          } else if constexpr (use_bft) {
+            x = draw_bft(prog, net.bft, get, u01, zs);
           } else {
             x = draw_factored<4>(fd, a.cpt, get, u01, zs);
           }
+          // lanes of one state word update disjoint fields: one XOR of (old ^ new) each
           uint32_t* wp = st + v * rs + roff;
-          atomicAnd(wp, ~(MASK << csh));
-          atomicOr(wp, uint32_t(x) << csh);
+          const uint32_t d = ((*wp >> csh) ^ uint32_t(x)) & MASK;
+          if (d) atomicXor(wp, d << csh);
         }
       }
       __syncwarp();
@@ -211,20 +458,27 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
   if (zs) atomicOr(&s_err, int(SG_ERR_ZERO_SUPPORT));
 
   // ---- write the tile back (flags restored)
-  for (int i = tid; i < n * mg * cpr; i += BIG_T) {
-    const int row = i / cpr, ch = i - row * cpr;
-    if (ch * 16 >= nload) continue;
-    const int v = row / mg, r = row - v * mg;
-    const uint32_t f = fl16[v * cpr + ch];
-    const uint32_t* src = st + size_t(v * a.mg + r) * wpr + ch * (16 / PER);
-    uint32_t o[4] = {0u, 0u, 0u, 0u};
+  for (int v = warp; v < n; v += BIG_W) {
+    for (int r = 0; r < mg; ++r) {
+      for (int ch = lane; ch * 16 < nload; ch += 32) {
+        const uint32_t f = fl16[v * cpr + ch];
+        const uint32_t* src = st + size_t(v * a.mg + r) * wpr + ch * (16 / PER);
+        uint32_t o[4] = {0u, 0u, 0u, 0u};
+        if constexpr (BITS == 2) {
+          const uint32_t w = src[0];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t x = BITS == 2 ? (src[0] >> (2 * k)) & 3u : (src[k >> 3] >> (4 * (k & 7))) & 15u;
-      o[k >> 2] |= (x | (((f >> k) & 1u) << 7)) << (8 * (k & 3));
+          for (int k = 0; k < 4; ++k) o[k] = state_bytes4(w, f, k);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const uint32_t x = (src[k >> 3] >> (4 * (k & 7))) & 15u;
+            o[k >> 2] |= (x | (((f >> k) & 1u) << 7)) << (8 * (k & 3));
+          }
+        }
+        __stcs(reinterpret_cast<int4*>(bt.states + (int64_t(v) * bt.m + rg0 + r) * bt.pitch + c0 + ch * 16),
+               make_int4(int(o[0]), int(o[1]), int(o[2]), int(o[3])));
+      }
     }
-    __stcs(reinterpret_cast<int4*>(bt.states + (int64_t(v) * bt.m + rg0 + r) * bt.pitch + c0 + ch * 16),
-           make_int4(int(o[0]), int(o[1]), int(o[2]), int(o[3])));
   }
   __syncthreads();
   if (tid == 0 && s_err) atomicOr(a.err, s_err);
@@ -241,7 +495,8 @@ static void launch_big(const sg_net& net, const sg_batch& bt, const SweepArgs& a
 
 bool sweep_big(const sg_net& net, const sg_batch& bt, const SweepArgs& a0, int rng_mode, cudaStream_t s) {
   if (net.n <= 32 || net.max_card > 16) return false;
-  const int bits = net.max_card <= 4 ? 2 : 4;
+  // 2-bit tiles need the blanket factor tables (built with the pack when cards <= 4)
+  const int bits = net.max_card <= 4 && net.bft_rows > 0 && net.bft ? 2 : 4;
   constexpr size_t budget = SG_BIG_SMEM;
   auto smem_of = [&](int mg, int tc) { return bits == 2 ? big_smem<2>(net.n, mg, tc) : big_smem<4>(net.n, mg, tc); };
   // widest tile (<= 1024 cases, multiple of 32) over all replicas; replica
@@ -258,6 +513,10 @@ bool sweep_big(const sg_net& net, const sg_batch& bt, const SweepArgs& a0, int r
   if (!tc) return false;
   // do not make tiles much wider than the batch
   while (tc > 64 && tc - 32 >= bt.cases) tc -= 32;
+  if (bits == 2) {
+    const int64_t blocks = (net.bft_rows + 255) / 256;
+    k_build_bft<<<int(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, s>>>(net, a0.cpt);
+  }
   SweepArgs a = a0;
   a.tc = tc;
   a.mg = mg;

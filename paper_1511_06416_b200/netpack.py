@@ -263,6 +263,80 @@ def layout(net: Network, coloring: Coloring | None = None,
                      int32=int32, int64=int64, scalars=scalars)
 
 
+BFT_MIN_VARS = 33  # the big-tile sweep's networks (sg_big.cu: n > 32)
+
+
+def blanket_factor_plan(net: Network, lay: NetLayout):
+    """Blanket factor tables of the big-tile sweep (sg_big.cu, cards <= 4).
+
+    Every factor of v's weight product (sampler.py:226-240) -- v's own CPT row
+    and, per child c, c's CPT entry as v runs over its states -- becomes one
+    row of 4 doubles (states of v, zero padded), so a draw gathers one
+    contiguous 32-byte row per factor instead of card strided cells.  Rows are
+    exact copies of CPT cells (``k_build_bft`` refreshes them from the CPTs at
+    each large-network sweep), so the product and every draw are unchanged.
+
+    Returns ``(start, desc, src, rows)`` or None:
+      desc at start[v] (int4 records): [card, npar, nchl, own row base];
+        ceil(npar/2) x [u, stride, u, stride] (own row += x_u * stride);
+        per child: [c, row base, nrec, 0] + nrec x [u, stride, u, stride]
+        (row = base + x_c + sum x_u * stride; unused halves have stride 0);
+      src[row] = [first CPT cell, cell step | card_v << 26].
+    """
+    n = net.num_vars
+    cards = lay.cards
+    if n < BFT_MIN_VARS or int(cards.max()) > 4:
+        return None
+    cpt_off = lay.cpt_off
+    start, desc, src = [0], [], []
+    rows = 0
+
+    def records(pairs):
+        out = []
+        for i in range(0, len(pairs), 2):
+            (u0, s0), (u1, s1) = pairs[i], pairs[i + 1] if i + 1 < len(pairs) else (pairs[i][0], 0)
+            out += [u0, s0, u1, s1]
+        return out
+
+    for v in range(n):
+        kv = int(cards[v])
+        ps = net.parent_strides(v)
+        nrow = int(lay.rows[v])
+        desc += [kv, len(net.parents[v]), len(net.children[v]), rows]
+        desc += records([(p, int(ps[j])) for j, p in enumerate(net.parents[v])])
+        r = np.arange(nrow, dtype=np.int64)
+        src.append(np.stack([cpt_off[v] + r * kv, np.full(nrow, 1 | (kv << 26), np.int64)], 1))
+        rows += nrow
+        for c in net.children[v]:
+            cc = int(cards[c])
+            cps = net.parent_strides(c)
+            j = net.parents[c].index(v)
+            others = [(q, p) for q, p in enumerate(net.parents[c]) if p != v]
+            # reduced mixed radix over the other parents (first most significant), x_c innermost
+            red = [1] * len(others)
+            for i in range(len(others) - 2, -1, -1):
+                red[i] = red[i + 1] * int(cards[others[i + 1][1]])
+            recs = records([(p, red[i] * cc) for i, (q, p) in enumerate(others)])
+            desc += [c, rows, len(recs) // 4, 0] + recs
+            nconf = int(np.prod([int(cards[p]) for _, p in others])) if others else 1
+            # row o * cc + x_c: cells cpt_off[c] + (sum_q x_q cps[q] + t cps[j]) * cc + x_c
+            o = np.arange(nconf, dtype=np.int64)
+            full = np.zeros(nconf, dtype=np.int64)
+            for i, (q, p) in enumerate(others):
+                full += ((o // red[i]) % int(cards[p])) * int(cps[q])
+            first = cpt_off[c] + (full[:, None] * cc + np.arange(cc)[None, :]).ravel()
+            step = int(cps[j]) * cc
+            if step >= 1 << 26:
+                return None
+            src.append(np.stack([first, np.full(first.size, step | (kv << 26), np.int64)], 1))
+            rows += first.size
+        start.append(len(desc))
+    if rows >= 2**31 or cpt_off[-1] >= 2**31:
+        return None
+    return (np.asarray(start, np.int32), np.asarray(desc, np.int32),
+            np.concatenate(src).astype(np.int32).ravel(), rows)
+
+
 def small_plan(net: Network, lay: NetLayout):
     """Packed-lane plan (``sg_small``) when the lane state fits in one byte.
 
@@ -420,6 +494,18 @@ class NetPack:
                 setattr(s, k, self.buf64.data_ptr() + 8 * offs64[k])
         s.blob32, s.blob32_words = self.buf32.data_ptr(), self.buf32.numel()
         s.blob64, s.blob64_words = self.buf64.data_ptr(), self.buf64.numel()
+        self.bft = None
+        bplan = blanket_factor_plan(net, lay)
+        if bplan is not None:
+            start, desc, src, rows = bplan
+            self.bft_prog = torch.from_numpy(np.concatenate([desc, start])).to(device)
+            self.bft_src = torch.from_numpy(src).to(device)
+            self.bft = torch.zeros(rows * 4, dtype=torch.float64, device=device)
+            s.bft_rows = rows
+            s.bft_desc = self.bft_prog.data_ptr()
+            s.bft_start = self.bft_prog.data_ptr() + 4 * len(desc)
+            s.bft_src = self.bft_src.data_ptr()
+            s.bft = self.bft.data_ptr()
         self.struct = s
         self.ref = ctypes.byref(self.struct)
         plan = small_plan(net, lay)

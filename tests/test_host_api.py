@@ -135,3 +135,58 @@ def test_pack_crumbs_matches_sgb_blocks(tmp_path):
     x = raw[:, :18].astype(np.int64)  # decode by hand
     dec = np.stack([(x >> (2 * k)) & 3 for k in range(4)], axis=-1).reshape(3, -1)[:, :70]
     np.testing.assert_array_equal(np.where(dec == 3, -1, dec), dense)
+
+
+def _bft_weights(start, desc, src, cpt, x, v):
+    """Host restatement of draw_bft's weight product (sg_big.cu) from the plan."""
+    def row_of(r):
+        base, sk = int(src[2 * r]), int(src[2 * r + 1])
+        step, k = sk & ((1 << 26) - 1), sk >> 26
+        return np.array([cpt[base + t * step] if t < k else 0.0 for t in range(4)])
+
+    p = int(start[v]) // 4
+    rec = desc.reshape(-1, 4)
+    card, npar, nchl, row = rec[p]
+    p += 1
+    for j in range(0, npar, 2):
+        u0, s0, u1, s1 = rec[p]
+        row += x[u0] * s0 + x[u1] * s1
+        p += 1
+    w = row_of(row)
+    for _ in range(nchl):
+        c, base, nrec, _z = rec[p]
+        p += 1
+        i = base + x[c]
+        for _q in range(nrec):
+            u0, s0, u1, s1 = rec[p]
+            i += x[u0] * s0 + x[u1] * s1
+            p += 1
+        w = w * row_of(i)
+    return w
+
+
+def test_blanket_factor_plan_reproduces_the_weight_product():
+    """Every row of the big-tile sweep's blanket factor tables is the CPT
+    entry the reference's weight product (sampler.py:226-240) multiplies."""
+    from paper_1511_06416_b200 import netgen, netpack
+
+    net = netgen.random_dag_network(60, max_parents=4, min_card=2, max_card=4, seed=9)
+    cpts = netgen.dirichlet_cpts(net, 1.0, seed=10)
+    lay = netpack.layout(net)
+    start, desc, src, rows = netpack.blanket_factor_plan(net, lay)
+    assert rows == len(src) // 2
+    cpt = np.concatenate([t.ravel() for t in cpts.tables])
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        x = [int(rng.integers(k)) for k in net.cardinalities]
+        for v in range(net.num_vars):
+            ref = np.zeros(4)
+            for t in range(net.cardinalities[v]):
+                xs = list(x)
+                xs[v] = t
+                w = cpts.tables[v][sum(xs[p] * s for p, s in zip(net.parents[v], net.parent_strides(v))), t]
+                for c in net.children[v]:
+                    ci = sum(xs[p] * s for p, s in zip(net.parents[c], net.parent_strides(c)))
+                    w = w * cpts.tables[c][ci, xs[c]]
+                ref[t] = w
+            np.testing.assert_array_equal(_bft_weights(start, desc, src, cpt, x, v), ref)
