@@ -447,6 +447,10 @@ typedef struct sg_finish {
   uint64_t* key_current;      /* [dev] [kps] */
   double* vprob;              /* [dev] [n][2^bits][4] or NULL: the packed path's full conditionals
                                  p_v(x | lane word) for sg_joint_tables (sp != NULL) */
+  double* cpt_host;           /* [cells] mapped pinned HOST memory or NULL: the new CPTs are also
+                                 stored there by the kernel that writes them (the step's result
+                                 read back without a copy node; visible once the call's work is
+                                 complete) */
 } sg_finish;
 
 /* sg_finish.flags: the packed table is the only consumer of this step's

@@ -76,6 +76,7 @@ struct FinishArgs {
   // cells' gamma draws (MAP: totals) in release_lg[0..cells) and their in-log
   // flags in the bytes after them; the readers normalise the rows themselves
   double* release_lg;
+  double* cpt_host;  // != NULL: mapped pinned host copy of the new CPTs
   int has_small;
   int early_inputs;  // the preceding sweep triggers only after its own wait: read total/prev/key before ours
   int packed_only;  // SG_FINISH_PACKED_ONLY: skip ptab/ftab, build stab from the CPTs
@@ -259,6 +260,8 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
       else dirichlet_row<K>(lg + base, inlog + base, card, cpt_s + base);
     });
     for (int s2 = 0; s2 < card; ++s2) f.cpt[base + s2] = cpt_s[base + s2];
+    if (f.cpt_host)
+      for (int s2 = 0; s2 < card; ++s2) f.cpt_host[base + s2] = cpt_s[base + s2];
   }
   const bool release_cpts = f.release_sync && !f.release_lg;
   if (release_cpts && tid < int(net.rows)) __threadfence();  // this thread's CPT rows are visible device-wide ...
@@ -337,6 +340,7 @@ inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
   a.kps = f->kps;
   a.key_current = f->key_current;
   a.vprob = sp ? f->vprob : nullptr;
+  a.cpt_host = f->cpt_host;
   a.early_inputs = 0;
   a.release_sync = nullptr;
   a.release_lg = nullptr;

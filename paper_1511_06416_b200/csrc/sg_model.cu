@@ -150,6 +150,10 @@ extern "C" int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_fi
     st = sg_small_tables(net, sp, f->ftab, f->stab, stream);
     if (st) return st;
   }
+  if (f->cpt_host) {
+    st = sg_copy_small(f->cpt_host, f->cpt, net->cells * int64_t(sizeof(double)), stream);
+    if (st) return st;
+  }
   if (f->clear_counts) cudaMemsetAsync(f->clear_counts, 0, sizeof(uint64_t) * net->cells, s);
   if (f->key_table) return sg_keys_advance(f->key_table, f->key_index, f->kps, f->key_current, stream);
   return check_launch("sg_step_finish");

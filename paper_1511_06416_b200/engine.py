@@ -286,8 +286,9 @@ class Engine:
         self._last_batch = db
 
     def finish_args(self, new_counts, prev_counts, key: int, key_dev: int | None = None, clear=None,
-                    cursor=None):
-        """``sg_finish`` of one visit: accumulate, CPT update, next visit's tables."""
+                    cursor=None, cpt_host: torch.Tensor | None = None):
+        """``sg_finish`` of one visit: accumulate, CPT update, next visit's tables
+        (``cpt_host``: pinned host tensor the kernel also stores the new CPTs in)."""
         cfg = self.cfg
         f = _lib.SgFinish()
         f.acc_mode = _lib.SG_ACC_MOVING if cfg.accumulator_mode == "moving_sum" else _lib.SG_ACC_EXPONENTIAL
@@ -307,6 +308,7 @@ class Engine:
         # the packed sweep reads only the packed words: build them straight from the CPTs
         f.flags = _lib.SG_FINISH_PACKED_ONLY if self.use_small else 0
         f.vprob = self.vprob.data_ptr() if self.joint else None
+        f.cpt_host = None if cpt_host is None else cpt_host.data_ptr()
         if cursor is not None:
             table, index, kps, current = cursor
             f.key_table, f.key_index, f.kps, f.key_current = table.data_ptr(), index.data_ptr(), kps, current.data_ptr()
@@ -504,9 +506,10 @@ class StepGraphs:
         form on the device.
 
         ``host_block`` (pinned, the private buffers' layout): every step()
-        also uploads this block into the OTHER parity's buffer -- the next
-        visit's input -- on a copy stream (a copy engine), overlapped with
-        the replay, ordered by events.  The copy is asynchronous: a caller
+        also uploads this block into the buffer of the visit after next
+        (three private buffers, so each upload has two replays' time to
+        land) on a copy stream (a copy engine), overlapped with the replays,
+        ordered by events.  The copy is asynchronous: a caller
         that refills ``host_block`` between steps must first wait for
         :attr:`upload_done` (the event of the last upload).  With the moving
         sum the replayed minibatch keeps its lanes resident, so the uploaded
@@ -558,7 +561,8 @@ class StepGraphs:
             src, _ = eng._obs_for(mb)
             bufs = []
             shape, dt = self.obs_geometry(eng.n, mb.size, self.obs_bits)
-            for _ in range(2):
+            # host-fed graphs keep three: the upload of visit k + 2 starts with visit k
+            for _ in range(3 if host_block is not None else 2):
                 b = torch.empty(shape, dtype=dt, device=d)
                 if self.nibbles:
                     b.copy_(pack_bits(src[:, :mb.size], shape[1] * 8 // self.obs_bits, self.obs_bits))
@@ -585,10 +589,10 @@ class StepGraphs:
             # uploads run on a copy stream outside the graphs (a copy engine,
             # never SM time), ordered by events against the replays
             self._up_stream = torch.cuda.Stream()
-            self._uploaded = [torch.cuda.Event(), torch.cuda.Event()]
-            self._up_pending = [False, False]
-            self._read_done = [torch.cuda.Event(), torch.cuda.Event()]
-            self._read_pending = [False, False]
+            self._uploaded = [torch.cuda.Event() for _ in bufs]
+            self._up_pending = [False] * len(bufs)
+            self._read_done = [torch.cuda.Event() for _ in bufs]
+            self._read_pending = [False] * len(bufs)
         for dev_t, host_t in self.readback:
             if not host_t.is_pinned() or host_t.numel() * host_t.element_size() < dev_t.numel() * dev_t.element_size():
                 raise ValueError("readback targets must be pinned host tensors large enough")
@@ -611,10 +615,11 @@ class StepGraphs:
         _lib.call("sg_keys_advance", self.table.data_ptr(), self.idx.data_ptr(), kps, self.cur.data_ptr(),
                   stream_handle())
         torch.cuda.synchronize()
-        for parity in (0, 1):
+        # graph k: count parity k % 2, observation buffer k % len(bufs) (2 or 6 graphs)
+        for k in range(2 if len(bufs) == 2 else 6):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self._record(parity)
+                self._record(k)
             self.graphs.append(g)
         torch.cuda.synchronize()
 
@@ -652,13 +657,14 @@ class StepGraphs:
             return (n, pitch * bits // 8), torch.uint8
         return (n, pitch), torch.int8
 
-    def _record(self, p: int) -> None:
+    def _record(self, k: int) -> None:
         eng, db, m, cfg = self.eng, self.db, self.m, self.eng.cfg
         s = stream_handle()
         size = self.mb.size
         cur = self.cur.data_ptr()
+        p = k % 2  # count parity
         new, prev = self.cbuf[p], self.cbuf[1 - p]
-        obs = self.obs_bufs[p]
+        obs = self.obs_bufs[k % len(self.obs_bufs)]
         # tables and keys of this visit are ready: the previous replay's finish built/advanced them
         if not eng.use_small:  # the packed sweep checks the block in its own launch
             if self._unpacked is not None:
@@ -671,8 +677,10 @@ class StepGraphs:
         S = cfg.sweeps_per_minibatch
         # step tail: accumulate, CPT update, next tables, clear `prev` (the next
         # replay's count buffer), advance the key cursor
+        # the CPT read-back rides in the tail kernel itself (zero-copy store into the pinned tensor)
+        cpt_host = next((h for d_, h in self.readback if d_.data_ptr() == eng.cpt.data_ptr()), None)
         f = eng.finish_args(new, prev, 0, key_dev=cur + 8 * S, clear=prev,
-                            cursor=(self.table, self.idx, self.kps, self.cur))
+                            cursor=(self.table, self.idx, self.kps, self.cur), cpt_host=cpt_host)
         self._finish_args.append(f)
         if self._tev is not None:
             _lib.call("sg_event_record", self._tev[2 * p], s)
@@ -701,6 +709,8 @@ class StepGraphs:
             eng.comm(new)
         eng.step_tail(f, s)
         for dev_t, host_t in self.readback:  # a kernel node (faster than a D2H memcpy node) into mapped pinned memory
+            if host_t is cpt_host:
+                continue
             nbytes = dev_t.numel() * dev_t.element_size()
             if nbytes % 8 == 0 and dev_t.data_ptr() % 8 == 0 and host_t.data_ptr() % 8 == 0:
                 _lib.call("sg_copy_small", host_t.data_ptr(), dev_t.data_ptr(), nbytes, s)
@@ -716,8 +726,12 @@ class StepGraphs:
         if mb is not None and self.host_block is not None:
             raise ValueError("this graph uploads its own host block; call step() without a minibatch")
         if self.host_block is not None:
-            # upload the NEXT visit's block into the other buffer while this replay runs
-            q = 1 - p
+            # three buffers: upload visit k + 2's block into the buffer visit k - 1 read
+            # while this replay runs, so an upload has two replays' time to land
+            nb = len(self.obs_bufs)
+            p = self.replayed % nb
+            q = (self.replayed + 2) % nb
+            gk = self.replayed % len(self.graphs)
             up = self._up_stream
             if self._read_pending[q]:
                 up.wait_event(self._read_done[q])  # the replay that last read buffer q has finished
@@ -738,7 +752,7 @@ class StepGraphs:
                 self._up_pending[p] = False
             if dbg is not None:
                 ev[2].record(main)
-            self.graphs[p].replay()
+            self.graphs[gk].replay()
             if dbg is not None:
                 ev[3].record(main)
                 dbg.append(ev)
@@ -793,8 +807,10 @@ class StepGraphs:
     @property
     def launches_per_step(self) -> int:
         eng = self.eng
-        readback = len(self.readback)
         one_cta = eng.pack.cells <= 4096  # sg_step_finish is one kernel, else six launches
+        # the CPTs' read-back is stored by the tail kernel (one copy launch inside the multi-launch tail)
+        cpt_rb = any(d_.data_ptr() == eng.cpt.data_ptr() for d_, _ in self.readback)
+        readback = len(self.readback) - (1 if cpt_rb and one_cta else 0)
         # the packed sweep folds in the range check; a packed block on the generic path is unpacked first
         check = 0 if eng.use_small else (2 if self._unpacked is not None else 1)
         keys = eng.cfg.sweeps_per_minibatch if eng.rng_mode == _lib.SG_RNG_NUMPY else 0
@@ -888,8 +904,9 @@ class StreamGraphs:
                   db.scratch.data_ptr(), db.pattern.data_ptr(), db.case_id.data_ptr(), db.lanes.data_ptr(), db.lane_ld,
                   cur + 8 * (S + 1), s)
         new = self.cbuf[p]
+        cpt_host = next((h for d_, h in self.readback if d_.data_ptr() == eng.cpt.data_ptr()), None)
         f = eng.finish_args(new, None, 0, key_dev=cur + 8 * S, clear=self.cbuf[1 - p],
-                            cursor=(self.table, self.idx, self.kps, self.cur))
+                            cursor=(self.table, self.idx, self.kps, self.cur), cpt_host=cpt_host)
         self._f = getattr(self, "_f", []) + [f]
         for sw in range(S):
             last = sw == S - 1
@@ -901,7 +918,8 @@ class StreamGraphs:
             eng.comm(new)
         eng.step_tail(f, s)
         for dev_t, host_t in self.readback:
-            _lib.call("sg_copy_small", host_t.data_ptr(), dev_t.data_ptr(), dev_t.numel() * dev_t.element_size(), s)
+            if host_t is not cpt_host:  # the CPTs are stored by the tail kernel itself
+                _lib.call("sg_copy_small", host_t.data_ptr(), dev_t.data_ptr(), dev_t.numel() * dev_t.element_size(), s)
 
     def step(self, mb) -> None:
         """Replay the next planned visit on minibatch ``mb`` (its block is copied into the graph's buffer:
@@ -951,4 +969,5 @@ class StreamGraphs:
     @property
     def launches_per_step(self) -> int:
         S = self.eng.cfg.sweeps_per_minibatch
-        return (1 if self._int8 is not None else 0) + 4 + (S - 1) + S + 1 + len(self.readback)
+        cpt_rb = any(d_.data_ptr() == self.eng.cpt.data_ptr() for d_, _ in self.readback)
+        return (1 if self._int8 is not None else 0) + 4 + (S - 1) + S + 1 + len(self.readback) - (1 if cpt_rb else 0)

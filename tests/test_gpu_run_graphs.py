@@ -146,3 +146,29 @@ def test_stream_graphs_sample_the_streamed_blocks(koller):
     g.step(mbs[2])
     torch.cuda.synchronize()
     assert torch.equal(eager.cpt, graphed.cpt) and torch.equal(eager.total, graphed.total)
+
+
+@pytest.mark.parametrize("n", [60, 400])
+def test_cpt_readback_stored_by_the_tail(n):
+    """StepGraphs(readback=[(cpt, pinned)]): the step tail stores the new CPTs
+    in the pinned tensor itself (sg_finish.cpt_host) -- the one-CTA tail and
+    the multi-launch tail of a model above its cell limit alike."""
+    from paper_1511_06416_b200 import netgen
+    from paper_1511_06416_b200.engine import Engine, StepGraphs
+
+    net = netgen.random_dag_network(n, max_parents=4, seed=31)
+    truth = netgen.dirichlet_cpts(net, 1.0, seed=32)
+    cases = 2048
+    obs = sg.forward_sample_device(net, truth, cases, seed=5, hide_fraction=0.3, mask_seed=6)
+    cfg = sg.SamplerConfig(same_m=2, minibatch_size=cases, num_passes=1, seed=9, rng="fast")
+    mb = next(iter(sg.DeviceSource(obs, cases, cases)))
+    eng = Engine(net, cfg)
+    eng.visit(mb, 0, 2)
+    host = torch.zeros(eng.pack.cells, dtype=torch.float64, pin_memory=True)
+    g = StepGraphs(eng, mb, 2, range(1, 4), readback=[(eng.cpt, host)])
+    for _ in range(3):
+        g.step()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(host.numpy(), eng.cpt.cpu().numpy())
+    g.finish()
+    assert (eng.pack.cells > 4096) == (n == 400)

@@ -16,7 +16,20 @@ obs = sg.forward_sample_device(net, truth, cases, seed=1, hide_fraction=0.5, mas
 mb = next(iter(sg.DeviceSource(obs, cases, cases)))
 
 
-def timed(g, steps=50):
+def warm_pcie(host):
+    """Bring the PCIe link out of its low-power state (bench.py does the same)."""
+    import time
+    scratch = torch.empty_like(host, device="cuda")
+    t = time.perf_counter()
+    while time.perf_counter() - t < 0.3:
+        for _ in range(8):
+            scratch.copy_(host, non_blocking=True)
+        torch.cuda.synchronize()
+
+
+def timed(g, steps=50, host=None):
+    if host is not None:
+        warm_pcie(host)
     for _ in range(3):
         g.step()
     torch.cuda.synchronize()
@@ -41,9 +54,10 @@ for rep in range(2):
     host.copy_(pack_bits(obs[:, :cases], shape[1] * 4, 2).cpu())
     cpt_host = torch.empty(eng.pack.cells, dtype=torch.float64, pin_memory=True)
     base = 3
-    for label, kw in [("plain", {}), ("host_block", {"host_block": host}),
+    for label, kw in [("plain", {}), ("readback", {"readback": [(eng.cpt, cpt_host)]}),
+                      ("host_block", {"host_block": host}),
                       ("host_block+readback", {"host_block": host, "readback": [(eng.cpt, cpt_host)]})]:
         g = StepGraphs(eng, mb, m, range(base, base + 60), obs_bits=2, **kw)
-        print(f"rep {rep} {label:22s} {timed(g):7.1f} us/step", flush=True)
+        print(f"rep {rep} {label:22s} {timed(g, host=host):7.1f} us/step", flush=True)
         g.finish()
         base += 70
