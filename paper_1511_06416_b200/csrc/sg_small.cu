@@ -604,7 +604,7 @@ static SmallOrd small_ord(const sg_small& sp) {
 //   [0, NP)        byte offset of row 0 of pattern P
 //   [NP, 2NP)      B_P | keep_P << 8 | (byte offset of dep_P) << 16
 //   dep_P[j]       latent field bits of compact column j (pdep(j, latent mask))
-//   rows_P[S][j]   alias entries (primary << B_P | alias), 2^bits rows of 2^B_P words
+//   rows_P[S][j]   alias entries (primary << B_P | alias), 2^bits rows of 2^B_P + 1 words
 
 #ifndef SG_JOINT_THREADS
 #define SG_JOINT_THREADS 1024
@@ -659,7 +659,8 @@ __device__ __forceinline__ uint32_t joint_alias_col(uint32_t row, uint32_t u) {
 template <int B, int QG, int NL>
 __device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[QG], uint32_t row0, uint32_t dep0,
                                             uint32_t keep) {
-  constexpr uint32_t kRowBytes = (1u << B) * 4u;  // rows 2^B words apart
+  constexpr uint32_t kRowBytes = ((1u << B) + 1u) * 4u;  // rows 2^B + 1 words apart (odd: lanes drawing
+                                                        // the same column of different rows use different banks)
 #pragma unroll
   for (int g = 0; g < QG; ++g) {
     const uint32_t u[4] = {r[g].a, r[g].b, r[g].c, r[g].d};
@@ -841,9 +842,8 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
     for (uint32_t o2 = 0; o2 < jbytes; o2 += 32768u)
       bulk_g2s(blob + o2, reinterpret_cast<const unsigned char*>(jblob_g) + o2, min(32768u, jbytes - o2), bar);
   }
+  for (int i = tid; i < sp.tab_words; i += NT) stab[i] = stab_g[i];
   const bool armed = zs_flag && *zs_flag != 0u;
-  if (armed)  // the per-variable tables are read only by the zero-support fallback
-    for (int i = tid; i < sp.tab_words; i += NT) stab[i] = stab_g[i];
   QuadSet qs;
   qs.row0 = uint32_t(q0) * uint32_t(lane_ld);
   qs.ld = uint32_t(lane_ld);
@@ -995,6 +995,7 @@ __device__ __forceinline__ void joint_alias_row(uint32_t* row, int B, bool two, 
     row[j0] = entry(j0, w0, d0, D0, E0);
     if (two) row[j0 + 1] = entry(j0 + 1, w1, d1, dl, el);
   }
+  if (lane == 0) row[K] = 0u;  // stride padding
   __syncwarp();
 }
 // Slice `slice` (lane words S in [slice * R/4, (slice+1) * R/4)) of pattern
@@ -1024,7 +1025,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
   const uint32_t* dep = reinterpret_cast<const uint32_t*>(reinterpret_cast<const unsigned char*>(jblob) + (meta >> 16));
   uint32_t* rows = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(jblob) + jblob[P]);
   const int R = 1 << sp.bits, K = 1 << B;
-  const int KS = K;  // row stride (alias columns are uniform: no structural bank conflicts)
+  const int KS = K + 1;  // row stride (odd: no bank conflicts between lanes of one column)
   const int rows_per = R / slices, r0 = slice * rows_per;
   double* vprob = reinterpret_cast<double*>(smem);  // [n][R][4]
   if (tid == 0 && part != 2) {
@@ -1139,9 +1140,7 @@ __device__ __forceinline__ void joint_slice(const sg_net& net, const sg_small& s
     const double left = __shfl_up_sync(0xffffffffu, x, 1);
     const double total = __shfl_sync(0xffffffffu, x, two ? 31 : K - 1);
     const double c0 = two ? (lane ? __dadd_rn(left, a) : a) : x;
-    if (r == 0) tail_stamp(5);
     joint_alias_row(rows + S * KS, B, two, lane, j0 < K ? c0 : 0.0, x, total, alias_sd[warp], alias_se[warp]);
-    if (r == 0) tail_stamp(6);
   }
 }
 
@@ -1347,6 +1346,7 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
       inlog[i] = __ldcg(il_g + i);
     }
     __syncthreads();
+    stamp(5);
     for (int row = tid; row < int(net.rows); row += blockDim.x) {
       const int v = net.row_var[row];
       const int card = net.card[v];
@@ -1361,6 +1361,7 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
     for (int i = tid; i < cells; i += blockDim.x) cpt_s[i] = __ldcg(f.cpt + i);
   }
   __syncthreads();
+  stamp(6);
   if (live) joint_cond_apply(net, sp, plan, plan_nf, cpt_s, reinterpret_cast<double*>(work));
   __syncthreads();
   joint_slice(net, sp, jp, cpt_s, nullptr, jblob, P, slice, work, false, true, 2, pidx, nsl);

@@ -408,7 +408,7 @@ def joint_plan(sp, cells: int):
     Patterns P (bit v = variable v latent, as sg_small_prepare buckets them):
     B_P latent bits, keep_P = the observed bits of the lane word, dep_P[j] =
     the lane bits of compact column j (bit i of j -> the i-th set bit of the
-    latent mask), 2^bits rows of 2^B_P alias entries, 2^B_P words apart.  Returns ``(SgJoint,
+    latent mask), 2^bits rows of 2^B_P alias entries, 2^B_P + 1 words apart.  Returns ``(SgJoint,
     header uint32 array)`` or None when the network does not qualify or the
     CTA's shared memory (blob + per-variable table + per-warp tally bins) does not
     fit.
@@ -438,9 +438,9 @@ def joint_plan(sp, cells: int):
     header_words = (2 * NP + len(dep) + 3) // 4 * 4
     row_off, words = [0] * NP, header_words
     for P in range(NP):
-        if B[P]:  # rows 2^B words apart (alias columns are uniform over a row: no structural bank conflicts)
+        if B[P]:  # rows 2^B + 1 words apart: odd stride, no bank conflicts between lanes
             row_off[P] = words
-            words += (1 << bits) * (1 << B[P])
+            words += (1 << bits) * ((1 << B[P]) + 1)
     words = (words + 3) // 4 * 4
     if max(dep_off) * 4 >= 1 << 16:
         return None

@@ -32,7 +32,9 @@ def _blob_rows(eng, P):
     B = int(head[jp.patterns + P] & 0xFF)
     off = int(head[P]) // 4
     R, K = 1 << eng.pack.small.bits, 1 << B
-    return blob[off:off + R * K].reshape(R, K)
+    rows = blob[off:off + R * (K + 1)].reshape(R, K + 1)  # odd row stride: one padding word
+    assert np.all(rows[:, K] == 0)
+    return rows[:, :K]
 
 
 def _check_tables(eng, onet, order):

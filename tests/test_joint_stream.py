@@ -120,7 +120,7 @@ def test_joint_plan_header_matches_restatement(koller):
     # rows follow the header in pattern order, 2^bits x 2^B words each
     offs = [int(head[P]) // 4 for P in range(1, NP)]
     assert offs[0] == jp.header_words and offs == sorted(offs)
-    assert jp.words == jp.header_words + sum(64 * (1 << tabs[P][0]) for P in range(1, NP))
+    assert jp.words == jp.header_words + sum(64 * ((1 << tabs[P][0]) + 1) for P in range(1, NP))
 
 
 def test_joint_plan_rejects_wide_lane_words():

@@ -79,8 +79,8 @@ for k in range(12):
         "slices flag seen (median)": statistics.median(T(b, 1) for b in sl) - t0,
         "slices conditionals done (median)": statistics.median(T(b, 3) for b in sl) - t0,
         "slices rows loop start (median)": statistics.median(T(b, 4) for b in sl) - t0,
-        "slices warp0 scan done (median)": statistics.median(T(b, 5) for b in sl) - t0,
-        "slices warp0 alias done (median)": statistics.median(T(b, 6) for b in sl) - t0,
+        "slices gammas loaded (median)": statistics.median(T(b, 5) for b in sl) - t0,
+        "slices Dirichlet rows (median)": statistics.median(T(b, 6) for b in sl) - t0,
         "slices median end": statistics.median(T(b, 2) for b in sl) - t0,
         "slices last end": max(T(b, 2) for b in sl) - t0,
         "slowest slice role": float(roles[max(sl, key=lambda b: T(b, 2))]),
@@ -89,8 +89,8 @@ for k in range(12):
         "slowest: flag seen": T(max(sl, key=lambda b: T(b, 2)), 1) - t0,
         "slowest: cond done": T(max(sl, key=lambda b: T(b, 2)), 3) - t0,
         "slowest: rows start": T(max(sl, key=lambda b: T(b, 2)), 4) - t0,
-        "slowest: warp0 scan": T(max(sl, key=lambda b: T(b, 2)), 5) - t0,
-        "slowest: warp0 alias": T(max(sl, key=lambda b: T(b, 2)), 6) - t0,
+        "slowest: gammas loaded": T(max(sl, key=lambda b: T(b, 2)), 5) - t0,
+        "slowest: Dirichlet rows": T(max(sl, key=lambda b: T(b, 2)), 6) - t0,
     }
     r["gap: prev tail end -> sweep start"] = (t0 - prev_end) if (prev_end and not cold) else 0
     prev_end = max(T(b, 2) for b in sl)
