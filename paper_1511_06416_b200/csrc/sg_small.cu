@@ -912,6 +912,21 @@ __device__ __forceinline__ void tail_stamp(int) {}
 __host__ __device__ __forceinline__ int joint_tail_slices(int B) { return B >= 6 ? 2 * SG_JOINT_TAB_SLICES : SG_JOINT_TAB_SLICES; }
 #define SG_JOINT_ROW_WARPS (FINISH_THREADS / 32)
 
+// Row slice k of the merged tail -> (pattern P, slice of P, slices of P):
+// patterns from the last down (the all-latent pattern, 64 columns, first:
+// the costliest slices take the first tickets, i.e. the earliest CTAs), P =
+// -1 past the end.  k_joint_prep lays the static preparation out the same way.
+__device__ __forceinline__ void tail_slice_of(const uint32_t* jblob, const sg_joint& jp, int k, int& P, int& slice,
+                                              int& nsl) {
+  slice = k;
+  nsl = SG_JOINT_TAB_SLICES;
+  for (P = jp.patterns - 1; P >= 0; --P) {
+    nsl = joint_tail_slices(int(jblob[jp.patterns + P] & 0xFFu));
+    if (slice < nsl) return;
+    slice -= nsl;
+  }
+}
+
 // One transition row as an alias table (one warp; K = 2^B columns, lane l
 // holds column l, or columns 2l, 2l+1 when K = 64).  Input: the inclusive fp64
 // cumulative sums of the row's products (c_own at the lane's first column,
@@ -1297,13 +1312,8 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   int2* plan = reinterpret_cast<int2*>(work + size_t(nr) * 4 * sizeof(double));
   int8_t* plan_nf = reinterpret_cast<int8_t*>(plan + size_t(nr) * SG_JOINT_MAXF);
   uint16_t* pidx = reinterpret_cast<uint16_t*>(plan_nf + ((size_t(nr) + 15) & ~size_t(15)));
-  // role -> (pattern, slice): patterns in order, joint_tail_slices(B_P) slices each
-  int P = 0, slice = role - 1, nsl = SG_JOINT_TAB_SLICES;
-  for (; P < jp.patterns; ++P) {
-    nsl = joint_tail_slices(int(jblob[jp.patterns + P] & 0xFFu));
-    if (slice < nsl) break;
-    slice -= nsl;
-  }
+  int P, slice, nsl;
+  tail_slice_of(jblob, jp, role - 1, P, slice, nsl);
   pdl_trigger();
   __shared__ __align__(8) uint64_t prep_bar;
   const bool live = (jblob[jp.patterns + P] & 0xFFu) != 0;
@@ -1392,13 +1402,9 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_joint_prep(const sg_net gnet
   int2* plan = reinterpret_cast<int2*>(work + size_t(nr) * 4 * sizeof(double));
   int8_t* plan_nf = reinterpret_cast<int8_t*>(plan + size_t(nr) * SG_JOINT_MAXF);
   uint16_t* pidx = reinterpret_cast<uint16_t*>(plan_nf + ((size_t(nr) + 15) & ~size_t(15)));
-  int P = 0, slice = blockIdx.x, nsl = SG_JOINT_TAB_SLICES;
-  for (; P < jp.patterns; ++P) {
-    nsl = joint_tail_slices(int(jblob[jp.patterns + P] & 0xFFu));
-    if (slice < nsl) break;
-    slice -= nsl;
-  }
-  if (P >= jp.patterns || !(jblob[jp.patterns + P] & 0xFFu)) return;
+  int P, slice, nsl;
+  tail_slice_of(jblob, jp, int(blockIdx.x), P, slice, nsl);
+  if (P < 0 || !(jblob[jp.patterns + P] & 0xFFu)) return;
   for (int i = tid; i < int(gnet.blob64_words); i += blockDim.x) b64[i] = __ldg(gnet.blob64 + i);
   for (int i = tid; i < int(gnet.blob32_words); i += blockDim.x) b32[i] = __ldg(gnet.blob32 + i);
   __syncthreads();
