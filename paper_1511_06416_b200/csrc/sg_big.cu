@@ -353,8 +353,9 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
       }
       const int rs = a.mg * wpr;  // words between variable rows of the tile (32-bit offsets throughout)
       if constexpr (use_bft) {
-        if (nmb < 0) {
-          // two cases per lane: it and it + 32 of the warp's 64-entry stride
+        if (nmb < 0 && mg == 1) {
+          // one replica (m = 1: no Philox block to share across replicas): two cases
+          // per lane, it and it + 32 of the warp's 64-entry stride
           for (int it = lane; it < total; it += 64) {
             const bool two = it + 32 < total;
             const int ca = wl[it], cb = wl[two ? it + 32 : it];
