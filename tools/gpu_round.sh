@@ -11,6 +11,7 @@ python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref_$R.json 2> 
 python bench.py --rng numpy --steps 20 --no-cpu-baseline > $O/bench_numpy_$R.json 2>&1; echo "numpy rc=$?"
 for w in c3 c4; do python bench.py --workload $w --steps 10 > $O/bench_${w}_$R.json 2>&1; echo "$w rc=$?"; done
 python bench.py --workload c5 > $O/bench_c5_$R.json 2>&1; echo "c5 rc=$?"
+python bench.py --workload c2s --no-cpu-baseline > $O/bench_c2s_$R.json 2>&1; echo "c2s rc=$?"
 L="python bench.py --steps 20 --warmup 3 --no-cpu-baseline"
 if $L > $O/plain_launch_$R.log 2>&1; then
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_$R.csv $L \

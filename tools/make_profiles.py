@@ -104,7 +104,8 @@ if (G / f"pytest_gpu_{R}.log").exists():
     shutil.copy(G / f"pytest_gpu_{R}.log", P / f"{R}_pytest_gpu.log")
 for src, dst in ((f"bench_{R}.json", f"{R}_bench.json"), (f"bench_ref_{R}.json", f"{R}_bench_reference.json"),
                  (f"bench_numpy_{R}.json", f"{R}_bench_numpy.json"), (f"bench_c3_{R}.json", f"{R}_bench_c3.json"),
-                 (f"bench_c4_{R}.json", f"{R}_bench_c4.json"), (f"bench_c5_{R}.json", f"{R}_bench_c5.json")):
+                 (f"bench_c4_{R}.json", f"{R}_bench_c4.json"), (f"bench_c5_{R}.json", f"{R}_bench_c5.json"),
+                 (f"bench_c2s_{R}.json", f"{R}_bench_c2s.json")):
     if (G / src).exists():
         lines = [l for l in (G / src).read_text().splitlines() if l.startswith("{")]
         if lines:
