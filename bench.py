@@ -828,6 +828,12 @@ def main() -> None:
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # communicator set-up lines (rank / nranks, NVLS, rings) on stderr, so a
+        # multi-GPU line can be checked against the ranks NCCL actually formed
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.workload == "c2s":
         if args.impl == "reference":
             args.workload = "c2"  # the reference arm of the same C2 workload
