@@ -179,7 +179,7 @@ KERNELS_PER_CALL = {
     "sg_build_tables": 1, "sg_rank_latent": 3, "sg_init_states": 1, "sg_sweep": 1, "sg_tally": 1,
     "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
-    "sg_small_tables": 1, "sg_small_prepare": 4, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
+    "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
     "sg_joint_tables": 1, "sg_joint_sweep": 1, "sg_step_tail_joint": 1, "sg_joint_prep": 1, "sg_copy_small": 1, "sg_noop": 1,
     "sg_keys_advance": 1, "sg_step_finish": 1, "sg_site_keys": 1, "sg_predict_tally": 1, "sg_unpack_nibbles": 1, "sg_unpack_crumbs": 1,
 }

@@ -42,10 +42,10 @@ __global__ void k_small_tables(const sg_net net, const sg_small sp, const uint32
 // Cases are bucketed by latent pattern with a deterministic block partition
 // (no hot global atomics): block b of SMALL_PREP_BLOCKS owns the cases
 // [b * chunk, (b + 1) * chunk); k_small_count writes its per-pattern counts
-// cnt[P][b], k_small_scan turns them into each (pattern, block) bucket's
-// first slot, and k_small_scatter places the block's cases from there (the
-// order inside a block's share of a bucket is irrelevant: results depend on
-// case ids only).
+// cnt[P][b], k_small_scatter derives each (pattern, block) bucket's first
+// slot from them and places the block's cases from there, and
+// k_small_init_lanes builds the lanes slot by slot (the order inside a
+// block's share of a bucket is irrelevant: results depend on case ids only).
 #define SMALL_PREP_BLOCKS 296
 __device__ __forceinline__ void small_chunk(int cases, int blocks, int b, int& lo, int& hi) {
   const int chunk = ((cases + blocks - 1) / blocks + 255) & ~255;
@@ -53,81 +53,115 @@ __device__ __forceinline__ void small_chunk(int cases, int blocks, int b, int& l
   hi = min(cases, lo + chunk);
 }
 
-__global__ void __launch_bounds__(256) k_small_count(const sg_small sp, const int8_t* __restrict__ obs, int ld,
-                                                     int cases, uint8_t* __restrict__ pattern_of_case,
-                                                     uint8_t* __restrict__ obsw_of_case, int* __restrict__ cnt) {
+// Four consecutive cases per thread: one 32-bit load per variable row.
+__global__ void __launch_bounds__(1024) k_small_count(const sg_small sp, const int8_t* __restrict__ obs, int ld,
+                                                      int cases, uint8_t* __restrict__ pattern_of_case,
+                                                      uint8_t* __restrict__ obsw_of_case, int* __restrict__ cnt,
+                                                      bool vec4) {
   __shared__ int h[SMALL_PATTERNS];
   for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x) h[i] = 0;
   __syncthreads();
   int lo, hi;
-  small_chunk(cases, gridDim.x, blockIdx.x, lo, hi);
-  for (int c0 = lo; c0 < hi; c0 += blockDim.x) {  // whole warps iterate (warp-aggregated counts below)
-    const int c = c0 + int(threadIdx.x);
-    uint32_t P = 0xFFFFFFFFu, obsw = 0;
+  small_chunk(cases, gridDim.x, blockIdx.x, lo, hi);  // lo is a multiple of 256
+  for (int c0 = lo; c0 < hi; c0 += 4 * int(blockDim.x)) {  // whole warps iterate (warp-aggregated counts below)
+    const int c = c0 + 4 * int(threadIdx.x);
+    uint32_t P[4] = {0u, 0u, 0u, 0u}, ow[4] = {0u, 0u, 0u, 0u};
     if (c < hi) {
-      P = 0;
       for (int v = 0; v < sp.n; ++v) {
-        const int o = obs[int64_t(v) * ld + c];
-        P |= uint32_t(o < 0) << v;
-        // observed fields of the lane word; out of range -> field 0 (the sweep's range
-        // check of this block raises SG_ERR_STATE_RANGE), never a neighbouring field
-        if (o >= 0 && o < sp.card[v]) obsw |= uint32_t(o) << sp.off[v];
+        const int8_t* row = obs + int64_t(v) * ld + c;
+        uint32_t w;
+        if (vec4) {  // 4-byte aligned rows: c + 3 < ld since ld >= cases rounded up to 4
+          w = *reinterpret_cast<const uint32_t*>(row);
+        } else {
+          w = 0;
+          for (int k = 0; k < 4 && c + k < hi; ++k) w |= uint32_t(uint8_t(row[k])) << (8 * k);
+        }
+        const int card = sp.card[v], off = sp.off[v];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int o = int(int8_t(w >> (8 * k)));
+          P[k] |= uint32_t(o < 0) << v;
+          // observed fields of the lane word; out of range -> field 0 (the sweep's range
+          // check of this block raises SG_ERR_STATE_RANGE), never a neighbouring field
+          if (o >= 0 && o < card) ow[k] |= uint32_t(o) << off;
+        }
       }
-      pattern_of_case[c] = uint8_t(P);
-      obsw_of_case[c] = uint8_t(obsw);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (c + k < hi) {
+          pattern_of_case[c + k] = uint8_t(P[k]);
+          obsw_of_case[c + k] = uint8_t(ow[k]);
+        }
     }
-    // one shared-memory atomic per distinct pattern in the warp
-    const uint32_t peers = __match_any_sync(0xffffffffu, P);
-    if (P != 0xFFFFFFFFu && (threadIdx.x & 31) == uint32_t(__ffs(peers) - 1)) atomicAdd(&h[P], __popc(peers));
+    // one shared-memory atomic per distinct pattern in the warp, per case position
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t Pk = c + k < hi ? P[k] : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, Pk);
+      if (Pk != 0xFFFFFFFFu && (threadIdx.x & 31) == uint32_t(__ffs(peers) - 1)) atomicAdd(&h[Pk], __popc(peers));
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x) cnt[i * gridDim.x + blockIdx.x] = h[i];
 }
 
-// Warp w scans patterns w, w + 32, ...: the exclusive scan of each pattern's
-// per-block counts, then the pattern offsets (exclusive over the pattern
-// totals) are added to every entry.
-__global__ void __launch_bounds__(1024) k_small_scan(int* __restrict__ cnt, int blocks, int patterns) {
-  __shared__ int total[SMALL_PATTERNS];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int P = warp; P < patterns; P += 32) {
-    int* row = cnt + P * blocks;
+// Place the block's cases into their pattern buckets (pattern[s], case_id[s]).
+// The block's first slot in bucket P = the cases of patterns < P (all
+// blocks) + the cases of P in blocks < this one, summed here from the
+// per-block counts (no separate scan launch).  Within a warp the cases of one
+// pattern claim consecutive slots with one shared atomic.
+__global__ void __launch_bounds__(1024) k_small_scatter(const int cases, const uint8_t* __restrict__ pattern_of_case,
+                                                        const int* __restrict__ cnt, const int patterns,
+                                                        uint8_t* __restrict__ pattern, int32_t* __restrict__ case_id) {
+  __shared__ int base[SMALL_PATTERNS], tot[SMALL_PATTERNS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nb = gridDim.x, me = blockIdx.x;
+  for (int P = warp; P < patterns; P += blockDim.x >> 5) {
+    int t = 0, pre = 0;
+    for (int b = lane; b < nb; b += 32) {
+      const int x = cnt[P * nb + b];
+      t += x;
+      pre += b < me ? x : 0;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+      pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    }
+    if (lane == 0) {
+      tot[P] = t;
+      base[P] = pre;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {  // + the exclusive scan of the pattern totals
     int carry = 0;
-    for (int b0 = 0; b0 < blocks; b0 += 32) {
-      const int b = b0 + lane;
-      const int x = b < blocks ? row[b] : 0;
+    for (int P0 = 0; P0 < patterns; P0 += 32) {
+      const int P = P0 + lane;
+      const int x = P < patterns ? tot[P] : 0;
       int inc = x;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += y;
       }
-      if (b < blocks) row[b] = carry + inc - x;
+      if (P < patterns) base[P] += carry + inc - x;
       carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    if (lane == 0) total[P] = carry;
   }
-  __syncthreads();
-  for (int P = warp; P < patterns; P += 32) {
-    int off = 0;
-    for (int q = 0; q < P; ++q) off += total[q];
-    int* row = cnt + P * blocks;
-    for (int b = lane; b < blocks; b += 32) row[b] += off;
-  }
-}
-
-// Place the cases into their pattern buckets (pattern[s], case_id[s]).
-__global__ void __launch_bounds__(256) k_small_scatter(const int cases, const uint8_t* __restrict__ pattern_of_case,
-                                                       const int* __restrict__ cursor, uint8_t* __restrict__ pattern,
-                                                       int32_t* __restrict__ case_id) {
-  __shared__ int cnt[SMALL_PATTERNS];
-  for (int i = threadIdx.x; i < SMALL_PATTERNS; i += blockDim.x) cnt[i] = cursor[i * gridDim.x + blockIdx.x];
   __syncthreads();
   int lo, hi;
-  small_chunk(cases, gridDim.x, blockIdx.x, lo, hi);
-  for (int c = lo + threadIdx.x; c < hi; c += blockDim.x) {
-    const uint32_t P = pattern_of_case[c];
-    const int s = atomicAdd(&cnt[P], 1);
+  small_chunk(cases, nb, me, lo, hi);
+  for (int c0 = lo; c0 < hi; c0 += blockDim.x) {  // whole warps iterate
+    const int c = c0 + int(threadIdx.x);
+    const bool valid = c < hi;
+    const uint32_t P = valid ? uint32_t(pattern_of_case[c]) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, P);
+    const int leader = __ffs(peers) - 1;
+    int first = 0;
+    if (valid && lane == leader) first = atomicAdd(&base[P], __popc(peers));
+    first = __shfl_sync(0xffffffffu, first, leader);
+    if (!valid) continue;
+    const int s = first + __popc(peers & lanemask_lt());
     pattern[s] = uint8_t(P);
     case_id[s] = c;
   }
@@ -136,22 +170,25 @@ __global__ void __launch_bounds__(256) k_small_scatter(const int cases, const ui
 // Build the lanes of every slot (in bucket order, so a warp's slots share a
 // latent pattern and its variable loop does not diverge): observed fields
 // from the data, latent fields from the FAST init stream (same draw as
-// k_init_states: Philox4x32(key, (case, v, r/4, purpose 1))[r%4] * card >> 32).
+// k_init_states: Philox4x32(key, (case, v, r/4, purpose 1))[r%4] * card >> 32;
+// the key's and the case's part of the first round computed once per slot).
 __global__ void __launch_bounds__(256) k_small_init_lanes(
     const sg_small sp, const uint8_t* __restrict__ obsw_of_case, int cases, int m, int64_t case_base,
     uint64_t init_key, const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id,
     uint8_t* __restrict__ lanes, int lane_ld, const uint64_t* __restrict__ init_key_dev) {
   if (init_key_dev) init_key = *init_key_dev;  // graph replay: the key cursor's init key
+  const FastKey fk = fast_key(init_key);
   uint32_t* out = reinterpret_cast<uint32_t*>(lanes);
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < cases; s += gridDim.x * blockDim.x) {
     const uint32_t P = pattern[s];
     const int c = case_id[s];
     const uint32_t obsw = obsw_of_case[c];
+    const FastCase fc = fast_case(fk, uint32_t(case_base + c));
     for (int q = 0; q < (m + 3) / 4; ++q) {
       uint32_t S[4] = {obsw, obsw, obsw, obsw};
       for (int v = 0; v < sp.n; ++v) {
         if (!((P >> v) & 1u)) continue;
-        const u32x4 w = fast_block(init_key, uint64_t(case_base + c), uint32_t(v), uint32_t(q), 1u);
+        const u32x4 w = fast_draw(fc, fast_word(uint32_t(v), uint32_t(q), 1u));
         const uint32_t ws[4] = {w.a, w.b, w.c, w.d};
 #pragma unroll
         for (int j = 0; j < 4; ++j) S[j] |= uint32_t((uint64_t(ws[j]) * uint32_t(sp.card[v])) >> 32) << sp.off[v];
@@ -1471,9 +1508,9 @@ extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t l
   int* cnt = scratch;                                                                     // [SMALL_PATTERNS][blocks]
   uint8_t* poc = reinterpret_cast<uint8_t*>(scratch + SMALL_PATTERNS * SMALL_PREP_BLOCKS);  // [cases] patterns
   uint8_t* ow = poc + cases;                                                               // [cases] observed fields
-  k_small_count<<<blocks, 256, 0, s>>>(*sp, obs, ld_obs, cases, poc, ow, cnt);
-  k_small_scan<<<1, 1024, 0, s>>>(cnt, blocks, 1 << sp->n);
-  k_small_scatter<<<blocks, 256, 0, s>>>(cases, poc, cnt, pattern, case_id);
+  const bool vec4 = ld_obs % 4 == 0 && ld_obs >= (cases + 3) / 4 * 4 && (reinterpret_cast<uintptr_t>(obs) & 3) == 0;
+  k_small_count<<<blocks, 1024, 0, s>>>(*sp, obs, ld_obs, cases, poc, ow, cnt, vec4);
+  k_small_scatter<<<blocks, 1024, 0, s>>>(cases, poc, cnt, 1 << sp->n, pattern, case_id);
   if (init)
     k_small_init_lanes<<<std::min((cases + 255) / 256, 148 * 8), 256, 0, s>>>(
         *sp, ow, cases, m, case_base, init_key, pattern, case_id, lanes, lane_ld, init_key_dev);

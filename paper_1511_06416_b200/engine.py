@@ -970,4 +970,4 @@ class StreamGraphs:
     def launches_per_step(self) -> int:
         S = self.eng.cfg.sweeps_per_minibatch
         cpt_rb = any(d_.data_ptr() == self.eng.cpt.data_ptr() for d_, _ in self.readback)
-        return (1 if self._int8 is not None else 0) + 4 + (S - 1) + S + 1 + len(self.readback) - (1 if cpt_rb else 0)
+        return (1 if self._int8 is not None else 0) + 3 + (S - 1) + S + 1 + len(self.readback) - (1 if cpt_rb else 0)
