@@ -1264,10 +1264,20 @@ __device__ __forceinline__ void joint_cond_apply(const sg_net& net, const sg_sma
       const int2 p0 = pl[0];
 #pragma unroll
       for (int t = 0; t < (KC ? KC : card); ++t) w[t] = cpt[p0.x + t];
-      for (int f = 1; f < n_f; ++f) {
-        const int2 pf = pl[f];
+      if (KC) {  // unrolled over the factor bound: every factor's loads issue together
 #pragma unroll
-        for (int t = 0; t < (KC ? KC : card); ++t) w[t] = __dmul_rn(w[t], cpt[pf.x + t * pf.y]);
+        for (int f = 1; f < SG_JOINT_MAXF; ++f) {
+          if (f < n_f) {
+            const int2 pf = pl[f];
+#pragma unroll
+            for (int t = 0; t < (KC ? KC : 1); ++t) w[t] = __dmul_rn(w[t], cpt[pf.x + t * pf.y]);
+          }
+        }
+      } else {
+        for (int f = 1; f < n_f; ++f) {
+          const int2 pf = pl[f];
+          for (int t = 0; t < card; ++t) w[t] = __dmul_rn(w[t], cpt[pf.x + t * pf.y]);
+        }
       }
       joint_conditional<KC>(w, card, out);
     });
