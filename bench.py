@@ -614,7 +614,7 @@ def our_arm(args, wl: Workload) -> None:
                     "host_enqueue_us_per_step": host_enqueue_us, "h2d_warmup": h2d_warm},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",
-            "kernel_path": ("packed-lane sg_joint_sweep + sg_step_finish + sg_joint_tables" if eng.joint else
+            "kernel_path": ("packed-lane sg_joint_sweep + merged step tail (sg_step_tail_joint)" if eng.joint else
                             "packed-lane sg_small_sweep + sg_step_finish" if eng.use_small else
                             "generic sg_sweep + sg_step_finish"),
             "clocks": clk.summary(),
