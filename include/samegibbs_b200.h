@@ -137,8 +137,9 @@ typedef struct sg_net {
      records): [card, npar, nchl, own row base], ceil(npar/2) x [u, stride, u,
      stride], per child [c, row base, nrec, 0] + nrec x [u, stride, u, stride]
      (child row = base + x_c + sum x_u * stride).  bft is device scratch that
-     every large-network sg_sweep rewrites from its cpt argument (one stream
-     per pack at a time). */
+     every large-network sg_sweep rewrites from its cpt argument: sweeps on
+     different streams need structs with different bft buffers (the Python
+     engine gives each engine its own copy, NetPack.private_ref). */
   int64_t bft_rows;
   const int32_t* bft_start;  /* [n+1] */
   const int32_t* bft_desc;

@@ -88,6 +88,9 @@ class Engine:
         self.dev = device()
         self.coloring = color_graph(moralize(net))
         self.pack = netpack(net, self.coloring)
+        # the pack is shared (cached per network); the large-network sweep's
+        # blanket-factor scratch is this engine's own
+        self.sweep_net, self._sweep_net_keep = self.pack.private_ref()
         self.n = net.num_vars
         self.case_base = case_base
         self.comm = comm  # optional count all-reduce hook (multi-GPU, see parallel.py)
@@ -266,11 +269,11 @@ class Engine:
                 self.packed_sweep(db, size, m, sweep_seed, None, counts_ptr, obs.data_ptr() if last else None, ld, s)
             elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
-                _lib.call("sg_sweep", self.pack.ref, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
+                _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
                           self.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, None, self.keys.data_ptr(), None, None,
                           counts_ptr, self.err.ptr, s)
             else:
-                _lib.call("sg_sweep", self.pack.ref, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
+                _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
                           self.ftab.data_ptr(), _lib.SG_RNG_FAST, sweep_seed, None, None, None, None, counts_ptr,
                           self.err.ptr, s)
         if timing is not None:
@@ -696,11 +699,11 @@ class StepGraphs:
                 # numpy stream: stream_key(sweep_seed, "var", v) hashed on the device from the
                 # cursor's sweep seed (sampler.py:245, rng.py:16-20), then the bit-exact sweep
                 site_keys(eng.keys, ":var:", eng.n, seed_dev=cur + 8 * sw)
-                _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
+                _lib.call("sg_sweep", eng.sweep_net, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, None, eng.keys.data_ptr(), None, None, counts_ptr,
                           eng.err.ptr, s)
             else:
-                _lib.call("sg_sweep", eng.pack.ref, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
+                _lib.call("sg_sweep", eng.sweep_net, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
                           eng.err.ptr, s)
         if self._tev is not None:

@@ -521,6 +521,19 @@ class NetPack:
             self.joint, self.joint_header = jplan
             self.joint_ref = ctypes.byref(self.joint)
 
+    def private_ref(self):
+        """A copy of the ``sg_net`` struct with its own blanket-factor scratch
+        (``bft``): what an engine passes to ``sg_sweep`` so that sweeps of one
+        cached pack on different streams never share the scratch they rebuild.
+        Returns ``(ctypes reference, keep-alive tuple)``."""
+        s = SgNet()
+        ctypes.memmove(ctypes.addressof(s), ctypes.addressof(self.struct), ctypes.sizeof(SgNet))
+        bft = None
+        if self.bft is not None:
+            bft = torch.zeros_like(self.bft)
+            s.bft = bft.data_ptr()
+        return ctypes.byref(s), (s, bft)
+
     @property
     def n(self) -> int:
         return self.layout.n

@@ -264,3 +264,42 @@ def test_generic_graph_with_packed_uploads_equals_eager(bits, max_card):
     g.step(hmb)
     torch.cuda.synchronize()
     assert b.err.read() & _lib.SG_ERR_STATE_RANGE
+
+
+def test_engines_sharing_a_pack_sweep_on_two_streams():
+    """Two engines of one network (one cached NetPack) sweeping concurrently on
+    two streams: each rebuilds its own blanket factor tables (private sg_net
+    copy), so both equal the same runs made one after the other."""
+    from paper_1511_06416_b200 import netgen
+    from paper_1511_06416_b200.engine import Engine
+
+    net = netgen.random_dag_network(120, max_parents=4, min_card=2, max_card=4, seed=41)
+    truth = netgen.dirichlet_cpts(net, 1.0, seed=42)
+    cases = 20_000
+    obs = sg.forward_sample_device(net, truth, cases, seed=43, hide_fraction=0.3, mask_seed=44)
+    mb = next(iter(sg.DeviceSource(obs, cases, cases)))
+
+    def engines():
+        out = []
+        for seed in (1, 2):
+            cfg = sg.SamplerConfig(same_m=1, minibatch_size=cases, num_passes=1, seed=seed, rng="fast")
+            out.append(Engine(net, cfg))
+        return out
+
+    seq = engines()
+    for e in seq:
+        for p in range(4):
+            e.visit(mb, p, 1)
+    torch.cuda.synchronize()
+    par = engines()
+    assert par[0].pack is par[1].pack
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    for p in range(4):
+        for e, s in zip(par, streams):
+            with torch.cuda.stream(s):
+                e.visit(mb, p, 1)
+    torch.cuda.synchronize()
+    for a, b in zip(seq, par):
+        np.testing.assert_array_equal(a.cpt.cpu().numpy(), b.cpt.cpu().numpy())
+        np.testing.assert_array_equal(a.lane_states(0).cpu().numpy(), b.lane_states(0).cpu().numpy())
