@@ -395,7 +395,7 @@ def our_arm(args, wl: Workload) -> None:
     for w in range(args.warmup):
         eng.visit(mb, w, M)
     torch.cuda.synchronize()
-    e2e_steps = max(3, min(args.steps, 200))  # long enough that one host hiccup does not dominate
+    e2e_steps = max(4, min(args.steps, 200)) // 2 * 2  # long enough that one host hiccup does not dominate
     graph_warm = 3
     first = args.warmup
     graphs = None
@@ -495,11 +495,15 @@ def our_arm(args, wl: Workload) -> None:
     cpt_host = torch.empty(eng.pack.cells, dtype=torch.float64, pin_memory=True)
     e2e_graphs = None
     if graphs is not None:
-        # host-fed step graphs: each replay uploads the next visit's pinned block on a
-        # side branch overlapped with the sweep, and reads the CPTs back at its end
+        # host-fed step graphs: each step() uploads the pinned blocks of the visits two
+        # ahead on a copy stream overlapped with the replay; every visit's tail stores its
+        # CPTs into pinned host memory; two visits per graph replay
         graphs.finish()
         e2e_graphs = StepGraphs(eng, mb, M, range(first + args.steps + 10, first + args.steps + 20 + e2e_steps),
-                                obs_bits=graphs.obs_bits, host_block=host_obs, readback=[(eng.cpt, cpt_host)])
+                                obs_bits=graphs.obs_bits, host_block=host_obs, readback=[(eng.cpt, cpt_host)],
+                                visits_per_replay=2)
+    per_call = e2e_graphs.vpr if e2e_graphs is not None else 1  # visits per e2e_step() call
+    e2e_calls = e2e_steps // per_call
 
     ready = [torch.cuda.Event(), torch.cuda.Event()]
 
@@ -544,13 +548,13 @@ def our_arm(args, wl: Workload) -> None:
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dbg = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)] if os.environ.get("SG_E2E_DEBUG") else None
+    dbg = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_calls)] if os.environ.get("SG_E2E_DEBUG") else None
     if dbg and e2e_graphs is not None:
         e2e_graphs.debug_events = []
     with ClockSampler(local) as e2e_clk:
         e0.record()
         h0 = time.perf_counter()
-        for k in range(e2e_steps):
+        for k in range(e2e_calls):
             e2e_step(k)
             if dbg:
                 dbg[k].record()
@@ -559,7 +563,7 @@ def our_arm(args, wl: Workload) -> None:
         torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if dbg:
-        print("e2e per-step us:", [round((dbg[k].elapsed_time(dbg[k + 1])) * 1e3, 1) for k in range(e2e_steps - 1)],
+        print("e2e per-call us:", [round((dbg[k].elapsed_time(dbg[k + 1])) * 1e3, 1) for k in range(e2e_calls - 1)],
               file=sys.stderr)
         if e2e_graphs is not None and e2e_graphs.debug_events:
             for k, ev in enumerate(e2e_graphs.debug_events[10:16]):
@@ -611,6 +615,10 @@ def our_arm(args, wl: Workload) -> None:
                     "mode": ("the C2 minibatch (moving sum, lanes resident) re-uploaded from pinned memory and "
                              "range-checked every step, CPTs read back every step; `--workload c2s` streams "
                              "different minibatches that each step samples"),
+                    "launch": (f"{per_call} visits per graph replay, uploads on a copy stream"
+                               if e2e_graphs is not None else "eager visits"),
+                    # the step's upload against the link: the e2e step is PCIe-bound when this nears the best rate
+                    "h2d_gbs": host_obs.numel() * host_obs.element_size() / (e2e_ms * 1e-3) / 1e9,
                     "host_enqueue_us_per_step": host_enqueue_us, "h2d_warmup": h2d_warm},
             "gpu_launches": launches,
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",

@@ -15,6 +15,7 @@ device; the running total is fp64 and follows the reference's rounding.
 from __future__ import annotations
 
 import ctypes
+import math
 import time
 
 import numpy as np
@@ -498,7 +499,7 @@ class StepGraphs:
 
     def __init__(self, eng: Engine, mb, m: int, pass_indices, obs_buffer: torch.Tensor | None = None,
                  nibbles: bool = False, host_block: torch.Tensor | None = None, readback=(), obs_bits: int = 8,
-                 timing: bool = False):
+                 timing: bool = False, visits_per_replay: int = 1):
         """``obs_buffer``: device int8 (n, pitch) tensor the graphs read the
         minibatch's observations from; the caller keeps it filled (e.g. a
         device-resident source).  Default: a private buffer that
@@ -523,8 +524,18 @@ class StepGraphs:
         (device tensor, pinned host tensor) copied back at the end of each
         replay (e.g. the CPTs).  ``timing``: external timing events bracket the
         sweep node(s) inside each graph; :meth:`sweep_ms` reads the last
-        replay's sweep duration (call after synchronising)."""
+        replay's sweep duration (call after synchronising).
+        ``visits_per_replay`` 2: each graph holds two consecutive visits (the
+        second sweep's prologue overlaps the first tail under PDL, and one
+        graph launch serves two visits); step() then replays two visits and
+        takes no minibatch (host-fed or device-resident observations)."""
         cfg = eng.cfg
+        self.vpr = int(visits_per_replay)
+        if self.vpr not in (1, 2):
+            raise ValueError("visits_per_replay must be 1 or 2")
+        pass_indices = list(pass_indices)
+        if self.vpr > 1 and (timing or len(pass_indices) % self.vpr):
+            raise ValueError("two visits per replay: an even number of visits, no sweep timing")
         if cfg.accumulator_mode != "moving_sum":
             raise ValueError("graph replay of resident minibatches needs the moving-sum accumulator")
         db = eng.latent.get(mb.index)
@@ -564,8 +575,9 @@ class StepGraphs:
             src, _ = eng._obs_for(mb)
             bufs = []
             shape, dt = self.obs_geometry(eng.n, mb.size, self.obs_bits)
-            # host-fed graphs keep three: the upload of visit k + 2 starts with visit k
-            for _ in range(3 if host_block is not None else 2):
+            # host-fed graphs keep 2 + visits_per_replay: the uploads for the visits two
+            # ahead start with the current replay, into buffers the previous replay read
+            for _ in range(2 + self.vpr if host_block is not None else 2):
                 b = torch.empty(shape, dtype=dt, device=d)
                 if self.nibbles:
                     b.copy_(pack_bits(src[:, :mb.size], shape[1] * 8 // self.obs_bits, self.obs_bits))
@@ -618,11 +630,14 @@ class StepGraphs:
         _lib.call("sg_keys_advance", self.table.data_ptr(), self.idx.data_ptr(), kps, self.cur.data_ptr(),
                   stream_handle())
         torch.cuda.synchronize()
-        # graph k: count parity k % 2, observation buffer k % len(bufs) (2 or 6 graphs)
-        for k in range(2 if len(bufs) == 2 else 6):
+        # visit k: count parity k % 2, observation buffer k % len(bufs); graph j holds
+        # visits j * vpr ... j * vpr + vpr - 1 of one period lcm(2, len(bufs))
+        period = 2 * len(bufs) // math.gcd(2, len(bufs))
+        for j in range(period // self.vpr):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self._record(k)
+                for i in range(self.vpr):
+                    self._record(j * self.vpr + i)
             self.graphs.append(g)
         torch.cuda.synchronize()
 
@@ -729,40 +744,50 @@ class StepGraphs:
         if mb is not None and self.host_block is not None:
             raise ValueError("this graph uploads its own host block; call step() without a minibatch")
         if self.host_block is not None:
-            # three buffers: upload visit k + 2's block into the buffer visit k - 1 read
-            # while this replay runs, so an upload has two replays' time to land
-            nb = len(self.obs_bufs)
-            p = self.replayed % nb
-            q = (self.replayed + 2) % nb
-            gk = self.replayed % len(self.graphs)
+            # upload the blocks of the visits two ahead (buffers the previous replay read)
+            # while this replay runs, so an upload has a replay's time to land
+            nb, vpr, k0 = len(self.obs_bufs), self.vpr, self.replayed
+            mine = [(k0 + i) % nb for i in range(vpr)]
+            gk = (k0 // vpr) % len(self.graphs)
             up = self._up_stream
-            if self._read_pending[q]:
-                up.wait_event(self._read_done[q])  # the replay that last read buffer q has finished
-            nxt = self.obs_bufs[q]
             dbg = self.debug_events
             if dbg is not None:
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                 ev[0].record(up)
-            _lib.call("sg_copy_async", nxt.data_ptr(), self.host_block.data_ptr(), nxt.numel() * nxt.element_size(),
-                      up.cuda_stream)
+            for i in range(vpr):
+                q = (k0 + 2 + i) % nb
+                if self._read_pending[q]:
+                    up.wait_event(self._read_done[q])  # the replay that last read buffer q has finished
+                nxt = self.obs_bufs[q]
+                _lib.call("sg_copy_async", nxt.data_ptr(), self.host_block.data_ptr(),
+                          nxt.numel() * nxt.element_size(), up.cuda_stream)
+                self._uploaded[q].record(up)
+                self.upload_done = self._uploaded[q]
+                self._up_pending[q] = True
             if dbg is not None:
                 ev[1].record(up)
-            self._uploaded[q].record(up)
-            self.upload_done = self._uploaded[q]
-            self._up_pending[q] = True
-            if self._up_pending[p]:
-                main.wait_event(self._uploaded[p])
-                self._up_pending[p] = False
+            for p in mine:
+                if self._up_pending[p]:
+                    main.wait_event(self._uploaded[p])
+                    self._up_pending[p] = False
             if dbg is not None:
                 ev[2].record(main)
             self.graphs[gk].replay()
             if dbg is not None:
                 ev[3].record(main)
                 dbg.append(ev)
-            self._read_done[p].record(main)
-            self._read_pending[p] = True
-            self.replayed += 1
-            _lib.launch_count += self.launches_per_step
+            for p in mine:
+                self._read_done[p].record(main)
+                self._read_pending[p] = True
+            self.replayed += vpr
+            _lib.launch_count += self.launches_per_step * vpr
+            return
+        if self.vpr > 1:
+            if mb is not None:
+                raise ValueError("two visits per replay take no minibatch")
+            self.graphs[(self.replayed // 2) % len(self.graphs)].replay()
+            self.replayed += 2
+            _lib.launch_count += self.launches_per_step * 2
             return
         if mb is not None:
             vals = mb.values
