@@ -245,8 +245,9 @@ def test_joint_graph_with_4bit_uploads_equals_eager(koller, bits):
     assert b.err.read() & _lib.SG_ERR_STATE_RANGE
 
 
-@pytest.mark.parametrize("rng,bits", [("joint", 4), ("joint", 2), ("joint", 8), ("fast", 8)])
-def test_host_fed_step_graphs_equal_eager(koller, rng, bits):
+@pytest.mark.parametrize("rng,bits,vpr", [("joint", 4, 1), ("joint", 2, 1), ("joint", 8, 1), ("fast", 8, 1),
+                                          ("joint", 2, 2), ("fast", 8, 2)])
+def test_host_fed_step_graphs_equal_eager(koller, rng, bits, vpr):
     """StepGraphs(host_block=...): each replay uploads the next visit's pinned
     block beside the sweep and reads the CPTs back -- same results as eager
     visits, and the read-back CPTs are the engine's."""
@@ -270,8 +271,9 @@ def test_host_fed_step_graphs_equal_eager(koller, rng, bits):
         host.fill_(-1)
         host[:, :cases].copy_(obs[:, :cases])
     cpt_host = torch.empty(b.pack.cells, dtype=torch.float64, pin_memory=True)
-    g = StepGraphs(b, mb, m, range(1, 5), obs_bits=bits, host_block=host, readback=[(b.cpt, cpt_host)])
-    for _ in range(4):
+    g = StepGraphs(b, mb, m, range(1, 5), obs_bits=bits, host_block=host, readback=[(b.cpt, cpt_host)],
+                   visits_per_replay=vpr)
+    for _ in range(4 // vpr):
         g.step()
     g.finish()
     torch.cuda.synchronize()
