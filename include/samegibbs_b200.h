@@ -175,6 +175,9 @@ int sg_abi_version(void);
 /* Stream-ordered copy (cudaMemcpyDefault: pinned host <-> device), recorded
    as a memcpy node when `stream` is capturing a CUDA graph. */
 int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* cudaMemcpy2DAsync: height rows of width bytes (pitches in bytes). */
+int sg_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                    int64_t height, void* stream);
 
 /* Small stream-ordered copy done by a kernel (8-byte aligned); dst may be
    pinned host memory (mapped through unified addressing). */

@@ -127,6 +127,7 @@ _SIGNATURES = {
                         c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p], c_int32),
     "sg_keys_advance": ([c_void_p, c_void_p, c_int32, c_void_p, c_void_p], c_int32),
     "sg_copy_async": ([c_void_p, c_void_p, c_int64, c_void_p], c_int32),
+    "sg_copy2d_async": ([c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_void_p], c_int32),
     "sg_copy_small": ([c_void_p, c_void_p, c_int64, c_void_p], c_int32),
     "sg_event_create": ([POINTER(c_uint64)], c_int32),
     "sg_event_record": ([c_uint64, c_void_p], c_int32),
@@ -181,7 +182,7 @@ KERNELS_PER_CALL = {
     "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
     "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
     "sg_joint_tables": 1, "sg_joint_sweep": 1, "sg_step_tail_joint": 1, "sg_joint_prep": 1, "sg_copy_small": 1, "sg_noop": 1,
-    "sg_keys_advance": 1, "sg_step_finish": 1, "sg_site_keys": 1, "sg_predict_tally": 1, "sg_unpack_nibbles": 1, "sg_unpack_crumbs": 1,
+    "sg_keys_advance": 1, "sg_copy2d_async": 1, "sg_step_finish": 1, "sg_site_keys": 1, "sg_predict_tally": 1, "sg_unpack_nibbles": 1, "sg_unpack_crumbs": 1,
 }
 launch_count = 0
 

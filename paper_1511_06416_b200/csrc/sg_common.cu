@@ -46,6 +46,56 @@ extern "C" int sg_copy_async(void* dst, const void* src, int64_t bytes, void* st
   return SG_OK;
 }
 
+namespace sg {
+// 16-byte vectors of a row block; the last partial vector of a row byte by byte
+__global__ void __launch_bounds__(256) k_copy_rows(unsigned char* __restrict__ dst, int64_t dpitch,
+                                                   const unsigned char* __restrict__ src, int64_t spitch,
+                                                   int64_t width, int64_t height) {
+  const int64_t vecs = width >> 4, tail = width & 15;
+  const int64_t per_row = vecs + (tail ? 1 : 0);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per_row * height;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / per_row, k = i - r * per_row;
+    if (k < vecs) {
+      reinterpret_cast<int4*>(dst + r * dpitch)[k] = __ldcs(reinterpret_cast<const int4*>(src + r * spitch) + k);
+    } else {
+      for (int64_t b = vecs << 4; b < width; ++b) dst[r * dpitch + b] = src[r * spitch + b];
+    }
+  }
+}
+}  // namespace sg
+
+// Row block copy (height rows of width bytes, pitches in bytes): a minibatch
+// block between (n, pitch) layouts.  Device to device with 16-byte aligned
+// rows: an SM kernel (a copy engine moved the 5 MB C2 block at ~0.3 TB/s);
+// otherwise cudaMemcpy2DAsync.
+extern "C" int sg_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                               int64_t height, void* stream) {
+  using namespace sg;
+  SG_REQUIRE(dst && src && width >= 0 && height >= 0 && dpitch >= width && spitch >= width,
+             "sg_copy2d_async: bad argument");
+  if (width == 0 || height == 0) return SG_OK;
+  cudaPointerAttributes ad{}, as{};
+  const bool dev = cudaPointerGetAttributes(&ad, dst) == cudaSuccess && cudaPointerGetAttributes(&as, src) == cudaSuccess &&
+                   ad.type == cudaMemoryTypeDevice && as.type == cudaMemoryTypeDevice;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0 &&
+                       dpitch % 16 == 0 && spitch % 16 == 0;
+  if (dev && aligned) {
+    const int64_t items = ((width + 15) >> 4) * height;
+    const int blocks = int(std::min<int64_t>((items + 255) / 256, 148 * 8));
+    k_copy_rows<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<unsigned char*>(dst), dpitch,
+                                                          static_cast<const unsigned char*>(src), spitch, width, height);
+    return check_launch("sg_copy2d_async");
+  }
+  const cudaError_t e = cudaMemcpy2DAsync(dst, size_t(dpitch), src, size_t(spitch), size_t(width), size_t(height),
+                                          cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    set_error("sg_copy2d_async: %s", cudaGetErrorString(e));
+    return SG_ECUDA;
+  }
+  return SG_OK;
+}
+
 // Small copy as a kernel (graph kernel nodes launch faster than memcpy
 // nodes): dst may be pinned host memory, which unified addressing maps into
 // the device's address space -- the step graph's CPT read-back.

@@ -51,6 +51,19 @@ class PinnedRing:
         return self.bufs[i], self.events[i]
 
 
+def copy_rows(dst: torch.Tensor, src: torch.Tensor, cols: int) -> None:
+    """``dst[:, :cols] = src[:, :cols]`` in stream order for device (or pinned)
+    row blocks: one 2-D copy (a byte-wise strided copy kernel moved the 5 MB
+    C2 block at ~0.3 TB/s)."""
+    if (dst.dim() == 2 and src.dim() == 2 and dst.dtype == src.dtype and dst.stride(1) == 1 and src.stride(1) == 1
+            and dst.shape[0] == src.shape[0] and (src.is_cuda or src.is_pinned())):
+        es = dst.element_size()
+        _lib.call("sg_copy2d_async", dst.data_ptr(), dst.stride(0) * es, src.data_ptr(), src.stride(0) * es, cols * es,
+                  dst.shape[0], stream_handle())
+    else:
+        dst[:, :cols].copy_(src[:, :cols], non_blocking=True)
+
+
 class SmallBatch:
     """Packed-lane minibatch (sg_small layout): one uint8 word per lane, slots bucketed by latent pattern."""
 
@@ -809,7 +822,7 @@ class StepGraphs:
                     if self.nibbles:
                         buf.copy_(src, non_blocking=True)
                     else:
-                        buf[:, :mb.size].copy_(src, non_blocking=True)
+                        copy_rows(buf, src, mb.size)
                 else:
                     # upload on the copy stream once the replay that last read this buffer is done,
                     # so it overlaps the other parity's replay
@@ -968,7 +981,7 @@ class StreamGraphs:
             if self.obs_bits < 8:
                 buf.copy_(vals, non_blocking=True)
             else:
-                buf[:, :self.size].copy_(vals, non_blocking=True)
+                copy_rows(buf, vals, self.size)
         else:
             host = vals.numpy() if isinstance(vals, torch.Tensor) else np.asarray(vals)
             if self.obs_bits == 8:

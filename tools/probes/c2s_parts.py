@@ -60,3 +60,6 @@ def drain():
 
 
 print("HostSource pass (8 blocks: H2D + decode), per block:", round(timed(drain, 3) / 8, 1), "us")
+from paper_1511_06416_b200.engine import copy_rows  # noqa: E402
+
+print("2-D copy of the int8 block (copy_rows):", round(timed(lambda: copy_rows(ob, obs, B)), 1), "us")
