@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(1024) k_small_scatter(const int cases, const u
 // from the data, latent fields from the FAST init stream (same draw as
 // k_init_states: Philox4x32(key, (case, v, r/4, purpose 1))[r%4] * card >> 32;
 // the key's and the case's part of the first round computed once per slot).
+template <int N>  // variables (compile-time: the variable loop unrolls, latent tests are warp-uniform)
 __global__ void __launch_bounds__(256) k_small_init_lanes(
     const sg_small sp, const uint8_t* __restrict__ obsw_of_case, int cases, int m, int64_t case_base,
     uint64_t init_key, const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id,
@@ -186,12 +187,16 @@ __global__ void __launch_bounds__(256) k_small_init_lanes(
     const FastCase fc = fast_case(fk, uint32_t(case_base + c));
     for (int q = 0; q < (m + 3) / 4; ++q) {
       uint32_t S[4] = {obsw, obsw, obsw, obsw};
-      for (int v = 0; v < sp.n; ++v) {
+#pragma unroll
+      for (int v = 0; v < N; ++v) {
         if (!((P >> v) & 1u)) continue;
         const u32x4 w = fast_draw(fc, fast_word(uint32_t(v), uint32_t(q), 1u));
-        const uint32_t ws[4] = {w.a, w.b, w.c, w.d};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) S[j] |= uint32_t((uint64_t(ws[j]) * uint32_t(sp.card[v])) >> 32) << sp.off[v];
+        const uint32_t card = uint32_t(sp.card[v]), off = uint32_t(sp.off[v]);
+        // (w * card) >> 32 of the 64-bit product: its high word
+        S[0] |= __umulhi(w.a, card) << off;
+        S[1] |= __umulhi(w.b, card) << off;
+        S[2] |= __umulhi(w.c, card) << off;
+        S[3] |= __umulhi(w.d, card) << off;
       }
       uint32_t word = 0;
 #pragma unroll
@@ -1521,9 +1526,24 @@ extern "C" int sg_small_prepare(const sg_small* sp, const int8_t* obs, int32_t l
   const bool vec4 = ld_obs % 4 == 0 && ld_obs >= (cases + 3) / 4 * 4 && (reinterpret_cast<uintptr_t>(obs) & 3) == 0;
   k_small_count<<<blocks, 1024, 0, s>>>(*sp, obs, ld_obs, cases, poc, ow, cnt, vec4);
   k_small_scatter<<<blocks, 1024, 0, s>>>(cases, poc, cnt, 1 << sp->n, pattern, case_id);
-  if (init)
-    k_small_init_lanes<<<std::min((cases + 255) / 256, 148 * 8), 256, 0, s>>>(
-        *sp, ow, cases, m, case_base, init_key, pattern, case_id, lanes, lane_ld, init_key_dev);
+  if (init) {
+    const int grid = std::min((cases + 255) / 256, 148 * 8);
+#define SG_INIT_LANES(N)                                                                                         \
+  case N:                                                                                                      \
+    k_small_init_lanes<N><<<grid, 256, 0, s>>>(*sp, ow, cases, m, case_base, init_key, pattern, case_id, lanes, \
+                                               lane_ld, init_key_dev);                                           \
+    break;
+    switch (sp->n) {
+      SG_INIT_LANES(1)
+      SG_INIT_LANES(2)
+      SG_INIT_LANES(3)
+      SG_INIT_LANES(4)
+      SG_INIT_LANES(5)
+      SG_INIT_LANES(6)
+      default: SG_INIT_LANES(7)
+    }
+#undef SG_INIT_LANES
+  }
   return check_launch("sg_small_prepare");
 }
 
