@@ -455,6 +455,16 @@ typedef struct sg_finish {
                                  stored there by the kernel that writes them (the step's result
                                  read back without a copy node; visible once the call's work is
                                  complete) */
+  /* sg_step_tail_joint only (NULL for sg_step_finish): range check of this step's
+     observation block (sampler.py:429-430) by the tail's row slices, beside the model
+     update (the preceding sg_joint_sweep is then called with obs = NULL): check_obs
+     [dev] int8 rows or packed .sgb rows (check_bits 8 / 4 / 2), check_ld bytes per
+     row, check_cases cases; out-of-range states set SG_ERR_STATE_RANGE in *check_err. */
+  const void* check_obs;
+  int32_t check_ld;
+  int32_t check_bits;
+  int32_t check_cases;
+  int32_t* check_err;
 } sg_finish;
 
 /* sg_finish.flags: the packed table is the only consumer of this step's

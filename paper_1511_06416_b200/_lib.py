@@ -82,7 +82,8 @@ class SgFinish(ctypes.Structure):
         ("key", c_uint64), ("key_dev", c_void_p), ("cpt", c_void_p), ("ptab", c_void_p), ("ftab", c_void_p),
         ("stab", c_void_p), ("clear_counts", c_void_p), ("key_table", c_void_p), ("key_index", c_void_p),
         ("kps", c_int32), ("flags", c_int32), ("key_current", c_void_p), ("vprob", c_void_p),
-        ("cpt_host", c_void_p),
+        ("cpt_host", c_void_p), ("check_obs", c_void_p), ("check_ld", c_int32), ("check_bits", c_int32),
+        ("check_cases", c_int32), ("check_err", c_void_p),
     ]
 
 

@@ -52,6 +52,62 @@ __device__ __forceinline__ void mean_row(const double* total, double a, int card
   for (int s = 0; s < (K ? K : card); ++s) out[s] = __ddiv_rn(sh[s], sum);
 }
 
+__device__ __forceinline__ uint32_t packed_invalid(uint32_t w, int card, int nib) {
+  if (nib == 2) {  // crumbs: 3 = missing; only 2 can be out of range (binary variables)
+    return card >= 3 ? 0u : ((w >> 1) & ~w & 0x55555555u);
+  }
+  const uint32_t lim = 0x01010101u * uint32_t(card - 1);  // nibbles: 15 = missing
+  const uint32_t xe = w & 0x0F0F0F0Fu, xo = (w >> 4) & 0x0F0F0F0Fu;
+  return (__vcmpgtu4(xe, lim) & ~__vcmpeq4(xe, 0x0F0F0F0Fu)) | (__vcmpgtu4(xo, lim) & ~__vcmpeq4(xo, 0x0F0F0F0Fu));
+}
+
+// Range check of an observation block (int8, or packed .sgb rows with nib 4 /
+// 2) by threads gtid = 0 .. gthreads - 1 of the caller's choosing: a whole grid
+// (the sweeps) or one CTA (the step tail's model update, while the sweep runs).
+__device__ __forceinline__ void obs_range_check_range(const sg_small& sp, const int8_t* __restrict__ obs, int ld_obs,
+                                                      int cases, int32_t* err, int nib, int gtid, int gthreads) {
+  if (!obs || cases <= 0) return;
+  const bool packed = nib == 4 || nib == 2;
+  const int per_word = packed ? 32 / nib : 4;  // cases per 32-bit word
+  const int words = (cases + per_word - 1) / per_word;
+  const int vecs = (words + 3) >> 2;
+  unsigned bad = 0;
+  for (int i = gtid; i < sp.n * vecs; i += gthreads) {
+    int v = 0, q = i;  // (row, vector): n <= 7 subtractions instead of a division
+    while (q >= vecs) {
+      q -= vecs;
+      ++v;
+    }
+    const int card = sp.card[v];
+    const uint4* row = reinterpret_cast<const uint4*>(obs + int64_t(v) * ld_obs);
+    const uint32_t lim = 0x01010101u * uint32_t(card - 1);
+    {
+      const uint4 x = __ldcs(row + q);
+      const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int first = (4 * q + k) * per_word;  // first case of this word
+        if (first >= cases) break;
+        uint32_t b = packed ? packed_invalid(wv[k], card, nib) : __vcmpgts4(wv[k], lim);
+        const int valid = cases - first;
+        if (valid < per_word) {  // the row's last word: cases past the minibatch do not count
+          const int field_bits = packed ? nib : 8;
+          if (packed && nib == 4) {  // planes: byte b of the even plane is case 2b, of the odd plane 2b + 1
+            uint32_t keep = 0;
+            for (int j = 0; j < valid; ++j) keep |= 0xFu << (4 * j);
+            const uint32_t we = wv[k] | ~keep;  // cases past `valid` read as missing (15)
+            b = packed_invalid(we, card, nib);
+          } else {
+            b &= valid * field_bits >= 32 ? 0xFFFFFFFFu : ((1u << (valid * field_bits)) - 1u);
+          }
+        }
+        bad |= b;
+      }
+    }
+  }
+  if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
+}
+
 struct FinishArgs {
   int acc_mode, map_estimate;
   double decay;
@@ -77,6 +133,9 @@ struct FinishArgs {
   // flags in the bytes after them; the readers normalise the rows themselves
   double* release_lg;
   double* cpt_host;  // != NULL: mapped pinned host copy of the new CPTs
+  const int8_t* check_obs;  // != NULL: the merged tail's row slices range-check this block
+  int check_ld, check_nib, check_cases;
+  int32_t* check_err;
   int has_small;
   int early_inputs;  // the preceding sweep triggers only after its own wait: read total/prev/key before ours
   int packed_only;  // SG_FINISH_PACKED_ONLY: skip ptab/ftab, build stab from the CPTs
@@ -319,6 +378,16 @@ __device__ __forceinline__ void step_finish_body(const sg_net& gnet, const Finis
 
 
 // Kernel-side copy of an sg_finish (+ optional packed plan).
+// The optional observation-block check of sg_finish is well formed.
+inline bool finish_check_ok(const sg_finish* f, const sg_small* sp) {
+  if (!f->check_obs) return true;
+  const int b = f->check_bits;
+  const int per_byte = b == 4 || b == 2 ? 8 / b : 1;
+  return sp && f->check_err && (b == 8 || b == 4 || b == 2 || b == 0) && f->check_ld % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(f->check_obs) & 15) == 0 && f->check_cases >= 0 &&
+         int64_t(f->check_ld) * per_byte >= f->check_cases;
+}
+
 inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
   FinishArgs a;
   a.acc_mode = f->acc_mode;
@@ -341,6 +410,11 @@ inline FinishArgs make_finish_args(const sg_finish* f, const sg_small* sp) {
   a.key_current = f->key_current;
   a.vprob = sp ? f->vprob : nullptr;
   a.cpt_host = f->cpt_host;
+  a.check_obs = sp ? static_cast<const int8_t*>(f->check_obs) : nullptr;
+  a.check_ld = f->check_ld;
+  a.check_nib = f->check_bits == 4 || f->check_bits == 2 ? f->check_bits : 0;
+  a.check_cases = f->check_cases;
+  a.check_err = f->check_err;
   a.early_inputs = 0;
   a.release_sync = nullptr;
   a.release_lg = nullptr;

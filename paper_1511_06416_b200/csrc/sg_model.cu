@@ -127,6 +127,7 @@ extern "C" int sg_step_finish(const sg_net* net, const sg_small* sp, const sg_fi
   SG_REQUIRE(net->max_card <= SG_MAX_CARD && net->max_mb <= SG_MAX_MB, "sg_step_finish: capacity exceeded");
   if (net->table_entries > 0) SG_REQUIRE(f->ptab && f->ftab, "sg_step_finish: tables required");
   if (sp) SG_REQUIRE(f->stab, "sg_step_finish: packed table required");
+  SG_REQUIRE(!f->check_obs, "sg_step_finish: the observation check is sg_step_tail_joint's");
   if (f->key_table) SG_REQUIRE(f->key_index && f->key_current && f->kps > 0, "sg_step_finish: bad key cursor");
   cudaStream_t s = (cudaStream_t)stream;
   if (finish_fits(*net, sp)) {

@@ -399,60 +399,11 @@ __device__ __forceinline__ bool small_units(const SmallOrd& o, const QuadSet& qs
 // rows (-1 = missing; bytes compared as signed SIMD lanes against card - 1)
 // or packed .sgb rows (nib = 4 / 2 bits per case, all-ones = missing).
 // Sets SG_ERR_STATE_RANGE.
-__device__ __forceinline__ uint32_t packed_invalid(uint32_t w, int card, int nib) {
-  if (nib == 2) {  // crumbs: 3 = missing; only 2 can be out of range (binary variables)
-    return card >= 3 ? 0u : ((w >> 1) & ~w & 0x55555555u);
-  }
-  const uint32_t lim = 0x01010101u * uint32_t(card - 1);  // nibbles: 15 = missing
-  const uint32_t xe = w & 0x0F0F0F0Fu, xo = (w >> 4) & 0x0F0F0F0Fu;
-  return (__vcmpgtu4(xe, lim) & ~__vcmpeq4(xe, 0x0F0F0F0Fu)) | (__vcmpgtu4(xo, lim) & ~__vcmpeq4(xo, 0x0F0F0F0Fu));
-}
-
 template <int NT>
 __device__ __forceinline__ void obs_range_check(const sg_small& sp, const int8_t* __restrict__ obs, int ld_obs,
                                                 int cases, int32_t* err, int nib) {
-  if (!obs || cases <= 0) return;
-  const int gtid = (blockIdx.y * gridDim.x + blockIdx.x) * NT + threadIdx.x;
-  const int gthreads = gridDim.x * gridDim.y * NT;
-  const bool packed = nib == 4 || nib == 2;
-  const int per_word = packed ? 32 / nib : 4;  // cases per 32-bit word
-  const int words = (cases + per_word - 1) / per_word;
-  const int vecs = (words + 3) >> 2;
-  unsigned bad = 0;
-  for (int i = gtid; i < sp.n * vecs; i += gthreads) {
-    int v = 0, q = i;  // (row, vector): n <= 7 subtractions instead of a division
-    while (q >= vecs) {
-      q -= vecs;
-      ++v;
-    }
-    const int card = sp.card[v];
-    const uint4* row = reinterpret_cast<const uint4*>(obs + int64_t(v) * ld_obs);
-    const uint32_t lim = 0x01010101u * uint32_t(card - 1);
-    {
-      const uint4 x = __ldcs(row + q);
-      const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int first = (4 * q + k) * per_word;  // first case of this word
-        if (first >= cases) break;
-        uint32_t b = packed ? packed_invalid(wv[k], card, nib) : __vcmpgts4(wv[k], lim);
-        const int valid = cases - first;
-        if (valid < per_word) {  // the row's last word: cases past the minibatch do not count
-          const int field_bits = packed ? nib : 8;
-          if (packed && nib == 4) {  // planes: byte b of the even plane is case 2b, of the odd plane 2b + 1
-            uint32_t keep = 0;
-            for (int j = 0; j < valid; ++j) keep |= 0xFu << (4 * j);
-            const uint32_t we = wv[k] | ~keep;  // cases past `valid` read as missing (15)
-            b = packed_invalid(we, card, nib);
-          } else {
-            b &= valid * field_bits >= 32 ? 0xFFFFFFFFu : ((1u << (valid * field_bits)) - 1u);
-          }
-        }
-        bad |= b;
-      }
-    }
-  }
-  if (bad) atomicOr(err, int(SG_ERR_STATE_RANGE));
+  obs_range_check_range(sp, obs, ld_obs, cases, err, nib, (blockIdx.y * gridDim.x + blockIdx.x) * NT + threadIdx.x,
+                        gridDim.x * gridDim.y * NT);
 }
 
 // The common end of both packed sweeps: ZeroSupport word, the minibatch's
@@ -954,6 +905,15 @@ __device__ __forceinline__ void tail_stamp(int) {}
 __host__ __device__ __forceinline__ int joint_tail_slices(int B) { return B >= 6 ? 2 * SG_JOINT_TAB_SLICES : SG_JOINT_TAB_SLICES; }
 #define SG_JOINT_ROW_WARPS (FINISH_THREADS / 32)
 
+// The row-slice map of the merged tail as a kernel parameter (built on the
+// host from the latent field widths): a slice knows its pattern without
+// reading the blob header first, so its preparation copy starts at once.
+#define SG_TAIL_ROLE_MAX 512
+struct TailRoles {
+  int count;                            // 0: walk the blob header (tail_slice_of)
+  uint16_t r[SG_TAIL_ROLE_MAX];         // P | slice << 7 | slices of P << 11
+};
+
 // Row slice k of the merged tail -> (pattern P, slice of P, slices of P):
 // patterns from the last down (the all-latent pattern, 64 columns, first:
 // the costliest slices take the first tickets, i.e. the earliest CTAs), P =
@@ -1328,9 +1288,15 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
                                                                     const sg_small sp, const sg_joint jp,
                                                                     uint32_t* jblob, uint32_t* sync,
                                                                     const unsigned char* __restrict__ prep,
-                                                                    int64_t prep_bytes) {
+                                                                    int64_t prep_bytes, const TailRoles roles) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_role;
+  // the step's observation block, range-checked by every CTA (a share each, by block
+  // index: before the role ticket) while the model update and the slices' preparation
+  // proceed -- the sweep skips its check then
+  if (f.check_obs)
+    obs_range_check_range(sp, f.check_obs, f.check_ld, f.check_cases, f.check_err, f.check_nib,
+                          int(blockIdx.x * blockDim.x + threadIdx.x), int(gridDim.x * blockDim.x));
   if (threadIdx.x == 0) s_role = int(atomicAdd(sync + 2, 1u));
   __syncthreads();
   const int role = s_role;  // 0: the model update; r >= 1: row slice r - 1
@@ -1365,10 +1331,19 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   int8_t* plan_nf = reinterpret_cast<int8_t*>(plan + size_t(nr) * SG_JOINT_MAXF);
   uint16_t* pidx = reinterpret_cast<uint16_t*>(plan_nf + ((size_t(nr) + 15) & ~size_t(15)));
   int P, slice, nsl;
-  tail_slice_of(jblob, jp, role - 1, P, slice, nsl);
+  bool live;
+  if (roles.count) {
+    const uint32_t e = roles.r[role - 1];
+    P = int(e & 127u);
+    slice = int((e >> 7) & 15u);
+    nsl = int(e >> 11);
+    live = P != 0;  // every other pattern has latent fields
+  } else {
+    tail_slice_of(jblob, jp, role - 1, P, slice, nsl);
+    live = (jblob[jp.patterns + P] & 0xFFu) != 0;
+  }
   pdl_trigger();
   __shared__ __align__(8) uint64_t prep_bar;
-  const bool live = (jblob[jp.patterns + P] & 0xFFu) != 0;
   // the static gather plan and row index lists of this slice: precomputed once
   // (sg_joint_prep) and brought in with one TMA bulk copy, or built here
   const bool prepped = prep != nullptr && live;
@@ -1829,6 +1804,7 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
              "sg_step_tail_joint: bad joint plan");
   if (net->table_entries > 0) SG_REQUIRE(f->ptab && f->ftab, "sg_step_tail_joint: tables required");
   if (f->key_table) SG_REQUIRE(f->key_index && f->key_current && f->kps > 0, "sg_step_tail_joint: bad key cursor");
+  SG_REQUIRE(finish_check_ok(f, sp), "sg_step_tail_joint: bad observation check (aligned rows, err word)");
   FinishArgs a = make_finish_args(f, sp);
   a.early_inputs = 1;    // k_joint_sweep triggers after its own wait
   a.vprob = nullptr;     // the slices derive their conditionals from the CPTs themselves
@@ -1857,7 +1833,25 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
   // one CTA for the model update + the row slices (joint_tail_slices per pattern)
   const dim3 grid(1 + joint_tail_slice_count(*sp, *jp));
   SG_REQUIRE(!prep || (reinterpret_cast<uintptr_t>(prep) & 15) == 0, "sg_step_tail_joint: prep must be 16-byte aligned");
+  TailRoles roles{};
+  {  // the order of tail_slice_of: patterns from the last down
+    int k = 0;
+    for (int P = jp->patterns - 1; P >= 0 && k >= 0; --P) {
+      int B = 0;
+      for (int v = 0; v < sp->n; ++v)
+        if ((P >> v) & 1) B += sp->width[v];
+      const int nsl = joint_tail_slices(B);
+      for (int s = 0; s < nsl; ++s) {
+        if (k >= SG_TAIL_ROLE_MAX || P > 127 || nsl > 31) {
+          k = -1;
+          break;
+        }
+        roles.r[k++] = uint16_t(P | (s << 7) | (nsl << 11));
+      }
+    }
+    roles.count = k > 0 ? k : 0;
+  }
   launch_pdl(k_step_tail_joint, grid, dim3(FINISH_THREADS), smem, (cudaStream_t)stream, *net, a, *sp, *jp, jblob,
-             sync, static_cast<const unsigned char*>(prep), joint_prep_slice_bytes(*sp, *jp));
+             sync, static_cast<const unsigned char*>(prep), joint_prep_slice_bytes(*sp, *jp), roles);
   return check_launch("sg_step_tail_joint");
 }

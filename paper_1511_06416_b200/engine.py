@@ -272,7 +272,8 @@ class Engine:
         prev = self.prev_counts.get(mb.index) if moving else None
         key = 0 if cfg.map_estimate else derive_seed(derive_seed(cfg.seed, "cpt_update", pass_index, mb.index),
                                                      "sample_cpts")
-        f = self.finish_args(new_counts, prev, key)
+        tail_check = self.tail_checks_obs
+        f = self.finish_args(new_counts, prev, key, check=(obs.data_ptr(), ld, 8, size) if tail_check else None)
         for sw in range(S):
             sweep_seed = derive_seed(cfg.seed, "sweep", pass_index, mb.index, sw)
             last = sw == S - 1
@@ -280,7 +281,8 @@ class Engine:
             if self.use_small:
                 if sw:
                     self.sweep_fence(s)
-                self.packed_sweep(db, size, m, sweep_seed, None, counts_ptr, obs.data_ptr() if last else None, ld, s)
+                self.packed_sweep(db, size, m, sweep_seed, None, counts_ptr,
+                                  obs.data_ptr() if last and not tail_check else None, ld, s)
             elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
                 _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
@@ -302,8 +304,16 @@ class Engine:
         self.batch_bytes = max(self.batch_bytes, self.n * m * size * 4 + m * size * 8)
         self._last_batch = db
 
+    @property
+    def tail_checks_obs(self) -> bool:
+        """The joint path range-checks a visit's observation block in the step
+        tail's row slices, while their preparation lands and the model update
+        draws the gammas (off the sweep's critical path); with a count all-reduce
+        between the two the sweep keeps the check."""
+        return self.joint and self.comm is None
+
     def finish_args(self, new_counts, prev_counts, key: int, key_dev: int | None = None, clear=None,
-                    cursor=None, cpt_host: torch.Tensor | None = None):
+                    cursor=None, cpt_host: torch.Tensor | None = None, check=None):
         """``sg_finish`` of one visit: accumulate, CPT update, next visit's tables
         (``cpt_host``: pinned host tensor the kernel also stores the new CPTs in)."""
         cfg = self.cfg
@@ -326,6 +336,9 @@ class Engine:
         f.flags = _lib.SG_FINISH_PACKED_ONLY if self.use_small else 0
         f.vprob = self.vprob.data_ptr() if self.joint else None
         f.cpt_host = None if cpt_host is None else cpt_host.data_ptr()
+        if check is not None:  # (observation block pointer, row bytes, bits per case, cases)
+            f.check_obs, f.check_ld, f.check_bits, f.check_cases = check
+            f.check_err = self.err.ptr
         if cursor is not None:
             table, index, kps, current = cursor
             f.key_table, f.key_index, f.kps, f.key_current = table.data_ptr(), index.data_ptr(), kps, current.data_ptr()
@@ -710,8 +723,10 @@ class StepGraphs:
         # replay's count buffer), advance the key cursor
         # the CPT read-back rides in the tail kernel itself (zero-copy store into the pinned tensor)
         cpt_host = next((h for d_, h in self.readback if d_.data_ptr() == eng.cpt.data_ptr()), None)
+        tail_check = eng.tail_checks_obs
         f = eng.finish_args(new, prev, 0, key_dev=cur + 8 * S, clear=prev,
-                            cursor=(self.table, self.idx, self.kps, self.cur), cpt_host=cpt_host)
+                            cursor=(self.table, self.idx, self.kps, self.cur), cpt_host=cpt_host,
+                            check=(obs.data_ptr(), self.ld, self.obs_bits, size) if tail_check else None)
         self._finish_args.append(f)
         if self._tev is not None:
             _lib.call("sg_event_record", self._tev[2 * p], s)
@@ -721,7 +736,8 @@ class StepGraphs:
             if eng.use_small:
                 if sw:
                     eng.sweep_fence(s)
-                eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr, obs.data_ptr() if last else None, self.ld, s,
+                eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr,
+                                 obs.data_ptr() if last and not tail_check else None, self.ld, s,
                                  obs_bits=self.obs_bits)
             elif eng.rng_mode == _lib.SG_RNG_NUMPY:
                 # numpy stream: stream_key(sweep_seed, "var", v) hashed on the device from the
@@ -946,15 +962,17 @@ class StreamGraphs:
                   cur + 8 * (S + 1), s)
         new = self.cbuf[p]
         cpt_host = next((h for d_, h in self.readback if d_.data_ptr() == eng.cpt.data_ptr()), None)
+        tail_check = eng.tail_checks_obs
         f = eng.finish_args(new, None, 0, key_dev=cur + 8 * S, clear=self.cbuf[1 - p],
-                            cursor=(self.table, self.idx, self.kps, self.cur), cpt_host=cpt_host)
+                            cursor=(self.table, self.idx, self.kps, self.cur), cpt_host=cpt_host,
+                            check=(obs.data_ptr(), self.ld, self.obs_bits, self.size) if tail_check else None)
         self._f = getattr(self, "_f", []) + [f]
         for sw in range(S):
             last = sw == S - 1
             if sw:
                 eng.sweep_fence(s)
             eng.packed_sweep(db, self.size, m, 0, cur + 8 * sw, new.data_ptr() if last else None,
-                             obs.data_ptr() if last else None, self.ld, s, obs_bits=self.obs_bits)
+                             obs.data_ptr() if last and not tail_check else None, self.ld, s, obs_bits=self.obs_bits)
         if eng.comm is not None:
             eng.comm(new)
         eng.step_tail(f, s)
