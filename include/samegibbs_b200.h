@@ -404,7 +404,10 @@ int sg_joint_smem(const sg_small* sp, const sg_joint* jp, int32_t cells, int64_t
    instead (exact ZeroSupport semantics).  obs_bits 4 or 2: obs is a packed
    .sgb block (ld_obs bytes per row, 8 / obs_bits cases per byte, case
    k * (8 / obs_bits) + h in bits [h * obs_bits, (h + 1) * obs_bits) of byte
-   k, all-ones = missing) and is range-checked in that form; 0 or 8: int8. */
+   k, all-ones = missing) and is range-checked in that form; 0 or 8: int8.
+   obs_bits | SG_OBS_PREFETCH_ONLY: the block is only pulled into L2 (the
+   following sg_step_tail_joint range-checks it, sg_finish.check_obs). */
+#define SG_OBS_PREFETCH_ONLY 0x100
 int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint32_t* stab,
                    const uint32_t* jblob, const uint8_t* pattern, const int32_t* case_id,
                    uint8_t* lanes, int32_t lane_ld, int32_t cases, int32_t num_real,

@@ -849,7 +849,18 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
   const FastKey fk = fast_key(key_dev ? *key_dev : key);
   // the minibatch's range check while the blob is in flight (no kernel of this
   // step writes the observation block)
-  obs_range_check<NT>(sp, obs, ld_obs, cases, err, obs_nib);
+  if (obs_nib & SG_OBS_PREFETCH_ONLY) {  // the step tail checks the block: warm L2 for it
+    const int nib = obs_nib & 0xFF;
+    const int per_byte = nib ? 8 / nib : 1;
+    const int lines = ((cases + per_byte - 1) / per_byte + 127) >> 7;
+    for (int i = (blockIdx.y * gridDim.x + blockIdx.x) * NT + threadIdx.x; i < lines * sp.n;
+         i += gridDim.x * gridDim.y * NT) {
+      const int v = i / lines;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(obs + int64_t(v) * ld_obs + (int64_t(i - v * lines) << 7)));
+    }
+  } else {
+    obs_range_check<NT>(sp, obs, ld_obs, cases, err, obs_nib);
+  }
   SG_SWEEP_STAMP(2);  // prologue issued (blob copy in flight, range check done)
   __syncthreads();
   mbar_wait(bar, 0);
@@ -1291,12 +1302,10 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
                                                                     int64_t prep_bytes, const TailRoles roles) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_role;
-  // the step's observation block, range-checked by every CTA (a share each, by block
-  // index: before the role ticket) while the model update and the slices' preparation
-  // proceed -- the sweep skips its check then
-  if (f.check_obs)
-    obs_range_check_range(sp, f.check_obs, f.check_ld, f.check_cases, f.check_err, f.check_nib,
-                          int(blockIdx.x * blockDim.x + threadIdx.x), int(gridDim.x * blockDim.x));
+  // the step's observation block is range-checked by every CTA (a share each, by block
+  // index) beside the model update and the slices' preparation -- the sweep only
+  // prefetches it then (SG_OBS_PREFETCH_ONLY)
+  const int check_t = int(blockIdx.x * blockDim.x + threadIdx.x), check_n = int(gridDim.x * blockDim.x);
   if (threadIdx.x == 0) s_role = int(atomicAdd(sync + 2, 1u));
   __syncthreads();
   const int role = s_role;  // 0: the model update; r >= 1: row slice r - 1
@@ -1308,6 +1317,8 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
 #endif
   stamp(0);
   if (role == 0) {  // releases sync[0] as soon as the new CPTs are written (f.release_sync)
+    if (f.check_obs)
+      obs_range_check_range(sp, f.check_obs, f.check_ld, f.check_cases, f.check_err, f.check_nib, check_t, check_n);
     step_finish_body(gnet, f, smem, FINISH_THREADS);
     stamp(1);
     return;
@@ -1357,6 +1368,9 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   }
   for (int i = tid; i < int(gnet.blob64_words); i += blockDim.x) b64[i] = __ldg(gnet.blob64 + i);
   for (int i = tid; i < int(gnet.blob32_words); i += blockDim.x) b32[i] = __ldg(gnet.blob32 + i);
+  // this CTA's share of the observation check (its loads overlap the preparation copy)
+  if (f.check_obs)
+    obs_range_check_range(sp, f.check_obs, f.check_ld, f.check_cases, f.check_err, f.check_nib, check_t, check_n);
   __syncthreads();
   const sg_net net = rebase_net(gnet, b32, b64);
   // every CPT index of this pattern's conditionals, while the sweep / CTA 0 still run
@@ -1705,6 +1719,8 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
   using namespace sg;
   SG_REQUIRE(sp && jp && stab && jblob && pattern && case_id && lanes && err, "sg_joint_sweep: null argument");
   SG_REQUIRE((reinterpret_cast<uintptr_t>(jblob) & 15) == 0, "sg_joint_sweep: blob must be 16-byte aligned");
+  const int prefetch_only = obs_bits & SG_OBS_PREFETCH_ONLY;
+  obs_bits &= ~SG_OBS_PREFETCH_ONLY;
   SG_REQUIRE(obs_bits == 0 || obs_bits == 8 || obs_bits == 4 || obs_bits == 2,
              "sg_joint_sweep: obs_bits must be 0/8 (int8), 4 or 2");
   const int per_byte = (obs_bits == 4 || obs_bits == 2) ? 8 / obs_bits : 1;
@@ -1716,7 +1732,7 @@ extern "C" int sg_joint_sweep(const sg_small* sp, const sg_joint* jp, const uint
     for (int v = 0; v < sp->n; ++v)
       SG_REQUIRE(sp->card[v] < (1 << obs_bits), "sg_joint_sweep: %d-bit observations need cards < %d", obs_bits,
                  1 << obs_bits);
-  const int obs_nibbles = per_byte > 1 ? obs_bits : 0;
+  const int obs_nibbles = (per_byte > 1 ? obs_bits : 0) | prefetch_only;
   SG_REQUIRE(sp->n >= 1 && sp->n <= SG_SMALL_MAXV, "sg_joint_sweep: bad plan");
   SG_REQUIRE(joint_plan_ok(*sp, *jp, cells), "sg_joint_sweep: joint plan does not fit (bits %d, words %d)", sp->bits,
              jp->words);

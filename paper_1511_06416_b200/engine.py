@@ -281,8 +281,8 @@ class Engine:
             if self.use_small:
                 if sw:
                     self.sweep_fence(s)
-                self.packed_sweep(db, size, m, sweep_seed, None, counts_ptr,
-                                  obs.data_ptr() if last and not tail_check else None, ld, s)
+                self.packed_sweep(db, size, m, sweep_seed, None, counts_ptr, obs.data_ptr() if last else None, ld, s,
+                                  prefetch_only=tail_check)
             elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
                 _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
@@ -346,7 +346,7 @@ class Engine:
         return f
 
     def packed_sweep(self, db, size: int, m: int, key: int, key_dev, counts_ptr, obs_ptr, ld: int, s,
-                     obs_bits: int = 8) -> None:
+                     obs_bits: int = 8, prefetch_only: bool = False) -> None:
         """Sweep + tally of a packed-lane minibatch: per-variable draws
         (sg_small_sweep) or, with rng="joint", one draw per lane (sg_joint_sweep;
         ``obs_bits`` 4 / 2: the range-checked block is packed, ``ld`` bytes per row)."""
@@ -354,8 +354,10 @@ class Engine:
                 self.case_base, key, key_dev, self.pack.small_jcell.data_ptr(), self.pack.cells, counts_ptr,
                 self.ftab.data_ptr() + 4 * self.pack.layout.scalars["ftab_size"], obs_ptr, ld)
         if self.joint:
+            # prefetch_only: the step tail range-checks the block; the sweep only warms L2 for it
+            bits = (obs_bits if obs_bits < 8 else 0) | (_lib.SG_OBS_PREFETCH_ONLY if prefetch_only else 0)
             _lib.call("sg_joint_sweep", self.pack.small_ref, self.pack.joint_ref, self.stab.data_ptr(),
-                      self.jblob.data_ptr(), *head, obs_bits if obs_bits < 8 else 0, self.err.ptr, s)
+                      self.jblob.data_ptr(), *head, bits, self.err.ptr, s)
         else:
             if obs_bits < 8:
                 raise ValueError("packed observation blocks are range-checked by the joint sweep only")
@@ -736,9 +738,8 @@ class StepGraphs:
             if eng.use_small:
                 if sw:
                     eng.sweep_fence(s)
-                eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr,
-                                 obs.data_ptr() if last and not tail_check else None, self.ld, s,
-                                 obs_bits=self.obs_bits)
+                eng.packed_sweep(db, size, m, 0, cur + 8 * sw, counts_ptr, obs.data_ptr() if last else None, self.ld,
+                                 s, obs_bits=self.obs_bits, prefetch_only=tail_check)
             elif eng.rng_mode == _lib.SG_RNG_NUMPY:
                 # numpy stream: stream_key(sweep_seed, "var", v) hashed on the device from the
                 # cursor's sweep seed (sampler.py:245, rng.py:16-20), then the bit-exact sweep
@@ -972,7 +973,8 @@ class StreamGraphs:
             if sw:
                 eng.sweep_fence(s)
             eng.packed_sweep(db, self.size, m, 0, cur + 8 * sw, new.data_ptr() if last else None,
-                             obs.data_ptr() if last and not tail_check else None, self.ld, s, obs_bits=self.obs_bits)
+                             obs.data_ptr() if last else None, self.ld, s, obs_bits=self.obs_bits,
+                             prefetch_only=tail_check)
         if eng.comm is not None:
             eng.comm(new)
         eng.step_tail(f, s)
