@@ -603,9 +603,10 @@ class StepGraphs:
             src, _ = eng._obs_for(mb)
             bufs = []
             shape, dt = self.obs_geometry(eng.n, mb.size, self.obs_bits)
-            # host-fed graphs keep 2 + visits_per_replay: the uploads for the visits two
-            # ahead start with the current replay, into buffers the previous replay read
-            for _ in range(2 + self.vpr if host_block is not None else 2):
+            # host-fed graphs keep 3 x visits_per_replay: the uploads for the visits two
+            # replays ahead start with the current replay, into the buffers the previous
+            # replay read, so each upload has two replays' time to land
+            for _ in range(3 * self.vpr if host_block is not None else 2):
                 b = torch.empty(shape, dtype=dt, device=d)
                 if self.nibbles:
                     b.copy_(pack_bits(src[:, :mb.size], shape[1] * 8 // self.obs_bits, self.obs_bits))
@@ -774,8 +775,8 @@ class StepGraphs:
         if mb is not None and self.host_block is not None:
             raise ValueError("this graph uploads its own host block; call step() without a minibatch")
         if self.host_block is not None:
-            # upload the blocks of the visits two ahead (buffers the previous replay read)
-            # while this replay runs, so an upload has a replay's time to land
+            # upload the blocks of the visits two replays ahead (buffers the previous replay
+            # read) while this replay runs, so an upload has two replays' time to land
             nb, vpr, k0 = len(self.obs_bufs), self.vpr, self.replayed
             mine = [(k0 + i) % nb for i in range(vpr)]
             gk = (k0 // vpr) % len(self.graphs)
@@ -785,7 +786,7 @@ class StepGraphs:
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                 ev[0].record(up)
             for i in range(vpr):
-                q = (k0 + 2 + i) % nb
+                q = (k0 + 2 * vpr + i) % nb
                 if self._read_pending[q]:
                     up.wait_event(self._read_done[q])  # the replay that last read buffer q has finished
                 nxt = self.obs_bufs[q]
