@@ -117,8 +117,12 @@ __global__ void __launch_bounds__(1024) k_small_scatter(const int cases, const u
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nb = gridDim.x, me = blockIdx.x;
   for (int P = warp; P < patterns; P += blockDim.x >> 5) {
     int t = 0, pre = 0;
-    for (int b = lane; b < nb; b += 32) {
-      const int x = cnt[P * nb + b];
+    // all of a lane's loads in flight together (SMALL_PREP_BLOCKS / 32 of them), not one
+    // L2 round trip after another
+#pragma unroll
+    for (int k = 0; k < (SMALL_PREP_BLOCKS + 31) / 32; ++k) {
+      const int b = lane + 32 * k;
+      const int x = b < nb ? cnt[P * nb + b] : 0;
       t += x;
       pre += b < me ? x : 0;
     }
