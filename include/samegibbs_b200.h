@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 1
+#define SG_ABI_VERSION 2  /* 2: sg_net blanket factor tables, sg_finish read-back and range check, sg_joint_sweep prefetch flag */
 
 typedef enum sg_status {
   SG_OK = 0,

@@ -24,6 +24,7 @@ SG_ERR_ZERO_SUPPORT, SG_ERR_STATE_RANGE, SG_ERR_REJECT_OVERFLOW = 1, 2, 4
 SG_RNG_FAST, SG_RNG_NUMPY, SG_RNG_INJECTED = 0, 1, 2
 SG_ACC_MOVING, SG_ACC_EXPONENTIAL = 0, 1
 SG_FINISH_PACKED_ONLY = 1
+ABI_VERSION = 2  # include/samegibbs_b200.h SG_ABI_VERSION
 SG_OBS_PREFETCH_ONLY = 0x100  # sg_joint_sweep obs_bits flag
 TALLY_CHUNK_CELLS = 12288
 REJ_SLACK = 64
@@ -164,7 +165,7 @@ def load(path: Path | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.sg_abi_version() != 1:
+    if lib.sg_abi_version() != ABI_VERSION:
         raise DeviceError("libsamegibbs_b200 ABI version mismatch")
     if path is None:
         _lib = lib

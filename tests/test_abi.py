@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(str(_lib.LIB_PATH))
     for name in declared():
         assert hasattr(lib, name), name
-    assert lib.sg_abi_version() == 1
+    assert lib.sg_abi_version() == _lib.ABI_VERSION == 2
     out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     for name in declared():
         assert re.search(rf"\bT {name}\b", out), name
