@@ -321,19 +321,32 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
     // members are handed out dynamically (costs differ); the first BIG_W go round-robin
     for (int vi = gs + warp; vi < ge;) {
       const int v = __ldg(net.order + vi);
-      // the latent cases of v, in order, into this warp's list: lane w < fw expands mask word w
-      const uint32_t word = lane < fw ? fl[v * fw + lane] : 0u;
-      const int cnt = __popc(word);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      // the latent cases of v, in order, into this warp's list: each lane
+      // expands one 16-bit half of a mask word (one word when the tile has
+      // more than 16 words per row), ranks from a warp scan of the counts,
+      // highest bit first
+      int total;
       {
-        int pos = incl - cnt;
-        for (uint32_t b = word; b; b &= b - 1) wl[pos++] = uint16_t(lane * 32 + __ffs(b) - 1);
+        const bool half = fw <= 16;
+        uint32_t bits = 0;
+        if (half) {
+          if (lane < 2 * fw) bits = (fl[v * fw + (lane >> 1)] >> ((lane & 1) << 4)) & 0xFFFFu;
+        } else if (lane < fw) {
+          bits = fl[v * fw + lane];
+        }
+        int incl = __popc(bits);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        total = __shfl_sync(0xffffffffu, incl, 31);
+        const int base = half ? lane << 4 : lane << 5;
+        for (int pos = incl; bits; --pos) {
+          const int hi = 31 - __clz(bits);
+          wl[pos - 1] = uint16_t(base + hi);
+          bits ^= 1u << hi;
+        }
       }
       __syncwarp();
       const int32_t* dv = net.var_desc + v * SG_DESC_WORDS;
@@ -352,11 +365,14 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
         }
       }
       const int rs = a.mg * wpr;  // words between variable rows of the tile (32-bit offsets throughout)
+      int it1 = lane;             // first list entry of the single-case loop below
       if constexpr (use_bft) {
         if (nmb < 0 && mg == 1) {
           // one replica (m = 1: no Philox block to share across replicas): two cases
-          // per lane, it and it + 32 of the warp's 64-entry stride
-          for (int it = lane; it < total; it += 64) {
+          // per lane, it and it + 32 of the warp's 64-entry stride; a final
+          // remainder of <= 32 cases takes one single-case round instead
+          int& it = it1;
+          for (; total - (it - lane) > 32; it += 64) {
             const bool two = it + 32 < total;
             const int ca = wl[it], cb = wl[two ? it + 32 : it];
             const int cwa = ca / PER, sa = (ca % PER) * BITS, cwb = cb / PER, sb = (cb % PER) * BITS;
@@ -390,14 +406,9 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
               }
             }
           }
-          __syncwarp();
-          int nx = 0;
-          if (lane == 0) nx = atomicAdd(&s_next, 1);
-          vi = __shfl_sync(0xffffffffu, nx, 0);
-          continue;
         }
       }
-      for (int it = lane; it < total; it += 32) {
+      for (int it = it1; it < total; it += 32) {
         const int c = wl[it];
         const int cw = c / PER, csh = (c % PER) * BITS;
         int64_t rank = 0;
