@@ -277,30 +277,43 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
   const int cpr = tc >> 4;  // 16-case chunks per row
   if (tid == 0) s_err = 0;
 
-  // ---- stage the tile: a warp per variable row, one int4 (16 cases) per lane step
-  for (int v = warp; v < n; v += BIG_W) {
+  // ---- stage the tile: a warp per variable row, one int4 (16 cases) per lane
+  // step, the rows of SB variables loaded together (all in flight before any
+  // is unpacked)
+  auto stage = [&](int v, int r, int ch, int4 val) {
+    if (r == 0) {  // every replica carries the shared latent mask
+      uint32_t f = BITS == 2 ? flag_word16(val) : flag_bits16(val);
+      const int cc = ch * 16;
+      if (cc + 16 > ncase) f &= cc >= ncase ? 0u : ((1u << (ncase - cc)) - 1u);
+      fl16[v * cpr + ch] = uint16_t(f);
+    }
+    uint32_t* dst = st + size_t(v * a.mg + r) * wpr + ch * (16 / PER);
+    if constexpr (BITS == 2) {
+      dst[0] = crumb_word(val);
+    } else {
+      val.x &= 0x7F7F7F7F;
+      val.y &= 0x7F7F7F7F;
+      val.z &= 0x7F7F7F7F;
+      val.w &= 0x7F7F7F7F;
+      pack16<BITS>(val, dst);
+    }
+  };
+  constexpr int SB = 4;
+  for (int v0 = warp; v0 < n; v0 += SB * BIG_W) {
     for (int r = 0; r < mg; ++r) {
       for (int ch = lane; ch < cpr; ch += 32) {
-        int4 val = make_int4(0, 0, 0, 0);
-        if (ch * 16 < nload)
-          val = __ldcs(reinterpret_cast<const int4*>(bt.states + (int64_t(v) * bt.m + rg0 + r) * bt.pitch + c0 +
-                                                     ch * 16));
-        if (r == 0) {  // every replica carries the shared latent mask
-          uint32_t f = BITS == 2 ? flag_word16(val) : flag_bits16(val);
-          const int cc = ch * 16;
-          if (cc + 16 > ncase) f &= cc >= ncase ? 0u : ((1u << (ncase - cc)) - 1u);
-          fl16[v * cpr + ch] = uint16_t(f);
+        int4 val[SB];
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+          const int v = v0 + k * BIG_W;
+          val[k] = make_int4(0, 0, 0, 0);
+          if (v < n && ch * 16 < nload)
+            val[k] = __ldcs(reinterpret_cast<const int4*>(bt.states + (int64_t(v) * bt.m + rg0 + r) * bt.pitch +
+                                                          c0 + ch * 16));
         }
-        uint32_t* dst = st + size_t(v * a.mg + r) * wpr + ch * (16 / PER);
-        if constexpr (BITS == 2) {
-          dst[0] = crumb_word(val);
-        } else {
-          val.x &= 0x7F7F7F7F;
-          val.y &= 0x7F7F7F7F;
-          val.z &= 0x7F7F7F7F;
-          val.w &= 0x7F7F7F7F;
-          pack16<BITS>(val, dst);
-        }
+#pragma unroll
+        for (int k = 0; k < SB; ++k)
+          if (v0 + k * BIG_W < n) stage(v0 + k * BIG_W, r, ch, val[k]);
       }
     }
   }
