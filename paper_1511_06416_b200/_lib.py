@@ -172,6 +172,31 @@ def load(path: Path | None = None) -> ctypes.CDLL:
     return lib
 
 
+# Checked builds (-DSG_CHECKED, lib_checked.so): each translation unit with
+# device-side index / protocol assertions exports sg_debug_checked_<tu>, which
+# reports (and clears) the first failing source line of that unit.
+CHECKED_LIB_PATH = Path(__file__).resolve().parent / "lib_checked.so"
+CHECKED_UNITS = ("big", "small", "sweep")
+
+
+def checked_lines(lib: ctypes.CDLL | None = None, probe: bool = False) -> dict[str, int]:
+    """{unit: first failing SG_DCHECK line (0 = none)} of a checked build; clears
+    the words.  ``probe`` first launches a kernel whose check fails on purpose."""
+    lib = lib or load()
+    out = {}
+    for tu in CHECKED_UNITS:
+        fn = getattr(lib, f"sg_debug_checked_{tu}", None)
+        if fn is None:
+            raise DeviceError(f"{LIB_PATH} is not a checked build (no sg_debug_checked_{tu})")
+        fn.argtypes = [POINTER(ctypes.c_uint32), c_int32]
+        fn.restype = c_int32
+        line = ctypes.c_uint32(0)
+        if fn(ctypes.byref(line), int(probe)) != SG_OK:
+            raise DeviceError(f"sg_debug_checked_{tu} failed: {lib.sg_last_error().decode(errors='replace')}")
+        out[tu] = int(line.value)
+    return out
+
+
 def check(status: int, what: str) -> None:
     if status != SG_OK:
         msg = load().sg_last_error().decode(errors="replace")

@@ -119,7 +119,7 @@ __device__ __forceinline__ int bft_child(const int4*& p, Get get) {
 // comparisons are never true (u * norm <= norm).
 template <class Get>
 __device__ __forceinline__ int draw_bft(const int4* __restrict__ prog, const double* __restrict__ bft, Get get,
-                                        double u, bool& zs) {
+                                        double u, bool& zs, int64_t nrows) {
   const int4 h = __ldg(prog);  // card, npar, nchl, own row base
   const int4* p = prog + 1;
   int row = h.w;
@@ -130,6 +130,7 @@ __device__ __forceinline__ int draw_bft(const int4* __restrict__ prog, const dou
     if (r.w) row += get(r.z) * r.w;
   }
   double w[4];
+  SG_DCHECK(row >= 0 && row < nrows);
   bft_row(bft, row, w);
   int k = 0;
 #pragma unroll 1
@@ -137,6 +138,7 @@ __device__ __forceinline__ int draw_bft(const int4* __restrict__ prog, const dou
     const int i0 = bft_child(p, get);
     const int i1 = bft_child(p, get);
     double f0[4], f1[4];
+    SG_DCHECK(i0 >= 0 && i1 >= 0 && i0 < nrows && i1 < nrows);
     bft_row(bft, i0, f0);
     bft_row(bft, i1, f1);
 #pragma unroll
@@ -145,6 +147,7 @@ __device__ __forceinline__ int draw_bft(const int4* __restrict__ prog, const dou
   if (k < h.z) {
     const int i0 = bft_child(p, get);
     double f0[4];
+    SG_DCHECK(i0 >= 0 && i0 < nrows);
     bft_row(bft, i0, f0);
 #pragma unroll
     for (int t = 0; t < 4; ++t) w[t] = __dmul_rn(w[t], f0[t]);
@@ -192,7 +195,8 @@ __device__ __forceinline__ uint32_t state_bytes4(uint32_t crumbs, uint32_t flags
 // pass over v's program serves both, and both cases' factor rows are in flight
 // together.  Tile word offsets ra / rb and field shifts sa / sb locate the
 // cases; per case the arithmetic is draw_bft's.
-__device__ __forceinline__ int2 get2(const uint32_t* st, int o, int ra, int rb, int sa, int sb) {
+__device__ __forceinline__ int2 get2(const uint32_t* st, int o, int ra, int rb, int sa, int sb, int lim) {
+  SG_DCHECK(o >= 0 && ra >= 0 && rb >= 0 && o + ra < lim && o + rb < lim);
   return make_int2(int((st[o + ra] >> sa) & 3u), int((st[o + rb] >> sb) & 3u));
 }
 __device__ __forceinline__ int bft_finish(const double (&w)[4], double u, bool& zs) {
@@ -209,44 +213,46 @@ __device__ __forceinline__ int bft_finish(const double (&w)[4], double u, bool& 
 }
 __device__ __forceinline__ int2 draw_bft2(const int4* __restrict__ prog, const double* __restrict__ bft,
                                           const uint32_t* st, int rs, int ra, int rb, int sa, int sb, double ua,
-                                          double ub, bool& zs) {
+                                          double ub, bool& zs, int lim, int64_t nrows) {
   const int4 h = __ldg(prog);  // card, npar, nchl, own row base
   const int4* p = prog + 1;
   int ia = h.w, ib = h.w;
 #pragma unroll 1
   for (int j = 0; j < h.y; j += 2, ++p) {
     const int4 r = __ldg(p);
-    int2 g = get2(st, r.x * rs, ra, rb, sa, sb);
+    int2 g = get2(st, r.x * rs, ra, rb, sa, sb, lim);
     ia += g.x * r.y;
     ib += g.y * r.y;
     if (r.w) {
-      g = get2(st, r.z * rs, ra, rb, sa, sb);
+      g = get2(st, r.z * rs, ra, rb, sa, sb, lim);
       ia += g.x * r.w;
       ib += g.y * r.w;
     }
   }
   double wa[4], wb[4];
+  SG_DCHECK(ia >= 0 && ib >= 0 && ia < nrows && ib < nrows);
   bft_row(bft, ia, wa);
   bft_row(bft, ib, wb);
 #pragma unroll 1
   for (int k = 0; k < h.z; ++k) {
     const int4 c = __ldg(p++);
-    int2 g = get2(st, c.x * rs, ra, rb, sa, sb);
+    int2 g = get2(st, c.x * rs, ra, rb, sa, sb, lim);
     ia = c.y + g.x;
     ib = c.y + g.y;
 #pragma unroll 1
     for (int q = 0; q < c.z; ++q, ++p) {
       const int4 r = __ldg(p);
-      g = get2(st, r.x * rs, ra, rb, sa, sb);
+      g = get2(st, r.x * rs, ra, rb, sa, sb, lim);
       ia += g.x * r.y;
       ib += g.y * r.y;
       if (r.w) {
-        g = get2(st, r.z * rs, ra, rb, sa, sb);
+        g = get2(st, r.z * rs, ra, rb, sa, sb, lim);
         ia += g.x * r.w;
         ib += g.y * r.w;
       }
     }
     double fa[4], fb[4];
+    SG_DCHECK(ia >= 0 && ib >= 0 && ia < nrows && ib < nrows);
     bft_row(bft, ia, fa);
     bft_row(bft, ib, fb);
 #pragma unroll
@@ -268,6 +274,7 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
   const int tc = a.tc, n = net.n;
   const int rg0 = blockIdx.y * a.mg, mg = min(a.mg, bt.m - rg0);  // replicas of this tile
   const int wpr = tc / PER;                                       // state words per (variable, replica) row
+  [[maybe_unused]] const int st_words = n * a.mg * wpr;
   uint32_t* st = sm;                                              // [n][a.mg][wpr]
   uint16_t* fl16 = reinterpret_cast<uint16_t*>(sm + size_t(n) * a.mg * wpr);  // [n][tc / 16] latent bits
   const int c0 = blockIdx.x * tc;
@@ -288,6 +295,7 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
       fl16[v * cpr + ch] = uint16_t(f);
     }
     uint32_t* dst = st + size_t(v * a.mg + r) * wpr + ch * (16 / PER);
+    SG_DCHECK(v < n && r < a.mg && ch < cpr && (v * a.mg + r) * wpr + ch * (16 / PER) + (BITS == 2 ? 0 : 1) < st_words);
     if constexpr (BITS == 2) {
       dst[0] = crumb_word(val);
     } else {
@@ -357,6 +365,7 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
         const int base = half ? lane << 4 : lane << 5;
         for (int pos = incl; bits; --pos) {
           const int hi = 31 - __clz(bits);
+          SG_DCHECK(pos >= 1 && pos <= tc && base + hi < ncase);
           wl[pos - 1] = uint16_t(base + hi);
           bits ^= 1u << hi;
         }
@@ -408,7 +417,7 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
                 ua = __ldg(a.uniforms + ioff + int64_t(r) * nmiss + rka);
                 ub = __ldg(a.uniforms + ioff + int64_t(r) * nmiss + rkb);
               }
-              const int2 x = draw_bft2(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs);
+              const int2 x = draw_bft2(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs, st_words, net.bft_rows);
               uint32_t* wa = st + v * rs + l * wpr + cwa;
               const uint32_t da = ((*wa >> sa) ^ uint32_t(x.x)) & MASK;
               if (da) atomicXor(wa, da << sa);
@@ -433,7 +442,10 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
         for (int l = 0; l < mg; ++l) {
           const int r = rg0 + l;
           const int roff = l * wpr + cw;  // + u * rs selects variable u
-          auto get = [&](int u) { return int((st[u * rs + roff] >> csh) & MASK); };
+          auto get = [&](int u) {
+            SG_DCHECK(u >= 0 && u < n && u * rs + roff < st_words);
+            return int((st[u * rs + roff] >> csh) & MASK);
+          };
           double u01;
           uint32_t u31 = 0;
           if (MODE == SG_RNG_FAST) {
@@ -463,7 +475,7 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
               for (int q = 0; q < card - 1; ++q) x += au > __ldg(p + q);
             }
           } else if constexpr (use_bft) {
-            x = draw_bft(prog, net.bft, get, u01, zs);
+            x = draw_bft(prog, net.bft, get, u01, zs, net.bft_rows);
           } else {
             x = draw_factored<4>(fd, a.cpt, get, u01, zs);
           }
@@ -558,3 +570,5 @@ bool sweep_big(const sg_net& net, const sg_batch& bt, const SweepArgs& a0, int r
 }
 
 }  // namespace sg
+
+SG_CHECKED_EXPORT(big)

@@ -586,6 +586,37 @@ void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 }  // namespace sg
 
+// ---------------------------------------------------------------- checked builds
+// -DSG_CHECKED (lib_checked.so; compute-sanitizer is closed on this GPU pool):
+// SG_DCHECK(cond) asserts an index or protocol invariant on the device and
+// records the first failing source line of its translation unit in a device
+// word, which sg_debug_checked_<tu>() reads and clears (SG_CHECKED_EXPORT).
+// Spin-waits take a bound (SG_SPIN_BOUNDED) and record a failure instead of
+// hanging.  In normal builds every check compiles to nothing.
+#ifdef SG_CHECKED
+static __device__ unsigned int sg_checked_line;
+#define SG_DCHECK(cond)                                                          \
+  do {                                                                           \
+    if (!(cond)) atomicCAS(&::sg_checked_line, 0u, static_cast<unsigned>(__LINE__)); \
+  } while (0)
+#define SG_CHECKED_EXPORT(tu)                                                        \
+  __global__ void sg_checked_probe_##tu() { SG_DCHECK(threadIdx.x != 0); }         \
+  extern "C" int sg_debug_checked_##tu(unsigned* line, int probe) {                 \
+    if (probe) sg_checked_probe_##tu<<<1, 32>>>();                                  \
+    unsigned zero = 0;                                                              \
+    if (cudaDeviceSynchronize() != cudaSuccess ||                                   \
+        cudaMemcpyFromSymbol(line, ::sg_checked_line, sizeof(unsigned)) != cudaSuccess || \
+        cudaMemcpyToSymbol(::sg_checked_line, &zero, sizeof(unsigned)) != cudaSuccess)    \
+      return ::sg::check_launch("sg_debug_checked_" #tu);                           \
+    return SG_OK;                                                                   \
+  }
+#else
+#define SG_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#define SG_CHECKED_EXPORT(tu)
+#endif
+
 #define SG_REQUIRE(cond, ...)        \
   do {                               \
     if (!(cond)) {                   \

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(1024) k_small_scatter(const int cases, const u
     first = __shfl_sync(0xffffffffu, first, leader);
     if (!valid) continue;
     const int s = first + __popc(peers & lanemask_lt());
+    SG_DCHECK(P < uint32_t(patterns) && s >= 0 && s < cases);
     pattern[s] = uint8_t(P);
     case_id[s] = c;
   }
@@ -296,6 +297,7 @@ __device__ __forceinline__ int joint_first_slot() {
 // must not count (past m, alias quads, padding cases) carry state 64 in
 // their tally byte, so the update needs no branch.
 __device__ __forceinline__ void joint_count(uint32_t base, uint32_t state) {
+  SG_DCHECK(state < 65u);  // kJointBins
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + state * 4u) : "memory");
 }
 static constexpr int kJointBins = 65;
@@ -639,8 +641,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // mass, else take its alias.  One LDS of the entry, one of the column's
 // latent field bits (dep): two dependent shared loads per lane.
 template <int B>
-__device__ __forceinline__ uint32_t joint_alias_col(uint32_t row, uint32_t u) {
+__device__ __forceinline__ uint32_t joint_alias_col(uint32_t row, uint32_t u, uint32_t lim) {
   const uint32_t i = u >> (32 - B);
+  SG_DCHECK(row + (i << 2) + 4 <= lim);
   uint32_t e;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(row + (i << 2)));
   const uint32_t f = u << B;                 // the low 32 - B bits, left-aligned
@@ -655,7 +658,7 @@ __device__ __forceinline__ uint32_t joint_alias_col(uint32_t row, uint32_t u) {
 // never stored or tallied.  row0 / dep0: shared-window addresses.
 template <int B, int QG, int NL>
 __device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[QG], uint32_t row0, uint32_t dep0,
-                                            uint32_t keep) {
+                                            uint32_t keep, uint32_t lim) {
   constexpr uint32_t kRowBytes = ((1u << B) + 1u) * 4u;  // rows 2^B + 1 words apart (odd: lanes drawing
                                                         // the same column of different rows use different banks)
 #pragma unroll
@@ -669,9 +672,10 @@ __device__ __forceinline__ void joint_quads(uint32_t (&w)[QG], const u32x4 (&r)[
 #ifdef SG_EXP_NOSEARCH  // timing experiment only: the column straight from the uniform (wrong results)
       const uint32_t col = u[j] >> (32 - B);
 #else
-      const uint32_t col = joint_alias_col<B>(row0 + S * kRowBytes, u[j]);
+      const uint32_t col = joint_alias_col<B>(row0 + S * kRowBytes, u[j], lim);
 #endif
       uint32_t lat;
+      SG_DCHECK(col < (1u << B) && dep0 + (col << 2) + 4 <= lim);
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lat) : "r"(dep0 + (col << 2)));
       xs[j] = (S & keep) | lat;
     }
@@ -686,7 +690,7 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
                                             const uint8_t* __restrict__ pattern, const int32_t* __restrict__ case_id,
                                             uint32_t hist_a, int cases, int num_real,
                                             int64_t case_base, const FastKey& fk, bool counts,
-                                            const uint32_t (&nw0)[QG], uint32_t nP0, int nc0) {
+                                            const uint32_t (&nw0)[QG], uint32_t nP0, int nc0, uint32_t blob_bytes) {
   const uint32_t* info = reinterpret_cast<const uint32_t*>(blob);
   const int stride = gridDim.x * NT;
   int s = joint_first_slot();
@@ -719,6 +723,7 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
       nP = pattern[usn];
       nc = case_id[usn];
     }
+    SG_DCHECK(P < uint32_t(np) && uint32_t(s) < qs.ld);
     const uint32_t meta = info[np + P];
     const int B = int(meta & 0xFFu);
     if (B) {  // warp-uniform: slots are bucketed by pattern
@@ -736,13 +741,14 @@ __device__ __forceinline__ void joint_units(const QuadSet& qs, const unsigned ch
       const uint32_t row0 = smem_u32(blob) + info[P];
       const uint32_t dep0 = smem_u32(blob) + (meta >> 16);
       const uint32_t keep = (meta >> 8) & 0xFFu;
+      [[maybe_unused]] const uint32_t lim = smem_u32(blob) + blob_bytes;
       switch (B) {
-        case 1: joint_quads<1, QG, NL>(w, r, row0, dep0, keep); break;
-        case 2: joint_quads<2, QG, NL>(w, r, row0, dep0, keep); break;
-        case 3: joint_quads<3, QG, NL>(w, r, row0, dep0, keep); break;
-        case 4: joint_quads<4, QG, NL>(w, r, row0, dep0, keep); break;
-        case 5: joint_quads<5, QG, NL>(w, r, row0, dep0, keep); break;
-        default: joint_quads<6, QG, NL>(w, r, row0, dep0, keep); break;
+        case 1: joint_quads<1, QG, NL>(w, r, row0, dep0, keep, lim); break;
+        case 2: joint_quads<2, QG, NL>(w, r, row0, dep0, keep, lim); break;
+        case 3: joint_quads<3, QG, NL>(w, r, row0, dep0, keep, lim); break;
+        case 4: joint_quads<4, QG, NL>(w, r, row0, dep0, keep, lim); break;
+        case 5: joint_quads<5, QG, NL>(w, r, row0, dep0, keep, lim); break;
+        default: joint_quads<6, QG, NL>(w, r, row0, dep0, keep, lim); break;
       }
     }
     const bool real_case = c < num_real;
@@ -875,10 +881,10 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
                                                         num_real, case_base, fk, counts != nullptr, nw0, nP0, nc0);
   } else if (NL < 4 && last == QG - 1 && q0 + QG == Q) {  // this row holds the partial final quad
     joint_units<QG, NT, NL>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
-                            counts != nullptr, nw0, nP0, nc0);
+                            counts != nullptr, nw0, nP0, nc0, jbytes);
   } else {
     joint_units<QG, NT, 4>(qs, blob, jp.patterns, lanes, pattern, case_id, hist_a, cases, num_real, case_base, fk,
-                           counts != nullptr, nw0, nP0, nc0);
+                           counts != nullptr, nw0, nP0, nc0, jbytes);
   }
   // per-warp bins -> CPT cells (jcell) -> one global atomic per touched cell
   small_epilogue<SG_SMALL_MAXV, NT>(sp, zs, hist8, cellacc, jcell, cells, nullptr, nullptr, 0, cases, err);
@@ -1313,6 +1319,7 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   if (threadIdx.x == 0) s_role = int(atomicAdd(sync + 2, 1u));
   __syncthreads();
   const int role = s_role;  // 0: the model update; r >= 1: row slice r - 1
+  SG_DCHECK(role >= 0 && role < int(gridDim.x));
 #ifdef SG_FINISH_TRACE
   if (threadIdx.x == 0) g_tail_trace_role[blockIdx.x] = role;
   auto stamp = [](int k) { tail_stamp(k); };
@@ -1387,10 +1394,21 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   pdl_wait();  // the sweep has finished reading the blob rows this grid overwrites
   if (tid == 0) {
     uint32_t r = 0;
+#ifdef SG_CHECKED
+    for (long long spin = 0;; ++spin) {  // bounded: a lost release is recorded, not a hang
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(sync) : "memory");
+      if (r) break;
+      if (spin > (1ll << 27)) {
+        SG_DCHECK(false);
+        break;
+      }
+    }
+#else
     for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(sync) : "memory");
       if (r) break;
     }
+#endif
   }
   __syncthreads();
   stamp(1);
@@ -1875,3 +1893,5 @@ extern "C" int sg_step_tail_joint(const sg_net* net, const sg_small* sp, const s
              sync, static_cast<const unsigned char*>(prep), joint_prep_slice_bytes(*sp, *jp), roles);
   return check_launch("sg_step_tail_joint");
 }
+
+SG_CHECKED_EXPORT(small)

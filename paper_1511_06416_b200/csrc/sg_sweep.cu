@@ -447,6 +447,7 @@ k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
               cfg += int(lane_row[__ldg(net.par_var + p) * mtc + c]) * __ldg(net.par_stride + p);
             const int64_t cell =
                 __ldg(net.cpt_off + v) + int64_t(cfg) * __ldg(net.card + v) + lane_row[v * mtc + c];
+            SG_DCHECK(cell >= __ldg(net.cpt_off + v) && cell < (v + 1 < n ? __ldg(net.cpt_off + v + 1) : net.cells));
             hist8[cell * SG_THREADS + slot] += 1;
           }
         }
@@ -511,6 +512,7 @@ k_tally(const sg_net net, const sg_batch bt, unsigned long long* counts,
       for (int p = __ldg(net.par_start + v), pe = __ldg(net.par_start + v + 1); p < pe; ++p)
         cfg += int64_t(base[__ldg(net.par_var + p) * vstride] & 0x7F) * __ldg(net.par_stride + p);
       const int64_t cell = __ldg(net.cpt_off + v) + cfg * __ldg(net.card + v) + (base[v * vstride] & 0x7F);
+      SG_DCHECK(cell >= __ldg(net.cpt_off + v) && cell < (v + 1 < net.n ? __ldg(net.cpt_off + v + 1) : net.cells));
       if (weights) atomicAdd(wcounts + cell, wt);
       else atomicAdd(counts + cell, 1ull);
     }
@@ -1083,3 +1085,5 @@ extern "C" int sg_tally_weighted(const sg_net* net, const sg_batch* batch, const
   k_tally<<<blocks, SG_THREADS, 0, (cudaStream_t)stream>>>(*net, *batch, nullptr, weights, counts);
   return check_launch("sg_tally_weighted");
 }
+
+SG_CHECKED_EXPORT(sweep)

@@ -1,3 +1,4 @@
+import os
 import sys
 from pathlib import Path
 
@@ -19,3 +20,15 @@ def koller():
     from paper_1511_06416_b200.io import bundled_network_path, load_network_file
 
     return load_network_file(bundled_network_path("koller"))
+
+
+@pytest.fixture(autouse=True)
+def _checked_build_asserts():
+    """Under SG_CHECKED_RUN=1 (tests/test_gpu_checked.py runs the parity suites
+    against lib_checked.so): after every test, no device-side SG_DCHECK failed."""
+    yield
+    if os.environ.get("SG_CHECKED_RUN") == "1":
+        from paper_1511_06416_b200 import _lib
+
+        hits = {tu: line for tu, line in _lib.checked_lines().items() if line}
+        assert not hits, f"device-side SG_DCHECK failed (translation unit: source line): {hits}"
