@@ -45,16 +45,16 @@ for k in range(12):
         torch.cuda.synchronize()
     sw = (ctypes.c_ulonglong * 1280)()
     lib.sg_debug_sweep_trace(ctypes.cast(sw, ctypes.c_void_p))
-    tt = (ctypes.c_ulonglong * (8 * 160 + 160))()
+    tt = (ctypes.c_ulonglong * (16 * 160 + 160))()
     lib.sg_debug_tail_trace(ctypes.cast(tt, ctypes.c_void_p))
     ft = (ctypes.c_ulonglong * 12)()
     lib.sg_debug_tail_finish_trace(ctypes.cast(ft, ctypes.c_void_p))
     nsw = 147
     t0 = min(sw[8 * b] for b in range(nsw))
-    roles = [int(tt[8 * 160 + b]) for b in range(129)]
+    roles = [int(tt[16 * 160 + b]) for b in range(129)]
     c0 = roles.index(0)
     sl = [b for b in range(129) if roles[b] >= 1]
-    T = lambda b, k: tt[8 * b + k]  # noqa: E731
+    T = lambda b, k: tt[16 * b + k]  # noqa: E731
     r = {
         "sweep first start": 0,
         "sweep last start": max(sw[8 * b] for b in range(nsw)) - t0,
@@ -73,7 +73,11 @@ for k in range(12):
         "tail: tables": ft[4] - t0,
         "tail: clear+keys": ft[6] - t0,
         "tail CTA0 end": T(c0, 1) - t0,
+        "slices entry (median)": statistics.median(T(b, 10) for b in sl) - t0,
+        "slices ticket (median)": statistics.median(T(b, 0) for b in sl) - t0,
         "slices last start": max(T(b, 0) for b in sl) - t0,
+        "slices blobs staged + share checked (median)": statistics.median(T(b, 8) for b in sl) - t0,
+        "slices part 1 done (median)": statistics.median(T(b, 9) for b in sl) - t0,
         "slices prep done (median)": statistics.median(T(b, 7) for b in sl) - t0,
         "slices prep done (last)": max(T(b, 7) for b in sl) - t0,
         "slices flag seen (median)": statistics.median(T(b, 1) for b in sl) - t0,
