@@ -906,13 +906,13 @@ k_joint_sweep(const sg_small sp, const SmallOrd o, const sg_joint jp, const uint
 
 // Trace stamps of the step tail's CTAs (debug builds, -DSG_FINISH_TRACE).
 #ifdef SG_FINISH_TRACE
-__device__ unsigned long long g_tail_trace[8 * 160];
+__device__ unsigned long long g_tail_trace[16 * 160];
 __device__ int g_tail_trace_role[160];
 __device__ __forceinline__ void tail_stamp(int k) {
   if (threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_tail_trace[blockIdx.x * 8 + k] = t;
+    g_tail_trace[blockIdx.x * 16 + k] = t;
   }
 }
 #else
@@ -1288,7 +1288,7 @@ extern "C" int sg_debug_tail_trace(unsigned long long* out) {
   if (cudaMemcpyFromSymbol(out, g_tail_trace, sizeof(g_tail_trace)) != cudaSuccess) return 2;
   int roles[160];
   if (cudaMemcpyFromSymbol(roles, g_tail_trace_role, sizeof(roles)) != cudaSuccess) return 2;
-  for (int i = 0; i < 160; ++i) out[8 * 160 + i] = (unsigned long long)roles[i];
+  for (int i = 0; i < 160; ++i) out[16 * 160 + i] = (unsigned long long)roles[i];
   return 0;
 }
 extern "C" int sg_debug_tail_finish_trace(unsigned long long* out) {  // this TU's copy of g_finish_trace
@@ -1316,6 +1316,9 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   // index) beside the model update and the slices' preparation -- the sweep only
   // prefetches it then (SG_OBS_PREFETCH_ONLY)
   const int check_t = int(blockIdx.x * blockDim.x + threadIdx.x), check_n = int(gridDim.x * blockDim.x);
+#ifdef SG_FINISH_TRACE
+  tail_stamp(10);  // entry, before the role ticket
+#endif
   if (threadIdx.x == 0) s_role = int(atomicAdd(sync + 2, 1u));
   __syncthreads();
   const int role = s_role;  // 0: the model update; r >= 1: row slice r - 1
@@ -1383,11 +1386,13 @@ __global__ void __launch_bounds__(FINISH_THREADS) k_step_tail_joint(const sg_net
   if (f.check_obs)
     obs_range_check_range(sp, f.check_obs, f.check_ld, f.check_cases, f.check_err, f.check_nib, check_t, check_n);
   __syncthreads();
+  stamp(8);  // blobs staged, share checked
   const sg_net net = rebase_net(gnet, b32, b64);
   // every CPT index of this pattern's conditionals, while the sweep / CTA 0 still run
   if (live) {
     if (!prepped) joint_cond_plan(net, sp, P, plan, plan_nf);
     joint_slice(net, sp, jp, nullptr, nullptr, jblob, P, slice, work, false, true, 1, prepped ? nullptr : pidx, nsl);
+    stamp(9);  // slice part 1 done
     if (prepped) mbar_wait(&prep_bar, 0);
   }
   stamp(7);
