@@ -87,15 +87,43 @@ __global__ void __launch_bounds__(256) k_build_bft(const sg_net net, const doubl
   }
 }
 
-__device__ __forceinline__ void bft_row(const double* __restrict__ bft, int row, double (&f)[4]) {
+// K = 4: the whole 32-byte row; K = 2 (binary variables): its first 16
+// bytes only -- entries 2 and 3 are the row's zero padding.
+template <int K = 4>
+__device__ __forceinline__ void bft_row(const double* __restrict__ bft, int row, double (&f)[K]) {
   const double2* p = reinterpret_cast<const double2*>(bft) + 2 * row;
-  const double2 a = __ldg(p), b = __ldg(p + 1);
+  const double2 a = __ldg(p);
   f[0] = a.x;
   f[1] = a.y;
-  f[2] = b.x;
-  f[3] = b.y;
+  if constexpr (K == 4) {
+    const double2 b = __ldg(p + 1);
+    f[2] = b.x;
+    f[3] = b.y;
+  }
 }
 
+// K = 2: the padded entries are exact zeros, so norm = w0 + w1 exactly and
+// the comparisons at w0 + w1 (+ 0) can never hold (u * norm <= norm): the one
+// comparison at w0 is the whole draw, bit-identical to K = 4.
+template <int K = 4>
+__device__ __forceinline__ int bft_finish(const double (&w)[K], double u, bool& zs) {
+  if constexpr (K == 2) {
+    const double norm = __dadd_rn(w[0], w[1]);
+    if (!(norm > 0.0)) zs = true;
+    return __dmul_rn(u, norm) > w[0];
+  } else {
+    const double norm = __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1]), w[2]), w[3]);
+    if (!(norm > 0.0)) zs = true;
+    const double au = __dmul_rn(u, norm);
+    double cum = w[0];
+    int x = au > cum;
+    cum = __dadd_rn(cum, w[1]);
+    x += au > cum;
+    cum = __dadd_rn(cum, w[2]);
+    x += au > cum;
+    return x;
+  }
+}
 // Row index of one child factor: base + x_c + sum x_u * stride over the
 // child's other parents (records of two; an unused half has stride 0).
 template <class Get>
@@ -117,7 +145,7 @@ __device__ __forceinline__ int bft_child(const int4*& p, Get get) {
 // cumulative comparisons.  Zero padding leaves every result bit-identical to
 // draw_factored for cards 2..4: padded weights add exact zeros and their
 // comparisons are never true (u * norm <= norm).
-template <class Get>
+template <int K, class Get>
 __device__ __forceinline__ int draw_bft(const int4* __restrict__ prog, const double* __restrict__ bft, Get get,
                                         double u, bool& zs, int64_t nrows) {
   const int4 h = __ldg(prog);  // card, npar, nchl, own row base
@@ -129,39 +157,30 @@ __device__ __forceinline__ int draw_bft(const int4* __restrict__ prog, const dou
     row += get(r.x) * r.y;
     if (r.w) row += get(r.z) * r.w;
   }
-  double w[4];
+  double w[K];
   SG_DCHECK(row >= 0 && row < nrows);
-  bft_row(bft, row, w);
+  bft_row<K>(bft, row, w);
   int k = 0;
 #pragma unroll 1
   for (; k + 1 < h.z; k += 2) {  // two children per step: both gathers in flight
     const int i0 = bft_child(p, get);
     const int i1 = bft_child(p, get);
-    double f0[4], f1[4];
+    double f0[K], f1[K];
     SG_DCHECK(i0 >= 0 && i1 >= 0 && i0 < nrows && i1 < nrows);
-    bft_row(bft, i0, f0);
-    bft_row(bft, i1, f1);
+    bft_row<K>(bft, i0, f0);
+    bft_row<K>(bft, i1, f1);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) w[t] = __dmul_rn(__dmul_rn(w[t], f0[t]), f1[t]);
+    for (int t = 0; t < K; ++t) w[t] = __dmul_rn(__dmul_rn(w[t], f0[t]), f1[t]);
   }
   if (k < h.z) {
     const int i0 = bft_child(p, get);
-    double f0[4];
+    double f0[K];
     SG_DCHECK(i0 >= 0 && i0 < nrows);
-    bft_row(bft, i0, f0);
+    bft_row<K>(bft, i0, f0);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) w[t] = __dmul_rn(w[t], f0[t]);
+    for (int t = 0; t < K; ++t) w[t] = __dmul_rn(w[t], f0[t]);
   }
-  const double norm = __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1]), w[2]), w[3]);
-  if (!(norm > 0.0)) zs = true;
-  const double au = __dmul_rn(u, norm);
-  double cum = w[0];
-  int x = au > cum;
-  cum = __dadd_rn(cum, w[1]);
-  x += au > cum;
-  cum = __dadd_rn(cum, w[2]);
-  x += au > cum;
-  return x;
+  return bft_finish<K>(w, u, zs);
 }
 
 // 2-bit tiles: whole-word bit tricks instead of per-case shifts.  A product
@@ -199,18 +218,7 @@ __device__ __forceinline__ int2 get2(const uint32_t* st, int o, int ra, int rb, 
   SG_DCHECK(o >= 0 && ra >= 0 && rb >= 0 && o + ra < lim && o + rb < lim);
   return make_int2(int((st[o + ra] >> sa) & 3u), int((st[o + rb] >> sb) & 3u));
 }
-__device__ __forceinline__ int bft_finish(const double (&w)[4], double u, bool& zs) {
-  const double norm = __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1]), w[2]), w[3]);
-  if (!(norm > 0.0)) zs = true;
-  const double au = __dmul_rn(u, norm);
-  double cum = w[0];
-  int x = au > cum;
-  cum = __dadd_rn(cum, w[1]);
-  x += au > cum;
-  cum = __dadd_rn(cum, w[2]);
-  x += au > cum;
-  return x;
-}
+template <int K>
 __device__ __forceinline__ int2 draw_bft2(const int4* __restrict__ prog, const double* __restrict__ bft,
                                           const uint32_t* st, int rs, int ra, int rb, int sa, int sb, double ua,
                                           double ub, bool& zs, int lim, int64_t nrows) {
@@ -229,10 +237,10 @@ __device__ __forceinline__ int2 draw_bft2(const int4* __restrict__ prog, const d
       ib += g.y * r.w;
     }
   }
-  double wa[4], wb[4];
+  double wa[K], wb[K];
   SG_DCHECK(ia >= 0 && ib >= 0 && ia < nrows && ib < nrows);
-  bft_row(bft, ia, wa);
-  bft_row(bft, ib, wb);
+  bft_row<K>(bft, ia, wa);
+  bft_row<K>(bft, ib, wb);
 #pragma unroll 1
   for (int k = 0; k < h.z; ++k) {
     const int4 c = __ldg(p++);
@@ -251,17 +259,17 @@ __device__ __forceinline__ int2 draw_bft2(const int4* __restrict__ prog, const d
         ib += g.y * r.w;
       }
     }
-    double fa[4], fb[4];
+    double fa[K], fb[K];
     SG_DCHECK(ia >= 0 && ib >= 0 && ia < nrows && ib < nrows);
-    bft_row(bft, ia, fa);
-    bft_row(bft, ib, fb);
+    bft_row<K>(bft, ia, fa);
+    bft_row<K>(bft, ib, fb);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < K; ++t) {
       wa[t] = __dmul_rn(wa[t], fa[t]);
       wb[t] = __dmul_rn(wb[t], fb[t]);
     }
   }
-  return make_int2(bft_finish(wa, ua, zs), bft_finish(wb, ub, zs));
+  return make_int2(bft_finish<K>(wa, ua, zs), bft_finish<K>(wb, ub, zs));
 }
 
 template <int MODE, int BITS>
@@ -417,7 +425,12 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
                 ua = __ldg(a.uniforms + ioff + int64_t(r) * nmiss + rka);
                 ub = __ldg(a.uniforms + ioff + int64_t(r) * nmiss + rkb);
               }
-              const int2 x = draw_bft2(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs, st_words, net.bft_rows);
+              const int2 x =
+                  card == 2
+                      ? draw_bft2<2>(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs, st_words,
+                                     net.bft_rows)
+                      : draw_bft2<4>(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs, st_words,
+                                     net.bft_rows);
               uint32_t* wa = st + v * rs + l * wpr + cwa;
               const uint32_t da = ((*wa >> sa) ^ uint32_t(x.x)) & MASK;
               if (da) atomicXor(wa, da << sa);
@@ -475,7 +488,8 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
               for (int q = 0; q < card - 1; ++q) x += au > __ldg(p + q);
             }
           } else if constexpr (use_bft) {
-            x = draw_bft(prog, net.bft, get, u01, zs, net.bft_rows);
+            x = card == 2 ? draw_bft<2>(prog, net.bft, get, u01, zs, net.bft_rows)
+                          : draw_bft<4>(prog, net.bft, get, u01, zs, net.bft_rows);
           } else {
             x = draw_factored<4>(fd, a.cpt, get, u01, zs);
           }
