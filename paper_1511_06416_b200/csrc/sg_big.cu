@@ -87,15 +87,17 @@ __global__ void __launch_bounds__(256) k_build_bft(const sg_net net, const doubl
   }
 }
 
-// K = 4: the whole 32-byte row; K = 2 (binary variables): its first 16
-// bytes only -- entries 2 and 3 are the row's zero padding.
+// K = 4: the whole 32-byte row; K = 2 / 3 (variables of 2 / 3 states): its
+// first 16 / 24 bytes only -- the rest is the row's zero padding.
 template <int K = 4>
 __device__ __forceinline__ void bft_row(const double* __restrict__ bft, int row, double (&f)[K]) {
   const double2* p = reinterpret_cast<const double2*>(bft) + 2 * row;
   const double2 a = __ldg(p);
   f[0] = a.x;
   f[1] = a.y;
-  if constexpr (K == 4) {
+  if constexpr (K == 3) {
+    f[2] = __ldg(reinterpret_cast<const double*>(p + 1));
+  } else if constexpr (K == 4) {
     const double2 b = __ldg(p + 1);
     f[2] = b.x;
     f[3] = b.y;
@@ -111,6 +113,11 @@ __device__ __forceinline__ int bft_finish(const double (&w)[K], double u, bool& 
     const double norm = __dadd_rn(w[0], w[1]);
     if (!(norm > 0.0)) zs = true;
     return __dmul_rn(u, norm) > w[0];
+  } else if constexpr (K == 3) {  // likewise: norm = (w0 + w1) + w2 exactly, no comparison at it
+    const double norm = __dadd_rn(__dadd_rn(w[0], w[1]), w[2]);
+    if (!(norm > 0.0)) zs = true;
+    const double au = __dmul_rn(u, norm);
+    return int(au > w[0]) + int(au > __dadd_rn(w[0], w[1]));
   } else {
     const double norm = __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1]), w[2]), w[3]);
     if (!(norm > 0.0)) zs = true;
@@ -429,6 +436,9 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
                   card == 2
                       ? draw_bft2<2>(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs, st_words,
                                      net.bft_rows)
+                  : card == 3
+                      ? draw_bft2<3>(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs, st_words,
+                                     net.bft_rows)
                       : draw_bft2<4>(prog, net.bft, st, rs, l * wpr + cwa, l * wpr + cwb, sa, sb, ua, ub, zs, st_words,
                                      net.bft_rows);
               uint32_t* wa = st + v * rs + l * wpr + cwa;
@@ -488,8 +498,9 @@ __global__ void __launch_bounds__(BIG_T, SG_BIG_MINB) k_sweep_big(const sg_net n
               for (int q = 0; q < card - 1; ++q) x += au > __ldg(p + q);
             }
           } else if constexpr (use_bft) {
-            x = card == 2 ? draw_bft<2>(prog, net.bft, get, u01, zs, net.bft_rows)
-                          : draw_bft<4>(prog, net.bft, get, u01, zs, net.bft_rows);
+            x = card == 2   ? draw_bft<2>(prog, net.bft, get, u01, zs, net.bft_rows)
+                : card == 3 ? draw_bft<3>(prog, net.bft, get, u01, zs, net.bft_rows)
+                            : draw_bft<4>(prog, net.bft, get, u01, zs, net.bft_rows);
           } else {
             x = draw_factored<4>(fd, a.cpt, get, u01, zs);
           }
