@@ -624,7 +624,8 @@ def our_arm(args, wl: Workload) -> None:
             "launch_mode": "cuda-graph replay per step" if graphs is not None else "eager",
             "kernel_path": ("packed-lane sg_joint_sweep + merged step tail (sg_step_tail_joint)" if eng.joint else
                             "packed-lane sg_small_sweep + sg_step_finish" if eng.use_small else
-                            "generic sg_sweep + sg_step_finish"),
+                            "device site keys + sg_np_uniforms + generic sg_sweep (injected) + sg_step_finish"
+                            if eng.rng_mode == _lib.SG_RNG_NUMPY else "generic sg_sweep + sg_step_finish"),
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -258,6 +258,16 @@ int sg_sweep(const sg_net* net, const sg_batch* batch, const double* cpt,
              const double* uniforms, const int64_t* inj_off, uint64_t* counts,
              int32_t* err, void* stream);
 
+/* The numpy-stream uniforms of one sweep, generated ahead of it so the
+   numpy-parity sweep runs as sg_sweep(SG_RNG_INJECTED, uniforms = out,
+   inj_off[v] = v * ld): out[v * ld + i] = random() word i of variable v's
+   stream (Philox4x64-10 under keys[2v], keys[2v + 1]; rng.py:16-25,
+   sampler.py:245) for i < m * nmiss[v].  Bit-identical to SG_RNG_NUMPY;
+   one Philox block per four uniforms instead of one per uniform.
+   ld % 4 == 0, ld >= m * cases; out 32-byte aligned, n * ld doubles. */
+int sg_np_uniforms(const sg_batch* batch, const uint64_t* keys, int32_t n, double* out, int64_t ld,
+                   void* stream);
+
 /* Count tally alone (tally_counts model.py:148-165) over lanes c < num_real. */
 int sg_tally(const sg_net* net, const sg_batch* batch, uint64_t* counts,
              void* stream);

@@ -138,6 +138,7 @@ _SIGNATURES = {
     "sg_event_destroy": ([c_uint64], c_int32),
     "sg_noop": ([c_int32, c_int32, c_int32, c_void_p], c_int32),
     "sg_flush_l2": ([c_void_p, c_void_p, c_int64, ctypes.c_uint32, c_void_p], c_int32),
+    "sg_np_uniforms": ([POINTER(SgBatch), c_void_p, c_int32, c_void_p, c_int64, c_void_p], c_int32),
     "sg_step_finish": ([POINTER(SgNet), c_void_p, POINTER(SgFinish), c_void_p], c_int32),
     "sg_unpack_nibbles": ([c_void_p, c_int64, c_void_p, c_int64, c_int32, c_int64, c_void_p], c_int32),
     "sg_unpack_crumbs": ([c_void_p, c_int64, c_void_p, c_int64, c_int32, c_int64, c_void_p], c_int32),
@@ -176,7 +177,7 @@ def load(path: Path | None = None) -> ctypes.CDLL:
 # device-side index / protocol assertions exports sg_debug_checked_<tu>, which
 # reports (and clears) the first failing source line of that unit.
 CHECKED_LIB_PATH = Path(__file__).resolve().parent / "lib_checked.so"
-CHECKED_UNITS = ("big", "small", "sweep")
+CHECKED_UNITS = ("aux", "big", "small", "sweep")
 
 
 def checked_lines(lib: ctypes.CDLL | None = None, probe: bool = False) -> dict[str, int]:
@@ -207,7 +208,7 @@ def check(status: int, what: str) -> None:
 KERNELS_PER_CALL = {
     "sg_build_tables": 1, "sg_rank_latent": 3, "sg_init_states": 1, "sg_sweep": 1, "sg_tally": 1,
     "sg_tally_weighted": 1, "sg_accumulate": 1, "sg_accumulate_f64": 1, "sg_mean_cpts": 1,
-    "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1,
+    "sg_sample_cpts": 1, "sg_forward_sample": 1, "sg_check_range": 1, "sg_np_uniforms": 1,
     "sg_small_tables": 1, "sg_small_prepare": 3, "sg_small_sweep": 1, "sg_small_import": 1, "sg_small_export": 1,
     "sg_joint_tables": 1, "sg_joint_sweep": 1, "sg_step_tail_joint": 1, "sg_joint_prep": 1, "sg_copy_small": 1, "sg_noop": 1,
     "sg_keys_advance": 1, "sg_copy2d_async": 1, "sg_step_finish": 1, "sg_site_keys": 1, "sg_predict_tally": 1, "sg_unpack_nibbles": 1, "sg_unpack_crumbs": 1,

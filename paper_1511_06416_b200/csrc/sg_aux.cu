@@ -144,6 +144,53 @@ extern "C" int sg_site_keys(const uint64_t* seed_dev, const char* prefix, int32_
 }
 
 // Host evaluation of the same code (tests pin it to hashlib.blake2b without a GPU).
+// numpy-stream uniforms of one sweep, generated ahead of it (the numpy-parity
+// sweep then runs in injected mode).  Variable v's stream is numpy's
+// Philox4x64-10 under stream_key(sweep_seed, "var", v) (sampler.py:245,
+// rng.py:16-25): its 64-bit word i is word i % 4 of the block at counter
+// i / 4 + 1, and random() is (word >> 11) * 2^-53.  The sweep consumes words
+// 0 .. m * nmiss[v] - 1 (index r * nmiss[v] + rank, sampler.py:245), i.e.
+// every word of every block: one thread per block writes four uniforms,
+// where the in-sweep draw computes a whole block per uniform.
+namespace sg {
+__global__ void __launch_bounds__(256) k_np_uniforms(const int64_t* __restrict__ nmiss,
+                                                     const uint64_t* __restrict__ keys, int m, double* __restrict__ out,
+                                                     int64_t ld) {
+  const int v = blockIdx.y;
+  const int64_t total = int64_t(m) * __ldg(nmiss + v);
+  const uint64_t k0 = __ldg(keys + 2 * v), k1 = __ldg(keys + 2 * v + 1);
+  double* o = out + int64_t(v) * ld;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; 4 * j < total;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const u64x4 w = philox4x64_10(u64x4{uint64_t(j) + 1ull, 0ull, 0ull, 0ull}, k0, k1);
+    const double u0 = double(w.a >> 11) * 0x1.0p-53, u1 = double(w.b >> 11) * 0x1.0p-53;
+    const double u2 = double(w.c >> 11) * 0x1.0p-53, u3 = double(w.d >> 11) * 0x1.0p-53;
+    SG_DCHECK(4 * j < ld);
+    if (4 * j + 4 <= total) {
+      reinterpret_cast<double2*>(o + 4 * j)[0] = make_double2(u0, u1);
+      reinterpret_cast<double2*>(o + 4 * j)[1] = make_double2(u2, u3);
+    } else {
+      o[4 * j] = u0;
+      if (4 * j + 1 < total) o[4 * j + 1] = u1;
+      if (4 * j + 2 < total) o[4 * j + 2] = u2;
+    }
+  }
+}
+}  // namespace sg
+
+extern "C" int sg_np_uniforms(const sg_batch* batch, const uint64_t* keys, int32_t n, double* out, int64_t ld,
+                              void* stream) {
+  using namespace sg;
+  SG_REQUIRE(batch && keys && out && n >= 1 && n <= 65535, "sg_np_uniforms: bad argument");
+  SG_REQUIRE(ld % 4 == 0 && ld >= int64_t(batch->m) * batch->cases && (reinterpret_cast<uintptr_t>(out) & 31) == 0,
+             "sg_np_uniforms: ld %lld must be a multiple of 4 and >= m * cases, out 32-byte aligned", (long long)ld);
+  const int64_t blocks = (int64_t(batch->m) * batch->cases + 3) / 4;
+  const int64_t ctas = (blocks + 255) / 256;
+  const dim3 grid(unsigned(ctas < 2048 ? (ctas > 0 ? ctas : 1) : 2048), unsigned(n));
+  k_np_uniforms<<<grid, 256, 0, (cudaStream_t)stream>>>(batch->nmiss, keys, batch->m, out, ld);
+  return check_launch("sg_np_uniforms");
+}
+
 extern "C" int sg_site_key_host(const char* text, int32_t len, uint64_t* out) {
   using namespace sg;
   SG_REQUIRE(out && len >= 0 && len <= 128 && (text || len == 0), "sg_site_key_host: bad argument");
@@ -162,3 +209,5 @@ extern "C" int sg_predict_tally(const int8_t* states, int64_t var_stride, const 
                                                                            max_card, freq, err);
   return check_launch("sg_predict_tally");
 }
+
+SG_CHECKED_EXPORT(aux)

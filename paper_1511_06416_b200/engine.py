@@ -64,6 +64,11 @@ def copy_rows(dst: torch.Tensor, src: torch.Tensor, cols: int) -> None:
         dst[:, :cols].copy_(src[:, :cols], non_blocking=True)
 
 
+# scratch for the numpy-parity sweep's pre-generated uniforms (n * m * cases
+# doubles); larger sweeps draw them inside the sweep instead
+NP_UNIFORM_BUDGET = 8 << 30
+
+
 class SmallBatch:
     """Packed-lane minibatch (sg_small layout): one uint8 word per lane, slots bucketed by latent pattern."""
 
@@ -124,6 +129,7 @@ class Engine:
         self.latent: dict[int, DeviceBatch] = {}   # moving-sum: resident lane states per minibatch
         self.nmiss_host: dict[int, np.ndarray] = {}
         self.keys = torch.empty((self.n, 2), dtype=torch.int64, device=d)
+        self._np_uniforms = {}  # row length -> (storage, aligned view, inj_off) of numpy_sweep
         self.rej = torch.empty(self.n * (_lib.REJ_SLACK + 2), dtype=torch.int64, device=d)
         self._obs_cache: dict[int, torch.Tensor] = {}
         self._obs_rings: dict[int, PinnedRing] = {}
@@ -159,6 +165,31 @@ class Engine:
         self._latent_hint = None   # latent share of the first generic minibatch (sg_batch.latent_permille)
 
     # ------------------------------------------------------------ helpers
+    def numpy_sweep(self, db, counts_ptr, s) -> None:
+        """One numpy-parity sweep (keys already in ``self.keys``): the sweep's
+        uniforms are generated ahead of it, four per Philox4x64 block
+        (``sg_np_uniforms``), and the sweep runs in injected mode -- bit-identical
+        to drawing them in the sweep (SG_RNG_NUMPY), which computes a whole block
+        per uniform and is kept beyond the scratch budget."""
+        ld = (db.m * db.cases + 3) // 4 * 4
+        if self.n * ld * 8 > NP_UNIFORM_BUDGET:
+            _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
+                      self.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, None, self.keys.data_ptr(), None, None,
+                      counts_ptr, self.err.ptr, s)
+            return
+        buf = self._np_uniforms.get(ld)
+        if buf is None:  # one buffer per row length, kept for the engine's life (graphs hold its address)
+            u = torch.empty(self.n * ld + 4, dtype=torch.float64, device=self.dev)
+            off = int((-u.data_ptr() % 32) // 8)  # 32-byte aligned rows
+            buf = (u, u[off:off + self.n * ld],
+                   torch.arange(self.n, dtype=torch.int64, device=self.dev) * ld)
+            self._np_uniforms[ld] = buf
+        _, uv, inj = buf
+        _lib.call("sg_np_uniforms", db.ref, self.keys.data_ptr(), self.n, uv.data_ptr(), ld, s)
+        _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
+                  self.ftab.data_ptr(), _lib.SG_RNG_INJECTED, 0, None, None, uv.data_ptr(), inj.data_ptr(),
+                  counts_ptr, self.err.ptr, s)
+
     def _upload_keys(self, seed: int, label: str, context: tuple) -> None:
         """Per-variable site keys of one sweep / latent init, hashed on the device."""
         var_keys(self.keys, seed, label, context, self.n)
@@ -285,9 +316,7 @@ class Engine:
                                   prefetch_only=tail_check)
             elif self.rng_mode == _lib.SG_RNG_NUMPY:
                 self._upload_keys(sweep_seed, "var", ())
-                _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
-                          self.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, None, self.keys.data_ptr(), None, None,
-                          counts_ptr, self.err.ptr, s)
+                self.numpy_sweep(db, counts_ptr, s)
             else:
                 _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
                           self.ftab.data_ptr(), _lib.SG_RNG_FAST, sweep_seed, None, None, None, None, counts_ptr,
@@ -745,9 +774,7 @@ class StepGraphs:
                 # numpy stream: stream_key(sweep_seed, "var", v) hashed on the device from the
                 # cursor's sweep seed (sampler.py:245, rng.py:16-20), then the bit-exact sweep
                 site_keys(eng.keys, ":var:", eng.n, seed_dev=cur + 8 * sw)
-                _lib.call("sg_sweep", eng.sweep_net, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
-                          eng.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, None, eng.keys.data_ptr(), None, None, counts_ptr,
-                          eng.err.ptr, s)
+                eng.numpy_sweep(db, counts_ptr, s)
             else:
                 _lib.call("sg_sweep", eng.sweep_net, db.ref, eng.cpt.data_ptr(), eng.ptab.data_ptr(),
                           eng.ftab.data_ptr(), _lib.SG_RNG_FAST, 0, cur + 8 * sw, None, None, None, counts_ptr,
