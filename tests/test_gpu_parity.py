@@ -185,3 +185,33 @@ def test_chunked_tally_oversized_run_bit_exact():
     got = sg.tally_counts(net, vals, w)
     for a, b in zip(got.tables, O.tally(onet, vals, w)):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_np_uniforms_equal_numpy_streams():
+    """sg_np_uniforms (the numpy-parity sweep's pre-generated draws) equals
+    numpy's Generator(Philox(key)).random() word for word, per variable, with
+    ragged stream lengths (m * nmiss[v], not multiples of 4) and an untouched tail."""
+    import ctypes
+
+    import torch
+
+    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200.sampler import DeviceBatch
+
+    n, m, cases = 3, 3, 37
+    nmiss = [0, 5, 37]
+    db = DeviceBatch(n, m, cases, cases, torch.device("cuda"))
+    db.nmiss.copy_(torch.tensor(nmiss, dtype=torch.int64))
+    keys = np.array([[11, 12], [2**63 + 5, 7], [123456789, 2**40 + 3]], dtype=np.uint64)
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    ld = (m * cases + 3) // 4 * 4
+    out = torch.full((n * ld + 4,), -1.0, dtype=torch.float64, device="cuda")
+    off = int((-out.data_ptr() % 32) // 8)
+    view = out[off:off + n * ld]
+    _lib.call("sg_np_uniforms", db.ref, kd.data_ptr(), n, view.data_ptr(), ld, None)
+    got = view.cpu().numpy().reshape(n, ld)
+    for v in range(n):
+        want = np.random.Generator(np.random.Philox(key=keys[v])).random(m * nmiss[v])
+        np.testing.assert_array_equal(got[v, :m * nmiss[v]], want)
+        assert (got[v, m * nmiss[v]:] == -1.0).all()
