@@ -499,8 +499,12 @@ def our_arm(args, wl: Workload) -> None:
         # ahead on a copy stream overlapped with the replay; every visit's tail stores its
         # CPTs into pinned host memory; two visits per graph replay
         graphs.finish()
+        # one pinned block per visit of a replay (the same minibatch twice): a
+        # replay's two uploads go as one copy
+        host_visits = torch.empty((2, *host_obs.shape), dtype=host_obs.dtype, pin_memory=True)
+        host_visits.copy_(host_obs.expand(2, *host_obs.shape))
         e2e_graphs = StepGraphs(eng, mb, M, range(first + args.steps + 10, first + args.steps + 20 + e2e_steps),
-                                obs_bits=graphs.obs_bits, host_block=host_obs, readback=[(eng.cpt, cpt_host)],
+                                obs_bits=graphs.obs_bits, host_block=host_visits, readback=[(eng.cpt, cpt_host)],
                                 visits_per_replay=2)
     per_call = e2e_graphs.vpr if e2e_graphs is not None else 1  # visits per e2e_step() call
     e2e_calls = e2e_steps // per_call

@@ -245,12 +245,15 @@ def test_joint_graph_with_4bit_uploads_equals_eager(koller, bits):
     assert b.err.read() & _lib.SG_ERR_STATE_RANGE
 
 
-@pytest.mark.parametrize("rng,bits,vpr", [("joint", 4, 1), ("joint", 2, 1), ("joint", 8, 1), ("fast", 8, 1),
-                                          ("joint", 2, 2), ("fast", 8, 2)])
-def test_host_fed_step_graphs_equal_eager(koller, rng, bits, vpr):
+@pytest.mark.parametrize("rng,bits,vpr,per_visit", [("joint", 4, 1, False), ("joint", 2, 1, False),
+                                                    ("joint", 8, 1, False), ("fast", 8, 1, False),
+                                                    ("joint", 2, 2, False), ("fast", 8, 2, False),
+                                                    ("joint", 2, 2, True), ("fast", 8, 2, True)])
+def test_host_fed_step_graphs_equal_eager(koller, rng, bits, vpr, per_visit):
     """StepGraphs(host_block=...): each replay uploads the next visit's pinned
     block beside the sweep and reads the CPTs back -- same results as eager
-    visits, and the read-back CPTs are the engine's."""
+    visits, and the read-back CPTs are the engine's.  ``per_visit``: one host
+    block per visit of a replay, both uploaded with one copy."""
     from paper_1511_06416_b200.engine import Engine, StepGraphs
     from paper_1511_06416_b200.io import pack_bits
 
@@ -270,9 +273,14 @@ def test_host_fed_step_graphs_equal_eager(koller, rng, bits, vpr):
     else:
         host.fill_(-1)
         host[:, :cases].copy_(obs[:, :cases])
+    if per_visit:
+        two = torch.empty((vpr, *shape), dtype=dt, pin_memory=True)
+        two.copy_(host.expand(vpr, *shape))
+        host = two
     cpt_host = torch.empty(b.pack.cells, dtype=torch.float64, pin_memory=True)
     g = StepGraphs(b, mb, m, range(1, 5), obs_bits=bits, host_block=host, readback=[(b.cpt, cpt_host)],
                    visits_per_replay=vpr)
+    assert g.host_per_visit == per_visit
     for _ in range(4 // vpr):
         g.step()
     g.finish()
@@ -283,3 +291,33 @@ def test_host_fed_step_graphs_equal_eager(koller, rng, bits, vpr):
     np.testing.assert_array_equal(a.prev_counts[0].cpu().numpy(), b.prev_counts[0].cpu().numpy())
     np.testing.assert_array_equal(a.lane_states(0)[:, :, :cases].cpu().numpy(),
                                   b.lane_states(0)[:, :, :cases].cpu().numpy())
+
+
+def test_per_visit_host_blocks_are_each_range_checked(koller):
+    """A bad state in the SECOND visit's block of a per-visit host block is
+    uploaded by the merged copy into that visit's buffer and flagged."""
+    from paper_1511_06416_b200 import _lib
+    from paper_1511_06416_b200.engine import Engine, StepGraphs
+
+    net, truth = koller
+    cases, m = 8_192, 4
+    obs = sg.forward_sample_device(net, truth, cases, seed=81, hide_fraction=0.5, mask_seed=82)
+    cfg = sg.SamplerConfig(same_m=m, minibatch_size=cases, num_passes=1, seed=29, rng="joint")
+    mb = next(iter(sg.DeviceSource(obs, cases, cases)))
+    b = Engine(net, cfg)
+    b.visit(mb, 0, m)
+    shape, dt = StepGraphs.obs_geometry(net.num_vars, cases, 8)
+    host = torch.full((2, *shape), -1, dtype=dt).pin_memory()
+    host[:, :, :cases].copy_(obs[:, :cases].unsqueeze(0).expand(2, -1, -1))
+    g = StepGraphs(b, mb, m, range(1, 13), obs_bits=8, host_block=host, visits_per_replay=2)
+    for _ in range(2):
+        g.step()
+    torch.cuda.synchronize()
+    assert b.err.read() == 0
+    g.upload_done.synchronize()
+    host[1, 0, 7] = 9  # variable 0 has 2 states; uploaded for visits 9 (replayed by the 5th step) and 11
+    for _ in range(4):
+        g.step()
+    g.finish()
+    torch.cuda.synchronize()
+    assert b.err.read() & _lib.SG_ERR_STATE_RANGE
