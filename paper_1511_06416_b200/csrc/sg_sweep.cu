@@ -806,9 +806,13 @@ template <bool V16>
 __global__ void __launch_bounds__(SG_THREADS, 4)
 k_tally_chunked(const sg_net net, const sg_batch bt, unsigned long long* __restrict__ counts) {
   extern __shared__ uint32_t hist[];
-  const int v0 = __ldg(net.tally_chunk + blockIdx.y), v1 = __ldg(net.tally_chunk + blockIdx.y + 1);
-  const int64_t cell0 = __ldg(net.cpt_off + v0);
-  const int64_t cell1 = v1 < net.n ? __ldg(net.cpt_off + v1) : net.cells;
+  const int c0v = __ldg(net.tally_chunk + blockIdx.y), c1v = __ldg(net.tally_chunk + blockIdx.y + 1);
+  const int64_t cell0 = __ldg(net.cpt_off + c0v);
+  const int64_t cell1 = c1v < net.n ? __ldg(net.cpt_off + c1v) : net.cells;
+  // grid z splits the run's variables (a few hundred in a run of small tables:
+  // one CTA per case slice alone leaves most SMs idle)
+  const int v0 = c0v + int(int64_t(c1v - c0v) * blockIdx.z / gridDim.z);
+  const int v1 = c0v + int(int64_t(c1v - c0v) * (blockIdx.z + 1) / gridDim.z);
   const bool local = cell1 - cell0 <= SG_TALLY_CHUNK_CELLS;
   const int ncell = int(cell1 - cell0);
   if (local)
@@ -894,7 +898,11 @@ static int tally_chunked(const sg_net& net, const sg_batch& bt, uint64_t* counts
   // ~4 CTAs per SM over all runs, each slice at least one work item per thread
   const int64_t want = std::max<int64_t>(1, (148 * 4 + net.tally_chunks - 1) / net.tally_chunks);
   const int slices = std::max(1, int(std::min<int64_t>(want, (work + SG_THREADS - 1) / SG_THREADS)));
-  const dim3 grid(slices, unsigned(net.tally_chunks));
+  // and the variables of each run over grid z, to ~8 CTAs per SM in all
+  const int64_t ctas = int64_t(slices) * net.tally_chunks;
+  const int vsplit = int(std::max<int64_t>(1, std::min<int64_t>((148 * 8 + ctas - 1) / ctas,
+                                                               std::max<int64_t>(1, int64_t(net.n) / net.tally_chunks))));
+  const dim3 grid(slices, unsigned(net.tally_chunks), unsigned(vsplit));
   auto cp = reinterpret_cast<unsigned long long*>(counts);
   if (v16)
     k_tally_chunked<true><<<grid, SG_THREADS, SG_TALLY_CHUNK_CELLS * 4, s>>>(net, bt, cp);
