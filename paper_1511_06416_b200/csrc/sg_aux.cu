@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(256) k_np_uniforms(const int64_t* __restrict__
                                                      const uint64_t* __restrict__ keys, int m, double* __restrict__ out,
                                                      int64_t ld) {
   const int v = blockIdx.y;
-  const int64_t total = int64_t(m) * __ldg(nmiss + v);
+  const int64_t want = int64_t(m) * __ldg(nmiss + v);
+  SG_DCHECK(want <= ld);
+  const int64_t total = want < ld ? want : ld;  // never past the row (the host sizes ld >= m * nmiss)
   const uint64_t k0 = __ldg(keys + 2 * v), k1 = __ldg(keys + 2 * v + 1);
   double* o = out + int64_t(v) * ld;
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; 4 * j < total;

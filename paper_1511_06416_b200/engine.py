@@ -172,7 +172,9 @@ class Engine:
         to drawing them in the sweep (SG_RNG_NUMPY), which computes a whole block
         per uniform and is kept beyond the scratch budget."""
         ld = (db.m * db.cases + 3) // 4 * 4
-        if self.n * ld * 8 > NP_UNIFORM_BUDGET:
+        # with a rank-prefix exchange nmiss counts every rank's latent cells (its
+        # streams are indexed globally): draw in the sweep
+        if self.n * ld * 8 > NP_UNIFORM_BUDGET or self.exchange is not None:
             _lib.call("sg_sweep", self.sweep_net, db.ref, self.cpt.data_ptr(), self.ptab.data_ptr(),
                       self.ftab.data_ptr(), _lib.SG_RNG_NUMPY, 0, None, self.keys.data_ptr(), None, None,
                       counts_ptr, self.err.ptr, s)

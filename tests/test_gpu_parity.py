@@ -6,6 +6,8 @@ computed in the reference's rounding order).  Sampled Dirichlet CPTs are
 checked statistically (see test_gpu_stats.py).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -191,7 +193,8 @@ def test_chunked_tally_oversized_run_bit_exact():
 def test_np_uniforms_equal_numpy_streams():
     """sg_np_uniforms (the numpy-parity sweep's pre-generated draws) equals
     numpy's Generator(Philox(key)).random() word for word, per variable, with
-    ragged stream lengths (m * nmiss[v], not multiples of 4) and an untouched tail."""
+    ragged stream lengths (m * nmiss[v], not multiples of 4), an untouched
+    tail, and a stream longer than its row clamped to the row."""
     import ctypes
 
     import torch
@@ -200,7 +203,7 @@ def test_np_uniforms_equal_numpy_streams():
     from paper_1511_06416_b200.sampler import DeviceBatch
 
     n, m, cases = 3, 3, 37
-    nmiss = [0, 5, 37]
+    nmiss = [0, 5, 40]  # 3 * 40 > ld: the last row is clamped to ld, nothing written past it
     db = DeviceBatch(n, m, cases, cases, torch.device("cuda"))
     db.nmiss.copy_(torch.tensor(nmiss, dtype=torch.int64))
     keys = np.array([[11, 12], [2**63 + 5, 7], [123456789, 2**40 + 3]], dtype=np.uint64)
@@ -212,6 +215,10 @@ def test_np_uniforms_equal_numpy_streams():
     _lib.call("sg_np_uniforms", db.ref, kd.data_ptr(), n, view.data_ptr(), ld, None)
     got = view.cpu().numpy().reshape(n, ld)
     for v in range(n):
-        want = np.random.Generator(np.random.Philox(key=keys[v])).random(m * nmiss[v])
-        np.testing.assert_array_equal(got[v, :m * nmiss[v]], want)
-        assert (got[v, m * nmiss[v]:] == -1.0).all()
+        k = min(m * nmiss[v], ld)
+        want = np.random.Generator(np.random.Philox(key=keys[v])).random(k)
+        np.testing.assert_array_equal(got[v, :k], want)
+        assert (got[v, k:] == -1.0).all()
+    assert (out[off + n * ld:].cpu().numpy() == -1.0).all()
+    if os.environ.get("SG_CHECKED_RUN") == "1":  # the checked build flags the oversized stream (and is cleared)
+        assert _lib.checked_lines()["aux"] > 0
