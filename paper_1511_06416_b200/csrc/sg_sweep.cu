@@ -268,7 +268,12 @@ template <int MODE, bool SMALL>
 #ifndef SG_SWEEP_NP_MINB
 #define SG_SWEEP_NP_MINB 3  // CTAs per SM for the NUMPY / INJECTED modes: 80 registers, a few spills, 37.5 % occupancy (2: 128 registers, 6 % slower)
 #endif
-__global__ void __launch_bounds__(SG_THREADS, MODE == SG_RNG_FAST ? 4 : SG_SWEEP_NP_MINB)
+#ifndef SG_SWEEP_INJ_MINB
+#define SG_SWEEP_INJ_MINB 4  // INJECTED (the numpy-parity sweep on pre-generated uniforms): no Philox state
+#endif
+__global__ void __launch_bounds__(SG_THREADS, MODE == SG_RNG_FAST       ? 4
+                                              : MODE == SG_RNG_INJECTED ? SG_SWEEP_INJ_MINB
+                                                                        : SG_SWEEP_NP_MINB)
 k_sweep(const sg_net net, const sg_batch bt, const SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_warp[SG_THREADS / 32];
